@@ -1,0 +1,142 @@
+/*
+ * ilug: the device-handle C ABI of the hot path — the plug points inside the
+ * reference's solve phase, each taking DEVICE pointers and a cudaStream_t
+ * (passed as void*). Handles own device memory and are read-only after
+ * creation except where noted; every call returns an ILUAMG_* status with
+ * the message in ilug_last_error() (same thread-local slot as
+ * iluamg_last_error()). Nothing here synchronises the stream unless stated.
+ *
+ * Reference interfaces replaced (file:line in /root/reference/proj):
+ *   ilug_factors_*      IluFactors + ilu_factorize/row_scale/row_col_scale
+ *                       (include/iluamg/ilu.hpp:33-62, src/ilu.cpp:271-333)      [K1]
+ *   ilug_sweep_upper    richardson_upper_scaled (include/iluamg/trisolve.hpp:46,
+ *                       src/trisolve.cpp:132-147) + the unscaled Jacobi form       [K2]
+ *   ilug_sweep_lower    richardson_lower (trisolve.hpp:39, src/trisolve.cpp:94-104) [K3]
+ *   ilug_smooth         smooth / ilu_smooth_sweep (include/iluamg/smoother.hpp:45-49,
+ *                       src/smoother.cpp:143-187)                                  [K4]
+ *   ilug_solve_lower/upper  solve_lower_direct / solve_upper_scaled_direct
+ *                       (trisolve.hpp:25-52), level-scheduled                        [K5]
+ *   ilug_spmv/residual  spmv_into / residual (include/iluamg/sparse.hpp:63-84)       [K6]
+ *   ilug_vcycle         vcycle (include/iluamg/amg.hpp:105, src/amg.cpp:394-418)
+ *                       incl. the coarse DenseLu::solve (src/dense.cpp:40-55)       [K6,K7]
+ *   ilug_gmres          krylov_solve/gmres_impl (include/iluamg/krylov.hpp:64-80),
+ *                       CGS2 orthogonalisation                                       [K8]
+ */
+#ifndef ILUG_H
+#define ILUG_H
+
+#include "iluamg_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ilug_factors_s ilug_factors;
+typedef struct ilug_dmatrix_s ilug_dmatrix;
+typedef struct ilug_smoother_s ilug_smoother;
+typedef struct ilug_hierarchy_s ilug_hierarchy;
+
+ILUAMG_API const char* ilug_last_error(void);
+ILUAMG_API int ilug_device_count(int* count);
+ILUAMG_API int ilug_set_device(int device);
+ILUAMG_API int ilug_synchronize(void* stream);
+
+/* ---- host matrices (SparseMatrix::from_csr, src/sparse.cpp:88-118) ---- */
+ILUAMG_API int ilug_matrix_from_csr(long long nrows, long long ncols, const long long* row_starts,
+                                    const long long* col_indices, const double* values,
+                                    iluamg_matrix** out);
+/* Copies into caller arrays sized rows+1 / nnz / nnz. */
+ILUAMG_API int ilug_matrix_copy_csr(const iluamg_matrix* A, long long* row_starts,
+                                    long long* col_indices, double* values);
+
+/* ---- host setup (no device needed; the north star keeps it on the host) ---- */
+/* ILU(0)/ILUT per the config's ilu.* keys (src/ilu.cpp:56-265): L strict, U with diagonal. */
+ILUAMG_API int ilug_ilu_factorize(const iluamg_matrix* A, const iluamg_config* cfg,
+                                  iluamg_matrix** L, iluamg_matrix** U);
+
+/* ---- K1-K5: factors ---- */
+/* Host ILU per the config's ilu.* keys, then upload + K1 scaling per `scaling`
+ * (0 none, 1 row, 2 row_col). upper_iteration: 0 scaled, 1 jacobi (unscaled).
+ * direct_plans != 0 also builds the level schedules for ilug_solve_*. */
+ILUAMG_API int ilug_factors_create(const iluamg_matrix* A, const iluamg_config* cfg, int scaling,
+                                   int upper_iteration, int direct_plans, ilug_factors** out);
+/* From explicit factors: L strictly lower (unit diagonal implicit), U upper with its diagonal. */
+ILUAMG_API int ilug_factors_from_csr(long long n, const long long* L_rows, const long long* L_cols,
+                                     const double* L_vals, const long long* U_rows,
+                                     const long long* U_cols, const double* U_vals, int scaling,
+                                     int upper_iteration, int direct_plans, ilug_factors** out);
+ILUAMG_API long long ilug_factors_rows(const ilug_factors* f);
+/* nnz of L (strict) and of U (with diagonal). */
+ILUAMG_API int ilug_factors_nnz(const ilug_factors* f, long long* nnz_L, long long* nnz_U);
+/* Download U as scaled on the device (unit diagonal when scaled) and the scale
+ * vectors (row_scale / col_scale may be NULL; flags bit0 = has row scale,
+ * bit1 = has col scale). Synchronises. */
+ILUAMG_API int ilug_factors_download_upper(const ilug_factors* f, long long* rows, long long* cols,
+                                           double* vals, double* row_scale, double* col_scale,
+                                           int* flags);
+/* y = richardson_lower(L, b, m); x = richardson_upper_scaled(f, b, m) (or the Jacobi
+ * form). Device pointers; b and the output must differ. */
+ILUAMG_API int ilug_sweep_lower(const ilug_factors* f, const double* b, double* y, long long m,
+                                void* stream);
+ILUAMG_API int ilug_sweep_upper(const ilug_factors* f, const double* b, double* x, long long m,
+                                void* stream);
+/* Host-buffer variants (copy in, sweep, copy out; synchronous) for end-to-end timing. */
+ILUAMG_API int ilug_sweep_upper_host(const ilug_factors* f, const double* b_host, double* x_host,
+                                     long long m);
+ILUAMG_API int ilug_solve_lower(const ilug_factors* f, const double* b, double* y, void* stream);
+ILUAMG_API int ilug_solve_upper(const ilug_factors* f, const double* b, double* x, void* stream);
+/* Sizes for the roofline: n, nnz of strict L, nnz of strict U, SELL padding. */
+ILUAMG_API int ilug_factors_stats(const ilug_factors* f, long long* n, long long* nnz_Ls,
+                                  long long* nnz_Us, long long* padded_Us, int* levels_L,
+                                  int* levels_U);
+ILUAMG_API void ilug_factors_free(ilug_factors* f);
+
+/* ---- K6: device operator ---- */
+ILUAMG_API int ilug_dmatrix_create(const iluamg_matrix* A, ilug_dmatrix** out);
+ILUAMG_API int ilug_spmv(const ilug_dmatrix* A, const double* x, double* y, void* stream);
+ILUAMG_API int ilug_residual(const ilug_dmatrix* A, const double* x, const double* b, double* r,
+                             void* stream);
+ILUAMG_API void ilug_dmatrix_free(ilug_dmatrix* A);
+
+/* ---- K4: smoother (which: 0 = finest-level config, 1 = fallback config) ---- */
+ILUAMG_API int ilug_smoother_create(const iluamg_matrix* A, const iluamg_config* cfg, int which,
+                                    ilug_smoother** out);
+/* x <- smooth(A, b, x); resnorm (host, may be NULL) receives |b - A x|_2 like
+ * the reference's return value (synchronises when requested). One in-flight
+ * call per handle (the handle owns its workspace). */
+ILUAMG_API int ilug_smooth(const ilug_smoother* s, const double* b, double* x, double* resnorm,
+                           void* stream);
+ILUAMG_API int ilug_ilu_smooth_sweep(const ilug_smoother* s, const double* b, double* x,
+                                     void* stream);
+ILUAMG_API void ilug_smoother_free(ilug_smoother* s);
+
+/* ---- K6/K7: AMG hierarchy and V-cycle ---- */
+ILUAMG_API int ilug_hierarchy_create(const iluamg_matrix* A, const iluamg_config* cfg,
+                                     ilug_hierarchy** out);
+/* Host-only setup (amg.* keys; src/amg.cpp:348-390): levels/matrices can be
+ * inspected, ilug_vcycle/ilug_gmres refuse it. */
+ILUAMG_API int ilug_hierarchy_create_host(const iluamg_matrix* A, const iluamg_config* cfg,
+                                          ilug_hierarchy** out);
+ILUAMG_API int ilug_hierarchy_levels(const ilug_hierarchy* h);
+/* which: 0 A, 1 P, 2 R of `level` as a new host matrix (parity downloads). */
+ILUAMG_API int ilug_hierarchy_level_matrix(const ilug_hierarchy* h, int level, int which,
+                                           iluamg_matrix** out);
+ILUAMG_API double ilug_hierarchy_operator_complexity(const ilug_hierarchy* h);
+/* z = M(r): z zeroed, one cycle (the precond lambda of src/driver.cpp:182-185).
+ * One in-flight call per handle. */
+ILUAMG_API int ilug_vcycle(ilug_hierarchy* h, const double* r, double* z, void* stream);
+/* Number of graph nodes (kernels + copies) one replayed V-cycle launches. */
+ILUAMG_API long long ilug_vcycle_graph_nodes(const ilug_hierarchy* h);
+ILUAMG_API void ilug_hierarchy_free(ilug_hierarchy* h);
+
+/* ---- K8: preconditioned (F)GMRES, krylov.* keys of cfg; device b, x (x = x0 in,
+ * solution out). iterations / final_relres may be NULL. Synchronises. Returns
+ * ILUAMG_NOT_CONVERGED when the criterion was missed. ---- */
+ILUAMG_API int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, double* x,
+                          long long* iterations, double* final_relres, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ILUG_H */

@@ -1,0 +1,372 @@
+// ORACLE / TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" shim over the *unmodified* reference C++ library compiled from
+// /root/reference/proj/src (see oracle/Makefile). Nothing under
+// paper_2111_09512_b200/ links or loads this; only tests/, __graft_entry__.smoke()
+// and bench.py's cpu_baseline / --impl reference legs do, as the checker.
+//
+// Every entry returns 0 on success, 2 (invalid) or 3 (numeric) on failure,
+// mirroring the reference's status mapping (src/capi.cpp:31-52), with the
+// message in ref_last_error().
+#include "iluamg/amg.hpp"
+#include "iluamg/config.hpp"
+#include "iluamg/dense.hpp"
+#include "iluamg/ilu.hpp"
+#include "iluamg/krylov.hpp"
+#include "iluamg/problems.hpp"
+#include "iluamg/rng.hpp"
+#include "iluamg/schur.hpp"
+#include "iluamg/smoother.hpp"
+#include "iluamg/sparse.hpp"
+#include "iluamg/trisolve.hpp"
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+using namespace iluamg;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int wrap(F&& f) {
+    try {
+        g_err.clear();
+        f();
+        return 0;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.kind() == ErrorKind::numeric ? 3 : 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+DenseVector vec(const double* p, int64_t n) { return DenseVector(p, p + n); }
+void out(const DenseVector& v, double* p) { std::memcpy(p, v.data(), v.size() * sizeof(double)); }
+
+struct Cfg {
+    SolverConfig c;
+};
+} // namespace
+
+#define API extern "C" __attribute__((visibility("default")))
+
+API const char* ref_last_error() { return g_err.c_str(); }
+
+// ---- matrices --------------------------------------------------------------
+API int ref_mat_from_csr(int64_t n, int64_t ncols, const int64_t* rp, const int64_t* ci,
+                         const double* v, void** outp) {
+    return wrap([&] {
+        const int64_t nnz = rp[n];
+        *outp = new SparseMatrix(SparseMatrix::from_csr(
+            n, ncols, std::vector<index_t>(rp, rp + n + 1), std::vector<index_t>(ci, ci + nnz),
+            std::vector<double>(v, v + nnz)));
+    });
+}
+API int ref_mat_generate(const char* spec, void** outp) {
+    return wrap([&] { *outp = new SparseMatrix(generate_problem(spec)); });
+}
+API void ref_mat_info(const void* A, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+    auto* M = static_cast<const SparseMatrix*>(A);
+    *nrows = M->nrows;
+    *ncols = M->ncols;
+    *nnz = M->nnz();
+}
+API void ref_mat_copy(const void* A, int64_t* rp, int64_t* ci, double* v) {
+    auto* M = static_cast<const SparseMatrix*>(A);
+    std::memcpy(rp, M->row_starts.data(), M->row_starts.size() * 8);
+    std::memcpy(ci, M->col_indices.data(), M->col_indices.size() * 8);
+    std::memcpy(v, M->values.data(), M->values.size() * 8);
+}
+API void ref_mat_free(void* A) { delete static_cast<SparseMatrix*>(A); }
+
+// ---- config ----------------------------------------------------------------
+API void* ref_cfg_create() { return new Cfg(); }
+API int ref_cfg_set(void* c, const char* k, const char* v) {
+    return wrap([&] { static_cast<Cfg*>(c)->c.set(k, v); });
+}
+API void ref_cfg_free(void* c) { delete static_cast<Cfg*>(c); }
+
+// ---- kernels (src/sparse.cpp, src/trisolve.cpp, src/smoother.cpp) ------------
+API int ref_spmv(const void* A, const double* x, double* y) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        out(spmv(*M, vec(x, M->ncols)), y);
+    });
+}
+API int ref_residual(const void* A, const double* x, const double* b, double* r) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        out(residual(*M, vec(x, M->ncols), vec(b, M->nrows)), r);
+    });
+}
+API int ref_richardson_lower(const void* L, const double* b, int64_t m, double* y) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(L);
+        out(richardson_lower(*M, vec(b, M->nrows), m), y);
+    });
+}
+API int ref_solve_lower_direct(const void* L, const double* b, double* y) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(L);
+        out(solve_lower_direct(*M, vec(b, M->nrows)), y);
+    });
+}
+API int ref_solve_upper_direct(const void* U, const double* b, double* y) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(U);
+        out(solve_upper_direct(*M, vec(b, M->nrows)), y);
+    });
+}
+API int ref_gauss_seidel_sweep(const void* A, const double* b, double* x) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        DenseVector xv = vec(x, M->nrows);
+        gauss_seidel_sweep(*M, vec(b, M->nrows), xv);
+        out(xv, x);
+    });
+}
+API int ref_departure(const void* T, int shape, double* d) {
+    return wrap([&] {
+        *d = departure_from_normality(*static_cast<const SparseMatrix*>(T),
+                                      static_cast<TriShape>(shape));
+    });
+}
+
+// ---- factors (src/ilu.cpp) ---------------------------------------------------
+API int ref_ilu_factor(const void* A, const void* cfg, void** outp) {
+    return wrap([&] {
+        *outp = new IluFactors(ilu_factorize(*static_cast<const SparseMatrix*>(A),
+                                             ilu_params_from(static_cast<const Cfg*>(cfg)->c)));
+    });
+}
+API int ref_factors_make(const void* L, const void* U, const double* rs, const double* cs,
+                         void** outp) {
+    return wrap([&] {
+        auto* f = new IluFactors();
+        f->L = *static_cast<const SparseMatrix*>(L);
+        f->U = *static_cast<const SparseMatrix*>(U);
+        const auto n = f->U.nrows;
+        if (rs) f->row_scale = vec(rs, n);
+        if (cs) f->col_scale = vec(cs, n);
+        f->nnz_L = f->L.nnz() + n;
+        f->nnz_U = f->U.nnz();
+        *outp = f;
+    });
+}
+// kind: 0 none, 1 row, 2 row_col (ScalingKind order, include/iluamg/schur.hpp:17)
+API int ref_factors_scale(const void* f, int kind, void** outp) {
+    return wrap([&] {
+        *outp = new IluFactors(
+            apply_scaling(*static_cast<const IluFactors*>(f), static_cast<ScalingKind>(kind)));
+    });
+}
+API void* ref_factors_L(const void* f) { return new SparseMatrix(static_cast<const IluFactors*>(f)->L); }
+API void* ref_factors_U(const void* f) { return new SparseMatrix(static_cast<const IluFactors*>(f)->U); }
+API int ref_factors_scales(const void* f, double* rs, double* cs) {
+    auto* F = static_cast<const IluFactors*>(f);
+    int flags = 0;
+    if (F->row_scale) {
+        flags |= 1;
+        if (rs) out(*F->row_scale, rs);
+    }
+    if (F->col_scale) {
+        flags |= 2;
+        if (cs) out(*F->col_scale, cs);
+    }
+    return flags;
+}
+API void ref_factors_free(void* f) { delete static_cast<IluFactors*>(f); }
+API int ref_richardson_upper_scaled(const void* f, const double* b, int64_t m, double* x) {
+    return wrap([&] {
+        auto* F = static_cast<const IluFactors*>(f);
+        out(richardson_upper_scaled(*F, vec(b, F->U.nrows), m), x);
+    });
+}
+API int ref_solve_upper_scaled_direct(const void* f, const double* b, double* x) {
+    return wrap([&] {
+        auto* F = static_cast<const IluFactors*>(f);
+        out(solve_upper_scaled_direct(*F, vec(b, F->U.nrows)), x);
+    });
+}
+
+// ---- smoother (src/smoother.cpp) ---------------------------------------------
+// which: 0 = finest-level smoother_from(cfg), 1 = fallback_smoother_from(cfg)
+API int ref_smoother_build(const void* A, const void* cfg, int which, void** outp) {
+    return wrap([&] {
+        const auto& c = static_cast<const Cfg*>(cfg)->c;
+        const SmootherConfig sc = which == 0 ? smoother_from(c) : fallback_smoother_from(c);
+        *outp = new SmootherState(build_smoother_state(*static_cast<const SparseMatrix*>(A), sc));
+    });
+}
+API int ref_smooth(const void* A, const void* st, const double* b, double* x, double* resnorm) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        DenseVector xv = vec(x, M->nrows);
+        const double r = smooth(*M, *static_cast<const SmootherState*>(st), vec(b, M->nrows), xv);
+        if (resnorm) *resnorm = r;
+        out(xv, x);
+    });
+}
+API int ref_ilu_smooth_sweep(const void* A, const void* st, const double* b, double* x) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        DenseVector xv = vec(x, M->nrows);
+        ilu_smooth_sweep(*M, *static_cast<const SmootherState*>(st), vec(b, M->nrows), xv);
+        out(xv, x);
+    });
+}
+API const void* ref_smoother_factors(const void* st) {
+    return &static_cast<const SmootherState*>(st)->factors;
+}
+API const void* ref_smoother_schur(const void* st) {
+    return static_cast<const SmootherState*>(st)->schur.get();
+}
+API void ref_smoother_free(void* st) { delete static_cast<SmootherState*>(st); }
+
+// ---- Schur partition (src/schur.cpp) -----------------------------------------
+API void ref_schur_sizes(const void* part, int64_t* ni, int64_t* nf, int64_t* p) {
+    auto* P = static_cast<const SchurPartition*>(part);
+    *ni = static_cast<int64_t>(P->interior_idx.size());
+    *nf = static_cast<int64_t>(P->interface_idx.size());
+    *p = P->p;
+}
+API void ref_schur_index(const void* part, int64_t* interior, int64_t* interface_) {
+    auto* P = static_cast<const SchurPartition*>(part);
+    std::memcpy(interior, P->interior_idx.data(), P->interior_idx.size() * 8);
+    std::memcpy(interface_, P->interface_idx.data(), P->interface_idx.size() * 8);
+}
+// which: 0 B, 1 E, 2 F, 3 C
+API void* ref_schur_block(const void* part, int which) {
+    auto* P = static_cast<const SchurPartition*>(part);
+    const SparseMatrix* m[4] = {&P->B, &P->E, &P->F, &P->C};
+    return new SparseMatrix(*m[which]);
+}
+API int64_t ref_schur_nblocks(const void* part) {
+    return static_cast<int64_t>(static_cast<const SchurPartition*>(part)->blocks.size());
+}
+API void ref_schur_block_range(const void* part, int64_t b, int64_t* begin, int64_t* end) {
+    auto& blk = static_cast<const SchurPartition*>(part)->blocks[static_cast<std::size_t>(b)];
+    *begin = blk.begin;
+    *end = blk.end;
+}
+API const void* ref_schur_block_factors(const void* part, int64_t b) {
+    return &static_cast<const SchurPartition*>(part)->blocks[static_cast<std::size_t>(b)].factors;
+}
+
+// ---- AMG (src/amg.cpp) ----------------------------------------------------------
+API int ref_amg_setup(const void* A, const void* cfg, void** outp) {
+    return wrap([&] {
+        *outp = new Hierarchy(setup(*static_cast<const SparseMatrix*>(A),
+                                    amg_params_from(static_cast<const Cfg*>(cfg)->c)));
+    });
+}
+API int64_t ref_amg_nlevels(const void* h) { return static_cast<const Hierarchy*>(h)->num_levels(); }
+// which: 0 A, 1 P, 2 R
+API void* ref_amg_level_mat(const void* h, int64_t k, int which) {
+    const Level& L = static_cast<const Hierarchy*>(h)->levels[static_cast<std::size_t>(k)];
+    const SparseMatrix* m[3] = {&L.A, &L.P, &L.R};
+    return new SparseMatrix(*m[which]);
+}
+API const void* ref_amg_level_smoother(const void* h, int64_t k) {
+    return &static_cast<const Hierarchy*>(h)->levels[static_cast<std::size_t>(k)].smoother;
+}
+API int ref_amg_vcycle(const void* h, const double* b, double* x) {
+    return wrap([&] {
+        auto* H = static_cast<const Hierarchy*>(h);
+        const auto n = H->levels.front().A.nrows;
+        DenseVector xv = vec(x, n);
+        vcycle(*H, vec(b, n), xv);
+        out(xv, x);
+    });
+}
+API double ref_amg_operator_complexity(const void* h) {
+    return static_cast<const Hierarchy*>(h)->operator_complexity();
+}
+API void ref_amg_free(void* h) { delete static_cast<Hierarchy*>(h); }
+
+// ---- Krylov (src/krylov.cpp) --------------------------------------------------------
+// Right-preconditioned (F)GMRES with the hierarchy's V-cycle, exactly as the
+// driver wires it (src/driver.cpp:175-193). hist holds 3 doubles per entry
+// (arnoldi_resnorm, true_resnorm, nrbe) for at most max_hist entries.
+API int ref_krylov_solve(const void* A, const void* h, const void* cfg, const double* b,
+                         double* x, int64_t* iters, int* converged, double* final_relres,
+                         double* hist, int64_t max_hist, int64_t* nhist, double* seconds) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        auto* H = static_cast<const Hierarchy*>(h);
+        const KrylovParams kp = krylov_params_from(static_cast<const Cfg*>(cfg)->c);
+        LinearOperator precond = [H](const DenseVector& r, DenseVector& z) {
+            z.assign(r.size(), 0.0);
+            vcycle(*H, r, z);
+        };
+        const DenseVector bv = vec(b, M->nrows);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto [xs, rep] = krylov_solve(*M, bv, DenseVector(bv.size(), 0.0), precond, kp);
+        if (seconds)
+            *seconds =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out(xs, x);
+        *iters = rep.iterations;
+        *converged = rep.converged ? 1 : 0;
+        *final_relres = rep.final_relres;
+        int64_t k = 0;
+        for (const auto& e : rep.history) {
+            if (k >= max_hist) break;
+            hist[3 * k] = e.arnoldi_resnorm;
+            hist[3 * k + 1] = e.true_resnorm;
+            hist[3 * k + 2] = e.nrbe;
+            ++k;
+        }
+        *nhist = k;
+    });
+}
+API int ref_make_rhs(const void* cfg, const void* A, double* b) {
+    return wrap([&] {
+        out(make_rhs(static_cast<const Cfg*>(cfg)->c, *static_cast<const SparseMatrix*>(A)), b);
+    });
+}
+API void ref_random_uniform(int64_t n, uint64_t seed, double* v) { out(random_uniform(n, seed), v); }
+API double ref_hash_unit(uint64_t seed, uint64_t i) { return hash_unit(seed, i); }
+
+// ---- timing helpers for the CPU baseline (bench.py cpu_baseline / --impl reference) ----
+// Times `reps` calls of richardson_upper_scaled exactly as the reference exposes it
+// (per-call split_triangular included, src/trisolve.cpp:132-147).
+API int ref_time_richardson_upper(const void* f, const double* b, int64_t m, int64_t reps,
+                                  double* seconds_best) {
+    return wrap([&] {
+        auto* F = static_cast<const IluFactors*>(f);
+        const DenseVector bv = vec(b, F->U.nrows);
+        double best = 1e300;
+        for (int64_t r = 0; r < reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            DenseVector x = richardson_upper_scaled(*F, bv, m);
+            const double s =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (x.empty()) best = -1.0;
+            best = std::min(best, s);
+        }
+        *seconds_best = best;
+    });
+}
+API int ref_time_smooth(const void* A, const void* st, const double* b, int64_t reps,
+                        double* seconds_best) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        const DenseVector bv = vec(b, M->nrows);
+        double best = 1e300;
+        for (int64_t r = 0; r < reps; ++r) {
+            DenseVector x(bv.size(), 0.0);
+            const auto t0 = std::chrono::steady_clock::now();
+            smooth(*M, *static_cast<const SmootherState*>(st), bv, x);
+            best = std::min(best, std::chrono::duration<double>(
+                                      std::chrono::steady_clock::now() - t0)
+                                      .count());
+        }
+        *seconds_best = best;
+    });
+}

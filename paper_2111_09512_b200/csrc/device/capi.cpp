@@ -1,0 +1,598 @@
+// The C ABI: iluamg_* (drop-in for the reference's include/iluamg.h, mirroring
+// src/capi.cpp's handle/status/last-error conventions) and ilug_* (device
+// handles for the individual hot-path subsystems). No exception crosses it.
+#include "../../../include/ilug.h"
+#include "../host/problems.hpp"
+#include "driver.hpp"
+
+#include <cmath>
+#include <exception>
+#include <string>
+
+struct iluamg_matrix_s {
+    ilug::Csr A;
+    std::string label;
+};
+struct iluamg_config_s {
+    ilug::Config cfg;
+};
+struct iluamg_report_s {
+    ilug::Report rep;
+    std::string json, text;
+    std::vector<std::string> csv;
+};
+struct ilug_factors_s {
+    ilug::DeviceIlu f;
+    long long nnz_L = 0, nnz_U = 0;
+};
+struct ilug_dmatrix_s {
+    ilug::DeviceMatrix M;
+};
+struct ilug_smoother_s {
+    ilug::Csr A;
+    ilug::DeviceMatrix dA;
+    ilug::DeviceSmoother s;
+    ilug::DBuf<double> r, scratch;
+};
+struct ilug_hierarchy_s {
+    ilug::HostHierarchy h;
+    ilug::DeviceHierarchy d;
+    bool on_device = false;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& fn) {
+    try {
+        g_err.clear();
+        return fn();
+    } catch (const ilug::Error& e) {
+        g_err = e.what();
+        return e.kind() == ilug::ErrorKind::numeric ? ILUAMG_ERR_NUMERIC : ILUAMG_ERR_INVALID;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return ILUAMG_ERR_NUMERIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return ILUAMG_ERR_INVALID;
+    }
+}
+
+void need(bool ok) {
+    if (!ok) ilug::fail_invalid("null argument");
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+iluamg_report* wrap(ilug::Report rep) {
+    auto* r = new iluamg_report_s{std::move(rep), {}, {}, {}};
+    r->json = r->rep.json();
+    r->text = r->rep.text();
+    for (const auto& t : r->rep.tables) r->csv.push_back(t.csv());
+    return r;
+}
+
+using RunFn = ilug::Report (*)(const ilug::Csr&, const ilug::Config&, const std::string&);
+
+int run(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_report** out, RunFn fn) {
+    return guarded([&] {
+        need(cfg && out);
+        *out = nullptr;
+        ilug::Report rep;
+        if (A) {
+            rep = fn(A->A, cfg->cfg, A->label);
+        } else {
+            const ilug::Csr M = ilug::load_matrix_from(cfg->cfg);
+            rep = fn(M, cfg->cfg, cfg->cfg.get("matrix"));
+        }
+        const int status = rep.status == 0 ? ILUAMG_OK : ILUAMG_NOT_CONVERGED;
+        if (status == ILUAMG_NOT_CONVERGED) g_err = "run completed without meeting its convergence criterion";
+        *out = wrap(std::move(rep));
+        return status;
+    });
+}
+
+ilug::Csr csr_from_ll(long long nrows, long long ncols, const long long* rp, const long long* ci,
+                      const double* v) {
+    need(rp != nullptr);
+    static_assert(sizeof(long long) == sizeof(ilug::i64));
+    return ilug::csr_from_arrays(nrows, ncols, reinterpret_cast<const ilug::i64*>(rp),
+                                 reinterpret_cast<const ilug::i64*>(ci), v);
+}
+
+ilug::ScalingKind scaling_of(int s) {
+    if (s < 0 || s > 2) ilug::fail_invalid("scaling must be 0 (none), 1 (row) or 2 (row_col)");
+    return static_cast<ilug::ScalingKind>(s);
+}
+
+ilug::UpperIteration upper_of(int u) {
+    if (u < 0 || u > 1) ilug::fail_invalid("upper_iteration must be 0 (scaled) or 1 (jacobi)");
+    return static_cast<ilug::UpperIteration>(u);
+}
+
+} // namespace
+
+extern "C" {
+
+// ============================================================ iluamg_* (drop-in)
+const char* iluamg_version(void) { return "0.1.0-b200"; }
+const char* iluamg_last_error(void) { return g_err.c_str(); }
+
+int iluamg_matrix_read(const char* path, iluamg_matrix** out) {
+    return guarded([&] {
+        need(path && out);
+        *out = new iluamg_matrix_s{ilug::mm_read(path), path};
+        return ILUAMG_OK;
+    });
+}
+int iluamg_matrix_generate(const char* spec, iluamg_matrix** out) {
+    return guarded([&] {
+        need(spec && out);
+        *out = new iluamg_matrix_s{ilug::generate_problem(spec), spec};
+        return ILUAMG_OK;
+    });
+}
+int iluamg_matrix_write(const iluamg_matrix* A, const char* path) {
+    return guarded([&] {
+        need(A && path);
+        ilug::mm_write(A->A, path);
+        return ILUAMG_OK;
+    });
+}
+long long iluamg_matrix_rows(const iluamg_matrix* A) { return A ? A->A.nrows : -1; }
+long long iluamg_matrix_cols(const iluamg_matrix* A) { return A ? A->A.ncols : -1; }
+long long iluamg_matrix_nnz(const iluamg_matrix* A) { return A ? A->A.nnz() : -1; }
+void iluamg_matrix_free(iluamg_matrix* A) { delete A; }
+
+int iluamg_config_create(iluamg_config** out) {
+    return guarded([&] {
+        need(out);
+        *out = new iluamg_config_s{};
+        return ILUAMG_OK;
+    });
+}
+int iluamg_config_load(iluamg_config* cfg, const char* path) {
+    return guarded([&] {
+        need(cfg && path);
+        cfg->cfg.load_file(path);
+        return ILUAMG_OK;
+    });
+}
+int iluamg_config_set(iluamg_config* cfg, const char* key, const char* value) {
+    return guarded([&] {
+        need(cfg && key && value);
+        cfg->cfg.set(key, value);
+        return ILUAMG_OK;
+    });
+}
+const char* iluamg_config_get(const iluamg_config* cfg, const char* key) {
+    if (!cfg || !key || !cfg->cfg.has(key)) return nullptr;
+    return cfg->cfg.get(key).c_str();
+}
+const char* iluamg_config_reference(void) {
+    static const std::string ref = ilug::Config::reference();
+    return ref.c_str();
+}
+void iluamg_config_free(iluamg_config* cfg) { delete cfg; }
+
+int iluamg_run_analyze(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_report** out) {
+    return run(A, cfg, out, &ilug::run_analyze);
+}
+int iluamg_run_solve(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_report** out) {
+    return run(A, cfg, out, &ilug::run_solve);
+}
+int iluamg_run_bench_trisolve(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_report** out) {
+    return run(A, cfg, out, &ilug::run_bench_trisolve);
+}
+int iluamg_run_schur_solve(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_report** out) {
+    return run(A, cfg, out, &ilug::run_schur_solve);
+}
+
+int iluamg_report_status(const iluamg_report* r) { return r ? r->rep.status : ILUAMG_ERR_INVALID; }
+int iluamg_report_scalar_count(const iluamg_report* r) {
+    return r ? static_cast<int>(r->rep.scalars.size()) : 0;
+}
+const char* iluamg_report_scalar_key(const iluamg_report* r, int i) {
+    if (!r || i < 0 || i >= static_cast<int>(r->rep.scalars.size())) return nullptr;
+    return r->rep.scalars[i].first.c_str();
+}
+const char* iluamg_report_scalar_value(const iluamg_report* r, int i) {
+    if (!r || i < 0 || i >= static_cast<int>(r->rep.scalars.size())) return nullptr;
+    return r->rep.scalars[i].second.c_str();
+}
+const char* iluamg_report_get(const iluamg_report* r, const char* key) {
+    if (!r || !key) return nullptr;
+    const std::string* v = r->rep.find(key);
+    return v ? v->c_str() : nullptr;
+}
+int iluamg_report_table_count(const iluamg_report* r) {
+    return r ? static_cast<int>(r->rep.tables.size()) : 0;
+}
+const char* iluamg_report_table_name(const iluamg_report* r, int i) {
+    if (!r || i < 0 || i >= static_cast<int>(r->rep.tables.size())) return nullptr;
+    return r->rep.tables[i].name.c_str();
+}
+const char* iluamg_report_table_csv(const iluamg_report* r, const char* name) {
+    if (!r || !name) return nullptr;
+    for (size_t i = 0; i < r->rep.tables.size(); ++i)
+        if (r->rep.tables[i].name == name) return r->csv[i].c_str();
+    return nullptr;
+}
+const char* iluamg_report_json(const iluamg_report* r) { return r ? r->json.c_str() : nullptr; }
+const char* iluamg_report_text(const iluamg_report* r) { return r ? r->text.c_str() : nullptr; }
+void iluamg_report_free(iluamg_report* r) { delete r; }
+
+// ============================================================ ilug_* (device handles)
+const char* ilug_last_error(void) { return g_err.c_str(); }
+
+int ilug_device_count(int* count) {
+    return guarded([&] {
+        need(count);
+        *count = 0;
+        const cudaError_t e = cudaGetDeviceCount(count);
+        if (e != cudaSuccess) *count = 0;
+        return ILUAMG_OK;
+    });
+}
+int ilug_set_device(int device) {
+    return guarded([&] {
+        ILUG_CUDA(cudaSetDevice(device));
+        return ILUAMG_OK;
+    });
+}
+int ilug_synchronize(void* stream) {
+    return guarded([&] {
+        ILUG_CUDA(cudaStreamSynchronize(S(stream)));
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_matrix_from_csr(long long nrows, long long ncols, const long long* rp, const long long* ci,
+                         const double* v, iluamg_matrix** out) {
+    return guarded([&] {
+        need(out);
+        *out = new iluamg_matrix_s{csr_from_ll(nrows, ncols, rp, ci, v), "csr"};
+        return ILUAMG_OK;
+    });
+}
+int ilug_matrix_copy_csr(const iluamg_matrix* A, long long* rp, long long* ci, double* v) {
+    return guarded([&] {
+        need(A && rp);
+        for (size_t i = 0; i < A->A.rp.size(); ++i) rp[i] = A->A.rp[i];
+        for (ilug::i64 k = 0; k < A->A.nnz(); ++k) {
+            if (ci) ci[k] = A->A.ci[k];
+            if (v) v[k] = A->A.v[k];
+        }
+        return ILUAMG_OK;
+    });
+}
+
+namespace {
+int make_factors(ilug::HostFactors hf, int scaling, int upper, int direct, ilug_factors** out) {
+    const ilug::ScalingKind sk = scaling_of(scaling);
+    const ilug::UpperIteration ui = upper_of(upper);
+    auto* f = new ilug_factors_s();
+    try {
+        f->nnz_L = hf.L.nnz();
+        f->nnz_U = hf.U.nnz();
+        f->f.build(hf, sk, ui, direct != 0, nullptr);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    *out = f;
+    return ILUAMG_OK;
+}
+} // namespace
+
+int ilug_factors_create(const iluamg_matrix* A, const iluamg_config* cfg, int scaling, int upper,
+                        int direct, ilug_factors** out) {
+    return guarded([&] {
+        need(A && cfg && out);
+        return make_factors(ilug::ilu_factorize(A->A, ilug::ilu_params_from(cfg->cfg)), scaling, upper,
+                            direct, out);
+    });
+}
+int ilug_factors_from_csr(long long n, const long long* Lr, const long long* Lc, const double* Lv,
+                          const long long* Ur, const long long* Uc, const double* Uv, int scaling,
+                          int upper, int direct, ilug_factors** out) {
+    return guarded([&] {
+        need(out);
+        ilug::HostFactors hf;
+        hf.L = csr_from_ll(n, n, Lr, Lc, Lv);
+        hf.U = csr_from_ll(n, n, Ur, Uc, Uv);
+        for (ilug::i64 i = 0; i < n; ++i) {
+            for (ilug::i64 k = hf.L.rp[i]; k < hf.L.rp[i + 1]; ++k)
+                if (hf.L.ci[k] >= i) ilug::fail_invalid("factors: L must be strictly lower triangular");
+            for (ilug::i64 k = hf.U.rp[i]; k < hf.U.rp[i + 1]; ++k)
+                if (hf.U.ci[k] < i) ilug::fail_invalid("factors: U must be upper triangular");
+        }
+        return make_factors(std::move(hf), scaling, upper, direct, out);
+    });
+}
+long long ilug_factors_rows(const ilug_factors* f) { return f ? f->f.n() : -1; }
+int ilug_factors_nnz(const ilug_factors* f, long long* nl, long long* nu) {
+    return guarded([&] {
+        need(f);
+        if (nl) *nl = f->nnz_L;
+        if (nu) *nu = f->nnz_U;
+        return ILUAMG_OK;
+    });
+}
+int ilug_factors_download_upper(const ilug_factors* f, long long* rows, long long* cols, double* vals,
+                                double* rs, double* cs, int* flags) {
+    return guarded([&] {
+        need(f);
+        const ilug::Csr U = f->f.scaled_upper_host();
+        if (rows)
+            for (size_t i = 0; i < U.rp.size(); ++i) rows[i] = U.rp[i];
+        for (ilug::i64 k = 0; k < U.nnz(); ++k) {
+            if (cols) cols[k] = U.ci[k];
+            if (vals) vals[k] = U.v[k];
+        }
+        int fl = 0;
+        if (f->f.has_rs()) {
+            fl |= 1;
+            if (rs) f->f.rs_buf().download(rs);
+        }
+        if (f->f.has_cs()) {
+            fl |= 2;
+            if (cs) f->f.cs_buf().download(cs);
+        }
+        ILUG_CUDA(cudaDeviceSynchronize());
+        if (flags) *flags = fl;
+        return ILUAMG_OK;
+    });
+}
+
+namespace {
+// Per-call workspace (3n) for the sweeps; allocated with stream-ordered malloc.
+struct Ws {
+    double* p = nullptr;
+    cudaStream_t s;
+    Ws(ilug::i64 n, cudaStream_t st) : s(st) {
+        ILUG_CUDA(cudaMallocAsync(&p, static_cast<size_t>(std::max<ilug::i64>(n, 1)) * sizeof(double), st));
+    }
+    ~Ws() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+} // namespace
+
+int ilug_sweep_lower(const ilug_factors* f, const double* b, double* y, long long m, void* stream) {
+    return guarded([&] {
+        need(f && b && y);
+        Ws ws(2 * f->f.n(), S(stream));
+        f->f.sweep_lower(b, y, m, ws.p, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_sweep_upper(const ilug_factors* f, const double* b, double* x, long long m, void* stream) {
+    return guarded([&] {
+        need(f && b && x);
+        Ws ws(3 * f->f.n(), S(stream));
+        f->f.sweep_upper(b, x, m, ws.p, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_sweep_upper_host(const ilug_factors* f, const double* bh, double* xh, long long m) {
+    return guarded([&] {
+        need(f && bh && xh);
+        const ilug::i64 n = f->f.n();
+        ilug::DBuf<double> b, x(n), ws(3 * std::max<ilug::i64>(n, 1));
+        b.upload(bh, n);
+        f->f.sweep_upper(b.p, x.p, m, ws.p, nullptr);
+        x.download(xh);
+        ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        return ILUAMG_OK;
+    });
+}
+int ilug_solve_lower(const ilug_factors* f, const double* b, double* y, void* stream) {
+    return guarded([&] {
+        need(f && b && y);
+        f->f.solve_lower(b, y, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_solve_upper(const ilug_factors* f, const double* b, double* x, void* stream) {
+    return guarded([&] {
+        need(f && b && x);
+        Ws ws(f->f.n(), S(stream));
+        f->f.solve_upper(b, x, ws.p, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_factors_stats(const ilug_factors* f, long long* n, long long* nl, long long* nu,
+                       long long* padded, int* lev_l, int* lev_u) {
+    return guarded([&] {
+        need(f);
+        if (n) *n = f->f.n();
+        if (nl) *nl = f->f.Ls().nnz;
+        if (nu) *nu = f->f.Us().nnz;
+        if (padded) *padded = f->f.Us().padded;
+        if (lev_l) *lev_l = f->f.lower_plan().levels();
+        if (lev_u) *lev_u = f->f.upper_plan().levels();
+        return ILUAMG_OK;
+    });
+}
+void ilug_factors_free(ilug_factors* f) { delete f; }
+
+int ilug_dmatrix_create(const iluamg_matrix* A, ilug_dmatrix** out) {
+    return guarded([&] {
+        need(A && out);
+        auto* d = new ilug_dmatrix_s();
+        try {
+            d->M.build(A->A, nullptr);
+            ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+        return ILUAMG_OK;
+    });
+}
+int ilug_spmv(const ilug_dmatrix* A, const double* x, double* y, void* stream) {
+    return guarded([&] {
+        need(A && x && y);
+        ilug::spmv(A->M.A, x, y, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_residual(const ilug_dmatrix* A, const double* x, const double* b, double* r, void* stream) {
+    return guarded([&] {
+        need(A && x && b && r);
+        ilug::residual(A->M.A, x, b, r, S(stream));
+        return ILUAMG_OK;
+    });
+}
+void ilug_dmatrix_free(ilug_dmatrix* A) { delete A; }
+
+int ilug_smoother_create(const iluamg_matrix* A, const iluamg_config* cfg, int which, ilug_smoother** out) {
+    return guarded([&] {
+        need(A && cfg && out);
+        const ilug::SmootherConfig sc =
+            which == 0 ? ilug::smoother_from(cfg->cfg) : ilug::fallback_smoother_from(cfg->cfg);
+        auto* s = new ilug_smoother_s();
+        try {
+            s->A = A->A;
+            s->dA.build(s->A, nullptr);
+            s->s.build(s->A, s->dA, sc, nullptr);
+            s->r.alloc(std::max<ilug::i64>(s->A.nrows, 1));
+            s->scratch.alloc(1);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+        return ILUAMG_OK;
+    });
+}
+int ilug_smooth(const ilug_smoother* s, const double* b, double* x, double* resnorm, void* stream) {
+    return guarded([&] {
+        need(s && b && x);
+        s->s.smooth(b, x, false, S(stream));
+        if (resnorm) {
+            ilug::residual(s->dA.A, x, b, s->r.p, S(stream));
+            ilug::nrm2sq_dev(s->r.p, s->A.nrows, s->scratch.p, S(stream));
+            double h = 0.0;
+            ILUG_CUDA(cudaMemcpyAsync(&h, s->scratch.p, sizeof h, cudaMemcpyDeviceToHost, S(stream)));
+            ILUG_CUDA(cudaStreamSynchronize(S(stream)));
+            *resnorm = std::sqrt(h);
+        }
+        return ILUAMG_OK;
+    });
+}
+int ilug_ilu_smooth_sweep(const ilug_smoother* s, const double* b, double* x, void* stream) {
+    return guarded([&] {
+        need(s && b && x);
+        if (s->s.config().kind != ilug::SmootherKind::ilu)
+            ilug::fail_invalid("ilu_smooth_sweep: smoother is not an ILU smoother");
+        s->s.ilu_sweep(b, x, false, S(stream));
+        return ILUAMG_OK;
+    });
+}
+void ilug_smoother_free(ilug_smoother* s) { delete s; }
+
+int ilug_hierarchy_create(const iluamg_matrix* A, const iluamg_config* cfg, ilug_hierarchy** out) {
+    return guarded([&] {
+        need(A && cfg && out);
+        auto* h = new ilug_hierarchy_s();
+        try {
+            h->h = ilug::amg_setup(A->A, ilug::amg_params_from(cfg->cfg));
+            h->d.set_use_graph(cfg->cfg.get_bool("device.graph"));
+            h->d.build(h->h, nullptr);
+            h->on_device = true;
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+        return ILUAMG_OK;
+    });
+}
+int ilug_hierarchy_create_host(const iluamg_matrix* A, const iluamg_config* cfg, ilug_hierarchy** out) {
+    return guarded([&] {
+        need(A && cfg && out);
+        auto* h = new ilug_hierarchy_s();
+        try {
+            h->h = ilug::amg_setup(A->A, ilug::amg_params_from(cfg->cfg));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+        return ILUAMG_OK;
+    });
+}
+int ilug_ilu_factorize(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_matrix** L,
+                       iluamg_matrix** U) {
+    return guarded([&] {
+        need(A && cfg && L && U);
+        ilug::HostFactors f = ilug::ilu_factorize(A->A, ilug::ilu_params_from(cfg->cfg));
+        *L = new iluamg_matrix_s{std::move(f.L), "L"};
+        *U = new iluamg_matrix_s{std::move(f.U), "U"};
+        return ILUAMG_OK;
+    });
+}
+int ilug_hierarchy_levels(const ilug_hierarchy* h) { return h ? static_cast<int>(h->h.num_levels()) : -1; }
+int ilug_hierarchy_level_matrix(const ilug_hierarchy* h, int level, int which, iluamg_matrix** out) {
+    return guarded([&] {
+        need(h && out);
+        if (level < 0 || level >= h->h.num_levels() || which < 0 || which > 2)
+            ilug::fail_invalid("hierarchy: level/which out of range");
+        const ilug::HostLevel& L = h->h.levels[level];
+        const ilug::Csr& M = which == 0 ? L.A : (which == 1 ? L.P : L.R);
+        *out = new iluamg_matrix_s{M, "level"};
+        return ILUAMG_OK;
+    });
+}
+double ilug_hierarchy_operator_complexity(const ilug_hierarchy* h) {
+    return h ? h->h.operator_complexity() : -1.0;
+}
+int ilug_vcycle(ilug_hierarchy* h, const double* r, double* z, void* stream) {
+    return guarded([&] {
+        need(h && r && z);
+        if (!h->on_device) ilug::fail_invalid("vcycle: hierarchy was created host-only");
+        h->d.vcycle(r, z, S(stream));
+        return ILUAMG_OK;
+    });
+}
+long long ilug_vcycle_graph_nodes(const ilug_hierarchy* h) { return h ? h->d.kernels_per_cycle() : -1; }
+void ilug_hierarchy_free(ilug_hierarchy* h) { delete h; }
+
+int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, double* x,
+               long long* iterations, double* final_relres, void* stream) {
+    return guarded([&] {
+        need(h && cfg && b && x);
+        if (!h->on_device) ilug::fail_invalid("gmres: hierarchy was created host-only");
+        ilug::KrylovParams p;
+        const auto& c = cfg->cfg;
+        p.flexible = c.get("krylov.method") == "fgmres";
+        if (!p.flexible && c.get("krylov.method") != "gmres")
+            ilug::fail_invalid("config: krylov.method must be gmres or fgmres");
+        p.restart = c.get_index("krylov.restart");
+        p.max_iters = c.get_index("krylov.max_iters");
+        p.tol = c.get_double("krylov.tol");
+        p.nrbe_criterion = c.get("krylov.criterion") == "nrbe";
+        p.record_history = c.get_bool("krylov.record_history");
+        p.anorm_seed = static_cast<std::uint64_t>(c.get_index("krylov.anorm_seed"));
+        p.form_iterates = c.get_bool("krylov.form_iterates");
+        p.estimate_anorm = p.form_iterates || p.nrbe_criterion;
+        const ilug::KrylovReport r =
+            ilug::device_gmres(h->d.A0(), h->h.levels[0].A, h->d, b, x, p, S(stream));
+        ILUG_CUDA(cudaStreamSynchronize(S(stream)));
+        if (iterations) *iterations = r.iterations;
+        if (final_relres) *final_relres = r.final_relres;
+        if (!r.converged) {
+            g_err = "run completed without meeting its convergence criterion";
+            return ILUAMG_NOT_CONVERGED;
+        }
+        return ILUAMG_OK;
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,306 @@
+#include "driver.hpp"
+#include "../host/problems.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+
+namespace ilug {
+
+namespace {
+
+double since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+KrylovParams krylov_from(const Config& c) {
+    KrylovParams p;
+    const std::string& m = c.get("krylov.method");
+    if (m == "gmres")
+        p.flexible = false;
+    else if (m == "fgmres")
+        p.flexible = true;
+    else
+        fail_invalid("config: krylov.method must be gmres or fgmres");
+    p.restart = c.get_index("krylov.restart");
+    p.max_iters = c.get_index("krylov.max_iters");
+    p.tol = c.get_double("krylov.tol");
+    const std::string& cr = c.get("krylov.criterion");
+    if (cr == "relres")
+        p.nrbe_criterion = false;
+    else if (cr == "nrbe")
+        p.nrbe_criterion = true;
+    else
+        fail_invalid("config: krylov.criterion must be relres or nrbe");
+    p.record_history = c.get_bool("krylov.record_history");
+    p.anorm_seed = static_cast<std::uint64_t>(c.get_index("krylov.anorm_seed"));
+    p.form_iterates = c.get_bool("krylov.form_iterates");
+    p.estimate_anorm = true;
+    return p;
+}
+
+struct SolveOutcome {
+    Vec x;
+    KrylovReport kr;
+    HostHierarchy hier;
+    double setup_seconds = 0.0, solve_seconds = 0.0;
+    i64 graph_nodes = 0;
+};
+
+SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& kp, const Vec& b,
+                        bool use_graph, cudaStream_t st) {
+    SolveOutcome oc;
+    const auto t0 = std::chrono::steady_clock::now();
+    oc.hier = amg_setup(A, ap);
+    DeviceHierarchy dh;
+    dh.set_use_graph(use_graph);
+    dh.build(oc.hier, st);
+    oc.setup_seconds = since(t0);
+
+    const i64 n = A.nrows;
+    DBuf<double> db, dx(n);
+    db.upload(b.data(), n, st);
+    vec_zero(dx.p, n, st);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    const auto t1 = std::chrono::steady_clock::now();
+    oc.kr = device_gmres(dh.A0(), A, dh, db.p, dx.p, kp, st);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    oc.solve_seconds = since(t1);
+    oc.x.resize(static_cast<size_t>(n));
+    dx.download(oc.x.data(), st);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    oc.graph_nodes = dh.kernels_per_cycle();
+    return oc;
+}
+
+void solve_scalars(Report& r, const SolveOutcome& oc, const KrylovParams& kp) {
+    r.add("method", kp.flexible ? "fgmres" : "gmres");
+    r.add("criterion", kp.nrbe_criterion ? "nrbe" : "relres");
+    r.add("tol", kp.tol);
+    r.add("iterations", oc.kr.iterations);
+    r.add("converged", oc.kr.converged);
+    r.add("false_convergence", oc.kr.false_convergence);
+    r.add("final_relres", oc.kr.final_relres);
+    r.add("final_nrbe", oc.kr.final_nrbe);
+    r.add("anorm_estimate", oc.kr.anorm_estimate);
+    r.add("levels", oc.hier.num_levels());
+    r.add("operator_complexity", oc.hier.operator_complexity());
+    const FlopsModel fm = flops_model(oc.hier);
+    r.add("flops_smoothing", static_cast<i64>(fm.smoothing));
+    r.add("flops_coarse_solve", static_cast<i64>(fm.coarse_solve));
+    r.add("flops_krylov_spmv", static_cast<i64>(fm.krylov_spmv));
+    r.add("setup_seconds", oc.setup_seconds);
+    r.add("solve_seconds", oc.solve_seconds);
+}
+
+void device_scalars(Report& r, const SolveOutcome& oc) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    r.add("device", static_cast<i64>(dev));
+    r.add("device_vcycles", oc.kr.vcycles);
+    r.add("vcycle_graph_nodes", oc.graph_nodes);
+}
+
+void history_tables(Report& r, const SolveOutcome& oc) {
+    const double bden = oc.kr.bnorm > 0.0 ? oc.kr.bnorm : 1.0;
+    ReportTable h;
+    h.name = "history";
+    h.columns = {"iter", "arnoldi_rel", "true_rel", "nrbe"};
+    for (const auto& e : oc.kr.history)
+        h.rows.push_back({std::to_string(e.iter), format_num(e.arnoldi / bden), format_num(e.true_res / bden),
+                          format_num(e.nrbe)});
+    r.tables.push_back(std::move(h));
+    ReportTable lv;
+    lv.name = "hierarchy";
+    lv.columns = {"level", "n", "nnz"};
+    for (i64 k = 0; k < oc.hier.num_levels(); ++k)
+        lv.rows.push_back({std::to_string(k), std::to_string(oc.hier.levels[k].A.nrows),
+                           std::to_string(oc.hier.levels[k].A.nnz())});
+    r.tables.push_back(std::move(lv));
+}
+
+} // namespace
+
+std::string format_num(double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.16e", v);
+    return buf;
+}
+
+std::string ReportTable::csv() const {
+    std::ostringstream o;
+    for (size_t c = 0; c < columns.size(); ++c) o << columns[c] << (c + 1 < columns.size() ? "," : "");
+    o << "\n";
+    for (const auto& row : rows) {
+        for (size_t c = 0; c < row.size(); ++c) o << row[c] << (c + 1 < row.size() ? "," : "");
+        o << "\n";
+    }
+    return o.str();
+}
+
+void Report::add(const std::string& k, double v) { add(k, format_num(v)); }
+
+const std::string* Report::find(const std::string& k) const {
+    for (const auto& [key, v] : scalars)
+        if (key == k) return &v;
+    return nullptr;
+}
+
+std::string Report::text() const {
+    std::ostringstream o;
+    for (const auto& [k, v] : scalars) o << k << " = " << v << "\n";
+    return o.str();
+}
+
+std::string Report::json() const {
+    auto esc = [](const std::string& s) {
+        std::string r;
+        for (char c : s) {
+            if (c == '"' || c == '\\') r += '\\';
+            r += c;
+        }
+        return r;
+    };
+    std::ostringstream o;
+    o << "{";
+    bool first = true;
+    for (const auto& [k, v] : scalars) {
+        if (!first) o << ",";
+        first = false;
+        o << "\"" << esc(k) << "\":\"" << esc(v) << "\"";
+    }
+    o << "}";
+    return o.str();
+}
+
+DeviceContext::DeviceContext(const Config& c) {
+    const i64 dev = c.get_index("device.id");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        fail_invalid("no CUDA device is available (this build has no CPU path)");
+    if (dev < 0 || dev >= count) fail_invalid("config: device.id out of range");
+    ILUG_CUDA(cudaSetDevice(static_cast<int>(dev)));
+    ILUG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+}
+
+DeviceContext::~DeviceContext() {
+    if (stream) cudaStreamDestroy(stream);
+}
+
+Report run_solve(const Csr& A, const Config& cfg, const std::string& label) {
+    const AmgParams ap = amg_params_from(cfg);
+    const KrylovParams kp = krylov_from(cfg);
+    const Vec b = make_rhs(cfg, A);
+    DeviceContext ctx(cfg);
+    const SolveOutcome oc = solve_with(A, ap, kp, b, cfg.get_bool("device.graph"), ctx.stream);
+    Report r;
+    r.status = oc.kr.converged ? 0 : 1;
+    r.add("matrix", label);
+    r.add("n", A.nrows);
+    r.add("nnz", A.nnz());
+    solve_scalars(r, oc, kp);
+    if (cfg.get("rhs") == "ones-times-A") {
+        double err = 0.0;
+        for (double v : oc.x) err = std::max(err, std::abs(v - 1.0));
+        r.add("ones_solution_inf_err", err);
+    }
+    device_scalars(r, oc);
+    history_tables(r, oc);
+    return r;
+}
+
+namespace {
+
+double dev_norm2(const double* v, i64 n, double* scratch, cudaStream_t st) {
+    nrm2sq_dev(v, n, scratch, st);
+    double h = 0.0;
+    ILUG_CUDA(cudaMemcpyAsync(&h, scratch, sizeof h, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    return std::sqrt(h);
+}
+
+// neumann_tail_norm (src/trisolve.cpp:158-180) with the products on the device.
+double tail_norm(const Sell& T, i64 p, i64 probes, std::uint64_t seed, double* scratch, cudaStream_t st) {
+    const i64 n = T.nrows;
+    if (p >= n) return 0.0;
+    DBuf<double> v(n), t(n);
+    double best = 0.0;
+    for (i64 s = 0; s < probes; ++s) {
+        Vec h = random_uniform(n, seed + static_cast<std::uint64_t>(s));
+        double nr = 0.0;
+        for (double x : h) nr += x * x;
+        nr = std::sqrt(nr);
+        if (nr > 0.0)
+            for (double& x : h) x /= nr;
+        v.upload(h.data(), n, st);
+        for (i64 k = 0; k < p; ++k) {
+            spmv(T, v.p, t.p, st);
+            std::swap(v.p, t.p);
+        }
+        best = std::max(best, dev_norm2(v.p, n, scratch, st));
+    }
+    return best;
+}
+
+} // namespace
+
+Report run_bench_trisolve(const Csr& A, const Config& cfg, const std::string& label) {
+    const IluParams ip = ilu_params_from(cfg);
+    ScalingKind sc = scaling_from(cfg);
+    if (sc == ScalingKind::none) sc = ScalingKind::row;
+    const i64 m_max = cfg.get_index("bench.m_max");
+    const auto seed = static_cast<std::uint64_t>(cfg.get_index("bench.seed"));
+    const i64 probes = cfg.get_index("bench.probes");
+    if (m_max < 1) fail_invalid("bench-trisolve: bench.m_max must be >= 1");
+    DeviceContext ctx(cfg);
+    cudaStream_t st = ctx.stream;
+    const HostFactors f = ilu_factorize(A, ip);
+    DeviceIlu dev;
+    dev.build(f, sc, UpperIteration::scaled, true, st);
+    const i64 n = A.nrows;
+    const Vec bh = random_uniform(n, seed);
+    DBuf<double> b, yl(n), yu(n), z(n), d(n), ws(3 * std::max<i64>(n, 1)), scr(1);
+    b.upload(bh.data(), n, st);
+    dev.solve_lower(b.p, yl.p, st);
+    dev.solve_upper(b.p, yu.p, ws.p, st);
+    const double nl = dev_norm2(yl.p, n, scr.p, st), nu = dev_norm2(yu.p, n, scr.p, st);
+    auto rel = [&](const double* a, const double* ref, double refn) {
+        vec_sub_into(d.p, a, ref, n, st);
+        const double e = dev_norm2(d.p, n, scr.p, st);
+        return refn > 0.0 ? e / refn : e;
+    };
+    ReportTable t;
+    t.name = "bench";
+    t.columns = {"factor", "m", "err_direct_rel", "tail_norm_estimate"};
+    for (i64 m = 1; m <= m_max; ++m) {
+        dev.sweep_lower(b.p, z.p, m, ws.p, st);
+        t.rows.push_back({"L", std::to_string(m), format_num(rel(z.p, yl.p, nl)),
+                          format_num(tail_norm(dev.Ls(), m, probes, seed, scr.p, st))});
+    }
+    for (i64 m = 1; m <= m_max; ++m) {
+        dev.sweep_upper(b.p, z.p, m, ws.p, st);
+        t.rows.push_back({"U", std::to_string(m), format_num(rel(z.p, yu.p, nu)),
+                          format_num(tail_norm(dev.Us(), m, probes, seed, scr.p, st))});
+    }
+    Report r;
+    r.add("matrix", label);
+    r.add("n", n);
+    r.add("variant", ip.variant == IluVariant::ilu0 ? "ilu0" : "ilut");
+    r.add("scaling", sc == ScalingKind::row ? "row" : "row_col");
+    r.add("m_max", m_max);
+    r.tables.push_back(std::move(t));
+    return r;
+}
+
+Report run_schur_solve(const Csr& A, const Config& cfg, const std::string& label) {
+    (void)A, (void)cfg, (void)label;
+    fail_invalid("schur-solve: the Schur-complement smoother is not available on the device yet");
+}
+
+Report run_analyze(const Csr& A, const Config& cfg, const std::string& label) {
+    (void)A, (void)cfg, (void)label;
+    fail_invalid("analyze: factor diagnostics are not part of the device build yet");
+}
+
+} // namespace ilug

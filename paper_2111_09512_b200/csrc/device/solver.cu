@@ -1,0 +1,409 @@
+// Device ILU factors, smoothers and the V-cycle (see solver.hpp).
+#include "solver.hpp"
+
+#include <cmath>
+
+namespace ilug {
+
+// ============================================================ DeviceMatrix
+void DeviceMatrix::build(const Csr& host, cudaStream_t st) {
+    n = host.nrows;
+    sell_from_host(A, host, Part::all, st);
+}
+
+// ============================================================ DeviceIlu (K1-K5)
+void DeviceIlu::build(const HostFactors& f, ScalingKind scaling, UpperIteration upper,
+                      bool direct_plans, cudaStream_t st) {
+    n_ = f.U.nrows;
+    scaling_ = scaling;
+    upper_ = upper;
+    sell_from_host(Ls_, f.L, Part::all, st);
+
+    DBuf<i64> rp;
+    DBuf<i32> ci;
+    DBuf<double> v;
+    rp.upload(f.U.rp.data(), n_ + 1, st);
+    ci.upload(f.U.ci.data(), f.U.nnz(), st);
+    v.upload(f.U.v.data(), f.U.nnz(), st);
+
+    const bool scale = upper == UpperIteration::scaled && scaling != ScalingKind::none;
+    if (!scale) {
+        // Unscaled factor: keep D for the Jacobi iteration / direct division.
+        d_.alloc(n_);
+        const i64 bad = extract_diag(n_, rp.p, ci.p, v.p, d_.p, st);
+        if (bad >= 0 && (upper == UpperIteration::jacobi || direct_plans))
+            fail_numeric("ilu factors: zero diagonal entry in U at row " + std::to_string(bad));
+    } else {
+        rs_.alloc(n_);
+        DBuf<double> dr, dc;
+        if (scaling == ScalingKind::row_col) {
+            cs_.alloc(n_);
+            dr.alloc(n_);
+            dc.alloc(n_);
+        }
+        const i64 bad = scale_upper(n_, rp.p, ci.p, v.p, scaling == ScalingKind::row ? 1 : 2, rs_.p,
+                                    cs_.p, dr.p, dc.p, st);
+        if (bad >= 0)
+            fail_numeric(std::string(scaling == ScalingKind::row ? "row_scale" : "row_col_scale") +
+                         ": zero diagonal entry in U at row " + std::to_string(bad));
+    }
+    sell_from_device_csr(Us_, f.U, rp.p, ci.p, v.p, Part::strict_upper, {}, st);
+    if (direct_plans) {
+        lower_plan_.build(f.L, LevelPlan::Kind::lower_unit, st);
+        upper_plan_.build(f.U, LevelPlan::Kind::upper, st, v.p);
+    }
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceIlu::sweep_lower(const double* b, double* y, i64 m, double* ws, cudaStream_t st) const {
+    if (m < 1) fail_invalid("richardson_lower: iteration count must be >= 1");
+    if (m == 1) return vec_copy(y, b, n_, st);
+    const double* cur = b;
+    for (i64 k = 2; k <= m; ++k) {
+        double* out = k == m && y != b ? y : ws + (k % 2) * n_;
+        residual(Ls_, cur, b, out, st); // y_k = b - L_s y_{k-1}
+        cur = out;
+    }
+    if (cur != y) vec_copy(y, cur, n_, st);
+}
+
+void DeviceIlu::sweep_upper(const double* b, double* x, i64 m, double* ws, cudaStream_t st) const {
+    if (m < 1) fail_invalid("richardson_upper_scaled: iteration count must be >= 1");
+    double* bs = ws;
+    if (upper_ == UpperIteration::jacobi) {
+        // x1 = D^-1 b; x_{k+1} = D^-1 (b - N x_k)
+        vec_div(bs, b, d_.p, n_, st);
+        const double* cur = bs;
+        for (i64 k = 2; k <= m; ++k) {
+            double* out = k == m ? x : ws + (1 + k % 2) * n_;
+            sweep_div(Us_, cur, b, d_.p, out, st);
+            cur = out;
+        }
+        if (cur != x) vec_copy(x, cur, n_, st);
+        return;
+    }
+    if (!has_rs()) fail_invalid("richardson_upper_scaled: factors carry no row scaling");
+    vec_div(bs, b, rs_.p, n_, st); // b_s = b / row_scale (division, src/trisolve.cpp:113)
+    const double* cur = bs;
+    for (i64 k = 2; k <= m; ++k) {
+        double* out = k == m ? x : ws + (1 + k % 2) * n_;
+        residual(Us_, cur, bs, out, st); // x_k = b_s - U_s x_{k-1}
+        cur = out;
+    }
+    if (has_cs())
+        vec_div(x, cur, cs_.p, n_, st);
+    else if (cur != x)
+        vec_copy(x, cur, n_, st);
+}
+
+void DeviceIlu::solve_lower(const double* b, double* y, cudaStream_t st) const {
+    if (!has_plans()) fail_invalid("ilu factors: level plans were not built (direct mode off)");
+    lower_plan_.solve(b, y, nullptr, st);
+}
+
+void DeviceIlu::solve_upper(const double* b, double* x, double* ws, cudaStream_t st) const {
+    if (!has_plans()) fail_invalid("ilu factors: level plans were not built (direct mode off)");
+    if (has_rs()) {
+        vec_div(ws, b, rs_.p, n_, st);
+        upper_plan_.solve(ws, x, nullptr, st);
+        if (has_cs()) vec_div(x, x, cs_.p, n_, st);
+    } else {
+        upper_plan_.solve(b, x, nullptr, st);
+    }
+}
+
+Vec DeviceIlu::download(const DBuf<double>& b) const {
+    Vec h(static_cast<size_t>(b.n));
+    b.download(h.data());
+    ILUG_CUDA(cudaDeviceSynchronize());
+    return h;
+}
+
+Csr DeviceIlu::scaled_upper_host() const {
+    const Csr S = sell_to_host(Us_);
+    Csr U;
+    U.nrows = U.ncols = n_;
+    U.rp.assign(static_cast<size_t>(n_) + 1, 0);
+    U.ci.reserve(static_cast<size_t>(S.nnz() + n_));
+    U.v.reserve(static_cast<size_t>(S.nnz() + n_));
+    Vec d;
+    if (!has_rs()) d = download(d_);
+    for (i64 i = 0; i < n_; ++i) {
+        U.ci.push_back(static_cast<i32>(i));
+        U.v.push_back(has_rs() ? 1.0 : d[i]);
+        for (i64 k = S.rp[i]; k < S.rp[i + 1]; ++k) U.ci.push_back(S.ci[k]), U.v.push_back(S.v[k]);
+        U.rp[i + 1] = static_cast<i64>(U.ci.size());
+    }
+    return U;
+}
+
+// ============================================================ DeviceSmoother
+namespace {
+
+Vec inverted_diag(const Csr& A, const char* what) {
+    Vec d = csr_diag(A);
+    for (i64 i = 0; i < A.nrows; ++i) {
+        if (d[i] == 0.0) fail_numeric(std::string(what) + ": zero diagonal at row " + std::to_string(i));
+        d[i] = 1.0 / d[i];
+    }
+    return d;
+}
+
+} // namespace
+
+void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg,
+                           cudaStream_t st) {
+    if (cfg.sweeps < 0) fail_invalid("build_smoother_state: sweeps must be >= 0");
+    if (cfg.poly_degree < 0) fail_invalid("build_smoother_state: poly_degree must be >= 0");
+    cfg_ = cfg;
+    n_ = A.nrows;
+    A_ = &dA;
+    switch (cfg.kind) {
+    case SmootherKind::jacobi: {
+        const Vec d = inverted_diag(A, "jacobi");
+        invd_.upload(d.data(), n_, st);
+        break;
+    }
+    case SmootherKind::l1_jacobi: {
+        Vec d(static_cast<size_t>(n_), 0.0);
+        for (i64 i = 0; i < n_; ++i)
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) d[i] += std::abs(A.v[k]);
+        for (i64 i = 0; i < n_; ++i) {
+            if (d[i] == 0.0)
+                fail_numeric("l1_jacobi: row " + std::to_string(i) + " is entirely zero");
+            d[i] = 1.0 / d[i];
+        }
+        invd_.upload(d.data(), n_, st);
+        break;
+    }
+    case SmootherKind::gauss_seidel: {
+        const Vec d = csr_diag(A);
+        for (i64 i = 0; i < n_; ++i)
+            if (d[i] == 0.0)
+                fail_numeric("gauss_seidel_sweep: zero diagonal at row " + std::to_string(i));
+        gs_ = std::make_unique<LevelPlan>();
+        gs_->build(A, LevelPlan::Kind::gauss_seidel, st);
+        break;
+    }
+    case SmootherKind::poly_gs: {
+        const Vec d = inverted_diag(A, "poly_gs");
+        invd_.upload(d.data(), n_, st);
+        sell_from_host(Lstrict_, A, Part::strict_lower, st);
+        break;
+    }
+    case SmootherKind::ilu: {
+        const bool rich = cfg.trisolve.mode == TriSolveMode::richardson;
+        if (rich && cfg.scaling == ScalingKind::none && cfg.trisolve.upper == UpperIteration::scaled)
+            fail_invalid("ilu smoother: the iterative U solve requires row or row/col scaling");
+        const HostFactors f = ilu_factorize(A, cfg.ilu_params);
+        ilu_ = std::make_unique<DeviceIlu>();
+        ilu_->build(f, cfg.scaling, rich ? cfg.trisolve.upper : UpperIteration::scaled, !rich, st);
+        break;
+    }
+    case SmootherKind::schur_ilut:
+        fail_invalid("schur_ilut: the Schur-complement smoother is not available on the device yet");
+    }
+    ws_.alloc(7 * std::max<i64>(n_, 1));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceSmoother::ilu_sweep(const double* b, double* x, bool x_zero, cudaStream_t st) const {
+    const DeviceIlu& f = *ilu_;
+    const i64 n = n_;
+    double* r = ws_.p;
+    double* ya = ws_.p + n;
+    double* yb = ws_.p + 2 * n;
+    double* bs = ws_.p + 3 * n;
+    double* xa = ws_.p + 4 * n;
+    double* xb = ws_.p + 5 * n;
+    const double* rr = b; // r = b - A*0 = b exactly when x == 0
+    if (!x_zero) {
+        residual(A_->A, x, b, r, st);
+        rr = r;
+    }
+    const TriSolveConfig& ts = cfg_.trisolve;
+    if (ts.mode == TriSolveMode::direct) {
+        f.solve_lower(rr, ya, st);
+        if (f.has_rs()) {
+            vec_div(bs, ya, f.rs(), n, st);
+            f.upper_plan().solve(bs, xa, nullptr, st);
+        } else {
+            f.upper_plan().solve(ya, xa, nullptr, st);
+        }
+        if (f.has_cs())
+            vec_acc_div(x, xa, f.cs(), n, st);
+        else
+            vec_acc(x, xa, n, st);
+        return;
+    }
+    const i64 mL = ts.m_lower, mU = ts.m_upper;
+    if (mL < 1) fail_invalid("richardson_lower: iteration count must be >= 1");
+    if (mU < 1) fail_invalid("richardson_upper_scaled: iteration count must be >= 1");
+    const bool jac = f.upper_iteration() == UpperIteration::jacobi;
+    const double* dv = jac ? f.diag() : f.rs();
+    // ---- L sweeps; the last one also produces x_1 of the U iteration (bs)
+    const double* y = rr;
+    if (mL == 1) {
+        vec_div(bs, rr, dv, n, st);
+    } else {
+        const double* cur = rr;
+        for (i64 k = 2; k <= mL; ++k) {
+            double* out = (k % 2) ? ya : yb;
+            if (k == mL) {
+                if (jac)
+                    sweep_both(f.Ls(), cur, rr, dv, out, bs, st); // y and x1 = y / d
+                else
+                    sweep_div(f.Ls(), cur, rr, dv, bs, st); // b_s = y / row_scale
+            } else {
+                residual(f.Ls(), cur, rr, out, st);
+            }
+            cur = out;
+        }
+        y = cur;
+    }
+    // ---- U sweeps; the last one accumulates into x (with the column unscale)
+    const double* rhs = jac ? y : bs;
+    const double* post = jac ? f.diag() : (f.has_cs() ? f.cs() : nullptr);
+    if (mU == 1) {
+        if (post)
+            vec_acc_div(x, jac ? y : bs, post, n, st);
+        else
+            vec_acc(x, bs, n, st);
+        return;
+    }
+    const double* cur = bs;
+    for (i64 k = 2; k <= mU; ++k) {
+        if (k == mU) {
+            sweep_acc(f.Us(), cur, rhs, post, x, st);
+        } else {
+            double* out = (k % 2) ? xa : xb;
+            if (jac)
+                sweep_div(f.Us(), cur, rhs, f.diag(), out, st);
+            else
+                residual(f.Us(), cur, rhs, out, st);
+            cur = out;
+        }
+    }
+}
+
+void DeviceSmoother::smooth(const double* b, double* x, bool x_zero, cudaStream_t st) const {
+    const i64 n = n_;
+    for (i64 s = 0; s < cfg_.sweeps; ++s) {
+        const bool zero = x_zero && s == 0;
+        switch (cfg_.kind) {
+        case SmootherKind::jacobi:
+        case SmootherKind::l1_jacobi:
+            residual_scale_step(A_->A, x, b, invd_.p, ws_.p, st);
+            vec_copy(x, ws_.p, n, st);
+            break;
+        case SmootherKind::gauss_seidel:
+            gs_->solve(b, ws_.p, x, st);
+            vec_copy(x, ws_.p, n, st);
+            break;
+        case SmootherKind::poly_gs: {
+            double* t0 = ws_.p;
+            double* t1 = ws_.p + n;
+            double* acc = ws_.p + 2 * n;
+            residual_scale_init(A_->A, x, b, invd_.p, t0, acc, st);
+            for (i64 j = 1; j <= cfg_.poly_degree; ++j) {
+                neg_scale_acc(Lstrict_, t0, invd_.p, t1, acc, st);
+                std::swap(t0, t1);
+            }
+            vec_acc(x, acc, n, st);
+            break;
+        }
+        case SmootherKind::ilu:
+            ilu_sweep(b, x, zero, st);
+            break;
+        case SmootherKind::schur_ilut:
+            fail_invalid("schur_ilut: not available on the device yet");
+        }
+    }
+}
+
+// ============================================================ DeviceHierarchy
+DeviceHierarchy::~DeviceHierarchy() {
+    if (exec_) cudaGraphExecDestroy(exec_);
+}
+
+void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st) {
+    const int L = static_cast<int>(h.levels.size());
+    levels_ = std::vector<Lev>(static_cast<size_t>(L));
+    for (int k = 0; k < L; ++k) {
+        const HostLevel& hl = h.levels[k];
+        Lev& lv = levels_[k];
+        lv.n = hl.A.nrows;
+        lv.A.build(hl.A, st);
+        if (k + 1 < L) {
+            sell_from_host(lv.P, hl.P, Part::all, st);
+            sell_from_host(lv.R, hl.R, Part::all, st);
+            lv.smoother.build(hl.A, lv.A, h.params.plan.for_level(k), st);
+        }
+        lv.b.alloc(std::max<i64>(lv.n, 1));
+        lv.x.alloc(std::max<i64>(lv.n, 1));
+        lv.r.alloc(std::max<i64>(lv.n, 1));
+    }
+    lu_.upload(h.coarse.lu.data(), static_cast<i64>(h.coarse.lu.size()), st);
+    piv_.upload(h.coarse.piv.data(), static_cast<i64>(h.coarse.piv.size()), st);
+    nu_ = h.params.cycles_nu;
+    if (exec_) cudaGraphExecDestroy(exec_);
+    exec_ = nullptr;
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceHierarchy::cycle(int k, bool x_zero, cudaStream_t st) {
+    Lev& lv = levels_[k];
+    if (k + 1 == num_levels()) {
+        dense_lu_solve_dev(lv.n, lu_.p, piv_.p, lv.b.p, lv.x.p, st);
+        return;
+    }
+    Lev& nx = levels_[k + 1];
+    lv.smoother.smooth(lv.b.p, lv.x.p, x_zero, st);
+    residual(lv.A.A, lv.x.p, lv.b.p, lv.r.p, st);
+    spmv(lv.R, lv.r.p, nx.b.p, st);
+    vec_zero(nx.x.p, nx.n, st);
+    for (i64 i = 0; i < nu_; ++i) cycle(k + 1, i == 0, st);
+    spmv_add(lv.P, nx.x.p, lv.x.p, st);
+    lv.smoother.smooth(lv.b.p, lv.x.p, false, st);
+}
+
+void DeviceHierarchy::vcycle_eager(const double* r, double* z, cudaStream_t st) {
+    Lev& l0 = levels_[0];
+    vec_copy(l0.b.p, r, l0.n, st);
+    vec_zero(l0.x.p, l0.n, st);
+    cycle(0, true, st);
+    vec_copy(z, l0.x.p, l0.n, st);
+}
+
+void DeviceHierarchy::vcycle(const double* r, double* z, cudaStream_t st) {
+    if (!use_graph_) return vcycle_eager(r, z, st);
+    Lev& l0 = levels_[0];
+    if (!exec_) {
+        // Capture the whole cycle once (fixed internal in/out buffers).
+        cudaStream_t cap;
+        ILUG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        cudaGraph_t g = nullptr;
+        ILUG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        try {
+            vec_zero(l0.x.p, l0.n, cap);
+            cycle(0, true, cap);
+        } catch (...) {
+            cudaStreamEndCapture(cap, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaStreamDestroy(cap);
+            throw;
+        }
+        ILUG_CUDA(cudaStreamEndCapture(cap, &g));
+        size_t nodes = 0;
+        ILUG_CUDA(cudaGraphGetNodes(g, nullptr, &nodes));
+        kernels_per_cycle_ = static_cast<i64>(nodes);
+        ILUG_CUDA(cudaGraphInstantiate(&exec_, g, 0));
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+    }
+    vec_copy(l0.b.p, r, l0.n, st);
+    ILUG_CUDA(cudaGraphLaunch(exec_, st));
+    vec_copy(z, l0.x.p, l0.n, st);
+}
+
+} // namespace ilug

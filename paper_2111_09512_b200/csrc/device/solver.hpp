@@ -1,0 +1,177 @@
+// Device-resident solve phase: ILU factors (K1-K5), smoothers (K4 + the
+// fallback family), the AMG V-cycle (K6/K7) and (F)GMRES with CGS2 (K8).
+//
+// Reference anchors: SmootherState/build_smoother_state/smooth
+// (include/iluamg/smoother.hpp:33-49, src/smoother.cpp:49-187), cycle_level
+// (src/amg.cpp:394-418), gmres_impl (src/krylov.cpp:75-238). Setup-phase data
+// (factors, hierarchy) comes from the host (csrc/host/), is uploaded once and is
+// read-only afterwards, so handles can be shared by concurrent solves on
+// different streams (the reference's threading contract, README.md:152-154).
+#pragma once
+
+#include "../host/amg.hpp"
+#include "../kernels/levelset.hpp"
+
+#include <memory>
+
+namespace ilug {
+
+/// Device copy of a square operator.
+struct DeviceMatrix {
+    Sell A;
+    i64 n = 0;
+    void build(const Csr& host, cudaStream_t st);
+};
+
+/// K1-K5: scaled ILU factors on the device plus the sweep/solve entry points.
+class DeviceIlu {
+public:
+    /// Uploads L (strict) and U (with diagonal), applies `scaling` with the K1
+    /// kernel, packs strict parts into SELL. Level plans are built when
+    /// `direct_plans` is set (trisolve.mode=direct or explicit sptrsv use).
+    void build(const HostFactors& f, ScalingKind scaling, UpperIteration upper, bool direct_plans,
+               cudaStream_t st);
+
+    i64 n() const { return n_; }
+    ScalingKind scaling() const { return scaling_; }
+    bool has_rs() const { return rs_.n > 0; }
+    bool has_cs() const { return cs_.n > 0; }
+    const double* rs() const { return rs_.p; }
+    const double* cs() const { return cs_.p; }
+    const double* diag() const { return d_.p; }
+    const Sell& Ls() const { return Ls_; }
+    const Sell& Us() const { return Us_; }
+    UpperIteration upper_iteration() const { return upper_; }
+
+    /// richardson_lower (src/trisolve.cpp:94-104): y = m sweeps from 0. ws: 2n doubles.
+    void sweep_lower(const double* b, double* y, i64 m, double* ws, cudaStream_t st) const;
+    /// richardson_upper_scaled (src/trisolve.cpp:132-147) or its Jacobi form on the
+    /// unscaled factor: x = m sweeps from 0 (pre/post scaling included). ws: 3n.
+    void sweep_upper(const double* b, double* x, i64 m, double* ws, cudaStream_t st) const;
+    /// Level-scheduled direct solves: solve_lower_direct and
+    /// solve_upper_scaled_direct / solve_upper_direct (src/trisolve.cpp:20-55,149-156). ws: n.
+    void solve_lower(const double* b, double* y, cudaStream_t st) const;
+    void solve_upper(const double* b, double* x, double* ws, cudaStream_t st) const;
+    bool has_plans() const { return lower_plan_.levels() > 0 || n_ == 0; }
+    const LevelPlan& lower_plan() const { return lower_plan_; }
+    const LevelPlan& upper_plan() const { return upper_plan_; }
+
+    /// Download the scaled factor U (unit diagonal re-inserted) for parity tests.
+    Csr scaled_upper_host() const;
+    Vec download(const DBuf<double>& b) const;
+    const DBuf<double>& rs_buf() const { return rs_; }
+    const DBuf<double>& cs_buf() const { return cs_; }
+
+private:
+    i64 n_ = 0;
+    ScalingKind scaling_ = ScalingKind::row;
+    UpperIteration upper_ = UpperIteration::scaled;
+    Sell Ls_, Us_;          // strict parts (Us_ scaled unless upper_ == jacobi)
+    DBuf<double> rs_, cs_, d_;
+    LevelPlan lower_plan_, upper_plan_;
+    Csr U_pattern_;          // host structure of U (values are the unscaled ones)
+};
+
+/// One level's smoother (src/smoother.cpp:161-187 `smooth`).
+class DeviceSmoother {
+public:
+    void build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg, cudaStream_t st);
+    /// x <- smooth(A, b, x). `x_zero`: caller guarantees x == 0 on entry, so the
+    /// first residual is b itself (bitwise what the SpMV would give).
+    void smooth(const double* b, double* x, bool x_zero, cudaStream_t st) const;
+    /// One ilu_smooth_sweep (src/smoother.cpp:143-159).
+    void ilu_sweep(const double* b, double* x, bool x_zero, cudaStream_t st) const;
+    const SmootherConfig& config() const { return cfg_; }
+    const DeviceIlu* ilu() const { return ilu_.get(); }
+    i64 n() const { return n_; }
+
+private:
+    SmootherConfig cfg_;
+    i64 n_ = 0;
+    const DeviceMatrix* A_ = nullptr;
+    std::unique_ptr<DeviceIlu> ilu_;
+    std::unique_ptr<LevelPlan> gs_;
+    Sell Lstrict_;               // poly_gs
+    DBuf<double> invd_;          // jacobi / l1 / poly_gs
+    mutable DBuf<double> ws_;    // workspace (r, y ping-pong, bs, x ping-pong)
+};
+
+/// The AMG V-cycle on the device, optionally replayed as one CUDA graph.
+class DeviceHierarchy {
+public:
+    void build(const HostHierarchy& h, cudaStream_t st);
+    /// z = M(r) with z zeroed first (the driver's precond lambda, src/driver.cpp:182-185).
+    void vcycle(const double* r, double* z, cudaStream_t st);
+    /// Same, without graph replay (direct kernel launches).
+    void vcycle_eager(const double* r, double* z, cudaStream_t st);
+    i64 n() const { return levels_.empty() ? 0 : levels_[0].n; }
+    int num_levels() const { return static_cast<int>(levels_.size()); }
+    const DeviceMatrix& A0() const { return levels_[0].A; }
+    const DeviceSmoother& smoother(int k) const { return levels_[k].smoother; }
+    void set_use_graph(bool g) { use_graph_ = g; }
+    i64 kernels_per_cycle() const { return kernels_per_cycle_; }
+
+private:
+    struct Lev {
+        i64 n = 0;
+        DeviceMatrix A;
+        Sell P, R;
+        DeviceSmoother smoother;
+        DBuf<double> b, x, r;
+    };
+    void cycle(int k, bool x_zero, cudaStream_t st);
+    std::vector<Lev> levels_;
+    DBuf<double> lu_;
+    DBuf<i64> piv_;
+    i64 nu_ = 1;
+    bool use_graph_ = true;
+    cudaGraphExec_t exec_ = nullptr;
+    cudaStream_t graph_stream_ = nullptr;
+    i64 kernels_per_cycle_ = 0;
+
+public:
+    DeviceHierarchy() = default;
+    DeviceHierarchy(const DeviceHierarchy&) = delete;
+    DeviceHierarchy& operator=(const DeviceHierarchy&) = delete;
+    ~DeviceHierarchy();
+};
+
+struct KrylovParams {
+    bool flexible = false;
+    i64 restart = 50;
+    i64 max_iters = 200;
+    double tol = 1e-5;
+    bool nrbe_criterion = false;
+    bool record_history = true;
+    std::uint64_t anorm_seed = 7;
+    /// Reference behaviour: form x_k every iteration (non-flexible GMRES applies
+    /// the preconditioner a second time, src/krylov.cpp:204-214) and record the
+    /// true residual / NRBE. false = form x only at the end of each restart
+    /// cycle (iteration counts unchanged under the relres criterion).
+    bool form_iterates = true;
+    bool estimate_anorm = true;
+};
+
+struct HistoryEntry {
+    i64 iter = 0;
+    double arnoldi = 0.0, true_res = 0.0, nrbe = 0.0;
+};
+
+struct KrylovReport {
+    i64 iterations = 0;
+    std::vector<HistoryEntry> history;
+    bool converged = false, false_convergence = false;
+    double anorm_estimate = 0.0, bnorm = 0.0, final_relres = 0.0, final_nrbe = 0.0;
+    i64 vcycles = 0;
+};
+
+/// Right-preconditioned (F)GMRES on the device, CGS2 orthogonalisation.
+/// Host work per iteration: Givens rotations on (j+2) scalars.
+KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierarchy& M,
+                          const double* b_dev, double* x_dev, const KrylovParams& p, cudaStream_t st);
+
+/// 50-step power iteration on A^T A (src/krylov.cpp:14-28) on the device.
+double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 steps,
+                                std::uint64_t seed, cudaStream_t st);
+
+} // namespace ilug

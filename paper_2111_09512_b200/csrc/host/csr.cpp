@@ -1,0 +1,299 @@
+#include "csr.hpp"
+
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+
+namespace ilug {
+
+int host_threads() {
+    static const int n = [] {
+        if (const char* e = std::getenv("ILUG_THREADS")) {
+            const int v = std::atoi(e);
+            if (v > 0) return v;
+        }
+        const unsigned hc = std::thread::hardware_concurrency();
+        return hc == 0 ? 1 : static_cast<int>(std::min(hc, 64u));
+    }();
+    return n;
+}
+
+void parallel_ranges(i64 n, const std::function<void(i64, i64, int)>& fn, i64 grain) {
+    if (n <= 0) return;
+    const int T = static_cast<int>(std::min<i64>(host_threads(), std::max<i64>(1, n / grain)));
+    if (T <= 1) {
+        fn(0, n, 0);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::exception_ptr err;
+    std::mutex mu;
+    for (int t = 0; t < T; ++t) {
+        const i64 b = n * t / T, e = n * (t + 1) / T;
+        pool.emplace_back([&, b, e, t] {
+            try {
+                fn(b, e, t);
+            } catch (...) {
+                std::lock_guard<std::mutex> g(mu);
+                if (!err) err = std::current_exception();
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    if (err) std::rethrow_exception(err);
+}
+
+Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_zeros) {
+    for (const auto& e : t)
+        if (e.i < 0 || e.i >= nrows || e.j < 0 || e.j >= ncols)
+            fail_invalid("from_triplets: index (" + std::to_string(e.i) + "," +
+                         std::to_string(e.j) + ") out of range");
+    std::stable_sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
+        return a.i != b.i ? a.i < b.i : a.j < b.j;
+    });
+    Csr A;
+    A.nrows = nrows;
+    A.ncols = ncols;
+    A.rp.assign(static_cast<size_t>(nrows) + 1, 0);
+    size_t k = 0;
+    while (k < t.size()) {
+        const i64 i = t[k].i, j = t[k].j;
+        double s = t[k].v;
+        for (++k; k < t.size() && t[k].i == i && t[k].j == j; ++k) s += t[k].v;
+        if (s == 0.0 && !keep_zeros) continue;
+        A.ci.push_back(static_cast<i32>(j));
+        A.v.push_back(s);
+        ++A.rp[static_cast<size_t>(i) + 1];
+    }
+    for (i64 i = 0; i < nrows; ++i) A.rp[i + 1] += A.rp[i];
+    return A;
+}
+
+void csr_validate(const Csr& A, const char* what) {
+    const std::string w(what);
+    if (static_cast<i64>(A.rp.size()) != A.nrows + 1 || A.rp[0] != 0)
+        fail_invalid(w + ": row_starts must have length nrows+1 and start at 0");
+    if (A.ci.size() != A.v.size()) fail_invalid(w + ": column/value length mismatch");
+    if (A.rp[A.nrows] != A.nnz()) fail_invalid(w + ": row_starts[nrows] != nnz");
+    if (A.ncols > 0x7fffffff) fail_invalid(w + ": more than 2^31-1 columns");
+    std::atomic<i64> bad{-1};
+    parallel_ranges(A.nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            if (A.rp[i] > A.rp[i + 1]) {
+                bad = i;
+                return;
+            }
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                const i64 j = A.ci[k];
+                if (j < 0 || j >= A.ncols || (k > A.rp[i] && A.ci[k - 1] >= j)) {
+                    bad = i;
+                    return;
+                }
+            }
+        }
+    });
+    if (bad >= 0)
+        fail_invalid(w + ": invalid CSR structure at row " + std::to_string(bad.load()) +
+                     " (row starts must not decrease; columns must be in range and strictly "
+                     "increasing)");
+}
+
+Csr csr_from_arrays(i64 nrows, i64 ncols, const i64* rp, const i64* ci, const double* v) {
+    if (nrows < 0 || ncols < 0) fail_invalid("from_csr: negative dimension");
+    if (!rp) fail_invalid("from_csr: null row_starts");
+    Csr A;
+    A.nrows = nrows;
+    A.ncols = ncols;
+    A.rp.assign(rp, rp + nrows + 1);
+    if (A.rp[0] != 0 || A.rp[nrows] < 0) fail_invalid("from_csr: row_starts[0] must be 0");
+    const i64 nnz = A.rp[nrows];
+    if (nnz > 0 && (!ci || !v)) fail_invalid("from_csr: null column/value arrays");
+    A.ci.resize(static_cast<size_t>(nnz));
+    A.v.assign(v, v + nnz);
+    for (i64 k = 0; k < nnz; ++k) {
+        if (ci[k] < 0 || ci[k] >= ncols) fail_invalid("from_csr: column index out of range");
+        A.ci[k] = static_cast<i32>(ci[k]);
+    }
+    csr_validate(A, "from_csr");
+    return A;
+}
+
+Csr csr_identity(i64 n) {
+    Csr I;
+    I.nrows = I.ncols = n;
+    I.rp.resize(static_cast<size_t>(n) + 1);
+    I.ci.resize(static_cast<size_t>(n));
+    I.v.assign(static_cast<size_t>(n), 1.0);
+    for (i64 i = 0; i <= n; ++i) I.rp[i] = i;
+    for (i64 i = 0; i < n; ++i) I.ci[i] = static_cast<i32>(i);
+    return I;
+}
+
+void csr_spmv(const Csr& A, const double* x, double* y) {
+    parallel_ranges(A.nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            double s = 0.0;
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) s += A.v[k] * x[A.ci[k]];
+            y[i] = s;
+        }
+    });
+}
+
+Csr csr_transpose(const Csr& A) {
+    Csr T;
+    T.nrows = A.ncols;
+    T.ncols = A.nrows;
+    const i64 nnz = A.nnz();
+    T.ci.resize(static_cast<size_t>(nnz));
+    T.v.resize(static_cast<size_t>(nnz));
+    // Per-chunk column histograms give every chunk its own write cursor per
+    // column; chunks cover ascending row ranges, so each row of T receives its
+    // entries in ascending source-row order, exactly like the serial bucket fill.
+    const int C = std::max(1, std::min<int>(host_threads(), static_cast<int>(A.nrows / 8192 + 1)));
+    std::vector<std::vector<i64>> cnt(static_cast<size_t>(C));
+    auto chunk_lo = [&](int c) { return A.nrows * c / C; };
+    parallel_ranges(C, [&](i64 b, i64 e, int) {
+        for (i64 c = b; c < e; ++c) {
+            auto& h = cnt[c];
+            h.assign(static_cast<size_t>(A.ncols), 0);
+            for (i64 k = A.rp[chunk_lo(static_cast<int>(c))]; k < A.rp[chunk_lo(static_cast<int>(c) + 1)]; ++k)
+                ++h[A.ci[k]];
+        }
+    }, 1);
+    T.rp.assign(static_cast<size_t>(A.ncols) + 1, 0);
+    // column totals, then per-chunk starting cursors
+    for (i64 j = 0; j < A.ncols; ++j) {
+        i64 tot = 0;
+        for (int c = 0; c < C; ++c) tot += cnt[c][j];
+        T.rp[j + 1] = tot;
+    }
+    for (i64 j = 0; j < A.ncols; ++j) T.rp[j + 1] += T.rp[j];
+    parallel_ranges(A.ncols, [&](i64 b, i64 e, int) {
+        for (i64 j = b; j < e; ++j) {
+            i64 cur = T.rp[j];
+            for (int c = 0; c < C; ++c) {
+                const i64 n = cnt[c][j];
+                cnt[c][j] = cur;
+                cur += n;
+            }
+        }
+    });
+    parallel_ranges(C, [&](i64 b, i64 e, int) {
+        for (i64 c = b; c < e; ++c) {
+            auto& cur = cnt[c];
+            for (i64 i = chunk_lo(static_cast<int>(c)); i < chunk_lo(static_cast<int>(c) + 1); ++i)
+                for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                    const i64 p = cur[A.ci[k]]++;
+                    T.ci[p] = static_cast<i32>(i);
+                    T.v[p] = A.v[k];
+                }
+        }
+    }, 1);
+    return T;
+}
+
+Csr csr_matmul(const Csr& A, const Csr& B) {
+    if (A.ncols != B.nrows) fail_invalid("matmul: dimension mismatch");
+    Csr C;
+    C.nrows = A.nrows;
+    C.ncols = B.ncols;
+    C.rp.assign(static_cast<size_t>(A.nrows) + 1, 0);
+    const int T = std::max(1, std::min<int>(host_threads() * 4, static_cast<int>(A.nrows / 2048 + 1)));
+    struct Piece {
+        std::vector<i32> ci;
+        std::vector<double> v;
+    };
+    std::vector<Piece> pieces(static_cast<size_t>(T));
+    auto lo = [&](int t) { return A.nrows * t / T; };
+    // Each worker keeps a dense accumulator + row marker over B's columns.
+    parallel_ranges(T, [&](i64 tb, i64 te, int) {
+        std::vector<double> work(static_cast<size_t>(B.ncols), 0.0);
+        std::vector<i64> mark(static_cast<size_t>(B.ncols), -1);
+        std::vector<i32> cols;
+        for (i64 t = tb; t < te; ++t) {
+            Piece& pc = pieces[t];
+            for (i64 i = lo(static_cast<int>(t)); i < lo(static_cast<int>(t) + 1); ++i) {
+                cols.clear();
+                for (i64 ka = A.rp[i]; ka < A.rp[i + 1]; ++ka) {
+                    const i64 k = A.ci[ka];
+                    const double aik = A.v[ka];
+                    for (i64 kb = B.rp[k]; kb < B.rp[k + 1]; ++kb) {
+                        const i32 j = B.ci[kb];
+                        if (mark[j] != i) {
+                            mark[j] = i;
+                            cols.push_back(j);
+                        }
+                        work[j] += aik * B.v[kb];
+                    }
+                }
+                std::sort(cols.begin(), cols.end());
+                i64 kept = 0;
+                for (i32 j : cols) {
+                    const double s = work[j];
+                    work[j] = 0.0;
+                    if (s == 0.0) continue;
+                    pc.ci.push_back(j);
+                    pc.v.push_back(s);
+                    ++kept;
+                }
+                C.rp[i + 1] = kept;
+            }
+        }
+    }, 1);
+    for (i64 i = 0; i < A.nrows; ++i) C.rp[i + 1] += C.rp[i];
+    C.ci.resize(static_cast<size_t>(C.rp[A.nrows]));
+    C.v.resize(static_cast<size_t>(C.rp[A.nrows]));
+    parallel_ranges(T, [&](i64 tb, i64 te, int) {
+        for (i64 t = tb; t < te; ++t) {
+            const i64 off = C.rp[lo(static_cast<int>(t))];
+            std::copy(pieces[t].ci.begin(), pieces[t].ci.end(), C.ci.begin() + off);
+            std::copy(pieces[t].v.begin(), pieces[t].v.end(), C.v.begin() + off);
+            Piece().ci.swap(pieces[t].ci);
+            Piece().v.swap(pieces[t].v);
+        }
+    }, 1);
+    return C;
+}
+
+std::tuple<Csr, Csr, Csr> csr_split_triangular(const Csr& A) {
+    if (A.nrows != A.ncols) fail_invalid("split_triangular: matrix must be square");
+    Csr L, D, U;
+    for (Csr* M : {&L, &D, &U}) {
+        M->nrows = A.nrows;
+        M->ncols = A.ncols;
+        M->rp.assign(static_cast<size_t>(A.nrows) + 1, 0);
+    }
+    for (i64 i = 0; i < A.nrows; ++i)
+        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            Csr& dst = A.ci[k] < i ? L : (A.ci[k] == i ? D : U);
+            dst.ci.push_back(A.ci[k]);
+            dst.v.push_back(A.v[k]);
+            ++dst.rp[i + 1];
+        }
+    for (Csr* M : {&L, &D, &U})
+        for (i64 i = 0; i < A.nrows; ++i) M->rp[i + 1] += M->rp[i];
+    return {std::move(L), std::move(D), std::move(U)};
+}
+
+Vec csr_diag(const Csr& A) {
+    if (A.nrows != A.ncols) fail_invalid("diag: matrix must be square");
+    Vec d(static_cast<size_t>(A.nrows), 0.0);
+    parallel_ranges(A.nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i)
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k)
+                if (A.ci[k] == i) {
+                    d[i] = A.v[k];
+                    break;
+                }
+    });
+    return d;
+}
+
+double frobenius_norm(const Csr& A) {
+    double s = 0.0;
+    for (double x : A.v) s += x * x;
+    return std::sqrt(s);
+}
+
+} // namespace ilug

@@ -1,0 +1,238 @@
+#include "ilu.hpp"
+
+#include <atomic>
+#include <cmath>
+#include <limits>
+#include <queue>
+
+namespace ilug {
+
+namespace {
+
+double row_norm2(const Csr& A, i64 i) {
+    double s = 0.0;
+    for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) s += A.v[k] * A.v[k];
+    return std::sqrt(s);
+}
+
+// Zero-pivot policy (src/ilu.cpp:23-31): `error` aborts, `replace` substitutes
+// sign(estimate) * max(droptol*|a_i|_2, 1e-16*|A|_F) (DBL_MIN if that is 0).
+double patch_pivot(double droptol, double rownorm, double anorm_f, PivotPatch policy, i64 step) {
+    if (policy == PivotPatch::error)
+        fail_numeric("zero pivot at step " + std::to_string(step) +
+                     " (no pivoting; rerun with pivot_patch=replace to substitute)");
+    double mag = std::max(droptol * rownorm, 1e-16 * anorm_f);
+    if (mag == 0.0) mag = std::numeric_limits<double>::min();
+    return mag; // the estimate is always 0.0 here, so the sign is +
+}
+
+} // namespace
+
+HostFactors ilu0(const Csr& A, PivotPatch patch) {
+    if (A.nrows != A.ncols) fail_invalid("ilu0: matrix must be square");
+    const i64 n = A.nrows;
+    std::vector<i64> dpos(static_cast<size_t>(n), -1);
+    for (i64 i = 0; i < n; ++i) {
+        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k)
+            if (A.ci[k] == i) dpos[i] = k;
+        if (dpos[i] < 0)
+            fail_invalid("ilu0: diagonal entry (" + std::to_string(i) + "," + std::to_string(i) +
+                         ") is structurally absent");
+    }
+    const double anorm_f = frobenius_norm(A);
+
+    // Wavefront levels of the lower-pattern DAG.
+    std::vector<i32> level(static_cast<size_t>(n), 0);
+    i32 nlev = 0;
+    for (i64 i = 0; i < n; ++i) {
+        i32 l = 0;
+        for (i64 k = A.rp[i]; k < dpos[i]; ++k) l = std::max(l, level[A.ci[k]] + 1);
+        level[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    std::vector<i64> lstart(static_cast<size_t>(nlev) + 1, 0), order(static_cast<size_t>(n));
+    for (i64 i = 0; i < n; ++i) ++lstart[level[i] + 1];
+    for (i32 l = 0; l < nlev; ++l) lstart[l + 1] += lstart[l];
+    {
+        std::vector<i64> cur(lstart.begin(), lstart.end() - 1);
+        for (i64 i = 0; i < n; ++i) order[cur[level[i]]++] = i;
+    }
+
+    std::vector<double> w(A.v);
+    std::atomic<i64> first_zero{n};
+    for (i32 l = 0; l < nlev; ++l) {
+        parallel_ranges(lstart[l + 1] - lstart[l], [&](i64 b, i64 e, int) {
+            for (i64 t = lstart[l] + b; t < lstart[l] + e; ++t) {
+                const i64 i = order[t];
+                const i64 end = A.rp[i + 1];
+                for (i64 k = A.rp[i]; k < dpos[i]; ++k) {
+                    const i64 c = A.ci[k];
+                    const double m = w[k] / w[dpos[c]];
+                    w[k] = m;
+                    // merge row c's strict upper part against row i's tail
+                    i64 p = k + 1;
+                    for (i64 kk = dpos[c] + 1; kk < A.rp[c + 1] && p < end; ++kk) {
+                        const i32 j = A.ci[kk];
+                        while (p < end && A.ci[p] < j) ++p;
+                        if (p < end && A.ci[p] == j) w[p] -= m * w[kk];
+                    }
+                }
+                if (w[dpos[i]] == 0.0) {
+                    if (patch == PivotPatch::error) {
+                        i64 cur = first_zero.load();
+                        while (i < cur && !first_zero.compare_exchange_weak(cur, i)) {
+                        }
+                        w[dpos[i]] = 1.0; // placeholder; the factorisation is abandoned
+                    } else {
+                        w[dpos[i]] = patch_pivot(0.0, row_norm2(A, i), anorm_f, patch, i);
+                    }
+                }
+            }
+        }, 256);
+    }
+    if (first_zero.load() < n) patch_pivot(0.0, 0.0, 0.0, PivotPatch::error, first_zero.load());
+
+    // Split into strict L and U (with diagonal), row-parallel.
+    HostFactors f;
+    for (Csr* M : {&f.L, &f.U}) {
+        M->nrows = M->ncols = n;
+        M->rp.assign(static_cast<size_t>(n) + 1, 0);
+    }
+    for (i64 i = 0; i < n; ++i) {
+        f.L.rp[i + 1] = f.L.rp[i] + (dpos[i] - A.rp[i]);
+        f.U.rp[i + 1] = f.U.rp[i] + (A.rp[i + 1] - dpos[i]);
+    }
+    f.L.ci.resize(static_cast<size_t>(f.L.rp[n]));
+    f.L.v.resize(static_cast<size_t>(f.L.rp[n]));
+    f.U.ci.resize(static_cast<size_t>(f.U.rp[n]));
+    f.U.v.resize(static_cast<size_t>(f.U.rp[n]));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            i64 pl = f.L.rp[i], pu = f.U.rp[i];
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                if (k < dpos[i])
+                    f.L.ci[pl] = A.ci[k], f.L.v[pl++] = w[k];
+                else
+                    f.U.ci[pu] = A.ci[k], f.U.v[pu++] = w[k];
+            }
+        }
+    });
+    return f;
+}
+
+HostFactors ilut(const Csr& A, const IluParams& p) {
+    if (A.nrows != A.ncols) fail_invalid("ilut: matrix must be square");
+    if (!(p.droptol >= 0.0) || !std::isfinite(p.droptol))
+        fail_invalid("ilut: droptol must be finite and >= 0");
+    if (p.lfill < 0) fail_invalid("ilut: lfill must be >= 0");
+    const i64 n = A.nrows;
+    const double anorm_f = frobenius_norm(A);
+
+    HostFactors f;
+    f.L.nrows = f.L.ncols = f.U.nrows = f.U.ncols = n;
+    f.L.rp.assign(1, 0);
+    f.U.rp.assign(1, 0);
+    f.L.rp.reserve(static_cast<size_t>(n) + 1);
+    f.U.rp.reserve(static_cast<size_t>(n) + 1);
+    std::vector<i64> udiag_pos(static_cast<size_t>(n), -1);
+
+    std::vector<double> w(static_cast<size_t>(n), 0.0);
+    std::vector<char> live(static_cast<size_t>(n), 0), orig(static_cast<size_t>(n), 0);
+    std::vector<i64> upper, kept, pat_part, fill_part;
+    std::priority_queue<i64, std::vector<i64>, std::greater<i64>> pending;
+
+    // Survivor selection (src/ilu.cpp:204-232): pattern entries pass on the
+    // threshold (applied to the U part only), fill competes for lfill slots.
+    auto select = [&](const std::vector<i64>& cols, bool lower, double tau) {
+        pat_part.clear();
+        fill_part.clear();
+        for (i64 j : cols) {
+            if (!live[j]) continue;
+            if (!lower && std::abs(w[j]) < tau) continue;
+            (orig[j] ? pat_part : fill_part).push_back(j);
+        }
+        const auto cap = static_cast<size_t>(p.lfill);
+        if (fill_part.size() > cap) {
+            std::nth_element(fill_part.begin(), fill_part.begin() + static_cast<std::ptrdiff_t>(cap),
+                             fill_part.end(), [&](i64 a, i64 b) {
+                                 const double va = std::abs(w[a]), vb = std::abs(w[b]);
+                                 return va != vb ? va > vb : a < b;
+                             });
+            fill_part.resize(cap);
+        }
+        pat_part.insert(pat_part.end(), fill_part.begin(), fill_part.end());
+        std::sort(pat_part.begin(), pat_part.end());
+    };
+
+    for (i64 i = 0; i < n; ++i) {
+        const double tau = p.droptol * row_norm2(A, i);
+        upper.clear();
+        kept.clear();
+        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const i64 j = A.ci[k];
+            w[j] = A.v[k];
+            live[j] = 1;
+            orig[j] = 1;
+            if (j < i)
+                pending.push(j);
+            else if (j > i)
+                upper.push_back(j);
+        }
+        while (!pending.empty()) {
+            const i64 k = pending.top();
+            pending.pop();
+            if (!live[k]) continue;
+            const double m = w[k] / f.U.v[udiag_pos[k]];
+            if (std::abs(m) < tau) {
+                w[k] = 0.0;
+                live[k] = 0;
+                continue;
+            }
+            w[k] = m;
+            kept.push_back(k);
+            for (i64 kk = udiag_pos[k] + 1; kk < f.U.rp[k + 1]; ++kk) {
+                const i64 j = f.U.ci[kk];
+                w[j] -= m * f.U.v[kk];
+                if (!live[j]) {
+                    live[j] = 1;
+                    if (j < i)
+                        pending.push(j);
+                    else if (j > i)
+                        upper.push_back(j);
+                }
+            }
+        }
+
+        select(kept, true, tau);
+        for (i64 j : pat_part) {
+            f.L.ci.push_back(static_cast<i32>(j));
+            f.L.v.push_back(w[j]);
+        }
+        f.L.rp.push_back(static_cast<i64>(f.L.ci.size()));
+
+        double d = w[i];
+        if (d == 0.0) d = patch_pivot(p.droptol, row_norm2(A, i), anorm_f, p.pivot_patch, i);
+        udiag_pos[i] = static_cast<i64>(f.U.ci.size());
+        f.U.ci.push_back(static_cast<i32>(i));
+        f.U.v.push_back(d);
+        select(upper, false, tau);
+        for (i64 j : pat_part) {
+            f.U.ci.push_back(static_cast<i32>(j));
+            f.U.v.push_back(w[j]);
+        }
+        f.U.rp.push_back(static_cast<i64>(f.U.ci.size()));
+
+        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) orig[A.ci[k]] = 0;
+        for (i64 j : kept) w[j] = 0.0, live[j] = 0;
+        w[i] = 0.0;
+        live[i] = 0;
+        for (i64 j : upper) w[j] = 0.0, live[j] = 0;
+    }
+    return f;
+}
+
+HostFactors ilu_factorize(const Csr& A, const IluParams& p) {
+    return p.variant == IluVariant::ilu0 ? ilu0(A, p.pivot_patch) : ilut(A, p);
+}
+
+} // namespace ilug

@@ -1,0 +1,312 @@
+#include "problems.hpp"
+
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <random>
+#include <sstream>
+
+namespace ilug {
+
+namespace {
+
+std::uint64_t splitmix(std::uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// Build a CSR from a per-row emitter: pass 1 counts, pass 2 fills, both
+// row-parallel. emit(i, cols, vals) must produce strictly increasing columns.
+template <typename Emit>
+Csr build_rows(i64 n, i64 ncols, int max_per_row, Emit emit) {
+    Csr A;
+    A.nrows = n;
+    A.ncols = ncols;
+    A.rp.assign(static_cast<size_t>(n) + 1, 0);
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        i32 c[64];
+        double v[64];
+        for (i64 i = b; i < e; ++i) A.rp[i + 1] = emit(i, c, v);
+    });
+    for (i64 i = 0; i < n; ++i) A.rp[i + 1] += A.rp[i];
+    A.ci.resize(static_cast<size_t>(A.rp[n]));
+    A.v.resize(static_cast<size_t>(A.rp[n]));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        i32 c[64];
+        double v[64];
+        for (i64 i = b; i < e; ++i) {
+            const int m = emit(i, c, v);
+            std::copy(c, c + m, A.ci.begin() + A.rp[i]);
+            std::copy(v, v + m, A.v.begin() + A.rp[i]);
+        }
+    });
+    (void)max_per_row;
+    return A;
+}
+
+void check_grid(i64 nx, i64 ny, i64 nz, const char* what) {
+    if (nx < 1 || ny < 1 || nz < 1) fail_invalid(std::string(what) + ": grid dimensions must be >= 1");
+    if (nx * ny * nz > 0x7fffffffLL) fail_invalid(std::string(what) + ": more than 2^31-1 rows");
+}
+
+} // namespace
+
+double hash_unit(std::uint64_t seed, std::uint64_t index) {
+    return static_cast<double>(splitmix(seed ^ splitmix(index)) >> 11) * 0x1.0p-53;
+}
+
+Vec random_uniform(i64 n, std::uint64_t seed) {
+    std::mt19937_64 gen(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    Vec v(static_cast<size_t>(n));
+    for (double& x : v) x = dist(gen);
+    return v;
+}
+
+Csr poisson1d(i64 n) {
+    if (n < 1) fail_invalid("poisson1d: n must be >= 1");
+    return build_rows(n, n, 3, [n](i64 i, i32* c, double* v) {
+        int m = 0;
+        if (i > 0) c[m] = static_cast<i32>(i - 1), v[m++] = -1.0;
+        c[m] = static_cast<i32>(i), v[m++] = 2.0;
+        if (i + 1 < n) c[m] = static_cast<i32>(i + 1), v[m++] = -1.0;
+        return m;
+    });
+}
+
+Csr anisotropic2d(i64 nx, i64 ny, double eps) {
+    if (nx < 1 || ny < 1) fail_invalid("anisotropic2d: grid dimensions must be >= 1");
+    if (!(eps > 0.0)) fail_invalid("anisotropic2d: eps must be > 0");
+    const double diag = 2.0 * eps + 2.0;
+    return build_rows(nx * ny, nx * ny, 5, [=](i64 i, i32* c, double* v) {
+        const i64 ix = i % nx, iy = i / nx;
+        int m = 0;
+        if (iy > 0) c[m] = static_cast<i32>(i - nx), v[m++] = -1.0;
+        if (ix > 0) c[m] = static_cast<i32>(i - 1), v[m++] = -eps;
+        c[m] = static_cast<i32>(i), v[m++] = diag;
+        if (ix + 1 < nx) c[m] = static_cast<i32>(i + 1), v[m++] = -eps;
+        if (iy + 1 < ny) c[m] = static_cast<i32>(i + nx), v[m++] = -1.0;
+        return m;
+    });
+}
+
+Csr poisson3d(i64 nx, i64 ny, i64 nz) {
+    check_grid(nx, ny, nz, "poisson3d");
+    const i64 pl = nx * ny;
+    return build_rows(pl * nz, pl * nz, 7, [=](i64 i, i32* c, double* v) {
+        const i64 ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
+        int m = 0;
+        auto put = [&](i64 j, double x) { c[m] = static_cast<i32>(j), v[m++] = x; };
+        if (iz > 0) put(i - pl, -1.0);
+        if (iy > 0) put(i - nx, -1.0);
+        if (ix > 0) put(i - 1, -1.0);
+        put(i, 6.0);
+        if (ix + 1 < nx) put(i + 1, -1.0);
+        if (iy + 1 < ny) put(i + nx, -1.0);
+        if (iz + 1 < nz) put(i + pl, -1.0);
+        return m;
+    });
+}
+
+namespace {
+
+template <typename Coef>
+Csr box27(i64 nx, i64 ny, i64 nz, Coef coef) {
+    const i64 pl = nx * ny;
+    return build_rows(pl * nz, pl * nz, 27, [=](i64 i, i32* c, double* v) {
+        const i64 ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
+        int m = 0, dpos = -1;
+        double diag = 0.0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (dx == 0 && dy == 0 && dz == 0) {
+                        dpos = m;
+                        c[m] = static_cast<i32>(i), v[m++] = 0.0;
+                        continue;
+                    }
+                    const int dist = (dx != 0) + (dy != 0) + (dz != 0);
+                    const bool inside = ix + dx >= 0 && ix + dx < nx && iy + dy >= 0 &&
+                                        iy + dy < ny && iz + dz >= 0 && iz + dz < nz;
+                    const i64 j = inside ? i + dz * pl + dy * nx + dx : -1;
+                    const double a = coef(i, j, dist); // off-diagonal magnitude
+                    diag += a;
+                    if (inside) c[m] = static_cast<i32>(j), v[m++] = -a;
+                }
+        v[dpos] = diag;
+        return m;
+    });
+}
+
+} // namespace
+
+Csr stencil27(i64 nx, i64 ny, i64 nz) {
+    check_grid(nx, ny, nz, "stencil27");
+    return box27(nx, ny, nz, [](i64, i64, int) { return 1.0; });
+}
+
+Csr pressure27(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
+    check_grid(nx, ny, nz, "pressure27");
+    auto kappa = [seed](i64 i) {
+        return std::pow(10.0, 4.0 * hash_unit(seed, static_cast<std::uint64_t>(i)) - 2.0);
+    };
+    return box27(nx, ny, nz, [=](i64 i, i64 j, int dist) {
+        const double w = dist == 1 ? 1.0 : (dist == 2 ? 0.5 : 0.25);
+        const double ki = kappa(i);
+        if (j < 0) return w * ki; // out-of-grid slot: hm(ki, ki) = ki
+        const double kj = kappa(j);
+        return w * (2.0 * ki * kj / (ki + kj));
+    });
+}
+
+Csr cutcell(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
+    check_grid(nx, ny, nz, "cutcell");
+    const i64 pl = nx * ny;
+    const double R = 0.3 * static_cast<double>(nx);
+    const double cx = 0.5 * nx, cy = 0.5 * ny, cz = 0.5 * nz;
+    auto cell = [=](i64 i, double& kappa, double& rho) {
+        const double x = static_cast<double>(i % nx) + 0.5 - cx;
+        const double y = static_cast<double>((i / nx) % ny) + 0.5 - cy;
+        const double z = static_cast<double>(i / pl) + 0.5 - cz;
+        const double r = std::sqrt(x * x + y * y + z * z);
+        rho = r < R ? 1000.0 : 1.0;
+        kappa = std::abs(r - R) < 0.75
+                    ? std::pow(10.0, 16.0 * hash_unit(seed, static_cast<std::uint64_t>(i)))
+                    : 1.0;
+    };
+    return build_rows(pl * nz, pl * nz, 7, [=](i64 i, i32* c, double* v) {
+        const i64 ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
+        double ki, ri;
+        cell(i, ki, ri);
+        auto face = [&](bool inside, i64 j) {
+            if (!inside) return ki / ri; // mirrored cell: (ki+ki)/2 * 2/(ri+ri)
+            double kj, rj;
+            cell(j, kj, rj);
+            return (ki + kj) / 2.0 * (2.0 / (ri + rj));
+        };
+        const bool in[6] = {iz > 0, iy > 0, ix > 0, ix + 1 < nx, iy + 1 < ny, iz + 1 < nz};
+        const i64 nb[6] = {i - pl, i - nx, i - 1, i + 1, i + nx, i + pl};
+        double f[6], diag = 0.0;
+        for (int s = 0; s < 6; ++s) {
+            f[s] = face(in[s], nb[s]);
+            diag += f[s];
+        }
+        int m = 0;
+        for (int s = 0; s < 3; ++s)
+            if (in[s]) c[m] = static_cast<i32>(nb[s]), v[m++] = -f[s];
+        c[m] = static_cast<i32>(i), v[m++] = diag;
+        for (int s = 3; s < 6; ++s)
+            if (in[s]) c[m] = static_cast<i32>(nb[s]), v[m++] = -f[s];
+        return m;
+    });
+}
+
+namespace {
+const char* kSpecs[] = {"poisson1d(",  "poisson2d(", "anisotropic2d(", "poisson3d(",
+                        "stencil27(",  "pressure27(", "cutcell("};
+}
+
+bool is_generator_spec(const std::string& s) {
+    for (const char* p : kSpecs)
+        if (s.rfind(p, 0) == 0) return true;
+    return false;
+}
+
+Csr generate_problem(const std::string& spec) {
+    const auto open = spec.find('('), close = spec.rfind(')');
+    if (open == std::string::npos || close == std::string::npos || close < open)
+        fail_invalid("generate_problem: malformed spec '" + spec + "'");
+    const std::string kind = spec.substr(0, open);
+    std::string args = spec.substr(open + 1, close - open - 1);
+    for (char& ch : args)
+        if (ch == ',') ch = ' ';
+    std::istringstream in(args);
+    auto need = [&](bool ok, const char* sig) {
+        if (!ok) fail_invalid("generate_problem: " + kind + " expects " + sig);
+    };
+    if (kind == "poisson1d") {
+        i64 n = 0;
+        need(static_cast<bool>(in >> n), "(n)");
+        return poisson1d(n);
+    }
+    if (kind == "poisson2d" || kind == "anisotropic2d") {
+        i64 nx = 0, ny = 0;
+        double eps = 1.0;
+        if (kind == "poisson2d")
+            need(static_cast<bool>(in >> nx >> ny), "(nx,ny)");
+        else
+            need(static_cast<bool>(in >> nx >> ny >> eps), "(nx,ny,eps)");
+        return anisotropic2d(nx, ny, eps);
+    }
+    i64 nx = 0, ny = 0, nz = 0;
+    need(static_cast<bool>(in >> nx >> ny >> nz), "(nx,ny,nz[,seed])");
+    std::uint64_t seed = 2111;
+    {
+        unsigned long long s;
+        if (in >> s) seed = s;
+    }
+    if (kind == "poisson3d") return poisson3d(nx, ny, nz);
+    if (kind == "stencil27") return stencil27(nx, ny, nz);
+    if (kind == "pressure27") return pressure27(nx, ny, nz, seed);
+    if (kind == "cutcell") return cutcell(nx, ny, nz, seed);
+    fail_invalid("generate_problem: unknown generator '" + kind + "'");
+}
+
+Csr mm_read(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) fail_io("mm_read: cannot open '" + path + "'");
+    std::string line;
+    if (!std::getline(in, line)) fail_io("mm_read: '" + path + "' is empty");
+    std::istringstream hdr(line);
+    std::string banner, object, format, field, sym;
+    hdr >> banner >> object >> format >> field >> sym;
+    auto low = [](std::string s) {
+        for (char& ch : s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+        return s;
+    };
+    if (banner != "%%MatrixMarket" || low(object) != "matrix")
+        fail_io("mm_read: '" + path + "' has a malformed Matrix Market header");
+    format = low(format), field = low(field), sym = low(sym);
+    if (format != "coordinate") fail_io("mm_read: only coordinate format is supported (got '" + format + "')");
+    if (field == "complex" || field == "pattern")
+        fail_io("mm_read: field type '" + field + "' is not supported; real matrices only");
+    if (field != "real" && field != "integer") fail_io("mm_read: unsupported field type '" + field + "'");
+    if (sym != "general" && sym != "symmetric")
+        fail_io("mm_read: unsupported symmetry '" + sym + "'; general and symmetric only");
+    const bool symmetric = sym == "symmetric";
+    while (std::getline(in, line))
+        if (!line.empty() && line[0] != '%') break;
+    std::istringstream sz(line);
+    i64 nr = 0, nc = 0, nnz = 0;
+    if (!(sz >> nr >> nc >> nnz) || nr < 0 || nc < 0 || nnz < 0)
+        fail_io("mm_read: '" + path + "' has a malformed size line");
+    std::vector<Triplet> t;
+    t.reserve(static_cast<size_t>(symmetric ? 2 * nnz : nnz));
+    for (i64 k = 0; k < nnz; ++k) {
+        i64 i = 0, j = 0;
+        double v = 0.0;
+        if (!(in >> i >> j >> v)) fail_io("mm_read: '" + path + "' truncated at entry " + std::to_string(k + 1));
+        if (i < 1 || i > nr || j < 1 || j > nc)
+            fail_io("mm_read: '" + path + "' index out of range at entry " + std::to_string(k + 1));
+        t.push_back({i - 1, j - 1, v});
+        if (symmetric && i != j) t.push_back({j - 1, i - 1, v});
+    }
+    return csr_from_triplets(nr, nc, std::move(t));
+}
+
+void mm_write(const Csr& A, const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) fail_io("mm_write: cannot open '" + path + "' for writing");
+    std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n",
+                 static_cast<long long>(A.nrows), static_cast<long long>(A.ncols),
+                 static_cast<long long>(A.nnz()));
+    for (i64 i = 0; i < A.nrows; ++i)
+        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k)
+            std::fprintf(f, "%lld %d %.17g\n", static_cast<long long>(i + 1), A.ci[k] + 1, A.v[k]);
+    if (std::fclose(f) != 0) fail_io("mm_write: write to '" + path + "' failed");
+}
+
+} // namespace ilug

@@ -1,0 +1,289 @@
+// BLAS-1 building blocks and the CGS2 orthogonalisation kernels (K8), plus
+// the coarse dense LU solve (K7).
+//
+// Reductions are deterministic: a fixed tiling (1024 rows per block), a fixed
+// in-block order (per-thread sequential, then warp shuffles, then warps in
+// order) and a single-block final pass over the per-block partials in order.
+// Repeated runs are bitwise identical; against the reference's sequential dot
+// (src/krylov.cpp:38-42) they differ only by summation order.
+#include "ops.hpp"
+
+namespace ilug {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kRows = 4;                 // rows per thread in the tiled reductions
+constexpr int kTile = kBlock * kRows;    // rows per block
+constexpr int kMaxVec = 64;              // max basis vectors per fused call (restart <= 63)
+
+inline unsigned ew_grid(i64 n) {
+    const i64 g = (n + kBlock - 1) / kBlock;
+    return static_cast<unsigned>(std::max<i64>(1, std::min<i64>(g, 148 * 64)));
+}
+
+__global__ void k_div(double* __restrict__ o, const double* __restrict__ a, const double* __restrict__ d,
+                      i64 n) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        o[i] = a[i] / d[i];
+}
+__global__ void k_acc(double* __restrict__ x, const double* __restrict__ z, i64 n) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        x[i] = x[i] + z[i];
+}
+__global__ void k_acc_div(double* __restrict__ x, const double* __restrict__ z,
+                          const double* __restrict__ d, i64 n) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        x[i] = x[i] + z[i] / d[i];
+}
+__global__ void k_scale_div(double* o, const double* w, double h, i64 n) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        o[i] = w[i] / h;
+}
+__global__ void k_sub_into(double* __restrict__ o, const double* __restrict__ a,
+                           const double* __restrict__ b, i64 n) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        o[i] = a[i] - b[i];
+}
+__global__ void k_add_into(double* __restrict__ o, const double* __restrict__ a,
+                           const double* __restrict__ b, i64 n) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        o[i] = a[i] + b[i];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Sum `per` values of thread-local partials for k outputs over the block:
+// red[w][j] per warp, then warps summed in order by thread j.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ hin,
+        double* __restrict__ w, const double* __restrict__ w2, i64 n, double* __restrict__ partial) {
+    // MODE 0: dot(w, w2) -> 1 output; MODE 1: ||w||^2; MODE 2: V^T w (k outputs);
+    // MODE 3: w -= V hin, then V^T w; MODE 4: w -= V hin, then ||w||^2.
+    __shared__ double red[kBlock / 32][kMaxVec];
+    __shared__ double hs[kMaxVec];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const i64 base = blockIdx.x * static_cast<i64>(kTile) + threadIdx.x;
+    if (MODE == 3 || MODE == 4) {
+        for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = hin[j];
+        __syncthreads();
+    }
+    double wv[kRows];
+#pragma unroll
+    for (int u = 0; u < kRows; ++u) {
+        const i64 i = base + u * kBlock;
+        wv[u] = i < n ? w[i] : 0.0;
+    }
+    if (MODE == 3 || MODE == 4) {
+        for (int j = 0; j < k; ++j) {
+            const double hj = hs[j];
+#pragma unroll
+            for (int u = 0; u < kRows; ++u) {
+                const i64 i = base + u * kBlock;
+                if (i < n) wv[u] = wv[u] - hj * V[j * ld + i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            const i64 i = base + u * kBlock;
+            if (i < n) w[i] = wv[u];
+        }
+    }
+    int nout = 1;
+    if (MODE == 0 || MODE == 1 || MODE == 4) {
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            const i64 i = base + u * kBlock;
+            const double o = MODE == 0 ? (i < n ? w2[i] : 0.0) : wv[u];
+            s += wv[u] * o;
+        }
+        s = warp_sum(s);
+        if (lane == 0) red[warp][0] = s;
+    } else {
+        nout = k;
+        for (int j = 0; j < k; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < kRows; ++u) {
+                const i64 i = base + u * kBlock;
+                if (i < n) s += V[j * ld + i] * wv[u];
+            }
+            s = warp_sum(s);
+            if (lane == 0) red[warp][j] = s;
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nout; j += blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < kBlock / 32; ++q) s += red[q][j];
+        partial[blockIdx.x * static_cast<i64>(kMaxVec) + j] = s;
+    }
+}
+
+// out[j] = sum over blocks b (in order, tree within one block) of partial[b][j]
+__global__ void k_finish(const double* __restrict__ partial, i64 nblocks, int nout,
+                         double* __restrict__ out) {
+    __shared__ double sm[kBlock];
+    for (int j = 0; j < nout; ++j) {
+        double s = 0.0;
+        for (i64 b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[b * kMaxVec + j];
+        sm[threadIdx.x] = s;
+        __syncthreads();
+        for (int o = kBlock / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[j] = sm[0];
+        __syncthreads();
+    }
+}
+
+__global__ void k_combine(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ c,
+                          const double* __restrict__ base, double* __restrict__ y, i64 n) {
+    __shared__ double cs[kMaxVec];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) cs[j] = c[j];
+    __syncthreads();
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        double s = base ? base[i] : 0.0;
+        for (int j = 0; j < k; ++j) s = s + cs[j] * V[j * ld + i];
+        y[i] = s;
+    }
+}
+
+// Thread-private scratch for the two-stage reductions, one per device.
+struct Scratch {
+    DBuf<double> partial;
+    i64 cap = 0;
+};
+Scratch& scratch() {
+    static thread_local Scratch s;
+    return s;
+}
+
+template <int MODE>
+void tiled(const double* V, i64 ld, int k, const double* hin, double* w, const double* w2, i64 n,
+           double* out, int nout, cudaStream_t st) {
+    if (k > kMaxVec) fail_invalid("CGS2: more than 64 basis vectors per call");
+    const i64 nb = std::max<i64>(1, (n + kTile - 1) / kTile);
+    Scratch& sc = scratch();
+    if (sc.cap < nb) {
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        sc.partial.alloc(nb * kMaxVec);
+        sc.cap = nb;
+    }
+    k_tiled<MODE><<<static_cast<unsigned>(nb), kBlock, 0, st>>>(V, ld, k, hin, w, w2, n, sc.partial.p);
+    ILUG_LAUNCH_CHECK();
+    k_finish<<<1, kBlock, 0, st>>>(sc.partial.p, nb, nout, out);
+    ILUG_LAUNCH_CHECK();
+}
+
+// K7: x = LU \ P b (src/dense.cpp:40-55). Forward elimination is parallel over
+// rows i > k (each x_i still receives its updates in ascending k); back
+// substitution runs on one thread to keep the reference's summation order.
+__global__ void k_dense_solve(i64 n, const double* __restrict__ lu, const i64* __restrict__ piv,
+                              const double* __restrict__ b, double* __restrict__ x) {
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[i];
+    __syncthreads();
+    for (i64 k = 0; k < n; ++k) {
+        if (threadIdx.x == 0 && piv[k] != k) {
+            const double t = x[piv[k]];
+            x[piv[k]] = x[k];
+            x[k] = t;
+        }
+        __syncthreads();
+        const double xk = x[k];
+        for (i64 i = k + 1 + threadIdx.x; i < n; i += blockDim.x) x[i] = x[i] - lu[i * n + k] * xk;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (i64 i = n; i-- > 0;) {
+            double s = x[i];
+            for (i64 j = i + 1; j < n; ++j) s = s - lu[i * n + j] * x[j];
+            x[i] = s / lu[i * n + i];
+        }
+}
+
+} // namespace
+
+void vec_copy(double* d, const double* s, i64 n, cudaStream_t st) {
+    if (n <= 0 || d == s) return;
+    ILUG_CUDA(cudaMemcpyAsync(d, s, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+void vec_zero(double* d, i64 n, cudaStream_t st) {
+    if (n > 0) ILUG_CUDA(cudaMemsetAsync(d, 0, static_cast<size_t>(n) * sizeof(double), st));
+}
+void vec_div(double* o, const double* a, const double* d, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_div<<<ew_grid(n), kBlock, 0, st>>>(o, a, d, n);
+    ILUG_LAUNCH_CHECK();
+}
+void vec_acc(double* x, const double* z, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_acc<<<ew_grid(n), kBlock, 0, st>>>(x, z, n);
+    ILUG_LAUNCH_CHECK();
+}
+void vec_acc_div(double* x, const double* z, const double* d, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_acc_div<<<ew_grid(n), kBlock, 0, st>>>(x, z, d, n);
+    ILUG_LAUNCH_CHECK();
+}
+void vec_scale_div(double* o, const double* w, double h, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_scale_div<<<ew_grid(n), kBlock, 0, st>>>(o, w, h, n);
+    ILUG_LAUNCH_CHECK();
+}
+void vec_add_into(double* o, const double* a, const double* b, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_add_into<<<ew_grid(n), kBlock, 0, st>>>(o, a, b, n);
+    ILUG_LAUNCH_CHECK();
+}
+void vec_sub_into(double* o, const double* a, const double* b, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_sub_into<<<ew_grid(n), kBlock, 0, st>>>(o, a, b, n);
+    ILUG_LAUNCH_CHECK();
+}
+void dot_dev(const double* a, const double* b, i64 n, double* out, cudaStream_t st) {
+    tiled<0>(nullptr, 0, 0, nullptr, const_cast<double*>(a), b, n, out, 1, st);
+}
+void nrm2sq_dev(const double* a, i64 n, double* out, cudaStream_t st) {
+    tiled<1>(nullptr, 0, 0, nullptr, const_cast<double*>(a), nullptr, n, out, 1, st);
+}
+void multi_dot(const double* V, i64 ld, int k, const double* w, i64 n, double* h, cudaStream_t st) {
+    tiled<2>(V, ld, k, nullptr, const_cast<double*>(w), nullptr, n, h, k, st);
+}
+void multi_axpy_dot(const double* V, i64 ld, int k, const double* hin, double* w, i64 n, double* hout,
+                    cudaStream_t st) {
+    tiled<3>(V, ld, k, hin, w, nullptr, n, hout, k, st);
+}
+void multi_axpy_nrm(const double* V, i64 ld, int k, const double* hin, double* w, i64 n, double* out,
+                    cudaStream_t st) {
+    tiled<4>(V, ld, k, hin, w, nullptr, n, out, 1, st);
+}
+void multi_combine(const double* V, i64 ld, int k, const double* c, const double* base, double* y,
+                   i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    if (k > kMaxVec) fail_invalid("combine: more than 64 basis vectors");
+    k_combine<<<ew_grid(n), kBlock, 0, st>>>(V, ld, k, c, base, y, n);
+    ILUG_LAUNCH_CHECK();
+}
+void dense_lu_solve_dev(i64 n, const double* lu, const i64* piv, const double* b, double* x,
+                        cudaStream_t st) {
+    if (n <= 0) return;
+    k_dense_solve<<<1, kBlock, 0, st>>>(n, lu, piv, b, x);
+    ILUG_LAUNCH_CHECK();
+}
+
+} // namespace ilug

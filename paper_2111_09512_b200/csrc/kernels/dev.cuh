@@ -1,0 +1,130 @@
+// Device-side vocabulary shared by every kernel TU: error checks, owned
+// device buffers, cache-hinted loads, and the SELL-32 matrix layout.
+//
+// Numerics contract: all kernels are compiled with --fmad=false, so a*b+c is a
+// rounded multiply followed by a rounded add exactly like the reference's x86-64
+// code (gcc -O2, no -march: no FMA). Thread-per-row kernels accumulate in
+// ascending column order from 0.0, which makes SpMV, residual and every sweep
+// bitwise identical to src/sparse.cpp:162-174 / src/trisolve.cpp:94-147.
+#pragma once
+
+#include "../host/common.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+namespace ilug {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define ILUG_CUDA(call)                                                   \
+    do {                                                                  \
+        cudaError_t e__ = (call);                                         \
+        if (e__ != cudaSuccess) ::ilug::cuda_fail(e__, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define ILUG_LAUNCH_CHECK() ILUG_CUDA(cudaGetLastError())
+
+constexpr int kSlice = 32; // SELL slice height = warp width: one row per lane
+
+/// Owned device allocation (cudaMalloc / cudaFree), move-only.
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    i64 n = 0;
+    DBuf() = default;
+    explicit DBuf(i64 count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n;
+            o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(i64 count) {
+        release();
+        n = count;
+        if (count > 0) ILUG_CUDA(cudaMalloc(&p, static_cast<size_t>(count) * sizeof(T)));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T* h, i64 count, cudaStream_t s = nullptr) {
+        if (count != n) alloc(count);
+        if (count > 0)
+            ILUG_CUDA(cudaMemcpyAsync(p, h, static_cast<size_t>(count) * sizeof(T),
+                                      cudaMemcpyHostToDevice, s));
+    }
+    void download(T* h, cudaStream_t s = nullptr) const {
+        if (n > 0)
+            ILUG_CUDA(cudaMemcpyAsync(h, p, static_cast<size_t>(n) * sizeof(T),
+                                      cudaMemcpyDeviceToHost, s));
+    }
+    i64 bytes() const { return n * static_cast<i64>(sizeof(T)); }
+};
+
+/// SELL-32 ("sliced ELLPACK", slice height 32, sigma = 1 or level-sorted):
+/// slice s stores its 32 rows column-major, entry t of lane l at
+/// slice_ptr[s] + 32*t + l, so a warp's t-th loads of values and columns are
+/// one fully coalesced 256 B / 128 B transaction. Per-row lengths predicate the
+/// loop (padding is never multiplied, so Inf/NaN propagate exactly as in CSR).
+/// Optional perm: SELL row p holds original row perm[p] (-1 = padding row);
+/// used for level-ordered copies where each level starts on a slice boundary.
+struct Sell {
+    i64 nrows = 0;   ///< logical rows (original numbering)
+    i64 ncols = 0;
+    i64 nrows_pad = 0; ///< SELL rows (multiple of 32)
+    i64 nnz = 0;     ///< stored (unpadded) entries
+    i64 padded = 0;  ///< entries incl. padding
+    int max_row = 0;
+    DBuf<i64> slice_ptr; ///< nrows_pad/32 + 1
+    DBuf<std::uint16_t> rowlen; ///< nrows_pad
+    DBuf<i32> cols;
+    DBuf<double> vals;
+    DBuf<i32> perm; ///< empty = identity
+    bool empty() const { return nrows == 0; }
+};
+
+/// Kernel-side view (trivially copyable).
+struct SellView {
+    const i64* __restrict__ slice_ptr;
+    const std::uint16_t* __restrict__ rowlen;
+    const i32* __restrict__ cols;
+    const double* __restrict__ vals;
+    const i32* __restrict__ perm;
+    i64 nrows_pad;
+};
+inline SellView view(const Sell& s) {
+    return {s.slice_ptr.p, s.rowlen.p, s.cols.p, s.vals.p, s.perm.p, s.nrows_pad};
+}
+
+int device_sm_count();
+
+} // namespace ilug
+
+#ifdef __CUDACC__
+namespace ilug {
+// Streaming (read-once) loads: bypass L1 allocation, keep L2 behaviour default.
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// Gathered vector entries: read-only path, cached (stencil reuse across rows).
+__device__ __forceinline__ double ld_gather(const double* p) { return __ldg(p); }
+} // namespace ilug
+#endif

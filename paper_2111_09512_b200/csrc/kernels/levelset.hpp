@@ -1,0 +1,37 @@
+// K5 level-scheduled solves (see levelset.cu).
+#pragma once
+
+#include "ops.hpp"
+
+namespace ilug {
+
+class LevelPlan {
+public:
+    enum class Kind { lower_unit, upper, gauss_seidel };
+
+    /// Analyse T's dependency DAG (strict lower part for lower_unit and
+    /// gauss_seidel, strict upper part for upper) and upload a level-ordered
+    /// SELL copy of T (all stored entries; the kernel skips the diagonal).
+    /// dev_vals (optional): device copy of T's values to use instead of T.v
+    /// (e.g. the K1-scaled U that only exists on the device).
+    void build(const Csr& T, Kind kind, cudaStream_t st, const double* dev_vals = nullptr);
+
+    /// lower_unit / upper: x = T^-1 b. gauss_seidel: x = one forward GS sweep
+    /// from xold (x and xold must differ).
+    void solve(const double* b, double* x, const double* xold, cudaStream_t st) const;
+
+    int levels() const { return nlev_; }
+    int grid() const { return grid_; }
+    const Sell& matrix() const { return M_; }
+
+private:
+    Kind kind_ = Kind::lower_unit;
+    Sell M_;
+    DBuf<i64> level_ptr_;
+    DBuf<unsigned> bar_;
+    int nlev_ = 0;
+    int grid_ = 1;
+    i64 max_level_rows_ = 0;
+};
+
+} // namespace ilug

@@ -1,0 +1,356 @@
+// SELL-32 construction and the thread-per-row product family (K2/K3/K6).
+//
+// One warp = one 32-row slice; lane l owns row 32*s + l and walks its entries
+// t = 0..len-1 at slice_ptr[s] + 32*t + l. Loads of values/columns are streamed
+// (L1 no-allocate, one 256 B / 128 B transaction per warp per t), the gathered
+// x entries go through the read-only cache where stencil neighbours hit.
+// Accumulation is ascending-column from 0.0 with separate multiply/add
+// (--fmad=false): bitwise equal to src/sparse.cpp:162-174.
+#include "ops.hpp"
+
+#include <cstdio>
+
+namespace ilug {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    const std::string msg = std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                            cudaGetErrorString(e) + ") in " + what + " at " + file + ":" +
+                            std::to_string(line);
+    // Launch/argument errors are caller errors (2); faults and OOM are numeric (3).
+    if (e == cudaErrorInvalidValue || e == cudaErrorInvalidConfiguration ||
+        e == cudaErrorInvalidDevicePointer || e == cudaErrorNoDevice ||
+        e == cudaErrorInsufficientDriver)
+        fail_invalid(msg);
+    fail_numeric(msg);
+}
+
+int device_sm_count() {
+    int dev = 0, n = 0;
+    ILUG_CUDA(cudaGetDevice(&dev));
+    ILUG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
+namespace {
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(i64 threads, int block = kBlock) {
+    return static_cast<unsigned>((threads + block - 1) / block);
+}
+
+// ---------------------------------------------------------------- SELL packing
+__global__ void k_sell_fill(i64 nrows_pad, const i32* __restrict__ perm, const i64* __restrict__ rp,
+                            const i32* __restrict__ ci, const double* __restrict__ v, int part,
+                            const i64* __restrict__ slice_ptr, i32* __restrict__ cols,
+                            double* __restrict__ vals) {
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= nrows_pad) return;
+    const i64 row = perm ? perm[p] : p;
+    if (row < 0) return;
+    i64 dst = slice_ptr[p >> 5] + (p & 31);
+    for (i64 k = rp[row]; k < rp[row + 1]; ++k) {
+        const i32 j = ci[k];
+        const bool keep = part == 0 || (part == 1 && j < row) || (part == 2 && j > row);
+        if (!keep) continue;
+        cols[dst] = j;
+        vals[dst] = v[k];
+        dst += kSlice;
+    }
+}
+
+__global__ void k_sell_unpack(i64 nrows_pad, const i32* __restrict__ perm,
+                              const i64* __restrict__ slice_ptr,
+                              const std::uint16_t* __restrict__ rowlen, const i32* __restrict__ cols,
+                              const double* __restrict__ vals, const i64* __restrict__ out_rp,
+                              i32* __restrict__ out_ci, double* __restrict__ out_v) {
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= nrows_pad) return;
+    const i64 row = perm ? perm[p] : p;
+    if (row < 0) return;
+    const i64 base = slice_ptr[p >> 5] + (p & 31);
+    i64 o = out_rp[row];
+    for (int t = 0; t < rowlen[p]; ++t, ++o) {
+        out_ci[o] = cols[base + static_cast<i64>(t) * kSlice];
+        out_v[o] = vals[base + static_cast<i64>(t) * kSlice];
+    }
+}
+
+// ------------------------------------------------------------ row products
+// Epilogues receive (row, s) with s the ascending-order row sum.
+struct EpiStore {
+    double* y;
+    __device__ void operator()(i64 r, double s) const { y[r] = s; }
+};
+struct EpiAdd {
+    double* acc;
+    __device__ void operator()(i64 r, double s) const { acc[r] = acc[r] + s; }
+};
+struct EpiResidual {
+    const double* b;
+    double* r;
+    __device__ void operator()(i64 i, double s) const { r[i] = b[i] - s; }
+};
+struct EpiDiv {
+    const double* rhs;
+    const double* d;
+    double* out;
+    __device__ void operator()(i64 i, double s) const { out[i] = (rhs[i] - s) / d[i]; }
+};
+struct EpiBoth {
+    const double* rhs;
+    const double* d;
+    double* out;
+    double* out2;
+    __device__ void operator()(i64 i, double s) const {
+        const double t = rhs[i] - s;
+        out[i] = t;
+        out2[i] = t / d[i];
+    }
+};
+struct EpiAcc {
+    const double* rhs;
+    double* acc;
+    __device__ void operator()(i64 i, double s) const { acc[i] = acc[i] + (rhs[i] - s); }
+};
+struct EpiAccDiv {
+    const double* rhs;
+    const double* d;
+    double* acc;
+    __device__ void operator()(i64 i, double s) const { acc[i] = acc[i] + (rhs[i] - s) / d[i]; }
+};
+struct EpiScaleAcc { // jacobi_like_sweep out of place: out = x + invd * (b - Ax)
+    const double* rhs;
+    const double* sc;
+    const double* xin;
+    double* out;
+    __device__ void operator()(i64 i, double s) const { out[i] = xin[i] + sc[i] * (rhs[i] - s); }
+};
+struct EpiScaleInit { // poly_gs: term = invd * r; acc = term
+    const double* rhs;
+    const double* sc;
+    double* term;
+    double* acc;
+    __device__ void operator()(i64 i, double s) const {
+        const double t = sc[i] * (rhs[i] - s);
+        term[i] = t;
+        acc[i] = t;
+    }
+};
+struct EpiNegScaleAcc { // poly_gs: term = -invd * t; acc += term
+    const double* sc;
+    double* term;
+    double* acc;
+    __device__ void operator()(i64 i, double s) const {
+        const double t = -sc[i] * s;
+        term[i] = t;
+        acc[i] = acc[i] + t;
+    }
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
+                                                    Epi epi) {
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= M.nrows_pad) return;
+    const i64 row = M.perm ? M.perm[p] : p;
+    if (row < 0 || row >= nrows) return;
+    const int len = M.rowlen[p];
+    const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
+    const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
+    double s = 0.0;
+    int t = 0;
+    // Four entries in flight per lane: issue the streamed loads, then the
+    // gathers, then accumulate in order (the order of the sum never changes).
+    for (; t + 4 <= len; t += 4) {
+        double a[4];
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = ld_stream(vp + (t + u) * kSlice);
+            c[u] = ld_stream(cp + (t + u) * kSlice);
+        }
+        double xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = ld_gather(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s = s + a[u] * xv[u];
+    }
+    for (; t < len; ++t) s = s + ld_stream(vp + t * kSlice) * ld_gather(x + ld_stream(cp + t * kSlice));
+    epi(row, s);
+}
+
+template <class Epi>
+void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
+    if (M.nrows_pad == 0) return;
+    k_rowdot<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    ILUG_LAUNCH_CHECK();
+}
+
+} // namespace
+
+// --------------------------------------------------------------- builders
+namespace {
+
+// rowlen per SELL row and slice offsets; `len_of(row)` gives the part length.
+template <typename LenOf>
+void layout(Sell& out, i64 nrows_pad, const std::vector<i32>& perm, LenOf len_of) {
+    std::vector<std::uint16_t> rl(static_cast<size_t>(nrows_pad), 0);
+    const i64 ns = nrows_pad / kSlice;
+    std::vector<i64> sp(static_cast<size_t>(ns) + 1, 0);
+    std::vector<i64> width(static_cast<size_t>(ns), 0);
+    std::vector<i64> nnz_part(static_cast<size_t>(std::max<i64>(ns, 1)), 0);
+    std::vector<int> mx(static_cast<size_t>(std::max<i64>(ns, 1)), 0);
+    bool too_long = false;
+    parallel_ranges(ns, [&](i64 b, i64 e, int) {
+        for (i64 s = b; s < e; ++s) {
+            i64 w = 0, tot = 0;
+            for (i64 l = 0; l < kSlice; ++l) {
+                const i64 p = s * kSlice + l;
+                const i64 row = perm.empty() ? p : perm[p];
+                const i64 len = (row < 0 || row >= out.nrows) ? 0 : len_of(row);
+                if (len > 65535) too_long = true;
+                rl[p] = static_cast<std::uint16_t>(len);
+                w = std::max(w, len);
+                tot += len;
+            }
+            width[s] = w;
+            nnz_part[s] = tot;
+            mx[s] = static_cast<int>(w);
+        }
+    });
+    if (too_long) fail_invalid("SELL: a row has more than 65535 entries");
+    for (i64 s = 0; s < ns; ++s) sp[s + 1] = sp[s] + width[s] * kSlice;
+    out.nrows_pad = nrows_pad;
+    out.padded = sp[ns];
+    out.nnz = 0;
+    out.max_row = 0;
+    for (i64 s = 0; s < ns; ++s) out.nnz += nnz_part[s], out.max_row = std::max(out.max_row, mx[s]);
+    out.slice_ptr.upload(sp.data(), ns + 1);
+    out.rowlen.upload(rl.data(), nrows_pad);
+    out.cols.alloc(out.padded);
+    out.vals.alloc(out.padded);
+    if (out.padded > 0) {
+        ILUG_CUDA(cudaMemset(out.cols.p, 0, static_cast<size_t>(out.padded) * sizeof(i32)));
+        ILUG_CUDA(cudaMemset(out.vals.p, 0, static_cast<size_t>(out.padded) * sizeof(double)));
+    }
+    if (!perm.empty())
+        out.perm.upload(perm.data(), nrows_pad);
+    else
+        out.perm.release();
+}
+
+i64 part_len(const Csr& A, i64 row, int pc) {
+    if (pc == 0) return A.rp[row + 1] - A.rp[row];
+    i64 c = 0;
+    for (i64 k = A.rp[row]; k < A.rp[row + 1]; ++k) c += pc == 1 ? A.ci[k] < row : A.ci[k] > row;
+    return c;
+}
+
+} // namespace
+
+void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i32* ci,
+                          const double* v, Part part, const std::vector<i32>& perm_host,
+                          cudaStream_t s) {
+    out.nrows = pattern.nrows;
+    out.ncols = pattern.ncols;
+    const i64 pad = perm_host.empty() ? (pattern.nrows + kSlice - 1) / kSlice * kSlice
+                                      : static_cast<i64>(perm_host.size());
+    const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
+    layout(out, pad, perm_host, [&](i64 row) { return part_len(pattern, row, pc); });
+    if (pad > 0 && pattern.nnz() > 0) {
+        k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.perm.p, rp, ci, v, pc,
+                                                     out.slice_ptr.p, out.cols.p, out.vals.p);
+        ILUG_LAUNCH_CHECK();
+    }
+}
+
+void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
+    out.nrows = A.nrows;
+    out.ncols = A.ncols;
+    const i64 pad = (A.nrows + kSlice - 1) / kSlice * kSlice;
+    const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
+    layout(out, pad, {}, [&](i64 row) { return part_len(A, row, pc); });
+    if (A.nnz() == 0 || pad == 0) return;
+    DBuf<i64> rp;
+    DBuf<i32> ci;
+    DBuf<double> v;
+    rp.upload(A.rp.data(), A.nrows + 1, s);
+    ci.upload(A.ci.data(), A.nnz(), s);
+    v.upload(A.v.data(), A.nnz(), s);
+    k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, nullptr, rp.p, ci.p, v.p, pc, out.slice_ptr.p,
+                                                 out.cols.p, out.vals.p);
+    ILUG_LAUNCH_CHECK();
+    ILUG_CUDA(cudaStreamSynchronize(s)); // temporaries die at scope exit
+}
+
+Csr sell_to_host(const Sell& M) {
+    Csr A;
+    A.nrows = M.nrows;
+    A.ncols = M.ncols;
+    std::vector<std::uint16_t> rl(static_cast<size_t>(M.nrows_pad));
+    std::vector<i32> perm(static_cast<size_t>(M.perm.n));
+    M.rowlen.download(rl.data());
+    if (M.perm.n) M.perm.download(perm.data());
+    ILUG_CUDA(cudaDeviceSynchronize());
+    A.rp.assign(static_cast<size_t>(M.nrows) + 1, 0);
+    for (i64 p = 0; p < M.nrows_pad; ++p) {
+        const i64 row = perm.empty() ? p : perm[p];
+        if (row >= 0 && row < M.nrows) A.rp[row + 1] = rl[p];
+    }
+    for (i64 i = 0; i < M.nrows; ++i) A.rp[i + 1] += A.rp[i];
+    A.ci.resize(static_cast<size_t>(A.rp[M.nrows]));
+    A.v.resize(static_cast<size_t>(A.rp[M.nrows]));
+    if (A.nnz() == 0) return A;
+    DBuf<i64> rp;
+    DBuf<i32> ci(A.nnz());
+    DBuf<double> v(A.nnz());
+    rp.upload(A.rp.data(), M.nrows + 1);
+    k_sell_unpack<<<grid_for(M.nrows_pad), kBlock>>>(M.nrows_pad, M.perm.p, M.slice_ptr.p, M.rowlen.p,
+                                                     M.cols.p, M.vals.p, rp.p, ci.p, v.p);
+    ILUG_LAUNCH_CHECK();
+    ci.download(A.ci.data());
+    v.download(A.v.data());
+    ILUG_CUDA(cudaDeviceSynchronize());
+    return A;
+}
+
+// -------------------------------------------------------------- launchers
+void spmv(const Sell& M, const double* x, double* y, cudaStream_t st) {
+    launch_rowdot(M, x, EpiStore{y}, st);
+}
+void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st) {
+    launch_rowdot(M, x, EpiAdd{acc}, st);
+}
+void residual(const Sell& M, const double* x, const double* b, double* r, cudaStream_t st) {
+    launch_rowdot(M, x, EpiResidual{b, r}, st);
+}
+void sweep_div(const Sell& M, const double* x, const double* rhs, const double* div, double* out,
+               cudaStream_t st) {
+    launch_rowdot(M, x, EpiDiv{rhs, div, out}, st);
+}
+void sweep_both(const Sell& M, const double* x, const double* rhs, const double* div, double* out,
+                double* out2, cudaStream_t st) {
+    launch_rowdot(M, x, EpiBoth{rhs, div, out, out2}, st);
+}
+void sweep_acc(const Sell& M, const double* x, const double* rhs, const double* div, double* acc,
+               cudaStream_t st) {
+    if (div)
+        launch_rowdot(M, x, EpiAccDiv{rhs, div, acc}, st);
+    else
+        launch_rowdot(M, x, EpiAcc{rhs, acc}, st);
+}
+void residual_scale_step(const Sell& M, const double* x, const double* rhs, const double* scale,
+                         double* out, cudaStream_t st) {
+    launch_rowdot(M, x, EpiScaleAcc{rhs, scale, x, out}, st);
+}
+void residual_scale_init(const Sell& M, const double* x, const double* rhs, const double* scale,
+                         double* term, double* acc, cudaStream_t st) {
+    launch_rowdot(M, x, EpiScaleInit{rhs, scale, term, acc}, st);
+}
+void neg_scale_acc(const Sell& M, const double* x, const double* scale, double* term, double* acc,
+                   cudaStream_t st) {
+    launch_rowdot(M, x, EpiNegScaleAcc{scale, term, acc}, st);
+}
+
+} // namespace ilug
