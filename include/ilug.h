@@ -108,6 +108,17 @@ ILUAMG_API int ilug_smooth(const ilug_smoother* s, const double* b, double* x, d
                            void* stream);
 ILUAMG_API int ilug_ilu_smooth_sweep(const ilug_smoother* s, const double* b, double* x,
                                      void* stream);
+/* Host-buffer smoother application (copy b, x in; smooth; copy x out; synchronous):
+ * the end-to-end form of ilug_smooth used for e2e timing. */
+ILUAMG_API int ilug_smooth_host(const ilug_smoother* s, const double* b_host, double* x_host);
+/* Sizes for byte accounting: n, nnz(A), nnz(strict L), nnz(strict U) (ILU kinds; 0 otherwise),
+ * SELL padded entries of strict U. */
+ILUAMG_API int ilug_smoother_stats(const ilug_smoother* s, long long* n, long long* nnz_A,
+                                   long long* nnz_Ls, long long* nnz_Us, long long* padded_Us);
+/* One bare sweep kernel of an ILU smoother's factor, for per-kernel timing:
+ * out = rhs - T x_in with T = strict L (which = 0) or strict (scaled) U (which = 1). */
+ILUAMG_API int ilug_smoother_sweep_once(const ilug_smoother* s, int which, const double* x_in,
+                                        const double* rhs, double* out, void* stream);
 ILUAMG_API void ilug_smoother_free(ilug_smoother* s);
 
 /* ---- K6/K7: AMG hierarchy and V-cycle ---- */

@@ -84,6 +84,9 @@ class Ref:
             "ref_hash_unit": (_d, [_u64, _u64]),
             "ref_time_richardson_upper": (_i, [_vp, _pd, _ll, _ll, _pd]),
             "ref_time_smooth": (_i, [_vp, _vp, _pd, _ll, _pd]),
+            "ref_run_solve": (_i, [_vp, _vp, _pvp]), "ref_report_get": (C.c_char_p, [_vp, C.c_char_p]),
+            "ref_report_status": (_i, [_vp]), "ref_report_table_csv": (_vp, [_vp, C.c_char_p]),
+            "ref_free_str": (None, [_vp]), "ref_report_free": (None, [_vp]),
             "iluamg_matrix_generate": (_i, [C.c_char_p, _pvp]), "iluamg_config_create": (_i, [_pvp]),
             "iluamg_config_set": (_i, [_vp, C.c_char_p, C.c_char_p]),
             "iluamg_run_solve": (_i, [_vp, _vp, _pvp]), "iluamg_report_get": (C.c_char_p, [_vp, C.c_char_p]),
@@ -267,22 +270,28 @@ class Ref:
         self._ok(self.L.ref_time_richardson_upper(f, _p(b, C.c_double), m, reps, C.byref(s)))
         return s.value
 
-    def run_solve(self, spec, kv):
-        """The reference's own public API path: iluamg_run_solve (src/capi.cpp:166-168)."""
-        A, cfg, rep = C.c_void_p(), C.c_void_p(), C.c_void_p()
-        self._ok(self.L.iluamg_matrix_generate(spec.encode(), C.byref(A)))
-        self._ok(self.L.iluamg_config_create(C.byref(cfg)))
-        for k, v in kv.items():
-            self._ok(self.L.iluamg_config_set(cfg, k.encode(), str(v).encode()))
-        st = self.L.iluamg_run_solve(A, cfg, C.byref(rep))
-        if st not in (0, 1):
-            raise RefError(self.L.iluamg_last_error().decode())
-        keys = ["iterations", "converged", "final_relres", "setup_seconds", "solve_seconds", "levels"]
-        out = {k: self.L.iluamg_report_get(rep, k.encode()).decode() for k in keys}
-        out["history"] = self.L.iluamg_report_table_csv(rep, b"history").decode()
-        self.L.iluamg_report_free(rep)
-        self.L.iluamg_config_free(cfg)
-        self.L.iluamg_matrix_free(A)
+    def run_solve(self, A, kv, keys=("iterations", "converged", "final_relres", "setup_seconds",
+                                      "solve_seconds", "levels", "operator_complexity")):
+        """The reference's own driver, run_solve (src/driver.cpp:239-260) — the body of
+        iluamg_run_solve (src/capi.cpp:166-168) — on a matrix given either as a
+        reference generator spec string or as (row_starts, col_indices, values)."""
+        if isinstance(A, str):
+            Ah = self.generate(A)
+        else:
+            Ah = self.mat(*A)
+        cfg = self.cfg(kv)
+        rep = C.c_void_p()
+        try:
+            self._ok(self.L.ref_run_solve(Ah, cfg, C.byref(rep)))
+        finally:
+            self.free_mat(Ah)
+            self.L.ref_cfg_free(cfg)
+        out = {k: self.L.ref_report_get(rep, k.encode()).decode() for k in keys}
+        out["status"] = self.L.ref_report_status(rep)
+        p = self.L.ref_report_table_csv(rep, b"history")
+        out["history"] = C.cast(p, C.c_char_p).value.decode()
+        self.L.ref_free_str(p)
+        self.L.ref_report_free(rep)
         return out
 
 

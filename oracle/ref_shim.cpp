@@ -370,3 +370,27 @@ API int ref_time_smooth(const void* A, const void* st, const double* b, int64_t 
         *seconds_best = best;
     });
 }
+
+// ---- the reference's own driver on a shim-held matrix (src/driver.cpp:239-260) ----
+#include "iluamg/driver.hpp"
+API int ref_run_solve(const void* A, const void* cfg, void** out) {
+    return wrap([&] {
+        *out = new Report(run_solve(*static_cast<const SparseMatrix*>(A), static_cast<const Cfg*>(cfg)->c,
+                                    "shim"));
+    });
+}
+API const char* ref_report_get(const void* r, const char* key) {
+    const std::string* v = static_cast<const Report*>(r)->find(key);
+    return v ? v->c_str() : nullptr;
+}
+API int ref_report_status(const void* r) { return static_cast<const Report*>(r)->status; }
+API char* ref_report_table_csv(const void* r, const char* name) {
+    const ReportTable* t = static_cast<const Report*>(r)->table(name);
+    if (!t) return nullptr;
+    const std::string s = t->csv();
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return buf;
+}
+API void ref_free_str(char* p) { std::free(p); }
+API void ref_report_free(void* r) { delete static_cast<Report*>(r); }

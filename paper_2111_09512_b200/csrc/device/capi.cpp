@@ -495,6 +495,42 @@ int ilug_ilu_smooth_sweep(const ilug_smoother* s, const double* b, double* x, vo
         return ILUAMG_OK;
     });
 }
+int ilug_smooth_host(const ilug_smoother* s, const double* bh, double* xh) {
+    return guarded([&] {
+        need(s && bh && xh);
+        const ilug::i64 n = s->A.nrows;
+        ilug::DBuf<double> b, x;
+        b.upload(bh, n);
+        x.upload(xh, n);
+        s->s.smooth(b.p, x.p, false, nullptr);
+        x.download(xh);
+        ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        return ILUAMG_OK;
+    });
+}
+int ilug_smoother_stats(const ilug_smoother* s, long long* n, long long* nnz_A, long long* nl,
+                        long long* nu, long long* padded) {
+    return guarded([&] {
+        need(s);
+        const ilug::DeviceIlu* f = s->s.ilu();
+        if (n) *n = s->A.nrows;
+        if (nnz_A) *nnz_A = s->A.nnz();
+        if (nl) *nl = f ? f->Ls().nnz : 0;
+        if (nu) *nu = f ? f->Us().nnz : 0;
+        if (padded) *padded = f ? f->Us().padded : 0;
+        return ILUAMG_OK;
+    });
+}
+int ilug_smoother_sweep_once(const ilug_smoother* s, int which, const double* x_in, const double* rhs,
+                             double* out, void* stream) {
+    return guarded([&] {
+        need(s && x_in && rhs && out);
+        const ilug::DeviceIlu* f = s->s.ilu();
+        if (!f) ilug::fail_invalid("sweep_once: smoother is not an ILU smoother");
+        ilug::residual(which == 0 ? f->Ls() : f->Us(), x_in, rhs, out, S(stream));
+        return ILUAMG_OK;
+    });
+}
 void ilug_smoother_free(ilug_smoother* s) { delete s; }
 
 int ilug_hierarchy_create(const iluamg_matrix* A, const iluamg_config* cfg, ilug_hierarchy** out) {

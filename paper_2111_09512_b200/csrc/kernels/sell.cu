@@ -40,14 +40,14 @@ inline unsigned grid_for(i64 threads, int block = kBlock) {
 }
 
 // ---------------------------------------------------------------- SELL packing
-__global__ void k_sell_fill(i64 nrows_pad, const i32* __restrict__ perm, const i64* __restrict__ rp,
+__global__ void k_sell_fill(i64 nrows_pad, i64 nrows, const i32* __restrict__ perm, const i64* __restrict__ rp,
                             const i32* __restrict__ ci, const double* __restrict__ v, int part,
                             const i64* __restrict__ slice_ptr, i32* __restrict__ cols,
                             double* __restrict__ vals) {
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
     if (p >= nrows_pad) return;
     const i64 row = perm ? perm[p] : p;
-    if (row < 0) return;
+    if (row < 0 || row >= nrows) return;
     i64 dst = slice_ptr[p >> 5] + (p & 31);
     for (i64 k = rp[row]; k < rp[row + 1]; ++k) {
         const i32 j = ci[k];
@@ -59,7 +59,7 @@ __global__ void k_sell_fill(i64 nrows_pad, const i32* __restrict__ perm, const i
     }
 }
 
-__global__ void k_sell_unpack(i64 nrows_pad, const i32* __restrict__ perm,
+__global__ void k_sell_unpack(i64 nrows_pad, i64 nrows, const i32* __restrict__ perm,
                               const i64* __restrict__ slice_ptr,
                               const std::uint16_t* __restrict__ rowlen, const i32* __restrict__ cols,
                               const double* __restrict__ vals, const i64* __restrict__ out_rp,
@@ -67,7 +67,7 @@ __global__ void k_sell_unpack(i64 nrows_pad, const i32* __restrict__ perm,
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
     if (p >= nrows_pad) return;
     const i64 row = perm ? perm[p] : p;
-    if (row < 0) return;
+    if (row < 0 || row >= nrows) return;
     const i64 base = slice_ptr[p >> 5] + (p & 31);
     i64 o = out_rp[row];
     for (int t = 0; t < rowlen[p]; ++t, ++o) {
@@ -259,7 +259,7 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
     layout(out, pad, perm_host, [&](i64 row) { return part_len(pattern, row, pc); });
     if (pad > 0 && pattern.nnz() > 0) {
-        k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.perm.p, rp, ci, v, pc,
+        k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp, ci, v, pc,
                                                      out.slice_ptr.p, out.cols.p, out.vals.p);
         ILUG_LAUNCH_CHECK();
     }
@@ -278,7 +278,7 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     rp.upload(A.rp.data(), A.nrows + 1, s);
     ci.upload(A.ci.data(), A.nnz(), s);
     v.upload(A.v.data(), A.nnz(), s);
-    k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, nullptr, rp.p, ci.p, v.p, pc, out.slice_ptr.p,
+    k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, nullptr, rp.p, ci.p, v.p, pc, out.slice_ptr.p,
                                                  out.cols.p, out.vals.p);
     ILUG_LAUNCH_CHECK();
     ILUG_CUDA(cudaStreamSynchronize(s)); // temporaries die at scope exit
@@ -306,7 +306,7 @@ Csr sell_to_host(const Sell& M) {
     DBuf<i32> ci(A.nnz());
     DBuf<double> v(A.nnz());
     rp.upload(A.rp.data(), M.nrows + 1);
-    k_sell_unpack<<<grid_for(M.nrows_pad), kBlock>>>(M.nrows_pad, M.perm.p, M.slice_ptr.p, M.rowlen.p,
+    k_sell_unpack<<<grid_for(M.nrows_pad), kBlock>>>(M.nrows_pad, M.nrows, M.perm.p, M.slice_ptr.p, M.rowlen.p,
                                                      M.cols.p, M.vals.p, rp.p, ci.p, v.p);
     ILUG_LAUNCH_CHECK();
     ci.download(A.ci.data());
