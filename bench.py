@@ -1,0 +1,326 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: the ILU(T) smoother application inside the AMG
+V-cycle on BASELINE config 2 (27-point variable-coefficient pressure matrix
+256^3, 16.7M rows, ILUT(1e-3, 5) factors, row-scaled U) on one B200.
+
+One "step" = one ilu_smooth_sweep (src/smoother.cpp:143-159) with
+m_L = m_U = 5 Richardson sweeps: residual SpMV + 4 L sweeps + 4 row-scaled U
+sweeps (the first iterate of each is exact, x1 = b), fused epilogues. The
+metric is achieved HBM GB/s with the fixed algorithmic-byte formula of
+SURVEY.md §8(d); the roofline object covers the dominant kernel
+(the scaled-U sweep). `--tts` adds the GMRES+AMG time-to-solution part of the
+metric (host setup + device solve) and the direct-sptrsv comparison.
+
+Multi-GPU (torchrun, N > 1): every rank smooths its own C2-sized row block
+(weak scaling; see DESIGN.md §6 for the halo-exchange plan), time = max over
+ranks. `--impl reference` times the reference's own CPU code on a bounded
+sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ILU sweep GB/s (% HBM peak); GMRES+AMG time-to-solution at 1/2/4/8 B200"
+SPEC = "pressure27(256,256,256)"
+SAMPLE_SPEC = "pressure27(256,256,16)"  # CPU baseline sample: 16 of the 256 z-planes
+ILU_KV = {"smoother.kind": "ilu", "ilu.variant": "ilut", "ilu.droptol": "1e-3", "ilu.lfill": "5",
+          "scaling": "row", "trisolve.mode": "richardson", "trisolve.m_lower": "5",
+          "trisolve.m_upper": "5", "smoother.sweeps": "1"}
+
+
+def sweep_bytes(n, nnz):
+    """One factor sweep / SpMV over a matrix with nnz stored entries (§8d)."""
+    return 12 * nnz + 28 * n + 4
+
+
+def step_bytes(n, nnz_a, nnz_l, nnz_u, m_l=5, m_u=5):
+    """Algorithmic bytes of one ilu_smooth_sweep: residual, (m_L-1) L sweeps
+    (+8n for the fused 1/row_scale of the last), (m_U-1) U sweeps (+8n for the
+    x += z read of the last)."""
+    return (sweep_bytes(n, nnz_a) + (m_l - 1) * sweep_bytes(n, nnz_l) + 8 * n
+            + (m_u - 1) * sweep_bytes(n, nnz_u) + 8 * n)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        time.sleep(0.1)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=5)
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_baseline(steps=2):
+    """The reference's own ilu_smooth_sweep (oracle/_ref, single-threaded, as the
+    reference is) on SAMPLE_SPEC; GB/s by the same formula."""
+    import numpy as np
+    from oracle import oracle
+    import paper_2111_09512_b200 as ilug
+    if not os.path.exists(oracle.REF_SO):
+        return None
+    ref = oracle.Ref()
+    A = ilug.Matrix.generate(SAMPLE_SPEC)  # generator only: the input
+    Acsr = A.csr()
+    Ar = ref.mat(*Acsr)
+    st = ref.smoother(Ar, ref.cfg(ILU_KV))
+    fr = ref.L.ref_smoother_factors(st)
+    L, U, _, _ = ref.factors_arrays(C_void(fr))
+    n = A.rows
+    nnz_l = len(L[1])
+    nnz_u = len(U[1]) - n
+    b = np.random.default_rng(1).uniform(-1, 1, n)
+    best = 1e300
+    for _ in range(steps):
+        x = np.zeros(n)
+        t = time.perf_counter()
+        ref.ilu_smooth_sweep(Ar, st, b, x)
+        best = min(best, time.perf_counter() - t)
+    gbs = step_bytes(n, A.nnz, nnz_l, nnz_u) / best / 1e9
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"{SAMPLE_SPEC} (16 of 256 z-planes, n={n}), ILUT(1e-3,5), one ilu_smooth_sweep "
+                      f"m_L=m_U=5 via the reference library, best of {steps}, {best * 1e3:.1f} ms/step"}
+
+
+def C_void(p):
+    import ctypes
+    return ctypes.c_void_p(p)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    base = cpu_baseline(steps=max(1, args.steps))
+    if base is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    v = base["value"]
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "impl": "reference", "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "ilu_smooth_sweep m5/5 on pressure27 ILUT(1e-3,5)", "sample": SAMPLE_SPEC},
+        "cpu_baseline": base, "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--spec", default=SPEC)
+    ap.add_argument("--tts", action="store_true", help="also run GMRES+AMG time-to-solution")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import paper_2111_09512_b200 as ilug
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ilug.lib.ilug_set_device(local)
+
+    t0 = time.perf_counter()
+    A = ilug.Matrix.generate(args.spec)
+    cfg = ilug.Config().update(ILU_KV)
+    S = ilug.Smoother(A, cfg)  # host ILUT + upload + K1 row scaling on the device
+    setup_s = time.perf_counter() - t0
+    import ctypes as C
+    n_, na, nl, nu, pad = (C.c_longlong() for _ in range(5))
+    ilug._check(ilug.lib.ilug_smoother_stats(S.h, C.byref(n_), C.byref(na), C.byref(nl), C.byref(nu), C.byref(pad)))
+    n, nnz_a, nnz_l, nnz_u, pad_u = n_.value, na.value, nl.value, nu.value, pad.value
+    B = step_bytes(n, nnz_a, nnz_l, nnz_u)
+
+    stream = torch.cuda.current_stream()
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    b = torch.rand(n, dtype=torch.float64, generator=g).cuda() * 2 - 1
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        S.smooth(b, x, stream=stream)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            S.smooth(b, x, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = B * world / (ms * 1e-3) / 1e9
+
+    # ---- roofline: the dominant kernel (scaled-U sweep), timed alone on the same stream
+    peak, peak_kind = peaks()
+    xin = torch.rand(n, dtype=torch.float64, generator=g).cuda()
+    out = torch.empty_like(xin)
+    reps = 50
+    kern = {}
+    for which, name, nnz in ((1, "u_sweep", nnz_u), (0, "l_sweep", nnz_l)):
+        for _ in range(3):
+            ilug._check(ilug.lib.ilug_smoother_sweep_once(S.h, which, xin.data_ptr(), b.data_ptr(),
+                                                          out.data_ptr(), stream.cuda_stream))
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            ilug._check(ilug.lib.ilug_smoother_sweep_once(S.h, which, xin.data_ptr(), b.data_ptr(),
+                                                          out.data_ptr(), stream.cuda_stream))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kms = e0.elapsed_time(e1) / reps
+        kern[name] = {"ms": kms, "gbs": sweep_bytes(n, nnz) / (kms * 1e-3) / 1e9, "bytes": sweep_bytes(n, nnz)}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "u_sweep_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    ach = kern["u_sweep"]["gbs"]
+    roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                "kernel": "k_rowdot<EpiResidual> on strict row-scaled U (SELL-32)",
+                "bytes_per_launch": kern["u_sweep"]["bytes"], "ms_per_launch": round(kern["u_sweep"]["ms"], 5),
+                "frac_of_8TBs_nominal": round(ach / 8000.0, 4),
+                "l_sweep_gbs": round(kern["l_sweep"]["gbs"], 1)}
+
+    # ---- e2e through the public host-buffer API (H2D of b, x and D2H of x every step)
+    bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh = torch.zeros(n, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b.cpu())
+    bp = bh.numpy().ctypes.data_as(C.POINTER(C.c_double))
+    xp = xh.numpy().ctypes.data_as(C.POINTER(C.c_double))
+    e2e_steps = max(3, min(args.steps, 20))
+    ilug._check(ilug.lib.ilug_smooth_host(S.h, bp, xp))
+    barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        ilug._check(ilug.lib.ilug_smooth_host(S.h, bp, xp))
+    e2e_s = (time.perf_counter() - t) / e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = {"value": round(B * world / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 16 * n,
+           "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_s * 1e3, 3),
+           "api": "ilug_smooth_host (pinned host b, x)"}
+
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"ilu_smooth_sweep (m_L=m_U=5, row-scaled ILUT(1e-3,5)) on {args.spec}",
+                   "n": n, "nnz_A": nnz_a, "nnz_L_strict": nnz_l, "nnz_U_strict": nnz_u,
+                   "sell_padding_U": round(pad_u / max(nnz_u, 1) - 1, 4), "bytes_per_step": B,
+                   "l2": "inputs (>= 5 GB per step) exceed the 126 MB L2; no flush needed",
+                   "parallelism": f"row-block x{world} (weak)", "host_setup_s": round(setup_s, 2)},
+        "frac_of_peak": round(value / world / peak, 4),
+        "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
+        "gpu_launches": 9 * args.steps,
+    }
+    if args.tts and rank == 0:
+        res["tts"] = time_to_solution(ilug, A)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def time_to_solution(ilug, A):
+    """GMRES+AMG (tol 1e-8 relres, PMIS, ILUT smoother on the finest level, GS
+    below) through iluamg_run_solve, iterative vs direct (level-scheduled) triangular solves."""
+    out = {}
+    base = dict(ILU_KV, **{"smoother.sweeps": "2", "krylov.tol": "1e-8", "amg.coarsening": "pmis",
+                           "krylov.form_iterates": "false"})
+    for mode in ("richardson", "direct"):
+        kv = dict(base, **{"trisolve.mode": mode})
+        rep = ilug.run_solve(A, ilug.Config().update(kv))
+        out[mode] = {"iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
+                     "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
+                     "final_relres": float(rep["final_relres"]), "levels": int(rep["levels"])}
+    out["speedup_iterative_vs_direct"] = round(out["direct"]["solve_s"] / out["richardson"]["solve_s"], 3)
+    return out
+
+
+if __name__ == "__main__":
+    main()

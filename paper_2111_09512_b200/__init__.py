@@ -74,6 +74,9 @@ _SIGS = {
     "ilug_residual": (_i, [_vp, _vp, _vp, _vp, _vp]), "ilug_dmatrix_free": (None, [_vp]),
     "ilug_smoother_create": (_i, [_vp, _vp, _i, _pvp]), "ilug_smooth": (_i, [_vp, _vp, _vp, _pd, _vp]),
     "ilug_ilu_smooth_sweep": (_i, [_vp, _vp, _vp, _vp]), "ilug_smoother_free": (None, [_vp]),
+    "ilug_smooth_host": (_i, [_vp, _pd, _pd]),
+    "ilug_smoother_stats": (_i, [_vp, _pll, _pll, _pll, _pll, _pll]),
+    "ilug_smoother_sweep_once": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ilug_hierarchy_create": (_i, [_vp, _vp, _pvp]), "ilug_hierarchy_create_host": (_i, [_vp, _vp, _pvp]),
     "ilug_hierarchy_levels": (_i, [_vp]), "ilug_hierarchy_level_matrix": (_i, [_vp, _i, _i, _pvp]),
     "ilug_hierarchy_operator_complexity": (_d, [_vp]), "ilug_vcycle": (_i, [_vp, _vp, _vp, _vp]),

@@ -2,6 +2,8 @@
 #include "solver.hpp"
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace ilug {
 
@@ -358,13 +360,37 @@ void DeviceHierarchy::cycle(int k, bool x_zero, cudaStream_t st) {
         return;
     }
     Lev& nx = levels_[k + 1];
+    // ILUG_TRACE=1 (eager mode only): per-level phase times on stderr.
+    static const bool trace = std::getenv("ILUG_TRACE") != nullptr;
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        static cudaEvent_t last = nullptr;
+        cudaEvent_t e;
+        ILUG_CUDA(cudaEventCreate(&e));
+        ILUG_CUDA(cudaEventRecord(e, st));
+        ILUG_CUDA(cudaEventSynchronize(e));
+        if (last) {
+            float ms = 0.f;
+            ILUG_CUDA(cudaEventElapsedTime(&ms, last, e));
+            std::fprintf(stderr, "[trace] level %d n=%lld %-10s %.3f ms\n", k, static_cast<long long>(lv.n),
+                         what, ms);
+            cudaEventDestroy(last);
+        }
+        last = e;
+    };
+    mark("enter");
     lv.smoother.smooth(lv.b.p, lv.x.p, x_zero, st);
+    mark("presmooth");
     residual(lv.A.A, lv.x.p, lv.b.p, lv.r.p, st);
     spmv(lv.R, lv.r.p, nx.b.p, st);
     vec_zero(nx.x.p, nx.n, st);
+    mark("restrict");
     for (i64 i = 0; i < nu_; ++i) cycle(k + 1, i == 0, st);
+    mark("coarse");
     spmv_add(lv.P, nx.x.p, lv.x.p, st);
+    mark("prolong");
     lv.smoother.smooth(lv.b.p, lv.x.p, false, st);
+    mark("postsmooth");
 }
 
 void DeviceHierarchy::vcycle_eager(const double* r, double* z, cudaStream_t st) {

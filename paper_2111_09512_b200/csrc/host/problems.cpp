@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <fstream>
+#include <memory>
 #include <random>
 #include <sstream>
 
@@ -150,14 +151,18 @@ Csr stencil27(i64 nx, i64 ny, i64 nz) {
 
 Csr pressure27(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
     check_grid(nx, ny, nz, "pressure27");
-    auto kappa = [seed](i64 i) {
-        return std::pow(10.0, 4.0 * hash_unit(seed, static_cast<std::uint64_t>(i)) - 2.0);
-    };
+    const i64 n = nx * ny * nz;
+    auto kap = std::make_shared<std::vector<double>>(static_cast<size_t>(n));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i)
+            (*kap)[i] = std::pow(10.0, 4.0 * hash_unit(seed, static_cast<std::uint64_t>(i)) - 2.0);
+    });
+    const double* kappa = kap->data();
     return box27(nx, ny, nz, [=](i64 i, i64 j, int dist) {
         const double w = dist == 1 ? 1.0 : (dist == 2 ? 0.5 : 0.25);
-        const double ki = kappa(i);
+        const double ki = kappa[i];
         if (j < 0) return w * ki; // out-of-grid slot: hm(ki, ki) = ki
-        const double kj = kappa(j);
+        const double kj = kappa[j];
         return w * (2.0 * ki * kj / (ki + kj));
     });
 }
