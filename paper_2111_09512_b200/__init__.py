@@ -191,7 +191,7 @@ class Matrix:
         return rp, ci, v
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
             lib.iluamg_matrix_free(self.h)
             self.h = C.c_void_p()
 
@@ -226,7 +226,7 @@ class Config:
         return self
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
             lib.iluamg_config_free(self.h)
             self.h = C.c_void_p()
 
@@ -367,7 +367,7 @@ class Factors:
         _check(lib.ilug_solve_upper(self.h, _ptr(b), _ptr(x), _stream(stream)))
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
             lib.ilug_factors_free(self.h)
             self.h = C.c_void_p()
 
@@ -385,7 +385,7 @@ class DeviceMatrix:
         _check(lib.ilug_residual(self.h, _ptr(x), _ptr(b), _ptr(r), _stream(stream)))
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
             lib.ilug_dmatrix_free(self.h)
             self.h = C.c_void_p()
 
@@ -405,7 +405,7 @@ class Smoother:
         _check(lib.ilug_ilu_smooth_sweep(self.h, _ptr(b), _ptr(x), _stream(stream)))
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
             lib.ilug_smoother_free(self.h)
             self.h = C.c_void_p()
 
@@ -444,6 +444,6 @@ class Hierarchy:
         return dict(status=st, iterations=it.value, final_relres=rr.value)
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
             lib.ilug_hierarchy_free(self.h)
             self.h = C.c_void_p()

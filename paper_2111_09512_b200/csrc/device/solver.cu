@@ -348,6 +348,7 @@ void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st) {
     lu_.upload(h.coarse.lu.data(), static_cast<i64>(h.coarse.lu.size()), st);
     piv_.upload(h.coarse.piv.data(), static_cast<i64>(h.coarse.piv.size()), st);
     nu_ = h.params.cycles_nu;
+    trace_ = std::getenv("ILUG_TRACE") != nullptr && !use_graph_;
     if (exec_) cudaGraphExecDestroy(exec_);
     exec_ = nullptr;
     ILUG_CUDA(cudaStreamSynchronize(st));
@@ -361,9 +362,8 @@ void DeviceHierarchy::cycle(int k, bool x_zero, cudaStream_t st) {
     }
     Lev& nx = levels_[k + 1];
     // ILUG_TRACE=1 (eager mode only): per-level phase times on stderr.
-    static const bool trace = std::getenv("ILUG_TRACE") != nullptr;
     auto mark = [&](const char* what) {
-        if (!trace) return;
+        if (!trace_) return;
         static cudaEvent_t last = nullptr;
         cudaEvent_t e;
         ILUG_CUDA(cudaEventCreate(&e));

@@ -125,6 +125,7 @@ private:
     DBuf<i64> piv_;
     i64 nu_ = 1;
     bool use_graph_ = true;
+    bool trace_ = false; // ILUG_TRACE (eager only): per-level phase times on stderr
     cudaGraphExec_t exec_ = nullptr;
     cudaStream_t graph_stream_ = nullptr;
     i64 kernels_per_cycle_ = 0;

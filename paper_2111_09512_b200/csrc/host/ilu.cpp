@@ -2,6 +2,8 @@
 
 #include <atomic>
 #include <cmath>
+#include <memory>
+#include <thread>
 #include <limits>
 #include <queue>
 
@@ -128,106 +130,162 @@ HostFactors ilut(const Csr& A, const IluParams& p) {
     const i64 n = A.nrows;
     const double anorm_f = frobenius_norm(A);
 
-    HostFactors f;
-    f.L.nrows = f.L.ncols = f.U.nrows = f.U.ncols = n;
-    f.L.rp.assign(1, 0);
-    f.U.rp.assign(1, 0);
-    f.L.rp.reserve(static_cast<size_t>(n) + 1);
-    f.U.rp.reserve(static_cast<size_t>(n) + 1);
-    std::vector<i64> udiag_pos(static_cast<size_t>(n), -1);
-
-    std::vector<double> w(static_cast<size_t>(n), 0.0);
-    std::vector<char> live(static_cast<size_t>(n), 0), orig(static_cast<size_t>(n), 0);
-    std::vector<i64> upper, kept, pat_part, fill_part;
-    std::priority_queue<i64, std::vector<i64>, std::greater<i64>> pending;
-
-    // Survivor selection (src/ilu.cpp:204-232): pattern entries pass on the
-    // threshold (applied to the U part only), fill competes for lfill slots.
-    auto select = [&](const std::vector<i64>& cols, bool lower, double tau) {
-        pat_part.clear();
-        fill_part.clear();
-        for (i64 j : cols) {
-            if (!live[j]) continue;
-            if (!lower && std::abs(w[j]) < tau) continue;
-            (orig[j] ? pat_part : fill_part).push_back(j);
-        }
-        const auto cap = static_cast<size_t>(p.lfill);
-        if (fill_part.size() > cap) {
-            std::nth_element(fill_part.begin(), fill_part.begin() + static_cast<std::ptrdiff_t>(cap),
-                             fill_part.end(), [&](i64 a, i64 b) {
-                                 const double va = std::abs(w[a]), vb = std::abs(w[b]);
-                                 return va != vb ? va > vb : a < b;
-                             });
-            fill_part.resize(cap);
-        }
-        pat_part.insert(pat_part.end(), fill_part.begin(), fill_part.end());
-        std::sort(pat_part.begin(), pat_part.end());
-    };
-
+    // Pipelined row-parallel ILUT. Row i's factor size is bounded a priori
+    // (pattern part of A's row + lfill per triangle), so every row owns a fixed
+    // slot and rows can be produced out of order by a pool of workers taking row
+    // indices in ascending order. Row i reads U rows k only after they are
+    // published (done[k], release/acquire) and eliminates in the serial heap
+    // order, so each row's arithmetic is exactly the serial algorithm's: the
+    // factors are bitwise independent of the worker count. The chain row i-1 ->
+    // row i (last multiplier popped) bounds the speed-up, not correctness.
+    std::vector<i64> loff(static_cast<size_t>(n) + 1, 0), uoff(static_cast<size_t>(n) + 1, 0);
     for (i64 i = 0; i < n; ++i) {
-        const double tau = p.droptol * row_norm2(A, i);
-        upper.clear();
-        kept.clear();
-        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
-            const i64 j = A.ci[k];
-            w[j] = A.v[k];
-            live[j] = 1;
-            orig[j] = 1;
-            if (j < i)
-                pending.push(j);
-            else if (j > i)
-                upper.push_back(j);
-        }
-        while (!pending.empty()) {
-            const i64 k = pending.top();
-            pending.pop();
-            if (!live[k]) continue;
-            const double m = w[k] / f.U.v[udiag_pos[k]];
-            if (std::abs(m) < tau) {
-                w[k] = 0.0;
-                live[k] = 0;
-                continue;
+        i64 lo = 0, up = 0;
+        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) lo += A.ci[k] < i, up += A.ci[k] > i;
+        loff[i + 1] = loff[i] + lo + p.lfill;
+        uoff[i + 1] = uoff[i] + 1 + up + p.lfill;
+    }
+    std::vector<i32> lci(static_cast<size_t>(loff[n])), uci(static_cast<size_t>(uoff[n]));
+    std::vector<double> lv(static_cast<size_t>(loff[n])), uv(static_cast<size_t>(uoff[n]));
+    std::vector<i64> llen(static_cast<size_t>(n), 0), ulen(static_cast<size_t>(n), 0);
+    std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(n)]);
+    for (i64 i = 0; i < n; ++i) done[i].store(0, std::memory_order_relaxed);
+    std::atomic<i64> next{0}, first_zero{n};
+
+    auto worker = [&]() {
+        std::vector<double> w(static_cast<size_t>(n), 0.0);
+        std::vector<char> live(static_cast<size_t>(n), 0), orig(static_cast<size_t>(n), 0);
+        std::vector<i64> upper, kept, pat_part, fill_part;
+        std::priority_queue<i64, std::vector<i64>, std::greater<i64>> pending;
+        // Survivor selection (src/ilu.cpp:204-232): pattern entries pass on the
+        // threshold (applied to the U part only), fill competes for lfill slots.
+        auto select = [&](const std::vector<i64>& cols, bool lower, double tau) {
+            pat_part.clear();
+            fill_part.clear();
+            for (i64 j : cols) {
+                if (!live[j]) continue;
+                if (!lower && std::abs(w[j]) < tau) continue;
+                (orig[j] ? pat_part : fill_part).push_back(j);
             }
-            w[k] = m;
-            kept.push_back(k);
-            for (i64 kk = udiag_pos[k] + 1; kk < f.U.rp[k + 1]; ++kk) {
-                const i64 j = f.U.ci[kk];
-                w[j] -= m * f.U.v[kk];
-                if (!live[j]) {
-                    live[j] = 1;
-                    if (j < i)
-                        pending.push(j);
-                    else if (j > i)
-                        upper.push_back(j);
+            const auto cap = static_cast<size_t>(p.lfill);
+            if (fill_part.size() > cap) {
+                std::nth_element(fill_part.begin(), fill_part.begin() + static_cast<std::ptrdiff_t>(cap),
+                                 fill_part.end(), [&](i64 a, i64 b) {
+                                     const double va = std::abs(w[a]), vb = std::abs(w[b]);
+                                     return va != vb ? va > vb : a < b;
+                                 });
+                fill_part.resize(cap);
+            }
+            pat_part.insert(pat_part.end(), fill_part.begin(), fill_part.end());
+            std::sort(pat_part.begin(), pat_part.end());
+        };
+        for (;;) {
+            const i64 i = next.fetch_add(1, std::memory_order_relaxed);
+            if (i >= n) return;
+            const double tau = p.droptol * row_norm2(A, i);
+            upper.clear();
+            kept.clear();
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                const i64 j = A.ci[k];
+                w[j] = A.v[k];
+                live[j] = 1;
+                orig[j] = 1;
+                if (j < i)
+                    pending.push(j);
+                else if (j > i)
+                    upper.push_back(j);
+            }
+            while (!pending.empty()) {
+                const i64 k = pending.top();
+                pending.pop();
+                if (!live[k]) continue;
+                for (int spin = 0; !done[k].load(std::memory_order_acquire); ++spin) {
+                    if (spin < 20000)
+                        __builtin_ia32_pause();
+                    else
+                        std::this_thread::yield();
+                }
+                const double m = w[k] / uv[uoff[k]];
+                if (std::abs(m) < tau) {
+                    w[k] = 0.0;
+                    live[k] = 0;
+                    continue;
+                }
+                w[k] = m;
+                kept.push_back(k);
+                for (i64 kk = uoff[k] + 1; kk < uoff[k] + ulen[k]; ++kk) {
+                    const i64 j = uci[kk];
+                    w[j] -= m * uv[kk];
+                    if (!live[j]) {
+                        live[j] = 1;
+                        if (j < i)
+                            pending.push(j);
+                        else if (j > i)
+                            upper.push_back(j);
+                    }
                 }
             }
-        }
+            select(kept, true, tau);
+            i64 o = loff[i];
+            for (i64 j : pat_part) lci[o] = static_cast<i32>(j), lv[o++] = w[j];
+            llen[i] = o - loff[i];
 
-        select(kept, true, tau);
-        for (i64 j : pat_part) {
-            f.L.ci.push_back(static_cast<i32>(j));
-            f.L.v.push_back(w[j]);
-        }
-        f.L.rp.push_back(static_cast<i64>(f.L.ci.size()));
+            double d = w[i];
+            if (d == 0.0) {
+                if (p.pivot_patch == PivotPatch::error) {
+                    i64 cur = first_zero.load();
+                    while (i < cur && !first_zero.compare_exchange_weak(cur, i)) {
+                    }
+                    d = 1.0; // placeholder: the factorisation is abandoned below
+                } else {
+                    d = patch_pivot(p.droptol, row_norm2(A, i), anorm_f, p.pivot_patch, i);
+                }
+            }
+            o = uoff[i];
+            uci[o] = static_cast<i32>(i), uv[o++] = d;
+            select(upper, false, tau);
+            for (i64 j : pat_part) uci[o] = static_cast<i32>(j), uv[o++] = w[j];
+            ulen[i] = o - uoff[i];
+            done[i].store(1, std::memory_order_release);
 
-        double d = w[i];
-        if (d == 0.0) d = patch_pivot(p.droptol, row_norm2(A, i), anorm_f, p.pivot_patch, i);
-        udiag_pos[i] = static_cast<i64>(f.U.ci.size());
-        f.U.ci.push_back(static_cast<i32>(i));
-        f.U.v.push_back(d);
-        select(upper, false, tau);
-        for (i64 j : pat_part) {
-            f.U.ci.push_back(static_cast<i32>(j));
-            f.U.v.push_back(w[j]);
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) orig[A.ci[k]] = 0;
+            for (i64 j : kept) w[j] = 0.0, live[j] = 0;
+            w[i] = 0.0;
+            live[i] = 0;
+            for (i64 j : upper) w[j] = 0.0, live[j] = 0;
         }
-        f.U.rp.push_back(static_cast<i64>(f.U.ci.size()));
-
-        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) orig[A.ci[k]] = 0;
-        for (i64 j : kept) w[j] = 0.0, live[j] = 0;
-        w[i] = 0.0;
-        live[i] = 0;
-        for (i64 j : upper) w[j] = 0.0, live[j] = 0;
+    };
+    const int T = static_cast<int>(std::max<i64>(1, std::min<i64>(std::min(host_threads(), 16), n / 2000)));
+    if (T == 1) {
+        worker();
+    } else {
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(worker);
+        for (auto& th : pool) th.join();
     }
+    if (first_zero.load() < n) patch_pivot(0.0, 0.0, 0.0, PivotPatch::error, first_zero.load());
+
+    HostFactors f;
+    for (Csr* M : {&f.L, &f.U}) {
+        M->nrows = M->ncols = n;
+        M->rp.assign(static_cast<size_t>(n) + 1, 0);
+    }
+    for (i64 i = 0; i < n; ++i) {
+        f.L.rp[i + 1] = f.L.rp[i] + llen[i];
+        f.U.rp[i + 1] = f.U.rp[i] + ulen[i];
+    }
+    f.L.ci.resize(static_cast<size_t>(f.L.rp[n]));
+    f.L.v.resize(static_cast<size_t>(f.L.rp[n]));
+    f.U.ci.resize(static_cast<size_t>(f.U.rp[n]));
+    f.U.v.resize(static_cast<size_t>(f.U.rp[n]));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            std::copy(lci.begin() + loff[i], lci.begin() + loff[i] + llen[i], f.L.ci.begin() + f.L.rp[i]);
+            std::copy(lv.begin() + loff[i], lv.begin() + loff[i] + llen[i], f.L.v.begin() + f.L.rp[i]);
+            std::copy(uci.begin() + uoff[i], uci.begin() + uoff[i] + ulen[i], f.U.ci.begin() + f.U.rp[i]);
+            std::copy(uv.begin() + uoff[i], uv.begin() + uoff[i] + ulen[i], f.U.v.begin() + f.U.rp[i]);
+        }
+    });
     return f;
 }
 

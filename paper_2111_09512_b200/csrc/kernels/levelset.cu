@@ -4,80 +4,145 @@
 //
 // Host analysis buckets rows into wavefront levels of the dependency DAG and
 // stores a level-ordered SELL-32 copy of the operator (each level padded to a
-// whole number of slices, so a warp never straddles two levels). One persistent
-// kernel walks the levels with a grid-wide barrier between them (cooperative
-// launch guarantees co-residency; tiny systems use one CTA and __syncthreads).
-// Each row is computed by one thread in the serial code's exact operation order
+// whole number of slices, so a warp never straddles two levels). Each row is
+// computed by one thread in the serial code's exact operation order
 // (s = b; s -= a_ij x_j ascending; x_i = s / d), so the result is bitwise the
 // sequential solve of src/trisolve.cpp:20-55 / src/smoother.cpp:113-132.
+//
+// Two schedules:
+//  * narrow DAGs (coarse AMG levels): one 1024-thread CTA walks the levels
+//    with __syncthreads between them (no grid-wide synchronisation at all);
+//  * wide DAGs (finest-level factors): sync-free wavefront — warps take
+//    32-row slices in level order from an atomic ticket and each row waits
+//    only on its own dependencies' completion flags (acquire/release through
+//    L2, epoch-stamped so nothing is reset between solves). A slice only
+//    depends on slices handed out before it, so progress never depends on CTA
+//    residency and no cooperative launch or global barrier is needed.
 #include "levelset.hpp"
 
+#include <cuda/atomic>
+
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 namespace ilug {
 
 namespace {
 
-constexpr int kBlock = 256;
-
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned g = *reinterpret_cast<volatile unsigned*>(gen);
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (*reinterpret_cast<volatile unsigned*>(gen) == g) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
+constexpr int kSmallBlock = 1024;
+constexpr int kFlagBlock = 256;
 
 // MODE 0: unit lower, strict storage: x_i = b_i - sum L_ij x_j
 // MODE 1: upper with stored diagonal: x_i = (b_i - sum_{j != i} U_ij x_j) / U_ii
 // MODE 2: Gauss-Seidel on A: x'_i = (b_i - sum_{j<i} a_ij x'_j - sum_{j>i} a_ij x_j) / a_ii
 template <int MODE>
-__global__ void __launch_bounds__(kBlock)
-k_levels(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b,
-         double* x, const double* __restrict__ xold, unsigned* bar) {
-    const i64 nth = static_cast<i64>(gridDim.x) * blockDim.x;
-    const i64 gt = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-    for (int L = 0; L < nlev; ++L) {
-        const i64 end = level_ptr[L + 1];
-        for (i64 p = level_ptr[L] + gt; p < end; p += nth) {
-            const i64 row = M.perm[p];
-            if (row < 0) continue;
-            const int len = M.rowlen[p];
-            const i64 base = M.slice_ptr[p >> 5] + (p & 31);
-            double s = b[row], d = 1.0;
-            for (int t = 0; t < len; ++t) {
-                const i64 q = base + static_cast<i64>(t) * kSlice;
-                const i32 j = M.cols[q];
-                const double a = M.vals[q];
-                if (MODE == 0) {
-                    s = s - a * __ldcg(x + j);
-                } else if (j == row) {
-                    d = a;
-                } else if (MODE == 1 || j < row) {
-                    s = s - a * __ldcg(x + j);
+__device__ __forceinline__ bool is_dep(i32 j, i64 row) {
+    return MODE == 1 ? j > row : j < row;
+}
+
+// One row in the serial operation order. Entries are processed in chunks of
+// kChunk: all column/value loads of a chunk are issued first, then the x
+// gathers (waiting on the producers' flags in the sync-free schedule), then
+// the ordered accumulation — a row costs ~2 memory latencies per chunk instead
+// of 2 per entry.
+constexpr int kChunk = 8;
+
+template <int MODE, bool FLAGS>
+__device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, const double* __restrict__ b,
+                                          double* x, const double* __restrict__ xold, unsigned* flags,
+                                          unsigned E) {
+    const int len = M.rowlen[p];
+    const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+    double s = b[row], d = 1.0;
+    for (int t0 = 0; t0 < len; t0 += kChunk) {
+        i32 c[kChunk];
+        double a[kChunk], xv[kChunk];
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            if (t0 + u < len) {
+                const i64 q = base + static_cast<i64>(t0 + u) * kSlice;
+                c[u] = __ldg(M.cols + q);
+                a[u] = __ldg(M.vals + q);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            xv[u] = 0.0;
+            if (t0 + u < len && !(MODE != 0 && c[u] == row)) {
+                const i32 j = c[u];
+                if (is_dep<MODE>(j, row)) {
+                    if (FLAGS) {
+                        cuda::atomic_ref<unsigned, cuda::thread_scope_device> f(flags[j]);
+                        while (f.load(cuda::memory_order_acquire) != E) {
+                        }
+                    }
+                    xv[u] = __ldcg(x + j);
                 } else {
-                    s = s - a * xold[j];
+                    xv[u] = xold[j]; // GS: not-yet-updated neighbour (MODE 2 only)
                 }
             }
-            x[row] = MODE == 0 ? s : s / d;
         }
-        if (L + 1 < nlev) {
-            if (gridDim.x == 1)
-                __syncthreads();
-            else
-                grid_barrier(bar, bar + 1);
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u) {
+            if (t0 + u < len) {
+                if (MODE != 0 && c[u] == row)
+                    d = a[u];
+                else
+                    s = s - a[u] * xv[u];
+            }
         }
     }
+    x[row] = MODE == 0 ? s : s / d;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kSmallBlock)
+k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b,
+             double* x, const double* __restrict__ xold) {
+    for (int L = 0; L < nlev; ++L) {
+        const i64 end = level_ptr[L + 1];
+        for (i64 p = level_ptr[L] + threadIdx.x; p < end; p += blockDim.x) {
+            const i64 row = M.perm[p];
+            if (row >= 0) level_row<MODE, false>(M, p, row, b, x, xold, nullptr, 0u);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_epoch_bump(unsigned* epoch, unsigned* ticket) {
+    *epoch = *epoch + 1u;
+    *ticket = 0u;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFlagBlock)
+k_levels_flags(SellView M, i64 nslices, const double* __restrict__ b, double* x,
+               const double* __restrict__ xold, unsigned* flags, const unsigned* __restrict__ epoch_p,
+               unsigned* ticket) {
+    const unsigned E = *epoch_p;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned s = 0;
+        if (lane == 0) s = atomicAdd(ticket, 1u);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= nslices) return;
+        const i64 p = static_cast<i64>(s) * kSlice + lane;
+        const i64 row = M.perm[p];
+        if (row < 0) continue;
+        level_row<MODE, true>(M, p, row, b, x, xold, flags, E);
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> f(flags[row]);
+        f.store(E, cuda::memory_order_release);
+    }
+}
+
+template <int MODE>
+const void* cta_kernel() {
+    return reinterpret_cast<const void*>(k_levels_cta<MODE>);
+}
+template <int MODE>
+const void* flag_kernel() {
+    return reinterpret_cast<const void*>(k_levels_flags<MODE>);
 }
 
 } // namespace
@@ -125,45 +190,48 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     ci.upload(T.ci.data(), T.nnz(), st);
     if (!dev_vals) v.upload(T.v.data(), T.nnz(), st);
     sell_from_device_csr(M_, T, rp.p, ci.p, dev_vals ? dev_vals : v.p, Part::all, perm, st);
-    bar_.alloc(2);
-    ILUG_CUDA(cudaMemsetAsync(bar_.p, 0, 2 * sizeof(unsigned), st));
-    ILUG_CUDA(cudaStreamSynchronize(st));
 
-    // Persistent grid: co-resident CTAs only (cooperative launch checks it).
-    int per_sm = 0;
-    switch (kind) {
-    case Kind::lower_unit:
-        ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels<0>, kBlock, 0));
-        break;
-    case Kind::upper:
-        ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels<1>, kBlock, 0));
-        break;
-    case Kind::gauss_seidel:
-        ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels<2>, kBlock, 0));
-        break;
+    // Narrow DAG (average level width below two CTAs' worth): one CTA.
+    single_cta_ = n == 0 || n / std::max(nl, 1) <= 2 * kSmallBlock;
+    if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | flags
+        if (std::string(force) == "cta") single_cta_ = true;
+        if (std::string(force) == "flags" && n > 0) single_cta_ = false;
     }
-    const i64 want = (max_level_rows_ + kBlock - 1) / kBlock;
-    const i64 cap = static_cast<i64>(std::max(1, per_sm)) * device_sm_count();
-    grid_ = static_cast<int>(std::max<i64>(1, std::min(want, cap)));
-    if (n <= 4 * kBlock * 8) grid_ = 1; // small systems: one CTA, block barriers only
+    if (!single_cta_) {
+        flags_.alloc(n + 2); // [0, n) row flags, n epoch, n+1 ticket
+        ILUG_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(n + 2) * sizeof(unsigned), st));
+        const i64 slices = M_.nrows_pad / kSlice;
+        grid_ = static_cast<int>(std::min<i64>((slices + kFlagBlock / 32 - 1) / (kFlagBlock / 32),
+                                               static_cast<i64>(device_sm_count()) * 8));
+    } else {
+        grid_ = 1;
+    }
+    ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
 void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream_t st) const {
     if (M_.nrows == 0) return;
     SellView mv = view(M_);
-    const i64* lp = level_ptr_.p;
-    int nl = nlev_;
-    unsigned* bar = bar_.p;
-    void* args[] = {&mv, &lp, &nl, &b, &x, &xold, &bar};
-    const void* fn = kind_ == Kind::lower_unit ? reinterpret_cast<const void*>(k_levels<0>)
-                     : kind_ == Kind::upper    ? reinterpret_cast<const void*>(k_levels<1>)
-                                               : reinterpret_cast<const void*>(k_levels<2>);
-    if (grid_ == 1) {
-        ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kBlock), args, 0, st));
-    } else {
-        ILUG_CUDA(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid_)), dim3(kBlock), args,
-                                              0, st));
+    const int mode = kind_ == Kind::lower_unit ? 0 : (kind_ == Kind::upper ? 1 : 2);
+    if (single_cta_) {
+        const i64* lp = level_ptr_.p;
+        int nl = nlev_;
+        void* args[] = {&mv, &lp, &nl, &b, &x, &xold};
+        const void* fn = mode == 0 ? cta_kernel<0>() : mode == 1 ? cta_kernel<1>() : cta_kernel<2>();
+        ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kSmallBlock), args, 0, st));
+        return;
     }
+    const i64 n = M_.nrows;
+    unsigned* flags = flags_.p;
+    unsigned* epoch = flags_.p + n;
+    unsigned* ticket = flags_.p + n + 1;
+    k_epoch_bump<<<1, 1, 0, st>>>(epoch, ticket);
+    ILUG_LAUNCH_CHECK();
+    i64 ns = M_.nrows_pad / kSlice;
+    const unsigned* ep = epoch;
+    void* args[] = {&mv, &ns, &b, &x, &xold, &flags, &ep, &ticket};
+    const void* fn = mode == 0 ? flag_kernel<0>() : mode == 1 ? flag_kernel<1>() : flag_kernel<2>();
+    ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid_)), dim3(kFlagBlock), args, 0, st));
 }
 
 } // namespace ilug

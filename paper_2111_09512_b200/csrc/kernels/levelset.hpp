@@ -28,7 +28,8 @@ private:
     Kind kind_ = Kind::lower_unit;
     Sell M_;
     DBuf<i64> level_ptr_;
-    DBuf<unsigned> bar_;
+    DBuf<unsigned> flags_; // sync-free schedule: row flags + epoch + ticket
+    bool single_cta_ = true;
     int nlev_ = 0;
     int grid_ = 1;
     i64 max_level_rows_ = 0;

@@ -212,3 +212,59 @@ def test_c3_cutcell_scaled_vs_unscaled(ilug, ref, port, torch_cuda):
         assert rel_err(_host(x), xs) < 1e-12
         errs.append(rel_err(xs, direct))
     assert errs[0] > errs[1] > errs[2]
+
+
+@pytest.mark.parametrize("schedule", ["cta", "flags"])
+@pytest.mark.parametrize("spec,kv", [("poisson3d(24,24,20)", {}),
+                                     ("pressure27(16,16,16)", {"ilu.variant": "ilut", "ilu.droptol": "1e-3",
+                                                               "ilu.lfill": "5"})])
+def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule, spec, kv):
+    """Both level-set schedules (single CTA / sync-free flags) give the serial
+    result bitwise, for the triangular solves and the Gauss-Seidel sweep."""
+    monkeypatch.setenv("ILUG_LEVELSET", schedule)
+    A, L, U, f, fr = _factors(ilug, ref, spec, kv, "row", direct=True)
+    b = np.random.default_rng(31).uniform(-1, 1, A.rows)
+    bd = _dev(torch_cuda, b)
+    y = torch_cuda.empty_like(bd)
+    f.solve_lower(bd, y)
+    assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
+    f.solve_upper(bd, y)
+    assert bitwise(_host(y), ref.solve_upper_scaled_direct(fr, b))
+    S = ilug.Smoother(A, ilug.Config().set("smoother.kind", "gauss_seidel"))
+    x0 = np.random.default_rng(32).uniform(-1, 1, A.rows)
+    xd = _dev(torch_cuda, x0)
+    S.smooth(bd, xd)
+    Ar = ref.mat(*A.csr())
+    want, _ = ref.smooth(Ar, ref.smoother(Ar, ref.cfg({"smoother.kind": "gauss_seidel"})), b, x0)
+    assert bitwise(_host(xd), want)
+
+
+def test_k5_wide_dag_flags_bitwise(ilug, ref, torch_cuda):
+    """A DAG wide enough for the sync-free schedule by default (n / levels > 2048)."""
+    A, L, U, f, fr = _factors(ilug, ref, "poisson3d(160,160,40)", {}, "row", direct=True)
+    st = f.stats()
+    assert A.rows / st["levels_L"] > 2048
+    b = np.random.default_rng(33).uniform(-1, 1, A.rows)
+    bd = _dev(torch_cuda, b)
+    y = torch_cuda.empty_like(bd)
+    for _ in range(2):  # epoch-stamped flags: repeated solves need no reset
+        f.solve_lower(bd, y)
+        assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
+        f.solve_upper(bd, y)
+        assert bitwise(_host(y), ref.solve_upper_scaled_direct(fr, b))
+
+
+def test_k5_direct_at_scale_bitwise(ilug, ref, torch_cuda):
+    """27-point 128^3 (2.1M rows, sync-free schedule): direct solves bitwise vs
+    the reference, and the triangular residual at rounding level."""
+    A, L, U, f, fr = _factors(ilug, ref, "pressure27(128,128,128)", {}, "row", direct=True)
+    st = f.stats()
+    assert A.rows / st["levels_U"] > 2048
+    b = np.random.default_rng(34).uniform(-1, 1, A.rows)
+    bd = _dev(torch_cuda, b)
+    y = torch_cuda.empty_like(bd)
+    f.solve_upper(bd, y)
+    got = _host(y)
+    assert bitwise(got, ref.solve_upper_scaled_direct(fr, b))
+    f.solve_lower(bd, y)
+    assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))

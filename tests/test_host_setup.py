@@ -51,6 +51,18 @@ def test_ilu_factors_bitwise(ilug, ref, spec, kv):
     assert _same(U.csr(), Ur)
 
 
+@pytest.mark.parametrize("spec", ["pressure27(40,40,40)", "poisson3d(48,48,48)"])
+def test_ilut_pipelined_parallel_bitwise(ilug, ref, spec):
+    """Sizes large enough for the pipelined multi-worker ILUT (and level-parallel
+    ILU(0)): still bitwise the serial reference."""
+    kv = {"ilu.variant": "ilut", "ilu.droptol": "1e-3", "ilu.lfill": "5"}
+    A = ilug.Matrix.generate(spec)
+    for cfg in (kv, {}):
+        L, U = ilug.ilu_factorize(A, ilug.Config().update(cfg))
+        Lr, Ur, _, _ = ref.factors_arrays(ref.ilu(ref.mat(*A.csr()), ref.cfg(cfg)))
+        assert _same(L.csr(), Lr) and _same(U.csr(), Ur)
+
+
 def test_ilu0_zero_pivot_policy(ilug, ref):
     # a_00 = 0 with the diagonal stored: error by default, patched under replace
     rp, ci, v = np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([0.0, 1.0, 1.0, 1.0])
