@@ -462,7 +462,7 @@ int ilug_smoother_create(const iluamg_matrix* A, const iluamg_config* cfg, int w
             s->dA.build(s->A, nullptr);
             s->s.build(s->A, s->dA, sc, nullptr);
             s->r.alloc(std::max<ilug::i64>(s->A.nrows, 1));
-            s->scratch.alloc(1);
+            s->scratch.alloc(1 + ilug::reduce_ws_doubles(s->A.nrows));
         } catch (...) {
             delete s;
             throw;
@@ -477,7 +477,7 @@ int ilug_smooth(const ilug_smoother* s, const double* b, double* x, double* resn
         s->s.smooth(b, x, false, S(stream));
         if (resnorm) {
             ilug::residual(s->dA.A, x, b, s->r.p, S(stream));
-            ilug::nrm2sq_dev(s->r.p, s->A.nrows, s->scratch.p, S(stream));
+            ilug::nrm2sq_dev(s->r.p, s->A.nrows, s->scratch.p, s->scratch.p + 1, S(stream));
             double h = 0.0;
             ILUG_CUDA(cudaMemcpyAsync(&h, s->scratch.p, sizeof h, cudaMemcpyDeviceToHost, S(stream)));
             ILUG_CUDA(cudaStreamSynchronize(S(stream)));

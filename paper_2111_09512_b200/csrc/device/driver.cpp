@@ -46,6 +46,7 @@ struct SolveOutcome {
     HostHierarchy hier;
     double setup_seconds = 0.0, solve_seconds = 0.0;
     i64 graph_nodes = 0;
+    i64 schur_interface = 0;
 };
 
 SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& kp, const Vec& b,
@@ -71,6 +72,8 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     dx.download(oc.x.data(), st);
     ILUG_CUDA(cudaStreamSynchronize(st));
     oc.graph_nodes = dh.kernels_per_cycle();
+    if (dh.num_levels() > 1 && dh.smoother(0).schur())
+        oc.schur_interface = dh.smoother(0).schur()->interface_size();
     return oc;
 }
 
@@ -213,7 +216,7 @@ Report run_solve(const Csr& A, const Config& cfg, const std::string& label) {
 namespace {
 
 double dev_norm2(const double* v, i64 n, double* scratch, cudaStream_t st) {
-    nrm2sq_dev(v, n, scratch, st);
+    nrm2sq_dev(v, n, scratch, scratch + 1, st);
     double h = 0.0;
     ILUG_CUDA(cudaMemcpyAsync(&h, scratch, sizeof h, cudaMemcpyDeviceToHost, st));
     ILUG_CUDA(cudaStreamSynchronize(st));
@@ -260,7 +263,7 @@ Report run_bench_trisolve(const Csr& A, const Config& cfg, const std::string& la
     dev.build(f, sc, UpperIteration::scaled, true, st);
     const i64 n = A.nrows;
     const Vec bh = random_uniform(n, seed);
-    DBuf<double> b, yl(n), yu(n), z(n), d(n), ws(3 * std::max<i64>(n, 1)), scr(1);
+    DBuf<double> b, yl(n), yu(n), z(n), d(n), ws(3 * std::max<i64>(n, 1)), scr(1 + reduce_ws_doubles(n));
     b.upload(bh.data(), n, st);
     dev.solve_lower(b.p, yl.p, st);
     dev.solve_upper(b.p, yu.p, ws.p, st);
@@ -293,9 +296,51 @@ Report run_bench_trisolve(const Csr& A, const Config& cfg, const std::string& la
     return r;
 }
 
+// run_schur_solve (src/driver.cpp:318-375): one solve per block count of
+// schur.blocks_list with the Schur smoother on the finest level, FGMRES forced
+// (the one-step interface GMRES makes the preconditioner nonstationary).
 Report run_schur_solve(const Csr& A, const Config& cfg, const std::string& label) {
-    (void)A, (void)cfg, (void)label;
-    fail_invalid("schur-solve: the Schur-complement smoother is not available on the device yet");
+    std::vector<i64> blocks;
+    {
+        std::string list = cfg.get("schur.blocks_list");
+        for (char& c : list)
+            if (c == ',') c = ' ';
+        std::istringstream in(list);
+        i64 p = 0;
+        while (in >> p) blocks.push_back(p);
+        if (blocks.empty()) fail_invalid("schur-solve: schur.blocks_list is empty");
+    }
+    KrylovParams kp = krylov_from(cfg);
+    kp.flexible = true;
+    const Vec b = make_rhs(cfg, A);
+    DeviceContext ctx(cfg);
+    Report r;
+    r.add("matrix", label);
+    r.add("n", A.nrows);
+    r.add("nnz", A.nnz());
+    r.add("method", "fgmres");
+    ReportTable t;
+    t.name = "schur";
+    t.columns = {"p", "interface_size", "iterations", "converged", "final_relres", "final_nrbe"};
+    i64 it_min = -1, it_max = -1;
+    for (i64 p : blocks) {
+        AmgParams ap = amg_params_from(cfg);
+        ap.plan.finest = schur_smoother_from(cfg);
+        ap.plan.finest.schur_blocks = p;
+        ap.plan.finest_levels = 1;
+        const SolveOutcome oc = solve_with(A, ap, kp, b, cfg.get_bool("device.graph"), ctx.stream);
+        t.rows.push_back({std::to_string(p), std::to_string(oc.schur_interface), std::to_string(oc.kr.iterations),
+                          oc.kr.converged ? "true" : "false", format_num(oc.kr.final_relres),
+                          format_num(oc.kr.final_nrbe)});
+        if (!oc.kr.converged) r.status = 1;
+        if (it_min < 0 || oc.kr.iterations < it_min) it_min = oc.kr.iterations;
+        if (it_max < 0 || oc.kr.iterations > it_max) it_max = oc.kr.iterations;
+    }
+    r.add("iterations_min", it_min);
+    r.add("iterations_max", it_max);
+    r.add("iterations_spread", it_max - it_min);
+    r.tables.push_back(std::move(t));
+    return r;
 }
 
 Report run_analyze(const Csr& A, const Config& cfg, const std::string& label) {

@@ -18,8 +18,9 @@ namespace {
 
 struct Scalars {
     DBuf<double> d;   // device scalars: h1[64] h2[64] nrm[1] misc[8]
+    DBuf<double> ws;  // reduction workspace
     std::vector<double> h;
-    Scalars() : d(64 * 2 + 16), h(64 * 2 + 16) {}
+    explicit Scalars(i64 n) : d(64 * 2 + 16), ws(reduce_ws_doubles(n)), h(64 * 2 + 16) {}
     double* h1() { return d.p; }
     double* h2() { return d.p + 64; }
     double* nrm() { return d.p + 128; }
@@ -27,7 +28,7 @@ struct Scalars {
 };
 
 double dev_norm(const double* v, i64 n, Scalars& s, cudaStream_t st) {
-    nrm2sq_dev(v, n, s.misc(), st);
+    nrm2sq_dev(v, n, s.misc(), s.ws.p, st);
     double h = 0.0;
     ILUG_CUDA(cudaMemcpyAsync(&h, s.misc(), sizeof h, cudaMemcpyDeviceToHost, st));
     ILUG_CUDA(cudaStreamSynchronize(st));
@@ -52,7 +53,7 @@ double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 st
     v.upload(v0.data(), A.n, st);
     w.alloc(A.n);
     u.alloc(A.n);
-    Scalars sc;
+    Scalars sc(A.n);
     for (i64 s = 0; s < steps; ++s) {
         spmv(A.A, v.p, w.p, st);
         spmv(At, w.p, u.p, st);
@@ -72,7 +73,7 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
     if (!(p.tol > 0.0)) fail_invalid("gmres: tol must be > 0");
     const i64 R = p.restart;
     KrylovReport rep;
-    Scalars sc;
+    Scalars sc(n);
     rep.anorm_estimate = p.estimate_anorm ? device_estimate_two_norm(A, A_host, 50, p.anorm_seed, st)
                                           : std::nan("");
     rep.bnorm = dev_norm(b, n, sc, st);
@@ -139,9 +140,9 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
             ++rep.vcycles;
             spmv(A.A, zj, w.p, st);
             const int k = static_cast<int>(j + 1);
-            multi_dot(V.p, n, k, w.p, n, sc.h1(), st);
-            multi_axpy_dot(V.p, n, k, sc.h1(), w.p, n, sc.h2(), st);
-            multi_axpy_nrm(V.p, n, k, sc.h2(), w.p, n, sc.nrm(), st);
+            multi_dot(V.p, n, k, w.p, n, sc.h1(), sc.ws.p, st);
+            multi_axpy_dot(V.p, n, k, sc.h1(), w.p, n, sc.h2(), sc.ws.p, st);
+            multi_axpy_nrm(V.p, n, k, sc.h2(), w.p, n, sc.nrm(), sc.ws.p, st);
             ILUG_CUDA(cudaMemcpyAsync(sc.h.data(), sc.d.p, sizeof(double) * 129, cudaMemcpyDeviceToHost, st));
             ILUG_CUDA(cudaStreamSynchronize(st));
             for (i64 i = 0; i <= j; ++i) h(i, j) = sc.h[i] + sc.h[64 + i];

@@ -1,0 +1,136 @@
+// K9: the ILUT Schur-complement smoother (reference: schur_smooth,
+// src/schur.cpp:158-219), device side. Every vector step is a kernel; the
+// three scalars of the one-iteration interface GMRES (beta, h11, h21^2) and
+// the step length alpha stay in device memory, so one application is a fixed
+// launch sequence with no host round trip (capturable in the V-cycle graph).
+#include "solver.hpp"
+
+namespace ilug {
+
+namespace {
+
+constexpr int kB = 256;
+
+inline unsigned grid_of(i64 n) {
+    return static_cast<unsigned>(std::max<i64>(1, std::min<i64>((n + kB - 1) / kB, 148 * 64)));
+}
+
+// fg[perm[i]] = r[i]: interior values first, then interface (src/schur.cpp:166-172)
+__global__ void k_split(i64 n, const i32* __restrict__ perm, const double* __restrict__ r,
+                        double* __restrict__ fg) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        fg[perm[i]] = r[i];
+}
+
+// x[i] += upd[perm[i]] (interior += x_I, interface += y; src/schur.cpp:214-217)
+__global__ void k_merge(i64 n, const i32* __restrict__ perm, const double* __restrict__ upd,
+                        double* __restrict__ x) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        x[i] = x[i] + upd[perm[i]];
+}
+
+// v1 = gt / beta with beta = sqrt(beta2) (only meaningful when beta > 0; for
+// beta == 0, gt == 0 and v1 = 0 keeps every later product zero).
+__global__ void k_normalize(i64 n, const double* __restrict__ gt, const double* __restrict__ sc,
+                            double* __restrict__ v1) {
+    const double beta = sqrt(sc[0]);
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        v1[i] = beta > 0.0 ? gt[i] / beta : 0.0;
+}
+
+// alpha = beta h11 / (h11^2 + h21^2) if the denominator is positive, else 0
+// (src/schur.cpp:197-204); y = alpha v1.
+__global__ void k_step(i64 n, const double* __restrict__ sc, const double* __restrict__ v1,
+                       double* __restrict__ y) {
+    const double beta = sqrt(sc[0]), h11 = sc[1], h21sq = sc[2];
+    const double denom = h11 * h11 + h21sq;
+    const bool go = beta > 0.0 && denom > 0.0;
+    const double alpha = go ? beta * h11 / denom : 0.0;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        y[i] = go ? alpha * v1[i] : 0.0;
+}
+
+} // namespace
+
+void DeviceSchur::build(const Csr& A, const SmootherConfig& cfg, cudaStream_t st) {
+    SchurSetup s = schur_partition(A, cfg.schur_blocks);
+    schur_factorize(s, cfg.ilu_params, cfg.scaling, cfg.trisolve);
+    n_ = A.nrows;
+    ni_ = static_cast<i64>(s.interior_idx.size());
+    nf_ = static_cast<i64>(s.interface_idx.size());
+    ts_ = cfg.trisolve;
+    const bool rich = ts_.mode == TriSolveMode::richardson;
+    blocks_.build(s.factors, cfg.scaling, UpperIteration::scaled, !rich, st);
+    sell_from_host(E_, s.E, Part::all, st);
+    sell_from_host(F_, s.F, Part::all, st);
+    sell_from_host(C_, s.C, Part::all, st);
+    std::vector<i32> perm(s.perm.begin(), s.perm.end());
+    perm_.upload(perm.data(), n_, st);
+    // ws: r(n) fg(n) t(ni) gt(nf) v1(nf) w(nf) tE(ni) tB(ni) upd(n) L/U sweep scratch 3*ni + ni
+    ws_.alloc(3 * n_ + 4 * ni_ + 3 * nf_ + 4 * ni_ + 8);
+    red_.alloc(reduce_ws_doubles(std::max(n_, i64{1})));
+    scal_.alloc(8);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceSchur::block_solve(const double* f, double* out, cudaStream_t st) const {
+    // block_solve (src/schur.cpp:137-156) over the block-diagonal interior factor
+    double* y = ws_.p + 3 * n_ + 4 * ni_ + 3 * nf_;
+    double* scr = y + ni_;
+    if (ts_.mode == TriSolveMode::direct) {
+        blocks_.solve_lower(f, y, st);
+        blocks_.solve_upper(y, out, scr, st);
+    } else {
+        blocks_.sweep_lower(f, y, ts_.m_lower, scr, st);
+        blocks_.sweep_upper(y, out, ts_.m_upper, scr, st);
+    }
+}
+
+void DeviceSchur::apply(const DeviceMatrix& A, const double* b, double* x, cudaStream_t st) const {
+    double* r = ws_.p;
+    double* fg = r + n_;         // [f | g]
+    double* upd = fg + n_;       // [x_I | y]
+    double* t = upd + n_;        // ni
+    double* tE = t + ni_;        // ni
+    double* tB = tE + ni_;       // ni
+    double* fi = tB + ni_;       // ni
+    double* gt = fi + ni_;       // nf
+    double* v1 = gt + nf_;       // nf
+    double* w = v1 + nf_;        // nf
+    double* f = fg;
+    double* g = fg + ni_;
+    double* xI = upd;
+    double* y = upd + ni_;
+    double* sc = scal_.p;        // beta^2, h11, h21^2
+
+    residual(A.A, x, b, r, st);
+    k_split<<<grid_of(n_), kB, 0, st>>>(n_, perm_.p, r, fg);
+    ILUG_LAUNCH_CHECK();
+    if (nf_ > 0) {
+        block_solve(f, t, st);
+        residual(F_, t, g, gt, st);                   // gt = g - F B^-1 f
+        nrm2sq_dev(gt, nf_, sc, red_.p, st);          // beta^2
+        k_normalize<<<grid_of(nf_), kB, 0, st>>>(nf_, gt, sc, v1);
+        ILUG_LAUNCH_CHECK();
+        spmv(E_, v1, tE, st);                         // E v1
+        block_solve(tE, tB, st);                      // B^-1 E v1
+        spmv(C_, v1, w, st);                          // w = C v1
+        residual(F_, tB, w, w, st);                   // w = w - F B^-1 E v1 (row-local: in-place safe)
+        dot_dev(v1, w, nf_, sc + 1, red_.p, st);      // h11
+        nrm2sq_diff_dev(w, v1, sc + 1, nf_, sc + 2, red_.p, st); // h21^2
+        k_step<<<grid_of(nf_), kB, 0, st>>>(nf_, sc, v1, y);
+        ILUG_LAUNCH_CHECK();
+        residual(E_, y, f, fi, st);                   // f - E y
+    } else {
+        vec_copy(fi, f, ni_, st);
+    }
+    block_solve(fi, xI, st);
+    k_merge<<<grid_of(n_), kB, 0, st>>>(n_, perm_.p, upd, x);
+    ILUG_LAUNCH_CHECK();
+}
+
+} // namespace ilug

@@ -203,7 +203,9 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         break;
     }
     case SmootherKind::schur_ilut:
-        fail_invalid("schur_ilut: the Schur-complement smoother is not available on the device yet");
+        schur_ = std::make_unique<DeviceSchur>();
+        schur_->build(A, cfg, st);
+        break;
     }
     ws_.alloc(7 * std::max<i64>(n_, 1));
     ILUG_CUDA(cudaStreamSynchronize(st));
@@ -318,7 +320,8 @@ void DeviceSmoother::smooth(const double* b, double* x, bool x_zero, cudaStream_
             ilu_sweep(b, x, zero, st);
             break;
         case SmootherKind::schur_ilut:
-            fail_invalid("schur_ilut: not available on the device yet");
+            schur_->apply(*A_, b, x, st);
+            break;
         }
     }
 }

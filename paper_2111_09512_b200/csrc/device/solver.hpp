@@ -10,6 +10,7 @@
 #pragma once
 
 #include "../host/amg.hpp"
+#include "../host/schur.hpp"
 #include "../kernels/levelset.hpp"
 
 #include <memory>
@@ -72,6 +73,30 @@ private:
     Csr U_pattern_;          // host structure of U (values are the unscaled ones)
 };
 
+/// K9: the ILUT Schur-complement smoother (src/schur.cpp:137-219) on the device.
+/// Block solves run on the block-diagonal factor of the interior unknowns (all
+/// blocks at once; rows never couple across blocks, so this is exactly the
+/// reference's per-block loop); the one-step interface GMRES keeps its scalars
+/// (beta, h11, h21^2, alpha) in device memory, so an application never syncs
+/// the host and can live inside the V-cycle graph.
+class DeviceSchur {
+public:
+    void build(const Csr& A, const SmootherConfig& cfg, cudaStream_t st);
+    /// x <- schur_smooth(A, b, x)
+    void apply(const DeviceMatrix& A, const double* b, double* x, cudaStream_t st) const;
+    i64 interface_size() const { return nf_; }
+    i64 interior_size() const { return ni_; }
+
+private:
+    void block_solve(const double* f, double* out, cudaStream_t st) const;
+    i64 n_ = 0, ni_ = 0, nf_ = 0;
+    TriSolveConfig ts_;
+    DeviceIlu blocks_;
+    Sell E_, F_, C_;
+    DBuf<i32> perm_;
+    mutable DBuf<double> ws_, red_, scal_;
+};
+
 /// One level's smoother (src/smoother.cpp:161-187 `smooth`).
 class DeviceSmoother {
 public:
@@ -83,6 +108,7 @@ public:
     void ilu_sweep(const double* b, double* x, bool x_zero, cudaStream_t st) const;
     const SmootherConfig& config() const { return cfg_; }
     const DeviceIlu* ilu() const { return ilu_.get(); }
+    const DeviceSchur* schur() const { return schur_.get(); }
     i64 n() const { return n_; }
 
 private:
@@ -90,6 +116,7 @@ private:
     i64 n_ = 0;
     const DeviceMatrix* A_ = nullptr;
     std::unique_ptr<DeviceIlu> ilu_;
+    std::unique_ptr<DeviceSchur> schur_;
     std::unique_ptr<LevelPlan> gs_;
     Sell Lstrict_;               // poly_gs
     DBuf<double> invd_;          // jacobi / l1 / poly_gs

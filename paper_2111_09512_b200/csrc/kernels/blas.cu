@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(kBlock)
 k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ hin,
         double* __restrict__ w, const double* __restrict__ w2, i64 n, double* __restrict__ partial) {
     // MODE 0: dot(w, w2) -> 1 output; MODE 1: ||w||^2; MODE 2: V^T w (k outputs);
-    // MODE 3: w -= V hin, then V^T w; MODE 4: w -= V hin, then ||w||^2.
+    // MODE 3: w -= V hin, then V^T w; MODE 4: w -= V hin, then ||w||^2;
+    // MODE 5: sum_i (w_i - h v_i)^2 with h = hin[0], v = w2 (Schur h21^2).
     __shared__ double red[kBlock / 32][kMaxVec];
     __shared__ double hs[kMaxVec];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -101,11 +102,17 @@ k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ 
         }
     }
     int nout = 1;
-    if (MODE == 0 || MODE == 1 || MODE == 4) {
+    if (MODE == 0 || MODE == 1 || MODE == 4 || MODE == 5) {
         double s = 0.0;
+        const double h = MODE == 5 ? hin[0] : 0.0;
 #pragma unroll
         for (int u = 0; u < kRows; ++u) {
             const i64 i = base + u * kBlock;
+            if (MODE == 5) {
+                const double dv = i < n ? wv[u] - h * w2[i] : 0.0;
+                s += dv * dv;
+                continue;
+            }
             const double o = MODE == 0 ? (i < n ? w2[i] : 0.0) : wv[u];
             s += wv[u] * o;
         }
@@ -163,30 +170,18 @@ __global__ void k_combine(const double* __restrict__ V, i64 ld, int k, const dou
     }
 }
 
-// Thread-private scratch for the two-stage reductions, one per device.
-struct Scratch {
-    DBuf<double> partial;
-    i64 cap = 0;
-};
-Scratch& scratch() {
-    static thread_local Scratch s;
-    return s;
-}
-
+// Two-stage reductions write their per-block partials into caller-owned
+// workspace (reduce_ws_doubles(n) doubles): no hidden state, graph-capturable,
+// and concurrent solves on different streams never share scratch.
 template <int MODE>
 void tiled(const double* V, i64 ld, int k, const double* hin, double* w, const double* w2, i64 n,
-           double* out, int nout, cudaStream_t st) {
+           double* out, int nout, double* ws, cudaStream_t st) {
     if (k > kMaxVec) fail_invalid("CGS2: more than 64 basis vectors per call");
+    if (!ws) fail_invalid("reduction: no workspace");
     const i64 nb = std::max<i64>(1, (n + kTile - 1) / kTile);
-    Scratch& sc = scratch();
-    if (sc.cap < nb) {
-        ILUG_CUDA(cudaStreamSynchronize(st));
-        sc.partial.alloc(nb * kMaxVec);
-        sc.cap = nb;
-    }
-    k_tiled<MODE><<<static_cast<unsigned>(nb), kBlock, 0, st>>>(V, ld, k, hin, w, w2, n, sc.partial.p);
+    k_tiled<MODE><<<static_cast<unsigned>(nb), kBlock, 0, st>>>(V, ld, k, hin, w, w2, n, ws);
     ILUG_LAUNCH_CHECK();
-    k_finish<<<1, kBlock, 0, st>>>(sc.partial.p, nb, nout, out);
+    k_finish<<<1, kBlock, 0, st>>>(ws, nb, nout, out);
     ILUG_LAUNCH_CHECK();
 }
 
@@ -255,22 +250,27 @@ void vec_sub_into(double* o, const double* a, const double* b, i64 n, cudaStream
     k_sub_into<<<ew_grid(n), kBlock, 0, st>>>(o, a, b, n);
     ILUG_LAUNCH_CHECK();
 }
-void dot_dev(const double* a, const double* b, i64 n, double* out, cudaStream_t st) {
-    tiled<0>(nullptr, 0, 0, nullptr, const_cast<double*>(a), b, n, out, 1, st);
+i64 reduce_ws_doubles(i64 n) { return std::max<i64>(1, (n + kTile - 1) / kTile) * kMaxVec; }
+void dot_dev(const double* a, const double* b, i64 n, double* out, double* ws, cudaStream_t st) {
+    tiled<0>(nullptr, 0, 0, nullptr, const_cast<double*>(a), b, n, out, 1, ws, st);
 }
-void nrm2sq_dev(const double* a, i64 n, double* out, cudaStream_t st) {
-    tiled<1>(nullptr, 0, 0, nullptr, const_cast<double*>(a), nullptr, n, out, 1, st);
+void nrm2sq_dev(const double* a, i64 n, double* out, double* ws, cudaStream_t st) {
+    tiled<1>(nullptr, 0, 0, nullptr, const_cast<double*>(a), nullptr, n, out, 1, ws, st);
 }
-void multi_dot(const double* V, i64 ld, int k, const double* w, i64 n, double* h, cudaStream_t st) {
-    tiled<2>(V, ld, k, nullptr, const_cast<double*>(w), nullptr, n, h, k, st);
+void nrm2sq_diff_dev(const double* w, const double* v, const double* h, i64 n, double* out, double* ws,
+                     cudaStream_t st) {
+    tiled<5>(nullptr, 0, 0, h, const_cast<double*>(w), v, n, out, 1, ws, st);
+}
+void multi_dot(const double* V, i64 ld, int k, const double* w, i64 n, double* h, double* ws, cudaStream_t st) {
+    tiled<2>(V, ld, k, nullptr, const_cast<double*>(w), nullptr, n, h, k, ws, st);
 }
 void multi_axpy_dot(const double* V, i64 ld, int k, const double* hin, double* w, i64 n, double* hout,
-                    cudaStream_t st) {
-    tiled<3>(V, ld, k, hin, w, nullptr, n, hout, k, st);
+                    double* ws, cudaStream_t st) {
+    tiled<3>(V, ld, k, hin, w, nullptr, n, hout, k, ws, st);
 }
 void multi_axpy_nrm(const double* V, i64 ld, int k, const double* hin, double* w, i64 n, double* out,
-                    cudaStream_t st) {
-    tiled<4>(V, ld, k, hin, w, nullptr, n, out, 1, st);
+                    double* ws, cudaStream_t st) {
+    tiled<4>(V, ld, k, hin, w, nullptr, n, out, 1, ws, st);
 }
 void multi_combine(const double* V, i64 ld, int k, const double* c, const double* base, double* y,
                    i64 n, cudaStream_t st) {

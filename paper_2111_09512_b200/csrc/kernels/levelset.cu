@@ -46,9 +46,7 @@ __device__ __forceinline__ bool is_dep(i32 j, i64 row) {
 // gathers (waiting on the producers' flags in the sync-free schedule), then
 // the ordered accumulation — a row costs ~2 memory latencies per chunk instead
 // of 2 per entry.
-constexpr int kChunk = 8;
-
-template <int MODE, bool FLAGS>
+template <int MODE, bool FLAGS, int kChunk = FLAGS ? 16 : 8>
 __device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, const double* __restrict__ b,
                                           double* x, const double* __restrict__ xold, unsigned* flags,
                                           unsigned E) {
@@ -192,7 +190,11 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     sell_from_device_csr(M_, T, rp.p, ci.p, dev_vals ? dev_vals : v.p, Part::all, perm, st);
 
     // Narrow DAG (average level width below two CTAs' worth): one CTA.
-    single_cta_ = n == 0 || n / std::max(nl, 1) <= 2 * kSmallBlock;
+    // One CTA only for tiny systems: with __syncthreads per level every level
+    // costs its full row latency; the sync-free schedule overlaps the loads of
+    // later levels with the wait on earlier ones, which wins as soon as there
+    // is more than a CTA's worth of rows.
+    single_cta_ = n <= 4 * kSmallBlock;
     if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | flags
         if (std::string(force) == "cta") single_cta_ = true;
         if (std::string(force) == "flags" && n > 0) single_cta_ = false;

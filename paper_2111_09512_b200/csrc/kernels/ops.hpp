@@ -69,19 +69,25 @@ void vec_add_into(double* out, const double* a, const double* b, i64 n, cudaStre
 void vec_sub_into(double* out, const double* a, const double* b, i64 n, cudaStream_t st); // out = a - b
 
 /// Deterministic reductions: fixed grid, per-block partial sums, ordered final pass.
-/// Results are written to device memory (out[0..]).
-void dot_dev(const double* a, const double* b, i64 n, double* out, cudaStream_t st);
-void nrm2sq_dev(const double* a, i64 n, double* out, cudaStream_t st);
+/// Results are written to device memory (out[0..]); `ws` is caller-owned device
+/// workspace of reduce_ws_doubles(n) doubles (one in-flight reduction per ws).
+i64 reduce_ws_doubles(i64 n);
+void dot_dev(const double* a, const double* b, i64 n, double* out, double* ws, cudaStream_t st);
+void nrm2sq_dev(const double* a, i64 n, double* out, double* ws, cudaStream_t st);
+/// out = sum_i (w_i - h v_i)^2 with the scalar h read from device memory
+void nrm2sq_diff_dev(const double* w, const double* v, const double* h, i64 n, double* out, double* ws,
+                     cudaStream_t st);
 
 /// CGS2 passes over the Krylov basis V (k vectors, leading dimension ld):
 /// h[0..k) = V^T w
-void multi_dot(const double* V, i64 ld, int k, const double* w, i64 n, double* h, cudaStream_t st);
+void multi_dot(const double* V, i64 ld, int k, const double* w, i64 n, double* h, double* ws,
+               cudaStream_t st);
 /// w -= V h_in; then h_out[0..k) = V^T w (fused: one read of V and w)
 void multi_axpy_dot(const double* V, i64 ld, int k, const double* h_in, double* w, i64 n,
-                    double* h_out, cudaStream_t st);
+                    double* h_out, double* ws, cudaStream_t st);
 /// w -= V h_in; then out[0] = ||w||^2 (fused)
 void multi_axpy_nrm(const double* V, i64 ld, int k, const double* h_in, double* w, i64 n,
-                    double* out, cudaStream_t st);
+                    double* out, double* ws, cudaStream_t st);
 /// y = base + sum_i c_i V_i (base may be null = 0.0), accumulated per element in
 /// ascending i exactly like the reference's x_k / vy loops (src/krylov.cpp:200-211).
 void multi_combine(const double* V, i64 ld, int k, const double* c, const double* base, double* y,

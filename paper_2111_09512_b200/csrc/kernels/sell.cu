@@ -8,7 +8,9 @@
 // (--fmad=false): bitwise equal to src/sparse.cpp:162-174.
 #include "ops.hpp"
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 namespace ilug {
 
@@ -148,7 +150,41 @@ struct EpiNegScaleAcc { // poly_gs: term = -invd * t; acc += term
     }
 };
 
+// Wider variant: eight entries per batch with predicated loads, so a row of up
+// to eight entries (the L factor's 7.5 on average at C2) costs one streamed
+// round trip plus one gather round trip.
 template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_rowdot8(SellView M, i64 nrows, const double* __restrict__ x,
+                                                     Epi epi) {
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= M.nrows_pad) return;
+    const i64 row = M.perm ? M.perm[p] : p;
+    if (row < 0 || row >= nrows) return;
+    const int len = M.rowlen[p];
+    const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
+    const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
+    double s = 0.0;
+    for (int t = 0; t < len; t += 8) {
+        double a[8], xv[8];
+        int c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (t + u < len) {
+                a[u] = ld_stream(vp + (t + u) * kSlice);
+                c[u] = ld_stream(cp + (t + u) * kSlice);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (t + u < len) xv[u] = ld_gather(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (t + u < len) s = s + a[u] * xv[u];
+    }
+    epi(row, s);
+}
+
+template <class Epi, bool HINT>
 __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
                                                     Epi epi) {
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
@@ -158,6 +194,11 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
     const int len = M.rowlen[p];
     const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
     const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
+    unsigned long long pf = 0, pl = 0;
+    if (HINT) pf = l2_policy_first(), pl = l2_policy_last();
+    auto lv = [&](int t) { return HINT ? ld_stream(vp + t * kSlice, pf) : ld_stream(vp + t * kSlice); };
+    auto lc = [&](int t) { return HINT ? ld_stream(cp + t * kSlice, pf) : ld_stream(cp + t * kSlice); };
+    auto lx = [&](int c) { return HINT ? ld_gather(x + c, pl) : ld_gather(x + c); };
     double s = 0.0;
     int t = 0;
     // Four entries in flight per lane: issue the streamed loads, then the
@@ -167,23 +208,40 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
         int c[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            a[u] = ld_stream(vp + (t + u) * kSlice);
-            c[u] = ld_stream(cp + (t + u) * kSlice);
+            a[u] = lv(t + u);
+            c[u] = lc(t + u);
         }
         double xv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = ld_gather(x + c[u]);
+        for (int u = 0; u < 4; ++u) xv[u] = lx(c[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) s = s + a[u] * xv[u];
     }
-    for (; t < len; ++t) s = s + ld_stream(vp + t * kSlice) * ld_gather(x + ld_stream(cp + t * kSlice));
+    for (; t < len; ++t) s = s + lv(t) * lx(lc(t));
     epi(row, s);
+}
+
+// Kernel variant knobs for A/B experiments (tools/probe_sweep.py):
+// ILUG_L2_HINTS=1 enables the L2 eviction-priority hints (measured neutral on
+// B200 at C2, so off by default); ILUG_ROWDOT=4|8 picks the batch width.
+bool l2_hints() {
+    const char* e = std::getenv("ILUG_L2_HINTS");
+    return e && e[0] == '1';
+}
+int rowdot_width() {
+    const char* e = std::getenv("ILUG_ROWDOT");
+    return e && e[0] == '4' ? 4 : 8;
 }
 
 template <class Epi>
 void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
     if (M.nrows_pad == 0) return;
-    k_rowdot<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    if (rowdot_width() == 8)
+        k_rowdot8<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (l2_hints())
+        k_rowdot<Epi, true><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    else
+        k_rowdot<Epi, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     ILUG_LAUNCH_CHECK();
 }
 
@@ -247,16 +305,61 @@ i64 part_len(const Csr& A, i64 row, int pc) {
     return c;
 }
 
+// SELL-C-sigma row order: within windows of sigma rows, rows sorted by
+// decreasing length so each 32-row slice holds rows of similar length (less
+// padding streamed). Returns an empty vector (natural order) when sorting would
+// cut the padded size by less than 3 % — then the extra perm read is not worth it.
+// sigma comes from ILUG_SELL_SIGMA (default 1024; 1 disables).
+template <typename LenOf>
+std::vector<i32> sigma_order(i64 n, LenOf len_of) {
+    const i64 sigma = [] {
+        const char* e = std::getenv("ILUG_SELL_SIGMA");
+        return e ? std::max<i64>(1, std::atoll(e)) : i64{1024};
+    }();
+    if (sigma <= 1 || n < 2 * kSlice) return {};
+    const i64 pad = (n + kSlice - 1) / kSlice * kSlice;
+    std::vector<i32> len(static_cast<size_t>(n));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) len[i] = static_cast<i32>(len_of(i));
+    });
+    std::vector<i32> perm(static_cast<size_t>(pad), -1);
+    for (i64 i = 0; i < n; ++i) perm[i] = static_cast<i32>(i);
+    const i64 wins = (n + sigma - 1) / sigma;
+    parallel_ranges(wins, [&](i64 b, i64 e, int) {
+        for (i64 w = b; w < e; ++w) {
+            auto lo = perm.begin() + w * sigma, hi = perm.begin() + std::min(n, (w + 1) * sigma);
+            std::stable_sort(lo, hi, [&](i32 a, i32 c) { return len[a] > len[c]; });
+        }
+    }, 1);
+    auto padded = [&](bool sorted) {
+        i64 tot = 0;
+        for (i64 s = 0; s < pad / kSlice; ++s) {
+            i32 w = 0;
+            for (i64 l = 0; l < kSlice; ++l) {
+                const i64 p = s * kSlice + l;
+                if (p < n) w = std::max(w, len[sorted ? perm[p] : p]);
+            }
+            tot += w;
+        }
+        return tot;
+    };
+    if (padded(true) > 0.97 * static_cast<double>(padded(false))) return {};
+    return perm;
+}
+
 } // namespace
 
 void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i32* ci,
-                          const double* v, Part part, const std::vector<i32>& perm_host,
+                          const double* v, Part part, const std::vector<i32>& perm_in,
                           cudaStream_t s) {
     out.nrows = pattern.nrows;
     out.ncols = pattern.ncols;
+    const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
+    const std::vector<i32> perm_host =
+        perm_in.empty() ? sigma_order(pattern.nrows, [&](i64 r) { return part_len(pattern, r, pc); })
+                        : perm_in;
     const i64 pad = perm_host.empty() ? (pattern.nrows + kSlice - 1) / kSlice * kSlice
                                       : static_cast<i64>(perm_host.size());
-    const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
     layout(out, pad, perm_host, [&](i64 row) { return part_len(pattern, row, pc); });
     if (pad > 0 && pattern.nnz() > 0) {
         k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp, ci, v, pc,
@@ -268,9 +371,10 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     out.nrows = A.nrows;
     out.ncols = A.ncols;
-    const i64 pad = (A.nrows + kSlice - 1) / kSlice * kSlice;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
-    layout(out, pad, {}, [&](i64 row) { return part_len(A, row, pc); });
+    const std::vector<i32> perm = sigma_order(A.nrows, [&](i64 r) { return part_len(A, r, pc); });
+    const i64 pad = perm.empty() ? (A.nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
+    layout(out, pad, perm, [&](i64 row) { return part_len(A, row, pc); });
     if (A.nnz() == 0 || pad == 0) return;
     DBuf<i64> rp;
     DBuf<i32> ci;
@@ -278,8 +382,8 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     rp.upload(A.rp.data(), A.nrows + 1, s);
     ci.upload(A.ci.data(), A.nnz(), s);
     v.upload(A.v.data(), A.nnz(), s);
-    k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, nullptr, rp.p, ci.p, v.p, pc, out.slice_ptr.p,
-                                                 out.cols.p, out.vals.p);
+    k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp.p, ci.p, v.p, pc,
+                                                 out.slice_ptr.p, out.cols.p, out.vals.p);
     ILUG_LAUNCH_CHECK();
     ILUG_CUDA(cudaStreamSynchronize(s)); // temporaries die at scope exit
 }

@@ -1,0 +1,65 @@
+"""GPU parity of K9, the ILUT Schur-complement smoother (src/schur.cpp), and
+of run_schur_solve (src/driver.cpp:318-375).
+
+One application is compared with the reference's schur_smooth: the block
+solves, SpMVs and the gather/scatter are bitwise, only the interface step's
+three reductions (beta, h11, h21^2) are summed in a different order, so the
+result agrees to ~1e-13 relative (bitwise when there is no interface, p=1)."""
+import numpy as np
+import pytest
+
+from conftest import bitwise, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+SCHUR = {"smoother.kind": "schur_ilut", "smoother.sweeps": "1", "schur.ilut.droptol": "1e-3",
+         "schur.ilut.lfill": "5", "schur.trisolve.mL": "10", "schur.trisolve.mU": "10"}
+
+
+@pytest.mark.parametrize("spec", ["poisson2d(24,24)", "poisson3d(12,12,12)", "pressure27(10,10,10)"])
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+@pytest.mark.parametrize("extra", [{}, {"schur.scaling": "row_col"}, {"trisolve.mode": "direct"}],
+                         ids=["row", "rowcol", "direct"])
+def test_schur_smooth_matches_reference(ilug, ref, torch_cuda, spec, p, extra):
+    kv = dict(SCHUR, **{"schur.blocks": str(p)}, **extra)
+    A = ilug.Matrix.generate(spec)
+    S = ilug.Smoother(A, ilug.Config().update(kv))
+    Ar = ref.mat(*A.csr())
+    Sr = ref.smoother(Ar, ref.cfg(kv))
+    rng = np.random.default_rng(40 + p)
+    b, x0 = rng.uniform(-1, 1, A.rows), rng.uniform(-1, 1, A.rows)
+    xd = _dev(torch_cuda, x0)
+    S.smooth(_dev(torch_cuda, b), xd)
+    torch_cuda.cuda.synchronize()
+    want, _ = ref.smooth(Ar, Sr, b, x0)
+    got = xd.cpu().numpy()
+    if p == 1:
+        assert bitwise(got, want)
+    else:
+        assert rel_err(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("kv", [{}, {"amg.coarsening": "pmis"}])
+def test_acceptance_c6_schur_iterations(ilug, ref, torch_cuda, kv):
+    """tests/acceptance.cpp:380-410: poisson2d(24,24), p = 1, 2, 4, 8 under FGMRES:
+    every count within +-1 of the reference's and the spread <= 3."""
+    base = dict(kv, **{"krylov.tol": "1e-8", "smoother.sweeps": "2", "schur.blocks_list": "1,2,4,8"})
+    rep = ilug.run_schur_solve(ilug.Matrix.generate("poisson2d(24,24)"), ilug.Config().update(base))
+    rows = rep.table_rows("schur")
+    assert [r["p"] for r in rows] == ["1", "2", "4", "8"]
+    its = []
+    A = ilug.Matrix.generate("poisson2d(24,24)").csr()
+    for r in rows:
+        assert r["converged"] == "true"
+        want = ref.run_solve(A, dict(base, **{"smoother.kind": "schur_ilut", "schur.blocks": r["p"],
+                                              "krylov.method": "fgmres"}))
+        assert abs(int(r["iterations"]) - int(want["iterations"])) <= 1
+        its.append(int(r["iterations"]))
+    assert max(its) - min(its) <= 3
+    assert int(rep["iterations_spread"]) == max(its) - min(its)
+    assert rows[0]["interface_size"] == "0" and int(rows[-1]["interface_size"]) > 0
