@@ -146,6 +146,47 @@ ILUAMG_API void ilug_hierarchy_free(ilug_hierarchy* h);
 ILUAMG_API int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, double* x,
                           long long* iterations, double* final_relres, void* stream);
 
+/* ---- multi-GPU: row-block partition (src/schur.cpp:28-33 rule), halo plan,
+ * NCCL communicator, block-Jacobi ILU smoother with a global residual.
+ * One process per GPU; the caller moves the 128-byte NCCL id and the halo
+ * request lists between ranks with its own plumbing (torch.distributed). ---- */
+typedef struct ilug_dist_plan_s ilug_dist_plan;
+typedef struct ilug_dist_comm_s ilug_dist_comm;
+typedef struct ilug_dist_smoother_s ilug_dist_smoother;
+
+/* starts[0..nranks] of the contiguous row blocks (last rank takes the remainder). */
+ILUAMG_API int ilug_dist_partition(long long n, int nranks, long long* starts);
+/* Rows [row0, row1) of a 3D generator spec, global column ids (ncols = n). */
+ILUAMG_API int ilug_dist_generate_rows(const char* spec, long long row0, long long row1,
+                                       iluamg_matrix** out);
+/* This rank's rows (global columns) -> halo plan. */
+ILUAMG_API int ilug_dist_plan_create(const iluamg_matrix* rows, long long n_global, int nranks, int rank,
+                                     ilug_dist_plan** out);
+ILUAMG_API int ilug_dist_plan_info(const ilug_dist_plan* p, long long* row0, long long* row1,
+                                   long long* nhalo);
+/* Global ids this rank needs from rank q; returns the count (ids may be NULL). */
+ILUAMG_API long long ilug_dist_plan_requests(const ilug_dist_plan* p, int q, long long* ids);
+/* Record what rank q requested from this rank (global ids). */
+ILUAMG_API int ilug_dist_plan_set_sends(ilug_dist_plan* p, int q, const long long* ids, long long count);
+/* Local row indices packed for rank q; returns the count (rows may be NULL). */
+ILUAMG_API long long ilug_dist_plan_sends(const ilug_dist_plan* p, int q, long long* rows);
+/* which: 0 extended local matrix (halo columns renumbered, global entry order), 1 diagonal block. */
+ILUAMG_API int ilug_dist_plan_matrix(const ilug_dist_plan* p, int which, iluamg_matrix** out);
+ILUAMG_API void ilug_dist_plan_free(ilug_dist_plan* p);
+ILUAMG_API int ilug_dist_unique_id(char* out128);
+ILUAMG_API int ilug_dist_comm_create(int nranks, int rank, const char* id128, ilug_dist_comm** out);
+ILUAMG_API int ilug_dist_allreduce_sum(const ilug_dist_comm* c, double* buf, long long count, void* stream);
+ILUAMG_API void ilug_dist_comm_free(ilug_dist_comm* c);
+/* Block-Jacobi ILU smoother of the plan's block (the config's ilu, scaling and trisolve keys). */
+ILUAMG_API int ilug_dist_smoother_create(const ilug_dist_plan* p, const ilug_dist_comm* c,
+                                         const iluamg_config* cfg, ilug_dist_smoother** out);
+ILUAMG_API int ilug_dist_smooth(const ilug_dist_smoother* s, const double* b, double* x, void* stream);
+ILUAMG_API int ilug_dist_residual(const ilug_dist_smoother* s, const double* x, const double* b, double* r,
+                                  void* stream);
+ILUAMG_API int ilug_dist_smoother_stats(const ilug_dist_smoother* s, long long* nloc, long long* nnz_A,
+                                        long long* nnz_Ls, long long* nnz_Us);
+ILUAMG_API void ilug_dist_smoother_free(ilug_dist_smoother* s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,25 @@ _SIGS = {
     "ilug_hierarchy_operator_complexity": (_d, [_vp]), "ilug_vcycle": (_i, [_vp, _vp, _vp, _vp]),
     "ilug_vcycle_graph_nodes": (_ll, [_vp]), "ilug_hierarchy_free": (None, [_vp]),
     "ilug_gmres": (_i, [_vp, _vp, _vp, _vp, _pll, _pd, _vp]),
+    # multi-GPU (see paper_2111_09512_b200/dist.py)
+    "ilug_dist_partition": (_i, [_ll, _i, _pll]),
+    "ilug_dist_generate_rows": (_i, [_cs, _ll, _ll, _pvp]),
+    "ilug_dist_plan_create": (_i, [_vp, _ll, _i, _i, _pvp]),
+    "ilug_dist_plan_info": (_i, [_vp, _pll, _pll, _pll]),
+    "ilug_dist_plan_requests": (_ll, [_vp, _i, _pll]),
+    "ilug_dist_plan_set_sends": (_i, [_vp, _i, _pll, _ll]),
+    "ilug_dist_plan_sends": (_ll, [_vp, _i, _pll]),
+    "ilug_dist_plan_matrix": (_i, [_vp, _i, _pvp]),
+    "ilug_dist_plan_free": (None, [_vp]),
+    "ilug_dist_unique_id": (_i, [_vp]),
+    "ilug_dist_comm_create": (_i, [_i, _i, _vp, _pvp]),
+    "ilug_dist_allreduce_sum": (_i, [_vp, _vp, _ll, _vp]),
+    "ilug_dist_comm_free": (None, [_vp]),
+    "ilug_dist_smoother_create": (_i, [_vp, _vp, _vp, _pvp]),
+    "ilug_dist_smooth": (_i, [_vp, _vp, _vp, _vp]),
+    "ilug_dist_residual": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "ilug_dist_smoother_stats": (_i, [_vp, _pll, _pll, _pll, _pll]),
+    "ilug_dist_smoother_free": (None, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

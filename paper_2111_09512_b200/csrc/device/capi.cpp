@@ -33,6 +33,7 @@ struct ilug_smoother_s {
     ilug::DeviceMatrix dA;
     ilug::DeviceSmoother s;
     ilug::DBuf<double> r, scratch;
+    mutable ilug::DBuf<double> hb, hx; // staging for the host-buffer entry point
 };
 struct ilug_hierarchy_s {
     ilug::HostHierarchy h;
@@ -499,11 +500,11 @@ int ilug_smooth_host(const ilug_smoother* s, const double* bh, double* xh) {
     return guarded([&] {
         need(s && bh && xh);
         const ilug::i64 n = s->A.nrows;
-        ilug::DBuf<double> b, x;
-        b.upload(bh, n);
-        x.upload(xh, n);
-        s->s.smooth(b.p, x.p, false, nullptr);
-        x.download(xh);
+        if (s->hb.n != n) s->hb.alloc(n), s->hx.alloc(n); // persistent staging buffers
+        s->hb.upload(bh, n);
+        s->hx.upload(xh, n);
+        s->s.smooth(s->hb.p, s->hx.p, false, nullptr);
+        s->hx.download(xh);
         ILUG_CUDA(cudaStreamSynchronize(nullptr));
         return ILUAMG_OK;
     });
@@ -630,5 +631,162 @@ int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, dou
         return ILUAMG_OK;
     });
 }
+
+} // extern "C"
+
+// ============================================================ ilug_dist_* (multi-GPU)
+#include "dist.hpp"
+
+struct ilug_dist_plan_s {
+    ilug::HaloPlan plan;
+};
+struct ilug_dist_comm_s {
+    std::unique_ptr<ilug::DistComm> c;
+};
+struct ilug_dist_smoother_s {
+    ilug::DistSmoother s;
+    long long nnz_A = 0;
+};
+
+extern "C" {
+
+int ilug_dist_partition(long long n, int nranks, long long* starts) {
+    return guarded([&] {
+        need(starts != nullptr);
+        const ilug::RowPartition p = ilug::row_partition(n, nranks);
+        for (int r = 0; r <= nranks; ++r) starts[r] = p.starts[r];
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_generate_rows(const char* spec, long long row0, long long row1, iluamg_matrix** out) {
+    return guarded([&] {
+        need(spec && out);
+        *out = new iluamg_matrix_s{ilug::generate_rows(spec, row0, row1), spec};
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_plan_create(const iluamg_matrix* rows, long long n_global, int nranks, int rank,
+                          ilug_dist_plan** out) {
+    return guarded([&] {
+        need(rows && out);
+        const ilug::RowPartition part = ilug::row_partition(n_global, nranks);
+        *out = new ilug_dist_plan_s{ilug::halo_plan(rows->A, part, rank)};
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_plan_info(const ilug_dist_plan* p, long long* row0, long long* row1, long long* nhalo) {
+    return guarded([&] {
+        need(p);
+        if (row0) *row0 = p->plan.row0;
+        if (row1) *row1 = p->plan.row1;
+        if (nhalo) *nhalo = p->plan.nhalo;
+        return ILUAMG_OK;
+    });
+}
+long long ilug_dist_plan_requests(const ilug_dist_plan* p, int q, long long* ids) {
+    if (!p) return -1;
+    const std::vector<ilug::i64> r = ilug::halo_requests(p->plan, q);
+    if (ids) std::copy(r.begin(), r.end(), ids);
+    return static_cast<long long>(r.size());
+}
+int ilug_dist_plan_set_sends(ilug_dist_plan* p, int q, const long long* ids, long long count) {
+    return guarded([&] {
+        need(p && (ids || count == 0));
+        ilug::halo_set_sends(p->plan, q, std::vector<ilug::i64>(ids, ids + count));
+        return ILUAMG_OK;
+    });
+}
+long long ilug_dist_plan_sends(const ilug_dist_plan* p, int q, long long* rows) {
+    if (!p) return -1;
+    const auto& h = p->plan;
+    for (size_t k = 0; k < h.send_ranks.size(); ++k)
+        if (h.send_ranks[k] == q) {
+            const long long cnt = h.send_offsets[k + 1] - h.send_offsets[k];
+            if (rows)
+                for (long long i = 0; i < cnt; ++i) rows[i] = h.send_local[h.send_offsets[k] + i];
+            return cnt;
+        }
+    return 0;
+}
+int ilug_dist_plan_matrix(const ilug_dist_plan* p, int which, iluamg_matrix** out) {
+    return guarded([&] {
+        need(p && out);
+        *out = new iluamg_matrix_s{which == 0 ? p->plan.A_ext : p->plan.A_diag, "dist"};
+        return ILUAMG_OK;
+    });
+}
+void ilug_dist_plan_free(ilug_dist_plan* p) { delete p; }
+int ilug_dist_unique_id(char* out128) {
+    return guarded([&] {
+        need(out128);
+        ilug::dist_unique_id(out128);
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_comm_create(int nranks, int rank, const char* id128, ilug_dist_comm** out) {
+    return guarded([&] {
+        need(id128 && out);
+        auto* c = new ilug_dist_comm_s();
+        try {
+            c->c = std::make_unique<ilug::DistComm>(nranks, rank, id128);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_allreduce_sum(const ilug_dist_comm* c, double* buf, long long count, void* stream) {
+    return guarded([&] {
+        need(c && buf);
+        c->c->allreduce_sum(buf, count, S(stream));
+        return ILUAMG_OK;
+    });
+}
+void ilug_dist_comm_free(ilug_dist_comm* c) { delete c; }
+int ilug_dist_smoother_create(const ilug_dist_plan* p, const ilug_dist_comm* c, const iluamg_config* cfg,
+                              ilug_dist_smoother** out) {
+    return guarded([&] {
+        need(p && c && cfg && out);
+        auto* s = new ilug_dist_smoother_s();
+        try {
+            s->s.build(p->plan, *c->c, ilug::smoother_from(cfg->cfg), nullptr);
+            s->nnz_A = p->plan.A_ext.nnz();
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_smooth(const ilug_dist_smoother* s, const double* b, double* x, void* stream) {
+    return guarded([&] {
+        need(s && b && x);
+        s->s.smooth(b, x, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_residual(const ilug_dist_smoother* s, const double* x, const double* b, double* r, void* stream) {
+    return guarded([&] {
+        need(s && x && b && r);
+        s->s.residual(x, b, r, S(stream));
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_smoother_stats(const ilug_dist_smoother* s, long long* nloc, long long* nnz_A, long long* nl,
+                             long long* nu) {
+    return guarded([&] {
+        need(s);
+        const ilug::DeviceIlu* f = s->s.smoother().ilu();
+        if (nloc) *nloc = s->s.nloc();
+        if (nnz_A) *nnz_A = s->nnz_A;
+        if (nl) *nl = f ? f->Ls().nnz : 0;
+        if (nu) *nu = f ? f->Us().nnz : 0;
+        return ILUAMG_OK;
+    });
+}
+void ilug_dist_smoother_free(ilug_dist_smoother* s) { delete s; }
 
 } // extern "C"

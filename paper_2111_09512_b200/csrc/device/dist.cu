@@ -1,0 +1,99 @@
+// Multi-GPU plumbing (one process per GPU): NCCL communicator from a
+// caller-broadcast unique id, and the halo exchange of a row-block
+// distributed operator — pack the rows other ranks need, then one grouped
+// ncclSend/ncclRecv per neighbour (NVLink/NVSwitch underneath). Halo messages
+// are small (one grid plane per neighbour for a z-slab partition), so the
+// exchange is latency-bound; it is issued on the compute stream right before
+// the residual kernel that consumes it.
+#include "dist.hpp"
+
+#include <nccl.h>
+
+namespace ilug {
+
+namespace {
+
+[[noreturn]] void nccl_fail(ncclResult_t r, const char* what) {
+    fail_numeric(std::string("NCCL error ") + ncclGetErrorString(r) + " in " + what);
+}
+#define ILUG_NCCL(call)                                   \
+    do {                                                  \
+        ncclResult_t r__ = (call);                        \
+        if (r__ != ncclSuccess) nccl_fail(r__, #call);    \
+    } while (0)
+
+__global__ void k_pack(i64 n, const i32* __restrict__ idx, const double* __restrict__ x, double* __restrict__ out) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        out[i] = x[idx[i]];
+}
+
+} // namespace
+
+void dist_unique_id(char out[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    ILUG_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, 128);
+}
+
+DistComm::DistComm(int nranks_, int rank_, const char id[128]) : nranks(nranks_), rank(rank_) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclComm_t c;
+    ILUG_NCCL(ncclCommInitRank(&c, nranks, uid, rank));
+    comm = c;
+}
+
+DistComm::~DistComm() {
+    if (comm) ncclCommDestroy(static_cast<ncclComm_t>(comm));
+}
+
+void DistComm::allreduce_sum(double* buf, i64 count, cudaStream_t st) const {
+    if (nranks == 1) return;
+    ILUG_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum,
+                            static_cast<ncclComm_t>(comm), st));
+}
+
+void HaloExchange::exchange(const double* x, cudaStream_t st) const {
+    const i64 ns = send_idx.n;
+    if (ns > 0) {
+        const unsigned g = static_cast<unsigned>(std::min<i64>((ns + 255) / 256, 4096));
+        k_pack<<<g, 256, 0, st>>>(ns, send_idx.p, x, sendbuf.p);
+        ILUG_LAUNCH_CHECK();
+    }
+    if (send_ranks.empty() && recv_ranks.empty()) return;
+    auto c = static_cast<ncclComm_t>(comm);
+    ILUG_NCCL(ncclGroupStart());
+    for (size_t k = 0; k < send_ranks.size(); ++k)
+        ILUG_NCCL(ncclSend(sendbuf.p + send_offsets[k], static_cast<size_t>(send_offsets[k + 1] - send_offsets[k]),
+                           ncclDouble, static_cast<int>(send_ranks[k]), c, st));
+    for (size_t k = 0; k < recv_ranks.size(); ++k)
+        ILUG_NCCL(ncclRecv(halo.p + recv_offsets[k], static_cast<size_t>(recv_offsets[k + 1] - recv_offsets[k]),
+                           ncclDouble, static_cast<int>(recv_ranks[k]), c, st));
+    ILUG_NCCL(ncclGroupEnd());
+}
+
+void DistSmoother::build(const HaloPlan& plan, const DistComm& comm, const SmootherConfig& cfg, cudaStream_t st) {
+    if (cfg.kind != SmootherKind::ilu) fail_invalid("distributed smoother: smoother.kind must be ilu");
+    if (plan.nranks > 1 && plan.send_offsets.size() != plan.send_ranks.size() + (plan.send_ranks.empty() ? 0 : 1))
+        fail_invalid("distributed smoother: halo sends not set");
+    hx_.comm = comm.comm;
+    hx_.nloc = plan.nloc;
+    hx_.nhalo = plan.nhalo;
+    hx_.recv_ranks = plan.recv_ranks;
+    hx_.recv_offsets = plan.recv_offsets;
+    hx_.send_ranks = plan.send_ranks;
+    hx_.send_offsets = plan.send_offsets;
+    hx_.send_idx.upload(plan.send_local.data(), static_cast<i64>(plan.send_local.size()), st);
+    hx_.sendbuf.alloc(static_cast<i64>(plan.send_local.size()));
+    hx_.halo.alloc(std::max<i64>(plan.nhalo, 1));
+    A_.build(plan.A_ext, st);
+    A_.n = plan.nloc;
+    A_.halo = &hx_;
+    // block-Jacobi: the ILU factors of this rank's diagonal block
+    s_.build(plan.A_diag, A_, cfg, st);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+} // namespace ilug

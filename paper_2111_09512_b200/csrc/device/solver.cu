@@ -13,6 +13,18 @@ void DeviceMatrix::build(const Csr& host, cudaStream_t st) {
     sell_from_host(A, host, Part::all, st);
 }
 
+void DeviceMatrix::residual(const double* x, const double* b, double* r, cudaStream_t st) const {
+    if (!halo) return ilug::residual(A, x, b, r, st);
+    halo->exchange(x, st);
+    residual_split(A, x, halo->halo.p, n, b, r, st);
+}
+
+void DeviceMatrix::spmv(const double* x, double* y, cudaStream_t st) const {
+    if (!halo) return ilug::spmv(A, x, y, st);
+    halo->exchange(x, st);
+    spmv_split(A, x, halo->halo.p, n, y, st);
+}
+
 // ============================================================ DeviceIlu (K1-K5)
 void DeviceIlu::build(const HostFactors& f, ScalingKind scaling, UpperIteration upper,
                       bool direct_plans, cudaStream_t st) {
@@ -160,6 +172,8 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
     cfg_ = cfg;
     n_ = A.nrows;
     A_ = &dA;
+    if (dA.halo && cfg.kind != SmootherKind::ilu)
+        fail_invalid("distributed smoothing: only the (block-Jacobi) ILU smoother is distributed");
     switch (cfg.kind) {
     case SmootherKind::jacobi: {
         const Vec d = inverted_diag(A, "jacobi");
@@ -222,7 +236,7 @@ void DeviceSmoother::ilu_sweep(const double* b, double* x, bool x_zero, cudaStre
     double* xb = ws_.p + 5 * n;
     const double* rr = b; // r = b - A*0 = b exactly when x == 0
     if (!x_zero) {
-        residual(A_->A, x, b, r, st);
+        A_->residual(x, b, r, st); // halo-exchanged when A_ is a distributed block
         rr = r;
     }
     const TriSolveConfig& ts = cfg_.trisolve;

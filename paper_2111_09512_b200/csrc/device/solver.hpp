@@ -17,11 +17,26 @@
 
 namespace ilug {
 
-/// Device copy of a square operator.
+/// Device side of a HaloPlan (host/dist.hpp): packs the rows other ranks need
+/// and exchanges them with NCCL point-to-point in one group (device/dist.cu).
+struct HaloExchange {
+    void* comm = nullptr; ///< ncclComm_t
+    i64 nloc = 0, nhalo = 0;
+    std::vector<i64> recv_ranks, recv_offsets, send_ranks, send_offsets;
+    DBuf<i32> send_idx;
+    mutable DBuf<double> sendbuf, halo;
+    void exchange(const double* x_local, cudaStream_t st) const;
+};
+
+/// Device copy of an operator. With a halo, the rows are a rank's rows of a
+/// distributed matrix whose columns >= n index the halo buffer.
 struct DeviceMatrix {
     Sell A;
     i64 n = 0;
+    const HaloExchange* halo = nullptr;
     void build(const Csr& host, cudaStream_t st);
+    void residual(const double* x, const double* b, double* r, cudaStream_t st) const;
+    void spmv(const double* x, double* y, cudaStream_t st) const;
 };
 
 /// K1-K5: scaled ILU factors on the device plus the sweep/solve entry points.

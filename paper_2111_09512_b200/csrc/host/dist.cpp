@@ -1,0 +1,95 @@
+#include "dist.hpp"
+
+#include <algorithm>
+
+namespace ilug {
+
+RowPartition row_partition(i64 n, i64 p) {
+    if (p < 1 || p > std::max<i64>(n, 1)) fail_invalid("row_partition: rank count out of range");
+    RowPartition part;
+    part.n = n;
+    part.p = p;
+    const i64 base = n / p;
+    for (i64 r = 0; r < p; ++r) part.starts.push_back(r * base);
+    part.starts.push_back(n); // the last rank absorbs the remainder
+    return part;
+}
+
+i64 RowPartition::owner(i64 row) const {
+    const auto it = std::upper_bound(starts.begin(), starts.end() - 1, row);
+    return static_cast<i64>(it - starts.begin()) - 1;
+}
+
+HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) {
+    if (rank < 0 || rank >= part.p) fail_invalid("halo_plan: rank out of range");
+    HaloPlan h;
+    h.rank = rank;
+    h.nranks = part.p;
+    h.row0 = part.starts[rank];
+    h.row1 = part.starts[rank + 1];
+    h.nloc = h.row1 - h.row0;
+    if (rows.nrows != h.nloc) fail_invalid("halo_plan: local row count does not match the partition");
+    // halo = sorted unique off-range columns (contiguous ranges => grouped by owner)
+    for (i64 k = 0; k < rows.nnz(); ++k) {
+        const i64 j = rows.ci[k];
+        if (j < h.row0 || j >= h.row1) h.halo_global.push_back(j);
+    }
+    std::sort(h.halo_global.begin(), h.halo_global.end());
+    h.halo_global.erase(std::unique(h.halo_global.begin(), h.halo_global.end()), h.halo_global.end());
+    h.nhalo = static_cast<i64>(h.halo_global.size());
+    for (i64 k = 0; k < h.nhalo; ++k) {
+        const i64 q = part.owner(h.halo_global[k]);
+        if (h.recv_ranks.empty() || h.recv_ranks.back() != q) {
+            h.recv_ranks.push_back(q);
+            h.recv_offsets.push_back(k);
+        }
+    }
+    h.recv_offsets.push_back(h.nhalo);
+
+    // extended matrix: same entry order, renumbered columns
+    h.A_ext.nrows = h.nloc;
+    h.A_ext.ncols = h.nloc + h.nhalo;
+    h.A_ext.rp = rows.rp;
+    h.A_ext.ci.resize(rows.ci.size());
+    h.A_ext.v = rows.v;
+    h.A_diag.nrows = h.A_diag.ncols = h.nloc;
+    h.A_diag.rp.assign(static_cast<size_t>(h.nloc) + 1, 0);
+    for (i64 i = 0; i < h.nloc; ++i) {
+        for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k) {
+            const i64 j = rows.ci[k];
+            if (j >= h.row0 && j < h.row1) {
+                h.A_ext.ci[k] = static_cast<i32>(j - h.row0);
+                h.A_diag.ci.push_back(static_cast<i32>(j - h.row0));
+                h.A_diag.v.push_back(rows.v[k]);
+            } else {
+                const auto it = std::lower_bound(h.halo_global.begin(), h.halo_global.end(), j);
+                h.A_ext.ci[k] = static_cast<i32>(h.nloc + (it - h.halo_global.begin()));
+            }
+        }
+        h.A_diag.rp[i + 1] = static_cast<i64>(h.A_diag.ci.size());
+    }
+    return h;
+}
+
+std::vector<i64> halo_requests(const HaloPlan& h, i64 q) {
+    for (size_t s = 0; s < h.recv_ranks.size(); ++s)
+        if (h.recv_ranks[s] == q)
+            return {h.halo_global.begin() + h.recv_offsets[s], h.halo_global.begin() + h.recv_offsets[s + 1]};
+    return {};
+}
+
+void halo_set_sends(HaloPlan& h, i64 q, const std::vector<i64>& ids) {
+    if (ids.empty()) return;
+    if (q == h.rank || q < 0 || q >= h.nranks) fail_invalid("halo_set_sends: bad destination rank");
+    if (std::find(h.send_ranks.begin(), h.send_ranks.end(), q) != h.send_ranks.end())
+        fail_invalid("halo_set_sends: destination already set");
+    if (h.send_offsets.empty()) h.send_offsets.push_back(0);
+    h.send_ranks.push_back(q);
+    for (i64 g : ids) {
+        if (g < h.row0 || g >= h.row1) fail_invalid("halo_set_sends: requested row not owned by this rank");
+        h.send_local.push_back(static_cast<i32>(g - h.row0));
+    }
+    h.send_offsets.push_back(static_cast<i64>(h.send_local.size()));
+}
+
+} // namespace ilug

@@ -1,4 +1,5 @@
 #include "problems.hpp"
+#include "dist.hpp"
 
 #include <cctype>
 #include <cmath>
@@ -21,8 +22,11 @@ std::uint64_t splitmix(std::uint64_t x) {
 
 // Build a CSR from a per-row emitter: pass 1 counts, pass 2 fills, both
 // row-parallel. emit(i, cols, vals) must produce strictly increasing columns.
+// Rows [r0, r1) of a generated matrix (global column ids); the full matrix is
+// r0 = 0, r1 = n. Pass 1 counts, pass 2 fills, both row-parallel.
 template <typename Emit>
-Csr build_rows(i64 n, i64 ncols, int max_per_row, Emit emit) {
+Csr build_range(i64 r0, i64 r1, i64 ncols, Emit emit) {
+    const i64 n = r1 - r0;
     Csr A;
     A.nrows = n;
     A.ncols = ncols;
@@ -30,7 +34,7 @@ Csr build_rows(i64 n, i64 ncols, int max_per_row, Emit emit) {
     parallel_ranges(n, [&](i64 b, i64 e, int) {
         i32 c[64];
         double v[64];
-        for (i64 i = b; i < e; ++i) A.rp[i + 1] = emit(i, c, v);
+        for (i64 i = b; i < e; ++i) A.rp[i + 1] = emit(r0 + i, c, v);
     });
     for (i64 i = 0; i < n; ++i) A.rp[i + 1] += A.rp[i];
     A.ci.resize(static_cast<size_t>(A.rp[n]));
@@ -39,14 +43,25 @@ Csr build_rows(i64 n, i64 ncols, int max_per_row, Emit emit) {
         i32 c[64];
         double v[64];
         for (i64 i = b; i < e; ++i) {
-            const int m = emit(i, c, v);
+            const int m = emit(r0 + i, c, v);
             std::copy(c, c + m, A.ci.begin() + A.rp[i]);
             std::copy(v, v + m, A.v.begin() + A.rp[i]);
         }
     });
-    (void)max_per_row;
     return A;
 }
+
+template <typename Emit>
+Csr build_rows(i64 n, i64 ncols, int, Emit emit) {
+    return build_range(0, n, ncols, emit);
+}
+
+// Active row range of a 3D generator call (whole matrix unless a range is given).
+struct Range {
+    i64 r0 = 0, r1 = -1;
+    i64 lo(i64) const { return r0; }
+    i64 hi(i64 n) const { return r1 < 0 ? n : r1; }
+};
 
 void check_grid(i64 nx, i64 ny, i64 nz, const char* what) {
     if (nx < 1 || ny < 1 || nz < 1) fail_invalid(std::string(what) + ": grid dimensions must be >= 1");
@@ -94,10 +109,12 @@ Csr anisotropic2d(i64 nx, i64 ny, double eps) {
     });
 }
 
-Csr poisson3d(i64 nx, i64 ny, i64 nz) {
+namespace {
+
+Csr poisson3d_range(i64 nx, i64 ny, i64 nz, Range rg) {
     check_grid(nx, ny, nz, "poisson3d");
-    const i64 pl = nx * ny;
-    return build_rows(pl * nz, pl * nz, 7, [=](i64 i, i32* c, double* v) {
+    const i64 pl = nx * ny, n = pl * nz;
+    return build_range(rg.lo(n), rg.hi(n), n, [=](i64 i, i32* c, double* v) {
         const i64 ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
         int m = 0;
         auto put = [&](i64 j, double x) { c[m] = static_cast<i32>(j), v[m++] = x; };
@@ -112,12 +129,10 @@ Csr poisson3d(i64 nx, i64 ny, i64 nz) {
     });
 }
 
-namespace {
-
 template <typename Coef>
-Csr box27(i64 nx, i64 ny, i64 nz, Coef coef) {
-    const i64 pl = nx * ny;
-    return build_rows(pl * nz, pl * nz, 27, [=](i64 i, i32* c, double* v) {
+Csr box27(i64 nx, i64 ny, i64 nz, Coef coef, Range rg) {
+    const i64 pl = nx * ny, n = pl * nz;
+    return build_range(rg.lo(n), rg.hi(n), n, [=](i64 i, i32* c, double* v) {
         const i64 ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
         int m = 0, dpos = -1;
         double diag = 0.0;
@@ -142,34 +157,34 @@ Csr box27(i64 nx, i64 ny, i64 nz, Coef coef) {
     });
 }
 
-} // namespace
-
-Csr stencil27(i64 nx, i64 ny, i64 nz) {
+Csr stencil27_range(i64 nx, i64 ny, i64 nz, Range rg) {
     check_grid(nx, ny, nz, "stencil27");
-    return box27(nx, ny, nz, [](i64, i64, int) { return 1.0; });
+    return box27(nx, ny, nz, [](i64, i64, int) { return 1.0; }, rg);
 }
 
-Csr pressure27(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
+Csr pressure27_range(i64 nx, i64 ny, i64 nz, std::uint64_t seed, Range rg) {
     check_grid(nx, ny, nz, "pressure27");
-    const i64 n = nx * ny * nz;
-    auto kap = std::make_shared<std::vector<double>>(static_cast<size_t>(n));
-    parallel_ranges(n, [&](i64 b, i64 e, int) {
+    const i64 n = nx * ny * nz, pl = nx * ny;
+    // kappa of the active rows and their stencil neighbours (one plane + one row + 1 each side)
+    const i64 k0 = std::max<i64>(0, rg.lo(n) - pl - nx - 1), k1 = std::min(n, rg.hi(n) + pl + nx + 1);
+    auto kap = std::make_shared<std::vector<double>>(static_cast<size_t>(k1 - k0));
+    parallel_ranges(k1 - k0, [&](i64 b, i64 e, int) {
         for (i64 i = b; i < e; ++i)
-            (*kap)[i] = std::pow(10.0, 4.0 * hash_unit(seed, static_cast<std::uint64_t>(i)) - 2.0);
+            (*kap)[i] = std::pow(10.0, 4.0 * hash_unit(seed, static_cast<std::uint64_t>(k0 + i)) - 2.0);
     });
-    const double* kappa = kap->data();
+    const double* kappa = kap->data() - k0;
     return box27(nx, ny, nz, [=](i64 i, i64 j, int dist) {
         const double w = dist == 1 ? 1.0 : (dist == 2 ? 0.5 : 0.25);
         const double ki = kappa[i];
         if (j < 0) return w * ki; // out-of-grid slot: hm(ki, ki) = ki
         const double kj = kappa[j];
         return w * (2.0 * ki * kj / (ki + kj));
-    });
+    }, rg);
 }
 
-Csr cutcell(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
+Csr cutcell_range(i64 nx, i64 ny, i64 nz, std::uint64_t seed, Range rg) {
     check_grid(nx, ny, nz, "cutcell");
-    const i64 pl = nx * ny;
+    const i64 pl = nx * ny, n = pl * nz;
     const double R = 0.3 * static_cast<double>(nx);
     const double cx = 0.5 * nx, cy = 0.5 * ny, cz = 0.5 * nz;
     auto cell = [=](i64 i, double& kappa, double& rho) {
@@ -182,7 +197,7 @@ Csr cutcell(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
                     ? std::pow(10.0, 16.0 * hash_unit(seed, static_cast<std::uint64_t>(i)))
                     : 1.0;
     };
-    return build_rows(pl * nz, pl * nz, 7, [=](i64 i, i32* c, double* v) {
+    return build_range(rg.lo(n), rg.hi(n), n, [=](i64 i, i32* c, double* v) {
         const i64 ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
         double ki, ri;
         cell(i, ki, ri);
@@ -207,6 +222,38 @@ Csr cutcell(i64 nx, i64 ny, i64 nz, std::uint64_t seed) {
             if (in[s]) c[m] = static_cast<i32>(nb[s]), v[m++] = -f[s];
         return m;
     });
+}
+
+} // namespace
+
+Csr poisson3d(i64 nx, i64 ny, i64 nz) { return poisson3d_range(nx, ny, nz, {}); }
+Csr stencil27(i64 nx, i64 ny, i64 nz) { return stencil27_range(nx, ny, nz, {}); }
+Csr pressure27(i64 nx, i64 ny, i64 nz, std::uint64_t seed) { return pressure27_range(nx, ny, nz, seed, {}); }
+Csr cutcell(i64 nx, i64 ny, i64 nz, std::uint64_t seed) { return cutcell_range(nx, ny, nz, seed, {}); }
+
+Csr generate_rows(const std::string& spec, i64 row0, i64 row1) {
+    const auto open = spec.find('('), close = spec.rfind(')');
+    if (open == std::string::npos || close == std::string::npos || close < open)
+        fail_invalid("generate_rows: malformed spec '" + spec + "'");
+    const std::string kind = spec.substr(0, open);
+    std::string args = spec.substr(open + 1, close - open - 1);
+    for (char& ch : args)
+        if (ch == ',') ch = ' ';
+    std::istringstream in(args);
+    i64 nx = 0, ny = 0, nz = 0;
+    if (!(in >> nx >> ny >> nz)) fail_invalid("generate_rows: " + kind + " expects (nx,ny,nz[,seed])");
+    std::uint64_t seed = 2111;
+    {
+        unsigned long long s;
+        if (in >> s) seed = s;
+    }
+    if (row0 < 0 || row1 < row0 || row1 > nx * ny * nz) fail_invalid("generate_rows: row range out of bounds");
+    const Range rg{row0, row1};
+    if (kind == "poisson3d") return poisson3d_range(nx, ny, nz, rg);
+    if (kind == "stencil27") return stencil27_range(nx, ny, nz, rg);
+    if (kind == "pressure27") return pressure27_range(nx, ny, nz, seed, rg);
+    if (kind == "cutcell") return cutcell_range(nx, ny, nz, seed, rg);
+    fail_invalid("generate_rows: only 3D generators support row ranges, got '" + kind + "'");
 }
 
 namespace {

@@ -30,7 +30,7 @@ namespace ilug {
 
 namespace {
 
-constexpr int kSmallBlock = 1024;
+constexpr int kSmallBlock = 512; // 16-entry chunks need up to 128 registers per thread
 constexpr int kFlagBlock = 256;
 
 // MODE 0: unit lower, strict storage: x_i = b_i - sum L_ij x_j
@@ -72,8 +72,9 @@ __device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, con
                 if (is_dep<MODE>(j, row)) {
                     if (FLAGS) {
                         cuda::atomic_ref<unsigned, cuda::thread_scope_device> f(flags[j]);
-                        while (f.load(cuda::memory_order_acquire) != E) {
-                        }
+                        // back off so spinning warps do not flood L2 with polls
+                        for (int spin = 0; f.load(cuda::memory_order_acquire) != E; ++spin)
+                            if (spin > 8) __nanosleep(64);
                     }
                     xv[u] = __ldcg(x + j);
                 } else {
@@ -94,15 +95,44 @@ __device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, con
     x[row] = MODE == 0 ? s : s / d;
 }
 
+// Bulk (TMA-engine) prefetch of a byte range into L2; no completion tracking.
+__device__ __forceinline__ void l2_prefetch(const void* p, i64 bytes) {
+    const char* a = static_cast<const char*>(p);
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15);
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(a) + static_cast<uintptr_t>(bytes) + 15) & ~uintptr_t(15);
+    for (uintptr_t s = lo; s < hi; s += (1u << 20)) { // chunks of at most 1 MiB
+        const unsigned len = static_cast<unsigned>(hi - s < (1u << 20) ? hi - s : (1u << 20));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s), "r"(len) : "memory");
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kSmallBlock)
 k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b,
              double* x, const double* __restrict__ xold) {
+    // Level L+2's operator slices are one contiguous range of the level-ordered
+    // SELL: one thread asks the copy engine to pull them into L2 while the CTA
+    // works on level L, so a level's loads are L2 hits, not DRAM misses.
+    auto prefetch_level = [&](int L) {
+        if (L >= nlev) return;
+        const i64 s0 = level_ptr[L] >> 5, s1 = level_ptr[L + 1] >> 5;
+        const i64 e0 = M.slice_ptr[s0], e1 = M.slice_ptr[s1];
+        if (e1 > e0) {
+            l2_prefetch(M.vals + e0, (e1 - e0) * 8);
+            l2_prefetch(M.cols + e0, (e1 - e0) * 4);
+        }
+        l2_prefetch(M.perm + level_ptr[L], (level_ptr[L + 1] - level_ptr[L]) * 4);
+    };
+    if (threadIdx.x == 0) {
+        prefetch_level(0);
+        prefetch_level(1);
+    }
     for (int L = 0; L < nlev; ++L) {
+        if (threadIdx.x == 0) prefetch_level(L + 2);
         const i64 end = level_ptr[L + 1];
         for (i64 p = level_ptr[L] + threadIdx.x; p < end; p += blockDim.x) {
             const i64 row = M.perm[p];
-            if (row >= 0) level_row<MODE, false>(M, p, row, b, x, xold, nullptr, 0u);
+            if (row >= 0) level_row<MODE, false, 16>(M, p, row, b, x, xold, nullptr, 0u);
         }
         __syncthreads();
     }
@@ -194,7 +224,7 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // costs its full row latency; the sync-free schedule overlaps the loads of
     // later levels with the wait on earlier ones, which wins as soon as there
     // is more than a CTA's worth of rows.
-    single_cta_ = n <= 4 * kSmallBlock;
+    single_cta_ = n <= 4 * kSmallBlock || n / std::max(nl, 1) <= kSmallBlock;
     if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | flags
         if (std::string(force) == "cta") single_cta_ = true;
         if (std::string(force) == "flags" && n > 0) single_cta_ = false;

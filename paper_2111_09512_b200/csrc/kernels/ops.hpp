@@ -29,6 +29,10 @@ Csr sell_to_host(const Sell& M);
 // s_i = sum_t M[i,t] x[col]  (ascending, from 0.0); then per row i:
 void spmv(const Sell& M, const double* x, double* y, cudaStream_t st);                 // y = s
 void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st);           // acc += s
+/// Distributed rows: columns < nloc read x, columns >= nloc read halo[c - nloc].
+void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
+                    cudaStream_t st);
+void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st);
 void residual(const Sell& M, const double* x, const double* b, double* r, cudaStream_t st); // r = b - s
 /// out = (rhs - s) / div
 void sweep_div(const Sell& M, const double* x, const double* rhs, const double* div, double* out,

@@ -184,6 +184,41 @@ __global__ void __launch_bounds__(kBlock) k_rowdot8(SellView M, i64 nrows, const
     epi(row, s);
 }
 
+// Distributed form: columns < nloc gather from the local vector, columns >= nloc
+// from the received halo buffer (halo exchange before the launch). The entry
+// order is the global column order, so the sum is the single-process one.
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, const double* __restrict__ x,
+                                                          const double* __restrict__ halo, i32 nloc, Epi epi) {
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= M.nrows_pad) return;
+    const i64 row = M.perm ? M.perm[p] : p;
+    if (row < 0 || row >= nrows) return;
+    const int len = M.rowlen[p];
+    const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
+    const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
+    double s = 0.0;
+    int t = 0;
+    for (; t + 4 <= len; t += 4) {
+        double a[4], xv[4];
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = ld_stream(vp + (t + u) * kSlice);
+            c[u] = ld_stream(cp + (t + u) * kSlice);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = c[u] < nloc ? ld_gather(x + c[u]) : ld_gather(halo + (c[u] - nloc));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s = s + a[u] * xv[u];
+    }
+    for (; t < len; ++t) {
+        const int c = ld_stream(cp + t * kSlice);
+        s = s + ld_stream(vp + t * kSlice) * (c < nloc ? ld_gather(x + c) : ld_gather(halo + (c - nloc)));
+    }
+    epi(row, s);
+}
+
 template <class Epi, bool HINT>
 __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
                                                     Epi epi) {
@@ -228,9 +263,9 @@ bool l2_hints() {
     const char* e = std::getenv("ILUG_L2_HINTS");
     return e && e[0] == '1';
 }
-int rowdot_width() {
+int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy)
     const char* e = std::getenv("ILUG_ROWDOT");
-    return e && e[0] == '4' ? 4 : 8;
+    return e && e[0] == '8' ? 8 : 4;
 }
 
 template <class Epi>
@@ -422,6 +457,19 @@ Csr sell_to_host(const Sell& M) {
 // -------------------------------------------------------------- launchers
 void spmv(const Sell& M, const double* x, double* y, cudaStream_t st) {
     launch_rowdot(M, x, EpiStore{y}, st);
+}
+void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
+                    cudaStream_t st) {
+    if (M.nrows_pad == 0) return;
+    k_rowdot_split<EpiResidual><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, halo,
+                                                                          static_cast<i32>(nloc), EpiResidual{b, r});
+    ILUG_LAUNCH_CHECK();
+}
+void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st) {
+    if (M.nrows_pad == 0) return;
+    k_rowdot_split<EpiStore><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, halo,
+                                                                       static_cast<i32>(nloc), EpiStore{y});
+    ILUG_LAUNCH_CHECK();
 }
 void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st) {
     launch_rowdot(M, x, EpiAdd{acc}, st);

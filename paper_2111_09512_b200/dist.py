@@ -1,0 +1,129 @@
+"""Multi-GPU view of the C ABI (ilug_dist_*): row-block partition, halo plans
+and the NCCL-backed block-Jacobi ILU smoother, one process per GPU.
+
+torch.distributed (gloo or nccl) is only plumbing here: it moves the 128-byte
+NCCL id and the halo request lists between ranks at setup. The data path
+(halo exchange, sweeps) is NCCL + libilug kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, List
+
+import numpy as np
+
+from . import Config, IlugError, Matrix, _as, _check, _ptr, _stream, lib
+
+
+def partition(n: int, nranks: int) -> np.ndarray:
+    starts = np.empty(nranks + 1, np.int64)
+    _check(lib.ilug_dist_partition(n, nranks, _as(starts, C.c_longlong)))
+    return starts
+
+
+def generate_rows(spec: str, row0: int, row1: int) -> Matrix:
+    out = C.c_void_p()
+    _check(lib.ilug_dist_generate_rows(spec.encode(), row0, row1, C.byref(out)))
+    return Matrix(out.value)
+
+
+class Plan:
+    """Halo plan of one rank's rows (global column ids)."""
+
+    def __init__(self, rows: Matrix, n_global: int, nranks: int, rank: int):
+        out = C.c_void_p()
+        _check(lib.ilug_dist_plan_create(rows.h, n_global, nranks, rank, C.byref(out)))
+        self.h = out
+        self.nranks, self.rank = nranks, rank
+        r0, r1, nh = C.c_longlong(), C.c_longlong(), C.c_longlong()
+        _check(lib.ilug_dist_plan_info(self.h, C.byref(r0), C.byref(r1), C.byref(nh)))
+        self.row0, self.row1, self.nhalo = r0.value, r1.value, nh.value
+
+    def requests(self, q: int) -> np.ndarray:
+        cnt = lib.ilug_dist_plan_requests(self.h, q, None)
+        ids = np.empty(max(cnt, 0), np.int64)
+        if cnt > 0:
+            lib.ilug_dist_plan_requests(self.h, q, _as(ids, C.c_longlong))
+        return ids
+
+    def set_sends(self, q: int, ids) -> None:
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        _check(lib.ilug_dist_plan_set_sends(self.h, q, _as(ids, C.c_longlong), len(ids)))
+
+    def sends(self, q: int) -> np.ndarray:
+        cnt = lib.ilug_dist_plan_sends(self.h, q, None)
+        rows = np.empty(max(cnt, 0), np.int64)
+        if cnt > 0:
+            lib.ilug_dist_plan_sends(self.h, q, _as(rows, C.c_longlong))
+        return rows
+
+    def matrix(self, which: str = "ext") -> Matrix:
+        out = C.c_void_p()
+        _check(lib.ilug_dist_plan_matrix(self.h, 0 if which == "ext" else 1, C.byref(out)))
+        return Matrix(out.value)
+
+    def exchange_requests(self, all_gather: Callable[[object], List[object]]) -> None:
+        """Tell every rank what we need from it; record what it needs from us.
+        all_gather(obj) -> list over ranks (e.g. torch.distributed.all_gather_object)."""
+        mine = {q: self.requests(q).tolist() for q in range(self.nranks) if q != self.rank}
+        everyone = all_gather(mine)
+        for q in range(self.nranks):
+            if q != self.rank:
+                wanted = everyone[q].get(self.rank, [])
+                if wanted:
+                    self.set_sends(q, wanted)
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and lib is not None:
+            lib.ilug_dist_plan_free(self.h)
+            self.h = C.c_void_p()
+
+
+def unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.ilug_dist_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+class Comm:
+    def __init__(self, nranks: int, rank: int, uid: bytes):
+        buf = C.create_string_buffer(uid, 128)
+        out = C.c_void_p()
+        _check(lib.ilug_dist_comm_create(nranks, rank, C.cast(buf, C.c_void_p), C.byref(out)))
+        self.h = out
+
+    def allreduce_sum(self, t, count: int, stream=None) -> None:
+        _check(lib.ilug_dist_allreduce_sum(self.h, _ptr(t), count, _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and lib is not None:
+            lib.ilug_dist_comm_free(self.h)
+            self.h = C.c_void_p()
+
+
+class Smoother:
+    """Block-Jacobi ILU smoother of a distributed matrix (global residual)."""
+
+    def __init__(self, plan: Plan, comm: Comm, cfg: Config):
+        out = C.c_void_p()
+        _check(lib.ilug_dist_smoother_create(plan.h, comm.h, cfg.h, C.byref(out)))
+        self.h = out
+
+    def smooth(self, b, x, stream=None):
+        _check(lib.ilug_dist_smooth(self.h, _ptr(b), _ptr(x), _stream(stream)))
+
+    def residual(self, x, b, r, stream=None):
+        _check(lib.ilug_dist_residual(self.h, _ptr(x), _ptr(b), _ptr(r), _stream(stream)))
+
+    def stats(self):
+        v = [C.c_longlong() for _ in range(4)]
+        _check(lib.ilug_dist_smoother_stats(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(("nloc", "nnz_A", "nnz_Ls", "nnz_Us"), (x.value for x in v)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and lib is not None:
+            lib.ilug_dist_smoother_free(self.h)
+            self.h = C.c_void_p()
+
+
+__all__ = ["partition", "generate_rows", "Plan", "unique_id", "Comm", "Smoother", "IlugError"]
