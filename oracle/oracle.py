@@ -85,6 +85,7 @@ class Ref:
             "ref_time_richardson_upper": (_i, [_vp, _pd, _ll, _ll, _pd]),
             "ref_time_smooth": (_i, [_vp, _vp, _pd, _ll, _pd]),
             "ref_run_solve": (_i, [_vp, _vp, _pvp]), "ref_report_get": (C.c_char_p, [_vp, C.c_char_p]),
+            "ref_run_analyze": (_i, [_vp, _vp, _pvp]),
             "ref_report_status": (_i, [_vp]), "ref_report_table_csv": (_vp, [_vp, C.c_char_p]),
             "ref_free_str": (None, [_vp]), "ref_report_free": (None, [_vp]),
             "iluamg_matrix_generate": (_i, [C.c_char_p, _pvp]), "iluamg_config_create": (_i, [_pvp]),
@@ -293,6 +294,25 @@ class Ref:
         self.L.ref_free_str(p)
         self.L.ref_report_free(rep)
         return out
+
+
+def _analyze(self, A, kv, keys=("dep_L", "dep_U", "dep_U_row", "dep_U_rowcol", "cond_L", "cond_U",
+                                 "striping_flagged", "nnz_L", "nnz_U")):
+    """The reference's run_analyze (src/driver.cpp:92-163) on (rp, ci, v)."""
+    Ah = self.mat(*A)
+    cfg = self.cfg(kv)
+    rep = C.c_void_p()
+    try:
+        self._ok(self.L.ref_run_analyze(Ah, cfg, C.byref(rep)))
+    finally:
+        self.free_mat(Ah)
+        self.L.ref_cfg_free(cfg)
+    out = {k: self.L.ref_report_get(rep, k.encode()).decode() for k in keys}
+    self.L.ref_report_free(rep)
+    return out
+
+
+Ref.run_analyze = _analyze
 
 
 class Port:

@@ -379,6 +379,12 @@ API int ref_run_solve(const void* A, const void* cfg, void** out) {
                                     "shim"));
     });
 }
+API int ref_run_analyze(const void* A, const void* cfg, void** out) {
+    return wrap([&] {
+        *out = new Report(run_analyze(*static_cast<const SparseMatrix*>(A), static_cast<const Cfg*>(cfg)->c,
+                                      "shim"));
+    });
+}
 API const char* ref_report_get(const void* r, const char* key) {
     const std::string* v = static_cast<const Report*>(r)->find(key);
     return v ? v->c_str() : nullptr;

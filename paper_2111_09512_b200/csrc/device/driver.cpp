@@ -358,9 +358,5 @@ Report run_schur_solve(const Csr& A, const Config& cfg, const std::string& label
     return r;
 }
 
-Report run_analyze(const Csr& A, const Config& cfg, const std::string& label) {
-    (void)A, (void)cfg, (void)label;
-    fail_invalid("analyze: factor diagnostics are not part of the device build yet");
-}
 
 } // namespace ilug

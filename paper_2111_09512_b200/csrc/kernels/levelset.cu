@@ -30,7 +30,7 @@ namespace ilug {
 
 namespace {
 
-constexpr int kSmallBlock = 512; // 16-entry chunks need up to 128 registers per thread
+constexpr int kSmallBlock = 384; // the prefetched row state needs ~150 registers per thread
 constexpr int kFlagBlock = 256;
 
 // MODE 0: unit lower, strict storage: x_i = b_i - sum L_ij x_j
@@ -127,13 +127,91 @@ k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const doub
         prefetch_level(0);
         prefetch_level(1);
     }
+    // Software pipeline: everything a row needs except x (its perm entry,
+    // length, slice base, b value and first kPre column/value pairs) is loaded
+    // for level L+1 before the barrier that ends level L, so the critical path
+    // per level is one gather of x plus the ordered accumulation.
+    constexpr int kPre = 16;
+    struct Next {
+        i64 p = -1, row = -1, base = 0;
+        int len = 0;
+        double bv = 0.0;
+        i32 c[kPre];
+        double a[kPre];
+    } nx;
+    auto fetch = [&](int L) {
+        nx.p = -1;
+        if (L >= nlev) return;
+        const i64 p = level_ptr[L] + threadIdx.x;
+        if (p >= level_ptr[L + 1]) return;
+        nx.p = p;
+        nx.row = M.perm[p];
+        if (nx.row < 0) return;
+        nx.len = M.rowlen[p];
+        nx.base = M.slice_ptr[p >> 5] + (p & 31);
+        nx.bv = b[nx.row];
+#pragma unroll
+        for (int u = 0; u < kPre; ++u)
+            if (u < nx.len) {
+                const i64 q = nx.base + static_cast<i64>(u) * kSlice;
+                nx.c[u] = __ldg(M.cols + q);
+                nx.a[u] = __ldg(M.vals + q);
+            }
+    };
+    fetch(0);
     for (int L = 0; L < nlev; ++L) {
         if (threadIdx.x == 0) prefetch_level(L + 2);
-        const i64 end = level_ptr[L + 1];
-        for (i64 p = level_ptr[L] + threadIdx.x; p < end; p += blockDim.x) {
-            const i64 row = M.perm[p];
-            if (row >= 0) level_row<MODE, false, 16>(M, p, row, b, x, xold, nullptr, 0u);
+        if (nx.p >= 0 && nx.row >= 0) {
+            const i64 row = nx.row;
+            double s = nx.bv, d = 1.0, xv[kPre];
+#pragma unroll
+            for (int u = 0; u < kPre; ++u) {
+                xv[u] = 0.0;
+                if (u < nx.len && !(MODE != 0 && nx.c[u] == row))
+                    xv[u] = (MODE == 2 && nx.c[u] > row) ? xold[nx.c[u]] : __ldcg(x + nx.c[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < kPre; ++u)
+                if (u < nx.len) {
+                    if (MODE != 0 && nx.c[u] == row)
+                        d = nx.a[u];
+                    else
+                        s = s - nx.a[u] * xv[u];
+                }
+            for (int t0 = kPre; t0 < nx.len; t0 += 8) { // long rows: the tail in batched chunks
+                i32 c[8];
+                double a[8], xt[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (t0 + u < nx.len) {
+                        const i64 q = nx.base + static_cast<i64>(t0 + u) * kSlice;
+                        c[u] = __ldg(M.cols + q);
+                        a[u] = __ldg(M.vals + q);
+                    }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    xt[u] = 0.0;
+                    if (t0 + u < nx.len && !(MODE != 0 && c[u] == row))
+                        xt[u] = (MODE == 2 && c[u] > row) ? xold[c[u]] : __ldcg(x + c[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (t0 + u < nx.len) {
+                        if (MODE != 0 && c[u] == row)
+                            d = a[u];
+                        else
+                            s = s - a[u] * xt[u];
+                    }
+            }
+            x[row] = MODE == 0 ? s : s / d;
         }
+        // rows beyond the first blockDim.x of a wide level
+        const i64 end = level_ptr[L + 1];
+        for (i64 p = level_ptr[L] + threadIdx.x + blockDim.x; p < end; p += blockDim.x) {
+            const i64 row = M.perm[p];
+            if (row >= 0) level_row<MODE, false, 8>(M, p, row, b, x, xold, nullptr, 0u);
+        }
+        fetch(L + 1);
         __syncthreads();
     }
 }
