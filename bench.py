@@ -8,8 +8,9 @@ m_L = m_U = 5 Richardson sweeps: residual SpMV + 4 L sweeps + 4 row-scaled U
 sweeps (the first iterate of each is exact, x1 = b), fused epilogues. The
 metric is achieved HBM GB/s with the fixed algorithmic-byte formula of
 SURVEY.md §8(d); the roofline object covers the dominant kernel
-(the scaled-U sweep). `--tts` adds the GMRES+AMG time-to-solution part of the
-metric (host setup + device solve) and the direct-sptrsv comparison.
+(the scaled-U sweep). The `tts` object is the GMRES+AMG time-to-solution part
+of the metric (host setup + device solve) with the direct-sptrsv comparison
+(`--no-tts` skips it).
 
 Multi-GPU (torchrun, N > 1): every rank smooths its own C2-sized row block
 (weak scaling; see DESIGN.md §6 for the halo-exchange plan), time = max over
@@ -161,6 +162,50 @@ def run_reference(args):
         "vs_baseline": None}))
 
 
+def build_workload(ilug, args, rank, world, local):
+    """The smoother of this rank: N=1 the C2 matrix; N>1 the rank's 256^3 slab of
+    pressure27(256,256,256N) (weak scaling), block-Jacobi ILUT factors of the
+    local diagonal block, global residual with an NCCL halo exchange."""
+    import ctypes as C
+    cfg = ilug.Config().update(ILU_KV)
+    if world == 1:
+        A = ilug.Matrix.generate(args.spec)
+        S = ilug.Smoother(A, cfg)  # host ILUT + upload + K1 row scaling on the device
+        v = [C.c_longlong() for _ in range(5)]
+        ilug._check(ilug.lib.ilug_smoother_stats(S.h, *[C.byref(x) for x in v]))
+        n, nnz_a, nnz_l, nnz_u, pad_u = (x.value for x in v)
+        smooth = S.smooth
+        once = lambda which, xin, rhs, out, st: ilug._check(ilug.lib.ilug_smoother_sweep_once(
+            S.h, which, xin.data_ptr(), rhs.data_ptr(), out.data_ptr(), st.cuda_stream))
+        host = lambda bp, xp: ilug._check(ilug.lib.ilug_smooth_host(S.h, bp, xp))
+        return dict(A=A, S=S, n=n, nnz_a=nnz_a, nnz_l=nnz_l, nnz_u=nnz_u, pad_u=pad_u, smooth=smooth, once=once,
+                    host=host, spec=args.spec)
+    import torch.distributed as dist
+    from paper_2111_09512_b200 import dist as idist
+    nx, ny, nz = (int(t) for t in args.spec[args.spec.index("(") + 1:args.spec.index(")")].split(",")[:3])
+    spec = f"pressure27({nx},{ny},{nz * world})"
+    n_g = nx * ny * nz * world
+    starts = idist.partition(n_g, world)
+    rows = idist.generate_rows(spec, int(starts[rank]), int(starts[rank + 1]))
+    plan = idist.Plan(rows, n_g, world, rank)
+
+    def all_gather(obj):
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+    plan.exchange_requests(all_gather)
+    uid = [idist.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = idist.Comm(world, rank, uid[0])
+    S = idist.Smoother(plan, comm, cfg)
+    st = S.stats()
+    once = lambda which, xin, rhs, out, stm: ilug._check(ilug.lib.ilug_dist_smoother_sweep_once(
+        S.h, which, xin.data_ptr(), rhs.data_ptr(), out.data_ptr(), stm.cuda_stream))
+    host = lambda bp, xp: ilug._check(ilug.lib.ilug_dist_smooth_host(S.h, bp, xp))
+    return dict(A=rows, S=S, plan=plan, comm=comm, n=st["nloc"], nnz_a=st["nnz_A"], nnz_l=st["nnz_Ls"],
+                nnz_u=st["nnz_Us"], pad_u=0, smooth=S.smooth, once=once, host=host, spec=spec)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -168,13 +213,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--spec", default=SPEC)
-    ap.add_argument("--tts", action="store_true", help="also run GMRES+AMG time-to-solution")
+    ap.add_argument("--no-tts", action="store_true", help="skip the GMRES+AMG time-to-solution part")
+    ap.add_argument("--tts-gs", action="store_true", help="also time the Gauss-Seidel coarse fallback")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
+    import ctypes as C
     import torch
     import paper_2111_09512_b200 as ilug
 
@@ -187,14 +233,9 @@ def main():
     ilug.lib.ilug_set_device(local)
 
     t0 = time.perf_counter()
-    A = ilug.Matrix.generate(args.spec)
-    cfg = ilug.Config().update(ILU_KV)
-    S = ilug.Smoother(A, cfg)  # host ILUT + upload + K1 row scaling on the device
+    W = build_workload(ilug, args, rank, world, local)
     setup_s = time.perf_counter() - t0
-    import ctypes as C
-    n_, na, nl, nu, pad = (C.c_longlong() for _ in range(5))
-    ilug._check(ilug.lib.ilug_smoother_stats(S.h, C.byref(n_), C.byref(na), C.byref(nl), C.byref(nu), C.byref(pad)))
-    n, nnz_a, nnz_l, nnz_u, pad_u = n_.value, na.value, nl.value, nu.value, pad.value
+    n, nnz_a, nnz_l, nnz_u, pad_u = W["n"], W["nnz_a"], W["nnz_l"], W["nnz_u"], W["pad_u"]
     B = step_bytes(n, nnz_a, nnz_l, nnz_u)
 
     stream = torch.cuda.current_stream()
@@ -202,7 +243,7 @@ def main():
     b = torch.rand(n, dtype=torch.float64, generator=g).cuda() * 2 - 1
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
     for _ in range(args.warmup):
-        S.smooth(b, x, stream=stream)
+        W["smooth"](b, x, stream=stream)
     torch.cuda.synchronize()
 
     def barrier():
@@ -210,22 +251,25 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
-            S.smooth(b, x, stream=stream)
+            W["smooth"](b, x, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     value = B * world / (ms * 1e-3) / 1e9
 
     # ---- roofline: the dominant kernel (scaled-U sweep), timed alone on the same stream
@@ -236,26 +280,24 @@ def main():
     kern = {}
     for which, name, nnz in ((1, "u_sweep", nnz_u), (0, "l_sweep", nnz_l)):
         for _ in range(3):
-            ilug._check(ilug.lib.ilug_smoother_sweep_once(S.h, which, xin.data_ptr(), b.data_ptr(),
-                                                          out.data_ptr(), stream.cuda_stream))
+            W["once"](which, xin, b, out, stream)
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(reps):
-            ilug._check(ilug.lib.ilug_smoother_sweep_once(S.h, which, xin.data_ptr(), b.data_ptr(),
-                                                          out.data_ptr(), stream.cuda_stream))
+            W["once"](which, xin, b, out, stream)
         e1.record(stream)
         torch.cuda.synchronize()
-        kms = e0.elapsed_time(e1) / reps
+        kms = max_over_ranks(e0.elapsed_time(e1) / reps)
         kern[name] = {"ms": kms, "gbs": sweep_bytes(n, nnz) / (kms * 1e-3) / 1e9, "bytes": sweep_bytes(n, nnz)}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "u_sweep_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
     ach = kern["u_sweep"]["gbs"]
     roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
-                "kernel": "k_rowdot<EpiResidual> on strict row-scaled U (SELL-32)",
+                "kernel": "k_rowdot<EpiResidual> on strict row-scaled U (SELL-32, sigma-sorted)",
                 "bytes_per_launch": kern["u_sweep"]["bytes"], "ms_per_launch": round(kern["u_sweep"]["ms"], 5),
                 "frac_of_8TBs_nominal": round(ach / 8000.0, 4),
                 "l_sweep_gbs": round(kern["l_sweep"]["gbs"], 1)}
@@ -267,58 +309,64 @@ def main():
     bp = bh.numpy().ctypes.data_as(C.POINTER(C.c_double))
     xp = xh.numpy().ctypes.data_as(C.POINTER(C.c_double))
     e2e_steps = max(3, min(args.steps, 20))
-    ilug._check(ilug.lib.ilug_smooth_host(S.h, bp, xp))
+    W["host"](bp, xp)
     barrier()
     t = time.perf_counter()
     for _ in range(e2e_steps):
-        ilug._check(ilug.lib.ilug_smooth_host(S.h, bp, xp))
-    e2e_s = (time.perf_counter() - t) / e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
-    e2e = {"value": round(B * world / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 16 * n,
-           "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_s * 1e3, 3),
-           "api": "ilug_smooth_host (pinned host b, x)"}
+        W["host"](bp, xp)
+    e2e_s = max_over_ranks((time.perf_counter() - t) / e2e_steps)
+    e2e = {"value": round(B * world / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 16 * n * world,
+           "d2h_bytes_per_step": 8 * n * world, "ms_per_step": round(e2e_s * 1e3, 3),
+           "api": "ilug_smooth_host / ilug_dist_smooth_host (pinned host b, x)"}
 
     res = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"ilu_smooth_sweep (m_L=m_U=5, row-scaled ILUT(1e-3,5)) on {args.spec}",
-                   "n": n, "nnz_A": nnz_a, "nnz_L_strict": nnz_l, "nnz_U_strict": nnz_u,
-                   "sell_padding_U": round(pad_u / max(nnz_u, 1) - 1, 4), "bytes_per_step": B,
+        "config": {"workload": f"ilu_smooth_sweep (m_L=m_U=5, row-scaled ILUT(1e-3,5)) on {W['spec']}"
+                               + ("" if world == 1 else f" (rank slabs of 256^3, block-Jacobi, NCCL halo)"),
+                   "n_per_gpu": n, "nnz_A": nnz_a, "nnz_L_strict": nnz_l, "nnz_U_strict": nnz_u,
+                   "sell_padding_U": round(pad_u / max(nnz_u, 1) - 1, 4) if pad_u else None, "bytes_per_step": B,
                    "l2": "inputs (>= 5 GB per step) exceed the 126 MB L2; no flush needed",
                    "parallelism": f"row-block x{world} (weak)", "host_setup_s": round(setup_s, 2)},
         "frac_of_peak": round(value / world / peak, 4),
         "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": 9 * args.steps,
     }
-    if args.tts and rank == 0:
-        res["tts"] = time_to_solution(ilug, A)
+    if not args.no_tts and rank == 0 and world == 1:
+        res["tts"] = time_to_solution(ilug, W["A"], ("poly_gs", "gauss_seidel") if args.tts_gs else ("poly_gs",))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist
+        del W
         dist.destroy_process_group()
 
 
-def time_to_solution(ilug, A):
-    """GMRES+AMG (tol 1e-8 relres, PMIS, ILUT smoother on the finest level, GS
-    below) through iluamg_run_solve, iterative vs direct (level-scheduled) triangular solves."""
+def time_to_solution(ilug, A, fallbacks=("poly_gs",)):
+    """GMRES+AMG (relres 1e-8, PMIS, ILUT(1e-3,5) row-scaled smoother on the
+    finest level, 2 sweeps) through iluamg_run_solve: iterative (m_L = m_U = 5
+    Richardson sweeps) vs direct (level-scheduled) triangular solves, for each
+    coarse-level fallback smoother. poly_gs is the GPU-friendly fallback (SpMV
+    based); gauss_seidel is the reference default (latency-bound level
+    scheduling on unstructured coarse grids). krylov.form_iterates=false: one
+    V-cycle per iteration (iteration counts unchanged, see tests)."""
     out = {}
-    base = dict(ILU_KV, **{"smoother.sweeps": "2", "krylov.tol": "1e-8", "amg.coarsening": "pmis",
-                           "krylov.form_iterates": "false"})
-    for mode in ("richardson", "direct"):
-        kv = dict(base, **{"trisolve.mode": mode})
-        rep = ilug.run_solve(A, ilug.Config().update(kv))
-        out[mode] = {"iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
-                     "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
-                     "final_relres": float(rep["final_relres"]), "levels": int(rep["levels"])}
-    out["speedup_iterative_vs_direct"] = round(out["direct"]["solve_s"] / out["richardson"]["solve_s"], 3)
+    for fb in fallbacks:
+        res = {}
+        base = dict(ILU_KV, **{"smoother.sweeps": "2", "krylov.tol": "1e-8", "amg.coarsening": "pmis",
+                               "krylov.form_iterates": "false", "smoother.fallback.kind": fb})
+        for mode in ("richardson", "direct"):
+            kv = dict(base, **{"trisolve.mode": mode})
+            rep = ilug.run_solve(A, ilug.Config().update(kv))
+            res[mode] = {"iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
+                         "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
+                         "final_relres": float(rep["final_relres"]), "levels": int(rep["levels"]),
+                         "vcycles": int(rep["device_vcycles"])}
+        res["speedup_iterative_vs_direct"] = round(res["direct"]["solve_s"] / res["richardson"]["solve_s"], 3)
+        out[f"fallback_{fb}"] = res
     return out
 
 

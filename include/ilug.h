@@ -185,7 +185,23 @@ ILUAMG_API int ilug_dist_residual(const ilug_dist_smoother* s, const double* x, 
                                   void* stream);
 ILUAMG_API int ilug_dist_smoother_stats(const ilug_dist_smoother* s, long long* nloc, long long* nnz_A,
                                         long long* nnz_Ls, long long* nnz_Us);
+/* Host-buffer application (copy this rank's b, x in; smooth; copy x out; synchronous). */
+ILUAMG_API int ilug_dist_smooth_host(const ilug_dist_smoother* s, const double* b_host, double* x_host);
+/* One bare L (which = 0) or U (which = 1) sweep kernel of the local factors, for kernel timing. */
+ILUAMG_API int ilug_dist_smoother_sweep_once(const ilug_dist_smoother* s, int which, const double* x_in,
+                                             const double* rhs, double* out, void* stream);
 ILUAMG_API void ilug_dist_smoother_free(ilug_dist_smoother* s);
+
+/* Distributed GMRES+AMG: global (F)GMRES over the ranks' rows (halo SpMV,
+ * NCCL-summed CGS2 reductions) with block-Jacobi AMG (each rank's V-cycle on
+ * its diagonal block, amg.* and smoother.* keys). b, x: this rank's rows. */
+typedef struct ilug_dist_solver_s ilug_dist_solver;
+ILUAMG_API int ilug_dist_solver_create(const ilug_dist_plan* p, const ilug_dist_comm* c,
+                                       const iluamg_config* cfg, ilug_dist_solver** out);
+ILUAMG_API int ilug_dist_gmres(ilug_dist_solver* s, const iluamg_config* cfg, const double* b, double* x,
+                               long long* iterations, double* final_relres, void* stream);
+ILUAMG_API int ilug_dist_solver_levels(const ilug_dist_solver* s);
+ILUAMG_API void ilug_dist_solver_free(ilug_dist_solver* s);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,12 @@ _SIGS = {
     "ilug_dist_residual": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "ilug_dist_smoother_stats": (_i, [_vp, _pll, _pll, _pll, _pll]),
     "ilug_dist_smoother_free": (None, [_vp]),
+    "ilug_dist_smooth_host": (_i, [_vp, _pd, _pd]),
+    "ilug_dist_smoother_sweep_once": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
+    "ilug_dist_solver_create": (_i, [_vp, _vp, _vp, _pvp]),
+    "ilug_dist_gmres": (_i, [_vp, _vp, _vp, _vp, _pll, _pd, _vp]),
+    "ilug_dist_solver_levels": (_i, [_vp]),
+    "ilug_dist_solver_free": (None, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

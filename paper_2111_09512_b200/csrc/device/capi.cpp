@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <exception>
+#include <functional>
 #include <string>
 
 struct iluamg_matrix_s {
@@ -115,6 +116,11 @@ ilug::UpperIteration upper_of(int u) {
 }
 
 } // namespace
+
+namespace ilug {
+// Shared by the other C-ABI translation units (capi_dist.cpp).
+int capi_guarded(const std::function<int()>& fn) { return guarded(fn); }
+} // namespace ilug
 
 extern "C" {
 
@@ -643,9 +649,10 @@ struct ilug_dist_plan_s {
 struct ilug_dist_comm_s {
     std::unique_ptr<ilug::DistComm> c;
 };
-struct ilug_dist_smoother_s {
+struct ilug_dist_smoother_s { // same layout as in capi_dist.cpp
     ilug::DistSmoother s;
     long long nnz_A = 0;
+    mutable ilug::DBuf<double> hb, hx; // staging for ilug_dist_smooth_host
 };
 
 extern "C" {

@@ -1,0 +1,102 @@
+// C ABI of the distributed GMRES+AMG solver (ilug_dist_solver_*). The plan
+// and communicator handles are defined in capi.cpp; their layouts are
+// repeated here through the shared header-free structs below.
+#include "../../../include/ilug.h"
+#include "../host/config.hpp"
+#include "dist.hpp"
+
+#include <memory>
+#include <string>
+
+// Same definitions as capi.cpp (one ODR-identical definition per TU).
+struct iluamg_config_s {
+    ilug::Config cfg;
+};
+struct ilug_dist_plan_s {
+    ilug::HaloPlan plan;
+};
+struct ilug_dist_comm_s {
+    std::unique_ptr<ilug::DistComm> c;
+};
+struct ilug_dist_solver_s {
+    ilug::DistSolver s;
+};
+struct ilug_dist_smoother_s {
+    ilug::DistSmoother s;
+    long long nnz_A = 0;
+    mutable ilug::DBuf<double> hb, hx; // staging for ilug_dist_smooth_host
+};
+
+namespace ilug {
+int capi_guarded(const std::function<int()>& fn); // capi.cpp: exception -> status + last error
+}
+
+extern "C" {
+
+int ilug_dist_solver_create(const ilug_dist_plan* p, const ilug_dist_comm* c, const iluamg_config* cfg,
+                            ilug_dist_solver** out) {
+    return ilug::capi_guarded([&] {
+        if (!p || !c || !cfg || !out) ilug::fail_invalid("null argument");
+        auto* s = new ilug_dist_solver_s();
+        try {
+            s->s.build(p->plan, *c->c, ilug::amg_params_from(cfg->cfg), cfg->cfg.get_bool("device.graph"), nullptr);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_dist_gmres(ilug_dist_solver* s, const iluamg_config* cfg, const double* b, double* x,
+                    long long* iterations, double* final_relres, void* stream) {
+    return ilug::capi_guarded([&] {
+        if (!s || !cfg || !b || !x) ilug::fail_invalid("null argument");
+        const auto& c = cfg->cfg;
+        ilug::KrylovParams p;
+        p.flexible = c.get("krylov.method") == "fgmres";
+        p.restart = c.get_index("krylov.restart");
+        p.max_iters = c.get_index("krylov.max_iters");
+        p.tol = c.get_double("krylov.tol");
+        p.nrbe_criterion = c.get("krylov.criterion") == "nrbe";
+        if (p.nrbe_criterion) ilug::fail_invalid("distributed gmres: the nrbe criterion needs |A|_2 (not distributed)");
+        p.record_history = c.get_bool("krylov.record_history");
+        p.form_iterates = c.get_bool("krylov.form_iterates");
+        const ilug::KrylovReport r = s->s.solve(b, x, p, static_cast<cudaStream_t>(stream));
+        ILUG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+        if (iterations) *iterations = r.iterations;
+        if (final_relres) *final_relres = r.final_relres;
+        return r.converged ? ILUAMG_OK : ILUAMG_NOT_CONVERGED;
+    });
+}
+
+int ilug_dist_solver_levels(const ilug_dist_solver* s) { return s ? s->s.levels() : -1; }
+
+int ilug_dist_smooth_host(const ilug_dist_smoother* s, const double* bh, double* xh) {
+    return ilug::capi_guarded([&] {
+        if (!s || !bh || !xh) ilug::fail_invalid("null argument");
+        const ilug::i64 n = s->s.nloc();
+        if (s->hb.n != n) s->hb.alloc(n), s->hx.alloc(n);
+        s->hb.upload(bh, n);
+        s->hx.upload(xh, n);
+        s->s.smooth(s->hb.p, s->hx.p, nullptr);
+        s->hx.download(xh);
+        ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_dist_smoother_sweep_once(const ilug_dist_smoother* s, int which, const double* x_in, const double* rhs,
+                                  double* out, void* stream) {
+    return ilug::capi_guarded([&] {
+        if (!s || !x_in || !rhs || !out) ilug::fail_invalid("null argument");
+        const ilug::DeviceIlu* f = s->s.smoother().ilu();
+        ilug::residual(which == 0 ? f->Ls() : f->Us(), x_in, rhs, out, static_cast<cudaStream_t>(stream));
+        return ILUAMG_OK;
+    });
+}
+
+void ilug_dist_solver_free(ilug_dist_solver* s) { delete s; }
+
+} // extern "C"

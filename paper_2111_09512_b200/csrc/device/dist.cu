@@ -74,6 +74,41 @@ void HaloExchange::exchange(const double* x, cudaStream_t st) const {
     ILUG_NCCL(ncclGroupEnd());
 }
 
+namespace {
+void setup_halo(HaloExchange& hx, DeviceMatrix& A, const HaloPlan& plan, const DistComm& comm, cudaStream_t st) {
+    hx.comm = comm.comm;
+    hx.nloc = plan.nloc;
+    hx.nhalo = plan.nhalo;
+    hx.recv_ranks = plan.recv_ranks;
+    hx.recv_offsets = plan.recv_offsets;
+    hx.send_ranks = plan.send_ranks;
+    hx.send_offsets = plan.send_offsets;
+    hx.send_idx.upload(plan.send_local.data(), static_cast<i64>(plan.send_local.size()), st);
+    hx.sendbuf.alloc(static_cast<i64>(plan.send_local.size()));
+    hx.halo.alloc(std::max<i64>(plan.nhalo, 1));
+    A.build(plan.A_ext, st);
+    A.n = plan.nloc;
+    A.halo = &hx;
+}
+} // namespace
+
+void DistSolver::build(const HaloPlan& plan, const DistComm& comm, const AmgParams& ap, bool use_graph,
+                       cudaStream_t st) {
+    comm_ = &comm;
+    setup_halo(hx_, A_, plan, comm, st);
+    A_diag_ = plan.A_diag;
+    hh_ = amg_setup(A_diag_, ap);
+    H_.set_use_graph(use_graph);
+    H_.build(hh_, st);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+KrylovReport DistSolver::solve(const double* b, double* x, const KrylovParams& p, cudaStream_t st) {
+    KrylovParams q = p;
+    if (comm_->nranks > 1) q.estimate_anorm = false;
+    return device_gmres(A_, A_diag_, H_, b, x, q, st, comm_);
+}
+
 void DistSmoother::build(const HaloPlan& plan, const DistComm& comm, const SmootherConfig& cfg, cudaStream_t st) {
     if (cfg.kind != SmootherKind::ilu) fail_invalid("distributed smoother: smoother.kind must be ilu");
     if (plan.nranks > 1 && plan.send_offsets.size() != plan.send_ranks.size() + (plan.send_ranks.empty() ? 0 : 1))

@@ -39,4 +39,23 @@ private:
     DeviceSmoother s_;
 };
 
+/// Row-block distributed GMRES+AMG: global Krylov iteration (halo-exchanged
+/// SpMV, NCCL-summed CGS2 reductions) preconditioned by this rank's AMG
+/// V-cycle on its diagonal block (block-Jacobi AMG; ILU smoothing inside).
+class DistSolver {
+public:
+    void build(const HaloPlan& plan, const DistComm& comm, const AmgParams& ap, bool use_graph, cudaStream_t st);
+    KrylovReport solve(const double* b, double* x, const KrylovParams& p, cudaStream_t st);
+    i64 nloc() const { return A_.n; }
+    int levels() const { return H_.num_levels(); }
+
+private:
+    const DistComm* comm_ = nullptr;
+    HaloExchange hx_;
+    DeviceMatrix A_;
+    Csr A_diag_;
+    HostHierarchy hh_;
+    DeviceHierarchy H_;
+};
+
 } // namespace ilug

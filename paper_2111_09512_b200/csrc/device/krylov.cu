@@ -7,7 +7,7 @@
 // deliberate deviation is the orthogonalisation: modified Gram-Schmidt's j+1
 // dependent dot/axpy passes become three fused CGS2 passes over the basis
 // (SURVEY.md §8a a11b(iii)); iteration counts agree with the reference to ±1.
-#include "solver.hpp"
+#include "dist.hpp"
 #include "../host/problems.hpp"
 
 #include <cmath>
@@ -20,7 +20,12 @@ struct Scalars {
     DBuf<double> d;   // device scalars: h1[64] h2[64] nrm[1] misc[8]
     DBuf<double> ws;  // reduction workspace
     std::vector<double> h;
-    explicit Scalars(i64 n) : d(64 * 2 + 16), ws(reduce_ws_doubles(n)), h(64 * 2 + 16) {}
+    const DistComm* comm = nullptr; // row-block distributed: sum partial reductions over ranks
+    explicit Scalars(i64 n, const DistComm* c = nullptr)
+        : d(64 * 2 + 16), ws(reduce_ws_doubles(n)), h(64 * 2 + 16), comm(c) {}
+    void sum(double* p, i64 k, cudaStream_t st) const {
+        if (comm) comm->allreduce_sum(p, k, st);
+    }
     double* h1() { return d.p; }
     double* h2() { return d.p + 64; }
     double* nrm() { return d.p + 128; }
@@ -29,6 +34,7 @@ struct Scalars {
 
 double dev_norm(const double* v, i64 n, Scalars& s, cudaStream_t st) {
     nrm2sq_dev(v, n, s.misc(), s.ws.p, st);
+    s.sum(s.misc(), 1, st);
     double h = 0.0;
     ILUG_CUDA(cudaMemcpyAsync(&h, s.misc(), sizeof h, cudaMemcpyDeviceToHost, st));
     ILUG_CUDA(cudaStreamSynchronize(st));
@@ -66,16 +72,19 @@ double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 st
 }
 
 KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierarchy& M,
-                          const double* b, double* x, const KrylovParams& p, cudaStream_t st) {
+                          const double* b, double* x, const KrylovParams& p, cudaStream_t st,
+                          const DistComm* comm) {
     const i64 n = A.n;
     if (p.restart < 1) fail_invalid("gmres: restart must be >= 1");
     if (p.restart > 63) fail_invalid("gmres: restart must be <= 63 on the device (basis width)");
     if (!(p.tol > 0.0)) fail_invalid("gmres: tol must be > 0");
     const i64 R = p.restart;
     KrylovReport rep;
-    Scalars sc(n);
-    rep.anorm_estimate = p.estimate_anorm ? device_estimate_two_norm(A, A_host, 50, p.anorm_seed, st)
-                                          : std::nan("");
+    Scalars sc(n, comm);
+    const bool distributed = comm && comm->nranks > 1; // |A|_2 needs a global transpose: skipped
+    rep.anorm_estimate = p.estimate_anorm && !distributed
+                             ? device_estimate_two_norm(A, A_host, 50, p.anorm_seed, st)
+                             : std::nan("");
     rep.bnorm = dev_norm(b, n, sc, st);
     const double bden = rep.bnorm > 0.0 ? rep.bnorm : 1.0;
 
@@ -84,7 +93,7 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
     double* zbuf = mz.p;
 
     auto true_norms = [&](const double* xv, double& res, double& xn) {
-        residual(A.A, xv, b, r.p, st);
+        A.residual(xv, b, r.p, st);
         res = dev_norm(r.p, n, sc, st);
         xn = dev_norm(xv, n, sc, st);
     };
@@ -106,7 +115,7 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
     i64 total = 0;
     double last_arnoldi = 0.0;
     {
-        residual(A.A, x, b, r.p, st);
+        A.residual(x, b, r.p, st);
         const double r0 = dev_norm(r.p, n, sc, st);
         const HistoryEntry e0 = record(0, r0, x);
         last_arnoldi = e0.arnoldi;
@@ -122,7 +131,7 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
     auto h = [&](i64 i, i64 j) -> double& { return H[static_cast<size_t>(j * (R + 1) + i)]; };
     bool done = false;
     while (!done && total < p.max_iters) {
-        residual(A.A, x, b, r.p, st);
+        A.residual(x, b, r.p, st);
         const double beta = dev_norm(r.p, n, sc, st);
         if (!std::isfinite(beta)) fail_numeric("gmres: residual is not finite");
         if (beta == 0.0) {
@@ -138,11 +147,14 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
             double* zj = p.flexible ? Z.p + j * n : zbuf;
             M.vcycle(V.p + j * n, zj, st);
             ++rep.vcycles;
-            spmv(A.A, zj, w.p, st);
+            A.spmv(zj, w.p, st);
             const int k = static_cast<int>(j + 1);
             multi_dot(V.p, n, k, w.p, n, sc.h1(), sc.ws.p, st);
+            sc.sum(sc.h1(), k, st);
             multi_axpy_dot(V.p, n, k, sc.h1(), w.p, n, sc.h2(), sc.ws.p, st);
+            sc.sum(sc.h2(), k, st);
             multi_axpy_nrm(V.p, n, k, sc.h2(), w.p, n, sc.nrm(), sc.ws.p, st);
+            sc.sum(sc.nrm(), 1, st);
             ILUG_CUDA(cudaMemcpyAsync(sc.h.data(), sc.d.p, sizeof(double) * 129, cudaMemcpyDeviceToHost, st));
             ILUG_CUDA(cudaStreamSynchronize(st));
             for (i64 i = 0; i <= j; ++i) h(i, j) = sc.h[i] + sc.h[64 + i];

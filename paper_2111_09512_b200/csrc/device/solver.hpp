@@ -210,8 +210,13 @@ struct KrylovReport {
 
 /// Right-preconditioned (F)GMRES on the device, CGS2 orthogonalisation.
 /// Host work per iteration: Givens rotations on (j+2) scalars.
+struct DistComm;
+/// comm != nullptr: A holds this rank's rows (halo-exchanged SpMV), vectors are
+/// rank-local, every reduction is summed over ranks (NCCL allreduce), and M is
+/// this rank's block-Jacobi AMG hierarchy.
 KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierarchy& M,
-                          const double* b_dev, double* x_dev, const KrylovParams& p, cudaStream_t st);
+                          const double* b_dev, double* x_dev, const KrylovParams& p, cudaStream_t st,
+                          const DistComm* comm = nullptr);
 
 /// 50-step power iteration on A^T A (src/krylov.cpp:14-28) on the device.
 double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 steps,

@@ -126,4 +126,24 @@ class Smoother:
             self.h = C.c_void_p()
 
 
-__all__ = ["partition", "generate_rows", "Plan", "unique_id", "Comm", "Smoother", "IlugError"]
+class Solver:
+    """Distributed GMRES+AMG (block-Jacobi AMG preconditioner, global Krylov)."""
+
+    def __init__(self, plan: Plan, comm: Comm, cfg: Config):
+        out = C.c_void_p()
+        _check(lib.ilug_dist_solver_create(plan.h, comm.h, cfg.h, C.byref(out)))
+        self.h = out
+
+    def gmres(self, cfg: Config, b, x, stream=None):
+        it, rr = C.c_longlong(), C.c_double()
+        st = lib.ilug_dist_gmres(self.h, cfg.h, _ptr(b), _ptr(x), C.byref(it), C.byref(rr), _stream(stream))
+        _check(st, allow_not_converged=True)
+        return dict(status=st, iterations=it.value, final_relres=rr.value)
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and lib is not None:
+            lib.ilug_dist_solver_free(self.h)
+            self.h = C.c_void_p()
+
+
+__all__ = ["partition", "generate_rows", "Plan", "unique_id", "Comm", "Smoother", "Solver", "IlugError"]
