@@ -7,14 +7,62 @@
 // the residual kernel that consumes it.
 #include "dist.hpp"
 
-#include <nccl.h>
+#include <nccl.h> // types only: the library is bound at run time (below)
+
+#include <dlfcn.h>
+
+#include <cstdlib>
 
 namespace ilug {
 
 namespace {
 
+// NCCL is resolved lazily with dlopen on first multi-GPU use, never linked:
+// (1) an already-loaded libnccl.so.2 (torch's, in a torch process) is reused;
+// (2) else ILUG_NCCL_LIB (set by paper_2111_09512_b200.dist to torch's bundled
+// copy) or the system libnccl.so.2. Linking the system 2.27 at build time would
+// shadow torch's 2.28 by SONAME and break `import torch` afterwards.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) GetUniqueId;
+    decltype(&ncclCommInitRank) CommInitRank;
+    decltype(&ncclCommDestroy) CommDestroy;
+    decltype(&ncclAllReduce) AllReduce;
+    decltype(&ncclSend) Send;
+    decltype(&ncclRecv) Recv;
+    decltype(&ncclGroupStart) GroupStart;
+    decltype(&ncclGroupEnd) GroupEnd;
+    decltype(&ncclGetErrorString) GetErrorString;
+};
+
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char* env = std::getenv("ILUG_NCCL_LIB");
+            h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!h) fail_invalid(std::string("NCCL library not found (set ILUG_NCCL_LIB): ") + dlerror());
+        NcclApi a{};
+        auto bind = [&](auto& fp, const char* name) {
+            fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+            if (!fp) fail_invalid(std::string("NCCL symbol missing: ") + name);
+        };
+        bind(a.GetUniqueId, "ncclGetUniqueId");
+        bind(a.CommInitRank, "ncclCommInitRank");
+        bind(a.CommDestroy, "ncclCommDestroy");
+        bind(a.AllReduce, "ncclAllReduce");
+        bind(a.Send, "ncclSend");
+        bind(a.Recv, "ncclRecv");
+        bind(a.GroupStart, "ncclGroupStart");
+        bind(a.GroupEnd, "ncclGroupEnd");
+        bind(a.GetErrorString, "ncclGetErrorString");
+        return a;
+    }();
+    return api;
+}
+
 [[noreturn]] void nccl_fail(ncclResult_t r, const char* what) {
-    fail_numeric(std::string("NCCL error ") + ncclGetErrorString(r) + " in " + what);
+    fail_numeric(std::string("NCCL error ") + nccl().GetErrorString(r) + " in " + what);
 }
 #define ILUG_NCCL(call)                                   \
     do {                                                  \
@@ -33,7 +81,7 @@ __global__ void k_pack(i64 n, const i32* __restrict__ idx, const double* __restr
 void dist_unique_id(char out[128]) {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
     ncclUniqueId id;
-    ILUG_NCCL(ncclGetUniqueId(&id));
+    ILUG_NCCL(nccl().GetUniqueId(&id));
     std::memcpy(out, &id, 128);
 }
 
@@ -41,17 +89,17 @@ DistComm::DistComm(int nranks_, int rank_, const char id[128]) : nranks(nranks_)
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);
     ncclComm_t c;
-    ILUG_NCCL(ncclCommInitRank(&c, nranks, uid, rank));
+    ILUG_NCCL(nccl().CommInitRank(&c, nranks, uid, rank));
     comm = c;
 }
 
 DistComm::~DistComm() {
-    if (comm) ncclCommDestroy(static_cast<ncclComm_t>(comm));
+    if (comm) nccl().CommDestroy(static_cast<ncclComm_t>(comm));
 }
 
 void DistComm::allreduce_sum(double* buf, i64 count, cudaStream_t st) const {
     if (nranks == 1) return;
-    ILUG_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum,
+    ILUG_NCCL(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum,
                             static_cast<ncclComm_t>(comm), st));
 }
 
@@ -64,14 +112,14 @@ void HaloExchange::exchange(const double* x, cudaStream_t st) const {
     }
     if (send_ranks.empty() && recv_ranks.empty()) return;
     auto c = static_cast<ncclComm_t>(comm);
-    ILUG_NCCL(ncclGroupStart());
+    ILUG_NCCL(nccl().GroupStart());
     for (size_t k = 0; k < send_ranks.size(); ++k)
-        ILUG_NCCL(ncclSend(sendbuf.p + send_offsets[k], static_cast<size_t>(send_offsets[k + 1] - send_offsets[k]),
+        ILUG_NCCL(nccl().Send(sendbuf.p + send_offsets[k], static_cast<size_t>(send_offsets[k + 1] - send_offsets[k]),
                            ncclDouble, static_cast<int>(send_ranks[k]), c, st));
     for (size_t k = 0; k < recv_ranks.size(); ++k)
-        ILUG_NCCL(ncclRecv(halo.p + recv_offsets[k], static_cast<size_t>(recv_offsets[k + 1] - recv_offsets[k]),
+        ILUG_NCCL(nccl().Recv(halo.p + recv_offsets[k], static_cast<size_t>(recv_offsets[k + 1] - recv_offsets[k]),
                            ncclDouble, static_cast<int>(recv_ranks[k]), c, st));
-    ILUG_NCCL(ncclGroupEnd());
+    ILUG_NCCL(nccl().GroupEnd());
 }
 
 namespace {

@@ -15,6 +15,26 @@ import numpy as np
 from . import Config, IlugError, Matrix, _as, _check, _ptr, _stream, lib
 
 
+def _prefer_torch_nccl() -> None:
+    """libilug binds NCCL lazily (dlopen). Point it at torch's bundled NCCL so a
+    process that imports torch (before or after) ends up with one NCCL copy."""
+    import os
+    if os.environ.get("ILUG_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl as nn  # torch's pip dependency
+        for base in list(getattr(nn, "__path__", [])):
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["ILUG_NCCL_LIB"] = cand
+                return
+    except ImportError:
+        pass
+
+
+_prefer_torch_nccl()
+
+
 def partition(n: int, nranks: int) -> np.ndarray:
     starts = np.empty(nranks + 1, np.int64)
     _check(lib.ilug_dist_partition(n, nranks, _as(starts, C.c_longlong)))
