@@ -89,6 +89,13 @@ ILUAMG_API int ilug_solve_upper(const ilug_factors* f, const double* b, double* 
 ILUAMG_API int ilug_factors_stats(const ilug_factors* f, long long* n, long long* nnz_Ls,
                                   long long* nnz_Us, long long* padded_Us, int* levels_L,
                                   int* levels_U);
+/* Wavefront (temporally blocked) sweep plans: tile counts of L and U (0 = the
+ * fused path is off for these factors, see ILUG_WAVEFRONT); whether a fused
+ * launch hit its bounded-spin guard since the last query (*stalled = 1: a
+ * scheduling bug, the affected results must be discarded); and how many work
+ * items had to wait for their inputs (schedule diagnostic). Resets both. */
+ILUAMG_API int ilug_factors_wave(const ilug_factors* f, long long* tiles_L, long long* tiles_U,
+                                 int* stalled, long long* waits);
 ILUAMG_API void ilug_factors_free(ilug_factors* f);
 
 /* ---- K6: device operator ---- */
@@ -115,6 +122,16 @@ ILUAMG_API int ilug_smooth_host(const ilug_smoother* s, const double* b_host, do
  * SELL padded entries of strict U. */
 ILUAMG_API int ilug_smoother_stats(const ilug_smoother* s, long long* n, long long* nnz_A,
                                    long long* nnz_Ls, long long* nnz_Us, long long* padded_Us);
+/* Same as ilug_factors_wave for an ILU smoother's factors (zeros for other kinds). */
+ILUAMG_API int ilug_smoother_wave(const ilug_smoother* s, long long* tiles_L, long long* tiles_U,
+                                  int* stalled, long long* waits);
+/* nsweeps (2..9) fused sweeps of one factor in one wavefront launch, for per-kernel
+ * timing: x_{k+1} = rhs - T x_k from x_1 = x_in, T = strict L (which = 0) or strict
+ * (scaled) U (which = 1); tmp: (nsweeps - 1) * n doubles; out = x_{nsweeps+1}.
+ * ILUAMG_ERR_INVALID when the smoother has no wavefront plan. */
+ILUAMG_API int ilug_smoother_sweeps_fused(const ilug_smoother* s, int which, int nsweeps,
+                                          const double* x_in, const double* rhs, double* tmp,
+                                          double* out, void* stream);
 /* One bare sweep kernel of an ILU smoother's factor, for per-kernel timing:
  * out = rhs - T x_in with T = strict L (which = 0) or strict (scaled) U (which = 1). */
 ILUAMG_API int ilug_smoother_sweep_once(const ilug_smoother* s, int which, const double* x_in,

@@ -69,6 +69,7 @@ _SIGS = {
     "ilug_sweep_upper_host": (_i, [_vp, _pd, _pd, _ll]),
     "ilug_solve_lower": (_i, [_vp, _vp, _vp, _vp]), "ilug_solve_upper": (_i, [_vp, _vp, _vp, _vp]),
     "ilug_factors_stats": (_i, [_vp, _pll, _pll, _pll, _pll, _pi, _pi]),
+    "ilug_factors_wave": (_i, [_vp, _pll, _pll, _pi, _pll]),
     "ilug_factors_free": (None, [_vp]),
     "ilug_dmatrix_create": (_i, [_vp, _pvp]), "ilug_spmv": (_i, [_vp, _vp, _vp, _vp]),
     "ilug_residual": (_i, [_vp, _vp, _vp, _vp, _vp]), "ilug_dmatrix_free": (None, [_vp]),
@@ -76,6 +77,8 @@ _SIGS = {
     "ilug_ilu_smooth_sweep": (_i, [_vp, _vp, _vp, _vp]), "ilug_smoother_free": (None, [_vp]),
     "ilug_smooth_host": (_i, [_vp, _pd, _pd]),
     "ilug_smoother_stats": (_i, [_vp, _pll, _pll, _pll, _pll, _pll]),
+    "ilug_smoother_wave": (_i, [_vp, _pll, _pll, _pi, _pll]),
+    "ilug_smoother_sweeps_fused": (_i, [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "ilug_smoother_sweep_once": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ilug_hierarchy_create": (_i, [_vp, _vp, _pvp]), "ilug_hierarchy_create_host": (_i, [_vp, _vp, _pvp]),
     "ilug_hierarchy_levels": (_i, [_vp]), "ilug_hierarchy_level_matrix": (_i, [_vp, _i, _i, _pvp]),
@@ -358,6 +361,12 @@ class Factors:
         return dict(n=n.value, nnz_Ls=nl.value, nnz_Us=nu.value, padded_Us=pad.value,
                     levels_L=ll.value, levels_U=lu.value)
 
+    def wave(self):
+        """Wavefront plan tile counts and the stalled flag (see ilug_factors_wave)."""
+        tl, tu, st, wt = C.c_longlong(), C.c_longlong(), C.c_int(), C.c_longlong()
+        _check(lib.ilug_factors_wave(self.h, C.byref(tl), C.byref(tu), C.byref(st), C.byref(wt)))
+        return dict(tiles_L=tl.value, tiles_U=tu.value, stalled=bool(st.value), waits=wt.value)
+
     def download_upper(self):
         nl, nu = C.c_longlong(), C.c_longlong()
         _check(lib.ilug_factors_nnz(self.h, C.byref(nl), C.byref(nu)))
@@ -428,6 +437,17 @@ class Smoother:
 
     def ilu_sweep(self, b, x, stream=None):
         _check(lib.ilug_ilu_smooth_sweep(self.h, _ptr(b), _ptr(x), _stream(stream)))
+
+    def wave(self):
+        """Wavefront plan tile counts and the stalled flag (see ilug_smoother_wave)."""
+        tl, tu, st, wt = C.c_longlong(), C.c_longlong(), C.c_int(), C.c_longlong()
+        _check(lib.ilug_smoother_wave(self.h, C.byref(tl), C.byref(tu), C.byref(st), C.byref(wt)))
+        return dict(tiles_L=tl.value, tiles_U=tu.value, stalled=bool(st.value), waits=wt.value)
+
+    def sweeps_fused(self, which: int, nsweeps: int, x_in, rhs, tmp, out, stream=None):
+        _check(lib.ilug_smoother_sweeps_fused(self.h, which, nsweeps, _ptr(x_in), _ptr(rhs),
+                                              _ptr(tmp) if tmp is not None else None, _ptr(out),
+                                              _stream(stream)))
 
     def __del__(self):
         if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit

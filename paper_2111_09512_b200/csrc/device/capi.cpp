@@ -372,7 +372,7 @@ struct Ws {
 int ilug_sweep_lower(const ilug_factors* f, const double* b, double* y, long long m, void* stream) {
     return guarded([&] {
         need(f && b && y);
-        Ws ws(2 * f->f.n(), S(stream));
+        Ws ws(f->f.sweep_ws(m), S(stream));
         f->f.sweep_lower(b, y, m, ws.p, S(stream));
         return ILUAMG_OK;
     });
@@ -380,7 +380,7 @@ int ilug_sweep_lower(const ilug_factors* f, const double* b, double* y, long lon
 int ilug_sweep_upper(const ilug_factors* f, const double* b, double* x, long long m, void* stream) {
     return guarded([&] {
         need(f && b && x);
-        Ws ws(3 * f->f.n(), S(stream));
+        Ws ws(f->f.sweep_ws(m) + f->f.n(), S(stream));
         f->f.sweep_upper(b, x, m, ws.p, S(stream));
         return ILUAMG_OK;
     });
@@ -389,7 +389,7 @@ int ilug_sweep_upper_host(const ilug_factors* f, const double* bh, double* xh, l
     return guarded([&] {
         need(f && bh && xh);
         const ilug::i64 n = f->f.n();
-        ilug::DBuf<double> b, x(n), ws(3 * std::max<ilug::i64>(n, 1));
+        ilug::DBuf<double> b, x(n), ws(std::max<ilug::i64>(f->f.sweep_ws(m) + n, 3));
         b.upload(bh, n);
         f->f.sweep_upper(b.p, x.p, m, ws.p, nullptr);
         x.download(xh);
@@ -422,6 +422,24 @@ int ilug_factors_stats(const ilug_factors* f, long long* n, long long* nl, long 
         if (padded) *padded = f->f.Us().padded;
         if (lev_l) *lev_l = f->f.lower_plan().levels();
         if (lev_u) *lev_u = f->f.upper_plan().levels();
+        return ILUAMG_OK;
+    });
+}
+namespace {
+void wave_report(const ilug::DeviceIlu* f, long long* tl, long long* tu, int* stalled, long long* waits) {
+    long long wl = 0, wu = 0;
+    const bool bad_l = f && ilug::wave_stalled(f->wave_L(), &wl);
+    const bool bad_u = f && ilug::wave_stalled(f->wave_U(), &wu);
+    if (tl) *tl = f ? f->wave_L().ntiles : 0;
+    if (tu) *tu = f ? f->wave_U().ntiles : 0;
+    if (stalled) *stalled = bad_l || bad_u ? 1 : 0;
+    if (waits) *waits = wl + wu;
+}
+} // namespace
+int ilug_factors_wave(const ilug_factors* f, long long* tl, long long* tu, int* stalled, long long* waits) {
+    return guarded([&] {
+        need(f);
+        wave_report(&f->f, tl, tu, stalled, waits);
         return ILUAMG_OK;
     });
 }
@@ -525,6 +543,26 @@ int ilug_smoother_stats(const ilug_smoother* s, long long* n, long long* nnz_A, 
         if (nl) *nl = f ? f->Ls().nnz : 0;
         if (nu) *nu = f ? f->Us().nnz : 0;
         if (padded) *padded = f ? f->Us().padded : 0;
+        return ILUAMG_OK;
+    });
+}
+int ilug_smoother_wave(const ilug_smoother* s, long long* tl, long long* tu, int* stalled, long long* waits) {
+    return guarded([&] {
+        need(s);
+        wave_report(s->s.ilu(), tl, tu, stalled, waits);
+        return ILUAMG_OK;
+    });
+}
+int ilug_smoother_sweeps_fused(const ilug_smoother* s, int which, int nsweeps, const double* x_in,
+                               const double* rhs, double* tmp, double* out, void* stream) {
+    return guarded([&] {
+        need(s && x_in && rhs && out && (tmp || nsweeps == 1));
+        const ilug::DeviceIlu* f = s->s.ilu();
+        if (which != 0 && which != 1) ilug::fail_invalid("sweeps_fused: which must be 0 (L) or 1 (U)");
+        if (!f || !(which ? f->wave_U() : f->wave_L()).ready())
+            ilug::fail_invalid("sweeps_fused: no wavefront plan (ILUG_WAVEFRONT)");
+        ilug::wave_sweeps(which ? f->Us() : f->Ls(), which ? f->wave_U() : f->wave_L(), nsweeps, x_in, rhs,
+                          nullptr, tmp, ilug::WaveLast::plain, nullptr, out, nullptr, S(stream));
         return ILUAMG_OK;
     });
 }

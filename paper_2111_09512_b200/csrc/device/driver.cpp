@@ -278,7 +278,7 @@ Report run_bench_trisolve(const Csr& A, const Config& cfg, const std::string& la
     dev.build(f, sc, UpperIteration::scaled, true, st);
     const i64 n = A.nrows;
     const Vec bh = random_uniform(n, seed);
-    DBuf<double> b, yl(n), yu(n), z(n), d(n), ws(3 * std::max<i64>(n, 1)), scr(1 + reduce_ws_doubles(n));
+    DBuf<double> b, yl(n), yu(n), z(n), d(n), ws(std::max<i64>(dev.sweep_ws(m_max) + n, 3)), scr(1 + reduce_ws_doubles(n));
     b.upload(bh.data(), n, st);
     dev.solve_lower(b.p, yl.p, st);
     dev.solve_upper(b.p, yu.p, ws.p, st);

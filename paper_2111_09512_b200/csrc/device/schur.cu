@@ -70,8 +70,9 @@ void DeviceSchur::build(const Csr& A, const SmootherConfig& cfg, cudaStream_t st
     sell_from_host(C_, s.C, Part::all, st);
     std::vector<i32> perm(s.perm.begin(), s.perm.end());
     perm_.upload(perm.data(), n_, st);
-    // ws: r(n) fg(n) t(ni) gt(nf) v1(nf) w(nf) tE(ni) tB(ni) upd(n) L/U sweep scratch 3*ni + ni
-    ws_.alloc(3 * n_ + 4 * ni_ + 3 * nf_ + 4 * ni_ + 8);
+    // ws: r(n) fg(n) t(ni) gt(nf) v1(nf) w(nf) tE(ni) tB(ni) upd(n) y(ni), then the L/U sweep scratch
+    const i64 sweep_ws = blocks_.sweep_ws(std::max(ts_.m_lower, ts_.m_upper)) + std::max<i64>(ni_, 1);
+    ws_.alloc(3 * n_ + 4 * ni_ + 3 * nf_ + ni_ + std::max<i64>(sweep_ws, 3 * ni_) + 8);
     red_.alloc(reduce_ws_doubles(std::max(n_, i64{1})));
     scal_.alloc(8);
     ILUG_CUDA(cudaStreamSynchronize(st));

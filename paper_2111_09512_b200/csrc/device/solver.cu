@@ -62,6 +62,10 @@ void DeviceIlu::build(const HostFactors& f, ScalingKind scaling, UpperIteration 
                          ": zero diagonal entry in U at row " + std::to_string(bad));
     }
     sell_from_device_csr(Us_, f.U, rp.p, ci.p, v.p, Part::strict_upper, {}, st);
+    if (wave_enabled(n_)) {
+        wave_build(wave_L_, f.L, Ls_, false, st);
+        wave_build(wave_U_, f.U, Us_, true, st);
+    }
     if (direct_plans) {
         lower_plan_.build(f.L, LevelPlan::Kind::lower_unit, st);
         upper_plan_.build(f.U, LevelPlan::Kind::upper, st, v.p);
@@ -69,9 +73,17 @@ void DeviceIlu::build(const HostFactors& f, ScalingKind scaling, UpperIteration 
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
+bool DeviceIlu::use_wave(bool upper, i64 m) const {
+    return m >= 3 && m <= kWaveMaxSweeps + 1 && (upper ? wave_U_ : wave_L_).ready();
+}
+
 void DeviceIlu::sweep_lower(const double* b, double* y, i64 m, double* ws, cudaStream_t st) const {
     if (m < 1) fail_invalid("richardson_lower: iteration count must be >= 1");
     if (m == 1) return vec_copy(y, b, n_, st);
+    if (use_wave(false, m) && y != b) {
+        return wave_sweeps(Ls_, wave_L_, static_cast<int>(m - 1), b, b, nullptr, ws, WaveLast::plain,
+                           nullptr, y, nullptr, st);
+    }
     const double* cur = b;
     for (i64 k = 2; k <= m; ++k) {
         double* out = k == m && y != b ? y : ws + (k % 2) * n_;
@@ -87,6 +99,10 @@ void DeviceIlu::sweep_upper(const double* b, double* x, i64 m, double* ws, cudaS
     if (upper_ == UpperIteration::jacobi) {
         // x1 = D^-1 b; x_{k+1} = D^-1 (b - N x_k)
         vec_div(bs, b, d_.p, n_, st);
+        if (use_wave(true, m)) {
+            return wave_sweeps(Us_, wave_U_, static_cast<int>(m - 1), bs, b, d_.p, ws + n_, WaveLast::div,
+                               d_.p, x, nullptr, st);
+        }
         const double* cur = bs;
         for (i64 k = 2; k <= m; ++k) {
             double* out = k == m ? x : ws + (1 + k % 2) * n_;
@@ -98,6 +114,10 @@ void DeviceIlu::sweep_upper(const double* b, double* x, i64 m, double* ws, cudaS
     }
     if (!has_rs()) fail_invalid("richardson_upper_scaled: factors carry no row scaling");
     vec_div(bs, b, rs_.p, n_, st); // b_s = b / row_scale (division, src/trisolve.cpp:113)
+    if (use_wave(true, m)) {
+        return wave_sweeps(Us_, wave_U_, static_cast<int>(m - 1), bs, bs, nullptr, ws + n_,
+                           has_cs() ? WaveLast::div : WaveLast::plain, has_cs() ? cs_.p : nullptr, x, nullptr, st);
+    }
     const double* cur = bs;
     for (i64 k = 2; k <= m; ++k) {
         double* out = k == m ? x : ws + (1 + k % 2) * n_;
@@ -221,7 +241,9 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         schur_->build(A, cfg, st);
         break;
     }
-    ws_.alloc(7 * std::max<i64>(n_, 1));
+    // r, y ping-pong, bs, x ping-pong, spare; then the wavefront intermediates
+    const i64 mmax = std::max(cfg.trisolve.m_lower, cfg.trisolve.m_upper);
+    ws_.alloc((7 + std::max<i64>(mmax - 2, 0)) * std::max<i64>(n_, 1));
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -261,8 +283,18 @@ void DeviceSmoother::ilu_sweep(const double* b, double* x, bool x_zero, cudaStre
     const double* dv = jac ? f.diag() : f.rs();
     // ---- L sweeps; the last one also produces x_1 of the U iteration (bs)
     const double* y = rr;
+    double* tmp = ws_.p + 7 * n; // wavefront intermediates (max(mL, mU) - 2 vectors)
     if (mL == 1) {
         vec_div(bs, rr, dv, n, st);
+    } else if (f.use_wave(false, mL)) {
+        // mL-1 fused sweeps; the last writes y (Jacobi form only) and x_1 = y / d
+        if (jac)
+            wave_sweeps(f.Ls(), f.wave_L(), static_cast<int>(mL - 1), rr, rr, nullptr, tmp, WaveLast::both, dv, ya,
+                        bs, st);
+        else
+            wave_sweeps(f.Ls(), f.wave_L(), static_cast<int>(mL - 1), rr, rr, nullptr, tmp, WaveLast::div, dv, bs,
+                        nullptr, st);
+        y = ya;
     } else {
         const double* cur = rr;
         for (i64 k = 2; k <= mL; ++k) {
@@ -287,6 +319,11 @@ void DeviceSmoother::ilu_sweep(const double* b, double* x, bool x_zero, cudaStre
             vec_acc_div(x, jac ? y : bs, post, n, st);
         else
             vec_acc(x, bs, n, st);
+        return;
+    }
+    if (f.use_wave(true, mU)) {
+        wave_sweeps(f.Us(), f.wave_U(), static_cast<int>(mU - 1), bs, rhs, jac ? f.diag() : nullptr, tmp,
+                    post ? WaveLast::acc_div : WaveLast::acc, post, x, nullptr, st);
         return;
     }
     const double* cur = bs;

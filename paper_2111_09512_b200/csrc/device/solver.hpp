@@ -12,6 +12,7 @@
 #include "../host/amg.hpp"
 #include "../host/schur.hpp"
 #include "../kernels/levelset.hpp"
+#include "../kernels/wavefront.hpp"
 
 #include <memory>
 
@@ -59,11 +60,20 @@ public:
     const Sell& Us() const { return Us_; }
     UpperIteration upper_iteration() const { return upper_; }
 
-    /// richardson_lower (src/trisolve.cpp:94-104): y = m sweeps from 0. ws: 2n doubles.
+    /// richardson_lower (src/trisolve.cpp:94-104): y = m sweeps from 0.
+    /// ws: sweep_ws(m) doubles.
     void sweep_lower(const double* b, double* y, i64 m, double* ws, cudaStream_t st) const;
     /// richardson_upper_scaled (src/trisolve.cpp:132-147) or its Jacobi form on the
-    /// unscaled factor: x = m sweeps from 0 (pre/post scaling included). ws: 3n.
+    /// unscaled factor: x = m sweeps from 0 (pre/post scaling included).
+    /// ws: sweep_ws(m) + n doubles.
     void sweep_upper(const double* b, double* x, i64 m, double* ws, cudaStream_t st) const;
+    /// Workspace (doubles) of sweep_lower with m sweeps; sweep_upper needs n more.
+    i64 sweep_ws(i64 m) const { return std::max<i64>(2, m) * n_; }
+    /// m sweeps of the U (upper) or L factor run as one wavefront launch
+    /// (m-1 fused sweeps after the first).
+    bool use_wave(bool upper, i64 m) const;
+    const WavePlan& wave_L() const { return wave_L_; }
+    const WavePlan& wave_U() const { return wave_U_; }
     /// Level-scheduled direct solves: solve_lower_direct and
     /// solve_upper_scaled_direct / solve_upper_direct (src/trisolve.cpp:20-55,149-156). ws: n.
     void solve_lower(const double* b, double* y, cudaStream_t st) const;
@@ -85,6 +95,7 @@ private:
     Sell Ls_, Us_;          // strict parts (Us_ scaled unless upper_ == jacobi)
     DBuf<double> rs_, cs_, d_;
     LevelPlan lower_plan_, upper_plan_;
+    WavePlan wave_L_, wave_U_; // fused multi-sweep plans (large n only, see wave_enabled)
     Csr U_pattern_;          // host structure of U (values are the unscaled ones)
 };
 

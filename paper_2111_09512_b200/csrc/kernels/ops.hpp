@@ -13,6 +13,8 @@ enum class Part { all, strict_lower, strict_upper };
 
 /// Upload a host CSR and pack the selected part into SELL-32 on the device.
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s);
+/// SELL-C-sigma sorting window in rows (ILUG_SELL_SIGMA, default 1024; <=1 = unsorted).
+i64 sell_sigma();
 
 /// Pack part of an already-uploaded CSR (device rp/ci/v; `pattern` is the host
 /// copy of its structure, used for the layout) into SELL-32. When

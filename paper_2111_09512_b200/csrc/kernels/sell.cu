@@ -283,6 +283,11 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
 } // namespace
 
 // --------------------------------------------------------------- builders
+i64 sell_sigma() {
+    const char* e = std::getenv("ILUG_SELL_SIGMA");
+    return e ? std::max<i64>(1, std::atoll(e)) : i64{1024};
+}
+
 namespace {
 
 // rowlen per SELL row and slice offsets; `len_of(row)` gives the part length.
@@ -347,10 +352,7 @@ i64 part_len(const Csr& A, i64 row, int pc) {
 // sigma comes from ILUG_SELL_SIGMA (default 1024; 1 disables).
 template <typename LenOf>
 std::vector<i32> sigma_order(i64 n, LenOf len_of) {
-    const i64 sigma = [] {
-        const char* e = std::getenv("ILUG_SELL_SIGMA");
-        return e ? std::max<i64>(1, std::atoll(e)) : i64{1024};
-    }();
+    const i64 sigma = sell_sigma();
     if (sigma <= 1 || n < 2 * kSlice) return {};
     const i64 pad = (n + kSlice - 1) / kSlice * kSlice;
     std::vector<i32> len(static_cast<size_t>(n));
