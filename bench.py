@@ -360,6 +360,9 @@ def time_to_solution(ilug, A, fallbacks=("poly_gs",)):
                                "krylov.form_iterates": "false", "smoother.fallback.kind": fb})
         for mode in ("richardson", "direct"):
             kv = dict(base, **{"trisolve.mode": mode})
+            # warm-up on a small matrix: lazy module loading of every kernel the
+            # solve uses happens here, not inside the timed solve below
+            ilug.run_solve(ilug.Matrix.generate("pressure27(24,24,24)"), ilug.Config().update(kv))
             rep = ilug.run_solve(A, ilug.Config().update(kv))
             res[mode] = {"iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
                          "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
