@@ -79,74 +79,104 @@ __global__ void k_sell_unpack(i64 nrows_pad, i64 nrows, const i32* __restrict__ 
 }
 
 // ------------------------------------------------------------ row products
-// Epilogues receive (row, s) with s the ascending-order row sum.
+// Epilogues receive (row, s) with s the ascending-order row sum. pre(row)
+// loads the row's vector operands. Read-modify-write epilogues (kEarly) have it
+// called BEFORE the row loop, so the output's read overlaps the streamed and
+// gathered loads instead of adding a dependent round trip at the end of every
+// thread (measured: U sweep with accumulate 668 -> see profiles); for plain
+// epilogues the early load measured slower (register pressure in the loop), so
+// it stays after the loop. The arithmetic is the same either way.
+struct None {};
 struct EpiStore {
+    static constexpr bool kEarly = false;
     double* y;
-    __device__ void operator()(i64 r, double s) const { y[r] = s; }
+    __device__ None pre(i64) const { return {}; }
+    __device__ void operator()(i64 r, double s, None) const { y[r] = s; }
 };
 struct EpiAdd {
+    static constexpr bool kEarly = true;
     double* acc;
-    __device__ void operator()(i64 r, double s) const { acc[r] = acc[r] + s; }
+    __device__ double pre(i64 r) const { return acc[r]; }
+    __device__ void operator()(i64 r, double s, double a) const { acc[r] = a + s; }
 };
 struct EpiResidual {
+    static constexpr bool kEarly = false;
     const double* b;
     double* r;
-    __device__ void operator()(i64 i, double s) const { r[i] = b[i] - s; }
+    __device__ double pre(i64 i) const { return __ldg(b + i); }
+    __device__ void operator()(i64 i, double s, double bi) const { r[i] = bi - s; }
 };
 struct EpiDiv {
+    static constexpr bool kEarly = false;
     const double* rhs;
     const double* d;
     double* out;
-    __device__ void operator()(i64 i, double s) const { out[i] = (rhs[i] - s) / d[i]; }
+    __device__ double2 pre(i64 i) const { return make_double2(__ldg(rhs + i), __ldg(d + i)); }
+    __device__ void operator()(i64 i, double s, double2 p) const { out[i] = (p.x - s) / p.y; }
 };
 struct EpiBoth {
+    static constexpr bool kEarly = false;
     const double* rhs;
     const double* d;
     double* out;
     double* out2;
-    __device__ void operator()(i64 i, double s) const {
-        const double t = rhs[i] - s;
+    __device__ double2 pre(i64 i) const { return make_double2(__ldg(rhs + i), __ldg(d + i)); }
+    __device__ void operator()(i64 i, double s, double2 p) const {
+        const double t = p.x - s;
         out[i] = t;
-        out2[i] = t / d[i];
+        out2[i] = t / p.y;
     }
 };
 struct EpiAcc {
+    static constexpr bool kEarly = true;
     const double* rhs;
     double* acc;
-    __device__ void operator()(i64 i, double s) const { acc[i] = acc[i] + (rhs[i] - s); }
+    __device__ double2 pre(i64 i) const { return make_double2(__ldg(rhs + i), acc[i]); }
+    __device__ void operator()(i64 i, double s, double2 p) const { acc[i] = p.y + (p.x - s); }
+};
+struct Pre3 {
+    double a, b, c;
 };
 struct EpiAccDiv {
+    static constexpr bool kEarly = true;
     const double* rhs;
     const double* d;
     double* acc;
-    __device__ void operator()(i64 i, double s) const { acc[i] = acc[i] + (rhs[i] - s) / d[i]; }
+    __device__ Pre3 pre(i64 i) const { return {__ldg(rhs + i), __ldg(d + i), acc[i]}; }
+    __device__ void operator()(i64 i, double s, Pre3 p) const { acc[i] = p.c + (p.a - s) / p.b; }
 };
 struct EpiScaleAcc { // jacobi_like_sweep out of place: out = x + invd * (b - Ax)
+    static constexpr bool kEarly = false;
     const double* rhs;
     const double* sc;
     const double* xin;
     double* out;
-    __device__ void operator()(i64 i, double s) const { out[i] = xin[i] + sc[i] * (rhs[i] - s); }
+    __device__ Pre3 pre(i64 i) const { return {__ldg(rhs + i), __ldg(sc + i), __ldg(xin + i)}; }
+    __device__ void operator()(i64 i, double s, Pre3 p) const { out[i] = p.c + p.b * (p.a - s); }
 };
 struct EpiScaleInit { // poly_gs: term = invd * r; acc = term
+    static constexpr bool kEarly = false;
     const double* rhs;
     const double* sc;
     double* term;
     double* acc;
-    __device__ void operator()(i64 i, double s) const {
-        const double t = sc[i] * (rhs[i] - s);
+    __device__ double2 pre(i64 i) const { return make_double2(__ldg(rhs + i), __ldg(sc + i)); }
+    __device__ void operator()(i64 i, double s, double2 p) const {
+        const double t = p.y * (p.x - s);
         term[i] = t;
         acc[i] = t;
     }
 };
 struct EpiNegScaleAcc { // poly_gs: term = -invd * t; acc += term
+    static constexpr bool kEarly = true;
     const double* sc;
     double* term;
     double* acc;
-    __device__ void operator()(i64 i, double s) const {
-        const double t = -sc[i] * s;
+    __device__ double2 pre(i64 i) const { return make_double2(__ldg(sc + i), acc[i]); }
+    __device__ void operator()(i64 i, double s, double2 p) const {
+        const double t = -p.x * s;
         term[i] = t;
-        acc[i] = acc[i] + t;
+        acc[i] = p.y + t;
     }
 };
 
@@ -160,6 +190,8 @@ __global__ void __launch_bounds__(kBlock) k_rowdot8(SellView M, i64 nrows, const
     if (p >= M.nrows_pad) return;
     const i64 row = M.perm ? M.perm[p] : p;
     if (row < 0 || row >= nrows) return;
+    decltype(epi.pre(row)) pr{};
+    if constexpr (Epi::kEarly) pr = epi.pre(row); // issued before the row loop
     const int len = M.rowlen[p];
     const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
     const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
@@ -181,7 +213,8 @@ __global__ void __launch_bounds__(kBlock) k_rowdot8(SellView M, i64 nrows, const
         for (int u = 0; u < 8; ++u)
             if (t + u < len) s = s + a[u] * xv[u];
     }
-    epi(row, s);
+    if constexpr (!Epi::kEarly) pr = epi.pre(row);
+    epi(row, s, pr);
 }
 
 // Distributed form: columns < nloc gather from the local vector, columns >= nloc
@@ -194,6 +227,8 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
     if (p >= M.nrows_pad) return;
     const i64 row = M.perm ? M.perm[p] : p;
     if (row < 0 || row >= nrows) return;
+    decltype(epi.pre(row)) pr{};
+    if constexpr (Epi::kEarly) pr = epi.pre(row); // issued before the row loop
     const int len = M.rowlen[p];
     const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
     const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
@@ -216,7 +251,8 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
         const int c = ld_stream(cp + t * kSlice);
         s = s + ld_stream(vp + t * kSlice) * (c < nloc ? ld_gather(x + c) : ld_gather(halo + (c - nloc)));
     }
-    epi(row, s);
+    if constexpr (!Epi::kEarly) pr = epi.pre(row);
+    epi(row, s, pr);
 }
 
 template <class Epi, bool HINT>
@@ -226,6 +262,8 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
     if (p >= M.nrows_pad) return;
     const i64 row = M.perm ? M.perm[p] : p;
     if (row < 0 || row >= nrows) return;
+    decltype(epi.pre(row)) pr{};
+    if constexpr (Epi::kEarly) pr = epi.pre(row); // issued before the row loop
     const int len = M.rowlen[p];
     const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
     const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
@@ -253,12 +291,17 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
         for (int u = 0; u < 4; ++u) s = s + a[u] * xv[u];
     }
     for (; t < len; ++t) s = s + lv(t) * lx(lc(t));
-    epi(row, s);
+    if constexpr (!Epi::kEarly) pr = epi.pre(row);
+    epi(row, s, pr);
 }
 
 // Kernel variant knobs for A/B experiments (tools/probe_sweep.py):
 // ILUG_L2_HINTS=1 enables the L2 eviction-priority hints (measured neutral on
 // B200 at C2, so off by default); ILUG_ROWDOT=4|8 picks the batch width.
+// Also measured and dropped (tools/probe_step.py, same-process A/B at C2):
+// programmatic dependent launch with the first four values/columns of a row
+// loaded before griddepcontrol.wait — U sweep 665 vs 608 us (the peeled head
+// and the tighter register budget cost more than the tail overlap gains).
 bool l2_hints() {
     const char* e = std::getenv("ILUG_L2_HINTS");
     return e && e[0] == '1';
