@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
     epi(row, s, pr);
 }
 
-template <class Epi, bool HINT>
+template <class Epi, bool HINT, bool PTAIL = true>
 __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
                                                     Epi epi) {
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
@@ -290,7 +290,28 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
 #pragma unroll
         for (int u = 0; u < 4; ++u) s = s + a[u] * xv[u];
     }
-    for (; t < len; ++t) s = s + lv(t) * lx(lc(t));
+    if constexpr (PTAIL) {
+        // the last len % 4 entries as one predicated batch: their loads are in
+        // flight together instead of one dependent round trip per entry
+        if (t < len) {
+            double a[3], xv[3];
+            int c[3];
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (t + u < len) {
+                    a[u] = lv(t + u);
+                    c[u] = lc(t + u);
+                }
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (t + u < len) xv[u] = lx(c[u]);
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (t + u < len) s = s + a[u] * xv[u];
+        }
+    } else {
+        for (; t < len; ++t) s = s + lv(t) * lx(lc(t));
+    }
     if constexpr (!Epi::kEarly) pr = epi.pre(row);
     epi(row, s, pr);
 }
@@ -306,6 +327,10 @@ bool l2_hints() {
     const char* e = std::getenv("ILUG_L2_HINTS");
     return e && e[0] == '1';
 }
+bool serial_tail() { // ILUG_TAIL=serial: the row tail one entry at a time (A/B)
+    const char* e = std::getenv("ILUG_TAIL");
+    return e && e[0] == 's';
+}
 int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy)
     const char* e = std::getenv("ILUG_ROWDOT");
     return e && e[0] == '8' ? 8 : 4;
@@ -318,6 +343,8 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         k_rowdot8<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else if (l2_hints())
         k_rowdot<Epi, true><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (serial_tail())
+        k_rowdot<Epi, false, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     ILUG_LAUNCH_CHECK();
