@@ -118,6 +118,14 @@ ILUAMG_API int ilug_ilu_smooth_sweep(const ilug_smoother* s, const double* b, do
 /* Host-buffer smoother application (copy b, x in; smooth; copy x out; synchronous):
  * the end-to-end form of ilug_smooth used for e2e timing. */
 ILUAMG_API int ilug_smooth_host(const ilug_smoother* s, const double* b_host, double* x_host);
+/* count independent smoother applications x_i <- smooth(A, b_i, x_i) on host
+ * buffers, pipelined: the copy-in of step i+1 and the copy-out of step i-1 run
+ * on their own streams while step i smooths (two device slots). Pinned host
+ * memory gives true overlap. Pairs may repeat only two or more positions
+ * apart (slot reuse is ordered; adjacent steps are in flight together).
+ * Returns after the last copy-out. */
+ILUAMG_API int ilug_smooth_host_many(const ilug_smoother* s, long long count, const double* const* b_host,
+                                     double* const* x_host);
 /* Sizes for byte accounting: n, nnz(A), nnz(strict L), nnz(strict U) (ILU kinds; 0 otherwise),
  * SELL padded entries of strict U. */
 ILUAMG_API int ilug_smoother_stats(const ilug_smoother* s, long long* n, long long* nnz_A,
@@ -204,6 +212,10 @@ ILUAMG_API int ilug_dist_smoother_stats(const ilug_dist_smoother* s, long long* 
                                         long long* nnz_Ls, long long* nnz_Us);
 /* Host-buffer application (copy this rank's b, x in; smooth; copy x out; synchronous). */
 ILUAMG_API int ilug_dist_smooth_host(const ilug_dist_smoother* s, const double* b_host, double* x_host);
+/* Pipelined multi-step form of ilug_dist_smooth_host (see ilug_smooth_host_many);
+ * collective: every rank calls it with the same count. */
+ILUAMG_API int ilug_dist_smooth_host_many(const ilug_dist_smoother* s, long long count,
+                                          const double* const* b_host, double* const* x_host);
 /* One bare L (which = 0) or U (which = 1) sweep kernel of the local factors, for kernel timing. */
 ILUAMG_API int ilug_dist_smoother_sweep_once(const ilug_dist_smoother* s, int which, const double* x_in,
                                              const double* rhs, double* out, void* stream);

@@ -76,6 +76,7 @@ _SIGS = {
     "ilug_smoother_create": (_i, [_vp, _vp, _i, _pvp]), "ilug_smooth": (_i, [_vp, _vp, _vp, _pd, _vp]),
     "ilug_ilu_smooth_sweep": (_i, [_vp, _vp, _vp, _vp]), "ilug_smoother_free": (None, [_vp]),
     "ilug_smooth_host": (_i, [_vp, _pd, _pd]),
+    "ilug_smooth_host_many": (_i, [_vp, _ll, _pvp, _pvp]),
     "ilug_smoother_stats": (_i, [_vp, _pll, _pll, _pll, _pll, _pll]),
     "ilug_smoother_wave": (_i, [_vp, _pll, _pll, _pi, _pll]),
     "ilug_smoother_sweeps_fused": (_i, [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]),
@@ -105,6 +106,7 @@ _SIGS = {
     "ilug_dist_smoother_stats": (_i, [_vp, _pll, _pll, _pll, _pll]),
     "ilug_dist_smoother_free": (None, [_vp]),
     "ilug_dist_smooth_host": (_i, [_vp, _pd, _pd]),
+    "ilug_dist_smooth_host_many": (_i, [_vp, _ll, _pvp, _pvp]),
     "ilug_dist_smoother_sweep_once": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
     "ilug_dist_solver_create": (_i, [_vp, _vp, _vp, _pvp]),
     "ilug_dist_gmres": (_i, [_vp, _vp, _vp, _vp, _pll, _pd, _vp]),
@@ -142,6 +144,19 @@ def _ptr(a) -> Optional[int]:
     if hasattr(a, "data_ptr"):
         return a.data_ptr()
     raise TypeError(f"cannot take a device pointer of {type(a)!r}")
+
+
+def _host_ptrs(arrs):
+    """void*[] of host float64 arrays (numpy arrays or CPU torch tensors)."""
+    ptrs = (C.c_void_p * max(len(arrs), 1))()
+    for i, a in enumerate(arrs):
+        if hasattr(a, "data_ptr"):
+            ptrs[i] = a.data_ptr()
+        else:
+            if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+                raise TypeError("host arrays must be contiguous float64")
+            ptrs[i] = a.ctypes.data
+    return ptrs
 
 
 def _stream(s) -> Optional[int]:
@@ -437,6 +452,11 @@ class Smoother:
 
     def ilu_sweep(self, b, x, stream=None):
         _check(lib.ilug_ilu_smooth_sweep(self.h, _ptr(b), _ptr(x), _stream(stream)))
+
+    def smooth_host_many(self, bs, xs):
+        """Pipelined x_i <- smooth(A, b_i, x_i) over host arrays (numpy or CPU
+        tensors; pinned memory overlaps the copies), ilug_smooth_host_many."""
+        _check(lib.ilug_smooth_host_many(self.h, len(bs), _host_ptrs(bs), _host_ptrs(xs)))
 
     def wave(self):
         """Wavefront plan tile counts and the stalled flag (see ilug_smoother_wave)."""

@@ -1,46 +1,13 @@
 // The C ABI: iluamg_* (drop-in for the reference's include/iluamg.h, mirroring
 // src/capi.cpp's handle/status/last-error conventions) and ilug_* (device
 // handles for the individual hot-path subsystems). No exception crosses it.
-#include "../../../include/ilug.h"
+#include "capi_handles.hpp"
 #include "../host/problems.hpp"
-#include "driver.hpp"
 
 #include <cmath>
 #include <exception>
 #include <functional>
 #include <string>
-
-struct iluamg_matrix_s {
-    ilug::Csr A;
-    std::string label;
-};
-struct iluamg_config_s {
-    ilug::Config cfg;
-};
-struct iluamg_report_s {
-    ilug::Report rep;
-    std::string json, text;
-    std::vector<std::string> csv;
-};
-struct ilug_factors_s {
-    ilug::DeviceIlu f;
-    long long nnz_L = 0, nnz_U = 0;
-};
-struct ilug_dmatrix_s {
-    ilug::DeviceMatrix M;
-};
-struct ilug_smoother_s {
-    ilug::Csr A;
-    ilug::DeviceMatrix dA;
-    ilug::DeviceSmoother s;
-    ilug::DBuf<double> r, scratch;
-    mutable ilug::DBuf<double> hb, hx; // staging for the host-buffer entry point
-};
-struct ilug_hierarchy_s {
-    ilug::HostHierarchy h;
-    ilug::DeviceHierarchy d;
-    bool on_device = false;
-};
 
 namespace {
 
@@ -533,6 +500,14 @@ int ilug_smooth_host(const ilug_smoother* s, const double* bh, double* xh) {
         return ILUAMG_OK;
     });
 }
+int ilug_smooth_host_many(const ilug_smoother* s, long long count, const double* const* bh, double* const* xh) {
+    return guarded([&] {
+        need(s && count >= 0 && (count == 0 || (bh && xh)));
+        s->pipe.run(s->A.nrows, count, bh, xh,
+                    [&](const double* b, double* x, cudaStream_t st) { s->s.smooth(b, x, false, st); });
+        return ILUAMG_OK;
+    });
+}
 int ilug_smoother_stats(const ilug_smoother* s, long long* n, long long* nnz_A, long long* nl,
                         long long* nu, long long* padded) {
     return guarded([&] {
@@ -679,20 +654,6 @@ int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, dou
 } // extern "C"
 
 // ============================================================ ilug_dist_* (multi-GPU)
-#include "dist.hpp"
-
-struct ilug_dist_plan_s {
-    ilug::HaloPlan plan;
-};
-struct ilug_dist_comm_s {
-    std::unique_ptr<ilug::DistComm> c;
-};
-struct ilug_dist_smoother_s { // same layout as in capi_dist.cpp
-    ilug::DistSmoother s;
-    long long nnz_A = 0;
-    mutable ilug::DBuf<double> hb, hx; // staging for ilug_dist_smooth_host
-};
-
 extern "C" {
 
 int ilug_dist_partition(long long n, int nranks, long long* starts) {

@@ -1,31 +1,7 @@
-// C ABI of the distributed GMRES+AMG solver (ilug_dist_solver_*). The plan
-// and communicator handles are defined in capi.cpp; their layouts are
-// repeated here through the shared header-free structs below.
-#include "../../../include/ilug.h"
-#include "../host/config.hpp"
-#include "dist.hpp"
-
-#include <memory>
-#include <string>
-
-// Same definitions as capi.cpp (one ODR-identical definition per TU).
-struct iluamg_config_s {
-    ilug::Config cfg;
-};
-struct ilug_dist_plan_s {
-    ilug::HaloPlan plan;
-};
-struct ilug_dist_comm_s {
-    std::unique_ptr<ilug::DistComm> c;
-};
-struct ilug_dist_solver_s {
-    ilug::DistSolver s;
-};
-struct ilug_dist_smoother_s {
-    ilug::DistSmoother s;
-    long long nnz_A = 0;
-    mutable ilug::DBuf<double> hb, hx; // staging for ilug_dist_smooth_host
-};
+// C ABI of the distributed GMRES+AMG solver (ilug_dist_solver_*) and the
+// pipelined host-buffer entry of the distributed smoother. Handle layouts:
+// capi_handles.hpp (shared with capi.cpp).
+#include "capi_handles.hpp"
 
 namespace ilug {
 int capi_guarded(const std::function<int()>& fn); // capi.cpp: exception -> status + last error
@@ -83,6 +59,16 @@ int ilug_dist_smooth_host(const ilug_dist_smoother* s, const double* bh, double*
         s->s.smooth(s->hb.p, s->hx.p, nullptr);
         s->hx.download(xh);
         ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_dist_smooth_host_many(const ilug_dist_smoother* s, long long count, const double* const* bh,
+                               double* const* xh) {
+    return ilug::capi_guarded([&] {
+        if (!s || count < 0 || (count > 0 && (!bh || !xh))) ilug::fail_invalid("null argument");
+        s->pipe.run(s->s.nloc(), count, bh, xh,
+                    [&](const double* b, double* x, cudaStream_t st) { s->s.smooth(b, x, st); });
         return ILUAMG_OK;
     });
 }

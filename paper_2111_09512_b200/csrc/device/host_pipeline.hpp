@@ -1,0 +1,70 @@
+// Streaming host-buffer pipeline behind ilug_smooth_host_many /
+// ilug_dist_smooth_host_many: copy-in, compute and copy-out of consecutive
+// independent steps on three streams with two device slots, so step i's
+// smoothing overlaps step i+1's H2D and step i-1's D2H (PCIe is full duplex).
+#pragma once
+
+#include "../kernels/dev.cuh"
+
+namespace ilug {
+
+struct HostPipeline {
+    cudaStream_t in = nullptr, run_st = nullptr, out = nullptr;
+    cudaEvent_t loaded[2] = {}, computed[2] = {}, drained[2] = {};
+    DBuf<double> b[2], x[2];
+
+    HostPipeline() = default;
+    HostPipeline(const HostPipeline&) = delete;
+    HostPipeline& operator=(const HostPipeline&) = delete;
+    ~HostPipeline() {
+        if (!in) return;
+        cudaStreamSynchronize(in), cudaStreamSynchronize(run_st), cudaStreamSynchronize(out);
+        for (int k = 0; k < 2; ++k)
+            cudaEventDestroy(loaded[k]), cudaEventDestroy(computed[k]), cudaEventDestroy(drained[k]);
+        cudaStreamDestroy(in), cudaStreamDestroy(run_st), cudaStreamDestroy(out);
+    }
+
+    /// step(b_dev, x_dev, stream) applies one step in place on x_dev.
+    /// Pairs (bh[i], xh[i]) may repeat only two or more positions apart.
+    template <class Step>
+    void run(i64 n, long long count, const double* const* bh, double* const* xh, Step&& step) {
+        ensure(n);
+        const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+        for (long long i = 0; i < count; ++i) {
+            if (!bh[i] || !xh[i]) fail_invalid("smooth_host_many: null host buffer");
+            const int k = static_cast<int>(i & 1);
+            // slot k is free once step i-2 is copied out (which follows its compute)
+            if (i >= 2) ILUG_CUDA(cudaStreamWaitEvent(in, drained[k], 0));
+            ILUG_CUDA(cudaMemcpyAsync(b[k].p, bh[i], bytes, cudaMemcpyHostToDevice, in));
+            ILUG_CUDA(cudaMemcpyAsync(x[k].p, xh[i], bytes, cudaMemcpyHostToDevice, in));
+            ILUG_CUDA(cudaEventRecord(loaded[k], in));
+            ILUG_CUDA(cudaStreamWaitEvent(run_st, loaded[k], 0));
+            step(b[k].p, x[k].p, run_st);
+            ILUG_CUDA(cudaEventRecord(computed[k], run_st));
+            ILUG_CUDA(cudaStreamWaitEvent(out, computed[k], 0));
+            ILUG_CUDA(cudaMemcpyAsync(xh[i], x[k].p, bytes, cudaMemcpyDeviceToHost, out));
+            ILUG_CUDA(cudaEventRecord(drained[k], out));
+        }
+        ILUG_CUDA(cudaStreamSynchronize(out));
+        ILUG_CUDA(cudaStreamSynchronize(run_st));
+        ILUG_CUDA(cudaStreamSynchronize(in));
+    }
+
+private:
+    void ensure(i64 n) {
+        if (!in) {
+            ILUG_CUDA(cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking));
+            ILUG_CUDA(cudaStreamCreateWithFlags(&run_st, cudaStreamNonBlocking));
+            ILUG_CUDA(cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) {
+                ILUG_CUDA(cudaEventCreateWithFlags(&loaded[k], cudaEventDisableTiming));
+                ILUG_CUDA(cudaEventCreateWithFlags(&computed[k], cudaEventDisableTiming));
+                ILUG_CUDA(cudaEventCreateWithFlags(&drained[k], cudaEventDisableTiming));
+            }
+        }
+        for (int k = 0; k < 2; ++k)
+            if (b[k].n != n) b[k].alloc(n), x[k].alloc(n);
+    }
+};
+
+} // namespace ilug

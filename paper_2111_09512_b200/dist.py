@@ -12,7 +12,7 @@ from typing import Callable, List
 
 import numpy as np
 
-from . import Config, IlugError, Matrix, _as, _check, _ptr, _stream, lib
+from . import Config, IlugError, Matrix, _as, _check, _host_ptrs, _ptr, _stream, lib
 
 
 def _prefer_torch_nccl() -> None:
@@ -134,6 +134,10 @@ class Smoother:
 
     def residual(self, x, b, r, stream=None):
         _check(lib.ilug_dist_residual(self.h, _ptr(x), _ptr(b), _ptr(r), _stream(stream)))
+
+    def smooth_host_many(self, bs, xs):
+        """Pipelined host-buffer smoothing (ilug_dist_smooth_host_many); collective."""
+        _check(lib.ilug_dist_smooth_host_many(self.h, len(bs), _host_ptrs(bs), _host_ptrs(xs)))
 
     def stats(self):
         v = [C.c_longlong() for _ in range(4)]

@@ -82,3 +82,24 @@ def test_dist_plan_two_virtual_ranks_structure(ilug):
     plans[1].set_sends(0, need01)
     plans[0].set_sends(1, need10)
     assert np.array_equal(plans[1].sends(0) + starts[1], need01)
+
+
+def test_dist_smooth_host_many_single_rank(ilug, torch_cuda):
+    """ilug_dist_smooth_host_many at one rank = the single-GPU smoother applied
+    to each host pair, bitwise."""
+    idist, A, plan, comm = _setup(ilug, "pressure27(14,14,14)")
+    cfg = ilug.Config().update(KV)
+    Sd = idist.Smoother(plan, comm, cfg)
+    S = ilug.Smoother(A, cfg)
+    rng = np.random.default_rng(8)
+    bs = [rng.uniform(-1, 1, A.rows) for _ in range(3)]
+    xs = [rng.uniform(-1, 1, A.rows) for _ in range(3)]
+    want = []
+    for b, x in zip(bs, xs):
+        xd = torch_cuda.from_numpy(x.copy()).cuda()
+        S.smooth(torch_cuda.from_numpy(b).cuda(), xd)
+        torch_cuda.cuda.synchronize()
+        want.append(xd.cpu().numpy())
+    Sd.smooth_host_many(bs, xs)
+    for got, w in zip(xs, want):
+        assert bitwise(got, w)

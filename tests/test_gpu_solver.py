@@ -154,3 +154,26 @@ def test_bench_trisolve_report(ilug, torch_cuda):
     rows = {(r["factor"], int(r["m"])): float(r["err_direct_rel"]) for r in rep.table_rows("bench")}
     assert rows[("U", 20)] < 2e-5 and rows[("U", 40)] < 1e-10
     assert rows[("L", 40)] < 1e-10
+
+
+def test_smooth_host_many_pipeline(ilug, torch_cuda):
+    """ilug_smooth_host_many (three streams, two device slots) = sequential
+    device smoothing of each pair, bitwise; a pair repeated two positions
+    apart sees its own previous output (slot reuse is ordered)."""
+    import numpy as np
+    from conftest import bitwise
+    A = ilug.Matrix.generate("poisson3d(24,22,20)")
+    S = ilug.Smoother(A, ilug.Config().update({"smoother.kind": "ilu", "trisolve.m_lower": 5,
+                                               "trisolve.m_upper": 5}))
+    rng = np.random.default_rng(9)
+    pairs = [(torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).pin_memory(),
+              torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).pin_memory()) for _ in range(3)]
+    order = [0, 1, 2, 0, 1, 0]  # repeats >= 2 positions apart
+    want = {k: (b.cuda(), x.cuda()) for k, (b, x) in enumerate(pairs)}
+    for k in order:
+        S.smooth(want[k][0], want[k][1])
+    torch_cuda.cuda.synchronize()
+    S.smooth_host_many([pairs[k][0] for k in order], [pairs[k][1] for k in order])
+    for k, (b, x) in enumerate(pairs):
+        assert bitwise(x.numpy(), want[k][1].cpu().numpy()), k
+    S.smooth_host_many([], [])  # empty batch is a no-op
