@@ -1,6 +1,9 @@
 #include "csr.hpp"
 
 #include <atomic>
+#include <condition_variable>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -19,6 +22,83 @@ int host_threads() {
     return n;
 }
 
+namespace {
+
+// Persistent worker pool behind parallel_ranges: setup routines call it
+// thousands of times (ILU(0) once per DAG level), so spawning threads per call
+// cost more than the work. Workers sleep on a generation counter; the caller
+// runs chunk 0 itself. A call from inside a worker, or while another host
+// thread holds the pool, falls back to fresh threads (never deadlocks).
+class Pool {
+public:
+    explicit Pool(int workers) {
+        for (int w = 0; w < workers; ++w) std::thread([this, w] { loop(w + 1); }).detach();
+    }
+    bool try_run(i64 n, int T, const std::function<void(i64, i64, int)>& fn) {
+        if (in_worker) return false;
+        std::unique_lock<std::mutex> own(busy_, std::try_to_lock);
+        if (!own.owns_lock()) return false;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            fn_ = &fn;
+            n_ = n;
+            T_ = T;
+            err_ = nullptr;
+            pending_ = T - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        run_chunk(0);
+        std::unique_lock<std::mutex> g(mu_);
+        done_.wait(g, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+        if (err_) std::rethrow_exception(err_);
+        return true;
+    }
+
+private:
+    void run_chunk(int t) {
+        const i64 b = n_ * t / T_, e = n_ * (t + 1) / T_;
+        try {
+            (*fn_)(b, e, t);
+        } catch (...) {
+            std::lock_guard<std::mutex> g(mu_);
+            if (!err_) err_ = std::current_exception();
+        }
+    }
+    void loop(int id) {
+        in_worker = true;
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (id >= T_) continue; // not needed for this call
+            }
+            run_chunk(id);
+            std::lock_guard<std::mutex> g(mu_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    static thread_local bool in_worker;
+    std::mutex busy_, mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(i64, i64, int)>* fn_ = nullptr;
+    i64 n_ = 0;
+    int T_ = 1, pending_ = 0;
+    unsigned long long gen_ = 0;
+    std::exception_ptr err_;
+};
+thread_local bool Pool::in_worker = false;
+
+Pool& pool() {
+    static Pool* p = new Pool(host_threads() - 1); // intentionally leaked: workers live for the process
+    return *p;
+}
+
+} // namespace
+
 void parallel_ranges(i64 n, const std::function<void(i64, i64, int)>& fn, i64 grain) {
     if (n <= 0) return;
     const int T = static_cast<int>(std::min<i64>(host_threads(), std::max<i64>(1, n / grain)));
@@ -26,12 +106,13 @@ void parallel_ranges(i64 n, const std::function<void(i64, i64, int)>& fn, i64 gr
         fn(0, n, 0);
         return;
     }
-    std::vector<std::thread> pool;
+    if (pool().try_run(n, T, fn)) return;
+    std::vector<std::thread> threads;
     std::exception_ptr err;
     std::mutex mu;
     for (int t = 0; t < T; ++t) {
         const i64 b = n * t / T, e = n * (t + 1) / T;
-        pool.emplace_back([&, b, e, t] {
+        threads.emplace_back([&, b, e, t] {
             try {
                 fn(b, e, t);
             } catch (...) {
@@ -40,7 +121,7 @@ void parallel_ranges(i64 n, const std::function<void(i64, i64, int)>& fn, i64 gr
             }
         });
     }
-    for (auto& th : pool) th.join();
+    for (auto& th : threads) th.join();
     if (err) std::rethrow_exception(err);
 }
 

@@ -62,23 +62,30 @@ HostFactors ilu0(const Csr& A, PivotPatch patch) {
 
     std::vector<double> w(A.v);
     std::atomic<i64> first_zero{n};
+    // per-worker column -> position-in-row markers (-1 = not in row i's pattern)
+    std::vector<std::vector<i32>> marks(static_cast<size_t>(host_threads()));
     for (i32 l = 0; l < nlev; ++l) {
-        parallel_ranges(lstart[l + 1] - lstart[l], [&](i64 b, i64 e, int) {
+        parallel_ranges(lstart[l + 1] - lstart[l], [&](i64 b, i64 e, int tid) {
+            std::vector<i32>& pos = marks[static_cast<size_t>(tid)];
+            if (pos.empty()) pos.assign(static_cast<size_t>(n), -1);
             for (i64 t = lstart[l] + b; t < lstart[l] + e; ++t) {
                 const i64 i = order[t];
-                const i64 end = A.rp[i + 1];
-                for (i64 k = A.rp[i]; k < dpos[i]; ++k) {
+                const i64 beg = A.rp[i], end = A.rp[i + 1];
+                for (i64 p = beg; p < end; ++p) pos[A.ci[p]] = static_cast<i32>(p - beg);
+                for (i64 k = beg; k < dpos[i]; ++k) {
                     const i64 c = A.ci[k];
                     const double m = w[k] / w[dpos[c]];
                     w[k] = m;
-                    // merge row c's strict upper part against row i's tail
-                    i64 p = k + 1;
-                    for (i64 kk = dpos[c] + 1; kk < A.rp[c + 1] && p < end; ++kk) {
-                        const i32 j = A.ci[kk];
-                        while (p < end && A.ci[p] < j) ++p;
-                        if (p < end && A.ci[p] == j) w[p] -= m * w[kk];
+                    // row c's strict upper part against row i's pattern; every
+                    // match lies after k (its column exceeds c), and each w[p]
+                    // receives its updates in ascending k, then ascending column:
+                    // the order of the reference's merge (src/ilu.cpp)
+                    for (i64 kk = dpos[c] + 1; kk < A.rp[c + 1]; ++kk) {
+                        const i32 q = pos[A.ci[kk]];
+                        if (q >= 0) w[beg + q] -= m * w[kk];
                     }
                 }
+                for (i64 p = beg; p < end; ++p) pos[A.ci[p]] = -1;
                 if (w[dpos[i]] == 0.0) {
                     if (patch == PivotPatch::error) {
                         i64 cur = first_zero.load();
