@@ -53,6 +53,11 @@ ILUAMG_API int ilug_matrix_copy_csr(const iluamg_matrix* A, long long* row_start
 /* ILU(0)/ILUT per the config's ilu.* keys (src/ilu.cpp:56-265): L strict, U with diagonal. */
 ILUAMG_API int ilug_ilu_factorize(const iluamg_matrix* A, const iluamg_config* cfg,
                                   iluamg_matrix** L, iluamg_matrix** U);
+/* The factorisation the device objects use: ILU(0) on the device (level-free,
+ * dependency-flag scheduled; bitwise equal to ilug_ilu_factorize), ILUT on the
+ * host. ILUG_ILU0_DEVICE=0 forces the host path. */
+ILUAMG_API int ilug_ilu_factorize_device(const iluamg_matrix* A, const iluamg_config* cfg,
+                                         iluamg_matrix** L, iluamg_matrix** U);
 
 /* ---- K1-K5: factors ---- */
 /* Host ILU per the config's ilu.* keys, then upload + K1 scaling per `scaling`

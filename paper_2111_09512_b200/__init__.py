@@ -61,6 +61,7 @@ _SIGS = {
     "ilug_matrix_from_csr": (_i, [_ll, _ll, _pll, _pll, _pd, _pvp]),
     "ilug_matrix_copy_csr": (_i, [_vp, _pll, _pll, _pd]),
     "ilug_ilu_factorize": (_i, [_vp, _vp, _pvp, _pvp]),
+    "ilug_ilu_factorize_device": (_i, [_vp, _vp, _pvp, _pvp]),
     "ilug_factors_create": (_i, [_vp, _vp, _i, _i, _i, _pvp]),
     "ilug_factors_from_csr": (_i, [_ll, _pll, _pll, _pd, _pll, _pll, _pd, _i, _i, _i, _pvp]),
     "ilug_factors_rows": (_ll, [_vp]), "ilug_factors_nnz": (_i, [_vp, _pll, _pll]),
@@ -334,6 +335,13 @@ def ilu_factorize(A: Matrix, cfg: Config):
     """Host ILU(0)/ILUT -> (L strict, U with diagonal) as Matrix handles."""
     L, U = C.c_void_p(), C.c_void_p()
     _check(lib.ilug_ilu_factorize(A.h, cfg.h, C.byref(L), C.byref(U)))
+    return Matrix(L.value), Matrix(U.value)
+
+
+def ilu_factorize_device(A: Matrix, cfg: Config):
+    """The device objects' factorisation: ILU(0) on the GPU, ILUT on the host."""
+    L, U = C.c_void_p(), C.c_void_p()
+    _check(lib.ilug_ilu_factorize_device(A.h, cfg.h, C.byref(L), C.byref(U)))
     return Matrix(L.value), Matrix(U.value)
 
 

@@ -120,7 +120,7 @@ Striping striping(const Csr& L, const Csr& U, double threshold) {
 Report run_analyze(const Csr& A, const Config& cfg, const std::string& label) {
     const auto t0 = std::chrono::steady_clock::now();
     const IluParams ip = ilu_params_from(cfg);
-    const HostFactors f = ilu_factorize(A, ip);
+    const HostFactors f = factorize(A, ip, nullptr);
     const double factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     DeviceContext ctx(cfg);
     cudaStream_t st = ctx.stream;

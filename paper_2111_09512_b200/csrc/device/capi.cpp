@@ -266,7 +266,7 @@ int ilug_factors_create(const iluamg_matrix* A, const iluamg_config* cfg, int sc
                         int direct, ilug_factors** out) {
     return guarded([&] {
         need(A && cfg && out);
-        return make_factors(ilug::ilu_factorize(A->A, ilug::ilu_params_from(cfg->cfg)), scaling, upper,
+        return make_factors(ilug::factorize(A->A, ilug::ilu_params_from(cfg->cfg), nullptr), scaling, upper,
                             direct, out);
     });
 }
@@ -589,6 +589,16 @@ int ilug_ilu_factorize(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_
     return guarded([&] {
         need(A && cfg && L && U);
         ilug::HostFactors f = ilug::ilu_factorize(A->A, ilug::ilu_params_from(cfg->cfg));
+        *L = new iluamg_matrix_s{std::move(f.L), "L"};
+        *U = new iluamg_matrix_s{std::move(f.U), "U"};
+        return ILUAMG_OK;
+    });
+}
+int ilug_ilu_factorize_device(const iluamg_matrix* A, const iluamg_config* cfg, iluamg_matrix** L,
+                              iluamg_matrix** U) {
+    return guarded([&] {
+        need(A && cfg && L && U);
+        ilug::HostFactors f = ilug::factorize(A->A, ilug::ilu_params_from(cfg->cfg), nullptr);
         *L = new iluamg_matrix_s{std::move(f.L), "L"};
         *U = new iluamg_matrix_s{std::move(f.U), "U"};
         return ILUAMG_OK;

@@ -273,7 +273,7 @@ Report run_bench_trisolve(const Csr& A, const Config& cfg, const std::string& la
     if (m_max < 1) fail_invalid("bench-trisolve: bench.m_max must be >= 1");
     DeviceContext ctx(cfg);
     cudaStream_t st = ctx.stream;
-    const HostFactors f = ilu_factorize(A, ip);
+    const HostFactors f = factorize(A, ip, st);
     DeviceIlu dev;
     dev.build(f, sc, UpperIteration::scaled, true, st);
     const i64 n = A.nrows;

@@ -231,7 +231,7 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         const bool rich = cfg.trisolve.mode == TriSolveMode::richardson;
         if (rich && cfg.scaling == ScalingKind::none && cfg.trisolve.upper == UpperIteration::scaled)
             fail_invalid("ilu smoother: the iterative U solve requires row or row/col scaling");
-        const HostFactors f = ilu_factorize(A, cfg.ilu_params);
+        const HostFactors f = factorize(A, cfg.ilu_params, st);
         ilu_ = std::make_unique<DeviceIlu>();
         ilu_->build(f, cfg.scaling, rich ? cfg.trisolve.upper : UpperIteration::scaled, !rich, st);
         break;

@@ -11,6 +11,7 @@
 
 #include "../host/amg.hpp"
 #include "../host/schur.hpp"
+#include "../kernels/ilu0.hpp"
 #include "../kernels/levelset.hpp"
 #include "../kernels/wavefront.hpp"
 

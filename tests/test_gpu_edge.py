@@ -104,3 +104,55 @@ def test_empty_matrix_like_reference(ilug, ref, torch_cuda):
     got = ilug.run_solve(ilug.Matrix.from_csr(0, 0, *empty), ilug.Config())
     for k in ("iterations", "converged", "levels"):
         assert got[k] == want[k], k
+
+
+@pytest.mark.parametrize("spec", ["poisson3d(17,13,11)", "pressure27(12,12,12)", "cutcell(14,14,14)",
+                                  "poisson2d(33,31)", "anisotropic2d(20,20,0.01)", "poisson2d(1,1)"])
+def test_device_ilu0_bitwise(ilug, ref, torch_cuda, spec):
+    """Device ILU(0) (dependency-flag scheduled) = host ILU(0) = the reference."""
+    A = ilug.Matrix.generate(spec)
+    cfg = ilug.Config()
+    Ld, Ud = ilug.ilu_factorize_device(A, cfg)
+    Lh, Uh = ilug.ilu_factorize(A, cfg)
+    for d, h in ((Ld.csr(), Lh.csr()), (Ud.csr(), Uh.csr())):
+        assert np.array_equal(d[0], h[0]) and np.array_equal(d[1], h[1])
+        assert bitwise(d[2], h[2])
+    Lr, Ur, _, _ = ref.factors_arrays(ref.ilu(ref.mat(*A.csr()), ref.cfg({})))
+    assert bitwise(Ud.csr()[2], Ur[2]) and bitwise(Ld.csr()[2], Lr[2])
+
+
+@pytest.mark.parametrize("patch", ["error", "replace"])
+def test_device_ilu0_zero_pivot(ilug, torch_cuda, patch):
+    """A structurally present but zero pivot: the same error (first row) or the
+    same substituted pivot as the host path."""
+    n = 6
+    rp = np.arange(0, 2 * n + 1, 2)[: n + 1].astype(np.int64)
+    rows, cols, vals = [], [], []
+    for i in range(n):  # lower bidiagonal with a zero diagonal at row 3
+        if i > 0:
+            rows.append(i), cols.append(i - 1), vals.append(-1.0)
+        rows.append(i), cols.append(i), vals.append(0.0 if i == 3 else 4.0)
+    rp = np.zeros(n + 1, np.int64)
+    for r in rows:
+        rp[r + 1] += 1
+    rp = np.cumsum(rp)
+    A = ilug.Matrix.from_csr(n, n, rp, np.array(cols, np.int64), np.array(vals))
+    cfg = ilug.Config().set("ilu.pivot_patch", patch)
+    if patch == "error":
+        for fn in (ilug.ilu_factorize, ilug.ilu_factorize_device):
+            with pytest.raises(ilug.IlugError) as e:
+                fn(A, cfg)
+            assert e.value.status == 3 and "step 3" in e.value.message
+    else:
+        Ld, Ud = ilug.ilu_factorize_device(A, cfg)
+        Lh, Uh = ilug.ilu_factorize(A, cfg)
+        assert bitwise(Ud.csr()[2], Uh.csr()[2]) and bitwise(Ld.csr()[2], Lh.csr()[2])
+
+
+def test_device_ilu0_large_bitwise(ilug, torch_cuda):
+    """2.1 M rows (deep DAG, many blocks waiting on earlier ones): bitwise."""
+    A = ilug.Matrix.generate("pressure27(128,128,128)")
+    cfg = ilug.Config()
+    Ld, Ud = ilug.ilu_factorize_device(A, cfg)
+    Lh, Uh = ilug.ilu_factorize(A, cfg)
+    assert bitwise(Ud.csr()[2], Uh.csr()[2]) and bitwise(Ld.csr()[2], Lh.csr()[2])
