@@ -385,6 +385,7 @@ DeviceHierarchy::~DeviceHierarchy() {
 void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st) {
     const int L = static_cast<int>(h.levels.size());
     levels_ = std::vector<Lev>(static_cast<size_t>(L));
+    SetupTimer tm("device");
     for (int k = 0; k < L; ++k) {
         const HostLevel& hl = h.levels[k];
         Lev& lv = levels_[k];
@@ -393,7 +394,9 @@ void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st) {
         if (k + 1 < L) {
             sell_from_host(lv.P, hl.P, Part::all, st);
             sell_from_host(lv.R, hl.R, Part::all, st);
+            tm.mark("A,P,R", k);
             lv.smoother.build(hl.A, lv.A, h.params.plan.for_level(k), st);
+            tm.mark("smoother", k);
         }
         lv.b.alloc(std::max<i64>(lv.n, 1));
         lv.x.alloc(std::max<i64>(lv.n, 1));

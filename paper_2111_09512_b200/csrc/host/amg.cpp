@@ -372,6 +372,7 @@ HostHierarchy amg_setup(const Csr& A, const AmgParams& prm) {
     if (prm.cycles_nu < 1) fail_invalid("setup: cycles_nu must be >= 1");
     HostHierarchy h;
     h.params = prm;
+    SetupTimer tm("amg");
     Csr cur = A;
     for (;;) {
         h.levels.emplace_back();
@@ -380,14 +381,21 @@ HostHierarchy amg_setup(const Csr& A, const AmgParams& prm) {
         const i64 k = h.num_levels() - 1;
         if (lev.A.nrows <= prm.coarse_size || k + 1 >= prm.max_levels) break;
         const Csr S = strength(lev.A, prm.theta);
+        tm.mark("strength", k);
         CfSplit sp = prm.coarsening == Coarsening::rs_greedy ? coarsen_rs_greedy(S)
                                                              : coarsen_pmis(S, prm.pmis_seed);
+        tm.mark("coarsen", k);
         if (static_cast<double>(sp.n_coarse) > 0.95 * static_cast<double>(lev.A.nrows)) break;
         Csr P = prm.interpolation == Interpolation::direct
                     ? interp_direct(lev.A, sp, S)
                     : interp_mm_ext(lev.A, sp, S, &lev.mm_ext_fallback_rows);
+        tm.mark("interp", k);
         Csr R = csr_transpose(P);
-        cur = csr_matmul(R, csr_matmul(lev.A, P));
+        tm.mark("transpose", k);
+        Csr AP = csr_matmul(lev.A, P);
+        tm.mark("A*P", k);
+        cur = csr_matmul(R, AP);
+        tm.mark("R*(AP)", k);
         lev.P = std::move(P);
         lev.R = std::move(R);
         lev.split = std::move(sp);

@@ -42,4 +42,16 @@ int host_threads();
 /// the thread count (bitwise reproducibility is a parity requirement).
 void parallel_ranges(i64 n, const std::function<void(i64, i64, int)>& fn, i64 grain = 4096);
 
+/// ILUG_TRACE_SETUP=1: wall time of setup phases on stderr (diagnostics only).
+class SetupTimer {
+public:
+    explicit SetupTimer(const char* scope);
+    void mark(const char* phase, i64 level = -1);
+
+private:
+    const char* scope_;
+    bool on_;
+    double t_;
+};
+
 } // namespace ilug

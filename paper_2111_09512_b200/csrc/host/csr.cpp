@@ -1,6 +1,8 @@
 #include "csr.hpp"
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <exception>
 #include <thread>
@@ -123,6 +125,26 @@ void parallel_ranges(i64 n, const std::function<void(i64, i64, int)>& fn, i64 gr
     }
     for (auto& th : threads) th.join();
     if (err) std::rethrow_exception(err);
+}
+
+namespace {
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+} // namespace
+
+SetupTimer::SetupTimer(const char* scope) : scope_(scope), on_(std::getenv("ILUG_TRACE_SETUP") != nullptr),
+                                            t_(now_s()) {}
+
+void SetupTimer::mark(const char* phase, i64 level) {
+    if (!on_) return;
+    const double t = now_s();
+    if (level >= 0)
+        std::fprintf(stderr, "[setup] %s level %lld %-10s %8.3f s\n", scope_, static_cast<long long>(level), phase,
+                     t - t_);
+    else
+        std::fprintf(stderr, "[setup] %s %-18s %8.3f s\n", scope_, phase, t - t_);
+    t_ = t;
 }
 
 Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_zeros) {
