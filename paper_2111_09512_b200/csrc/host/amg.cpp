@@ -40,12 +40,22 @@ enum : char { kFree = 0, kC = 1, kF = 2 };
 // order dependent, src/amg.cpp:56-84), then number the C-points.
 CfSplit finish_split(const Csr& S, std::vector<char>& st) {
     const i64 n = S.nrows;
-    for (i64 i = 0; i < n; ++i) {
-        if (st[i] != kF) continue;
-        bool ok = false;
-        for (i64 k = S.rp[i]; k < S.rp[i + 1] && !ok; ++k) ok = st[S.ci[k]] == kC;
-        if (!ok) st[i] = kC;
-    }
+    // Promotions only ever add C-points, so an F-point that already has a
+    // strong C-neighbour keeps it: find the candidates in parallel, then run
+    // the order-dependent pass over the candidates only (same result).
+    auto lacks_c = [&](i64 i) {
+        for (i64 k = S.rp[i]; k < S.rp[i + 1]; ++k)
+            if (st[S.ci[k]] == kC) return false;
+        return true;
+    };
+    std::vector<std::vector<i64>> cand(static_cast<size_t>(host_threads()));
+    parallel_ranges(n, [&](i64 b, i64 e, int t) {
+        for (i64 i = b; i < e; ++i)
+            if (st[i] == kF && lacks_c(i)) cand[static_cast<size_t>(t)].push_back(i);
+    });
+    for (const auto& list : cand) // chunks hold ascending index ranges, in chunk order
+        for (const i64 i : list)
+            if (lacks_c(i)) st[i] = kC;
     CfSplit sp;
     sp.is_coarse.resize(static_cast<size_t>(n));
     sp.coarse_index.assign(static_cast<size_t>(n), -1);
@@ -210,14 +220,23 @@ CfSplit coarsen_pmis(const Csr& S, std::uint64_t seed) {
 
 Csr interp_direct(const Csr& A, const CfSplit& sp, const Csr& S) {
     const i64 n = A.nrows;
+    // The weights are recomputed per pass (classification is one pass over the
+    // row) instead of being stored per row: no per-row heap allocation.
+    auto weights = [&](i64 i) -> const std::vector<std::pair<i64, double>>& {
+        thread_local RowClass rc;
+        thread_local std::vector<std::pair<i64, double>> w;
+        classify(A, S, sp, i, rc);
+        direct_weights(rc, w);
+        return w;
+    };
     std::vector<int> status(static_cast<size_t>(n), 0);
-    std::vector<std::vector<std::pair<i64, double>>> rows(static_cast<size_t>(n));
     parallel_ranges(n, [&](i64 b, i64 e, int) {
         RowClass rc;
+        std::vector<std::pair<i64, double>> w;
         for (i64 i = b; i < e; ++i) {
             if (sp.is_coarse[i]) continue;
             classify(A, S, sp, i, rc);
-            status[i] = direct_weights(rc, rows[i]);
+            status[i] = direct_weights(rc, w);
         }
     });
     for (i64 i = 0; i < n; ++i)
@@ -227,7 +246,7 @@ Csr interp_direct(const Csr& A, const CfSplit& sp, const Csr& S) {
         [&](i64 i) {
             if (sp.is_coarse[i]) return i64{1};
             i64 c = 0;
-            for (auto& [j, w] : rows[i]) c += w != 0.0; // from_triplets drops exact zeros
+            for (auto& [j, w] : weights(i)) c += w != 0.0; // from_triplets drops exact zeros
             return c;
         },
         [&](i64 i, i32* c, double* v) {
@@ -235,9 +254,8 @@ Csr interp_direct(const Csr& A, const CfSplit& sp, const Csr& S) {
                 *c = static_cast<i32>(sp.coarse_index[i]), *v = 1.0;
                 return;
             }
-            for (auto& [j, w] : rows[i])
+            for (auto& [j, w] : weights(i))
                 if (w != 0.0) *c++ = static_cast<i32>(sp.coarse_index[j]), *v++ = w;
-            std::vector<std::pair<i64, double>>().swap(rows[i]);
         });
 }
 
@@ -373,7 +391,8 @@ HostHierarchy amg_setup(const Csr& A, const AmgParams& prm) {
     HostHierarchy h;
     h.params = prm;
     SetupTimer tm("amg");
-    Csr cur = A;
+    Csr cur = csr_copy(A);
+    tm.mark("copy A");
     for (;;) {
         h.levels.emplace_back();
         HostLevel& lev = h.levels.back();

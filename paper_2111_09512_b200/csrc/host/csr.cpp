@@ -222,6 +222,24 @@ Csr csr_from_arrays(i64 nrows, i64 ncols, const i64* rp, const i64* ci, const do
     return A;
 }
 
+Csr csr_copy(const Csr& A) {
+    Csr C;
+    C.nrows = A.nrows;
+    C.ncols = A.ncols;
+    C.rp.resize(A.rp.size());
+    C.ci.resize(A.ci.size());
+    C.v.resize(A.v.size());
+    auto copy = [](const auto& src, auto& dst) {
+        parallel_ranges(static_cast<i64>(src.size()), [&](i64 b, i64 e, int) {
+            std::copy(src.begin() + b, src.begin() + e, dst.begin() + b);
+        }, 1 << 20);
+    };
+    copy(A.rp, C.rp);
+    copy(A.ci, C.ci);
+    copy(A.v, C.v);
+    return C;
+}
+
 Csr csr_identity(i64 n) {
     Csr I;
     I.nrows = I.ncols = n;

@@ -13,12 +13,34 @@
 
 namespace ilug {
 
+/// Allocator whose value-construction is default-initialisation: resize() of
+/// the big CSR arrays does not zero-fill them on one thread; the parallel
+/// loops that fill them touch the pages first (first-touch is the dominant
+/// cost of assembling multi-GB operators on the host).
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    using std::allocator<T>::allocator;
+    template <class U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        if constexpr (sizeof...(Args) == 0)
+            ::new (static_cast<void*>(p)) U;
+        else
+            ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+};
+template <class T>
+using RawVec = std::vector<T, NoInitAlloc<T>>;
+
 struct Csr {
     i64 nrows = 0;
     i64 ncols = 0;
-    std::vector<i64> rp{0};
-    std::vector<i32> ci;
-    std::vector<double> v;
+    RawVec<i64> rp{0};
+    RawVec<i32> ci;
+    RawVec<double> v;
 
     i64 nnz() const { return static_cast<i64>(v.size()); }
     i64 row_len(i64 i) const { return rp[i + 1] - rp[i]; }
@@ -37,6 +59,8 @@ Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_ze
 Csr csr_from_arrays(i64 nrows, i64 ncols, const i64* rp, const i64* ci, const double* v);
 void csr_validate(const Csr& A, const char* what);
 
+/// Parallel deep copy (first touch spread over the worker pool).
+Csr csr_copy(const Csr& A);
 Csr csr_identity(i64 n);
 
 /// y = A x, one row per task, ascending columns from 0.0 (src/sparse.cpp:162-174).

@@ -60,7 +60,7 @@ HostFactors ilu0(const Csr& A, PivotPatch patch) {
         for (i64 i = 0; i < n; ++i) order[cur[level[i]]++] = i;
     }
 
-    std::vector<double> w(A.v);
+    std::vector<double> w(A.v.begin(), A.v.end());
     std::atomic<i64> first_zero{n};
     // per-worker column -> position-in-row markers (-1 = not in row i's pattern)
     std::vector<std::vector<i32>> marks(static_cast<size_t>(host_threads()));
