@@ -146,14 +146,18 @@ HostFactors ilut(const Csr& A, const IluParams& p) {
     // factors are bitwise independent of the worker count. The chain row i-1 ->
     // row i (last multiplier popped) bounds the speed-up, not correctness.
     std::vector<i64> loff(static_cast<size_t>(n) + 1, 0), uoff(static_cast<size_t>(n) + 1, 0);
-    for (i64 i = 0; i < n; ++i) {
-        i64 lo = 0, up = 0;
-        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) lo += A.ci[k] < i, up += A.ci[k] > i;
-        loff[i + 1] = loff[i] + lo + p.lfill;
-        uoff[i + 1] = uoff[i] + 1 + up + p.lfill;
-    }
-    std::vector<i32> lci(static_cast<size_t>(loff[n])), uci(static_cast<size_t>(uoff[n]));
-    std::vector<double> lv(static_cast<size_t>(loff[n])), uv(static_cast<size_t>(uoff[n]));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            i64 lo = 0, up = 0;
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) lo += A.ci[k] < i, up += A.ci[k] > i;
+            loff[i + 1] = lo + p.lfill;
+            uoff[i + 1] = 1 + up + p.lfill;
+        }
+    });
+    for (i64 i = 0; i < n; ++i) loff[i + 1] += loff[i], uoff[i + 1] += uoff[i];
+    // slot arrays: no zero fill (multi-GB at C2); each row writes its own slots
+    RawVec<i32> lci(static_cast<size_t>(loff[n])), uci(static_cast<size_t>(uoff[n]));
+    RawVec<double> lv(static_cast<size_t>(loff[n])), uv(static_cast<size_t>(uoff[n]));
     std::vector<i64> llen(static_cast<size_t>(n), 0), ulen(static_cast<size_t>(n), 0);
     std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[static_cast<size_t>(n)]);
     for (i64 i = 0; i < n; ++i) done[i].store(0, std::memory_order_relaxed);
