@@ -236,11 +236,8 @@ HostFactors ilut(const Csr& A, const IluParams& p) {
                     }
                 }
             }
-            select(kept, true, tau);
-            i64 o = loff[i];
-            for (i64 j : pat_part) lci[o] = static_cast<i32>(j), lv[o++] = w[j];
-            llen[i] = o - loff[i];
-
+            // U part first: it is all row i+1 waits for (done[i]); the L part's
+            // selection is off that chain (both only read w, so the order is free)
             double d = w[i];
             if (d == 0.0) {
                 if (p.pivot_patch == PivotPatch::error) {
@@ -252,12 +249,17 @@ HostFactors ilut(const Csr& A, const IluParams& p) {
                     d = patch_pivot(p.droptol, row_norm2(A, i), anorm_f, p.pivot_patch, i);
                 }
             }
-            o = uoff[i];
+            i64 o = uoff[i];
             uci[o] = static_cast<i32>(i), uv[o++] = d;
             select(upper, false, tau);
             for (i64 j : pat_part) uci[o] = static_cast<i32>(j), uv[o++] = w[j];
             ulen[i] = o - uoff[i];
             done[i].store(1, std::memory_order_release);
+
+            select(kept, true, tau);
+            o = loff[i];
+            for (i64 j : pat_part) lci[o] = static_cast<i32>(j), lv[o++] = w[j];
+            llen[i] = o - loff[i];
 
             for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) orig[A.ci[k]] = 0;
             for (i64 j : kept) w[j] = 0.0, live[j] = 0;
