@@ -362,7 +362,7 @@ namespace {
 
 // rowlen per SELL row and slice offsets; `len_of(row)` gives the part length.
 template <typename LenOf>
-void layout(Sell& out, i64 nrows_pad, const std::vector<i32>& perm, LenOf len_of) {
+void layout(Sell& out, i64 nrows_pad, const std::vector<i32>& perm, LenOf len_of, cudaStream_t st) {
     std::vector<std::uint16_t> rl(static_cast<size_t>(nrows_pad), 0);
     const i64 ns = nrows_pad / kSlice;
     std::vector<i64> sp(static_cast<size_t>(ns) + 1, 0);
@@ -394,16 +394,20 @@ void layout(Sell& out, i64 nrows_pad, const std::vector<i32>& perm, LenOf len_of
     out.nnz = 0;
     out.max_row = 0;
     for (i64 s = 0; s < ns; ++s) out.nnz += nnz_part[s], out.max_row = std::max(out.max_row, mx[s]);
-    out.slice_ptr.upload(sp.data(), ns + 1);
-    out.rowlen.upload(rl.data(), nrows_pad);
+    // Everything on the builder's stream: the fill kernel that follows runs on
+    // it, and a legacy-stream copy/memset is NOT ordered with a non-blocking
+    // stream (a pageable-memory cudaMemcpyAsync may still be in flight when it
+    // returns) — that race corrupted large operators built on a solver stream.
+    out.slice_ptr.upload(sp.data(), ns + 1, st);
+    out.rowlen.upload(rl.data(), nrows_pad, st);
     out.cols.alloc(out.padded);
     out.vals.alloc(out.padded);
     if (out.padded > 0) {
-        ILUG_CUDA(cudaMemset(out.cols.p, 0, static_cast<size_t>(out.padded) * sizeof(i32)));
-        ILUG_CUDA(cudaMemset(out.vals.p, 0, static_cast<size_t>(out.padded) * sizeof(double)));
+        ILUG_CUDA(cudaMemsetAsync(out.cols.p, 0, static_cast<size_t>(out.padded) * sizeof(i32), st));
+        ILUG_CUDA(cudaMemsetAsync(out.vals.p, 0, static_cast<size_t>(out.padded) * sizeof(double), st));
     }
     if (!perm.empty())
-        out.perm.upload(perm.data(), nrows_pad);
+        out.perm.upload(perm.data(), nrows_pad, st);
     else
         out.perm.release();
 }
@@ -467,7 +471,7 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
                         : perm_in;
     const i64 pad = perm_host.empty() ? (pattern.nrows + kSlice - 1) / kSlice * kSlice
                                       : static_cast<i64>(perm_host.size());
-    layout(out, pad, perm_host, [&](i64 row) { return part_len(pattern, row, pc); });
+    layout(out, pad, perm_host, [&](i64 row) { return part_len(pattern, row, pc); }, s);
     if (pad > 0 && pattern.nnz() > 0) {
         k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp, ci, v, pc,
                                                      out.slice_ptr.p, out.cols.p, out.vals.p);
@@ -481,7 +485,7 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
     const std::vector<i32> perm = sigma_order(A.nrows, [&](i64 r) { return part_len(A, r, pc); });
     const i64 pad = perm.empty() ? (A.nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
-    layout(out, pad, perm, [&](i64 row) { return part_len(A, row, pc); });
+    layout(out, pad, perm, [&](i64 row) { return part_len(A, row, pc); }, s);
     if (A.nnz() == 0 || pad == 0) return;
     DBuf<i64> rp;
     DBuf<i32> ci;
@@ -496,6 +500,7 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
 }
 
 Csr sell_to_host(const Sell& M) {
+    ILUG_CUDA(cudaDeviceSynchronize()); // M may still be written on another stream
     Csr A;
     A.nrows = M.nrows;
     A.ncols = M.ncols;
