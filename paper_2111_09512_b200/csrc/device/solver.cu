@@ -242,8 +242,10 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         break;
     }
     // r, y ping-pong, bs, x ping-pong, spare; then the wavefront intermediates
+    // (only when a fused plan exists)
     const i64 mmax = std::max(cfg.trisolve.m_lower, cfg.trisolve.m_upper);
-    ws_.alloc((7 + std::max<i64>(mmax - 2, 0)) * std::max<i64>(n_, 1));
+    const bool wave = ilu_ && (ilu_->wave_L().ready() || ilu_->wave_U().ready());
+    ws_.alloc((7 + (wave ? std::max<i64>(mmax - 2, 0) : 0)) * std::max<i64>(n_, 1));
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 

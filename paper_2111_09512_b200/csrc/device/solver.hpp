@@ -69,7 +69,9 @@ public:
     /// ws: sweep_ws(m) + n doubles.
     void sweep_upper(const double* b, double* x, i64 m, double* ws, cudaStream_t st) const;
     /// Workspace (doubles) of sweep_lower with m sweeps; sweep_upper needs n more.
-    i64 sweep_ws(i64 m) const { return std::max<i64>(2, m) * n_; }
+    i64 sweep_ws(i64 m) const {
+        return ((wave_L_.ready() || wave_U_.ready()) ? std::max<i64>(2, m) : 2) * n_;
+    }
     /// m sweeps of the U (upper) or L factor run as one wavefront launch
     /// (m-1 fused sweeps after the first).
     bool use_wave(bool upper, i64 m) const;

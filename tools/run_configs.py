@@ -10,7 +10,7 @@ c3: cut-cell 256^3 (coefficient jumps over 16 decades): dep(U) vs dep(D^-1 U)
     at 64^3 via run_analyze, and at 256^3 scaled vs unscaled-Jacobi sweep time
     and error to the direct solve for m = 5, 20, 40.
 c5: ILUT Schur-complement smoother under FGMRES (run_schur_solve) on
-    pressure27(128^3): iterations and time for 1, 2, 4, 8 sub-domains."""
+    pressure27(64^3): iterations and time for 1, 2, 4, 8 sub-domains."""
 import json
 import os
 import sys
@@ -74,7 +74,7 @@ if "c3" in which:
     print(json.dumps({"config": "C3 cutcell(256,256,256) ILU(0)", **sweeps("cutcell(256,256,256)", [5, 20, 40])}),
           flush=True)
 if "c5" in which:
-    spec = "pressure27(128,128,128)"
+    spec = "pressure27(64,64,64)"
     A = ilug.Matrix.generate(spec)
     t = time.time()
     rep = ilug.run_schur_solve(A, ilug.Config().update({"krylov.tol": "1e-8"}))
