@@ -13,8 +13,8 @@ of the metric (host setup + device solve) with the direct-sptrsv comparison
 (`--no-tts` skips it).
 
 Multi-GPU (torchrun, N > 1): every rank smooths its own C2-sized row block
-(weak scaling; see DESIGN.md §6 for the halo-exchange plan), time = max over
-ranks. `--impl reference` times the reference's own CPU code on a bounded
+(weak scaling, global residual through the NCCL halo exchange),
+time = max over ranks; `tts` is then the distributed GMRES+AMG solve. `--impl reference` times the reference's own CPU code on a bounded
 sample of the same workload (rank 0 only).
 """
 from __future__ import annotations
@@ -162,13 +162,13 @@ def run_reference(args):
         "vs_baseline": None}))
 
 
-def build_workload(ilug, args, rank, world, local):
+def build_workload(ilug, args, rank, world, local, use_dist=False):
     """The smoother of this rank: N=1 the C2 matrix; N>1 the rank's 256^3 slab of
     pressure27(256,256,256N) (weak scaling), block-Jacobi ILUT factors of the
     local diagonal block, global residual with an NCCL halo exchange."""
     import ctypes as C
     cfg = ilug.Config().update(ILU_KV)
-    if world == 1:
+    if not use_dist:
         A = ilug.Matrix.generate(args.spec)
         S = ilug.Smoother(A, cfg)  # host ILUT + upload + K1 row scaling on the device
         v = [C.c_longlong() for _ in range(5)]
@@ -216,6 +216,8 @@ def main():
     ap.add_argument("--no-tts", action="store_true", help="skip the GMRES+AMG time-to-solution part")
     ap.add_argument("--tts-gs", action="store_true", help="also time the Gauss-Seidel coarse fallback")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the distributed (N > 1) code path even with one rank (validation)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -226,14 +228,18 @@ def main():
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ilug.lib.ilug_set_device(local)
 
     t0 = time.perf_counter()
-    W = build_workload(ilug, args, rank, world, local)
+    W = build_workload(ilug, args, rank, world, local, use_dist)
     setup_s = time.perf_counter() - t0
     n, nnz_a, nnz_l, nnz_u, pad_u = W["n"], W["nnz_a"], W["nnz_l"], W["nnz_u"], W["pad_u"]
     B = step_bytes(n, nnz_a, nnz_l, nnz_u)
@@ -247,12 +253,12 @@ def main():
     torch.cuda.synchronize()
 
     def barrier():
-        if world > 1:
+        if use_dist:
             import torch.distributed as dist
             dist.barrier()
 
     def max_over_ranks(v):
-        if world == 1:
+        if not use_dist:
             return v
         import torch.distributed as dist
         t = torch.tensor([v], dtype=torch.float64, device="cuda")
@@ -291,7 +297,7 @@ def main():
         kern[name] = {"ms": kms, "gbs": sweep_bytes(n, nnz) / (kms * 1e-3) / 1e9, "bytes": sweep_bytes(n, nnz)}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "u_sweep_traffic.json")
-    if os.path.exists(tpath) and world == 1:
+    if os.path.exists(tpath) and not use_dist:
         with open(tpath) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
     ach = kern["u_sweep"]["gbs"]
@@ -328,7 +334,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"ilu_smooth_sweep (m_L=m_U=5, row-scaled ILUT(1e-3,5)) on {W['spec']}"
-                               + ("" if world == 1 else f" (rank slabs of 256^3, block-Jacobi, NCCL halo)"),
+                               + ("" if not use_dist else " (rank slabs of 256^3, block-Jacobi, NCCL halo)"),
                    "n_per_gpu": n, "nnz_A": nnz_a, "nnz_L_strict": nnz_l, "nnz_U_strict": nnz_u,
                    "sell_padding_U": round(pad_u / max(nnz_u, 1) - 1, 4) if pad_u else None, "bytes_per_step": B,
                    "l2": "inputs (>= 5 GB per step) exceed the 126 MB L2; no flush needed",
@@ -337,16 +343,52 @@ def main():
         "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": 9 * args.steps,
     }
-    if not args.no_tts and rank == 0 and world == 1:
+    if not args.no_tts and not use_dist:
         res["tts"] = time_to_solution(ilug, W["A"], ("poly_gs", "gauss_seidel") if args.tts_gs else ("poly_gs",))
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    elif not args.no_tts:
+        tts = dist_time_to_solution(ilug, W, b, barrier, max_over_ranks)
+        if rank == 0:
+            res["tts"] = tts
+    if rank == 0 and not use_dist and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(res))
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
         del W
         dist.destroy_process_group()
+
+
+def dist_time_to_solution(ilug, W, b, barrier, max_over_ranks):
+    """N > 1: distributed GMRES+AMG on the ranks' slabs (global Krylov with NCCL
+    reductions, block-Jacobi AMG with the ILUT smoother, global residuals with
+    the NCCL halo exchange); setup and solve timed as the max over ranks."""
+    import torch
+    from paper_2111_09512_b200 import dist as idist
+    kv = dict(ILU_KV, **{"smoother.sweeps": "2", "krylov.tol": "1e-8", "amg.coarsening": "pmis",
+                         "krylov.form_iterates": "false", "smoother.fallback.kind": "poly_gs"})
+    cfg = ilug.Config().update(kv)
+    try:
+        barrier()
+        t = time.perf_counter()
+        solver = idist.Solver(W["plan"], W["comm"], cfg)
+        torch.cuda.synchronize()
+        setup = max_over_ranks(time.perf_counter() - t)
+        x = torch.zeros_like(b)
+        # warm-up (lazy module loading, V-cycle graph capture) outside the timed solve
+        solver.gmres(ilug.Config().update(dict(kv, **{"krylov.max_iters": "2"})), b, x)
+        x.zero_()
+        barrier()
+        t = time.perf_counter()
+        out = solver.gmres(cfg, b, x)
+        torch.cuda.synchronize()
+        solve = max_over_ranks(time.perf_counter() - t)
+        return {"distributed": {"iterations": out["iterations"], "converged": out["status"] == 0,
+                                "final_relres": out["final_relres"], "setup_s": round(setup, 3),
+                                "solve_s": round(solve, 4),
+                                "preconditioner": "block-Jacobi AMG (rank-local hierarchy), ILUT smoother"}}
+    except Exception as e:  # report, never lose the bench line
+        return {"distributed": {"error": str(e)[:300]}}
 
 
 def time_to_solution(ilug, A, fallbacks=("poly_gs",)):

@@ -153,7 +153,10 @@ void DistSolver::build(const HaloPlan& plan, const DistComm& comm, const AmgPara
 
 KrylovReport DistSolver::solve(const double* b, double* x, const KrylovParams& p, cudaStream_t st) {
     KrylovParams q = p;
-    if (comm_->nranks > 1) q.estimate_anorm = false;
+    // |A|_2 needs a global transpose (skipped across ranks); with the relres
+    // criterion and no per-iteration iterates nothing in the solve reads it
+    // (the single-process driver moves it out of the timed region likewise)
+    if (comm_->nranks > 1 || (!q.form_iterates && !q.nrbe_criterion)) q.estimate_anorm = false;
     return device_gmres(A_, A_diag_, H_, b, x, q, st, comm_);
 }
 
