@@ -2,6 +2,7 @@
 #include "../host/problems.hpp"
 
 #include <chrono>
+#include <future>
 #include <cmath>
 #include <cstdio>
 #include <sstream>
@@ -53,10 +54,21 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
                         bool use_graph, cudaStream_t st) {
     SolveOutcome oc;
     const auto t0 = std::chrono::steady_clock::now();
+    // The finest level's ILUT (host; its row-to-row pipeline leaves most cores
+    // idle) runs concurrently with the AMG setup that does not need it.
+    // Identical factors either way (same function, same input).
+    const SmootherConfig& s0 = ap.plan.for_level(0);
+    std::future<HostFactors> f0;
+    if (s0.kind == SmootherKind::ilu && s0.ilu_params.variant == IluVariant::ilut && A.nrows > ap.coarse_size)
+        f0 = std::async(std::launch::async, [&] { return ilu_factorize(A, s0.ilu_params); });
     oc.hier = amg_setup(A, ap);
+    HostFactors pre;
+    const bool have_pre = f0.valid();
+    if (have_pre) pre = f0.get();
     DeviceHierarchy dh;
     dh.set_use_graph(use_graph);
-    dh.build(oc.hier, st);
+    // the level-0 smoother is ILU only when the hierarchy has more than one level
+    dh.build(oc.hier, st, have_pre && oc.hier.num_levels() > 1 ? &pre : nullptr);
     oc.setup_seconds = since(t0);
 
     const i64 n = A.nrows;

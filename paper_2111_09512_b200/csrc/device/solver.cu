@@ -186,7 +186,7 @@ Vec inverted_diag(const Csr& A, const char* what) {
 } // namespace
 
 void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg,
-                           cudaStream_t st) {
+                           cudaStream_t st, HostFactors* pre) {
     if (cfg.sweeps < 0) fail_invalid("build_smoother_state: sweeps must be >= 0");
     if (cfg.poly_degree < 0) fail_invalid("build_smoother_state: poly_degree must be >= 0");
     cfg_ = cfg;
@@ -231,7 +231,7 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         const bool rich = cfg.trisolve.mode == TriSolveMode::richardson;
         if (rich && cfg.scaling == ScalingKind::none && cfg.trisolve.upper == UpperIteration::scaled)
             fail_invalid("ilu smoother: the iterative U solve requires row or row/col scaling");
-        const HostFactors f = factorize(A, cfg.ilu_params, st);
+        const HostFactors f = pre ? std::move(*pre) : factorize(A, cfg.ilu_params, st);
         ilu_ = std::make_unique<DeviceIlu>();
         ilu_->build(f, cfg.scaling, rich ? cfg.trisolve.upper : UpperIteration::scaled, !rich, st);
         break;
@@ -384,7 +384,7 @@ DeviceHierarchy::~DeviceHierarchy() {
     if (exec_) cudaGraphExecDestroy(exec_);
 }
 
-void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st) {
+void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st, HostFactors* level0) {
     const int L = static_cast<int>(h.levels.size());
     levels_ = std::vector<Lev>(static_cast<size_t>(L));
     SetupTimer tm("device");
@@ -397,7 +397,7 @@ void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st) {
             sell_from_host(lv.P, hl.P, Part::all, st);
             sell_from_host(lv.R, hl.R, Part::all, st);
             tm.mark("A,P,R", k);
-            lv.smoother.build(hl.A, lv.A, h.params.plan.for_level(k), st);
+            lv.smoother.build(hl.A, lv.A, h.params.plan.for_level(k), st, k == 0 ? level0 : nullptr);
             tm.mark("smoother", k);
         }
         lv.b.alloc(std::max<i64>(lv.n, 1));

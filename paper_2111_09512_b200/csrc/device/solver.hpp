@@ -129,7 +129,9 @@ private:
 /// One level's smoother (src/smoother.cpp:161-187 `smooth`).
 class DeviceSmoother {
 public:
-    void build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg, cudaStream_t st);
+    /// `pre`: factors of A computed ahead (moved from; ILU kinds only).
+    void build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg, cudaStream_t st,
+               HostFactors* pre = nullptr);
     /// x <- smooth(A, b, x). `x_zero`: caller guarantees x == 0 on entry, so the
     /// first residual is b itself (bitwise what the SpMV would give).
     void smooth(const double* b, double* x, bool x_zero, cudaStream_t st) const;
@@ -155,7 +157,8 @@ private:
 /// The AMG V-cycle on the device, optionally replayed as one CUDA graph.
 class DeviceHierarchy {
 public:
-    void build(const HostHierarchy& h, cudaStream_t st);
+    /// `level0`: the finest level's ILU factors computed ahead (see solve_with).
+    void build(const HostHierarchy& h, cudaStream_t st, HostFactors* level0 = nullptr);
     /// z = M(r) with z zeroed first (the driver's precond lambda, src/driver.cpp:182-185).
     void vcycle(const double* r, double* z, cudaStream_t st);
     /// Same, without graph replay (direct kernel launches).
