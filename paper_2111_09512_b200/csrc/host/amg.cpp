@@ -166,54 +166,57 @@ CfSplit coarsen_pmis(const Csr& S, std::uint64_t seed) {
                     hash_unit(seed, static_cast<std::uint64_t>(i));
     });
     std::vector<char> st(static_cast<size_t>(n), kFree), fresh(static_cast<size_t>(n), 0);
-    i64 remaining = n;
-    while (remaining > 0) {
+    // Rounds are synchronous (every decision reads the state at the round's
+    // start), so working on the compacted list of still-free points gives the
+    // same split as sweeping all n points every round.
+    std::vector<i64> live(static_cast<size_t>(n));
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) live[i] = i;
+    });
+    const int T = host_threads();
+    std::vector<std::vector<i64>> keep(static_cast<size_t>(T)), picked(static_cast<size_t>(T));
+    while (!live.empty()) {
+        const i64 m = static_cast<i64>(live.size());
         // Local maxima among still-free strong neighbours (both directions).
-        std::atomic<i64> found{0};
-        parallel_ranges(n, [&](i64 b, i64 e, int) {
-            i64 f = 0;
-            for (i64 i = b; i < e; ++i) {
-                fresh[i] = 0;
-                if (st[i] != kFree) continue;
+        for (auto& v : picked) v.clear();
+        parallel_ranges(m, [&](i64 b, i64 e, int t) {
+            for (i64 q = b; q < e; ++q) {
+                const i64 i = live[q];
                 bool top = true;
                 for (const Csr* G : {&S, &St})
                     for (i64 k = G->rp[i]; top && k < G->rp[i + 1]; ++k) {
                         const i64 j = G->ci[k];
                         if (j != i && st[j] == kFree && wt[j] >= wt[i]) top = false;
                     }
-                if (top) fresh[i] = 1, ++f;
+                if (top) picked[static_cast<size_t>(t)].push_back(i);
             }
-            found += f;
         });
-        if (found == 0)
-            for (i64 i = 0; i < n; ++i)
-                if (st[i] == kFree) {
-                    fresh[i] = 1;
-                    found = 1;
-                    break;
-                }
-        parallel_ranges(n, [&](i64 b, i64 e, int) {
-            for (i64 i = b; i < e; ++i)
-                if (fresh[i]) st[i] = kC;
-        });
-        remaining -= found;
+        i64 found = 0;
+        for (const auto& v : picked) found += static_cast<i64>(v.size());
+        if (found == 0) picked[0].push_back(live[0]); // smallest free index (live stays ascending)
+        for (const auto& v : picked)
+            for (const i64 i : v) fresh[i] = 1, st[i] = kC;
         // A free point becomes F iff a fresh C-point strongly depends on it,
         // i.e. some i in S-row(j) is fresh (equivalent to the St scatter).
-        std::atomic<i64> newf{0};
-        parallel_ranges(n, [&](i64 b, i64 e, int) {
-            i64 f = 0;
-            for (i64 j = b; j < e; ++j) {
+        for (auto& v : keep) v.clear();
+        parallel_ranges(m, [&](i64 b, i64 e, int t) {
+            for (i64 q = b; q < e; ++q) {
+                const i64 j = live[q];
                 if (st[j] != kFree) continue;
-                for (i64 k = S.rp[j]; k < S.rp[j + 1]; ++k)
-                    if (fresh[S.ci[k]]) {
-                        st[j] = kF;
-                        ++f;
-                        break;
-                    }
+                bool hit = false;
+                for (i64 k = S.rp[j]; k < S.rp[j + 1] && !hit; ++k) hit = fresh[S.ci[k]] != 0;
+                if (hit)
+                    st[j] = kF;
+                else
+                    keep[static_cast<size_t>(t)].push_back(j);
             }
-            newf += f;
         });
-        remaining -= newf;
+        for (const auto& v : picked)
+            for (const i64 i : v) fresh[i] = 0;
+        std::vector<i64> next;
+        next.reserve(static_cast<size_t>(m));
+        for (const auto& v : keep) next.insert(next.end(), v.begin(), v.end()); // chunks in ascending order
+        live.swap(next);
     }
     return finish_split(S, st);
 }

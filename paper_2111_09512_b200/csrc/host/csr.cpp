@@ -1,6 +1,7 @@
 #include "csr.hpp"
 
 #include <atomic>
+#include <memory>
 #include <chrono>
 #include <cstdio>
 #include <condition_variable>
@@ -327,10 +328,20 @@ Csr csr_matmul(const Csr& A, const Csr& B) {
     };
     std::vector<Piece> pieces(static_cast<size_t>(T));
     auto lo = [&](int t) { return A.nrows * t / T; };
-    // Each worker keeps a dense accumulator + row marker over B's columns.
+    // Each worker keeps a dense accumulator + row marker over B's columns,
+    // calloc'ed: the OS hands out zero pages lazily, so a worker only faults in
+    // the pages of the columns its rows reach (a zero-filled n_coarse-sized
+    // array per worker cost more than the product at 100 M rows).
+    struct FreeDel {
+        void operator()(void* p) const { std::free(p); }
+    };
     parallel_ranges(T, [&](i64 tb, i64 te, int) {
-        std::vector<double> work(static_cast<size_t>(B.ncols), 0.0);
-        std::vector<i64> mark(static_cast<size_t>(B.ncols), -1);
+        const size_t nc = static_cast<size_t>(std::max<i64>(B.ncols, 1));
+        std::unique_ptr<double, FreeDel> work_mem(static_cast<double*>(std::calloc(nc, sizeof(double))));
+        std::unique_ptr<i64, FreeDel> mark_mem(static_cast<i64*>(std::calloc(nc, sizeof(i64))));
+        if (!work_mem || !mark_mem) fail_numeric("matmul: out of host memory");
+        double* work = work_mem.get();
+        i64* mark = mark_mem.get(); // row i marks with i + 1 (0 = untouched)
         std::vector<i32> cols;
         for (i64 t = tb; t < te; ++t) {
             Piece& pc = pieces[t];
@@ -341,8 +352,8 @@ Csr csr_matmul(const Csr& A, const Csr& B) {
                     const double aik = A.v[ka];
                     for (i64 kb = B.rp[k]; kb < B.rp[k + 1]; ++kb) {
                         const i32 j = B.ci[kb];
-                        if (mark[j] != i) {
-                            mark[j] = i;
+                        if (mark[j] != i + 1) {
+                            mark[j] = i + 1;
                             cols.push_back(j);
                         }
                         work[j] += aik * B.v[kb];
