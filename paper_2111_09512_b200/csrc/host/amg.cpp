@@ -158,7 +158,9 @@ CfSplit coarsen_rs_greedy(const Csr& S) {
 
 CfSplit coarsen_pmis(const Csr& S, std::uint64_t seed) {
     const i64 n = S.nrows;
+    SetupTimer tm("pmis");
     const Csr St = csr_transpose(S);
+    tm.mark("transpose S");
     std::vector<double> wt(static_cast<size_t>(n));
     parallel_ranges(n, [&](i64 b, i64 e, int) {
         for (i64 i = b; i < e; ++i)
@@ -175,7 +177,10 @@ CfSplit coarsen_pmis(const Csr& S, std::uint64_t seed) {
     });
     const int T = host_threads();
     std::vector<std::vector<i64>> keep(static_cast<size_t>(T)), picked(static_cast<size_t>(T));
+    tm.mark("weights");
+    i64 rounds = 0;
     while (!live.empty()) {
+        ++rounds;
         const i64 m = static_cast<i64>(live.size());
         // Local maxima among still-free strong neighbours (both directions).
         for (auto& v : picked) v.clear();
@@ -218,7 +223,10 @@ CfSplit coarsen_pmis(const Csr& S, std::uint64_t seed) {
         for (const auto& v : keep) next.insert(next.end(), v.begin(), v.end()); // chunks in ascending order
         live.swap(next);
     }
-    return finish_split(S, st);
+    tm.mark("rounds", rounds);
+    CfSplit sp = finish_split(S, st);
+    tm.mark("finish split");
+    return sp;
 }
 
 Csr interp_direct(const Csr& A, const CfSplit& sp, const Csr& S) {

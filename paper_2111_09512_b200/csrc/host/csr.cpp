@@ -269,49 +269,41 @@ Csr csr_transpose(const Csr& A) {
     const i64 nnz = A.nnz();
     T.ci.resize(static_cast<size_t>(nnz));
     T.v.resize(static_cast<size_t>(nnz));
-    // Per-chunk column histograms give every chunk its own write cursor per
-    // column; chunks cover ascending row ranges, so each row of T receives its
-    // entries in ascending source-row order, exactly like the serial bucket fill.
-    const int C = std::max(1, std::min<int>(host_threads(), static_cast<int>(A.nrows / 8192 + 1)));
-    std::vector<std::vector<i64>> cnt(static_cast<size_t>(C));
-    auto chunk_lo = [&](int c) { return A.nrows * c / C; };
-    parallel_ranges(C, [&](i64 b, i64 e, int) {
-        for (i64 c = b; c < e; ++c) {
-            auto& h = cnt[c];
-            h.assign(static_cast<size_t>(A.ncols), 0);
-            for (i64 k = A.rp[chunk_lo(static_cast<int>(c))]; k < A.rp[chunk_lo(static_cast<int>(c) + 1)]; ++k)
-                ++h[A.ci[k]];
-        }
-    }, 1);
     T.rp.assign(static_cast<size_t>(A.ncols) + 1, 0);
-    // column totals, then per-chunk starting cursors
-    for (i64 j = 0; j < A.ncols; ++j) {
-        i64 tot = 0;
-        for (int c = 0; c < C; ++c) tot += cnt[c][j];
-        T.rp[j + 1] = tot;
-    }
+    // Column counts (atomic), offsets, an atomic-cursor scatter, then each row
+    // of T sorted by source row: the same ascending source-row order as the
+    // serial bucket fill, without per-thread column histograms (those were
+    // threads x ncols words — gigabytes at 100 M rows).
+    parallel_ranges(nnz, [&](i64 b, i64 e, int) {
+        for (i64 k = b; k < e; ++k)
+            std::atomic_ref<i64>(T.rp[static_cast<size_t>(A.ci[k]) + 1]).fetch_add(1, std::memory_order_relaxed);
+    }, 1 << 16);
     for (i64 j = 0; j < A.ncols; ++j) T.rp[j + 1] += T.rp[j];
+    RawVec<i64> cur(static_cast<size_t>(A.ncols));
     parallel_ranges(A.ncols, [&](i64 b, i64 e, int) {
-        for (i64 j = b; j < e; ++j) {
-            i64 cur = T.rp[j];
-            for (int c = 0; c < C; ++c) {
-                const i64 n = cnt[c][j];
-                cnt[c][j] = cur;
-                cur += n;
+        for (i64 j = b; j < e; ++j) cur[j] = T.rp[j];
+    });
+    parallel_ranges(A.nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i)
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                const i64 p = std::atomic_ref<i64>(cur[A.ci[k]]).fetch_add(1, std::memory_order_relaxed);
+                T.ci[p] = static_cast<i32>(i);
+                T.v[p] = A.v[k];
             }
+    });
+    parallel_ranges(A.ncols, [&](i64 b, i64 e, int) {
+        std::vector<std::pair<i32, double>> tmp;
+        for (i64 j = b; j < e; ++j) {
+            const i64 lo = T.rp[j], hi = T.rp[j + 1];
+            bool sorted = true;
+            for (i64 p = lo + 1; p < hi && sorted; ++p) sorted = T.ci[p - 1] < T.ci[p];
+            if (sorted) continue;
+            tmp.clear();
+            for (i64 p = lo; p < hi; ++p) tmp.emplace_back(T.ci[p], T.v[p]);
+            std::sort(tmp.begin(), tmp.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+            for (i64 p = lo; p < hi; ++p) T.ci[p] = tmp[p - lo].first, T.v[p] = tmp[p - lo].second;
         }
     });
-    parallel_ranges(C, [&](i64 b, i64 e, int) {
-        for (i64 c = b; c < e; ++c) {
-            auto& cur = cnt[c];
-            for (i64 i = chunk_lo(static_cast<int>(c)); i < chunk_lo(static_cast<int>(c) + 1); ++i)
-                for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
-                    const i64 p = cur[A.ci[k]]++;
-                    T.ci[p] = static_cast<i32>(i);
-                    T.v[p] = A.v[k];
-                }
-        }
-    }, 1);
     return T;
 }
 
