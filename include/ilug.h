@@ -53,9 +53,10 @@ ILUAMG_API int ilug_matrix_copy_csr(const iluamg_matrix* A, long long* row_start
 /* ILU(0)/ILUT per the config's ilu.* keys (src/ilu.cpp:56-265): L strict, U with diagonal. */
 ILUAMG_API int ilug_ilu_factorize(const iluamg_matrix* A, const iluamg_config* cfg,
                                   iluamg_matrix** L, iluamg_matrix** U);
-/* The factorisation the device objects use: ILU(0) on the device (level-free,
- * dependency-flag scheduled; bitwise equal to ilug_ilu_factorize), ILUT on the
- * host. ILUG_ILU0_DEVICE=0 forces the host path. */
+/* The factorisation the device objects use: ILU(0) (thread per row) and ILUT
+ * (warp per row) on the device, level-free and dependency-flag scheduled;
+ * bitwise equal to ilug_ilu_factorize. ILUG_ILU0_DEVICE=0 / ILUG_ILUT_DEVICE=0
+ * force the host path. */
 ILUAMG_API int ilug_ilu_factorize_device(const iluamg_matrix* A, const iluamg_config* cfg,
                                          iluamg_matrix** L, iluamg_matrix** U);
 

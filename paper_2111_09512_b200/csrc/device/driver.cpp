@@ -54,10 +54,9 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
                         bool use_graph, cudaStream_t st) {
     SolveOutcome oc;
     const auto t0 = std::chrono::steady_clock::now();
-    // The finest level's factorisation (ILUT on the host, whose row-to-row
-    // pipeline leaves most cores idle; ILU(0) on the device) runs concurrently
-    // with the host AMG setup, which does not need it and does not touch the
-    // GPU. Identical factors either way (same function, same input).
+    // The finest level's factorisation (ILU(0)/ILUT on the device) runs
+    // concurrently with the host AMG setup, which does not need it and does
+    // not touch the GPU. Identical factors either way (same function, same input).
     const SmootherConfig& s0 = ap.plan.for_level(0);
     std::future<HostFactors> f0;
     if (s0.kind == SmootherKind::ilu && A.nrows > ap.coarse_size)

@@ -169,6 +169,7 @@ HostFactors ilu0_device(const Csr& A, PivotPatch patch, cudaStream_t st) {
 
 HostFactors factorize(const Csr& A, const IluParams& p, cudaStream_t st) {
     if (p.variant == IluVariant::ilu0 && ilu0_on_device()) return ilu0_device(A, p.pivot_patch, st);
+    if (p.variant == IluVariant::ilut && ilut_on_device()) return ilut_device(A, p, st);
     return ilu_factorize(A, p);
 }
 

@@ -1,0 +1,474 @@
+// ILUT(droptol, lfill) on the device, bitwise equal to
+// the reference's dual-threshold ILUT (src/ilu.cpp:120-265) and to host/ilu.cpp.
+//
+// One warp per row, rows taken in ascending order from an atomic ticket by a
+// persistent grid, so a row only ever waits on rows claimed before it (no
+// deadlock whatever the residency). The working row w lives in the warp's
+// shared memory as a column-sorted list (col, value, flags). The reference's
+// min-heap of pending lower columns is exactly an ascending scan of that list:
+// fill from U row k only adds columns > k, so it lands behind the scan point.
+// Per multiplier k (ascending):
+//   wait for done[k] (epoch-stamped, acquire), m = w_k / u_kk, drop if
+//   |m| < tau, else every lane takes entries of U row k, binary-searches its
+//   column in the list (update w_j -= m*u_kj in place) or marks it new; new
+//   entries are merged by shifting the tail from the back, chunk by chunk.
+// Each w_j receives the serial algorithm's updates in the same order (k
+// ascending), with separate multiply/subtract (--fmad=false), so every value
+// is bitwise the reference's. Survivor selection follows src/ilu.cpp:190-219:
+// U part on |w| >= tau, pattern entries kept, fill ranked by (|w| desc,
+// column asc) for lfill slots; L part = kept multipliers with the same fill
+// cap. The U row is published (done[i], release) before the L part is
+// selected, since only U rows are on the row-to-row chain.
+//
+// Working rows longer than the shared-memory capacity set an overflow flag;
+// every remaining row then publishes immediately and the host relaunches with
+// a larger capacity (fewer warps per CTA). A bounded spin turns a scheduling
+// bug into an error instead of a hung GPU.
+#include "ilu0.hpp"
+
+#include <cub/device/device_scan.cuh>
+#include <cuda/atomic>
+
+#include <cfloat>
+#include <climits>
+#include <cstdlib>
+
+namespace ilug {
+
+namespace {
+
+constexpr unsigned char kLive = 1, kOrig = 2, kKept = 4, kSel = 8, kDrop = 16;
+
+struct IlutArgs {
+    i64 n;
+    const i64* rp;
+    const i32* ci;
+    const double* av;
+    const double* tau;   // droptol * |a_i|_2 per row
+    i64 lfill;
+    double anorm_f;
+    int patch;           // 0 error, 1 replace
+    double droptol;
+    const i64* uoff;     // U slot of row i: [uoff[i], uoff[i+1])
+    const i64* loff;
+    i32* uci;
+    double* uv;
+    i32* ulen;
+    i32* lci;
+    double* lv;
+    i32* llen;
+    unsigned* done;
+    const unsigned* epoch;
+    unsigned long long* ticket;
+    unsigned long long* first_zero;
+    unsigned* err;       // [0] wait timeout, [1] overflow (needed capacity)
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Rank fill candidates in [beg, end) that carry `want` and not kOrig: keep the
+// lfill best by (|w| desc, column asc) (the reference's nth_element comparator,
+// src/ilu.cpp:206-211). Pattern candidates are always kept. Marks kSel.
+__device__ __forceinline__ void select_part(const i32* scol, const double* sval, unsigned char* sflag, int beg,
+                                            int end, unsigned char want, bool upper, double tau, i64 lfill,
+                                            int lane) {
+    // pass 1: which candidates pass (U part: the threshold), count fill
+    int nfill = 0;
+    for (int q = beg + lane; q < end; q += 32) {
+        unsigned char f = sflag[q];
+        bool pass = (f & want) && !(upper && fabs(sval[q]) < tau);
+        if (pass) {
+            f |= kSel;
+            if (!(f & kOrig)) ++nfill;
+        } else {
+            f &= static_cast<unsigned char>(~kSel);
+        }
+        sflag[q] = f;
+    }
+    for (int o = 16; o; o >>= 1) nfill += __shfl_xor_sync(0xffffffffu, nfill, o);
+    __syncwarp();
+    if (nfill <= lfill) return;
+    // pass 2: rank each fill candidate against all others; losers get kDrop
+    // (the ranking reads only kSel/kOrig, so marking while others rank is safe)
+    for (int q = beg + lane; q < end; q += 32) {
+        const unsigned char f = sflag[q];
+        if (!(f & kSel) || (f & kOrig)) continue;
+        const double vq = fabs(sval[q]);
+        const i32 cq = scol[q];
+        i64 rank = 0;
+        for (int r = beg; r < end; ++r) {
+            const unsigned char g = sflag[r];
+            if (!(g & kSel) || (g & kOrig) || r == q) continue;
+            const double vr = fabs(sval[r]);
+            rank += (vr != vq) ? (vr > vq) : (scol[r] < cq);
+        }
+        if (rank >= lfill) sflag[q] = f | kDrop;
+    }
+    __syncwarp();
+    for (int q = beg + lane; q < end; q += 32) {
+        const unsigned char f = sflag[q];
+        if (f & kDrop) sflag[q] = static_cast<unsigned char>(f & ~(kSel | kDrop));
+    }
+    __syncwarp();
+}
+
+// Write the kSel entries of [beg, end) (ascending columns) to out_c/out_v; returns the count.
+__device__ __forceinline__ int emit(const i32* scol, const double* sval, const unsigned char* sflag, int beg,
+                                    int end, i32* out_c, double* out_v, int lane) {
+    int base = 0;
+    for (int q0 = beg; q0 < end; q0 += 32) {
+        const int q = q0 + lane;
+        const bool s = q < end && (sflag[q] & kSel);
+        const unsigned b = __ballot_sync(0xffffffffu, s);
+        if (s) {
+            const int o = base + __popc(b & lanemask_lt());
+            out_c[o] = scol[q];
+            out_v[o] = sval[q];
+        }
+        base += __popc(b);
+    }
+    return base;
+}
+
+template <int CAP, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_ilut(IlutArgs a) {
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // [WARPS*CAP values][WARPS*CAP columns][WARPS*32 merge positions][WARPS*CAP flags]
+    i32* const col_base = reinterpret_cast<i32*>(smem + static_cast<size_t>(WARPS) * CAP);
+    double* const sval = smem + static_cast<size_t>(warp) * CAP;
+    i32* const scol = col_base + static_cast<size_t>(warp) * CAP;
+    i32* const snew = col_base + static_cast<size_t>(WARPS) * CAP + warp * 32;
+    unsigned char* const sflag = reinterpret_cast<unsigned char*>(col_base + static_cast<size_t>(WARPS) * CAP +
+                                                                  WARPS * 32) + static_cast<size_t>(warp) * CAP;
+    const unsigned E = *a.epoch;
+    const unsigned full = 0xffffffffu;
+
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1ull);
+        const i64 i = static_cast<i64>(__shfl_sync(full, t, 0));
+        if (i >= a.n) return;
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> fi(a.done[i]);
+        const i64 beg = a.rp[i];
+        const int alen = static_cast<int>(a.rp[i + 1] - beg);
+        unsigned ov = 0;
+        if (lane == 0) ov = *reinterpret_cast<volatile unsigned*>(a.err + 1);
+        bool bad = __shfl_sync(full, ov, 0) != 0u;
+        if (!bad && alen > CAP) {
+            if (lane == 0) atomicMax(a.err + 1, static_cast<unsigned>(alen));
+            bad = true;
+        }
+        if (bad) { // capacity exceeded somewhere: publish and let the host relaunch
+            __syncwarp();
+            if (lane == 0) fi.store(E, cuda::memory_order_release);
+            continue;
+        }
+        for (int q = lane; q < alen; q += 32) {
+            scol[q] = a.ci[beg + q];
+            sval[q] = a.av[beg + q];
+            sflag[q] = kLive | kOrig;
+        }
+        int len = alen;
+        const double tau = a.tau[i];
+        __syncwarp();
+
+        int p = 0;
+        for (; p < len && !bad; ++p) {
+            const i32 k = scol[p];
+            if (k >= i) break;
+            cuda::atomic_ref<unsigned, cuda::thread_scope_device> fk(a.done[k]);
+            if (fk.load(cuda::memory_order_acquire) != E) {
+                long long spins = 0;
+                while (fk.load(cuda::memory_order_acquire) != E) {
+                    if (++spins > (1ll << 26)) { // seconds: a scheduling bug, not a slow row
+                        atomicExch(a.err, 1u);
+                        break;
+                    }
+                    __nanosleep(32);
+                }
+            }
+            const i64 ub = a.uoff[k];
+            const double m = sval[p] / a.uv[ub];
+            __syncwarp();
+            if (fabs(m) < tau) { // dual-threshold drop of the multiplier
+                if (lane == 0) sval[p] = 0.0, sflag[p] = 0;
+                __syncwarp();
+                continue;
+            }
+            if (lane == 0) sval[p] = m, sflag[p] = kLive | kKept | (sflag[p] & kOrig);
+            const int ul = a.ulen[k];
+            for (int c = 1; c < ul; c += 32) {
+                const int kk = c + lane;
+                const bool act = kk < ul;
+                const i32 j = act ? a.uci[ub + kk] : INT_MAX;
+                const double u = act ? a.uv[ub + kk] : 0.0;
+                int lo = p + 1, hi = len;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (scol[mid] < j) lo = mid + 1;
+                    else hi = mid;
+                }
+                const bool found = act && lo < len && scol[lo] == j;
+                const double prod = m * u;
+                if (found) sval[lo] = sval[lo] - prod;
+                const unsigned nm = __ballot_sync(full, act && !found);
+                if (nm == 0u) {
+                    __syncwarp();
+                    continue;
+                }
+                const int nnew = __popc(nm);
+                if (len + nnew > CAP) {
+                    if (lane == 0) atomicMax(a.err + 1, static_cast<unsigned>(len + nnew));
+                    bad = true;
+                    break;
+                }
+                const int rank = __popc(nm & lanemask_lt());
+                if (act && !found) snew[rank] = lo;
+                __syncwarp();
+                const int minpos = snew[0];
+                // shift the tail [minpos, len) up by the number of new entries before
+                // each element, from the back (destinations never reach unread slots)
+                for (int top = len; top > minpos; top -= 32) {
+                    const int q = top - 1 - lane;
+                    const bool mv = q >= minpos;
+                    i32 cc = 0;
+                    double vv = 0.0;
+                    unsigned char ff = 0;
+                    int dst = 0;
+                    if (mv) {
+                        cc = scol[q], vv = sval[q], ff = sflag[q];
+                        int l2 = 0, h2 = nnew;
+                        while (l2 < h2) {
+                            const int md = (l2 + h2) >> 1;
+                            if (snew[md] <= q) l2 = md + 1;
+                            else h2 = md;
+                        }
+                        dst = q + l2;
+                    }
+                    __syncwarp();
+                    if (mv) scol[dst] = cc, sval[dst] = vv, sflag[dst] = ff;
+                    __syncwarp();
+                }
+                if (act && !found) {
+                    const int dst = lo + rank;
+                    scol[dst] = j;
+                    sval[dst] = 0.0 - prod; // w_j was 0.0: 0.0 - m*u, not -(m*u)
+                    sflag[dst] = kLive;
+                }
+                len += nnew;
+                __syncwarp();
+            }
+        }
+        if (bad) {
+            __syncwarp();
+            if (lane == 0) fi.store(E, cuda::memory_order_release);
+            continue;
+        }
+        // p: first position with column >= i
+        const bool hasd = p < len && scol[p] == static_cast<i32>(i);
+        double d = hasd ? sval[p] : 0.0;
+        if (d == 0.0) {
+            if (a.patch == 0) {
+                if (lane == 0) atomicMin(a.first_zero, static_cast<unsigned long long>(i));
+                d = 1.0; // placeholder; the factorisation is abandoned
+            } else {
+                // patched_pivot(0.0, droptol, |a_i|_2, |A|_F): max(droptol*|a_i|_2, 1e-16*|A|_F)
+                const double zr = a.tau[i], fl = 1e-16 * a.anorm_f;
+                d = zr < fl ? fl : zr;
+                if (d == 0.0) d = DBL_MIN;
+            }
+        }
+        const int ub = p + (hasd ? 1 : 0);
+        select_part(scol, sval, sflag, ub, len, kLive, true, tau, a.lfill, lane);
+        const i64 uo = a.uoff[i];
+        const int nu = emit(scol, sval, sflag, ub, len, a.uci + uo + 1, a.uv + uo + 1, lane);
+        if (lane == 0) {
+            a.uci[uo] = static_cast<i32>(i);
+            a.uv[uo] = d;
+            a.ulen[i] = nu + 1;
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) fi.store(E, cuda::memory_order_release);
+
+        select_part(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, lane);
+        const i64 lo = a.loff[i];
+        const int nl = emit(scol, sval, sflag, 0, p, a.lci + lo, a.lv + lo, lane);
+        if (lane == 0) a.llen[i] = nl;
+        __syncwarp();
+    }
+}
+
+__global__ void k_ilut_prep(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci,
+                            const double* __restrict__ av, double droptol, i64 lfill, double* __restrict__ tau,
+                            i64* __restrict__ ucap, i64* __restrict__ lcap) {
+    const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    i64 lo = 0, up = 0;
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+        s = s + av[k] * av[k]; // row_two_norm: ascending, from 0.0
+        lo += ci[k] < i;
+        up += ci[k] > i;
+    }
+    tau[i] = droptol * sqrt(s);
+    ucap[i + 1] = 1 + up + lfill;
+    lcap[i + 1] = lo + lfill;
+    if (i == 0) ucap[0] = lcap[0] = 0;
+}
+
+__global__ void k_ilut_bump(unsigned* epoch, unsigned long long* ticket, unsigned* err) {
+    *epoch = *epoch + 1u;
+    *ticket = 0ull;
+    err[0] = err[1] = 0u;
+}
+
+__global__ void k_len_to_rp(i64 n, const i32* __restrict__ len, i64* __restrict__ rp1) {
+    const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) rp1[i + 1] = len[i];
+    if (i == 0) rp1[0] = 0;
+}
+
+// warp per row: slot -> compact CSR
+__global__ void k_compact(i64 n, const i64* __restrict__ off, const i64* __restrict__ rp, const i32* __restrict__ sc,
+                          const double* __restrict__ sv, i32* __restrict__ oc, double* __restrict__ ov) {
+    const i64 i = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const i64 b = rp[i], len = rp[i + 1] - b, o = off[i];
+    for (i64 q = lane; q < len; q += 32) {
+        oc[b + q] = sc[o + q];
+        ov[b + q] = sv[o + q];
+    }
+}
+
+void inclusive_scan(i64* d, i64 count, cudaStream_t st) {
+    size_t tmp = 0;
+    ILUG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, d, d, count, st));
+    DBuf<char> t(static_cast<i64>(tmp));
+    ILUG_CUDA(cub::DeviceScan::InclusiveSum(t.p, tmp, d, d, count, st));
+    ILUG_CUDA(cudaStreamSynchronize(st)); // t is freed on return
+}
+
+template <int CAP, int WARPS>
+void launch_ilut(const IlutArgs& a, cudaStream_t st) {
+    constexpr size_t smem = static_cast<size_t>(WARPS) * CAP * (sizeof(double) + sizeof(i32) + 1) +
+                            static_cast<size_t>(WARPS) * 32 * sizeof(i32);
+    auto* fn = k_ilut<CAP, WARPS>;
+    ILUG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, smem));
+    if (per_sm < 1) fail_invalid("ilut (device): kernel does not fit an SM");
+    const i64 grid = std::min<i64>(static_cast<i64>(per_sm) * device_sm_count(), (a.n + WARPS - 1) / WARPS);
+    fn<<<static_cast<unsigned>(std::max<i64>(grid, 1)), WARPS * 32, smem, st>>>(a);
+    ILUG_LAUNCH_CHECK();
+}
+
+} // namespace
+
+bool ilut_on_device() {
+    const char* e = std::getenv("ILUG_ILUT_DEVICE");
+    return !(e && e[0] == '0');
+}
+
+HostFactors ilut_device(const Csr& A, const IluParams& p, cudaStream_t st) {
+    if (A.nrows != A.ncols) fail_invalid("ilut: matrix must be square");
+    if (!(p.droptol >= 0.0) || !std::isfinite(p.droptol)) fail_invalid("ilut: droptol must be finite and >= 0");
+    if (p.lfill < 0) fail_invalid("ilut: lfill must be >= 0");
+    const i64 n = A.nrows;
+    HostFactors f;
+    for (Csr* M : {&f.L, &f.U}) {
+        M->nrows = M->ncols = n;
+        M->rp.assign(static_cast<size_t>(n) + 1, 0);
+    }
+    if (n == 0) return f;
+    SetupTimer tm("ilut-device");
+    const double anorm_f = frobenius_norm(A);
+    const i64 nnz = A.nnz();
+    DBuf<i64> rp, uoff(n + 1), loff(n + 1);
+    DBuf<i32> ci;
+    DBuf<double> av, tau(n);
+    rp.upload(A.rp.data(), n + 1, st);
+    ci.upload(A.ci.data(), nnz, st);
+    av.upload(A.v.data(), nnz, st);
+    const unsigned g = static_cast<unsigned>((n + 255) / 256);
+    k_ilut_prep<<<g, 256, 0, st>>>(n, rp.p, ci.p, av.p, p.droptol, p.lfill, tau.p, uoff.p, loff.p);
+    ILUG_LAUNCH_CHECK();
+    inclusive_scan(uoff.p, n + 1, st);
+    inclusive_scan(loff.p, n + 1, st);
+    i64 ucap = 0, lcap = 0;
+    ILUG_CUDA(cudaMemcpyAsync(&ucap, uoff.p + n, sizeof ucap, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaMemcpyAsync(&lcap, loff.p + n, sizeof lcap, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    tm.mark("upload + slots");
+    DBuf<i32> uci(ucap), lci(lcap), ulen(n), llen(n);
+    DBuf<double> uv(ucap), lv(lcap);
+    DBuf<unsigned> sync(n + 3); // done flags, epoch, err[2]
+    DBuf<unsigned long long> ctl(2); // ticket, first zero
+    ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
+    IlutArgs a{n,       rp.p,   ci.p,   av.p,   tau.p,   p.lfill, anorm_f, p.pivot_patch == PivotPatch::error ? 0 : 1,
+               p.droptol, uoff.p, loff.p, uci.p, uv.p, ulen.p, lci.p, lv.p, llen.p, sync.p, sync.p + n,
+               ctl.p,   ctl.p + 1, sync.p + n + 1};
+    unsigned err[2] = {0, 0};
+    for (int cap_level = 0;; ++cap_level) {
+        const unsigned long long init[2] = {0ull, ~0ull};
+        ILUG_CUDA(cudaMemcpyAsync(ctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+        k_ilut_bump<<<1, 1, 0, st>>>(sync.p + n, ctl.p, sync.p + n + 1);
+        ILUG_LAUNCH_CHECK();
+        if (cap_level == 0)
+            launch_ilut<256, 8>(a, st);
+        else if (cap_level == 1)
+            launch_ilut<1024, 4>(a, st);
+        else
+            launch_ilut<6144, 2>(a, st);
+        ILUG_CUDA(cudaMemcpyAsync(err, sync.p + n + 1, sizeof err, cudaMemcpyDeviceToHost, st));
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        if (err[0]) fail_numeric("ilut (device): dependency wait timed out (scheduling error)");
+        if (err[1] == 0) break;
+        if (cap_level == 2 || err[1] > 6144)
+            fail_invalid("ilut (device): a working row needs " + std::to_string(err[1]) +
+                         " entries (> 6144); set ILUG_ILUT_DEVICE=0 to factor on the host");
+    }
+    tm.mark("factor kernel");
+    unsigned long long fz = 0;
+    ILUG_CUDA(cudaMemcpyAsync(&fz, ctl.p + 1, sizeof fz, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    if (fz != ~0ull)
+        fail_numeric("zero pivot at step " + std::to_string(fz) +
+                     " (no pivoting; rerun with pivot_patch=replace to substitute)");
+    // compact the slots into CSR and download
+    for (int part = 0; part < 2; ++part) {
+        Csr& M = part == 0 ? f.L : f.U;
+        const DBuf<i32>& len = part == 0 ? llen : ulen;
+        DBuf<i64> mrp(n + 1);
+        k_len_to_rp<<<g, 256, 0, st>>>(n, len.p, mrp.p);
+        ILUG_LAUNCH_CHECK();
+        inclusive_scan(mrp.p, n + 1, st);
+        i64 nz = 0;
+        ILUG_CUDA(cudaMemcpyAsync(&nz, mrp.p + n, sizeof nz, cudaMemcpyDeviceToHost, st));
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        DBuf<i32> mc(nz);
+        DBuf<double> mv(nz);
+        if (nz > 0) {
+            const unsigned gw = static_cast<unsigned>((n * 32 + 255) / 256);
+            k_compact<<<gw, 256, 0, st>>>(n, part == 0 ? loff.p : uoff.p, mrp.p, part == 0 ? lci.p : uci.p,
+                                          part == 0 ? lv.p : uv.p, mc.p, mv.p);
+            ILUG_LAUNCH_CHECK();
+        }
+        M.ci.resize(static_cast<size_t>(nz));
+        M.v.resize(static_cast<size_t>(nz));
+        mrp.download(M.rp.data(), st);
+        mc.download(M.ci.data(), st);
+        mv.download(M.v.data(), st);
+        ILUG_CUDA(cudaStreamSynchronize(st));
+    }
+    tm.mark("compact + download");
+    return f;
+}
+
+} // namespace ilug
