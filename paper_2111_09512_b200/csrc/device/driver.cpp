@@ -58,11 +58,11 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     // concurrently with the host AMG setup, which does not need it and does
     // not touch the GPU. Identical factors either way (same function, same input).
     const SmootherConfig& s0 = ap.plan.for_level(0);
-    std::future<HostFactors> f0;
+    std::future<DevFactors> f0;
     if (s0.kind == SmootherKind::ilu && A.nrows > ap.coarse_size)
-        f0 = std::async(std::launch::async, [&] { return factorize(A, s0.ilu_params, st); });
+        f0 = std::async(std::launch::async, [&] { return factorize_resident(A, s0.ilu_params, st, true); });
     oc.hier = amg_setup(A, ap);
-    HostFactors pre;
+    DevFactors pre;
     const bool have_pre = f0.valid();
     if (have_pre) pre = f0.get();
     DeviceHierarchy dh;

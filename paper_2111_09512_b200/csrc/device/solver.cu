@@ -13,6 +13,11 @@ void DeviceMatrix::build(const Csr& host, cudaStream_t st) {
     sell_from_host(A, host, Part::all, st);
 }
 
+void DeviceMatrix::build(const Csr& host, const i64* rp, const i32* ci, const double* v, cudaStream_t st) {
+    n = host.nrows;
+    sell_from_device_rows(A, host.nrows, host.ncols, host.rp, 0, rp, ci, v, Part::all, st);
+}
+
 void DeviceMatrix::residual(const double* x, const double* b, double* r, cudaStream_t st) const {
     if (!halo) return ilug::residual(A, x, b, r, st);
     halo->exchange(x, st);
@@ -28,23 +33,37 @@ void DeviceMatrix::spmv(const double* x, double* y, cudaStream_t st) const {
 // ============================================================ DeviceIlu (K1-K5)
 void DeviceIlu::build(const HostFactors& f, ScalingKind scaling, UpperIteration upper,
                       bool direct_plans, cudaStream_t st) {
-    n_ = f.U.nrows;
+    DevFactors df = DevFactors::upload(f, st);
+    finish(df, &f, scaling, upper, direct_plans, st);
+}
+
+void DeviceIlu::build(DevFactors&& df, ScalingKind scaling, UpperIteration upper, bool direct_plans,
+                      cudaStream_t st) {
+    DevFactors own = std::move(df);
+    finish(own, nullptr, scaling, upper, direct_plans, st);
+}
+
+void DeviceIlu::finish(DevFactors& df, const HostFactors* host, ScalingKind scaling, UpperIteration upper,
+                       bool direct_plans, cudaStream_t st) {
+    n_ = df.n;
     scaling_ = scaling;
     upper_ = upper;
-    sell_from_host(Ls_, f.L, Part::all, st);
-
-    DBuf<i64> rp;
-    DBuf<i32> ci;
-    DBuf<double> v;
-    rp.upload(f.U.rp.data(), n_ + 1, st);
-    ci.upload(f.U.ci.data(), f.U.nnz(), st);
-    v.upload(f.U.v.data(), f.U.nnz(), st);
+    // host patterns are needed only by the wavefront and level-set plans, and by
+    // factors whose U rows do not all start with the diagonal
+    HostFactors pulled;
+    const bool need_host = !host && (wave_enabled(n_) || direct_plans || !df.diag_first);
+    if (need_host) pulled = df.to_host(st);
+    const HostFactors* hp = host ? host : (need_host ? &pulled : nullptr);
+    sell_from_device_rows(Ls_, n_, n_, df.Lrp_h, 0, df.Lrp.p, df.Lci.p, df.Lv.p, Part::all, st);
+    const i64* rp = df.Urp.p;
+    const i32* ci = df.Uci.p;
+    double* v = df.Uv.p;
 
     const bool scale = upper == UpperIteration::scaled && scaling != ScalingKind::none;
     if (!scale) {
         // Unscaled factor: keep D for the Jacobi iteration / direct division.
         d_.alloc(n_);
-        const i64 bad = extract_diag(n_, rp.p, ci.p, v.p, d_.p, st);
+        const i64 bad = extract_diag(n_, rp, ci, v, d_.p, st);
         if (bad >= 0 && (upper == UpperIteration::jacobi || direct_plans))
             fail_numeric("ilu factors: zero diagonal entry in U at row " + std::to_string(bad));
     } else {
@@ -55,20 +74,22 @@ void DeviceIlu::build(const HostFactors& f, ScalingKind scaling, UpperIteration 
             dr.alloc(n_);
             dc.alloc(n_);
         }
-        const i64 bad = scale_upper(n_, rp.p, ci.p, v.p, scaling == ScalingKind::row ? 1 : 2, rs_.p,
-                                    cs_.p, dr.p, dc.p, st);
+        const i64 bad = scale_upper(n_, rp, ci, v, scaling == ScalingKind::row ? 1 : 2, rs_.p, cs_.p, dr.p, dc.p, st);
         if (bad >= 0)
             fail_numeric(std::string(scaling == ScalingKind::row ? "row_scale" : "row_col_scale") +
                          ": zero diagonal entry in U at row " + std::to_string(bad));
     }
-    sell_from_device_csr(Us_, f.U, rp.p, ci.p, v.p, Part::strict_upper, {}, st);
+    if (df.diag_first)
+        sell_from_device_rows(Us_, n_, n_, df.Urp_h, 1, rp, ci, v, Part::strict_upper, st);
+    else
+        sell_from_device_csr(Us_, hp->U, rp, ci, v, Part::strict_upper, {}, st);
     if (wave_enabled(n_)) {
-        wave_build(wave_L_, f.L, Ls_, false, st);
-        wave_build(wave_U_, f.U, Us_, true, st);
+        wave_build(wave_L_, hp->L, Ls_, false, st);
+        wave_build(wave_U_, hp->U, Us_, true, st);
     }
     if (direct_plans) {
-        lower_plan_.build(f.L, LevelPlan::Kind::lower_unit, st);
-        upper_plan_.build(f.U, LevelPlan::Kind::upper, st, v.p);
+        lower_plan_.build(hp->L, LevelPlan::Kind::lower_unit, st);
+        upper_plan_.build(hp->U, LevelPlan::Kind::upper, st, v);
     }
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
@@ -186,7 +207,7 @@ Vec inverted_diag(const Csr& A, const char* what) {
 } // namespace
 
 void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg,
-                           cudaStream_t st, HostFactors* pre) {
+                           cudaStream_t st, DevFactors* pre) {
     if (cfg.sweeps < 0) fail_invalid("build_smoother_state: sweeps must be >= 0");
     if (cfg.poly_degree < 0) fail_invalid("build_smoother_state: poly_degree must be >= 0");
     cfg_ = cfg;
@@ -231,9 +252,9 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         const bool rich = cfg.trisolve.mode == TriSolveMode::richardson;
         if (rich && cfg.scaling == ScalingKind::none && cfg.trisolve.upper == UpperIteration::scaled)
             fail_invalid("ilu smoother: the iterative U solve requires row or row/col scaling");
-        const HostFactors f = pre ? std::move(*pre) : factorize(A, cfg.ilu_params, st);
         ilu_ = std::make_unique<DeviceIlu>();
-        ilu_->build(f, cfg.scaling, rich ? cfg.trisolve.upper : UpperIteration::scaled, !rich, st);
+        ilu_->build(pre ? std::move(*pre) : factorize_resident(A, cfg.ilu_params, st), cfg.scaling,
+                    rich ? cfg.trisolve.upper : UpperIteration::scaled, !rich, st);
         break;
     }
     case SmootherKind::schur_ilut:
@@ -384,7 +405,7 @@ DeviceHierarchy::~DeviceHierarchy() {
     if (exec_) cudaGraphExecDestroy(exec_);
 }
 
-void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st, HostFactors* level0) {
+void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st, DevFactors* level0) {
     const int L = static_cast<int>(h.levels.size());
     levels_ = std::vector<Lev>(static_cast<size_t>(L));
     SetupTimer tm("device");
@@ -392,7 +413,13 @@ void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st, HostFactors
         const HostLevel& hl = h.levels[k];
         Lev& lv = levels_[k];
         lv.n = hl.A.nrows;
-        lv.A.build(hl.A, st);
+        if (k == 0 && level0 && level0->Av.n == hl.A.nnz() && hl.A.nnz() > 0) {
+            lv.A.build(hl.A, level0->Arp.p, level0->Aci.p, level0->Av.p, st); // the factorisation's upload
+            ILUG_CUDA(cudaStreamSynchronize(st));
+            level0->Arp.release(), level0->Aci.release(), level0->Av.release();
+        } else {
+            lv.A.build(hl.A, st);
+        }
         if (k + 1 < L) {
             sell_from_host(lv.P, hl.P, Part::all, st);
             sell_from_host(lv.R, hl.R, Part::all, st);

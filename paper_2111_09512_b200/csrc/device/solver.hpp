@@ -37,6 +37,8 @@ struct DeviceMatrix {
     i64 n = 0;
     const HaloExchange* halo = nullptr;
     void build(const Csr& host, cudaStream_t st);
+    /// From a device CSR copy of `host` (same rows/columns/values).
+    void build(const Csr& host, const i64* rp, const i32* ci, const double* v, cudaStream_t st);
     void residual(const double* x, const double* b, double* r, cudaStream_t st) const;
     void spmv(const double* x, double* y, cudaStream_t st) const;
 };
@@ -49,6 +51,10 @@ public:
     /// `direct_plans` is set (trisolve.mode=direct or explicit sptrsv use).
     void build(const HostFactors& f, ScalingKind scaling, UpperIteration upper, bool direct_plans,
                cudaStream_t st);
+    /// Same from device-resident factors (consumed: U is scaled in place and
+    /// packed, then the CSR copies are freed). No host round trip of the
+    /// factors unless a wavefront or level-set plan needs the patterns.
+    void build(DevFactors&& f, ScalingKind scaling, UpperIteration upper, bool direct_plans, cudaStream_t st);
 
     i64 n() const { return n_; }
     ScalingKind scaling() const { return scaling_; }
@@ -92,6 +98,9 @@ public:
     const DBuf<double>& cs_buf() const { return cs_; }
 
 private:
+    void finish(DevFactors& df, const HostFactors* host, ScalingKind scaling, UpperIteration upper,
+                bool direct_plans, cudaStream_t st);
+
     i64 n_ = 0;
     ScalingKind scaling_ = ScalingKind::row;
     UpperIteration upper_ = UpperIteration::scaled;
@@ -99,7 +108,6 @@ private:
     DBuf<double> rs_, cs_, d_;
     LevelPlan lower_plan_, upper_plan_;
     WavePlan wave_L_, wave_U_; // fused multi-sweep plans (large n only, see wave_enabled)
-    Csr U_pattern_;          // host structure of U (values are the unscaled ones)
 };
 
 /// K9: the ILUT Schur-complement smoother (src/schur.cpp:137-219) on the device.
@@ -131,7 +139,7 @@ class DeviceSmoother {
 public:
     /// `pre`: factors of A computed ahead (moved from; ILU kinds only).
     void build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg, cudaStream_t st,
-               HostFactors* pre = nullptr);
+               DevFactors* pre = nullptr);
     /// x <- smooth(A, b, x). `x_zero`: caller guarantees x == 0 on entry, so the
     /// first residual is b itself (bitwise what the SpMV would give).
     void smooth(const double* b, double* x, bool x_zero, cudaStream_t st) const;
@@ -158,7 +166,7 @@ private:
 class DeviceHierarchy {
 public:
     /// `level0`: the finest level's ILU factors computed ahead (see solve_with).
-    void build(const HostHierarchy& h, cudaStream_t st, HostFactors* level0 = nullptr);
+    void build(const HostHierarchy& h, cudaStream_t st, DevFactors* level0 = nullptr);
     /// z = M(r) with z zeroed first (the driver's precond lambda, src/driver.cpp:182-185).
     void vcycle(const double* r, double* z, cudaStream_t st);
     /// Same, without graph replay (direct kernel launches).

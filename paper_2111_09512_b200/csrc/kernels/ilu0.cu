@@ -82,6 +82,23 @@ k_ilu0(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, const i64*
     fi.store(E, cuda::memory_order_release);
 }
 
+// w (A's pattern) -> strict L and U (diagonal first) on the device, thread per row
+__global__ void k_ilu0_split(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci,
+                             const i64* __restrict__ dpos, const double* __restrict__ w,
+                             const i64* __restrict__ lrp, const i64* __restrict__ urp, i32* __restrict__ lci,
+                             double* __restrict__ lv, i32* __restrict__ uci, double* __restrict__ uv) {
+    const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    i64 pl = lrp[i], pu = urp[i];
+    const i64 di = dpos[i];
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+        if (k < di)
+            lci[pl] = ci[k], lv[pl++] = w[k];
+        else
+            uci[pu] = ci[k], uv[pu++] = w[k];
+    }
+}
+
 } // namespace
 
 bool ilu0_on_device() {
@@ -89,7 +106,42 @@ bool ilu0_on_device() {
     return !(e && e[0] == '0');
 }
 
-HostFactors ilu0_device(const Csr& A, PivotPatch patch, cudaStream_t st) {
+HostFactors DevFactors::to_host(cudaStream_t st) const {
+    HostFactors f;
+    for (int part = 0; part < 2; ++part) {
+        Csr& M = part == 0 ? f.L : f.U;
+        M.nrows = M.ncols = n;
+        M.rp = part == 0 ? Lrp_h : Urp_h;
+        const DBuf<i32>& c = part == 0 ? Lci : Uci;
+        const DBuf<double>& v = part == 0 ? Lv : Uv;
+        M.ci.resize(static_cast<size_t>(c.n));
+        M.v.resize(static_cast<size_t>(v.n));
+        c.download(M.ci.data(), st);
+        v.download(M.v.data(), st);
+    }
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    return f;
+}
+
+DevFactors DevFactors::upload(const HostFactors& f, cudaStream_t st) {
+    DevFactors d;
+    d.n = f.U.nrows;
+    d.Lrp_h = f.L.rp;
+    d.Urp_h = f.U.rp;
+    d.Lrp.upload(f.L.rp.data(), d.n + 1, st);
+    d.Urp.upload(f.U.rp.data(), d.n + 1, st);
+    d.Lci.upload(f.L.ci.data(), f.L.nnz(), st);
+    d.Uci.upload(f.U.ci.data(), f.U.nnz(), st);
+    d.Lv.upload(f.L.v.data(), f.L.nnz(), st);
+    d.Uv.upload(f.U.v.data(), f.U.nnz(), st);
+    d.diag_first = true;
+    for (i64 i = 0; i < d.n && d.diag_first; ++i)
+        d.diag_first = f.U.rp[i] < f.U.rp[i + 1] && f.U.ci[f.U.rp[i]] == i;
+    ILUG_CUDA(cudaStreamSynchronize(st)); // host vectors may die after return
+    return d;
+}
+
+DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool keep_A) {
     if (A.nrows != A.ncols) fail_invalid("ilu0: matrix must be square");
     const i64 n = A.nrows;
     std::vector<i64> dpos(static_cast<size_t>(n), -1);
@@ -104,73 +156,83 @@ HostFactors ilu0_device(const Csr& A, PivotPatch patch, cudaStream_t st) {
                          ") is structurally absent");
     const double anorm_f = frobenius_norm(A);
     const i64 nnz = A.nnz();
-    std::vector<double> w(static_cast<size_t>(nnz));
-    if (n > 0) {
-        DBuf<i64> rp, dp;
-        DBuf<i32> ci;
-        DBuf<double> a, wd;
-        rp.upload(A.rp.data(), n + 1, st);
-        ci.upload(A.ci.data(), nnz, st);
-        dp.upload(dpos.data(), n, st);
-        a.upload(A.v.data(), nnz, st);
-        wd.alloc(nnz);
-        ILUG_CUDA(cudaMemcpyAsync(wd.p, a.p, static_cast<size_t>(nnz) * sizeof(double), cudaMemcpyDeviceToDevice,
-                                  st));
-        DBuf<unsigned> sync(n + 3); // done flags, epoch, ticket, error
-        ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
-        DBuf<unsigned long long> fz(1);
-        const unsigned long long init = ~0ull;
-        ILUG_CUDA(cudaMemcpyAsync(fz.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
-        unsigned* epoch = sync.p + n;
-        k_ilu0_bump<<<1, 1, 0, st>>>(epoch, epoch + 1);
-        ILUG_LAUNCH_CHECK();
-        const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
-        k_ilu0<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dp.p, a.p, wd.p, sync.p, epoch, epoch + 1, fz.p, epoch + 2,
-                                     patch == PivotPatch::error ? 0 : 1, anorm_f);
-        ILUG_LAUNCH_CHECK();
-        unsigned long long h = 0;
-        unsigned bad = 0;
-        ILUG_CUDA(cudaMemcpyAsync(&h, fz.p, sizeof h, cudaMemcpyDeviceToHost, st));
-        ILUG_CUDA(cudaMemcpyAsync(&bad, epoch + 2, sizeof bad, cudaMemcpyDeviceToHost, st));
-        wd.download(w.data(), st);
-        ILUG_CUDA(cudaStreamSynchronize(st));
-        if (bad) fail_numeric("ilu0 (device): dependency wait timed out (scheduling error)");
-        if (h != ~0ull)
-            fail_numeric("zero pivot at step " + std::to_string(h) +
-                         " (no pivoting; rerun with pivot_patch=replace to substitute)");
-    }
-    // split into strict L and U (with diagonal)
-    HostFactors f;
-    for (Csr* M : {&f.L, &f.U}) {
-        M->nrows = M->ncols = n;
-        M->rp.assign(static_cast<size_t>(n) + 1, 0);
-    }
+    DevFactors f;
+    f.n = n;
+    f.diag_first = true;
+    f.Lrp_h.assign(static_cast<size_t>(n) + 1, 0);
+    f.Urp_h.assign(static_cast<size_t>(n) + 1, 0);
     for (i64 i = 0; i < n; ++i) {
-        f.L.rp[i + 1] = f.L.rp[i] + (dpos[i] - A.rp[i]);
-        f.U.rp[i + 1] = f.U.rp[i] + (A.rp[i + 1] - dpos[i]);
+        f.Lrp_h[i + 1] = f.Lrp_h[i] + (dpos[i] - A.rp[i]);
+        f.Urp_h[i + 1] = f.Urp_h[i] + (A.rp[i + 1] - dpos[i]);
     }
-    f.L.ci.resize(static_cast<size_t>(f.L.rp[n]));
-    f.L.v.resize(static_cast<size_t>(f.L.rp[n]));
-    f.U.ci.resize(static_cast<size_t>(f.U.rp[n]));
-    f.U.v.resize(static_cast<size_t>(f.U.rp[n]));
-    parallel_ranges(n, [&](i64 b, i64 e, int) {
-        for (i64 i = b; i < e; ++i) {
-            i64 pl = f.L.rp[i], pu = f.U.rp[i];
-            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
-                if (k < dpos[i])
-                    f.L.ci[pl] = A.ci[k], f.L.v[pl++] = w[k];
-                else
-                    f.U.ci[pu] = A.ci[k], f.U.v[pu++] = w[k];
-            }
-        }
-    });
+    if (n == 0) {
+        f.Lrp.upload(f.Lrp_h.data(), 1, st);
+        f.Urp.upload(f.Urp_h.data(), 1, st);
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        return f;
+    }
+    DBuf<i64> rp, dp;
+    DBuf<i32> ci;
+    DBuf<double> a, wd;
+    rp.upload(A.rp.data(), n + 1, st);
+    ci.upload(A.ci.data(), nnz, st);
+    dp.upload(dpos.data(), n, st);
+    a.upload(A.v.data(), nnz, st);
+    wd.alloc(nnz);
+    ILUG_CUDA(cudaMemcpyAsync(wd.p, a.p, static_cast<size_t>(nnz) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    DBuf<unsigned> sync(n + 3); // done flags, epoch, ticket, error
+    ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
+    DBuf<unsigned long long> fz(1);
+    const unsigned long long init = ~0ull;
+    ILUG_CUDA(cudaMemcpyAsync(fz.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
+    unsigned* epoch = sync.p + n;
+    k_ilu0_bump<<<1, 1, 0, st>>>(epoch, epoch + 1);
+    ILUG_LAUNCH_CHECK();
+    const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
+    k_ilu0<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dp.p, a.p, wd.p, sync.p, epoch, epoch + 1, fz.p, epoch + 2,
+                                 patch == PivotPatch::error ? 0 : 1, anorm_f);
+    ILUG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    unsigned bad = 0;
+    ILUG_CUDA(cudaMemcpyAsync(&h, fz.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaMemcpyAsync(&bad, epoch + 2, sizeof bad, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    if (bad) fail_numeric("ilu0 (device): dependency wait timed out (scheduling error)");
+    if (h != ~0ull)
+        fail_numeric("zero pivot at step " + std::to_string(h) +
+                     " (no pivoting; rerun with pivot_patch=replace to substitute)");
+    f.Lrp.upload(f.Lrp_h.data(), n + 1, st);
+    f.Urp.upload(f.Urp_h.data(), n + 1, st);
+    f.Lci.alloc(f.Lrp_h[n]);
+    f.Lv.alloc(f.Lrp_h[n]);
+    f.Uci.alloc(f.Urp_h[n]);
+    f.Uv.alloc(f.Urp_h[n]);
+    k_ilu0_split<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dp.p, wd.p, f.Lrp.p, f.Urp.p, f.Lci.p, f.Lv.p, f.Uci.p,
+                                       f.Uv.p);
+    ILUG_LAUNCH_CHECK();
+    ILUG_CUDA(cudaStreamSynchronize(st)); // temporaries die at scope exit
+    if (keep_A) f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(a);
     return f;
+}
+
+HostFactors ilu0_device(const Csr& A, PivotPatch patch, cudaStream_t st) {
+    return ilu0_resident(A, patch, st).to_host(st);
+}
+
+HostFactors ilut_device(const Csr& A, const IluParams& p, cudaStream_t st) {
+    return ilut_resident(A, p, st).to_host(st);
 }
 
 HostFactors factorize(const Csr& A, const IluParams& p, cudaStream_t st) {
     if (p.variant == IluVariant::ilu0 && ilu0_on_device()) return ilu0_device(A, p.pivot_patch, st);
     if (p.variant == IluVariant::ilut && ilut_on_device()) return ilut_device(A, p, st);
     return ilu_factorize(A, p);
+}
+
+DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A) {
+    if (p.variant == IluVariant::ilu0 && ilu0_on_device()) return ilu0_resident(A, p.pivot_patch, st, keep_A);
+    if (p.variant == IluVariant::ilut && ilut_on_device()) return ilut_resident(A, p, st, keep_A);
+    return DevFactors::upload(ilu_factorize(A, p), st);
 }
 
 } // namespace ilug

@@ -6,6 +6,36 @@
 
 namespace ilug {
 
+/// Incomplete factors resident on the device, CSR: L strict (unit diagonal
+/// implicit), U upper. `diag_first`: every U row starts with its diagonal
+/// (true for every factorisation here), so the strict-upper part of row r has
+/// Urp_h[r+1] - Urp_h[r] - 1 entries and the SELL layout needs only the row
+/// starts on the host (Lrp_h / Urp_h), not the columns or values.
+struct DevFactors {
+    i64 n = 0;
+    DBuf<i64> Lrp, Urp;
+    DBuf<i32> Lci, Uci;
+    DBuf<double> Lv, Uv;
+    RawVec<i64> Lrp_h, Urp_h;
+    bool diag_first = false;
+    /// The factorised matrix's device CSR, kept when requested (keep_A) so the
+    /// level-0 operator is built from it instead of a second upload.
+    DBuf<i64> Arp;
+    DBuf<i32> Aci;
+    DBuf<double> Av;
+
+    /// Download to host CSR (parity tests, the direct-solve level plans).
+    HostFactors to_host(cudaStream_t st) const;
+    static DevFactors upload(const HostFactors& f, cudaStream_t st);
+};
+
+/// Device-resident ILU(0) / ILUT (no host round trip of the factors).
+DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool keep_A = false);
+DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false);
+/// factorize() that leaves the factors on the device (host factorisations,
+/// when forced with ILUG_ILU0_DEVICE=0 / ILUG_ILUT_DEVICE=0, are uploaded).
+DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false);
+
 /// ILU(0) of A on the device, bitwise equal to host ilu0 (and the reference):
 /// same zero-pivot policy and error messages. Returns host factors (the device
 /// object builders take their patterns from the host copies).

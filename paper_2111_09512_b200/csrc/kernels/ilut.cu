@@ -376,17 +376,22 @@ bool ilut_on_device() {
     return !(e && e[0] == '0');
 }
 
-HostFactors ilut_device(const Csr& A, const IluParams& p, cudaStream_t st) {
+DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A) {
     if (A.nrows != A.ncols) fail_invalid("ilut: matrix must be square");
     if (!(p.droptol >= 0.0) || !std::isfinite(p.droptol)) fail_invalid("ilut: droptol must be finite and >= 0");
     if (p.lfill < 0) fail_invalid("ilut: lfill must be >= 0");
     const i64 n = A.nrows;
-    HostFactors f;
-    for (Csr* M : {&f.L, &f.U}) {
-        M->nrows = M->ncols = n;
-        M->rp.assign(static_cast<size_t>(n) + 1, 0);
+    DevFactors f;
+    f.n = n;
+    f.diag_first = true;
+    f.Lrp_h.assign(static_cast<size_t>(n) + 1, 0);
+    f.Urp_h.assign(static_cast<size_t>(n) + 1, 0);
+    if (n == 0) {
+        f.Lrp.upload(f.Lrp_h.data(), 1, st);
+        f.Urp.upload(f.Urp_h.data(), 1, st);
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        return f;
     }
-    if (n == 0) return f;
     SetupTimer tm("ilut-device");
     const double anorm_f = frobenius_norm(A);
     const i64 nnz = A.nnz();
@@ -441,33 +446,36 @@ HostFactors ilut_device(const Csr& A, const IluParams& p, cudaStream_t st) {
     if (fz != ~0ull)
         fail_numeric("zero pivot at step " + std::to_string(fz) +
                      " (no pivoting; rerun with pivot_patch=replace to substitute)");
-    // compact the slots into CSR and download
+    // compact the slots into CSR (stays on the device; row starts to the host)
+    if (keep_A) {
+        f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(av);
+    } else {
+        rp.release(), ci.release(), av.release();
+    }
     for (int part = 0; part < 2; ++part) {
-        Csr& M = part == 0 ? f.L : f.U;
         const DBuf<i32>& len = part == 0 ? llen : ulen;
-        DBuf<i64> mrp(n + 1);
+        DBuf<i64>& mrp = part == 0 ? f.Lrp : f.Urp;
+        mrp.alloc(n + 1);
         k_len_to_rp<<<g, 256, 0, st>>>(n, len.p, mrp.p);
         ILUG_LAUNCH_CHECK();
         inclusive_scan(mrp.p, n + 1, st);
-        i64 nz = 0;
-        ILUG_CUDA(cudaMemcpyAsync(&nz, mrp.p + n, sizeof nz, cudaMemcpyDeviceToHost, st));
+        RawVec<i64>& hrp = part == 0 ? f.Lrp_h : f.Urp_h;
+        mrp.download(hrp.data(), st);
         ILUG_CUDA(cudaStreamSynchronize(st));
-        DBuf<i32> mc(nz);
-        DBuf<double> mv(nz);
+        const i64 nz = hrp[n];
+        DBuf<i32>& mc = part == 0 ? f.Lci : f.Uci;
+        DBuf<double>& mv = part == 0 ? f.Lv : f.Uv;
+        mc.alloc(nz);
+        mv.alloc(nz);
         if (nz > 0) {
             const unsigned gw = static_cast<unsigned>((n * 32 + 255) / 256);
             k_compact<<<gw, 256, 0, st>>>(n, part == 0 ? loff.p : uoff.p, mrp.p, part == 0 ? lci.p : uci.p,
                                           part == 0 ? lv.p : uv.p, mc.p, mv.p);
             ILUG_LAUNCH_CHECK();
         }
-        M.ci.resize(static_cast<size_t>(nz));
-        M.v.resize(static_cast<size_t>(nz));
-        mrp.download(M.rp.data(), st);
-        mc.download(M.ci.data(), st);
-        mv.download(M.v.data(), st);
-        ILUG_CUDA(cudaStreamSynchronize(st));
     }
-    tm.mark("compact + download");
+    ILUG_CUDA(cudaStreamSynchronize(st)); // slot arrays die at scope exit
+    tm.mark("compact");
     return f;
 }
 

@@ -24,6 +24,12 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
                           const double* v, Part part, const std::vector<i32>& perm_host,
                           cudaStream_t s);
 
+/// Same from device CSR arrays when only the row starts are on the host: the
+/// selected part of row r has rp_host[r+1] - rp_host[r] - skip entries (skip =
+/// 1 for the strict upper part of a factor whose rows start with the diagonal).
+void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& rp_host, i64 skip, const i64* rp,
+                           const i32* ci, const double* v, Part part, cudaStream_t s);
+
 /// Unpack a SELL back to host CSR (tests / parity downloads).
 Csr sell_to_host(const Sell& M);
 

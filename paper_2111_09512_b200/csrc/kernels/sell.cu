@@ -479,6 +479,22 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
     }
 }
 
+void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& rp_host, i64 skip, const i64* rp,
+                           const i32* ci, const double* v, Part part, cudaStream_t s) {
+    out.nrows = nrows;
+    out.ncols = ncols;
+    const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
+    auto len = [&](i64 r) { return rp_host[r + 1] - rp_host[r] - skip; };
+    const std::vector<i32> perm = sigma_order(nrows, len);
+    const i64 pad = perm.empty() ? (nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
+    layout(out, pad, perm, len, s);
+    if (pad > 0 && rp_host[nrows] > 0) {
+        k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp, ci, v, pc, out.slice_ptr.p,
+                                                     out.cols.p, out.vals.p);
+        ILUG_LAUNCH_CHECK();
+    }
+}
+
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     out.nrows = A.nrows;
     out.ncols = A.ncols;
