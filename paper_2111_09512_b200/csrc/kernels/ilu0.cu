@@ -42,17 +42,7 @@ k_ilu0(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, const i64*
     const i64 beg = rp[i], end = rp[i + 1], di = dpos[i];
     for (i64 k = beg; k < di; ++k) {
         const i64 c = ci[k];
-        cuda::atomic_ref<unsigned, cuda::thread_scope_device> f(done[c]);
-        if (f.load(cuda::memory_order_acquire) != E) {
-            long long spins = 0;
-            while (f.load(cuda::memory_order_acquire) != E) {
-                if (++spins > (1ll << 26)) { // seconds: a scheduling bug, not a slow row
-                    atomicExch(err, 1u);
-                    break;
-                }
-                __nanosleep(64);
-            }
-        }
+        if (!wait_flag<64>(done + c, E)) atomicExch(err, 1u);
         const double m = w[k] / w[dpos[c]];
         w[k] = m;
         // merge row c's strict upper part against row i's tail (ascending columns)

@@ -135,7 +135,7 @@ __device__ __forceinline__ int emit(const i32* scol, const double* sval, const u
 }
 
 template <int CAP, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_ilut(IlutArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // [WARPS*CAP values][WARPS*CAP columns][WARPS*32 merge positions][WARPS*CAP flags]
@@ -181,19 +181,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_ilut(IlutArgs a) {
         for (; p < len && !bad; ++p) {
             const i32 k = scol[p];
             if (k >= i) break;
-            cuda::atomic_ref<unsigned, cuda::thread_scope_device> fk(a.done[k]);
-            if (fk.load(cuda::memory_order_acquire) != E) {
-                long long spins = 0;
-                while (fk.load(cuda::memory_order_acquire) != E) {
-                    if (++spins > (1ll << 26)) { // seconds: a scheduling bug, not a slow row
-                        atomicExch(a.err, 1u);
-                        break;
-                    }
-                    __nanosleep(32);
-                }
-            }
-            const i64 ub = a.uoff[k];
-            const double m = sval[p] / a.uv[ub];
+            // the slot of U row k is fixed before row k is done: address its
+            // first 32 entries ahead, then fetch length, pivot and entries in
+            // one round trip once the flag is seen (slot entries past the
+            // length are never used)
+            const i64 ub = __ldg(a.uoff + k);
+            const bool in_slot = lane + 1 < __ldg(a.uoff + k + 1) - ub;
+            if (!wait_flag(a.done + k, E)) atomicExch(a.err, 1u);
+            const int ul = a.ulen[k];
+            const double ukk = a.uv[ub];
+            const i32 j0 = in_slot ? a.uci[ub + 1 + lane] : INT_MAX;
+            const double u0 = in_slot ? a.uv[ub + 1 + lane] : 0.0;
+            const double m = sval[p] / ukk;
             __syncwarp();
             if (fabs(m) < tau) { // dual-threshold drop of the multiplier
                 if (lane == 0) sval[p] = 0.0, sflag[p] = 0;
@@ -201,12 +200,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_ilut(IlutArgs a) {
                 continue;
             }
             if (lane == 0) sval[p] = m, sflag[p] = kLive | kKept | (sflag[p] & kOrig);
-            const int ul = a.ulen[k];
             for (int c = 1; c < ul; c += 32) {
                 const int kk = c + lane;
                 const bool act = kk < ul;
-                const i32 j = act ? a.uci[ub + kk] : INT_MAX;
-                const double u = act ? a.uv[ub + kk] : 0.0;
+                const i32 j = !act ? INT_MAX : (c == 1 ? j0 : a.uci[ub + kk]);
+                const double u = !act ? 0.0 : (c == 1 ? u0 : a.uv[ub + kk]);
                 int lo = p + 1, hi = len;
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
@@ -292,8 +290,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_ilut(IlutArgs a) {
             a.uv[uo] = d;
             a.ulen[i] = nu + 1;
         }
-        __threadfence();
-        __syncwarp();
+        __syncwarp(); // orders every lane's row writes before lane 0's release (cumulative)
         if (lane == 0) fi.store(E, cuda::memory_order_release);
 
         select_part(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, lane);

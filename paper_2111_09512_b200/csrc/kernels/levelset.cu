@@ -71,10 +71,12 @@ __device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, con
                 const i32 j = c[u];
                 if (is_dep<MODE>(j, row)) {
                     if (FLAGS) {
-                        cuda::atomic_ref<unsigned, cuda::thread_scope_device> f(flags[j]);
-                        // back off so spinning warps do not flood L2 with polls
-                        for (int spin = 0; f.load(cuda::memory_order_acquire) != E; ++spin)
-                            if (spin > 8) __nanosleep(64);
+                        // relaxed polls with back-off, one acquire once seen
+                        if (ld_acquire_flag(flags + j) != E) {
+                            for (int spin = 0; ld_relaxed_flag(flags + j) != E; ++spin)
+                                if (spin > 8) __nanosleep(64);
+                            (void)ld_acquire_flag(flags + j);
+                        }
                     }
                     xv[u] = __ldcg(x + j);
                 } else {
