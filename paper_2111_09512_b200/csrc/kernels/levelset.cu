@@ -64,25 +64,27 @@ __device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, con
                 a[u] = __ldg(M.vals + q);
             }
         }
+        if (FLAGS) {
+            // every producer flag of the chunk polled at once (relaxed, all in
+            // flight), then one acquire fence for the chunk: ~1 round trip per
+            // chunk instead of one serial acquire (LD.STRONG + CCTL.IVALL) per
+            // dependency
+            bool ready = false;
+            for (int spin = 0; !ready; ++spin) {
+                ready = true;
+#pragma unroll
+                for (int u = 0; u < kChunk; ++u)
+                    if (t0 + u < len && !(MODE != 0 && c[u] == row) && is_dep<MODE>(c[u], row))
+                        ready &= ld_relaxed_flag(flags + c[u]) == E;
+                if (!ready && spin > 8) __nanosleep(64);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
             xv[u] = 0.0;
-            if (t0 + u < len && !(MODE != 0 && c[u] == row)) {
-                const i32 j = c[u];
-                if (is_dep<MODE>(j, row)) {
-                    if (FLAGS) {
-                        // relaxed polls with back-off, one acquire once seen
-                        if (ld_acquire_flag(flags + j) != E) {
-                            for (int spin = 0; ld_relaxed_flag(flags + j) != E; ++spin)
-                                if (spin > 8) __nanosleep(64);
-                            (void)ld_acquire_flag(flags + j);
-                        }
-                    }
-                    xv[u] = __ldcg(x + j);
-                } else {
-                    xv[u] = xold[j]; // GS: not-yet-updated neighbour (MODE 2 only)
-                }
-            }
+            if (t0 + u < len && !(MODE != 0 && c[u] == row))
+                xv[u] = is_dep<MODE>(c[u], row) ? __ldcg(x + c[u]) : xold[c[u]]; // xold: GS (MODE 2) only
         }
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
@@ -108,10 +110,30 @@ __device__ __forceinline__ void l2_prefetch(const void* p, i64 bytes) {
     }
 }
 
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+// Level-synchronous schedule on one thread-block cluster (1..16 CTAs on one
+// GPC): the cluster's threads split each level's rows, and a hardware cluster
+// barrier (barrier.cluster arrive.release / wait.acquire, ~0.2 us) separates
+// the levels, so a level costs one row latency plus the barrier, with up to 16
+// SMs of load bandwidth instead of one. x crosses CTAs through L2 (__ldcg),
+// ordered by the barrier's release/acquire at cluster scope.
 template <int MODE>
 __global__ void __launch_bounds__(kSmallBlock)
 k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b,
              double* x, const double* __restrict__ xold) {
+    const unsigned crank = cluster_rank(), csize = cluster_size();
+    const i64 gtid = static_cast<i64>(crank) * blockDim.x + threadIdx.x;
+    const i64 gthreads = static_cast<i64>(csize) * blockDim.x;
     // Level L+2's operator slices are one contiguous range of the level-ordered
     // SELL: one thread asks the copy engine to pull them into L2 while the CTA
     // works on level L, so a level's loads are L2 hits, not DRAM misses.
@@ -125,7 +147,7 @@ k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const doub
         }
         l2_prefetch(M.perm + level_ptr[L], (level_ptr[L + 1] - level_ptr[L]) * 4);
     };
-    if (threadIdx.x == 0) {
+    if (gtid == 0) {
         prefetch_level(0);
         prefetch_level(1);
     }
@@ -144,7 +166,7 @@ k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const doub
     auto fetch = [&](int L) {
         nx.p = -1;
         if (L >= nlev) return;
-        const i64 p = level_ptr[L] + threadIdx.x;
+        const i64 p = level_ptr[L] + gtid;
         if (p >= level_ptr[L + 1]) return;
         nx.p = p;
         nx.row = M.perm[p];
@@ -162,7 +184,7 @@ k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const doub
     };
     fetch(0);
     for (int L = 0; L < nlev; ++L) {
-        if (threadIdx.x == 0) prefetch_level(L + 2);
+        if (gtid == 0) prefetch_level(L + 2);
         if (nx.p >= 0 && nx.row >= 0) {
             const i64 row = nx.row;
             double s = nx.bv, d = 1.0, xv[kPre];
@@ -207,14 +229,145 @@ k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const doub
             }
             x[row] = MODE == 0 ? s : s / d;
         }
-        // rows beyond the first blockDim.x of a wide level
+        // rows beyond the cluster's first gthreads of a wide level
         const i64 end = level_ptr[L + 1];
-        for (i64 p = level_ptr[L] + threadIdx.x + blockDim.x; p < end; p += blockDim.x) {
+        for (i64 p = level_ptr[L] + gtid + gthreads; p < end; p += gthreads) {
             const i64 row = M.perm[p];
             if (row >= 0) level_row<MODE, false, 8>(M, p, row, b, x, xold, nullptr, 0u);
         }
         fetch(L + 1);
-        __syncthreads();
+        if (csize > 1) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                         "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster schedule, warp per row (the default for narrow DAGs: coarse AMG
+// levels' Gauss-Seidel, factor solves with few rows per level).
+//
+// A thread-per-row kernel on one SM issues a row's ~40 dependent
+// gather/multiply/subtract steps serially with almost no other warps to hide
+// their latency (ncu: ~1000 issued instructions per level per warp at 85
+// cycles each, 15-40 us per level). Here a warp takes a row: lane t loads
+// entry t (and t+32), gathers its x value and forms the product a_t * x_t —
+// the same rounded product the serial loop forms — and the ordered
+// accumulation s = b - p_0 - p_1 - ... runs as a chain of shuffles, so the
+// result is still bitwise the serial one. The warps of a thread-block cluster
+// (up to 16 CTAs on one GPC) split each level's rows; a hardware cluster
+// barrier (barrier.cluster arrive.release / wait.acquire) separates levels.
+// Row metadata is loaded two levels ahead and the first row's columns/values
+// one level ahead, so a level costs one x gather plus the shuffle chain.
+constexpr int kWarpBlock = 512;
+constexpr int kMaxSmemLevels = 6000; // level_ptr staged in (static) shared memory
+
+struct RowMeta {
+    i64 row = -1; // -1: no row / padding
+    i64 base = 0;
+    int len = 0;
+};
+struct RowData {
+    i32 c0 = -1, c1 = -1;
+    double a0 = 0.0, a1 = 0.0, bv = 0.0;
+};
+
+template <int MODE>
+__device__ __forceinline__ void warp_row(const SellView& M, const RowMeta& m, const RowData& r, int lane,
+                                         const double* __restrict__ b, double* x,
+                                         const double* __restrict__ xold) {
+    const unsigned full = 0xffffffffu;
+    const i64 row = m.row;
+    double s = r.bv, d = 1.0;
+    for (int t0 = 0; t0 < m.len; t0 += 32) {
+        const int t = t0 + lane;
+        const bool act = t < m.len;
+        i32 c;
+        double a;
+        if (t0 == 0) {
+            c = r.c0, a = r.a0;
+        } else if (t0 == 32) {
+            c = r.c1, a = r.a1;
+        } else {
+            c = act ? __ldg(M.cols + m.base + static_cast<i64>(t) * kSlice) : -1;
+            a = act ? __ldg(M.vals + m.base + static_cast<i64>(t) * kSlice) : 0.0;
+        }
+        const bool isd = act && MODE != 0 && c == row;
+        double xv = 0.0;
+        if (act && !isd) xv = is_dep<MODE>(c, row) ? __ldcg(x + c) : __ldg(xold + c); // xold: GS only
+        const double prod = a * xv; // the serial loop's rounded product
+        const unsigned dm = __ballot_sync(full, isd);
+        if (dm) d = __shfl_sync(full, a, __ffs(dm) - 1);
+        const int cnt = min(32, m.len - t0);
+        for (int u = 0; u < cnt; ++u) {
+            const double pu = __shfl_sync(full, prod, u);
+            if (!((dm >> u) & 1u)) s = s - pu;
+        }
+    }
+    if (lane == 0) x[row] = MODE == 0 ? s : s / d;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kWarpBlock, 1)
+k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b, double* x,
+              const double* __restrict__ xold) {
+    __shared__ i64 slp[kMaxSmemLevels + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned csize = cluster_size();
+    const i64 gw = static_cast<i64>(cluster_rank()) * (kWarpBlock / 32) + warp;
+    const i64 GW = static_cast<i64>(csize) * (kWarpBlock / 32);
+    for (int l = threadIdx.x; l <= nlev; l += blockDim.x) slp[l] = level_ptr[l];
+    __syncthreads();
+
+    auto load_meta = [&](int L, RowMeta& m) {
+        m.row = -1;
+        if (L >= nlev) return;
+        const i64 p = slp[L] + gw;
+        if (p >= slp[L + 1]) return;
+        m.row = M.perm[p];
+        m.len = M.rowlen[p];
+        m.base = M.slice_ptr[p >> 5] + (p & 31);
+    };
+    auto load_data = [&](const RowMeta& m, RowData& r) {
+        if (m.row < 0) return;
+        r.c0 = lane < m.len ? __ldg(M.cols + m.base + static_cast<i64>(lane) * kSlice) : -1;
+        r.a0 = lane < m.len ? __ldg(M.vals + m.base + static_cast<i64>(lane) * kSlice) : 0.0;
+        r.c1 = lane + 32 < m.len ? __ldg(M.cols + m.base + static_cast<i64>(lane + 32) * kSlice) : -1;
+        r.a1 = lane + 32 < m.len ? __ldg(M.vals + m.base + static_cast<i64>(lane + 32) * kSlice) : 0.0;
+        r.bv = b[m.row];
+    };
+
+    RowMeta mc, m1, m2;
+    RowData dc, d1;
+    load_meta(0, mc);
+    load_data(mc, dc);
+    load_meta(1, m1);
+    for (int L = 0; L < nlev; ++L) {
+        load_data(m1, d1);  // level L+1's first row, one level ahead
+        load_meta(L + 2, m2); // two ahead
+        if (mc.row >= 0) warp_row<MODE>(M, mc, dc, lane, b, x, xold);
+        // further rows of a level wider than the cluster's warps
+        for (i64 p = slp[L] + gw + GW; p < slp[L + 1]; p += GW) {
+            RowMeta m;
+            RowData r;
+            m.row = M.perm[p];
+            if (m.row < 0) continue;
+            m.len = M.rowlen[p];
+            m.base = M.slice_ptr[p >> 5] + (p & 31);
+            load_data(m, r);
+            warp_row<MODE>(M, m, r, lane, b, x, xold);
+        }
+        mc = m1;
+        dc = d1;
+        m1 = m2;
+        if (csize > 1) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                         "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            __syncthreads();
+        }
     }
 }
 
@@ -249,8 +402,49 @@ const void* cta_kernel() {
     return reinterpret_cast<const void*>(k_levels_cta<MODE>);
 }
 template <int MODE>
+const void* warp_kernel() {
+    return reinterpret_cast<const void*>(k_levels_warp<MODE>);
+}
+template <int MODE>
 const void* flag_kernel() {
     return reinterpret_cast<const void*>(k_levels_flags<MODE>);
+}
+
+} // namespace
+
+namespace {
+
+// Largest cluster of k_levels_warp CTAs (512 threads, one per SM) the device
+// can co-schedule on one GPC.
+i64 max_cluster_ctas() {
+    static const i64 c = [] {
+        const void* fns[] = {warp_kernel<0>(), warp_kernel<1>(), warp_kernel<2>()};
+        for (const void* fn : fns)
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+                (void)cudaGetLastError();
+        for (int want : {16, 8, 4, 2}) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(want));
+            cfg.blockDim = dim3(kWarpBlock);
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = static_cast<unsigned>(want);
+            attr[0].val.clusterDim.y = attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            bool ok = true;
+            for (const void* fn : fns) {
+                int nclusters = 0;
+                if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+                    (void)cudaGetLastError();
+                    ok = false;
+                }
+            }
+            if (ok) return static_cast<i64>(want);
+        }
+        return i64{1};
+    }();
+    return c;
 }
 
 } // namespace
@@ -299,16 +493,24 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     if (!dev_vals) v.upload(T.v.data(), T.nnz(), st);
     sell_from_device_csr(M_, T, rp.p, ci.p, dev_vals ? dev_vals : v.p, Part::all, perm, st);
 
-    // Narrow DAG (average level width below two CTAs' worth): one CTA.
-    // One CTA only for tiny systems: with __syncthreads per level every level
-    // costs its full row latency; the sync-free schedule overlaps the loads of
-    // later levels with the wait on earlier ones, which wins as soon as there
-    // is more than a CTA's worth of rows.
-    single_cta_ = n <= 4 * kSmallBlock || n / std::max(nl, 1) <= kSmallBlock;
-    if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | flags
-        if (std::string(force) == "cta") single_cta_ = true;
+    // Level-synchronous on one cluster (warp per row) unless the levels
+    // are wider than the cluster's warps can take in one pass on average (then
+    // the sync-free flag schedule uses the whole GPU). Cluster size: enough
+    // CTAs for the widest level's slices, capped by what one GPC co-schedules.
+    const i64 cmax = max_cluster_ctas();
+    const i64 avg = n / std::max(nl, 1);
+    single_cta_ = n <= 4 * kSmallBlock || avg <= cmax * (kWarpBlock / 32) * 4; // <= 4 rows per warp
+    old_cta_ = false;
+    if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | cta1 | flags
+        if (std::string(force) == "cta" || std::string(force) == "cta1") single_cta_ = true;
+        if (std::string(force) == "cta1") old_cta_ = true;
         if (std::string(force) == "flags" && n > 0) single_cta_ = false;
     }
+    cluster_ = 1;
+    if (nl > kMaxSmemLevels) old_cta_ = true; // level pointers do not fit the warp kernel's shared memory
+    if (single_cta_ && !old_cta_)
+        cluster_ = static_cast<int>(
+            std::clamp<i64>((max_level_rows_ + kWarpBlock / 32 - 1) / (kWarpBlock / 32), 1, cmax));
     if (!single_cta_) {
         flags_.alloc(n + 2); // [0, n) row flags, n epoch, n+1 ticket
         ILUG_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(n + 2) * sizeof(unsigned), st));
@@ -329,8 +531,23 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
         const i64* lp = level_ptr_.p;
         int nl = nlev_;
         void* args[] = {&mv, &lp, &nl, &b, &x, &xold};
-        const void* fn = mode == 0 ? cta_kernel<0>() : mode == 1 ? cta_kernel<1>() : cta_kernel<2>();
-        ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kSmallBlock), args, 0, st));
+        if (old_cta_) { // the one-CTA register-pipelined kernel (A/B, tests)
+            const void* fn = mode == 0 ? cta_kernel<0>() : mode == 1 ? cta_kernel<1>() : cta_kernel<2>();
+            ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kSmallBlock), args, 0, st));
+            return;
+        }
+        const void* fn = mode == 0 ? warp_kernel<0>() : mode == 1 ? warp_kernel<1>() : warp_kernel<2>();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(cluster_));
+        cfg.blockDim = dim3(kWarpBlock);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(cluster_);
+        attr[0].val.clusterDim.y = attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ILUG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
         return;
     }
     const i64 n = M_.nrows;

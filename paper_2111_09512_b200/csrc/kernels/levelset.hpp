@@ -21,7 +21,8 @@ public:
     void solve(const double* b, double* x, const double* xold, cudaStream_t st) const;
 
     int levels() const { return nlev_; }
-    int grid() const { return grid_; }
+    int grid() const { return single_cta_ ? cluster_ : grid_; }
+    bool cluster_schedule() const { return single_cta_; }
     const Sell& matrix() const { return M_; }
 
 private:
@@ -32,6 +33,8 @@ private:
     bool single_cta_ = true;
     int nlev_ = 0;
     int grid_ = 1;
+    int cluster_ = 1;       // CTAs of the level-synchronous cluster schedule
+    bool old_cta_ = false;  // ILUG_LEVELSET=cta1: the one-CTA register-pipelined kernel
     i64 max_level_rows_ = 0;
 };
 

@@ -214,13 +214,14 @@ def test_c3_cutcell_scaled_vs_unscaled(ilug, ref, port, torch_cuda):
     assert errs[0] > errs[1] > errs[2]
 
 
-@pytest.mark.parametrize("schedule", ["cta", "flags"])
+@pytest.mark.parametrize("schedule", ["cta", "cta1", "flags"])
 @pytest.mark.parametrize("spec,kv", [("poisson3d(24,24,20)", {}),
                                      ("pressure27(16,16,16)", {"ilu.variant": "ilut", "ilu.droptol": "1e-3",
                                                                "ilu.lfill": "5"})])
 def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule, spec, kv):
-    """Both level-set schedules (single CTA / sync-free flags) give the serial
-    result bitwise, for the triangular solves and the Gauss-Seidel sweep."""
+    """Every level-set schedule (cluster-synchronous, single CTA, sync-free
+    flags) gives the serial result bitwise, for the triangular solves and the
+    Gauss-Seidel sweep."""
     monkeypatch.setenv("ILUG_LEVELSET", schedule)
     A, L, U, f, fr = _factors(ilug, ref, spec, kv, "row", direct=True)
     b = np.random.default_rng(31).uniform(-1, 1, A.rows)
@@ -239,8 +240,12 @@ def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule,
     assert bitwise(_host(xd), want)
 
 
-def test_k5_wide_dag_flags_bitwise(ilug, ref, torch_cuda):
-    """A DAG wide enough for the sync-free schedule by default (n / levels > 2048)."""
+@pytest.mark.parametrize("schedule", ["", "cta", "flags"])
+def test_k5_wide_dag_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule):
+    """A wide DAG (n / levels > 2048: levels wider than a cluster's threads,
+    so cluster threads take several rows per level)."""
+    if schedule:
+        monkeypatch.setenv("ILUG_LEVELSET", schedule)
     A, L, U, f, fr = _factors(ilug, ref, "poisson3d(160,160,40)", {}, "row", direct=True)
     st = f.stats()
     assert A.rows / st["levels_L"] > 2048

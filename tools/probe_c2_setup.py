@@ -7,7 +7,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("ILUG_TRACE_SETUP", "1")
+if "ILUG_TRACE_SETUP" not in os.environ:
+    os.environ["ILUG_TRACE_SETUP"] = "1"
 import paper_2111_09512_b200 as ilug  # noqa: E402
 
 spec = sys.argv[1] if len(sys.argv) > 1 else "pressure27(256,256,256)"
