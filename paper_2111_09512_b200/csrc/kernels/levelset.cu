@@ -261,7 +261,8 @@ k_levels_cta(SellView M, const i64* __restrict__ level_ptr, int nlev, const doub
 // barrier (barrier.cluster arrive.release / wait.acquire) separates levels.
 // Row metadata is loaded two levels ahead and the first row's columns/values
 // one level ahead, so a level costs one x gather plus the shuffle chain.
-constexpr int kWarpBlock = 512;
+constexpr int kWarpBlock = 512;       // narrow levels (fewer warps per barrier)
+constexpr int kWarpBlockWide = 1024;  // levels with more rows than 2 per warp of a 512-thread cluster
 constexpr int kMaxSmemLevels = 6000; // level_ptr staged in (static) shared memory
 
 struct RowMeta {
@@ -309,15 +310,15 @@ __device__ __forceinline__ void warp_row(const SellView& M, const RowMeta& m, co
     if (lane == 0) x[row] = MODE == 0 ? s : s / d;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kWarpBlock, 1)
+template <int MODE, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 1)
 k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b, double* x,
               const double* __restrict__ xold) {
     __shared__ i64 slp[kMaxSmemLevels + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned csize = cluster_size();
-    const i64 gw = static_cast<i64>(cluster_rank()) * (kWarpBlock / 32) + warp;
-    const i64 GW = static_cast<i64>(csize) * (kWarpBlock / 32);
+    const i64 gw = static_cast<i64>(cluster_rank()) * (BLOCK / 32) + warp;
+    const i64 GW = static_cast<i64>(csize) * (BLOCK / 32);
     for (int l = threadIdx.x; l <= nlev; l += blockDim.x) slp[l] = level_ptr[l];
     __syncthreads();
 
@@ -401,9 +402,9 @@ template <int MODE>
 const void* cta_kernel() {
     return reinterpret_cast<const void*>(k_levels_cta<MODE>);
 }
-template <int MODE>
+template <int MODE, int BLOCK = kWarpBlock>
 const void* warp_kernel() {
-    return reinterpret_cast<const void*>(k_levels_warp<MODE>);
+    return reinterpret_cast<const void*>(k_levels_warp<MODE, BLOCK>);
 }
 template <int MODE>
 const void* flag_kernel() {
@@ -418,24 +419,25 @@ namespace {
 // can co-schedule on one GPC.
 i64 max_cluster_ctas() {
     static const i64 c = [] {
-        const void* fns[] = {warp_kernel<0>(), warp_kernel<1>(), warp_kernel<2>()};
+        const void* fns[] = {warp_kernel<0>(), warp_kernel<1>(), warp_kernel<2>(), warp_kernel<0, kWarpBlockWide>(),
+                             warp_kernel<1, kWarpBlockWide>(), warp_kernel<2, kWarpBlockWide>()};
         for (const void* fn : fns)
             if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
                 (void)cudaGetLastError();
         for (int want : {16, 8, 4, 2}) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(want));
-            cfg.blockDim = dim3(kWarpBlock);
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = static_cast<unsigned>(want);
-            attr[0].val.clusterDim.y = attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
             bool ok = true;
-            for (const void* fn : fns) {
+            for (int f = 0; f < 6; ++f) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(static_cast<unsigned>(want));
+                cfg.blockDim = dim3(f < 3 ? kWarpBlock : kWarpBlockWide);
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = static_cast<unsigned>(want);
+                attr[0].val.clusterDim.y = attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
                 int nclusters = 0;
-                if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+                if (cudaOccupancyMaxActiveClusters(&nclusters, fns[f], &cfg) != cudaSuccess || nclusters < 1) {
                     (void)cudaGetLastError();
                     ok = false;
                 }
@@ -499,7 +501,8 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // CTAs for the widest level's slices, capped by what one GPC co-schedules.
     const i64 cmax = max_cluster_ctas();
     const i64 avg = n / std::max(nl, 1);
-    single_cta_ = n <= 4 * kSmallBlock || avg <= cmax * (kWarpBlock / 32) * 4; // <= 4 rows per warp
+    single_cta_ = n <= 4 * kSmallBlock || avg <= cmax * (kWarpBlockWide / 32) * 4; // <= 4 rows per warp
+    block_ = avg > cmax * (kWarpBlock / 32) * 2 ? kWarpBlockWide : kWarpBlock;
     old_cta_ = false;
     if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | cta1 | flags
         if (std::string(force) == "cta" || std::string(force) == "cta1") single_cta_ = true;
@@ -510,7 +513,7 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     if (nl > kMaxSmemLevels) old_cta_ = true; // level pointers do not fit the warp kernel's shared memory
     if (single_cta_ && !old_cta_)
         cluster_ = static_cast<int>(
-            std::clamp<i64>((max_level_rows_ + kWarpBlock / 32 - 1) / (kWarpBlock / 32), 1, cmax));
+            std::clamp<i64>((max_level_rows_ + block_ / 32 - 1) / (block_ / 32), 1, cmax));
     if (!single_cta_) {
         flags_.alloc(n + 2); // [0, n) row flags, n epoch, n+1 ticket
         ILUG_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(n + 2) * sizeof(unsigned), st));
@@ -536,10 +539,13 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
             ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kSmallBlock), args, 0, st));
             return;
         }
-        const void* fn = mode == 0 ? warp_kernel<0>() : mode == 1 ? warp_kernel<1>() : warp_kernel<2>();
+        const bool wide = block_ == kWarpBlockWide;
+        const void* fn = mode == 0   ? (wide ? warp_kernel<0, kWarpBlockWide>() : warp_kernel<0>())
+                         : mode == 1 ? (wide ? warp_kernel<1, kWarpBlockWide>() : warp_kernel<1>())
+                                     : (wide ? warp_kernel<2, kWarpBlockWide>() : warp_kernel<2>());
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(cluster_));
-        cfg.blockDim = dim3(kWarpBlock);
+        cfg.blockDim = dim3(static_cast<unsigned>(block_));
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;

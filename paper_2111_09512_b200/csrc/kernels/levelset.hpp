@@ -35,6 +35,7 @@ private:
     int grid_ = 1;
     int cluster_ = 1;       // CTAs of the level-synchronous cluster schedule
     bool old_cta_ = false;  // ILUG_LEVELSET=cta1: the one-CTA register-pipelined kernel
+    int block_ = 512;       // threads per CTA of the warp-per-row cluster kernel
     i64 max_level_rows_ = 0;
 };
 
