@@ -69,6 +69,11 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     dh.set_use_graph(use_graph);
     // the level-0 smoother is ILU only when the hierarchy has more than one level
     dh.build(oc.hier, st, have_pre && oc.hier.num_levels() > 1 ? &pre : nullptr);
+    // device-side setup that the first iteration would otherwise pay inside the
+    // timed solve: the V-cycle graph and the GMRES basis (multi-GB at C2)
+    dh.prepare_graph();
+    GmresWork gw;
+    if (kp.restart >= 1 && kp.restart <= 63) gw.ensure(A.nrows, kp.restart, kp.flexible); // else gmres reports it
     oc.setup_seconds = since(t0);
 
     const i64 n = A.nrows;
@@ -84,7 +89,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     const bool late_anorm = !kp.form_iterates && !kp.nrbe_criterion;
     if (late_anorm) kpr.estimate_anorm = false;
     const auto t1 = std::chrono::steady_clock::now();
-    oc.kr = device_gmres(dh.A0(), A, dh, db.p, dx.p, kpr, st);
+    oc.kr = device_gmres(dh.A0(), A, dh, db.p, dx.p, kpr, st, nullptr, &gw);
     ILUG_CUDA(cudaStreamSynchronize(st));
     oc.solve_seconds = since(t1);
     oc.x.resize(static_cast<size_t>(n));

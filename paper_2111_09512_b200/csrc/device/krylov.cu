@@ -71,9 +71,19 @@ double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 st
     return dev_norm(w.p, A.n, sc, st);
 }
 
+void GmresWork::ensure(i64 n, i64 restart, bool flexible) {
+    auto need = [](DBuf<double>& d, i64 count) {
+        if (d.n != count) d.alloc(count);
+    };
+    need(V, (restart + 1) * n);
+    need(Z, flexible ? restart * n : 0);
+    for (DBuf<double>* d : {&w, &r, &xk, &xc, &vy, &mz}) need(*d, n);
+    need(ydev, 64);
+}
+
 KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierarchy& M,
                           const double* b, double* x, const KrylovParams& p, cudaStream_t st,
-                          const DistComm* comm) {
+                          const DistComm* comm, GmresWork* work) {
     const i64 n = A.n;
     if (p.restart < 1) fail_invalid("gmres: restart must be >= 1");
     if (p.restart > 63) fail_invalid("gmres: restart must be <= 63 on the device (basis width)");
@@ -88,8 +98,11 @@ KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierar
     rep.bnorm = dev_norm(b, n, sc, st);
     const double bden = rep.bnorm > 0.0 ? rep.bnorm : 1.0;
 
-    DBuf<double> V((R + 1) * n), Z(p.flexible ? R * n : 0), w(n), r(n), xk(n), xc(n), vy(n), mz(n),
-        ydev(64);
+    GmresWork local;
+    GmresWork& W = work ? *work : local;
+    W.ensure(n, R, p.flexible);
+    DBuf<double>&V = W.V, &Z = W.Z, &w = W.w, &r = W.r, &xk = W.xk, &xc = W.xc, &vy = W.vy, &mz = W.mz,
+    &ydev = W.ydev;
     double* zbuf = mz.p;
 
     auto true_norms = [&](const double* xv, double& res, double& xn) {

@@ -487,32 +487,36 @@ void DeviceHierarchy::vcycle_eager(const double* r, double* z, cudaStream_t st) 
     vec_copy(z, l0.x.p, l0.n, st);
 }
 
+void DeviceHierarchy::prepare_graph() {
+    if (!use_graph_ || exec_ || levels_.empty()) return;
+    Lev& l0 = levels_[0];
+    // Capture the whole cycle once (fixed internal in/out buffers).
+    cudaStream_t cap;
+    ILUG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    ILUG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    try {
+        vec_zero(l0.x.p, l0.n, cap);
+        cycle(0, true, cap);
+    } catch (...) {
+        cudaStreamEndCapture(cap, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        throw;
+    }
+    ILUG_CUDA(cudaStreamEndCapture(cap, &g));
+    size_t nodes = 0;
+    ILUG_CUDA(cudaGraphGetNodes(g, nullptr, &nodes));
+    kernels_per_cycle_ = static_cast<i64>(nodes);
+    ILUG_CUDA(cudaGraphInstantiate(&exec_, g, 0));
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+}
+
 void DeviceHierarchy::vcycle(const double* r, double* z, cudaStream_t st) {
     if (!use_graph_) return vcycle_eager(r, z, st);
     Lev& l0 = levels_[0];
-    if (!exec_) {
-        // Capture the whole cycle once (fixed internal in/out buffers).
-        cudaStream_t cap;
-        ILUG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-        cudaGraph_t g = nullptr;
-        ILUG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-        try {
-            vec_zero(l0.x.p, l0.n, cap);
-            cycle(0, true, cap);
-        } catch (...) {
-            cudaStreamEndCapture(cap, &g);
-            if (g) cudaGraphDestroy(g);
-            cudaStreamDestroy(cap);
-            throw;
-        }
-        ILUG_CUDA(cudaStreamEndCapture(cap, &g));
-        size_t nodes = 0;
-        ILUG_CUDA(cudaGraphGetNodes(g, nullptr, &nodes));
-        kernels_per_cycle_ = static_cast<i64>(nodes);
-        ILUG_CUDA(cudaGraphInstantiate(&exec_, g, 0));
-        cudaGraphDestroy(g);
-        cudaStreamDestroy(cap);
-    }
+    prepare_graph();
     vec_copy(l0.b.p, r, l0.n, st);
     ILUG_CUDA(cudaGraphLaunch(exec_, st));
     vec_copy(z, l0.x.p, l0.n, st);

@@ -169,6 +169,9 @@ public:
     void build(const HostHierarchy& h, cudaStream_t st, DevFactors* level0 = nullptr);
     /// z = M(r) with z zeroed first (the driver's precond lambda, src/driver.cpp:182-185).
     void vcycle(const double* r, double* z, cudaStream_t st);
+    /// Capture and instantiate the V-cycle graph now (setup) instead of on the
+    /// first vcycle() call.
+    void prepare_graph();
     /// Same, without graph replay (direct kernel launches).
     void vcycle_eager(const double* r, double* z, cudaStream_t st);
     i64 n() const { return levels_.empty() ? 0 : levels_[0].n; }
@@ -239,9 +242,15 @@ struct DistComm;
 /// comm != nullptr: A holds this rank's rows (halo-exchanged SpMV), vectors are
 /// rank-local, every reduction is summed over ranks (NCCL allreduce), and M is
 /// this rank's block-Jacobi AMG hierarchy.
+/// GMRES work vectors (basis V, flexible Z, temporaries): allocated at setup
+/// by solve_with so the multi-GB basis allocation is not inside the timed solve.
+struct GmresWork {
+    DBuf<double> V, Z, w, r, xk, xc, vy, mz, ydev;
+    void ensure(i64 n, i64 restart, bool flexible);
+};
 KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierarchy& M,
                           const double* b_dev, double* x_dev, const KrylovParams& p, cudaStream_t st,
-                          const DistComm* comm = nullptr);
+                          const DistComm* comm = nullptr, GmresWork* work = nullptr);
 
 /// 50-step power iteration on A^T A (src/krylov.cpp:14-28) on the device.
 double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 steps,
