@@ -29,6 +29,12 @@ namespace ilug {
 
 constexpr int kSlice = 32; // SELL slice height = warp width: one row per lane
 
+/// Host -> device copy of a large pageable buffer through pinned staging
+/// buffers filled by the host worker pool (the driver's own pageable path
+/// stages single-threaded, ~5 GB/s). Returns once src is no longer needed.
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
+constexpr size_t kStagedMin = size_t{32} << 20; // smaller copies take the plain path
+
 /// Owned device allocation (cudaMalloc / cudaFree), move-only.
 template <typename T>
 struct DBuf {
@@ -60,9 +66,11 @@ struct DBuf {
     }
     void upload(const T* h, i64 count, cudaStream_t s = nullptr) {
         if (count != n) alloc(count);
-        if (count > 0)
-            ILUG_CUDA(cudaMemcpyAsync(p, h, static_cast<size_t>(count) * sizeof(T),
-                                      cudaMemcpyHostToDevice, s));
+        const size_t bytes = static_cast<size_t>(count) * sizeof(T);
+        if (bytes >= kStagedMin)
+            h2d_staged(p, h, bytes, s);
+        else if (count > 0)
+            ILUG_CUDA(cudaMemcpyAsync(p, h, bytes, cudaMemcpyHostToDevice, s));
     }
     void download(T* h, cudaStream_t s = nullptr) const {
         if (n > 0)

@@ -8,6 +8,9 @@
 // (--fmad=false): bitwise equal to src/sparse.cpp:162-174.
 #include "ops.hpp"
 
+#include <cstring>
+#include <mutex>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -352,6 +355,43 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
 
 } // namespace
 
+// ------------------------------------------------------------ staged uploads
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    constexpr size_t kChunk = size_t{64} << 20;
+    static std::mutex mu;
+    static void* buf[2] = {nullptr, nullptr};
+    static cudaEvent_t ev[2];
+    static bool ok = false, tried = false;
+    std::lock_guard<std::mutex> g(mu);
+    if (!tried) {
+        tried = true;
+        ok = cudaHostAlloc(&buf[0], kChunk, cudaHostAllocDefault) == cudaSuccess &&
+             cudaHostAlloc(&buf[1], kChunk, cudaHostAllocDefault) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) (void)cudaGetLastError();
+    }
+    if (!ok) {
+        ILUG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    const char* in = static_cast<const char*>(src);
+    char* out = static_cast<char*>(dst);
+    int k = 0;
+    for (size_t off = 0; off < bytes; off += kChunk, k ^= 1) {
+        const size_t len = std::min(kChunk, bytes - off);
+        ILUG_CUDA(cudaEventSynchronize(ev[k])); // the DMA that last read buf[k] is done
+        char* b = static_cast<char*>(buf[k]);
+        constexpr i64 kPiece = i64{1} << 20;
+        parallel_ranges((static_cast<i64>(len) + kPiece - 1) / kPiece, [&](i64 lo, i64 hi, int) {
+            const size_t a = static_cast<size_t>(lo * kPiece), e = std::min(len, static_cast<size_t>(hi * kPiece));
+            std::memcpy(b + a, in + off + a, e - a);
+        }, 4);
+        ILUG_CUDA(cudaMemcpyAsync(out + off, b, len, cudaMemcpyHostToDevice, s));
+        ILUG_CUDA(cudaEventRecord(ev[k], s));
+    }
+}
+
 // --------------------------------------------------------------- builders
 i64 sell_sigma() {
     const char* e = std::getenv("ILUG_SELL_SIGMA");
@@ -434,7 +474,9 @@ std::vector<i32> sigma_order(i64 n, LenOf len_of) {
         for (i64 i = b; i < e; ++i) len[i] = static_cast<i32>(len_of(i));
     });
     std::vector<i32> perm(static_cast<size_t>(pad), -1);
-    for (i64 i = 0; i < n; ++i) perm[i] = static_cast<i32>(i);
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) perm[i] = static_cast<i32>(i);
+    });
     const i64 wins = (n + sigma - 1) / sigma;
     parallel_ranges(wins, [&](i64 b, i64 e, int) {
         for (i64 w = b; w < e; ++w) {
@@ -443,15 +485,23 @@ std::vector<i32> sigma_order(i64 n, LenOf len_of) {
         }
     }, 1);
     auto padded = [&](bool sorted) {
-        i64 tot = 0;
-        for (i64 s = 0; s < pad / kSlice; ++s) {
-            i32 w = 0;
-            for (i64 l = 0; l < kSlice; ++l) {
-                const i64 p = s * kSlice + l;
-                if (p < n) w = std::max(w, len[sorted ? perm[p] : p]);
+        const i64 ns = pad / kSlice;
+        const int T = host_threads();
+        std::vector<i64> part(static_cast<size_t>(T) + 1, 0);
+        parallel_ranges(ns, [&](i64 b, i64 e, int t) {
+            i64 tot = 0;
+            for (i64 s = b; s < e; ++s) {
+                i32 w = 0;
+                for (i64 l = 0; l < kSlice; ++l) {
+                    const i64 p = s * kSlice + l;
+                    if (p < n) w = std::max(w, len[sorted ? perm[p] : p]);
+                }
+                tot += w;
             }
-            tot += w;
-        }
+            part[static_cast<size_t>(t)] += tot;
+        });
+        i64 tot = 0;
+        for (i64 v : part) tot += v;
         return tot;
     };
     if (padded(true) > 0.97 * static_cast<double>(padded(false))) return {};
@@ -481,13 +531,16 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
 
 void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& rp_host, i64 skip, const i64* rp,
                            const i32* ci, const double* v, Part part, cudaStream_t s) {
+    SetupTimer tm("sell-dev");
     out.nrows = nrows;
     out.ncols = ncols;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
     auto len = [&](i64 r) { return rp_host[r + 1] - rp_host[r] - skip; };
     const std::vector<i32> perm = sigma_order(nrows, len);
+    tm.mark("sigma order");
     const i64 pad = perm.empty() ? (nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
     layout(out, pad, perm, len, s);
+    tm.mark("layout+upload");
     if (pad > 0 && rp_host[nrows] > 0) {
         k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp, ci, v, pc, out.slice_ptr.p,
                                                      out.cols.p, out.vals.p);
@@ -496,12 +549,15 @@ void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& r
 }
 
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
+    SetupTimer tm("sell-host");
     out.nrows = A.nrows;
     out.ncols = A.ncols;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
     const std::vector<i32> perm = sigma_order(A.nrows, [&](i64 r) { return part_len(A, r, pc); });
+    tm.mark("sigma order");
     const i64 pad = perm.empty() ? (A.nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
     layout(out, pad, perm, [&](i64 row) { return part_len(A, row, pc); }, s);
+    tm.mark("layout+upload");
     if (A.nnz() == 0 || pad == 0) return;
     DBuf<i64> rp;
     DBuf<i32> ci;
@@ -509,10 +565,13 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     rp.upload(A.rp.data(), A.nrows + 1, s);
     ci.upload(A.ci.data(), A.nnz(), s);
     v.upload(A.v.data(), A.nnz(), s);
+    ILUG_CUDA(cudaStreamSynchronize(s));
+    tm.mark("csr upload");
     k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp.p, ci.p, v.p, pc,
                                                  out.slice_ptr.p, out.cols.p, out.vals.p);
     ILUG_LAUNCH_CHECK();
     ILUG_CUDA(cudaStreamSynchronize(s)); // temporaries die at scope exit
+    tm.mark("fill");
 }
 
 Csr sell_to_host(const Sell& M) {
