@@ -3,6 +3,10 @@
 
 #include <chrono>
 #include <future>
+#include <thread>
+#include <mutex>
+#include <deque>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <sstream>
@@ -61,14 +65,77 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     std::future<DevFactors> f0;
     if (s0.kind == SmootherKind::ilu && A.nrows > ap.coarse_size)
         f0 = std::async(std::launch::async, [&] { return factorize_resident(A, s0.ilu_params, st, true); });
-    oc.hier = amg_setup(A, ap);
-    DevFactors pre;
-    const bool have_pre = f0.valid();
-    if (have_pre) pre = f0.get();
+    // The device objects of level k are built (own stream, own thread) as soon
+    // as the host setup has finished level k, overlapping the host setup of
+    // the coarser levels. Level 0's smoother takes the factors computed above.
     DeviceHierarchy dh;
     dh.set_use_graph(use_graph);
-    // the level-0 smoother is ILU only when the hierarchy has more than one level
-    dh.build(oc.hier, st, have_pre && oc.hier.num_levels() > 1 ? &pre : nullptr);
+    dh.begin();
+    cudaStream_t bst = nullptr;
+    ILUG_CUDA(cudaStreamCreateWithFlags(&bst, cudaStreamNonBlocking));
+    struct Item {
+        i64 k;
+        const HostLevel* lev;
+        bool last;
+    };
+    std::mutex qm;
+    std::condition_variable qcv;
+    std::deque<Item> queue;
+    bool closed = false;
+    std::exception_ptr build_err;
+    DevFactors pre;
+    bool have_pre = false;
+    std::thread builder([&] {
+        for (;;) {
+            Item it;
+            {
+                std::unique_lock<std::mutex> g(qm);
+                qcv.wait(g, [&] { return closed || !queue.empty(); });
+                if (queue.empty()) return;
+                it = queue.front();
+                queue.pop_front();
+            }
+            if (build_err) continue; // drain after a failure
+            try {
+                DevFactors* l0 = nullptr;
+                if (it.k == 0 && !it.last && f0.valid()) { // the level-0 smoother uses the early factors
+                    pre = f0.get();
+                    have_pre = true;
+                    l0 = &pre;
+                }
+                dh.build_level(static_cast<int>(it.k), *it.lev, ap.plan.for_level(it.k), it.last, l0, bst);
+            } catch (...) {
+                build_err = std::current_exception();
+            }
+        }
+    });
+    auto close_queue = [&] {
+        {
+            std::lock_guard<std::mutex> g(qm);
+            closed = true;
+        }
+        qcv.notify_all();
+        builder.join();
+        cudaStreamDestroy(bst);
+    };
+    try {
+        oc.hier = amg_setup(A, ap, [&](i64 k, const HostLevel& lev, bool last) {
+            {
+                std::lock_guard<std::mutex> g(qm);
+                queue.push_back({k, &lev, last});
+            }
+            qcv.notify_one();
+        });
+    } catch (...) {
+        close_queue();
+        if (f0.valid()) f0.wait();
+        throw;
+    }
+    close_queue();
+    if (f0.valid()) pre = f0.get(); // single-level hierarchies: still surface factorisation errors
+    (void)have_pre;
+    if (build_err) std::rethrow_exception(build_err);
+    dh.finish(oc.hier, st);
     // device-side setup that the first iteration would otherwise pay inside the
     // timed solve: the V-cycle graph and the GMRES basis (multi-GB at C2)
     dh.prepare_graph();

@@ -407,30 +407,45 @@ DeviceHierarchy::~DeviceHierarchy() {
 
 void DeviceHierarchy::build(const HostHierarchy& h, cudaStream_t st, DevFactors* level0) {
     const int L = static_cast<int>(h.levels.size());
-    levels_ = std::vector<Lev>(static_cast<size_t>(L));
+    begin();
+    for (int k = 0; k < L; ++k)
+        build_level(k, h.levels[k], h.params.plan.for_level(k), k + 1 == L, k == 0 ? level0 : nullptr, st);
+    finish(h, st);
+}
+
+void DeviceHierarchy::begin() {
+    levels_.clear();
+    if (exec_) cudaGraphExecDestroy(exec_);
+    exec_ = nullptr;
+}
+
+void DeviceHierarchy::build_level(int k, const HostLevel& hl, const SmootherConfig& sc, bool last,
+                                  DevFactors* level0, cudaStream_t st) {
+    if (k != num_levels()) fail_invalid("device hierarchy: levels must be built in order");
     SetupTimer tm("device");
-    for (int k = 0; k < L; ++k) {
-        const HostLevel& hl = h.levels[k];
-        Lev& lv = levels_[k];
-        lv.n = hl.A.nrows;
-        if (k == 0 && level0 && level0->Av.n == hl.A.nnz() && hl.A.nnz() > 0) {
-            lv.A.build(hl.A, level0->Arp.p, level0->Aci.p, level0->Av.p, st); // the factorisation's upload
-            ILUG_CUDA(cudaStreamSynchronize(st));
-            level0->Arp.release(), level0->Aci.release(), level0->Av.release();
-        } else {
-            lv.A.build(hl.A, st);
-        }
-        if (k + 1 < L) {
-            sell_from_host(lv.P, hl.P, Part::all, st);
-            sell_from_host(lv.R, hl.R, Part::all, st);
-            tm.mark("A,P,R", k);
-            lv.smoother.build(hl.A, lv.A, h.params.plan.for_level(k), st, k == 0 ? level0 : nullptr);
-            tm.mark("smoother", k);
-        }
-        lv.b.alloc(std::max<i64>(lv.n, 1));
-        lv.x.alloc(std::max<i64>(lv.n, 1));
-        lv.r.alloc(std::max<i64>(lv.n, 1));
+    Lev& lv = levels_.emplace_back();
+    lv.n = hl.A.nrows;
+    if (k == 0 && level0 && level0->Av.n == hl.A.nnz() && hl.A.nnz() > 0) {
+        lv.A.build(hl.A, level0->Arp.p, level0->Aci.p, level0->Av.p, st); // the factorisation's upload
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        level0->Arp.release(), level0->Aci.release(), level0->Av.release();
+    } else {
+        lv.A.build(hl.A, st);
     }
+    if (!last) {
+        sell_from_host(lv.P, hl.P, Part::all, st);
+        sell_from_host(lv.R, hl.R, Part::all, st);
+        tm.mark("A,P,R", k);
+        lv.smoother.build(hl.A, lv.A, sc, st, level0);
+        tm.mark("smoother", k);
+    }
+    lv.b.alloc(std::max<i64>(lv.n, 1));
+    lv.x.alloc(std::max<i64>(lv.n, 1));
+    lv.r.alloc(std::max<i64>(lv.n, 1));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
+void DeviceHierarchy::finish(const HostHierarchy& h, cudaStream_t st) {
     lu_.upload(h.coarse.lu.data(), static_cast<i64>(h.coarse.lu.size()), st);
     piv_.upload(h.coarse.piv.data(), static_cast<i64>(h.coarse.piv.size()), st);
     nu_ = h.params.cycles_nu;

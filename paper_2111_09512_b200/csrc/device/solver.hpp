@@ -15,6 +15,7 @@
 #include "../kernels/levelset.hpp"
 #include "../kernels/wavefront.hpp"
 
+#include <deque>
 #include <memory>
 
 namespace ilug {
@@ -167,6 +168,12 @@ class DeviceHierarchy {
 public:
     /// `level0`: the finest level's ILU factors computed ahead (see solve_with).
     void build(const HostHierarchy& h, cudaStream_t st, DevFactors* level0 = nullptr);
+    /// Incremental form of build(): begin(), then build_level() for k = 0, 1, ...
+    /// in order (each as soon as the host level is final), then finish(h).
+    void begin();
+    void build_level(int k, const HostLevel& hl, const SmootherConfig& sc, bool last, DevFactors* level0,
+                     cudaStream_t st);
+    void finish(const HostHierarchy& h, cudaStream_t st);
     /// z = M(r) with z zeroed first (the driver's precond lambda, src/driver.cpp:182-185).
     void vcycle(const double* r, double* z, cudaStream_t st);
     /// Capture and instantiate the V-cycle graph now (setup) instead of on the
@@ -190,7 +197,7 @@ private:
         DBuf<double> b, x, r;
     };
     void cycle(int k, bool x_zero, cudaStream_t st);
-    std::vector<Lev> levels_;
+    std::deque<Lev> levels_; // stable addresses: smoothers point at their level's operator
     DBuf<double> lu_;
     DBuf<i64> piv_;
     i64 nu_ = 1;

@@ -393,7 +393,7 @@ Vec dense_lu_solve(const DenseLu& f, const Vec& b) {
     return x;
 }
 
-HostHierarchy amg_setup(const Csr& A, const AmgParams& prm) {
+HostHierarchy amg_setup(const Csr& A, const AmgParams& prm, const LevelReady& on_level) {
     if (A.nrows != A.ncols) fail_invalid("setup: matrix must be square");
     if (!(prm.theta > 0.0 && prm.theta <= 1.0)) fail_invalid("setup: theta must lie in (0, 1]");
     if (prm.coarse_size < 1) fail_invalid("setup: coarse_size must be >= 1");
@@ -401,6 +401,7 @@ HostHierarchy amg_setup(const Csr& A, const AmgParams& prm) {
     if (prm.cycles_nu < 1) fail_invalid("setup: cycles_nu must be >= 1");
     HostHierarchy h;
     h.params = prm;
+    h.levels.reserve(static_cast<size_t>(prm.max_levels)); // stable level addresses for on_level
     SetupTimer tm("amg");
     Csr cur = csr_copy(A);
     tm.mark("copy A");
@@ -429,7 +430,9 @@ HostHierarchy amg_setup(const Csr& A, const AmgParams& prm) {
         lev.P = std::move(P);
         lev.R = std::move(R);
         lev.split = std::move(sp);
+        if (on_level) on_level(k, lev, false);
     }
+    if (on_level) on_level(h.num_levels() - 1, h.levels.back(), true);
     h.coarse = dense_lu_factor(h.levels.back().A);
     return h;
 }

@@ -92,7 +92,12 @@ CfSplit coarsen_pmis(const Csr& S, std::uint64_t seed);
 Csr interp_direct(const Csr& A, const CfSplit& split, const Csr& S);
 Csr interp_mm_ext(const Csr& A, const CfSplit& split, const Csr& S, i64* fallback_rows);
 
-HostHierarchy amg_setup(const Csr& A, const AmgParams& params);
+/// on_level(k, level, last) runs on the calling thread as soon as level k is
+/// final (A, and P/R unless last): consumers (the device builder) may read the
+/// level concurrently with the setup of the next ones. Level addresses are
+/// stable (the level vector is reserved up front and moved, never reallocated).
+using LevelReady = std::function<void(i64, const HostLevel&, bool)>;
+HostHierarchy amg_setup(const Csr& A, const AmgParams& params, const LevelReady& on_level = {});
 
 struct FlopsModel {
     std::int64_t smoothing = 0, coarse_solve = 0, krylov_spmv = 0;
