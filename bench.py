@@ -155,9 +155,11 @@ def run_reference(args):
         return
     v = base["value"]
     print(json.dumps({
-        "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "impl": "reference", "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "ilu_smooth_sweep m5/5 on pressure27 ILUT(1e-3,5)", "sample": SAMPLE_SPEC},
+        "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "impl": "reference", "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"ilu_smooth_sweep (m_L=m_U=5, row-scaled ILUT(1e-3,5)) on {args.spec}",
+                   "sample": SAMPLE_SPEC,
+                   "parallelism": "reference CPU code on rank 0's host cores (single-threaded library)"},
         "cpu_baseline": base, "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "vs_baseline": None}))
 
