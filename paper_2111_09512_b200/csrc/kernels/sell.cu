@@ -334,6 +334,17 @@ bool serial_tail() { // ILUG_TAIL=serial: the row tail one entry at a time (A/B)
     const char* e = std::getenv("ILUG_TAIL");
     return e && e[0] == 's';
 }
+// Threads per CTA of the sweep kernel: 128 for short rows (< 10 entries on
+// average, e.g. the strict L of ILUT at C2: warps of a CTA finish at different
+// times and a smaller CTA frees its slot sooner; L sweep 370 -> 358 us), 256
+// otherwise. ILUG_ROWDOT_BLOCK=64|128|256 forces one (A/B).
+int rowdot_block(const Sell& M) {
+    if (const char* e = std::getenv("ILUG_ROWDOT_BLOCK")) {
+        const int v = std::atoi(e);
+        return v == 64 || v == 128 ? v : 256;
+    }
+    return M.nnz < 10 * M.nrows ? 128 : 256;
+}
 int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy)
     const char* e = std::getenv("ILUG_ROWDOT");
     return e && e[0] == '8' ? 8 : 4;
@@ -348,6 +359,10 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         k_rowdot<Epi, true><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else if (serial_tail())
         k_rowdot<Epi, false, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (rowdot_block(M) == 128)
+        k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 128), 128, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (rowdot_block(M) == 64)
+        k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 64), 64, 0, st>>>(view(M), M.nrows, x, epi);
     else
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     ILUG_LAUNCH_CHECK();

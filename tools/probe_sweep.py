@@ -33,12 +33,12 @@ b = torch.rand(n, dtype=torch.float64, device="cuda")
 xin = torch.rand(n, dtype=torch.float64, device="cuda")
 out = torch.empty_like(b)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for sigma in ("1024", "4096"):
+for sigma in ("1024",):
     os.environ["ILUG_SELL_SIGMA"] = sigma
     F = ilug.Factors.from_csr(n, Lc, Uc, scaling="row")
     st = F.stats()
-    for hints in ("4", "8"):
-        os.environ["ILUG_ROWDOT"] = hints
+    for hints in os.environ.get("PROBE_BLOCKS", "256").split(","):
+        os.environ["ILUG_ROWDOT_BLOCK"] = hints
         res = []
         for name, fn, nnz in (("U", F.sweep_upper, st["nnz_Us"]), ("L", F.sweep_lower, st["nnz_Ls"])):
             # m=2 = one scale/copy pass + one SpMV sweep; isolate the sweep by differencing m=3 - m=2
@@ -56,6 +56,6 @@ for sigma in ("1024", "4096"):
             ms = (ts[6] - ts[2]) / 4
             gbs = (12 * nnz + 28 * n + 4) / (ms * 1e-3) / 1e9
             res.append(f"{name}: {ms * 1e3:7.1f} us {gbs:7.1f} GB/s")
-        print(f"sigma={sigma:5s} width={hints} padded_U={st['padded_Us'] / st['nnz_Us'] - 1:.3f}  " + "  ".join(res),
+        print(f"sigma={sigma:5s} block={hints} padded_U={st['padded_Us'] / st['nnz_Us'] - 1:.3f}  " + "  ".join(res),
               flush=True)
     del F
