@@ -273,3 +273,28 @@ def test_k5_direct_at_scale_bitwise(ilug, ref, torch_cuda):
     assert bitwise(got, ref.solve_upper_scaled_direct(fr, b))
     f.solve_lower(bd, y)
     assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
+
+
+@pytest.mark.parametrize("schedule", ["", "cta", "flags"])
+def test_k5_deep_chain_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule):
+    """A 1D chain (7000 levels of one row: more levels than the warp-per-row
+    cluster kernel keeps in shared memory, so the default takes the one-CTA
+    kernel): direct solves and the Gauss-Seidel sweep stay bitwise."""
+    if schedule:
+        monkeypatch.setenv("ILUG_LEVELSET", schedule)
+    A, L, U, f, fr = _factors(ilug, ref, "poisson1d(7000)", {}, "row", direct=True)
+    assert f.stats()["levels_L"] == 7000
+    b = np.random.default_rng(35).uniform(-1, 1, A.rows)
+    bd = _dev(torch_cuda, b)
+    y = torch_cuda.empty_like(bd)
+    f.solve_lower(bd, y)
+    assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
+    f.solve_upper(bd, y)
+    assert bitwise(_host(y), ref.solve_upper_scaled_direct(fr, b))
+    S = ilug.Smoother(A, ilug.Config().set("smoother.kind", "gauss_seidel"))
+    x0 = np.random.default_rng(36).uniform(-1, 1, A.rows)
+    xd = _dev(torch_cuda, x0)
+    S.smooth(bd, xd)
+    Ar = ref.mat(*A.csr())
+    want, _ = ref.smooth(Ar, ref.smoother(Ar, ref.cfg({"smoother.kind": "gauss_seidel"})), b, x0)
+    assert bitwise(_host(xd), want)
