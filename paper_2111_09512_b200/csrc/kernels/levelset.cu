@@ -275,42 +275,65 @@ struct RowData {
     double a0 = 0.0, a1 = 0.0, bv = 0.0;
 };
 
-template <int MODE>
-__device__ __forceinline__ void warp_row(const SellView& M, const RowMeta& m, const RowData& r, int lane,
-                                         const double* __restrict__ b, double* x,
-                                         const double* __restrict__ xold) {
+// Q rows per warp at once (one per prefetch slot): every slot's x gathers are
+// issued before any slot's shuffle chain, so the slots' memory latencies
+// overlap. Entries 0..63 come from the prefetched registers; longer rows load
+// the rest inline.
+template <int MODE, int Q>
+__device__ __forceinline__ void warp_rows(const SellView& M, const RowMeta (&m)[Q], const RowData (&r)[Q], int lane,
+                                          double* x, const double* __restrict__ xold) {
     const unsigned full = 0xffffffffu;
-    const i64 row = m.row;
-    double s = r.bv, d = 1.0;
-    for (int t0 = 0; t0 < m.len; t0 += 32) {
-        const int t = t0 + lane;
-        const bool act = t < m.len;
-        i32 c;
-        double a;
-        if (t0 == 0) {
-            c = r.c0, a = r.a0;
-        } else if (t0 == 32) {
-            c = r.c1, a = r.a1;
-        } else {
-            c = act ? __ldg(M.cols + m.base + static_cast<i64>(t) * kSlice) : -1;
-            a = act ? __ldg(M.vals + m.base + static_cast<i64>(t) * kSlice) : 0.0;
-        }
-        const bool isd = act && MODE != 0 && c == row;
-        double xv = 0.0;
-        if (act && !isd) xv = is_dep<MODE>(c, row) ? __ldcg(x + c) : __ldg(xold + c); // xold: GS only
-        const double prod = a * xv; // the serial loop's rounded product
-        const unsigned dm = __ballot_sync(full, isd);
-        if (dm) d = __shfl_sync(full, a, __ffs(dm) - 1);
-        const int cnt = min(32, m.len - t0);
-        for (int u = 0; u < cnt; ++u) {
-            const double pu = __shfl_sync(full, prod, u);
-            if (!((dm >> u) & 1u)) s = s - pu;
-        }
+    double s[Q], d[Q];
+    int maxlen = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        s[q] = r[q].bv;
+        d[q] = 1.0;
+        if (m[q].row >= 0) maxlen = max(maxlen, m[q].len);
     }
-    if (lane == 0) x[row] = MODE == 0 ? s : s / d;
+    for (int t0 = 0; t0 < maxlen; t0 += 32) {
+        double prod[Q];
+        unsigned dm[Q];
+        int cnt[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const i64 row = m[q].row;
+            const bool valid = row >= 0 && t0 < m[q].len; // warp-uniform
+            const int t = t0 + lane;
+            const bool act = valid && t < m[q].len;
+            i32 c;
+            double a;
+            if (t0 == 0) {
+                c = r[q].c0, a = r[q].a0;
+            } else if (t0 == 32) {
+                c = r[q].c1, a = r[q].a1;
+            } else {
+                c = act ? __ldg(M.cols + m[q].base + static_cast<i64>(t) * kSlice) : -1;
+                a = act ? __ldg(M.vals + m[q].base + static_cast<i64>(t) * kSlice) : 0.0;
+            }
+            const bool isd = act && MODE != 0 && c == row;
+            double xv = 0.0;
+            if (act && !isd) xv = is_dep<MODE>(c, row) ? __ldcg(x + c) : __ldg(xold + c); // xold: GS only
+            prod[q] = a * xv; // the serial loop's rounded product
+            dm[q] = __ballot_sync(full, isd);
+            if (dm[q]) d[q] = __shfl_sync(full, a, __ffs(dm[q]) - 1);
+            cnt[q] = valid ? min(32, m[q].len - t0) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            for (int u = 0; u < cnt[q]; ++u) {
+                const double pu = __shfl_sync(full, prod[q], u);
+                if (!((dm[q] >> u) & 1u)) s[q] = s[q] - pu;
+            }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (m[q].row >= 0) x[m[q].row] = MODE == 0 ? s[q] : s[q] / d[q];
+    }
 }
 
-template <int MODE, int BLOCK>
+template <int MODE, int BLOCK, int Q>
 __global__ void __launch_bounds__(BLOCK, 1)
 k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b, double* x,
               const double* __restrict__ xold) {
@@ -322,10 +345,11 @@ k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const dou
     for (int l = threadIdx.x; l <= nlev; l += blockDim.x) slp[l] = level_ptr[l];
     __syncthreads();
 
-    auto load_meta = [&](int L, RowMeta& m) {
+    // slot q of level L: the level's row gw + q * GW
+    auto load_meta = [&](int L, int q, RowMeta& m) {
         m.row = -1;
         if (L >= nlev) return;
-        const i64 p = slp[L] + gw;
+        const i64 p = slp[L] + gw + q * GW;
         if (p >= slp[L + 1]) return;
         m.row = M.perm[p];
         m.len = M.rowlen[p];
@@ -340,29 +364,38 @@ k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const dou
         r.bv = b[m.row];
     };
 
-    RowMeta mc, m1, m2;
-    RowData dc, d1;
-    load_meta(0, mc);
-    load_data(mc, dc);
-    load_meta(1, m1);
+    RowMeta mc[Q], m1[Q], m2[Q];
+    RowData dc[Q], d1[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        load_meta(0, q, mc[q]);
+        load_data(mc[q], dc[q]);
+        load_meta(1, q, m1[q]);
+    }
     for (int L = 0; L < nlev; ++L) {
-        load_data(m1, d1);  // level L+1's first row, one level ahead
-        load_meta(L + 2, m2); // two ahead
-        if (mc.row >= 0) warp_row<MODE>(M, mc, dc, lane, b, x, xold);
-        // further rows of a level wider than the cluster's warps
-        for (i64 p = slp[L] + gw + GW; p < slp[L + 1]; p += GW) {
-            RowMeta m;
-            RowData r;
-            m.row = M.perm[p];
-            if (m.row < 0) continue;
-            m.len = M.rowlen[p];
-            m.base = M.slice_ptr[p >> 5] + (p & 31);
-            load_data(m, r);
-            warp_row<MODE>(M, m, r, lane, b, x, xold);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            load_data(m1[q], d1[q]);  // level L+1's rows, one level ahead
+            load_meta(L + 2, q, m2[q]); // two ahead
         }
-        mc = m1;
-        dc = d1;
-        m1 = m2;
+        warp_rows<MODE, Q>(M, mc, dc, lane, x, xold);
+        // further rows of a level wider than the cluster's warps x slots
+        for (i64 p = slp[L] + gw + Q * GW; p < slp[L + 1]; p += GW) {
+            RowMeta m[1];
+            RowData r[1];
+            m[0].row = M.perm[p];
+            if (m[0].row < 0) continue;
+            m[0].len = M.rowlen[p];
+            m[0].base = M.slice_ptr[p >> 5] + (p & 31);
+            load_data(m[0], r[0]);
+            warp_rows<MODE, 1>(M, m, r, lane, x, xold);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            mc[q] = m1[q];
+            dc[q] = d1[q];
+            m1[q] = m2[q];
+        }
         if (csize > 1) {
             asm volatile("barrier.cluster.arrive.release.aligned;\n"
                          "barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -402,9 +435,9 @@ template <int MODE>
 const void* cta_kernel() {
     return reinterpret_cast<const void*>(k_levels_cta<MODE>);
 }
-template <int MODE, int BLOCK = kWarpBlock>
+template <int MODE, int BLOCK = kWarpBlock, int Q = 1>
 const void* warp_kernel() {
-    return reinterpret_cast<const void*>(k_levels_warp<MODE, BLOCK>);
+    return reinterpret_cast<const void*>(k_levels_warp<MODE, BLOCK, Q>);
 }
 template <int MODE>
 const void* flag_kernel() {
@@ -419,17 +452,19 @@ namespace {
 // can co-schedule on one GPC.
 i64 max_cluster_ctas() {
     static const i64 c = [] {
-        const void* fns[] = {warp_kernel<0>(), warp_kernel<1>(), warp_kernel<2>(), warp_kernel<0, kWarpBlockWide>(),
-                             warp_kernel<1, kWarpBlockWide>(), warp_kernel<2, kWarpBlockWide>()};
+        const void* fns[] = {warp_kernel<0>(),       warp_kernel<1>(),       warp_kernel<2>(),
+                             warp_kernel<0, kWarpBlockWide>(), warp_kernel<1, kWarpBlockWide>(),
+                             warp_kernel<2, kWarpBlockWide>(), warp_kernel<0, kWarpBlock, 2>(),
+                             warp_kernel<1, kWarpBlock, 2>(), warp_kernel<2, kWarpBlock, 2>()};
         for (const void* fn : fns)
             if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
                 (void)cudaGetLastError();
         for (int want : {16, 8, 4, 2}) {
             bool ok = true;
-            for (int f = 0; f < 6; ++f) {
+            for (int f = 0; f < 9; ++f) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3(static_cast<unsigned>(want));
-                cfg.blockDim = dim3(f < 3 ? kWarpBlock : kWarpBlockWide);
+                cfg.blockDim = dim3(f >= 3 && f < 6 ? kWarpBlockWide : kWarpBlock);
                 cudaLaunchAttribute attr[1];
                 attr[0].id = cudaLaunchAttributeClusterDimension;
                 attr[0].val.clusterDim.x = static_cast<unsigned>(want);
@@ -502,7 +537,15 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     const i64 cmax = max_cluster_ctas();
     const i64 avg = n / std::max(nl, 1);
     single_cta_ = n <= 4 * kSmallBlock || avg <= cmax * (kWarpBlockWide / 32) * 4; // <= 4 rows per warp
+    // wide levels (> 2 rows per warp of a 512-thread cluster): 1024-thread
+    // CTAs. ILUG_LEVELSET_WIDE=slots2 takes 512-thread CTAs with two rows per
+    // warp prefetched and processed together instead (measured slower at the
+    // C2 level-1 GS: 33.5 vs 27.0 ms per presmooth — rows past the prefetched
+    // slots serialise within the warp either way).
+    slots_ = 1;
     block_ = avg > cmax * (kWarpBlock / 32) * 2 ? kWarpBlockWide : kWarpBlock;
+    if (const char* w = std::getenv("ILUG_LEVELSET_WIDE"))
+        if (std::string(w) == "slots2" && block_ == kWarpBlockWide) block_ = kWarpBlock, slots_ = 2;
     old_cta_ = false;
     if (const char* force = std::getenv("ILUG_LEVELSET")) { // test hook: cta | cta1 | flags
         if (std::string(force) == "cta" || std::string(force) == "cta1") single_cta_ = true;
@@ -513,7 +556,7 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     if (nl > kMaxSmemLevels) old_cta_ = true; // level pointers do not fit the warp kernel's shared memory
     if (single_cta_ && !old_cta_)
         cluster_ = static_cast<int>(
-            std::clamp<i64>((max_level_rows_ + block_ / 32 - 1) / (block_ / 32), 1, cmax));
+            std::clamp<i64>((max_level_rows_ + block_ / 32 * slots_ - 1) / (block_ / 32 * slots_), 1, cmax));
     if (!single_cta_) {
         flags_.alloc(n + 2); // [0, n) row flags, n epoch, n+1 ticket
         ILUG_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(n + 2) * sizeof(unsigned), st));
@@ -539,10 +582,11 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
             ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kSmallBlock), args, 0, st));
             return;
         }
-        const bool wide = block_ == kWarpBlockWide;
-        const void* fn = mode == 0   ? (wide ? warp_kernel<0, kWarpBlockWide>() : warp_kernel<0>())
-                         : mode == 1 ? (wide ? warp_kernel<1, kWarpBlockWide>() : warp_kernel<1>())
-                                     : (wide ? warp_kernel<2, kWarpBlockWide>() : warp_kernel<2>());
+        const bool wide = block_ == kWarpBlockWide, two = slots_ == 2;
+        const void* fn =
+            mode == 0   ? (wide ? warp_kernel<0, kWarpBlockWide>() : two ? warp_kernel<0, kWarpBlock, 2>() : warp_kernel<0>())
+            : mode == 1 ? (wide ? warp_kernel<1, kWarpBlockWide>() : two ? warp_kernel<1, kWarpBlock, 2>() : warp_kernel<1>())
+                        : (wide ? warp_kernel<2, kWarpBlockWide>() : two ? warp_kernel<2, kWarpBlock, 2>() : warp_kernel<2>());
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(cluster_));
         cfg.blockDim = dim3(static_cast<unsigned>(block_));

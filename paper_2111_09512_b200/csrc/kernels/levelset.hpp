@@ -36,6 +36,7 @@ private:
     int cluster_ = 1;       // CTAs of the level-synchronous cluster schedule
     bool old_cta_ = false;  // ILUG_LEVELSET=cta1: the one-CTA register-pipelined kernel
     int block_ = 512;       // threads per CTA of the warp-per-row cluster kernel
+    int slots_ = 1;         // rows per warp prefetched and processed together
     i64 max_level_rows_ = 0;
 };
 
