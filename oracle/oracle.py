@@ -59,7 +59,8 @@ class Ref:
         sig = {
             "ref_last_error": (C.c_char_p, []),
             "ref_mat_from_csr": (_i, [_ll, _ll, _pll, _pll, _pd, _pvp]),
-            "ref_mat_generate": (_i, [C.c_char_p, _pvp]),
+            "ref_mat_generate": (_i, [C.c_char_p, _pvp]), "ref_mat_read": (_i, [C.c_char_p, _pvp]),
+            "ref_mat_write": (_i, [_vp, C.c_char_p]),
             "ref_mat_info": (None, [_vp, _pll, _pll, _pll]), "ref_mat_copy": (None, [_vp, _pll, _pll, _pd]),
             "ref_mat_free": (None, [_vp]), "ref_cfg_create": (_vp, []),
             "ref_cfg_set": (_i, [_vp, C.c_char_p, C.c_char_p]), "ref_cfg_free": (None, [_vp]),
@@ -111,6 +112,16 @@ class Ref:
         self._ok(self.L.ref_mat_from_csr(n, n if ncols is None else ncols, _p(rp, C.c_int64),
                                          _p(ci, C.c_int64), _p(v, C.c_double), C.byref(out)))
         return out
+
+    def read(self, path):
+        """The reference's own Matrix Market reader (src/matrix_market.cpp)."""
+        out = C.c_void_p()
+        self._ok(self.L.ref_mat_read(path.encode(), C.byref(out)))
+        return out
+
+    def write(self, h, path):
+        """The reference's own Matrix Market writer."""
+        self._ok(self.L.ref_mat_write(h, path.encode()))
 
     def generate(self, spec):
         out = C.c_void_p()

@@ -13,6 +13,7 @@
 #include "iluamg/dense.hpp"
 #include "iluamg/ilu.hpp"
 #include "iluamg/krylov.hpp"
+#include "iluamg/matrix_market.hpp"
 #include "iluamg/problems.hpp"
 #include "iluamg/rng.hpp"
 #include "iluamg/schur.hpp"
@@ -66,6 +67,12 @@ API int ref_mat_from_csr(int64_t n, int64_t ncols, const int64_t* rp, const int6
             n, ncols, std::vector<index_t>(rp, rp + n + 1), std::vector<index_t>(ci, ci + nnz),
             std::vector<double>(v, v + nnz)));
     });
+}
+API int ref_mat_read(const char* path, void** outp) { // src/matrix_market.cpp mm_read
+    return wrap([&] { *outp = new SparseMatrix(mm_read(std::string(path))); });
+}
+API int ref_mat_write(const void* A, const char* path) { // src/matrix_market.cpp mm_write
+    return wrap([&] { mm_write(*static_cast<const SparseMatrix*>(A), std::string(path)); });
 }
 API int ref_mat_generate(const char* spec, void** outp) {
     return wrap([&] { *outp = new SparseMatrix(generate_problem(spec)); });

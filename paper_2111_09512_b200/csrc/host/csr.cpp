@@ -148,12 +148,17 @@ void SetupTimer::mark(const char* phase, i64 level) {
     t_ = t;
 }
 
-Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_zeros) {
-    for (const auto& e : t)
-        if (e.i < 0 || e.i >= nrows || e.j < 0 || e.j >= ncols)
-            fail_invalid("from_triplets: index (" + std::to_string(e.i) + "," +
-                         std::to_string(e.j) + ") out of range");
-    std::stable_sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
+namespace {
+
+[[noreturn]] void bad_triplet(const Triplet& e) {
+    fail_invalid("from_triplets: index (" + std::to_string(e.i) + "," + std::to_string(e.j) + ") out of range");
+}
+
+// Serial form, the reference's exactly (src/sparse.cpp:49-86): std::sort by
+// (row, col) — not stable, so three or more duplicates of one entry are summed
+// in the order introsort leaves them, which only the same sort reproduces.
+Csr from_triplets_serial(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_zeros) {
+    std::sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
         return a.i != b.i ? a.i < b.i : a.j < b.j;
     });
     Csr A;
@@ -171,6 +176,87 @@ Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_ze
         ++A.rp[static_cast<size_t>(i) + 1];
     }
     for (i64 i = 0; i < nrows; ++i) A.rp[i + 1] += A.rp[i];
+    return A;
+}
+
+} // namespace
+
+Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_zeros) {
+    const i64 nt = static_cast<i64>(t.size());
+    // the first out-of-range triplet in input order, as the serial check reports it
+    std::atomic<i64> first_bad{nt};
+    parallel_ranges(nt, [&](i64 b, i64 e, int) {
+        for (i64 k = b; k < e; ++k) {
+            const Triplet& x = t[k];
+            if (x.i < 0 || x.i >= nrows || x.j < 0 || x.j >= ncols) {
+                i64 cur = first_bad.load();
+                while (k < cur && !first_bad.compare_exchange_weak(cur, k)) {
+                }
+                return;
+            }
+        }
+    });
+    if (first_bad.load() < nt) bad_triplet(t[first_bad.load()]);
+    if (nt < (i64{1} << 20)) return from_triplets_serial(nrows, ncols, std::move(t), keep_zeros);
+
+    // Parallel form with the same result whenever no entry occurs three or more
+    // times (two duplicates sum to the same value in either order): bucket
+    // triplet indices by row, sort each bucket by (column, input index), sum
+    // duplicates, drop exact zeros. Triple duplicates fall back to the serial
+    // std::sort, whose order for them is the reference's.
+    std::unique_ptr<std::atomic<i64>[]> cnt(new std::atomic<i64>[static_cast<size_t>(nrows) + 1]);
+    parallel_ranges(nrows + 1, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) cnt[i].store(0, std::memory_order_relaxed);
+    });
+    parallel_ranges(nt, [&](i64 b, i64 e, int) {
+        for (i64 k = b; k < e; ++k) cnt[t[k].i + 1].fetch_add(1, std::memory_order_relaxed);
+    });
+    std::vector<i64> start(static_cast<size_t>(nrows) + 1, 0);
+    for (i64 i = 0; i < nrows; ++i) start[i + 1] = start[i] + cnt[i + 1].load(std::memory_order_relaxed);
+    parallel_ranges(nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) cnt[i].store(start[i], std::memory_order_relaxed);
+    });
+    RawVec<i64> idx(static_cast<size_t>(nt));
+    parallel_ranges(nt, [&](i64 b, i64 e, int) {
+        for (i64 k = b; k < e; ++k) idx[cnt[t[k].i].fetch_add(1, std::memory_order_relaxed)] = k;
+    });
+    Csr A;
+    A.nrows = nrows;
+    A.ncols = ncols;
+    A.rp.assign(static_cast<size_t>(nrows) + 1, 0);
+    RawVec<i32> cj(static_cast<size_t>(nt));
+    RawVec<double> cv(static_cast<size_t>(nt));
+    std::vector<i64> kept(static_cast<size_t>(nrows), 0);
+    std::atomic<bool> triple{false};
+    parallel_ranges(nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            i64* lo = idx.data() + start[i];
+            i64* hi = idx.data() + start[i + 1];
+            std::sort(lo, hi, [&](i64 a, i64 c) { return t[a].j != t[c].j ? t[a].j < t[c].j : a < c; });
+            i64 o = start[i];
+            for (i64* q = lo; q < hi;) {
+                const i64 j = t[*q].j;
+                double s = t[*q].v;
+                i64 dup = 1;
+                for (++q; q < hi && t[*q].j == j; ++q, ++dup) s += t[*q].v;
+                if (dup >= 3) triple.store(true, std::memory_order_relaxed);
+                if (s == 0.0 && !keep_zeros) continue;
+                cj[o] = static_cast<i32>(j);
+                cv[o++] = s;
+            }
+            kept[i] = o - start[i];
+        }
+    });
+    if (triple.load()) return from_triplets_serial(nrows, ncols, std::move(t), keep_zeros);
+    for (i64 i = 0; i < nrows; ++i) A.rp[i + 1] = A.rp[i] + kept[i];
+    A.ci.resize(static_cast<size_t>(A.rp[nrows]));
+    A.v.resize(static_cast<size_t>(A.rp[nrows]));
+    parallel_ranges(nrows, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            std::copy(cj.begin() + start[i], cj.begin() + start[i] + kept[i], A.ci.begin() + A.rp[i]);
+            std::copy(cv.begin() + start[i], cv.begin() + start[i] + kept[i], A.v.begin() + A.rp[i]);
+        }
+    });
     return A;
 }
 

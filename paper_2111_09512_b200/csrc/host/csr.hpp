@@ -51,8 +51,9 @@ struct Triplet {
     double v;
 };
 
-/// Sort by (row, col), sum duplicates in input order, drop exact zeros unless
-/// keep_zeros (SparseMatrix::from_triplets, src/sparse.cpp:49-86).
+/// Sort by (row, col), sum duplicates, drop exact zeros unless keep_zeros
+/// (SparseMatrix::from_triplets, src/sparse.cpp:49-86; its std::sort order for
+/// repeated entries). Parallel above 2^20 triplets.
 Csr csr_from_triplets(i64 nrows, i64 ncols, std::vector<Triplet> t, bool keep_zeros = false);
 
 /// Validating adopt (SparseMatrix::from_csr, src/sparse.cpp:88-118).

@@ -1,7 +1,14 @@
 #include "problems.hpp"
 #include "dist.hpp"
 
+#include <atomic>
+#include <charconv>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <cctype>
+#include <cfloat>
 #include <cmath>
 #include <cstdio>
 #include <fstream>
@@ -307,8 +314,117 @@ Csr generate_problem(const std::string& spec) {
     fail_invalid("generate_problem: unknown generator '" + kind + "'");
 }
 
+namespace {
+
+bool mm_space(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r'; }
+
+// Parallel parse of the entry section data[0, size): tokens are maximal
+// non-whitespace runs (the reference reads entries with operator>>, so line
+// breaks carry no meaning). Fills i/j (1-based) and v for the first nnz
+// entries. Returns false on anything the plain from_chars path does not parse
+// exactly like operator>> would (a sign '+', inf/nan, out-of-range numbers,
+// trailing garbage in a token, fewer than 3*nnz tokens): the caller then
+// re-reads the file with the reference-order stream parser.
+bool mm_parse_entries(const char* data, size_t size, i64 nnz, std::vector<i64>& I, std::vector<i64>& J,
+                      std::vector<double>& V) {
+    const i64 need = 3 * nnz;
+    const int T = std::max(1, host_threads() * 4);
+    std::vector<size_t> cut(static_cast<size_t>(T) + 1, size);
+    cut[0] = 0;
+    for (int c = 1; c < T; ++c) {
+        size_t p = size * static_cast<size_t>(c) / static_cast<size_t>(T);
+        while (p < size && !mm_space(data[p])) ++p; // chunk edges on whitespace
+        cut[c] = std::max(p, cut[c - 1]);
+    }
+    std::vector<i64> ntok(static_cast<size_t>(T) + 1, 0);
+    parallel_ranges(T, [&](i64 b, i64 e, int) {
+        for (i64 c = b; c < e; ++c) {
+            i64 n = 0;
+            bool in = false;
+            for (size_t p = cut[c]; p < cut[c + 1]; ++p) {
+                const bool sp = mm_space(data[p]);
+                n += !sp && !in;
+                in = !sp;
+            }
+            ntok[c + 1] = n;
+        }
+    }, 1);
+    for (int c = 0; c < T; ++c) ntok[c + 1] += ntok[c];
+    if (ntok[T] < need) return false;
+    I.resize(static_cast<size_t>(nnz));
+    J.resize(static_cast<size_t>(nnz));
+    V.resize(static_cast<size_t>(nnz));
+    std::atomic<bool> ok{true};
+    parallel_ranges(T, [&](i64 b, i64 e, int) {
+        for (i64 c = b; c < e && ok.load(std::memory_order_relaxed); ++c) {
+            i64 g = ntok[c];
+            size_t p = cut[c];
+            const size_t end = cut[c + 1];
+            while (p < end && g < need) {
+                while (p < end && mm_space(data[p])) ++p;
+                if (p >= end) break;
+                size_t q = p;
+                while (q < end && !mm_space(data[q])) ++q;
+                const char* a = data + p;
+                const char* z = data + q;
+                const i64 ent = g / 3;
+                // a digit or '.' first, after at most one '-': no '+', inf or nan
+                const char* d0 = *a == '-' && a + 1 < z ? a + 1 : a;
+                if (*d0 != '.' && !(*d0 >= '0' && *d0 <= '9')) {
+                    ok = false;
+                    return;
+                }
+                if (g % 3 < 2) {
+                    i64 x = 0;
+                    const auto r = std::from_chars(a, z, x);
+                    if (r.ec != std::errc() || r.ptr != z) {
+                        ok = false;
+                        return;
+                    }
+                    (g % 3 == 0 ? I : J)[static_cast<size_t>(ent)] = x;
+                } else {
+                    double x = 0.0;
+                    const auto r = std::from_chars(a, z, x, std::chars_format::general);
+                    // subnormal results: the stream parser's range handling decides
+                    if (r.ec != std::errc() || r.ptr != z || (x != 0.0 && std::abs(x) < DBL_MIN)) {
+                        ok = false;
+                        return;
+                    }
+                    V[static_cast<size_t>(ent)] = x;
+                }
+                ++g;
+                p = q;
+            }
+        }
+    }, 1);
+    return ok.load();
+}
+
+} // namespace
+
+// src/matrix_market.cpp semantics (header/size checks, entry errors by entry
+// number, symmetric storage expanded, then from_triplets: duplicates summed in
+// input order, exact zeros dropped). The entry section is parsed in parallel
+// from a memory map; files the fast parser declines are read with the
+// reference-order stream parser (mm_read_stream), so results and errors are
+// the reference's either way.
+Csr mm_read_stream(std::istream& in, const std::string& path, i64 nr, i64 nc, i64 nnz, bool symmetric) {
+    std::vector<Triplet> t;
+    t.reserve(static_cast<size_t>(symmetric ? 2 * nnz : nnz));
+    for (i64 k = 0; k < nnz; ++k) {
+        i64 i = 0, j = 0;
+        double v = 0.0;
+        if (!(in >> i >> j >> v)) fail_io("mm_read: '" + path + "' truncated at entry " + std::to_string(k + 1));
+        if (i < 1 || i > nr || j < 1 || j > nc)
+            fail_io("mm_read: '" + path + "' index out of range at entry " + std::to_string(k + 1));
+        t.push_back({i - 1, j - 1, v});
+        if (symmetric && i != j) t.push_back({j - 1, i - 1, v});
+    }
+    return csr_from_triplets(nr, nc, std::move(t));
+}
+
 Csr mm_read(const std::string& path) {
-    std::ifstream in(path);
+    std::ifstream in(path, std::ios::binary);
     if (!in) fail_io("mm_read: cannot open '" + path + "'");
     std::string line;
     if (!std::getline(in, line)) fail_io("mm_read: '" + path + "' is empty");
@@ -335,30 +451,98 @@ Csr mm_read(const std::string& path) {
     i64 nr = 0, nc = 0, nnz = 0;
     if (!(sz >> nr >> nc >> nnz) || nr < 0 || nc < 0 || nnz < 0)
         fail_io("mm_read: '" + path + "' has a malformed size line");
-    std::vector<Triplet> t;
-    t.reserve(static_cast<size_t>(symmetric ? 2 * nnz : nnz));
-    for (i64 k = 0; k < nnz; ++k) {
-        i64 i = 0, j = 0;
-        double v = 0.0;
-        if (!(in >> i >> j >> v)) fail_io("mm_read: '" + path + "' truncated at entry " + std::to_string(k + 1));
-        if (i < 1 || i > nr || j < 1 || j > nc)
-            fail_io("mm_read: '" + path + "' index out of range at entry " + std::to_string(k + 1));
-        t.push_back({i - 1, j - 1, v});
-        if (symmetric && i != j) t.push_back({j - 1, i - 1, v});
+    const std::streamoff body = in.tellg();
+
+    // fast path: map the file, parse the entry section in parallel
+    if (body >= 0 && nnz > 0) {
+        const int fd = ::open(path.c_str(), O_RDONLY);
+        struct stat st {};
+        if (fd >= 0 && ::fstat(fd, &st) == 0 && st.st_size > body) {
+            const size_t fsize = static_cast<size_t>(st.st_size);
+            void* m = ::mmap(nullptr, fsize, PROT_READ, MAP_PRIVATE, fd, 0);
+            ::close(fd);
+            if (m != MAP_FAILED) {
+                std::vector<i64> I, J;
+                std::vector<double> V;
+                const bool ok = mm_parse_entries(static_cast<const char*>(m) + body, fsize - static_cast<size_t>(body),
+                                                 nnz, I, J, V);
+                ::munmap(m, fsize);
+                if (ok) {
+                    // first out-of-range entry in order, as the stream parser reports it
+                    std::atomic<i64> bad{nnz};
+                    parallel_ranges(nnz, [&](i64 b, i64 e, int) {
+                        for (i64 k = b; k < e; ++k)
+                            if (I[k] < 1 || I[k] > nr || J[k] < 1 || J[k] > nc) {
+                                i64 cur = bad.load();
+                                while (k < cur && !bad.compare_exchange_weak(cur, k)) {
+                                }
+                                return;
+                            }
+                    });
+                    if (bad.load() < nnz)
+                        fail_io("mm_read: '" + path + "' index out of range at entry " +
+                                std::to_string(bad.load() + 1));
+                    // triplets in input order (a symmetric off-diagonal entry is followed by its mirror)
+                    std::vector<i64> off(static_cast<size_t>(nnz) + 1, 0);
+                    if (symmetric) {
+                        parallel_ranges(nnz, [&](i64 b, i64 e, int) {
+                            for (i64 k = b; k < e; ++k) off[k + 1] = I[k] != J[k];
+                        });
+                        for (i64 k = 0; k < nnz; ++k) off[k + 1] += off[k];
+                    }
+                    std::vector<Triplet> t(static_cast<size_t>(nnz + off[nnz]));
+                    parallel_ranges(nnz, [&](i64 b, i64 e, int) {
+                        for (i64 k = b; k < e; ++k) {
+                            const i64 o = k + off[k];
+                            t[o] = {I[k] - 1, J[k] - 1, V[k]};
+                            if (symmetric && I[k] != J[k]) t[o + 1] = {J[k] - 1, I[k] - 1, V[k]};
+                        }
+                    });
+                    return csr_from_triplets(nr, nc, std::move(t));
+                }
+            }
+        } else if (fd >= 0) {
+            ::close(fd);
+        }
+        in.clear();
+        in.seekg(body);
     }
-    return csr_from_triplets(nr, nc, std::move(t));
+    return mm_read_stream(in, path, nr, nc, nnz, symmetric);
 }
 
+// Same text as src/matrix_market.cpp mm_write ("%.17g" values, 1-based
+// indices, one entry per line); rows are formatted in parallel blocks and
+// written in order.
 void mm_write(const Csr& A, const std::string& path) {
     FILE* f = std::fopen(path.c_str(), "w");
     if (!f) fail_io("mm_write: cannot open '" + path + "' for writing");
     std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n",
                  static_cast<long long>(A.nrows), static_cast<long long>(A.ncols),
                  static_cast<long long>(A.nnz()));
-    for (i64 i = 0; i < A.nrows; ++i)
-        for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k)
-            std::fprintf(f, "%lld %d %.17g\n", static_cast<long long>(i + 1), A.ci[k] + 1, A.v[k]);
-    if (std::fclose(f) != 0) fail_io("mm_write: write to '" + path + "' failed");
+    constexpr i64 kRows = 1 << 16; // rows per formatted block
+    const i64 nblk = (A.nrows + kRows - 1) / kRows;
+    bool ok = true;
+    for (i64 b0 = 0; b0 < nblk && ok; b0 += 64) { // 64 blocks in flight at a time
+        const i64 b1 = std::min(nblk, b0 + 64);
+        std::vector<std::string> text(static_cast<size_t>(b1 - b0));
+        parallel_ranges(b1 - b0, [&](i64 lo, i64 hi, int) {
+            char buf[96];
+            for (i64 bb = lo; bb < hi; ++bb) {
+                std::string& out = text[static_cast<size_t>(bb)];
+                const i64 r0 = (b0 + bb) * kRows, r1 = std::min(A.nrows, r0 + kRows);
+                out.reserve(static_cast<size_t>(A.rp[r1] - A.rp[r0]) * 36);
+                for (i64 i = r0; i < r1; ++i)
+                    for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                        const int m = std::snprintf(buf, sizeof buf, "%lld %d %.17g\n", static_cast<long long>(i + 1),
+                                                    A.ci[k] + 1, A.v[k]);
+                        out.append(buf, static_cast<size_t>(m));
+                    }
+            }
+        }, 1);
+        for (const std::string& t : text)
+            if (std::fwrite(t.data(), 1, t.size(), f) != t.size()) ok = false;
+    }
+    if (std::fclose(f) != 0 || !ok) fail_io("mm_write: write to '" + path + "' failed");
 }
 
 } // namespace ilug
