@@ -431,6 +431,115 @@ k_levels_flags(SellView M, i64 nslices, const double* __restrict__ b, double* x,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Sync-free schedule with the solution values as their own flags (default for
+// wide DAGs). x is filled with a signalling-NaN sentinel that arithmetic never
+// produces (GPU results are quiet NaNs), every row publishes its value with a
+// single relaxed 64-bit store, and a row polls its dependencies' x entries
+// directly: the value it is waiting for is the value it needs, so there is no
+// separate flag, no acquire fence and no release fence on the critical path
+// (one L2 round trip per level instead of ~4 plus two MEMBARs; the separate
+// flag form measured 7.5-18.7 us per level at C2 vs 2.5 us for cuSPARSE SpSV).
+// A row whose result has the sentinel's exact bits (only possible when an
+// empty row copies that sNaN from b) publishes the canonical NaN instead.
+constexpr unsigned long long kXSentinel = 0x7FF0DEAD5EA1ED01ull; // signalling NaN
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(double* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void k_fill_sentinel(double* x, i64 n) {
+    const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) reinterpret_cast<unsigned long long*>(x)[i] = kXSentinel;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFlagBlock)
+k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x, const double* __restrict__ xold,
+                unsigned* ticket, unsigned* err) {
+    constexpr int kChunk = 16;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned sl = 0;
+        if (lane == 0) sl = atomicAdd(ticket, 1u);
+        sl = __shfl_sync(0xffffffffu, sl, 0);
+        if (sl >= nslices) return;
+        const i64 p = static_cast<i64>(sl) * kSlice + lane;
+        const i64 row = M.perm[p];
+        if (row < 0) continue;
+        const int len = M.rowlen[p];
+        const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+        double s = b[row], d = 1.0;
+        for (int t0 = 0; t0 < len; t0 += kChunk) {
+            i32 c[kChunk];
+            double a[kChunk], xv[kChunk];
+#pragma unroll
+            for (int u = 0; u < kChunk; ++u)
+                if (t0 + u < len) {
+                    const i64 q = base + static_cast<i64>(t0 + u) * kSlice;
+                    c[u] = __ldg(M.cols + q);
+                    a[u] = __ldg(M.vals + q);
+                }
+            // dependencies: poll the values themselves (all of the chunk in flight)
+            unsigned pend = 0;
+#pragma unroll
+            for (int u = 0; u < kChunk; ++u) {
+                xv[u] = 0.0;
+                if (t0 + u < len && !(MODE != 0 && c[u] == row)) {
+                    if (is_dep<MODE>(c[u], row)) {
+                        const unsigned long long v = ld_relaxed_u64(x + c[u]);
+                        xv[u] = __longlong_as_double(static_cast<long long>(v));
+                        if (v == kXSentinel) pend |= 1u << u;
+                    } else {
+                        xv[u] = __ldg(xold + c[u]); // GS (MODE 2) only
+                    }
+                }
+            }
+            long long spins = 0;
+            while (pend) {
+                if (++spins > (1ll << 26)) { // seconds: a scheduling bug, not a slow producer
+                    atomicExch(err, 1u);
+                    break;
+                }
+                __nanosleep(32);
+#pragma unroll
+                for (int u = 0; u < kChunk; ++u)
+                    if ((pend >> u) & 1u) {
+                        const unsigned long long v = ld_relaxed_u64(x + c[u]);
+                        if (v != kXSentinel) {
+                            xv[u] = __longlong_as_double(static_cast<long long>(v));
+                            pend &= ~(1u << u);
+                        }
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < kChunk; ++u)
+                if (t0 + u < len) {
+                    if (MODE != 0 && c[u] == row)
+                        d = a[u];
+                    else
+                        s = s - a[u] * xv[u];
+                }
+        }
+        const double r = MODE == 0 ? s : s / d;
+        unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(r));
+        if (bits == kXSentinel) bits = 0x7FFFFFFFFFFFFFFFull; // the canonical NaN
+        st_relaxed_u64(x + row, bits);
+    }
+}
+
+__global__ void k_ticket_reset(unsigned* ticket) { *ticket = 0u; }
+
+template <int MODE>
+const void* vflag_kernel() {
+    return reinterpret_cast<const void*>(k_levels_vflags<MODE>);
+}
+
 template <int MODE>
 const void* cta_kernel() {
     return reinterpret_cast<const void*>(k_levels_cta<MODE>);
@@ -536,7 +645,10 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // CTAs for the widest level's slices, capped by what one GPC co-schedules.
     const i64 cmax = max_cluster_ctas();
     const i64 avg = n / std::max(nl, 1);
-    single_cta_ = n <= 4 * kSmallBlock || avg <= cmax * (kWarpBlockWide / 32) * 4; // <= 4 rows per warp
+    // measured: the cluster kernel wins up to a few hundred rows per level
+    // (coarse-level GS at 128^3: 258 rows/level 3.3 vs 4.6 ms), the value-flag
+    // kernel beyond (ILUT factors at 128^3, 1564 rows/level: 4.9 vs 10.6 ms L)
+    single_cta_ = n <= 4 * kSmallBlock || avg <= 512;
     // wide levels (> 2 rows per warp of a 512-thread cluster): 1024-thread
     // CTAs. ILUG_LEVELSET_WIDE=slots2 takes 512-thread CTAs with two rows per
     // warp prefetched and processed together instead (measured slower at the
@@ -557,9 +669,14 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     if (single_cta_ && !old_cta_)
         cluster_ = static_cast<int>(
             std::clamp<i64>((max_level_rows_ + block_ / 32 * slots_ - 1) / (block_ / 32 * slots_), 1, cmax));
+    value_flags_ = true;
+    if (const char* force = std::getenv("ILUG_LEVELSET"))
+        if (std::string(force) == "flags") value_flags_ = false; // the separate-flag form (A/B, tests)
+    if (const char* force = std::getenv("ILUG_LEVELSET"))
+        if (std::string(force) == "vflags" && n > 0) single_cta_ = false;
     if (!single_cta_) {
-        flags_.alloc(n + 2); // [0, n) row flags, n epoch, n+1 ticket
-        ILUG_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(n + 2) * sizeof(unsigned), st));
+        flags_.alloc(n + 3); // [0, n) row flags, n epoch, n+1 ticket, n+2 wait timeout
+        ILUG_CUDA(cudaMemsetAsync(flags_.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
         const i64 slices = M_.nrows_pad / kSlice;
         grid_ = static_cast<int>(std::min<i64>((slices + kFlagBlock / 32 - 1) / (kFlagBlock / 32),
                                                static_cast<i64>(device_sm_count()) * 8));
@@ -604,9 +721,20 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
     unsigned* flags = flags_.p;
     unsigned* epoch = flags_.p + n;
     unsigned* ticket = flags_.p + n + 1;
+    i64 ns = M_.nrows_pad / kSlice;
+    if (value_flags_ && x != b && x != xold) {
+        // the solution entries are the flags: fill x with the sentinel, reset the ticket
+        k_fill_sentinel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, n);
+        k_ticket_reset<<<1, 1, 0, st>>>(ticket);
+        ILUG_LAUNCH_CHECK();
+        unsigned* err = flags_.p + n + 2;
+        void* args[] = {&mv, &ns, &b, &x, &xold, &ticket, &err};
+        const void* fn = mode == 0 ? vflag_kernel<0>() : mode == 1 ? vflag_kernel<1>() : vflag_kernel<2>();
+        ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid_)), dim3(kFlagBlock), args, 0, st));
+        return;
+    }
     k_epoch_bump<<<1, 1, 0, st>>>(epoch, ticket);
     ILUG_LAUNCH_CHECK();
-    i64 ns = M_.nrows_pad / kSlice;
     const unsigned* ep = epoch;
     void* args[] = {&mv, &ns, &b, &x, &xold, &flags, &ep, &ticket};
     const void* fn = mode == 0 ? flag_kernel<0>() : mode == 1 ? flag_kernel<1>() : flag_kernel<2>();

@@ -37,6 +37,7 @@ private:
     bool old_cta_ = false;  // ILUG_LEVELSET=cta1: the one-CTA register-pipelined kernel
     int block_ = 512;       // threads per CTA of the warp-per-row cluster kernel
     int slots_ = 1;         // rows per warp prefetched and processed together
+    bool value_flags_ = true; // sync-free schedule polls x itself (sentinel-filled) instead of flags
     i64 max_level_rows_ = 0;
 };
 

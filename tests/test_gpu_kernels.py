@@ -214,14 +214,14 @@ def test_c3_cutcell_scaled_vs_unscaled(ilug, ref, port, torch_cuda):
     assert errs[0] > errs[1] > errs[2]
 
 
-@pytest.mark.parametrize("schedule", ["cta", "cta1", "flags"])
+@pytest.mark.parametrize("schedule", ["cta", "cta1", "flags", "vflags"])
 @pytest.mark.parametrize("spec,kv", [("poisson3d(24,24,20)", {}),
                                      ("pressure27(16,16,16)", {"ilu.variant": "ilut", "ilu.droptol": "1e-3",
                                                                "ilu.lfill": "5"})])
 def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule, spec, kv):
     """Every level-set schedule (cluster-synchronous, single CTA, sync-free
-    flags) gives the serial result bitwise, for the triangular solves and the
-    Gauss-Seidel sweep."""
+    separate flags, sync-free value flags) gives the serial result bitwise, for
+    the triangular solves and the Gauss-Seidel sweep."""
     monkeypatch.setenv("ILUG_LEVELSET", schedule)
     A, L, U, f, fr = _factors(ilug, ref, spec, kv, "row", direct=True)
     b = np.random.default_rng(31).uniform(-1, 1, A.rows)
@@ -240,7 +240,7 @@ def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule,
     assert bitwise(_host(xd), want)
 
 
-@pytest.mark.parametrize("schedule", ["", "cta", "flags"])
+@pytest.mark.parametrize("schedule", ["", "cta", "flags", "vflags"])
 def test_k5_wide_dag_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule):
     """A wide DAG (n / levels > 2048: levels wider than a cluster's threads,
     so cluster threads take several rows per level)."""
@@ -275,7 +275,7 @@ def test_k5_direct_at_scale_bitwise(ilug, ref, torch_cuda):
     assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
 
 
-@pytest.mark.parametrize("schedule", ["", "cta", "flags"])
+@pytest.mark.parametrize("schedule", ["", "cta", "flags", "vflags"])
 def test_k5_deep_chain_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule):
     """A 1D chain (7000 levels of one row: more levels than the warp-per-row
     cluster kernel keeps in shared memory, so the default takes the one-CTA
