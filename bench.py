@@ -407,17 +407,28 @@ def time_to_solution(ilug, A, fallbacks=("poly_gs",)):
         res = {}
         base = dict(ILU_KV, **{"smoother.sweeps": "2", "krylov.tol": "1e-8", "amg.coarsening": "pmis",
                                "krylov.form_iterates": "false", "smoother.fallback.kind": fb})
-        for mode in ("richardson", "direct"):
-            kv = dict(base, **{"trisolve.mode": mode})
+        modes = ("richardson", "direct") + (("direct_cusparse",) if fb == "poly_gs" else ())
+        for mode in modes:
+            # direct_cusparse: the same direct solve through cuSPARSE SpSV (ILUG_DIRECT=cusparse),
+            # the library comparison point for the level-scheduled K5 kernels
+            kv = dict(base, **{"trisolve.mode": "direct" if mode == "direct_cusparse" else mode})
+            if mode == "direct_cusparse":
+                os.environ["ILUG_DIRECT"] = "cusparse"
             # warm-up on a small matrix: lazy module loading of every kernel the
             # solve uses happens here, not inside the timed solve below
             ilug.run_solve(ilug.Matrix.generate("pressure27(24,24,24)"), ilug.Config().update(kv))
-            rep = ilug.run_solve(A, ilug.Config().update(kv))
+            try:
+                rep = ilug.run_solve(A, ilug.Config().update(kv))
+            finally:
+                os.environ.pop("ILUG_DIRECT", None)
             res[mode] = {"iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
                          "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
                          "final_relres": float(rep["final_relres"]), "levels": int(rep["levels"]),
                          "vcycles": int(rep["device_vcycles"])}
         res["speedup_iterative_vs_direct"] = round(res["direct"]["solve_s"] / res["richardson"]["solve_s"], 3)
+        if "direct_cusparse" in res:
+            res["speedup_iterative_vs_cusparse_direct"] = round(
+                res["direct_cusparse"]["solve_s"] / res["richardson"]["solve_s"], 3)
         out[f"fallback_{fb}"] = res
     return out
 

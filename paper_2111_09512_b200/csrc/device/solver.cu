@@ -90,6 +90,12 @@ void DeviceIlu::finish(DevFactors& df, const HostFactors* host, ScalingKind scal
     if (direct_plans) {
         lower_plan_.build(hp->L, LevelPlan::Kind::lower_unit, st);
         upper_plan_.build(hp->U, LevelPlan::Kind::upper, st, v);
+        if (direct_uses_cusparse()) {
+            cs_lower_ = std::make_unique<CusparseTri>();
+            cs_lower_->build(n_, df.Lrp.p, df.Lci.p, df.Lv.p, df.Lv.n, true, st);
+            cs_upper_ = std::make_unique<CusparseTri>();
+            cs_upper_->build(n_, df.Urp.p, df.Uci.p, v, df.Uv.n, false, st);
+        }
     }
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
@@ -151,19 +157,29 @@ void DeviceIlu::sweep_upper(const double* b, double* x, i64 m, double* ws, cudaS
         vec_copy(x, cur, n_, st);
 }
 
+void DeviceIlu::lower_direct(const double* b, double* y, cudaStream_t st) const {
+    if (cs_lower_) return cs_lower_->solve(b, y, st);
+    lower_plan_.solve(b, y, nullptr, st);
+}
+
+void DeviceIlu::upper_direct(const double* b, double* x, cudaStream_t st) const {
+    if (cs_upper_) return cs_upper_->solve(b, x, st);
+    upper_plan_.solve(b, x, nullptr, st);
+}
+
 void DeviceIlu::solve_lower(const double* b, double* y, cudaStream_t st) const {
     if (!has_plans()) fail_invalid("ilu factors: level plans were not built (direct mode off)");
-    lower_plan_.solve(b, y, nullptr, st);
+    lower_direct(b, y, st);
 }
 
 void DeviceIlu::solve_upper(const double* b, double* x, double* ws, cudaStream_t st) const {
     if (!has_plans()) fail_invalid("ilu factors: level plans were not built (direct mode off)");
     if (has_rs()) {
         vec_div(ws, b, rs_.p, n_, st);
-        upper_plan_.solve(ws, x, nullptr, st);
+        upper_direct(ws, x, st);
         if (has_cs()) vec_div(x, x, cs_.p, n_, st);
     } else {
-        upper_plan_.solve(b, x, nullptr, st);
+        upper_direct(b, x, st);
     }
 }
 
@@ -289,9 +305,9 @@ void DeviceSmoother::ilu_sweep(const double* b, double* x, bool x_zero, cudaStre
         f.solve_lower(rr, ya, st);
         if (f.has_rs()) {
             vec_div(bs, ya, f.rs(), n, st);
-            f.upper_plan().solve(bs, xa, nullptr, st);
+            f.upper_direct(bs, xa, st);
         } else {
-            f.upper_plan().solve(ya, xa, nullptr, st);
+            f.upper_direct(ya, xa, st);
         }
         if (f.has_cs())
             vec_acc_div(x, xa, f.cs(), n, st);

@@ -14,6 +14,7 @@
 #include "../kernels/ilu0.hpp"
 #include "../kernels/levelset.hpp"
 #include "../kernels/wavefront.hpp"
+#include "spsv_cusparse.hpp"
 
 #include <deque>
 #include <memory>
@@ -91,6 +92,10 @@ public:
     bool has_plans() const { return lower_plan_.levels() > 0 || n_ == 0; }
     const LevelPlan& lower_plan() const { return lower_plan_; }
     const LevelPlan& upper_plan() const { return upper_plan_; }
+    /// The triangular solves behind solve_lower/solve_upper without the scaling
+    /// steps: K5 level schedules, or cuSPARSE SpSV under ILUG_DIRECT=cusparse.
+    void lower_direct(const double* b, double* y, cudaStream_t st) const;
+    void upper_direct(const double* b, double* x, cudaStream_t st) const;
 
     /// Download the scaled factor U (unit diagonal re-inserted) for parity tests.
     Csr scaled_upper_host() const;
@@ -108,6 +113,7 @@ private:
     Sell Ls_, Us_;          // strict parts (Us_ scaled unless upper_ == jacobi)
     DBuf<double> rs_, cs_, d_;
     LevelPlan lower_plan_, upper_plan_;
+    std::unique_ptr<CusparseTri> cs_lower_, cs_upper_; // ILUG_DIRECT=cusparse
     WavePlan wave_L_, wave_U_; // fused multi-sweep plans (large n only, see wave_enabled)
 };
 
