@@ -156,3 +156,27 @@ def test_device_ilu0_large_bitwise(ilug, torch_cuda):
     Ld, Ud = ilug.ilu_factorize_device(A, cfg)
     Lh, Uh = ilug.ilu_factorize(A, cfg)
     assert bitwise(Ud.csr()[2], Uh.csr()[2]) and bitwise(Ld.csr()[2], Lh.csr()[2])
+
+
+@pytest.mark.parametrize("kind", ["gauss_seidel", "ilu"])
+def test_setup_pipeline_errors_propagate(ilug, ref, torch_cuda, kind):
+    """A failure inside the overlapped setup (the device builder thread for a
+    GS smoother with a zero diagonal, the early factorisation thread for an ILU
+    zero pivot) surfaces as the reference's status-3 error, and the next solve
+    in the process still works."""
+    A = ilug.Matrix.generate("poisson2d(16,16)")
+    rp, ci, v = A.csr()
+    v = v.copy()
+    row = 37
+    for k in range(rp[row], rp[row + 1]):
+        if ci[k] == row:
+            v[k] = 0.0  # structurally present, numerically zero diagonal
+    kv = {"krylov.tol": "1e-8", "smoother.kind": kind, "amg.coarsening": "pmis", "amg.coarse_size": "16"}
+    with pytest.raises(Exception) as er:
+        ref.run_solve((rp, ci, v), kv)
+    assert "[status 3]" in str(er.value)
+    with pytest.raises(ilug.IlugError) as e:
+        ilug.run_solve(ilug.Matrix.from_csr(A.rows, A.rows, rp, ci, v), ilug.Config().update(kv))
+    assert e.value.status == 3
+    ok = ilug.run_solve(A, ilug.Config().update(kv))
+    assert ok["converged"] == "true"
