@@ -59,6 +59,12 @@ ILUAMG_API int ilug_ilu_factorize(const iluamg_matrix* A, const iluamg_config* c
  * force the host path. */
 ILUAMG_API int ilug_ilu_factorize_device(const iluamg_matrix* A, const iluamg_config* cfg,
                                          iluamg_matrix** L, iluamg_matrix** U);
+/* Device sparse products (kernels/spgemm.cu), bitwise equal to the host
+ * SparseMatrix::multiply (src/sparse.cpp:176-231): C = A B, and the AMG
+ * Galerkin operator C = R (A P) with A P kept on the device. */
+ILUAMG_API int ilug_matmul_device(const iluamg_matrix* A, const iluamg_matrix* B, iluamg_matrix** C);
+ILUAMG_API int ilug_galerkin_device(const iluamg_matrix* A, const iluamg_matrix* P, const iluamg_matrix* R,
+                                    iluamg_matrix** C);
 
 /* ---- K1-K5: factors ---- */
 /* Host ILU per the config's ilu.* keys, then upload + K1 scaling per `scaling`

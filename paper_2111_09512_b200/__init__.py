@@ -62,6 +62,7 @@ _SIGS = {
     "ilug_matrix_copy_csr": (_i, [_vp, _pll, _pll, _pd]),
     "ilug_ilu_factorize": (_i, [_vp, _vp, _pvp, _pvp]),
     "ilug_ilu_factorize_device": (_i, [_vp, _vp, _pvp, _pvp]),
+    "ilug_matmul_device": (_i, [_vp, _vp, _pvp]), "ilug_galerkin_device": (_i, [_vp, _vp, _vp, _pvp]),
     "ilug_factors_create": (_i, [_vp, _vp, _i, _i, _i, _pvp]),
     "ilug_factors_from_csr": (_i, [_ll, _pll, _pll, _pd, _pll, _pll, _pd, _i, _i, _i, _pvp]),
     "ilug_factors_rows": (_ll, [_vp]), "ilug_factors_nnz": (_i, [_vp, _pll, _pll]),
@@ -338,8 +339,22 @@ def ilu_factorize(A: Matrix, cfg: Config):
     return Matrix(L.value), Matrix(U.value)
 
 
+def matmul_device(A: Matrix, B: Matrix) -> Matrix:
+    """C = A B on the device (bitwise the host/reference SpGEMM)."""
+    out = C.c_void_p()
+    _check(lib.ilug_matmul_device(A.h, B.h, C.byref(out)))
+    return Matrix(out.value)
+
+
+def galerkin_device(A: Matrix, P: Matrix, R: Matrix) -> Matrix:
+    """R (A P) on the device (the AMG coarse operator)."""
+    out = C.c_void_p()
+    _check(lib.ilug_galerkin_device(A.h, P.h, R.h, C.byref(out)))
+    return Matrix(out.value)
+
+
 def ilu_factorize_device(A: Matrix, cfg: Config):
-    """The device objects' factorisation: ILU(0) on the GPU, ILUT on the host."""
+    """The device objects' factorisation: ILU(0) and ILUT on the GPU."""
     L, U = C.c_void_p(), C.c_void_p()
     _check(lib.ilug_ilu_factorize_device(A.h, cfg.h, C.byref(L), C.byref(U)))
     return Matrix(L.value), Matrix(U.value)

@@ -2,6 +2,7 @@
 // src/capi.cpp's handle/status/last-error conventions) and ilug_* (device
 // handles for the individual hot-path subsystems). No exception crosses it.
 #include "capi_handles.hpp"
+#include "../kernels/spgemm.hpp"
 #include "../host/problems.hpp"
 
 #include <cmath>
@@ -601,6 +602,21 @@ int ilug_ilu_factorize_device(const iluamg_matrix* A, const iluamg_config* cfg, 
         ilug::HostFactors f = ilug::factorize(A->A, ilug::ilu_params_from(cfg->cfg), nullptr);
         *L = new iluamg_matrix_s{std::move(f.L), "L"};
         *U = new iluamg_matrix_s{std::move(f.U), "U"};
+        return ILUAMG_OK;
+    });
+}
+int ilug_matmul_device(const iluamg_matrix* A, const iluamg_matrix* B, iluamg_matrix** C) {
+    return guarded([&] {
+        need(A && B && C);
+        *C = new iluamg_matrix_s{ilug::spgemm_device_host(A->A, B->A, nullptr), "C"};
+        return ILUAMG_OK;
+    });
+}
+int ilug_galerkin_device(const iluamg_matrix* A, const iluamg_matrix* P, const iluamg_matrix* R,
+                         iluamg_matrix** C) {
+    return guarded([&] {
+        need(A && P && R && C);
+        *C = new iluamg_matrix_s{ilug::galerkin_device(A->A, P->A, R->A, nullptr), "RAP"};
         return ILUAMG_OK;
     });
 }

@@ -1,5 +1,6 @@
 #include "driver.hpp"
 #include "../host/problems.hpp"
+#include "../kernels/spgemm.hpp"
 
 #include <chrono>
 #include <future>
@@ -118,8 +119,21 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
         builder.join();
         cudaStreamDestroy(bst);
     };
+    // Galerkin products on the GPU (own stream), bitwise the host SpGEMM
+    AmgParams apd = ap;
+    cudaStream_t gst = nullptr;
+    if (galerkin_on_device()) {
+        ILUG_CUDA(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
+        apd.galerkin = [gst](const Csr& Ak, const Csr& P, const Csr& R) { return galerkin_device(Ak, P, R, gst); };
+    }
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() {
+            if (s) cudaStreamDestroy(s);
+        }
+    } gguard{gst};
     try {
-        oc.hier = amg_setup(A, ap, [&](i64 k, const HostLevel& lev, bool last) {
+        oc.hier = amg_setup(A, apd, [&](i64 k, const HostLevel& lev, bool last) {
             {
                 std::lock_guard<std::mutex> g(qm);
                 queue.push_back({k, &lev, last});

@@ -423,10 +423,15 @@ HostHierarchy amg_setup(const Csr& A, const AmgParams& prm, const LevelReady& on
         tm.mark("interp", k);
         Csr R = csr_transpose(P);
         tm.mark("transpose", k);
-        Csr AP = csr_matmul(lev.A, P);
-        tm.mark("A*P", k);
-        cur = csr_matmul(R, AP);
-        tm.mark("R*(AP)", k);
+        if (prm.galerkin) {
+            cur = prm.galerkin(lev.A, P, R);
+            tm.mark("R*(A*P) device", k);
+        } else {
+            Csr AP = csr_matmul(lev.A, P);
+            tm.mark("A*P", k);
+            cur = csr_matmul(R, AP);
+            tm.mark("R*(AP)", k);
+        }
         lev.P = std::move(P);
         lev.R = std::move(R);
         lev.split = std::move(sp);

@@ -55,6 +55,9 @@ struct AmgParams {
     i64 cycles_nu = 1;
     std::uint64_t pmis_seed = 1;
     SmootherPlan plan;
+    /// Galerkin product R (A P) override (the device SpGEMM when the setup runs
+    /// next to a GPU, kernels/spgemm.cu); empty: host csr_matmul. Same bits.
+    std::function<Csr(const Csr& A, const Csr& P, const Csr& R)> galerkin;
 };
 
 struct CfSplit {
