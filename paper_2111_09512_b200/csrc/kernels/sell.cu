@@ -183,6 +183,43 @@ struct EpiNegScaleAcc { // poly_gs: term = -invd * t; acc += term
     }
 };
 
+// Small operators (coarse AMG levels): a warp per row. A thread-per-row
+// kernel on a level of a few thousand rows of 30-40 entries is pure latency —
+// ~10 dependent batches per row, 23-33 us per launch whatever the size (ncu,
+// C2 V-cycle: 135 such launches, 2.8 ms of 22.5 ms). Here lane t loads entry t
+// and its x, forms the product a_t * x_t (the serial loop's rounded product),
+// and the in-order sum s = 0 + p_0 + p_1 + ... runs as a shuffle chain, so the
+// result is bitwise the thread-per-row kernel's. Lane 0 applies the epilogue.
+template <class Epi>
+__global__ void __launch_bounds__(kBlock) k_rowdot_warp(SellView M, i64 nrows, const double* __restrict__ x,
+                                                         Epi epi) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const i64 w0 = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+    const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+    for (i64 p = w0; p < M.nrows_pad; p += nw) {
+        const i64 row = M.perm ? M.perm[p] : p;
+        if (row < 0 || row >= nrows) continue;
+        const int len = M.rowlen[p];
+        const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+        decltype(epi.pre(row)) pr{};
+        if (lane == 0) pr = epi.pre(row);
+        double s = 0.0;
+        for (int t0 = 0; t0 < len; t0 += 32) {
+            const int t = t0 + lane;
+            double prod = 0.0;
+            if (t < len) {
+                const i64 q = base + static_cast<i64>(t) * kSlice;
+                prod = ld_stream(M.vals + q) * ld_gather(x + ld_stream(M.cols + q));
+            }
+            const int cnt = min(32, len - t0);
+            for (int u = 0; u < cnt; ++u) s = s + __shfl_sync(full, prod, u);
+        }
+        if (lane == 0) epi(row, s, pr);
+    }
+}
+constexpr i64 kWarpRowMax = 65536; // operators up to this many rows take k_rowdot_warp
+
 // Wider variant: eight entries per batch with predicated loads, so a row of up
 // to eight entries (the L factor's 7.5 on average at C2) costs one streamed
 // round trip plus one gather round trip.
@@ -345,6 +382,10 @@ int rowdot_block(const Sell& M) {
     }
     return M.nnz < 10 * M.nrows ? 128 : 256;
 }
+bool warp_rows_enabled() { // ILUG_WARP_ROWS=0: small operators keep the thread-per-row kernel (A/B)
+    const char* e = std::getenv("ILUG_WARP_ROWS");
+    return !(e && e[0] == '0');
+}
 int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy)
     const char* e = std::getenv("ILUG_ROWDOT");
     return e && e[0] == '8' ? 8 : 4;
@@ -353,6 +394,14 @@ int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy
 template <class Epi>
 void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
     if (M.nrows_pad == 0) return;
+    if (M.nrows_pad <= kWarpRowMax && warp_rows_enabled()) {
+        const i64 warps = M.nrows_pad;
+        const unsigned g = static_cast<unsigned>(std::min<i64>((warps * 32 + kBlock - 1) / kBlock,
+                                                               static_cast<i64>(device_sm_count()) * 8));
+        k_rowdot_warp<Epi><<<g, kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+        ILUG_LAUNCH_CHECK();
+        return;
+    }
     if (rowdot_width() == 8)
         k_rowdot8<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else if (l2_hints())
