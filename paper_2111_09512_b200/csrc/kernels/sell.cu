@@ -371,16 +371,16 @@ bool serial_tail() { // ILUG_TAIL=serial: the row tail one entry at a time (A/B)
     const char* e = std::getenv("ILUG_TAIL");
     return e && e[0] == 's';
 }
-// Threads per CTA of the sweep kernel: 128 for short rows (< 10 entries on
-// average, e.g. the strict L of ILUT at C2: warps of a CTA finish at different
-// times and a smaller CTA frees its slot sooner; L sweep 370 -> 358 us), 256
-// otherwise. ILUG_ROWDOT_BLOCK=64|128|256 forces one (A/B).
-int rowdot_block(const Sell& M) {
+// Threads per CTA of the sweep kernel: 256. ILUG_ROWDOT_BLOCK=64|128 (A/B):
+// 128-thread CTAs for the short-row L factor looked 3 % faster in one run but
+// lost in an interleaved same-process A/B (L sweep 355-387 us at 256 vs
+// 372-472 us at 128, tools/probe_sweep.py).
+int rowdot_block(const Sell&) {
     if (const char* e = std::getenv("ILUG_ROWDOT_BLOCK")) {
         const int v = std::atoi(e);
         return v == 64 || v == 128 ? v : 256;
     }
-    return M.nnz < 10 * M.nrows ? 128 : 256;
+    return 256;
 }
 bool warp_rows_enabled() { // ILUG_WARP_ROWS=0: small operators keep the thread-per-row kernel (A/B)
     const char* e = std::getenv("ILUG_WARP_ROWS");

@@ -33,7 +33,7 @@ b = torch.rand(n, dtype=torch.float64, device="cuda")
 xin = torch.rand(n, dtype=torch.float64, device="cuda")
 out = torch.empty_like(b)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for sigma in ("1024",):
+for sigma in os.environ.get("PROBE_SIGMAS", "1024").split(","):
     os.environ["ILUG_SELL_SIGMA"] = sigma
     F = ilug.Factors.from_csr(n, Lc, Uc, scaling="row")
     st = F.stats()
