@@ -77,6 +77,12 @@ ILUAMG_API int ilug_factors_from_csr(long long n, const long long* L_rows, const
                                      const double* L_vals, const long long* U_rows,
                                      const long long* U_cols, const double* U_vals, int scaling,
                                      int upper_iteration, int direct_plans, ilug_factors** out);
+/* Numeric refactorisation of ILU(0) factors (created by ilug_factors_create with
+ * ilu.variant=ilu0) for a matrix with the same pattern (the time-stepping case,
+ * P:636-648): the symbolic data stay on the device, only values are uploaded;
+ * the result is bitwise the factors a fresh ilug_factors_create would build.
+ * Status 2 if the pattern differs or the factors are not ILU(0). */
+ILUAMG_API int ilug_factors_refactor(ilug_factors* f, const iluamg_matrix* A);
 ILUAMG_API long long ilug_factors_rows(const ilug_factors* f);
 /* nnz of L (strict) and of U (with diagonal). */
 ILUAMG_API int ilug_factors_nnz(const ilug_factors* f, long long* nnz_L, long long* nnz_U);

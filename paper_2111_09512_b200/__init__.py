@@ -65,7 +65,7 @@ _SIGS = {
     "ilug_matmul_device": (_i, [_vp, _vp, _pvp]), "ilug_galerkin_device": (_i, [_vp, _vp, _vp, _pvp]),
     "ilug_factors_create": (_i, [_vp, _vp, _i, _i, _i, _pvp]),
     "ilug_factors_from_csr": (_i, [_ll, _pll, _pll, _pd, _pll, _pll, _pd, _i, _i, _i, _pvp]),
-    "ilug_factors_rows": (_ll, [_vp]), "ilug_factors_nnz": (_i, [_vp, _pll, _pll]),
+    "ilug_factors_rows": (_ll, [_vp]), "ilug_factors_refactor": (_i, [_vp, _vp]), "ilug_factors_nnz": (_i, [_vp, _pll, _pll]),
     "ilug_factors_download_upper": (_i, [_vp, _pll, _pll, _pd, _pd, _pd, _pi]),
     "ilug_sweep_lower": (_i, [_vp, _vp, _vp, _ll, _vp]), "ilug_sweep_upper": (_i, [_vp, _vp, _vp, _ll, _vp]),
     "ilug_sweep_upper_host": (_i, [_vp, _pd, _pd, _ll]),
@@ -390,6 +390,10 @@ class Factors:
     @property
     def rows(self) -> int:
         return lib.ilug_factors_rows(self.h)
+
+    def refactor(self, A: Matrix):
+        """New values, same pattern (ILU(0) factors): ilug_factors_refactor."""
+        _check(lib.ilug_factors_refactor(self.h, A.h))
 
     def stats(self):
         n, nl, nu, pad = C.c_longlong(), C.c_longlong(), C.c_longlong(), C.c_longlong()

@@ -267,8 +267,28 @@ int ilug_factors_create(const iluamg_matrix* A, const iluamg_config* cfg, int sc
                         int direct, ilug_factors** out) {
     return guarded([&] {
         need(A && cfg && out);
-        return make_factors(ilug::factorize(A->A, ilug::ilu_params_from(cfg->cfg), nullptr), scaling, upper,
-                            direct, out);
+        const ilug::IluParams ip = ilug::ilu_params_from(cfg->cfg);
+        const int st = make_factors(ilug::factorize(A->A, ip, nullptr), scaling, upper, direct, out);
+        if (ip.variant == ilug::IluVariant::ilu0) {
+            (*out)->ilu0 = true;
+            (*out)->patch = ip.pivot_patch;
+            (*out)->a_rp = A->A.rp;
+            (*out)->a_hash = ilug::csr_pattern_hash(A->A);
+        }
+        return st;
+    });
+}
+int ilug_factors_refactor(ilug_factors* f, const iluamg_matrix* A) {
+    return guarded([&] {
+        need(f && A);
+        if (!f->ilu0) ilug::fail_invalid("refactor: only ILU(0) factors (fixed pattern) can be refactorised");
+        if (!f->sym) { // later calls are checked against the symbolic data (the same pattern)
+            if (A->A.rp != f->a_rp || ilug::csr_pattern_hash(A->A) != f->a_hash)
+                ilug::fail_invalid("refactor: the matrix pattern differs from the factorised one");
+            f->sym = ilug::Ilu0Symbolic::analyse(A->A, nullptr);
+        }
+        f->f.refactor(f->sym->factor(A->A, f->patch, nullptr), nullptr);
+        return ILUAMG_OK;
     });
 }
 int ilug_factors_from_csr(long long n, const long long* Lr, const long long* Lc, const double* Lv,

@@ -28,6 +28,13 @@ struct iluamg_report_s {
 struct ilug_factors_s {
     ilug::DeviceIlu f;
     long long nnz_L = 0, nnz_U = 0;
+    // ILU(0) handles: the factorised pattern (row starts + column hash) and the
+    // device symbolic data, built on the first refactorisation
+    bool ilu0 = false;
+    ilug::PivotPatch patch = ilug::PivotPatch::error;
+    ilug::RawVec<ilug::i64> a_rp;
+    std::uint64_t a_hash = 0;
+    std::unique_ptr<ilug::Ilu0Symbolic> sym;
 };
 struct ilug_dmatrix_s {
     ilug::DeviceMatrix M;

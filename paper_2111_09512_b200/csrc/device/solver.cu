@@ -100,6 +100,38 @@ void DeviceIlu::finish(DevFactors& df, const HostFactors* host, ScalingKind scal
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
+void DeviceIlu::refactor(DevFactors&& dfin, cudaStream_t st) {
+    DevFactors df = std::move(dfin);
+    if (df.n != n_) fail_invalid("ilu refactor: dimension mismatch");
+    if (wave_L_.ready() || wave_U_.ready())
+        fail_invalid("ilu refactor: the wavefront plans (ILUG_WAVEFRONT) are not refilled");
+    sell_refill(Ls_, df.Lrp.p, df.Lci.p, df.Lv.p, Part::all, st);
+    const i64* rp = df.Urp.p;
+    const i32* ci = df.Uci.p;
+    double* v = df.Uv.p;
+    const bool direct_plans = lower_plan_.levels() > 0;
+    const bool scale = upper_ == UpperIteration::scaled && scaling_ != ScalingKind::none;
+    if (!scale) {
+        const i64 bad = extract_diag(n_, rp, ci, v, d_.p, st);
+        if (bad >= 0 && (upper_ == UpperIteration::jacobi || direct_plans))
+            fail_numeric("ilu factors: zero diagonal entry in U at row " + std::to_string(bad));
+    } else {
+        DBuf<double> dr, dc;
+        if (scaling_ == ScalingKind::row_col) dr.alloc(n_), dc.alloc(n_);
+        const i64 bad = scale_upper(n_, rp, ci, v, scaling_ == ScalingKind::row ? 1 : 2, rs_.p, cs_.p, dr.p, dc.p, st);
+        if (bad >= 0)
+            fail_numeric(std::string(scaling_ == ScalingKind::row ? "row_scale" : "row_col_scale") +
+                         ": zero diagonal entry in U at row " + std::to_string(bad));
+    }
+    sell_refill(Us_, rp, ci, v, Part::strict_upper, st);
+    if (direct_plans) {
+        lower_plan_.refill(df.Lrp.p, df.Lci.p, df.Lv.p, st);
+        upper_plan_.refill(rp, ci, v, st);
+    }
+    if (cs_lower_ || cs_upper_) fail_invalid("ilu refactor: the cuSPARSE comparison path is not refilled");
+    ILUG_CUDA(cudaStreamSynchronize(st));
+}
+
 bool DeviceIlu::use_wave(bool upper, i64 m) const {
     return m >= 3 && m <= kWaveMaxSweeps + 1 && (upper ? wave_U_ : wave_L_).ready();
 }

@@ -57,6 +57,10 @@ public:
     /// packed, then the CSR copies are freed). No host round trip of the
     /// factors unless a wavefront or level-set plan needs the patterns.
     void build(DevFactors&& f, ScalingKind scaling, UpperIteration upper, bool direct_plans, cudaStream_t st);
+    /// Numeric refactorisation: new factors with the pattern these were built
+    /// from (Ilu0Symbolic::factor) — K1 scaling and every SELL copy (sweeps,
+    /// level plans) refilled in place, no layout work, no host round trip.
+    void refactor(DevFactors&& f, cudaStream_t st);
 
     i64 n() const { return n_; }
     ScalingKind scaling() const { return scaling_; }

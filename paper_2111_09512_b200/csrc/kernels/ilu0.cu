@@ -91,6 +91,46 @@ __global__ void k_ilu0_split(i64 n, const i64* __restrict__ rp, const i32* __res
 
 } // namespace
 
+namespace {
+
+// The elimination proper, into wd (a copy of the values a). |A|_F (a serial
+// sum over every value, as the reference computes it) only matters for a
+// patched zero pivot, so it is computed only if one occurs: the first launch
+// detects zero pivots; under pivot_patch=replace a second launch then runs
+// with the norm. Without zero pivots both policies give the same factors.
+void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const double* a, double* wd, i64 nnz,
+                    PivotPatch patch, const Csr& A, cudaStream_t st) {
+    DBuf<unsigned> sync(n + 3); // done flags, epoch, ticket, error
+    ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
+    DBuf<unsigned long long> fz(1);
+    unsigned* epoch = sync.p + n;
+    double anorm_f = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const unsigned long long init = ~0ull;
+        ILUG_CUDA(cudaMemcpyAsync(fz.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        ILUG_CUDA(cudaMemcpyAsync(wd, a, static_cast<size_t>(nnz) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        k_ilu0_bump<<<1, 1, 0, st>>>(epoch, epoch + 1);
+        ILUG_LAUNCH_CHECK();
+        const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
+        k_ilu0<<<g, kBlock, 0, st>>>(n, rp, ci, dpos, a, wd, sync.p, epoch, epoch + 1, fz.p, epoch + 2, pass,
+                                     anorm_f);
+        ILUG_LAUNCH_CHECK();
+        unsigned long long h = 0;
+        unsigned bad = 0;
+        ILUG_CUDA(cudaMemcpyAsync(&h, fz.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        ILUG_CUDA(cudaMemcpyAsync(&bad, epoch + 2, sizeof bad, cudaMemcpyDeviceToHost, st));
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        if (bad) fail_numeric("ilu0 (device): dependency wait timed out (scheduling error)");
+        if (h == ~0ull || pass == 1) return;
+        if (patch == PivotPatch::error)
+            fail_numeric("zero pivot at step " + std::to_string(h) +
+                         " (no pivoting; rerun with pivot_patch=replace to substitute)");
+        anorm_f = frobenius_norm(A);
+    }
+}
+
+} // namespace
+
 bool ilu0_on_device() {
     const char* e = std::getenv("ILUG_ILU0_DEVICE");
     return !(e && e[0] == '0');
@@ -144,7 +184,6 @@ DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool k
         if (dpos[i] < 0)
             fail_invalid("ilu0: diagonal entry (" + std::to_string(i) + "," + std::to_string(i) +
                          ") is structurally absent");
-    const double anorm_f = frobenius_norm(A);
     const i64 nnz = A.nnz();
     DevFactors f;
     f.n = n;
@@ -169,39 +208,110 @@ DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool k
     dp.upload(dpos.data(), n, st);
     a.upload(A.v.data(), nnz, st);
     wd.alloc(nnz);
-    ILUG_CUDA(cudaMemcpyAsync(wd.p, a.p, static_cast<size_t>(nnz) * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    DBuf<unsigned> sync(n + 3); // done flags, epoch, ticket, error
-    ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
-    DBuf<unsigned long long> fz(1);
-    const unsigned long long init = ~0ull;
-    ILUG_CUDA(cudaMemcpyAsync(fz.p, &init, sizeof init, cudaMemcpyHostToDevice, st));
-    unsigned* epoch = sync.p + n;
-    k_ilu0_bump<<<1, 1, 0, st>>>(epoch, epoch + 1);
-    ILUG_LAUNCH_CHECK();
-    const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
-    k_ilu0<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dp.p, a.p, wd.p, sync.p, epoch, epoch + 1, fz.p, epoch + 2,
-                                 patch == PivotPatch::error ? 0 : 1, anorm_f);
-    ILUG_LAUNCH_CHECK();
-    unsigned long long h = 0;
-    unsigned bad = 0;
-    ILUG_CUDA(cudaMemcpyAsync(&h, fz.p, sizeof h, cudaMemcpyDeviceToHost, st));
-    ILUG_CUDA(cudaMemcpyAsync(&bad, epoch + 2, sizeof bad, cudaMemcpyDeviceToHost, st));
-    ILUG_CUDA(cudaStreamSynchronize(st));
-    if (bad) fail_numeric("ilu0 (device): dependency wait timed out (scheduling error)");
-    if (h != ~0ull)
-        fail_numeric("zero pivot at step " + std::to_string(h) +
-                     " (no pivoting; rerun with pivot_patch=replace to substitute)");
+    ilu0_eliminate(n, rp.p, ci.p, dp.p, a.p, wd.p, nnz, patch, A, st);
     f.Lrp.upload(f.Lrp_h.data(), n + 1, st);
     f.Urp.upload(f.Urp_h.data(), n + 1, st);
     f.Lci.alloc(f.Lrp_h[n]);
     f.Lv.alloc(f.Lrp_h[n]);
     f.Uci.alloc(f.Urp_h[n]);
     f.Uv.alloc(f.Urp_h[n]);
+    const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
     k_ilu0_split<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dp.p, wd.p, f.Lrp.p, f.Urp.p, f.Lci.p, f.Lv.p, f.Uci.p,
                                        f.Uv.p);
     ILUG_LAUNCH_CHECK();
     ILUG_CUDA(cudaStreamSynchronize(st)); // temporaries die at scope exit
     if (keep_A) f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(a);
+    return f;
+}
+
+// Thread-count-independent hash of a column array (blocks hashed in
+// parallel, combined in block order).
+std::uint64_t csr_pattern_hash(const Csr& A) {
+    const i64 nnz = A.nnz();
+    constexpr i64 kB = i64{1} << 20;
+    const i64 nb = (nnz + kB - 1) / kB;
+    std::vector<std::uint64_t> part(static_cast<size_t>(std::max<i64>(nb, 1)), 0);
+    parallel_ranges(nb, [&](i64 b, i64 e, int) {
+        for (i64 blk = b; blk < e; ++blk) {
+            std::uint64_t h = 1469598103934665603ull;
+            for (i64 k = blk * kB; k < std::min(nnz, (blk + 1) * kB); ++k)
+                h = (h ^ static_cast<std::uint32_t>(A.ci[k])) * 1099511628211ull;
+            part[static_cast<size_t>(blk)] = h;
+        }
+    }, 1);
+    std::uint64_t h = static_cast<std::uint64_t>(nnz);
+    for (std::uint64_t x : part) h = (h ^ x) * 1099511628211ull + 0x9e3779b97f4a7c15ull;
+    return h;
+}
+
+std::unique_ptr<Ilu0Symbolic> Ilu0Symbolic::analyse(const Csr& A, cudaStream_t st) {
+    if (A.nrows != A.ncols) fail_invalid("ilu0: matrix must be square");
+    auto s = std::make_unique<Ilu0Symbolic>();
+    const i64 n = s->n = A.nrows;
+    s->nnz = A.nnz();
+    std::vector<i64> dpos(static_cast<size_t>(n), -1);
+    parallel_ranges(n, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i)
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k)
+                if (A.ci[k] == i) dpos[i] = k;
+    });
+    for (i64 i = 0; i < n; ++i)
+        if (dpos[i] < 0)
+            fail_invalid("ilu0: diagonal entry (" + std::to_string(i) + "," + std::to_string(i) +
+                         ") is structurally absent");
+    s->rp_h = A.rp;
+    s->Lrp_h.assign(static_cast<size_t>(n) + 1, 0);
+    s->Urp_h.assign(static_cast<size_t>(n) + 1, 0);
+    for (i64 i = 0; i < n; ++i) {
+        s->Lrp_h[i + 1] = s->Lrp_h[i] + (dpos[i] - A.rp[i]);
+        s->Urp_h[i + 1] = s->Urp_h[i] + (A.rp[i + 1] - dpos[i]);
+    }
+    s->ci_hash = csr_pattern_hash(A);
+    s->rp.upload(A.rp.data(), n + 1, st);
+    s->ci.upload(A.ci.data(), s->nnz, st);
+    s->dpos.upload(dpos.data(), n, st);
+    s->Lrp.upload(s->Lrp_h.data(), n + 1, st);
+    s->Urp.upload(s->Urp_h.data(), n + 1, st);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    return s;
+}
+
+DevFactors Ilu0Symbolic::factor(const Csr& A, PivotPatch patch, cudaStream_t st) const {
+    SetupTimer tm("ilu0-refactor");
+    if (A.nrows != n || A.nnz() != nnz || A.rp != rp_h || csr_pattern_hash(A) != ci_hash)
+        fail_invalid("ilu0 refactor: the matrix pattern differs from the analysed one");
+    tm.mark("pattern check");
+    DevFactors f;
+    f.n = n;
+    f.diag_first = true;
+    f.Lrp_h = Lrp_h;
+    f.Urp_h = Urp_h;
+    if (n == 0) {
+        f.Lrp.upload(Lrp_h.data(), 1, st);
+        f.Urp.upload(Urp_h.data(), 1, st);
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        return f;
+    }
+    DBuf<double> a, wd;
+    a.upload(A.v.data(), nnz, st);
+    wd.alloc(nnz);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    tm.mark("upload values");
+    ilu0_eliminate(n, rp.p, ci.p, dpos.p, a.p, wd.p, nnz, patch, A, st);
+    tm.mark("factor kernel");
+    f.Lrp.alloc(n + 1);
+    f.Urp.alloc(n + 1);
+    ILUG_CUDA(cudaMemcpyAsync(f.Lrp.p, Lrp.p, static_cast<size_t>(n + 1) * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+    ILUG_CUDA(cudaMemcpyAsync(f.Urp.p, Urp.p, static_cast<size_t>(n + 1) * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+    f.Lci.alloc(Lrp_h[n]);
+    f.Lv.alloc(Lrp_h[n]);
+    f.Uci.alloc(Urp_h[n]);
+    f.Uv.alloc(Urp_h[n]);
+    const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
+    k_ilu0_split<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dpos.p, wd.p, f.Lrp.p, f.Urp.p, f.Lci.p, f.Lv.p, f.Uci.p,
+                                       f.Uv.p);
+    ILUG_LAUNCH_CHECK();
+    ILUG_CUDA(cudaStreamSynchronize(st));
     return f;
 }
 

@@ -4,6 +4,9 @@
 #include "../host/ilu.hpp"
 #include "ops.hpp"
 
+#include <cstdint>
+#include <memory>
+
 namespace ilug {
 
 /// Incomplete factors resident on the device, CSR: L strict (unit diagonal
@@ -35,6 +38,26 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
 /// factorize() that leaves the factors on the device (host factorisations,
 /// when forced with ILUG_ILU0_DEVICE=0 / ILUG_ILUT_DEVICE=0, are uploaded).
 DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false);
+
+/// Hash of a CSR's column pattern (pattern checks for refactorisation).
+std::uint64_t csr_pattern_hash(const Csr& A);
+
+/// Symbolic part of ILU(0) kept on the device for numeric refactorisations
+/// of matrices with the same pattern (the time-stepping case of the paper's
+/// finest level): row starts, columns, diagonal positions, the L/U
+/// split pattern. factor() uploads only the new values, eliminates, and
+/// splits; the result is bitwise the fresh ilu0_resident of the new matrix.
+struct Ilu0Symbolic {
+    i64 n = 0, nnz = 0;
+    DBuf<i64> rp, dpos, Lrp, Urp;
+    DBuf<i32> ci;
+    RawVec<i64> rp_h, Lrp_h, Urp_h;
+    std::uint64_t ci_hash = 0;
+
+    static std::unique_ptr<Ilu0Symbolic> analyse(const Csr& A, cudaStream_t st);
+    /// Same errors as ilu0 (zero pivot); invalid if A's pattern differs.
+    DevFactors factor(const Csr& A, PivotPatch patch, cudaStream_t st) const;
+};
 
 /// ILU(0) of A on the device, bitwise equal to host ilu0 (and the reference):
 /// same zero-pivot policy and error messages. Returns host factors (the device

@@ -390,7 +390,7 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
         return f;
     }
     SetupTimer tm("ilut-device");
-    const double anorm_f = frobenius_norm(A);
+    double anorm_f = 0.0; // |A|_F: computed only if a zero pivot is patched (see ilu0_eliminate)
     const i64 nnz = A.nnz();
     DBuf<i64> rp, uoff(n + 1), loff(n + 1);
     DBuf<i32> ci;
@@ -413,36 +413,42 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
     DBuf<unsigned> sync(n + 3); // done flags, epoch, err[2]
     DBuf<unsigned long long> ctl(2); // ticket, first zero
     ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
-    IlutArgs a{n,       rp.p,   ci.p,   av.p,   tau.p,   p.lfill, anorm_f, p.pivot_patch == PivotPatch::error ? 0 : 1,
+    IlutArgs a{n,       rp.p,   ci.p,   av.p,   tau.p,   p.lfill, anorm_f, 0,
                p.droptol, uoff.p, loff.p, uci.p, uv.p, ulen.p, lci.p, lv.p, llen.p, sync.p, sync.p + n,
                ctl.p,   ctl.p + 1, sync.p + n + 1};
     unsigned err[2] = {0, 0};
-    for (int cap_level = 0;; ++cap_level) {
-        const unsigned long long init[2] = {0ull, ~0ull};
-        ILUG_CUDA(cudaMemcpyAsync(ctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
-        k_ilut_bump<<<1, 1, 0, st>>>(sync.p + n, ctl.p, sync.p + n + 1);
-        ILUG_LAUNCH_CHECK();
-        if (cap_level == 0)
-            launch_ilut<256, 8>(a, st);
-        else if (cap_level == 1)
-            launch_ilut<1024, 4>(a, st);
-        else
-            launch_ilut<6144, 2>(a, st);
-        ILUG_CUDA(cudaMemcpyAsync(err, sync.p + n + 1, sizeof err, cudaMemcpyDeviceToHost, st));
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int cap_level = 0;; ++cap_level) {
+            const unsigned long long init[2] = {0ull, ~0ull};
+            ILUG_CUDA(cudaMemcpyAsync(ctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+            k_ilut_bump<<<1, 1, 0, st>>>(sync.p + n, ctl.p, sync.p + n + 1);
+            ILUG_LAUNCH_CHECK();
+            if (cap_level == 0)
+                launch_ilut<256, 8>(a, st);
+            else if (cap_level == 1)
+                launch_ilut<1024, 4>(a, st);
+            else
+                launch_ilut<6144, 2>(a, st);
+            ILUG_CUDA(cudaMemcpyAsync(err, sync.p + n + 1, sizeof err, cudaMemcpyDeviceToHost, st));
+            ILUG_CUDA(cudaStreamSynchronize(st));
+            if (err[0]) fail_numeric("ilut (device): dependency wait timed out (scheduling error)");
+            if (err[1] == 0) break;
+            if (cap_level == 2 || err[1] > 6144)
+                fail_invalid("ilut (device): a working row needs " + std::to_string(err[1]) +
+                             " entries (> 6144); set ILUG_ILUT_DEVICE=0 to factor on the host");
+        }
+        tm.mark("factor kernel");
+        unsigned long long fz = 0;
+        ILUG_CUDA(cudaMemcpyAsync(&fz, ctl.p + 1, sizeof fz, cudaMemcpyDeviceToHost, st));
         ILUG_CUDA(cudaStreamSynchronize(st));
-        if (err[0]) fail_numeric("ilut (device): dependency wait timed out (scheduling error)");
-        if (err[1] == 0) break;
-        if (cap_level == 2 || err[1] > 6144)
-            fail_invalid("ilut (device): a working row needs " + std::to_string(err[1]) +
-                         " entries (> 6144); set ILUG_ILUT_DEVICE=0 to factor on the host");
+        if (fz == ~0ull || pass == 1) break;
+        if (p.pivot_patch == PivotPatch::error)
+            fail_numeric("zero pivot at step " + std::to_string(fz) +
+                         " (no pivoting; rerun with pivot_patch=replace to substitute)");
+        anorm_f = frobenius_norm(A); // patched pivots: rerun with the reference's |A|_F
+        a.anorm_f = anorm_f;
+        a.patch = 1;
     }
-    tm.mark("factor kernel");
-    unsigned long long fz = 0;
-    ILUG_CUDA(cudaMemcpyAsync(&fz, ctl.p + 1, sizeof fz, cudaMemcpyDeviceToHost, st));
-    ILUG_CUDA(cudaStreamSynchronize(st));
-    if (fz != ~0ull)
-        fail_numeric("zero pivot at step " + std::to_string(fz) +
-                     " (no pivoting; rerun with pivot_patch=replace to substitute)");
     // compact the slots into CSR (stays on the device; row starts to the host)
     if (keep_A) {
         f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(av);

@@ -686,6 +686,10 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
+void LevelPlan::refill(const i64* rp, const i32* ci, const double* v, cudaStream_t st) {
+    sell_refill(M_, rp, ci, v, Part::all, st);
+}
+
 void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream_t st) const {
     if (M_.nrows == 0) return;
     SellView mv = view(M_);

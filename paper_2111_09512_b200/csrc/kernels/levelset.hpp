@@ -16,6 +16,10 @@ public:
     /// (e.g. the K1-scaled U that only exists on the device).
     void build(const Csr& T, Kind kind, cudaStream_t st, const double* dev_vals = nullptr);
 
+    /// New values for the same pattern (device CSR of T): the level-ordered copy
+    /// is refilled in place (numeric refactorisation).
+    void refill(const i64* rp, const i32* ci, const double* v, cudaStream_t st);
+
     /// lower_unit / upper: x = T^-1 b. gauss_seidel: x = one forward GS sweep
     /// from xold (x and xold must differ).
     void solve(const double* b, double* x, const double* xold, cudaStream_t st) const;

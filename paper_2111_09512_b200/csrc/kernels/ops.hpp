@@ -30,6 +30,10 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
 void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& rp_host, i64 skip, const i64* rp,
                            const i32* ci, const double* v, Part part, cudaStream_t s);
 
+/// Rewrite the entries of an existing SELL from a device CSR with the pattern
+/// it was built from (numeric refactorisation: layout and permutation reused).
+void sell_refill(Sell& M, const i64* rp, const i32* ci, const double* v, Part part, cudaStream_t s);
+
 /// Unpack a SELL back to host CSR (tests / parity downloads).
 Csr sell_to_host(const Sell& M);
 

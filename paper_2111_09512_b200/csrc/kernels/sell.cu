@@ -612,6 +612,14 @@ void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& r
     }
 }
 
+void sell_refill(Sell& M, const i64* rp, const i32* ci, const double* v, Part part, cudaStream_t s) {
+    if (M.nrows_pad == 0 || M.padded == 0) return;
+    const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
+    k_sell_fill<<<grid_for(M.nrows_pad), kBlock, 0, s>>>(M.nrows_pad, M.nrows, M.perm.p, rp, ci, v, pc,
+                                                         M.slice_ptr.p, M.cols.p, M.vals.p);
+    ILUG_LAUNCH_CHECK();
+}
+
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     SetupTimer tm("sell-host");
     out.nrows = A.nrows;

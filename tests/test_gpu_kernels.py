@@ -326,3 +326,46 @@ def test_direct_cusparse_comparison_path(ilug, ref, torch_cuda, monkeypatch):
     monkeypatch.delenv("ILUG_DIRECT")
     want = ilug.run_solve(A, ilug.Config().update(kv))
     assert got["converged"] == "true" and abs(int(got["iterations"]) - int(want["iterations"])) <= 1
+
+
+@pytest.mark.parametrize("scaling,upper,direct", [("row", "scaled", True), ("row_col", "scaled", False),
+                                                  ("none", "jacobi", True)])
+def test_ilu0_refactor_bitwise(ilug, ref, torch_cuda, scaling, upper, direct):
+    """Numeric refactorisation with the same pattern (new coefficients, seed 7):
+    sweeps and direct solves bitwise those of factors built from scratch."""
+    A1 = ilug.Matrix.generate("pressure27(20,18,16,2111)")
+    A2 = ilug.Matrix.generate("pressure27(20,18,16,7)")
+    assert np.array_equal(A1.csr()[1], A2.csr()[1])
+    cfg = ilug.Config()
+    f = ilug.Factors.create(A1, cfg, scaling=scaling, upper=upper, direct=direct)
+    f.refactor(A2)
+    g = ilug.Factors.create(A2, cfg, scaling=scaling, upper=upper, direct=direct)
+    b = np.random.default_rng(51).uniform(-1, 1, A2.rows)
+    bd = _dev(torch_cuda, b)
+    y1, y2 = torch_cuda.empty_like(bd), torch_cuda.empty_like(bd)
+    for m in (1, 3, 6):
+        f.sweep_lower(bd, y1, m), g.sweep_lower(bd, y2, m)
+        assert bitwise(_host(y1), _host(y2))
+        f.sweep_upper(bd, y1, m), g.sweep_upper(bd, y2, m)
+        assert bitwise(_host(y1), _host(y2))
+    if direct:
+        f.solve_lower(bd, y1), g.solve_lower(bd, y2)
+        assert bitwise(_host(y1), _host(y2))
+        f.solve_upper(bd, y1), g.solve_upper(bd, y2)
+        assert bitwise(_host(y1), _host(y2))
+    f.refactor(A1)  # and back: the symbolic data are reused
+    h = ilug.Factors.create(A1, cfg, scaling=scaling, upper=upper, direct=direct)
+    f.sweep_upper(bd, y1, 4), h.sweep_upper(bd, y2, 4)
+    assert bitwise(_host(y1), _host(y2))
+
+
+def test_ilu0_refactor_rejects_other_patterns(ilug, torch_cuda):
+    f = ilug.Factors.create(ilug.Matrix.generate("pressure27(10,10,10)"), ilug.Config())
+    with pytest.raises(ilug.IlugError) as e:
+        f.refactor(ilug.Matrix.generate("poisson3d(10,10,10)"))
+    assert e.value.status == 2 and "pattern" in e.value.message
+    t = ilug.Factors.create(ilug.Matrix.generate("pressure27(10,10,10)"),
+                            ilug.Config().update({"ilu.variant": "ilut", "ilu.droptol": "1e-3", "ilu.lfill": "5"}))
+    with pytest.raises(ilug.IlugError) as e:
+        t.refactor(ilug.Matrix.generate("pressure27(10,10,10)"))
+    assert e.value.status == 2
