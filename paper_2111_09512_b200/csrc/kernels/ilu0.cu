@@ -32,13 +32,18 @@ __global__ void k_ilu0_bump(unsigned* epoch, unsigned* ticket) {
 __global__ void __launch_bounds__(kBlock)
 k_ilu0(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, const i64* __restrict__ dpos,
        const double* __restrict__ a, double* w, unsigned* done, const unsigned* __restrict__ epoch_p,
-       unsigned* ticket, unsigned long long* first_zero, unsigned* err, int patch, double anorm_f) {
+       unsigned* ticket, unsigned long long* first_zero, unsigned* err, int patch, double anorm_f,
+       const i32* __restrict__ order) {
     __shared__ unsigned s_blk;
     if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
     __syncthreads();
     const unsigned E = *epoch_p;
-    const i64 i = static_cast<i64>(s_blk) * kBlock + threadIdx.x;
-    if (i >= n) return;
+    const i64 t = static_cast<i64>(s_blk) * kBlock + threadIdx.x;
+    if (t >= n) return;
+    // rows in wavefront (level) order when given: a block then holds rows of one
+    // level (independent) instead of a chain of x-neighbours, and a row's
+    // dependencies are always in earlier blocks (no deadlock)
+    const i64 i = order ? order[t] : t;
     const i64 beg = rp[i], end = rp[i + 1], di = dpos[i];
     for (i64 k = beg; k < di; ++k) {
         const i64 c = ci[k];
@@ -99,7 +104,7 @@ namespace {
 // detects zero pivots; under pivot_patch=replace a second launch then runs
 // with the norm. Without zero pivots both policies give the same factors.
 void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const double* a, double* wd, i64 nnz,
-                    PivotPatch patch, const Csr& A, cudaStream_t st) {
+                    PivotPatch patch, const Csr& A, const i32* order, cudaStream_t st) {
     DBuf<unsigned> sync(n + 3); // done flags, epoch, ticket, error
     ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
     DBuf<unsigned long long> fz(1);
@@ -113,7 +118,7 @@ void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const 
         ILUG_LAUNCH_CHECK();
         const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
         k_ilu0<<<g, kBlock, 0, st>>>(n, rp, ci, dpos, a, wd, sync.p, epoch, epoch + 1, fz.p, epoch + 2, pass,
-                                     anorm_f);
+                                     anorm_f, order);
         ILUG_LAUNCH_CHECK();
         unsigned long long h = 0;
         unsigned bad = 0;
@@ -130,6 +135,26 @@ void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const 
 }
 
 } // namespace
+
+// Rows sorted by wavefront level of the lower-pattern DAG (level[i] = 1 +
+// max level of its lower neighbours), stable within a level.
+std::vector<i32> ilu0_level_order(const Csr& A, const std::vector<i64>& dpos) {
+    const i64 n = A.nrows;
+    std::vector<i32> level(static_cast<size_t>(n), 0);
+    i32 nlev = n > 0 ? 1 : 0;
+    for (i64 i = 0; i < n; ++i) {
+        i32 l = 0;
+        for (i64 k = A.rp[i]; k < dpos[i]; ++k) l = std::max(l, level[A.ci[k]] + 1);
+        level[i] = l;
+        nlev = std::max(nlev, l + 1);
+    }
+    std::vector<i64> start(static_cast<size_t>(nlev) + 1, 0);
+    for (i64 i = 0; i < n; ++i) ++start[level[i] + 1];
+    for (i32 l = 0; l < nlev; ++l) start[l + 1] += start[l];
+    std::vector<i32> order(static_cast<size_t>(n));
+    for (i64 i = 0; i < n; ++i) order[start[level[i]]++] = static_cast<i32>(i);
+    return order;
+}
 
 bool ilu0_on_device() {
     const char* e = std::getenv("ILUG_ILU0_DEVICE");
@@ -208,7 +233,12 @@ DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool k
     dp.upload(dpos.data(), n, st);
     a.upload(A.v.data(), nnz, st);
     wd.alloc(nnz);
-    ilu0_eliminate(n, rp.p, ci.p, dp.p, a.p, wd.p, nnz, patch, A, st);
+    DBuf<i32> ord;
+    {
+        const std::vector<i32> o = ilu0_level_order(A, dpos);
+        ord.upload(o.data(), n, st);
+    }
+    ilu0_eliminate(n, rp.p, ci.p, dp.p, a.p, wd.p, nnz, patch, A, ord.p, st);
     f.Lrp.upload(f.Lrp_h.data(), n + 1, st);
     f.Urp.upload(f.Urp_h.data(), n + 1, st);
     f.Lci.alloc(f.Lrp_h[n]);
@@ -267,6 +297,10 @@ std::unique_ptr<Ilu0Symbolic> Ilu0Symbolic::analyse(const Csr& A, cudaStream_t s
         s->Urp_h[i + 1] = s->Urp_h[i] + (A.rp[i + 1] - dpos[i]);
     }
     s->ci_hash = csr_pattern_hash(A);
+    {
+        const std::vector<i32> o = ilu0_level_order(A, dpos);
+        s->order.upload(o.data(), n, st);
+    }
     s->rp.upload(A.rp.data(), n + 1, st);
     s->ci.upload(A.ci.data(), s->nnz, st);
     s->dpos.upload(dpos.data(), n, st);
@@ -297,7 +331,7 @@ DevFactors Ilu0Symbolic::factor(const Csr& A, PivotPatch patch, cudaStream_t st)
     wd.alloc(nnz);
     ILUG_CUDA(cudaStreamSynchronize(st));
     tm.mark("upload values");
-    ilu0_eliminate(n, rp.p, ci.p, dpos.p, a.p, wd.p, nnz, patch, A, st);
+    ilu0_eliminate(n, rp.p, ci.p, dpos.p, a.p, wd.p, nnz, patch, A, order.p, st);
     tm.mark("factor kernel");
     f.Lrp.alloc(n + 1);
     f.Urp.alloc(n + 1);

@@ -50,7 +50,7 @@ std::uint64_t csr_pattern_hash(const Csr& A);
 struct Ilu0Symbolic {
     i64 n = 0, nnz = 0;
     DBuf<i64> rp, dpos, Lrp, Urp;
-    DBuf<i32> ci;
+    DBuf<i32> ci, order; // order: rows by wavefront level (the elimination's schedule)
     RawVec<i64> rp_h, Lrp_h, Urp_h;
     std::uint64_t ci_hash = 0;
 
