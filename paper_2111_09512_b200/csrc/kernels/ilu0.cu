@@ -4,9 +4,9 @@
 // One thread per row. Row i needs rows c < i of its lower pattern finished;
 // instead of level barriers every row waits on its dependencies' epoch-stamped
 // done flags, just before it uses each one (sync-free, like the K5 flag
-// schedule). CTAs take their row block from an atomic ticket, so a block only
-// ever waits on blocks that were scheduled before it: no deadlock whatever the
-// residency. Each row performs the serial algorithm's operations in its order
+// schedule). CTAs take their row block from an atomic ticket over the rows in
+// wavefront (level) order, so a block holds independent rows and only ever
+// waits on blocks scheduled before it: no deadlock whatever the residency. Each row performs the serial algorithm's operations in its order
 // (multipliers by ascending k, then the merge of row c's strict upper part in
 // ascending column order), with separate multiply/subtract (--fmad=false), so
 // the factors are bitwise the host ones. A bounded spin turns a scheduling bug
