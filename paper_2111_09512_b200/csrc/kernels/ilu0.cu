@@ -77,6 +77,85 @@ k_ilu0(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, const i64*
     fi.store(E, cuda::memory_order_release);
 }
 
+// Warp-per-row form (rows of at most 64 entries, the common case): the row's
+// values live in the lanes' registers (entries l and l+32 on lane l), and the
+// merge of row c's strict upper part is a broadcast of its (column, value)
+// pairs — one load round trip per dependency instead of the thread form's
+// serial scan. Each entry still receives its updates in ascending k with the
+// same multiply/subtract, so the factors are bitwise those of k_ilu0.
+constexpr int kWarpRowsPerCta = 8;
+
+__global__ void __launch_bounds__(kWarpRowsPerCta * 32)
+k_ilu0_warp(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, const i64* __restrict__ dpos,
+            const double* __restrict__ a, double* w, unsigned* done, const unsigned* __restrict__ epoch_p,
+            unsigned* ticket, unsigned long long* first_zero, unsigned* err, int patch, double anorm_f,
+            const i32* __restrict__ order) {
+    __shared__ unsigned s_blk;
+    if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned full = 0xffffffffu;
+    const unsigned E = *epoch_p;
+    const int lane = threadIdx.x & 31;
+    const i64 t = static_cast<i64>(s_blk) * kWarpRowsPerCta + (threadIdx.x >> 5);
+    if (t >= n) return;
+    const i64 i = order ? order[t] : t;
+    const i64 beg = rp[i], len = rp[i + 1] - beg, dq = dpos[i] - beg;
+    // row values in registers: slot 0 = entry lane, slot 1 = entry lane + 32
+    const bool h0 = lane < len, h1 = lane + 32 < len;
+    const i32 j0 = h0 ? ci[beg + lane] : -1, j1 = h1 ? ci[beg + lane + 32] : -1;
+    double v0 = h0 ? w[beg + lane] : 0.0, v1 = h1 ? w[beg + lane + 32] : 0.0;
+    for (i64 q = 0; q < dq; ++q) {
+        const int src = static_cast<int>(q & 31);
+        const i32 c = __shfl_sync(full, q < 32 ? j0 : j1, src);
+        if (!wait_flag<64>(done + c, E)) atomicExch(err, 1u);
+        const i64 dc = dpos[c], ce = rp[c + 1];
+        const double wk = __shfl_sync(full, q < 32 ? v0 : v1, src);
+        const double m = wk / w[dc];
+        if (lane == src) {
+            if (q < 32) v0 = m;
+            else v1 = m;
+        }
+        // row c's strict upper part, 32 entries at a time
+        for (i64 cb = dc + 1; cb < ce; cb += 32) {
+            const bool has = cb + lane < ce;
+            const i32 jc = has ? ci[cb + lane] : -1;
+            const double vc = has ? w[cb + lane] : 0.0;
+            const int cnt = ce - cb < 32 ? static_cast<int>(ce - cb) : 32;
+            for (int u = 0; u < cnt; ++u) {
+                const i32 ju = __shfl_sync(full, jc, u);
+                const double vu = __shfl_sync(full, vc, u);
+                if (h0 && j0 == ju) v0 = v0 - m * vu;
+                if (h1 && j1 == ju) v1 = v1 - m * vu;
+            }
+        }
+    }
+    // zero pivot (the lane holding the diagonal)
+    const int dl = static_cast<int>(dq & 31);
+    if (lane == dl) {
+        double& d = dq < 32 ? v0 : v1;
+        if (d == 0.0) {
+            if (patch == 0) {
+                atomicMin(first_zero, static_cast<unsigned long long>(i));
+                d = 1.0; // placeholder; the factorisation is abandoned
+            } else {
+                double s2 = 0.0;
+                for (i64 k = beg; k < beg + len; ++k) s2 = s2 + a[k] * a[k];
+                const double zr = 0.0 * sqrt(s2), fl = 1e-16 * anorm_f;
+                double mag = zr < fl ? fl : zr; // std::max(zr, fl)
+                if (mag == 0.0) mag = DBL_MIN;
+                d = mag;
+            }
+        }
+    }
+    if (h0) w[beg + lane] = v0;
+    if (h1) w[beg + lane + 32] = v1;
+    __syncwarp(); // every lane's row write before lane 0's release (cumulative)
+    if (lane == 0) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> fi(done[i]);
+        fi.store(E, cuda::memory_order_release);
+    }
+}
+
 // w (A's pattern) -> strict L and U (diagonal first) on the device, thread per row
 __global__ void k_ilu0_split(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci,
                              const i64* __restrict__ dpos, const double* __restrict__ w,
@@ -103,8 +182,15 @@ namespace {
 // patched zero pivot, so it is computed only if one occurs: the first launch
 // detects zero pivots; under pivot_patch=replace a second launch then runs
 // with the norm. Without zero pivots both policies give the same factors.
+bool ilu0_warp_enabled() { // ILUG_ILU0_WARP=0: the thread-per-row kernel (A/B)
+    const char* e = std::getenv("ILUG_ILU0_WARP");
+    return !(e && e[0] == '0');
+}
+
 void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const double* a, double* wd, i64 nnz,
                     PivotPatch patch, const Csr& A, const i32* order, cudaStream_t st) {
+    i64 max_row = 0;
+    for (i64 r = 0; r < A.nrows; ++r) max_row = std::max(max_row, A.rp[r + 1] - A.rp[r]);
     DBuf<unsigned> sync(n + 3); // done flags, epoch, ticket, error
     ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
     DBuf<unsigned long long> fz(1);
@@ -116,9 +202,15 @@ void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const 
         ILUG_CUDA(cudaMemcpyAsync(wd, a, static_cast<size_t>(nnz) * sizeof(double), cudaMemcpyDeviceToDevice, st));
         k_ilu0_bump<<<1, 1, 0, st>>>(epoch, epoch + 1);
         ILUG_LAUNCH_CHECK();
-        const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
-        k_ilu0<<<g, kBlock, 0, st>>>(n, rp, ci, dpos, a, wd, sync.p, epoch, epoch + 1, fz.p, epoch + 2, pass,
-                                     anorm_f, order);
+        if (max_row <= 64 && ilu0_warp_enabled()) {
+            const unsigned g = static_cast<unsigned>((n + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
+            k_ilu0_warp<<<g, kWarpRowsPerCta * 32, 0, st>>>(n, rp, ci, dpos, a, wd, sync.p, epoch, epoch + 1, fz.p,
+                                                            epoch + 2, pass, anorm_f, order);
+        } else {
+            const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
+            k_ilu0<<<g, kBlock, 0, st>>>(n, rp, ci, dpos, a, wd, sync.p, epoch, epoch + 1, fz.p, epoch + 2, pass,
+                                         anorm_f, order);
+        }
         ILUG_LAUNCH_CHECK();
         unsigned long long h = 0;
         unsigned bad = 0;
