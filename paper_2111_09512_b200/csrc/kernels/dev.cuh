@@ -33,6 +33,9 @@ constexpr int kSlice = 32; // SELL slice height = warp width: one row per lane
 /// buffers filled by the host worker pool (the driver's own pageable path
 /// stages single-threaded, ~5 GB/s). Returns once src is no longer needed.
 void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
+/// Device -> host counterpart (pageable destination): DMA into pinned chunks,
+/// copied out by the worker pool. Synchronous with respect to the host.
+void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
 constexpr size_t kStagedMin = size_t{32} << 20; // smaller copies take the plain path
 
 /// Owned device allocation (cudaMalloc / cudaFree), move-only.
@@ -73,9 +76,11 @@ struct DBuf {
             ILUG_CUDA(cudaMemcpyAsync(p, h, bytes, cudaMemcpyHostToDevice, s));
     }
     void download(T* h, cudaStream_t s = nullptr) const {
-        if (n > 0)
-            ILUG_CUDA(cudaMemcpyAsync(h, p, static_cast<size_t>(n) * sizeof(T),
-                                      cudaMemcpyDeviceToHost, s));
+        const size_t bytes = static_cast<size_t>(n) * sizeof(T);
+        if (bytes >= kStagedMin)
+            d2h_staged(h, p, bytes, s);
+        else if (n > 0)
+            ILUG_CUDA(cudaMemcpyAsync(h, p, bytes, cudaMemcpyDeviceToHost, s));
     }
     i64 bytes() const { return n * static_cast<i64>(sizeof(T)); }
 };

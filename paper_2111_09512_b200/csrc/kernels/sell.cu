@@ -456,6 +456,49 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     }
 }
 
+void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    constexpr size_t kChunk = size_t{64} << 20;
+    static std::mutex mu;
+    static void* buf[2] = {nullptr, nullptr};
+    static cudaEvent_t ev[2];
+    static bool ok = false, tried = false;
+    std::lock_guard<std::mutex> g(mu);
+    if (!tried) {
+        tried = true;
+        ok = cudaHostAlloc(&buf[0], kChunk, cudaHostAllocDefault) == cudaSuccess &&
+             cudaHostAlloc(&buf[1], kChunk, cudaHostAllocDefault) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) (void)cudaGetLastError();
+    }
+    if (!ok) {
+        ILUG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        ILUG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const char* in = static_cast<const char*>(src);
+    char* out = static_cast<char*>(dst);
+    const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+    // chunk c lands in buf[c & 1]; chunk c+1's DMA runs while chunk c is copied out
+    auto issue = [&](size_t c) {
+        const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+        ILUG_CUDA(cudaMemcpyAsync(buf[c & 1], in + off, len, cudaMemcpyDeviceToHost, s));
+        ILUG_CUDA(cudaEventRecord(ev[c & 1], s));
+    };
+    issue(0);
+    for (size_t c = 0; c < nchunk; ++c) {
+        if (c + 1 < nchunk) issue(c + 1);
+        ILUG_CUDA(cudaEventSynchronize(ev[c & 1]));
+        const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+        const char* b = static_cast<const char*>(buf[c & 1]);
+        constexpr i64 kPiece = i64{1} << 20;
+        parallel_ranges((static_cast<i64>(len) + kPiece - 1) / kPiece, [&](i64 lo, i64 hi, int) {
+            const size_t a = static_cast<size_t>(lo * kPiece), e = std::min(len, static_cast<size_t>(hi * kPiece));
+            std::memcpy(out + off + a, b + a, e - a);
+        }, 4);
+    }
+}
+
 // --------------------------------------------------------------- builders
 i64 sell_sigma() {
     const char* e = std::getenv("ILUG_SELL_SIGMA");
