@@ -276,10 +276,11 @@ Csr spgemm_device_host(const Csr& A, const Csr& B, cudaStream_t st) {
 }
 
 // Off by default: with the rest of the AMG setup on the host, the operand
-// uploads and the coarse-operator download cost more than the host SpGEMM
-// saves (C2 level 0: 1.14 s device incl. 0.65 s upload / 0.20 s download vs
-// 1.03 s host on 16 cores; C4 level 0: 5.9 s, 3.3 s of it the pageable
-// download, vs 4.8 s). The kernels are the building block for a device-resident
+// uploads and the coarse-operator download eat the gain, and the products
+// compete with the concurrent device factorisation for the GPU and the
+// staging buffers (C2 level 0: 1.14 s device vs 1.03 s host on 16 cores, C2
+// setup +2.9 s with it on; C4 level 0 with staged downloads: 2.2 s vs 5.0 s,
+// setup 21.3 vs 23.6 s). The kernels are the building block for a device-resident
 // hierarchy setup. ILUG_GALERKIN_DEVICE=1 enables it.
 bool galerkin_on_device() {
     const char* e = std::getenv("ILUG_GALERKIN_DEVICE");
