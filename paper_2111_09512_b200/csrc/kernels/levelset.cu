@@ -4,20 +4,22 @@
 //
 // Host analysis buckets rows into wavefront levels of the dependency DAG and
 // stores a level-ordered SELL-32 copy of the operator (each level padded to a
-// whole number of slices, so a warp never straddles two levels). Each row is
-// computed by one thread in the serial code's exact operation order
-// (s = b; s -= a_ij x_j ascending; x_i = s / d), so the result is bitwise the
-// sequential solve of src/trisolve.cpp:20-55 / src/smoother.cpp:113-132.
+// whole number of slices, so a warp never straddles two levels). Every row is
+// computed in the serial code's exact operation order (s = b; s -= a_ij x_j
+// ascending; x_i = s / d), so the result is bitwise the sequential solve of
+// src/trisolve.cpp:20-55 / src/smoother.cpp:113-132.
 //
-// Two schedules:
-//  * narrow DAGs (coarse AMG levels): one 1024-thread CTA walks the levels
-//    with __syncthreads between them (no grid-wide synchronisation at all);
-//  * wide DAGs (finest-level factors): sync-free wavefront — warps take
-//    32-row slices in level order from an atomic ticket and each row waits
-//    only on its own dependencies' completion flags (acquire/release through
-//    L2, epoch-stamped so nothing is reset between solves). A slice only
-//    depends on slices handed out before it, so progress never depends on CTA
-//    residency and no cooperative launch or global barrier is needed.
+// Schedules (LevelPlan::build picks by the average rows per level):
+//  * narrow DAGs (<= 512 rows per level: coarse AMG levels): k_levels_warp,
+//    one thread-block cluster walks the levels with barrier.cluster between
+//    them; a warp per row (products in parallel, ordered shuffle-chain sum);
+//  * wide DAGs (finest-level factors): k_levels_vflags, sync-free — warps take
+//    32-row slices in level order from an atomic ticket, thread per row, and
+//    the solution entries themselves are the completion flags (sentinel-
+//    filled x, relaxed 64-bit publish/poll). A slice only depends on slices
+//    handed out before it, so progress never depends on CTA residency.
+//  * A/B and test forms: k_levels_cta (one CTA, thread per row, ILUG_LEVELSET=
+//    cta1) and k_levels_flags (separate epoch-stamped flags, =flags).
 #include "levelset.hpp"
 
 #include <cuda/atomic>
