@@ -67,9 +67,10 @@ ILUAMG_API int ilug_galerkin_device(const iluamg_matrix* A, const iluamg_matrix*
                                     iluamg_matrix** C);
 
 /* ---- K1-K5: factors ---- */
-/* Host ILU per the config's ilu.* keys, then upload + K1 scaling per `scaling`
- * (0 none, 1 row, 2 row_col). upper_iteration: 0 scaled, 1 jacobi (unscaled).
- * direct_plans != 0 also builds the level schedules for ilug_solve_*. */
+/* ILU(0)/ILUT per the config's ilu.* keys (on the device, bitwise the host and
+ * reference factors), then K1 scaling per `scaling` (0 none, 1 row, 2 row_col).
+ * upper_iteration: 0 scaled, 1 jacobi (unscaled). direct_plans != 0 also builds
+ * the level schedules for ilug_solve_*. */
 ILUAMG_API int ilug_factors_create(const iluamg_matrix* A, const iluamg_config* cfg, int scaling,
                                    int upper_iteration, int direct_plans, ilug_factors** out);
 /* From explicit factors: L strictly lower (unit diagonal implicit), U upper with its diagonal. */
