@@ -295,18 +295,38 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
     epi(row, s, pr);
 }
 
-template <class Epi, bool HINT, bool PTAIL = true>
+// HOIST: the row length and slice start (valid for every p < nrows_pad,
+// padding slots included) are loaded together with perm[p]: a padding slot
+// runs the row with len = 0 and skips the epilogue instead of exiting early,
+// so there is no branch for the compiler to sink the loads past and the row's
+// metadata costs one memory round trip instead of two (SASS without it:
+// LDG perm -> EXIT -> LDG rowlen/slice_ptr).
+template <class Epi, bool HINT, bool PTAIL = true, bool HOIST = true>
 __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
                                                     Epi epi) {
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
     if (p >= M.nrows_pad) return;
-    const i64 row = M.perm ? M.perm[p] : p;
-    if (row < 0 || row >= nrows) return;
+    int len = 0;
+    i64 sp = 0;
+    if constexpr (HOIST) {
+        len = M.rowlen[p];
+        sp = M.slice_ptr[p >> 5];
+    }
+    i64 row = M.perm ? M.perm[p] : p;
+    const bool valid = row >= 0 && row < nrows;
+    if constexpr (HOIST) {
+        if (!valid) len = 0, row = 0;
+    } else {
+        if (!valid) return;
+    }
     decltype(epi.pre(row)) pr{};
     if constexpr (Epi::kEarly) pr = epi.pre(row); // issued before the row loop
-    const int len = M.rowlen[p];
-    const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
-    const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
+    if constexpr (!HOIST) {
+        len = M.rowlen[p];
+        sp = M.slice_ptr[p >> 5];
+    }
+    const double* vp = M.vals + sp + (p & 31);
+    const int* cp = M.cols + sp + (p & 31);
     unsigned long long pf = 0, pl = 0;
     if (HINT) pf = l2_policy_first(), pl = l2_policy_last();
     auto lv = [&](int t) { return HINT ? ld_stream(vp + t * kSlice, pf) : ld_stream(vp + t * kSlice); };
@@ -353,7 +373,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
         for (; t < len; ++t) s = s + lv(t) * lx(lc(t));
     }
     if constexpr (!Epi::kEarly) pr = epi.pre(row);
-    epi(row, s, pr);
+    if (valid) epi(row, s, pr);
 }
 
 // Kernel variant knobs for A/B experiments (tools/probe_sweep.py):
@@ -386,6 +406,10 @@ bool warp_rows_enabled() { // ILUG_WARP_ROWS=0: small operators keep the thread-
     const char* e = std::getenv("ILUG_WARP_ROWS");
     return !(e && e[0] == '0');
 }
+bool rowdot_hoist() { // ILUG_ROWDOT_HOIST=0: row metadata loaded after the padding check (A/B)
+    const char* e = std::getenv("ILUG_ROWDOT_HOIST");
+    return !(e && e[0] == '0');
+}
 int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy)
     const char* e = std::getenv("ILUG_ROWDOT");
     return e && e[0] == '8' ? 8 : 4;
@@ -412,6 +436,8 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 128), 128, 0, st>>>(view(M), M.nrows, x, epi);
     else if (rowdot_block(M) == 64)
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 64), 64, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (!rowdot_hoist())
+        k_rowdot<Epi, false, true, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     ILUG_LAUNCH_CHECK();

@@ -37,8 +37,9 @@ for sigma in os.environ.get("PROBE_SIGMAS", "1024").split(","):
     os.environ["ILUG_SELL_SIGMA"] = sigma
     F = ilug.Factors.from_csr(n, Lc, Uc, scaling="row")
     st = F.stats()
-    for hints in os.environ.get("PROBE_BLOCKS", "256").split(","):
-        os.environ["ILUG_ROWDOT_BLOCK"] = hints
+    var = os.environ.get("PROBE_VAR", "ILUG_ROWDOT_BLOCK")  # the A/B knob to sweep
+    for rep, hints in enumerate(os.environ.get("PROBE_BLOCKS", "256").split(",")):
+        os.environ[var] = hints
         res = []
         for name, fn, nnz in (("U", F.sweep_upper, st["nnz_Us"]), ("L", F.sweep_lower, st["nnz_Ls"])):
             # m=2 = one scale/copy pass + one SpMV sweep; isolate the sweep by differencing m=3 - m=2
@@ -56,6 +57,6 @@ for sigma in os.environ.get("PROBE_SIGMAS", "1024").split(","):
             ms = (ts[6] - ts[2]) / 4
             gbs = (12 * nnz + 28 * n + 4) / (ms * 1e-3) / 1e9
             res.append(f"{name}: {ms * 1e3:7.1f} us {gbs:7.1f} GB/s")
-        print(f"sigma={sigma:5s} block={hints} padded_U={st['padded_Us'] / st['nnz_Us'] - 1:.3f}  " + "  ".join(res),
+        print(f"sigma={sigma:5s} {var}={hints} padded_U={st['padded_Us'] / st['nnz_Us'] - 1:.3f}  " + "  ".join(res),
               flush=True)
     del F
