@@ -265,13 +265,15 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
                                                           const double* __restrict__ halo, i32 nloc, Epi epi) {
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
     if (p >= M.nrows_pad) return;
-    const i64 row = M.perm ? M.perm[p] : p;
-    if (row < 0 || row >= nrows) return;
+    int len = M.rowlen[p]; // row metadata in the same round trip as perm (see k_rowdot HOIST)
+    const i64 sp = M.slice_ptr[p >> 5];
+    i64 row = M.perm ? M.perm[p] : p;
+    const bool valid = row >= 0 && row < nrows;
+    if (!valid) len = 0, row = 0;
     decltype(epi.pre(row)) pr{};
     if constexpr (Epi::kEarly) pr = epi.pre(row); // issued before the row loop
-    const int len = M.rowlen[p];
-    const double* vp = M.vals + M.slice_ptr[p >> 5] + (p & 31);
-    const int* cp = M.cols + M.slice_ptr[p >> 5] + (p & 31);
+    const double* vp = M.vals + sp + (p & 31);
+    const int* cp = M.cols + sp + (p & 31);
     double s = 0.0;
     int t = 0;
     for (; t + 4 <= len; t += 4) {
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
         s = s + ld_stream(vp + t * kSlice) * (c < nloc ? ld_gather(x + c) : ld_gather(halo + (c - nloc)));
     }
     if constexpr (!Epi::kEarly) pr = epi.pre(row);
-    epi(row, s, pr);
+    if (valid) epi(row, s, pr);
 }
 
 // HOIST: the row length and slice start (valid for every p < nrows_pad,
