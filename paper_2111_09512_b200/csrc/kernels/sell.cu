@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
 // so there is no branch for the compiler to sink the loads past and the row's
 // metadata costs one memory round trip instead of two (SASS without it:
 // LDG perm -> EXIT -> LDG rowlen/slice_ptr).
-template <class Epi, bool HINT, bool PTAIL = true, bool HOIST = true>
+template <class Epi, bool HINT, bool PTAIL = true, bool HOIST = true, bool EARLY = Epi::kEarly>
 __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
                                                     Epi epi) {
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
         if (!valid) return;
     }
     decltype(epi.pre(row)) pr{};
-    if constexpr (Epi::kEarly) pr = epi.pre(row); // issued before the row loop
+    if constexpr (EARLY) pr = epi.pre(row); // issued before the row loop
     if constexpr (!HOIST) {
         len = M.rowlen[p];
         sp = M.slice_ptr[p >> 5];
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
     } else {
         for (; t < len; ++t) s = s + lv(t) * lx(lc(t));
     }
-    if constexpr (!Epi::kEarly) pr = epi.pre(row);
+    if constexpr (!EARLY) pr = epi.pre(row);
     if (valid) epi(row, s, pr);
 }
 
@@ -408,6 +408,10 @@ bool warp_rows_enabled() { // ILUG_WARP_ROWS=0: small operators keep the thread-
     const char* e = std::getenv("ILUG_WARP_ROWS");
     return !(e && e[0] == '0');
 }
+bool rowdot_early() { // ILUG_ROWDOT_EARLY=1: every epilogue's inputs loaded before the row loop (A/B)
+    const char* e = std::getenv("ILUG_ROWDOT_EARLY");
+    return e && e[0] == '1';
+}
 bool rowdot_hoist() { // ILUG_ROWDOT_HOIST=0: row metadata loaded after the padding check (A/B)
     const char* e = std::getenv("ILUG_ROWDOT_HOIST");
     return !(e && e[0] == '0');
@@ -438,6 +442,8 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 128), 128, 0, st>>>(view(M), M.nrows, x, epi);
     else if (rowdot_block(M) == 64)
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 64), 64, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (rowdot_early())
+        k_rowdot<Epi, false, true, true, true><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else if (!rowdot_hoist())
         k_rowdot<Epi, false, true, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else
