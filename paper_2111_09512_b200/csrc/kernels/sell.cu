@@ -190,7 +190,7 @@ struct EpiNegScaleAcc { // poly_gs: term = -invd * t; acc += term
 // and its x, forms the product a_t * x_t (the serial loop's rounded product),
 // and the in-order sum s = 0 + p_0 + p_1 + ... runs as a shuffle chain, so the
 // result is bitwise the thread-per-row kernel's. Lane 0 applies the epilogue.
-template <class Epi>
+template <class Epi, bool HOIST = true>
 __global__ void __launch_bounds__(kBlock) k_rowdot_warp(SellView M, i64 nrows, const double* __restrict__ x,
                                                          Epi epi) {
     const unsigned full = 0xffffffffu;
@@ -198,10 +198,18 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_warp(SellView M, i64 nrows, c
     const i64 w0 = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
     const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
     for (i64 p = w0; p < M.nrows_pad; p += nw) {
-        const i64 row = M.perm ? M.perm[p] : p;
-        if (row < 0 || row >= nrows) continue;
-        const int len = M.rowlen[p];
-        const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+        // HOIST: row metadata in the same round trip as perm (see k_rowdot)
+        int len = HOIST ? M.rowlen[p] : 0;
+        i64 base = HOIST ? M.slice_ptr[p >> 5] + (p & 31) : 0;
+        i64 row = M.perm ? M.perm[p] : p;
+        const bool valid = row >= 0 && row < nrows;
+        if (!HOIST) {
+            if (!valid) continue;
+            len = M.rowlen[p];
+            base = M.slice_ptr[p >> 5] + (p & 31);
+        } else if (!valid) {
+            len = 0, row = 0;
+        }
         decltype(epi.pre(row)) pr{};
         if (lane == 0) pr = epi.pre(row);
         double s = 0.0;
@@ -215,7 +223,7 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_warp(SellView M, i64 nrows, c
             const int cnt = min(32, len - t0);
             for (int u = 0; u < cnt; ++u) s = s + __shfl_sync(full, prod, u);
         }
-        if (lane == 0) epi(row, s, pr);
+        if (lane == 0 && valid) epi(row, s, pr);
     }
 }
 constexpr i64 kWarpRowMax = 65536; // operators up to this many rows take k_rowdot_warp
@@ -428,7 +436,10 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         const i64 warps = M.nrows_pad;
         const unsigned g = static_cast<unsigned>(std::min<i64>((warps * 32 + kBlock - 1) / kBlock,
                                                                static_cast<i64>(device_sm_count()) * 8));
-        k_rowdot_warp<Epi><<<g, kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+        if (rowdot_hoist())
+            k_rowdot_warp<Epi><<<g, kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+        else
+            k_rowdot_warp<Epi, false><<<g, kBlock, 0, st>>>(view(M), M.nrows, x, epi);
         ILUG_LAUNCH_CHECK();
         return;
     }
