@@ -460,7 +460,10 @@ __global__ void k_fill_sentinel(double* x, i64 n) {
     if (i < n) reinterpret_cast<unsigned long long*>(x)[i] = kXSentinel;
 }
 
-template <int MODE>
+// HOIST: the row length and slice start are loaded with perm[p] (a padding
+// slot runs len = 0 and publishes nothing) instead of after the padding test,
+// which the compiler otherwise turns into two dependent round trips.
+template <int MODE, bool HOIST = true>
 __global__ void __launch_bounds__(kFlagBlock)
 k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x, const double* __restrict__ xold,
                 unsigned* ticket, unsigned* err) {
@@ -472,10 +475,17 @@ k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x
         sl = __shfl_sync(0xffffffffu, sl, 0);
         if (sl >= nslices) return;
         const i64 p = static_cast<i64>(sl) * kSlice + lane;
-        const i64 row = M.perm[p];
-        if (row < 0) continue;
-        const int len = M.rowlen[p];
-        const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+        int len = HOIST ? M.rowlen[p] : 0;
+        i64 base = HOIST ? M.slice_ptr[p >> 5] + (p & 31) : 0;
+        i64 row = M.perm[p];
+        const bool valid = row >= 0;
+        if (!HOIST) {
+            if (!valid) continue;
+            len = M.rowlen[p];
+            base = M.slice_ptr[p >> 5] + (p & 31);
+        } else if (!valid) {
+            len = 0, row = 0;
+        }
         double s = b[row], d = 1.0;
         for (int t0 = 0; t0 < len; t0 += kChunk) {
             i32 c[kChunk];
@@ -531,7 +541,7 @@ k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x
         const double r = MODE == 0 ? s : s / d;
         unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(r));
         if (bits == kXSentinel) bits = 0x7FFFFFFFFFFFFFFFull; // the canonical NaN
-        st_relaxed_u64(x + row, bits);
+        if (valid) st_relaxed_u64(x + row, bits);
     }
 }
 
@@ -539,7 +549,13 @@ __global__ void k_ticket_reset(unsigned* ticket) { *ticket = 0u; }
 
 template <int MODE>
 const void* vflag_kernel() {
-    return reinterpret_cast<const void*>(k_levels_vflags<MODE>);
+    // ILUG_LEVELSET_HOIST=1: hoisted row metadata (A/B; bitwise the same). Off
+    // by default: C2 direct solve 3.87/4.28 s hoisted vs 3.84/4.61 s without
+    // in an interleaved A/B (no clear gain; the hoisted MODE 0 form spills
+    // 32 B), unlike the sweep kernels where the hoist measured +2-9 %.
+    const char* e = std::getenv("ILUG_LEVELSET_HOIST");
+    if (e && e[0] == '1') return reinterpret_cast<const void*>(k_levels_vflags<MODE>);
+    return reinterpret_cast<const void*>(k_levels_vflags<MODE, false>);
 }
 
 template <int MODE>
