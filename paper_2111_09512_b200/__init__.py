@@ -137,27 +137,47 @@ def _check(status: int, allow_not_converged: bool = False) -> int:
     raise IlugError(status, lib.iluamg_last_error().decode())
 
 
-def _ptr(a) -> Optional[int]:
-    """Device (or host) address of a tensor / int / None."""
+def _ptr(a, n: Optional[int] = None) -> Optional[int]:
+    """Device address of a CUDA float64 tensor / raw int / None.
+
+    Tensors are checked before their address crosses the C ABI: they must be
+    CUDA, float64, contiguous and hold at least ``n`` elements (a CPU or short
+    tensor would otherwise turn into out-of-bounds device accesses that poison
+    the CUDA context). Raw integers are trusted as-is.
+    """
     if a is None:
         return None
     if isinstance(a, int):
         return a
     if hasattr(a, "data_ptr"):
+        if not getattr(a, "is_cuda", False):
+            raise TypeError(f"expected a CUDA tensor, got a tensor on {getattr(a, 'device', '?')}")
+        if str(a.dtype) != "torch.float64":
+            raise TypeError(f"expected a float64 tensor, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError("expected a contiguous tensor")
+        if n is not None and a.numel() < n:
+            raise ValueError(f"tensor has {a.numel()} elements, the operator needs {n}")
         return a.data_ptr()
     raise TypeError(f"cannot take a device pointer of {type(a)!r}")
 
 
-def _host_ptrs(arrs):
-    """void*[] of host float64 arrays (numpy arrays or CPU torch tensors)."""
+def _host_ptrs(arrs, n: Optional[int] = None):
+    """void*[] of host float64 arrays (numpy arrays or CPU torch tensors) of >= n elements."""
     ptrs = (C.c_void_p * max(len(arrs), 1))()
     for i, a in enumerate(arrs):
         if hasattr(a, "data_ptr"):
+            if getattr(a, "is_cuda", False) or str(a.dtype) != "torch.float64" or not a.is_contiguous():
+                raise TypeError("host tensors must be contiguous float64 CPU tensors")
+            size = a.numel()
             ptrs[i] = a.data_ptr()
         else:
             if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
                 raise TypeError("host arrays must be contiguous float64")
+            size = a.size
             ptrs[i] = a.ctypes.data
+        if n is not None and size < n:
+            raise ValueError(f"host array has {size} elements, the operator needs {n}")
     return ptrs
 
 
@@ -425,10 +445,12 @@ class Factors:
         return (rp, ci, v), (rs if fl.value & 1 else None), (cs if fl.value & 2 else None)
 
     def sweep_lower(self, b, y, m, stream=None):
-        _check(lib.ilug_sweep_lower(self.h, _ptr(b), _ptr(y), m, _stream(stream)))
+        n = self.rows
+        _check(lib.ilug_sweep_lower(self.h, _ptr(b, n), _ptr(y, n), m, _stream(stream)))
 
     def sweep_upper(self, b, x, m, stream=None):
-        _check(lib.ilug_sweep_upper(self.h, _ptr(b), _ptr(x), m, _stream(stream)))
+        n = self.rows
+        _check(lib.ilug_sweep_upper(self.h, _ptr(b, n), _ptr(x, n), m, _stream(stream)))
 
     def sweep_upper_host(self, b: np.ndarray, m: int) -> np.ndarray:
         b = _np(b, np.float64)
@@ -437,10 +459,12 @@ class Factors:
         return x
 
     def solve_lower(self, b, y, stream=None):
-        _check(lib.ilug_solve_lower(self.h, _ptr(b), _ptr(y), _stream(stream)))
+        n = self.rows
+        _check(lib.ilug_solve_lower(self.h, _ptr(b, n), _ptr(y, n), _stream(stream)))
 
     def solve_upper(self, b, x, stream=None):
-        _check(lib.ilug_solve_upper(self.h, _ptr(b), _ptr(x), _stream(stream)))
+        n = self.rows
+        _check(lib.ilug_solve_upper(self.h, _ptr(b, n), _ptr(x, n), _stream(stream)))
 
     def __del__(self):
         if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
@@ -453,12 +477,13 @@ class DeviceMatrix:
         out = C.c_void_p()
         _check(lib.ilug_dmatrix_create(A.h, C.byref(out)))
         self.h = out
+        self.n, self.ncols = A.rows, A.cols
 
     def spmv(self, x, y, stream=None):
-        _check(lib.ilug_spmv(self.h, _ptr(x), _ptr(y), _stream(stream)))
+        _check(lib.ilug_spmv(self.h, _ptr(x, self.ncols), _ptr(y, self.n), _stream(stream)))
 
     def residual(self, x, b, r, stream=None):
-        _check(lib.ilug_residual(self.h, _ptr(x), _ptr(b), _ptr(r), _stream(stream)))
+        _check(lib.ilug_residual(self.h, _ptr(x, self.ncols), _ptr(b, self.n), _ptr(r, self.n), _stream(stream)))
 
     def __del__(self):
         if getattr(self, "h", None) and self.h.value and lib is not None:  # not at interpreter exit
@@ -471,19 +496,23 @@ class Smoother:
         out = C.c_void_p()
         _check(lib.ilug_smoother_create(A.h, cfg.h, which, C.byref(out)))
         self.h = out
+        self.n = A.rows
 
     def smooth(self, b, x, stream=None, want_norm=False):
         nrm = C.c_double()
-        _check(lib.ilug_smooth(self.h, _ptr(b), _ptr(x), C.byref(nrm) if want_norm else None, _stream(stream)))
+        _check(lib.ilug_smooth(self.h, _ptr(b, self.n), _ptr(x, self.n), C.byref(nrm) if want_norm else None,
+                               _stream(stream)))
         return nrm.value if want_norm else None
 
     def ilu_sweep(self, b, x, stream=None):
-        _check(lib.ilug_ilu_smooth_sweep(self.h, _ptr(b), _ptr(x), _stream(stream)))
+        _check(lib.ilug_ilu_smooth_sweep(self.h, _ptr(b, self.n), _ptr(x, self.n), _stream(stream)))
 
     def smooth_host_many(self, bs, xs):
         """Pipelined x_i <- smooth(A, b_i, x_i) over host arrays (numpy or CPU
         tensors; pinned memory overlaps the copies), ilug_smooth_host_many."""
-        _check(lib.ilug_smooth_host_many(self.h, len(bs), _host_ptrs(bs), _host_ptrs(xs)))
+        if len(bs) != len(xs):
+            raise ValueError("bs and xs must have the same length")
+        _check(lib.ilug_smooth_host_many(self.h, len(bs), _host_ptrs(bs, self.n), _host_ptrs(xs, self.n)))
 
     def wave(self):
         """Wavefront plan tile counts and the stalled flag (see ilug_smoother_wave)."""
@@ -492,8 +521,8 @@ class Smoother:
         return dict(tiles_L=tl.value, tiles_U=tu.value, stalled=bool(st.value), waits=wt.value)
 
     def sweeps_fused(self, which: int, nsweeps: int, x_in, rhs, tmp, out, stream=None):
-        _check(lib.ilug_smoother_sweeps_fused(self.h, which, nsweeps, _ptr(x_in), _ptr(rhs),
-                                              _ptr(tmp) if tmp is not None else None, _ptr(out),
+        _check(lib.ilug_smoother_sweeps_fused(self.h, which, nsweeps, _ptr(x_in, self.n), _ptr(rhs, self.n),
+                                              _ptr(tmp, self.n) if tmp is not None else None, _ptr(out, self.n),
                                               _stream(stream)))
 
     def __del__(self):
@@ -508,6 +537,7 @@ class Hierarchy:
         fn = lib.ilug_hierarchy_create_host if host_only else lib.ilug_hierarchy_create
         _check(fn(A.h, cfg.h, C.byref(out)))
         self.h = out
+        self.n = A.rows
 
     @property
     def levels(self) -> int:
@@ -523,7 +553,7 @@ class Hierarchy:
         return lib.ilug_hierarchy_operator_complexity(self.h)
 
     def vcycle(self, r, z, stream=None):
-        _check(lib.ilug_vcycle(self.h, _ptr(r), _ptr(z), _stream(stream)))
+        _check(lib.ilug_vcycle(self.h, _ptr(r, self.n), _ptr(z, self.n), _stream(stream)))
 
     @property
     def graph_nodes(self) -> int:
@@ -531,7 +561,8 @@ class Hierarchy:
 
     def gmres(self, cfg: Config, b, x, stream=None):
         it, rr = C.c_longlong(), C.c_double()
-        st = lib.ilug_gmres(self.h, cfg.h, _ptr(b), _ptr(x), C.byref(it), C.byref(rr), _stream(stream))
+        st = lib.ilug_gmres(self.h, cfg.h, _ptr(b, self.n), _ptr(x, self.n), C.byref(it), C.byref(rr),
+                            _stream(stream))
         _check(st, allow_not_converged=True)
         return dict(status=st, iterations=it.value, final_relres=rr.value)
 

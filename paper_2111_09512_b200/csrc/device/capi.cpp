@@ -389,6 +389,7 @@ int ilug_solve_lower(const ilug_factors* f, const double* b, double* y, void* st
     return guarded([&] {
         need(f && b && y);
         f->f.solve_lower(b, y, S(stream));
+        ilug::levelset_check_error(S(stream));
         return ILUAMG_OK;
     });
 }
@@ -397,6 +398,7 @@ int ilug_solve_upper(const ilug_factors* f, const double* b, double* x, void* st
         need(f && b && x);
         Ws ws(f->f.n(), S(stream));
         f->f.solve_upper(b, x, ws.p, S(stream));
+        ilug::levelset_check_error(S(stream));
         return ILUAMG_OK;
     });
 }

@@ -38,6 +38,11 @@ constexpr int kFlagBlock = 256;
 // MODE 0: unit lower, strict storage: x_i = b_i - sum L_ij x_j
 // MODE 1: upper with stored diagonal: x_i = (b_i - sum_{j != i} U_ij x_j) / U_ii
 // MODE 2: Gauss-Seidel on A: x'_i = (b_i - sum_{j<i} a_ij x'_j - sum_{j>i} a_ij x_j) / a_ii
+// Set by a sync-free kernel whose dependency wait exceeded its bound (a
+// scheduling fault, never a slow producer); read and cleared by
+// levelset_check_error() at the callers' sync points.
+__device__ unsigned g_levelset_timeout;
+
 template <int MODE>
 __device__ __forceinline__ bool is_dep(i32 j, i64 row) {
     return MODE == 1 ? j > row : j < row;
@@ -79,6 +84,10 @@ __device__ __forceinline__ void level_row(const SellView& M, i64 p, i64 row, con
                     if (t0 + u < len && !(MODE != 0 && c[u] == row) && is_dep<MODE>(c[u], row))
                         ready &= ld_relaxed_flag(flags + c[u]) == E;
                 if (!ready && spin > 8) __nanosleep(64);
+                if (!ready && spin > (1 << 24)) { // seconds: a scheduling bug, not a slow producer
+                    atomicExch(&g_levelset_timeout, 1u);
+                    break;
+                }
             }
             asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
@@ -466,7 +475,7 @@ __global__ void k_fill_sentinel(double* x, i64 n) {
 template <int MODE, bool HOIST = true>
 __global__ void __launch_bounds__(kFlagBlock)
 k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x, const double* __restrict__ xold,
-                unsigned* ticket, unsigned* err) {
+                unsigned* ticket) {
     constexpr int kChunk = 16;
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -515,7 +524,7 @@ k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x
             long long spins = 0;
             while (pend) {
                 if (++spins > (1ll << 26)) { // seconds: a scheduling bug, not a slow producer
-                    atomicExch(err, 1u);
+                    atomicExch(&g_levelset_timeout, 1u);
                     break;
                 }
                 __nanosleep(32);
@@ -749,8 +758,7 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
         k_fill_sentinel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, n);
         k_ticket_reset<<<1, 1, 0, st>>>(ticket);
         ILUG_LAUNCH_CHECK();
-        unsigned* err = flags_.p + n + 2;
-        void* args[] = {&mv, &ns, &b, &x, &xold, &ticket, &err};
+        void* args[] = {&mv, &ns, &b, &x, &xold, &ticket};
         const void* fn = mode == 0 ? vflag_kernel<0>() : mode == 1 ? vflag_kernel<1>() : vflag_kernel<2>();
         ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid_)), dim3(kFlagBlock), args, 0, st));
         return;
@@ -761,6 +769,17 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
     void* args[] = {&mv, &ns, &b, &x, &xold, &flags, &ep, &ticket};
     const void* fn = mode == 0 ? flag_kernel<0>() : mode == 1 ? flag_kernel<1>() : flag_kernel<2>();
     ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid_)), dim3(kFlagBlock), args, 0, st));
+}
+
+void levelset_check_error(cudaStream_t st) {
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    unsigned v = 0;
+    ILUG_CUDA(cudaMemcpyFromSymbol(&v, g_levelset_timeout, sizeof v));
+    if (v) {
+        const unsigned zero = 0;
+        ILUG_CUDA(cudaMemcpyToSymbol(g_levelset_timeout, &zero, sizeof zero));
+        fail_numeric("level-scheduled solve: a dependency wait timed out (scheduling fault); the result is invalid");
+    }
 }
 
 } // namespace ilug

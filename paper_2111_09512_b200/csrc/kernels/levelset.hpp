@@ -45,4 +45,8 @@ private:
     i64 max_level_rows_ = 0;
 };
 
+/// Sync `st`, then raise ERR_NUMERIC if a sync-free level-set kernel hit its
+/// dependency-wait bound since the last check (and clear the flag).
+void levelset_check_error(cudaStream_t st);
+
 } // namespace ilug
