@@ -214,11 +214,23 @@ ILUAMG_API long long ilug_dist_plan_requests(const ilug_dist_plan* p, int q, lon
 ILUAMG_API int ilug_dist_plan_set_sends(ilug_dist_plan* p, int q, const long long* ids, long long count);
 /* Local row indices packed for rank q; returns the count (rows may be NULL). */
 ILUAMG_API long long ilug_dist_plan_sends(const ilug_dist_plan* p, int q, long long* rows);
-/* which: 0 extended local matrix (halo columns renumbered, global entry order), 1 diagonal block. */
+/* which: 0 extended local matrix (halo columns renumbered, global entry order), 1 diagonal block,
+ * 2 off-block entries (halo columns, extended numbering). */
 ILUAMG_API int ilug_dist_plan_matrix(const ilug_dist_plan* p, int which, iluamg_matrix** out);
 ILUAMG_API void ilug_dist_plan_free(ilug_dist_plan* p);
 ILUAMG_API int ilug_dist_unique_id(char* out128);
 ILUAMG_API int ilug_dist_comm_create(int nranks, int rank, const char* id128, ilug_dist_comm** out);
+/* In-process rank group: the ranks are host threads of one process (any
+ * devices, several may share one GPU). Every collective synchronises the
+ * caller's stream and meets the other ranks at a host barrier, so kernels
+ * never wait on each other — the single-GPU stand-in for the NCCL path. */
+typedef struct ilug_dist_group_s ilug_dist_group;
+ILUAMG_API int ilug_dist_group_create(int nranks, ilug_dist_group** out);
+ILUAMG_API void ilug_dist_group_free(ilug_dist_group* g);
+ILUAMG_API int ilug_dist_comm_create_local(ilug_dist_group* g, int rank, ilug_dist_comm** out);
+/* Complete a plan's send lists over the communicator (collective; replaces
+ * the caller-side request exchange). */
+ILUAMG_API int ilug_dist_plan_exchange(ilug_dist_plan* p, const ilug_dist_comm* c);
 ILUAMG_API int ilug_dist_allreduce_sum(const ilug_dist_comm* c, double* buf, long long count, void* stream);
 ILUAMG_API void ilug_dist_comm_free(ilug_dist_comm* c);
 /* Block-Jacobi ILU smoother of the plan's block (the config's ilu, scaling and trisolve keys). */
@@ -240,16 +252,34 @@ ILUAMG_API int ilug_dist_smoother_sweep_once(const ilug_dist_smoother* s, int wh
                                              const double* rhs, double* out, void* stream);
 ILUAMG_API void ilug_dist_smoother_free(ilug_dist_smoother* s);
 
-/* Distributed GMRES+AMG: global (F)GMRES over the ranks' rows (halo SpMV,
- * NCCL-summed CGS2 reductions) with block-Jacobi AMG (each rank's V-cycle on
- * its diagonal block, amg.* and smoother.* keys). b, x: this rank's rows. */
+/* Distributed GMRES+AMG: the GLOBAL hierarchy `h` (a host
+ * hierarchy handle, ilug_hierarchy_create_host; every rank passes the same
+ * one) is row-block partitioned level by level: A_k / P_k rows by the level's
+ * partition, R_k rows by the next level's, halo exchanges before every global
+ * product, rank-local smoothers (block-Jacobi ILU / poly-GS, hybrid GS, global
+ * Jacobi / l1), the coarsest rhs all-gathered and solved on every rank.
+ * Global (F)GMRES over the ranks' rows with summed CGS2 reductions (replaces
+ * gmres_impl + the V-cycle lambda, src/krylov.cpp:75-238, src/driver.cpp:182-185).
+ * b, x, r, z: this rank's rows. All calls are collective. */
 typedef struct ilug_dist_solver_s ilug_dist_solver;
-ILUAMG_API int ilug_dist_solver_create(const ilug_dist_plan* p, const ilug_dist_comm* c,
-                                       const iluamg_config* cfg, ilug_dist_solver** out);
+ILUAMG_API int ilug_dist_solver_create(const ilug_hierarchy* h, const ilug_dist_comm* c, ilug_dist_solver** out);
 ILUAMG_API int ilug_dist_gmres(ilug_dist_solver* s, const iluamg_config* cfg, const double* b, double* x,
                                long long* iterations, double* final_relres, void* stream);
+ILUAMG_API int ilug_dist_vcycle(ilug_dist_solver* s, const double* r, double* z, void* stream);
+ILUAMG_API int ilug_dist_solver_info(const ilug_dist_solver* s, long long* row0, long long* nloc, int* levels);
 ILUAMG_API int ilug_dist_solver_levels(const ilug_dist_solver* s);
 ILUAMG_API void ilug_dist_solver_free(ilug_dist_solver* s);
+
+/* Host-only view of the per-level distribution (no device work): the halo
+ * plans a rank's distributed V-cycle uses (tests, tooling). which: 0 A, 1 R,
+ * 2 P (levels before the last smoothed one); ilug_dist_levels_last: the last
+ * smoothed level's whole R (which 0) and its rows of P (which 1). */
+typedef struct ilug_dist_levels_s ilug_dist_levels;
+ILUAMG_API int ilug_dist_level_plans(const ilug_hierarchy* h, int nranks, int rank, ilug_dist_levels** out);
+ILUAMG_API int ilug_dist_levels_count(const ilug_dist_levels* l);
+ILUAMG_API int ilug_dist_levels_plan(const ilug_dist_levels* l, int k, int which, ilug_dist_plan** out);
+ILUAMG_API int ilug_dist_levels_last(const ilug_dist_levels* l, int which, iluamg_matrix** out);
+ILUAMG_API void ilug_dist_levels_free(ilug_dist_levels* l);
 
 #ifdef __cplusplus
 }

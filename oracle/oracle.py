@@ -81,6 +81,10 @@ class Ref:
             "ref_amg_level_mat": (_vp, [_vp, _ll, _i]), "ref_amg_vcycle": (_i, [_vp, _pd, _pd]),
             "ref_amg_operator_complexity": (_d, [_vp]), "ref_amg_free": (None, [_vp]),
             "ref_krylov_solve": (_i, [_vp, _vp, _vp, _pd, _pd, _pll, _pi, _pd, _pd, _ll, _pll, _pd]),
+            "ref_dist_setup": (_i, [_vp, _vp, _i, _pvp]), "ref_dist_free": (None, [_vp]),
+            "ref_dist_nlevels": (_ll, [_vp]), "ref_dist_vcycle": (_i, [_vp, _pd, _pd]),
+            "ref_dist_smooth": (_i, [_vp, _ll, _pd, _pd]),
+            "ref_dist_krylov": (_i, [_vp, _vp, _vp, _pd, _pd, _pll, _pi, _pd]),
             "ref_make_rhs": (_i, [_vp, _vp, _pd]), "ref_random_uniform": (None, [_ll, _u64, _pd]),
             "ref_hash_unit": (_d, [_u64, _u64]),
             "ref_time_richardson_upper": (_i, [_vp, _pd, _ll, _ll, _pd]),
@@ -265,6 +269,30 @@ class Ref:
                                          C.byref(nh), C.byref(secs)))
         return dict(x=x, iterations=it.value, converged=bool(conv.value), final_relres=rr.value,
                     history=hist[: 3 * nh.value].reshape(-1, 3), seconds=secs.value)
+
+    # -- composed oracle of the p-rank row-block distributed solve (block smoothers)
+    def dist_setup(self, A, cfg, p):
+        out = C.c_void_p()
+        self._ok(self.L.ref_dist_setup(A, cfg, p, C.byref(out)))
+        return out
+
+    def dist_vcycle(self, d, b, x):
+        b, x = _f64(b), _f64(x).copy()
+        self._ok(self.L.ref_dist_vcycle(d, _p(b, C.c_double), _p(x, C.c_double)))
+        return x
+
+    def dist_smooth(self, d, k, b, x):
+        b, x = _f64(b), _f64(x).copy()
+        self._ok(self.L.ref_dist_smooth(d, k, _p(b, C.c_double), _p(x, C.c_double)))
+        return x
+
+    def dist_krylov(self, A, d, cfg, b):
+        b = _f64(b)
+        x = np.empty_like(b)
+        it, conv, rr = C.c_int64(), C.c_int(), C.c_double()
+        self._ok(self.L.ref_dist_krylov(A, d, cfg, _p(b, C.c_double), _p(x, C.c_double), C.byref(it),
+                                        C.byref(conv), C.byref(rr)))
+        return dict(x=x, iterations=it.value, converged=bool(conv.value), final_relres=rr.value)
 
     def make_rhs(self, cfg, A, n):
         b = np.empty(n)

@@ -24,7 +24,9 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <tuple>
 
 using namespace iluamg;
 
@@ -380,6 +382,156 @@ API int ref_time_smooth(const void* A, const void* st, const double* b, int64_t 
 
 // ---- the reference's own driver on a shim-held matrix (src/driver.cpp:239-260) ----
 #include "iluamg/driver.hpp"
+// ---- composed oracle of the row-block distributed solve ----
+// p ranks, contiguous row blocks per level (base = n/p, last rank takes the
+// remainder, src/schur.cpp:28-33). No new arithmetic: the reference hierarchy
+// with each level's smoother state rebuilt from the block-diagonal part —
+//   ilu:     factors of blockdiag(A_k) (build_smoother_state on the block matrix)
+//   poly_gs: strict lower part of blockdiag(A_k)
+//   jacobi / l1_jacobi: unchanged (global)
+//   gauss_seidel (hybrid): b' = residual(A_off, x, b), then gauss_seidel_sweep
+//            on blockdiag(A_k) — sweeps times
+// and cycle_level (src/amg.cpp:394-408) restated around those smoothers.
+namespace {
+struct DistRef {
+    Hierarchy h;
+    int p = 1;
+    std::vector<SparseMatrix> blk, off;
+    std::vector<SmootherState> st;
+};
+
+index_t owner_of(index_t i, index_t n, int p) {
+    const index_t base = n / p;
+    if (base == 0) return p - 1;
+    return std::min<index_t>(i / base, p - 1);
+}
+
+void split_blocks(const SparseMatrix& A, int p, SparseMatrix& blk, SparseMatrix& off) {
+    std::vector<index_t> rb{0}, ro{0}, cb, co;
+    std::vector<double> vb, vo;
+    for (index_t i = 0; i < A.nrows; ++i) {
+        const index_t oi = owner_of(i, A.nrows, p);
+        for (index_t k = A.row_starts[i]; k < A.row_starts[i + 1]; ++k) {
+            const index_t j = A.col_indices[k];
+            if (owner_of(j, A.ncols, p) == oi) {
+                cb.push_back(j);
+                vb.push_back(A.values[k]);
+            } else {
+                co.push_back(j);
+                vo.push_back(A.values[k]);
+            }
+        }
+        rb.push_back(static_cast<index_t>(cb.size()));
+        ro.push_back(static_cast<index_t>(co.size()));
+    }
+    blk = SparseMatrix::from_csr(A.nrows, A.ncols, std::move(rb), std::move(cb), std::move(vb));
+    off = SparseMatrix::from_csr(A.nrows, A.ncols, std::move(ro), std::move(co), std::move(vo));
+}
+
+void dist_smooth(const DistRef& d, std::size_t k, const DenseVector& b, DenseVector& x) {
+    const Level& lev = d.h.levels[k];
+    const SmootherState& st = d.st[k];
+    if (st.kind != SmootherKind::gauss_seidel) {
+        smooth(lev.A, st, b, x);
+        return;
+    }
+    for (index_t s = 0; s < st.config.sweeps; ++s) {
+        const DenseVector bp = residual(d.off[k], x, b);
+        gauss_seidel_sweep(d.blk[k], bp, x);
+    }
+}
+
+void dist_cycle(const DistRef& d, index_t k, const DenseVector& b, DenseVector& x) {
+    const Level& lev = d.h.levels[static_cast<std::size_t>(k)];
+    if (k + 1 == d.h.num_levels()) {
+        x = d.h.coarse_lu.solve(b);
+        return;
+    }
+    dist_smooth(d, static_cast<std::size_t>(k), b, x);
+    const DenseVector r = residual(lev.A, x, b);
+    const DenseVector rc = spmv(lev.R, r);
+    DenseVector v(static_cast<std::size_t>(lev.P.ncols), 0.0);
+    for (index_t i = 0; i < d.h.params.cycles_nu; ++i) dist_cycle(d, k + 1, rc, v);
+    const DenseVector corr = spmv(lev.P, v);
+    for (std::size_t i = 0; i < x.size(); ++i) x[i] += corr[i];
+    dist_smooth(d, static_cast<std::size_t>(k), b, x);
+}
+} // namespace
+
+API int ref_dist_setup(const void* A, const void* cfg, int p, void** outp) {
+    return wrap([&] {
+        auto d = std::make_unique<DistRef>();
+        d->h = setup(*static_cast<const SparseMatrix*>(A), amg_params_from(static_cast<const Cfg*>(cfg)->c));
+        d->p = p;
+        const std::size_t L = d->h.levels.size();
+        for (std::size_t k = 0; k + 1 < L; ++k) {
+            const SparseMatrix& Ak = d->h.levels[k].A;
+            const SmootherConfig& sc = d->h.params.plan.for_level(static_cast<index_t>(k));
+            SparseMatrix blk, off;
+            split_blocks(Ak, p, blk, off);
+            SmootherState st;
+            switch (sc.kind) {
+            case SmootherKind::ilu:
+                st = build_smoother_state(blk, sc); // block-Jacobi factors
+                st.n = Ak.nrows;
+                st.nnz = Ak.nnz(); // applied with the global A (its residual)
+                break;
+            case SmootherKind::poly_gs:
+                st = build_smoother_state(Ak, sc);
+                st.strict_lower = std::get<0>(split_triangular(blk));
+                break;
+            case SmootherKind::schur_ilut:
+                fail_invalid("ref_dist_setup: schur_ilut has its own distributed form");
+            default:
+                st = build_smoother_state(Ak, sc);
+            }
+            d->blk.push_back(std::move(blk));
+            d->off.push_back(std::move(off));
+            d->st.push_back(std::move(st));
+        }
+        *outp = d.release();
+    });
+}
+API void ref_dist_free(void* d) { delete static_cast<DistRef*>(d); }
+API int64_t ref_dist_nlevels(const void* d) { return static_cast<const DistRef*>(d)->h.num_levels(); }
+API int ref_dist_vcycle(const void* dp, const double* b, double* x) {
+    return wrap([&] {
+        auto* d = static_cast<const DistRef*>(dp);
+        const auto n = d->h.levels.front().A.nrows;
+        DenseVector xv = vec(x, n);
+        dist_cycle(*d, 0, vec(b, n), xv);
+        out(xv, x);
+    });
+}
+API int ref_dist_smooth(const void* dp, int64_t k, const double* b, double* x) {
+    return wrap([&] {
+        auto* d = static_cast<const DistRef*>(dp);
+        if (k < 0 || k + 1 >= d->h.num_levels()) fail_invalid("ref_dist_smooth: not a smoothed level");
+        const auto n = d->h.levels[static_cast<std::size_t>(k)].A.nrows;
+        DenseVector xv = vec(x, n);
+        dist_smooth(*d, static_cast<std::size_t>(k), vec(b, n), xv);
+        out(xv, x);
+    });
+}
+API int ref_dist_krylov(const void* A, const void* dp, const void* cfg, const double* b, double* x,
+                        int64_t* iters, int* converged, double* final_relres) {
+    return wrap([&] {
+        auto* M = static_cast<const SparseMatrix*>(A);
+        auto* d = static_cast<const DistRef*>(dp);
+        const KrylovParams kp = krylov_params_from(static_cast<const Cfg*>(cfg)->c);
+        LinearOperator precond = [d](const DenseVector& r, DenseVector& z) {
+            z.assign(r.size(), 0.0);
+            dist_cycle(*d, 0, r, z);
+        };
+        const DenseVector bv = vec(b, M->nrows);
+        auto [xs, rep] = krylov_solve(*M, bv, DenseVector(bv.size(), 0.0), precond, kp);
+        out(xs, x);
+        *iters = rep.iterations;
+        *converged = rep.converged ? 1 : 0;
+        *final_relres = rep.final_relres;
+    });
+}
+
 API int ref_run_solve(const void* A, const void* cfg, void** out) {
     return wrap([&] {
         *out = new Report(run_solve(*static_cast<const SparseMatrix*>(A), static_cast<const Cfg*>(cfg)->c,

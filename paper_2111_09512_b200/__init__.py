@@ -100,6 +100,9 @@ _SIGS = {
     "ilug_dist_plan_free": (None, [_vp]),
     "ilug_dist_unique_id": (_i, [_vp]),
     "ilug_dist_comm_create": (_i, [_i, _i, _vp, _pvp]),
+    "ilug_dist_group_create": (_i, [_i, _pvp]), "ilug_dist_group_free": (None, [_vp]),
+    "ilug_dist_comm_create_local": (_i, [_vp, _i, _pvp]),
+    "ilug_dist_plan_exchange": (_i, [_vp, _vp]),
     "ilug_dist_allreduce_sum": (_i, [_vp, _vp, _ll, _vp]),
     "ilug_dist_comm_free": (None, [_vp]),
     "ilug_dist_smoother_create": (_i, [_vp, _vp, _vp, _pvp]),
@@ -110,10 +113,17 @@ _SIGS = {
     "ilug_dist_smooth_host": (_i, [_vp, _pd, _pd]),
     "ilug_dist_smooth_host_many": (_i, [_vp, _ll, _pvp, _pvp]),
     "ilug_dist_smoother_sweep_once": (_i, [_vp, _i, _vp, _vp, _vp, _vp]),
-    "ilug_dist_solver_create": (_i, [_vp, _vp, _vp, _pvp]),
+    "ilug_dist_solver_create": (_i, [_vp, _vp, _pvp]),
     "ilug_dist_gmres": (_i, [_vp, _vp, _vp, _vp, _pll, _pd, _vp]),
+    "ilug_dist_vcycle": (_i, [_vp, _vp, _vp, _vp]),
+    "ilug_dist_solver_info": (_i, [_vp, _pll, _pll, _pi]),
     "ilug_dist_solver_levels": (_i, [_vp]),
     "ilug_dist_solver_free": (None, [_vp]),
+    "ilug_dist_level_plans": (_i, [_vp, _i, _i, _pvp]),
+    "ilug_dist_levels_count": (_i, [_vp]),
+    "ilug_dist_levels_plan": (_i, [_vp, _i, _i, _pvp]),
+    "ilug_dist_levels_last": (_i, [_vp, _i, _pvp]),
+    "ilug_dist_levels_free": (None, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

@@ -687,7 +687,7 @@ int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, dou
         p.form_iterates = c.get_bool("krylov.form_iterates");
         p.estimate_anorm = p.form_iterates || p.nrbe_criterion;
         const ilug::KrylovReport r =
-            ilug::device_gmres(h->d.A0(), h->h.levels[0].A, h->d, b, x, p, S(stream));
+            ilug::device_gmres(h->d.A0(), &h->h.levels[0].A, ilug::vcycle_of(h->d), b, x, p, S(stream));
         ILUG_CUDA(cudaStreamSynchronize(S(stream)));
         if (iterations) *iterations = r.iterations;
         if (final_relres) *final_relres = r.final_relres;
@@ -765,7 +765,8 @@ long long ilug_dist_plan_sends(const ilug_dist_plan* p, int q, long long* rows) 
 int ilug_dist_plan_matrix(const ilug_dist_plan* p, int which, iluamg_matrix** out) {
     return guarded([&] {
         need(p && out);
-        *out = new iluamg_matrix_s{which == 0 ? p->plan.A_ext : p->plan.A_diag, "dist"};
+        if (which < 0 || which > 2) ilug::fail_invalid("plan matrix: which must be 0 (ext), 1 (diag) or 2 (off)");
+        *out = new iluamg_matrix_s{which == 0 ? p->plan.A_ext : which == 1 ? p->plan.A_diag : p->plan.A_off, "dist"};
         return ILUAMG_OK;
     });
 }
@@ -780,14 +781,29 @@ int ilug_dist_unique_id(char* out128) {
 int ilug_dist_comm_create(int nranks, int rank, const char* id128, ilug_dist_comm** out) {
     return guarded([&] {
         need(id128 && out);
-        auto* c = new ilug_dist_comm_s();
-        try {
-            c->c = std::make_unique<ilug::DistComm>(nranks, rank, id128);
-        } catch (...) {
-            delete c;
-            throw;
-        }
-        *out = c;
+        *out = new ilug_dist_comm_s{std::make_unique<ilug::DistComm>(ilug::make_nccl_transport(nranks, rank, id128))};
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_group_create(int nranks, ilug_dist_group** out) {
+    return guarded([&] {
+        need(out);
+        *out = new ilug_dist_group_s{std::make_shared<ilug::LocalGroup>(nranks)};
+        return ILUAMG_OK;
+    });
+}
+void ilug_dist_group_free(ilug_dist_group* g) { delete g; }
+int ilug_dist_comm_create_local(ilug_dist_group* g, int rank, ilug_dist_comm** out) {
+    return guarded([&] {
+        need(g && out);
+        *out = new ilug_dist_comm_s{std::make_unique<ilug::DistComm>(ilug::make_local_transport(g->g, rank))};
+        return ILUAMG_OK;
+    });
+}
+int ilug_dist_plan_exchange(ilug_dist_plan* p, const ilug_dist_comm* c) {
+    return guarded([&] {
+        need(p && c);
+        ilug::plan_exchange(p->plan, *c->c->t);
         return ILUAMG_OK;
     });
 }

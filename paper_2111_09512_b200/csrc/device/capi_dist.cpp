@@ -9,13 +9,12 @@ int capi_guarded(const std::function<int()>& fn); // capi.cpp: exception -> stat
 
 extern "C" {
 
-int ilug_dist_solver_create(const ilug_dist_plan* p, const ilug_dist_comm* c, const iluamg_config* cfg,
-                            ilug_dist_solver** out) {
+int ilug_dist_solver_create(const ilug_hierarchy* h, const ilug_dist_comm* c, ilug_dist_solver** out) {
     return ilug::capi_guarded([&] {
-        if (!p || !c || !cfg || !out) ilug::fail_invalid("null argument");
+        if (!h || !c || !out) ilug::fail_invalid("null argument");
         auto* s = new ilug_dist_solver_s();
         try {
-            s->s.build(p->plan, *c->c, ilug::amg_params_from(cfg->cfg), cfg->cfg.get_bool("device.graph"), nullptr);
+            s->s.build(h->h, *c->c, nullptr);
         } catch (...) {
             delete s;
             throw;
@@ -32,6 +31,8 @@ int ilug_dist_gmres(ilug_dist_solver* s, const iluamg_config* cfg, const double*
         const auto& c = cfg->cfg;
         ilug::KrylovParams p;
         p.flexible = c.get("krylov.method") == "fgmres";
+        if (!p.flexible && c.get("krylov.method") != "gmres")
+            ilug::fail_invalid("config: krylov.method must be gmres or fgmres");
         p.restart = c.get_index("krylov.restart");
         p.max_iters = c.get_index("krylov.max_iters");
         p.tol = c.get_double("krylov.tol");
@@ -47,7 +48,58 @@ int ilug_dist_gmres(ilug_dist_solver* s, const iluamg_config* cfg, const double*
     });
 }
 
+int ilug_dist_vcycle(ilug_dist_solver* s, const double* r, double* z, void* stream) {
+    return ilug::capi_guarded([&] {
+        if (!s || !r || !z) ilug::fail_invalid("null argument");
+        s->s.vcycle(r, z, static_cast<cudaStream_t>(stream));
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_dist_solver_info(const ilug_dist_solver* s, long long* row0, long long* nloc, int* levels) {
+    return ilug::capi_guarded([&] {
+        if (!s) ilug::fail_invalid("null argument");
+        if (row0) *row0 = s->s.row0();
+        if (nloc) *nloc = s->s.nloc();
+        if (levels) *levels = s->s.levels();
+        return ILUAMG_OK;
+    });
+}
+
 int ilug_dist_solver_levels(const ilug_dist_solver* s) { return s ? s->s.levels() : -1; }
+
+int ilug_dist_level_plans(const ilug_hierarchy* h, int nranks, int rank, ilug_dist_levels** out) {
+    return ilug::capi_guarded([&] {
+        if (!h || !out) ilug::fail_invalid("null argument");
+        *out = new ilug_dist_levels_s{ilug::dist_level_plans(h->h, nranks, rank)};
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_dist_levels_count(const ilug_dist_levels* l) { return l ? static_cast<int>(l->levels.size()) : -1; }
+
+int ilug_dist_levels_plan(const ilug_dist_levels* l, int k, int which, ilug_dist_plan** out) {
+    return ilug::capi_guarded([&] {
+        if (!l || !out) ilug::fail_invalid("null argument");
+        if (k < 0 || k >= static_cast<int>(l->levels.size())) ilug::fail_invalid("level out of range");
+        const ilug::DistLevelPlan& d = l->levels[k];
+        if (which < 0 || which > 2 || (d.last && which > 0))
+            ilug::fail_invalid("which: 0 = A, 1 = R, 2 = P (R/P of the last smoothed level are not halo plans)");
+        *out = new ilug_dist_plan_s{which == 0 ? d.A : which == 1 ? d.R : d.P};
+        return ILUAMG_OK;
+    });
+}
+
+int ilug_dist_levels_last(const ilug_dist_levels* l, int which, iluamg_matrix** out) {
+    return ilug::capi_guarded([&] {
+        if (!l || !out || l->levels.empty()) ilug::fail_invalid("null argument or no smoothed level");
+        const ilug::DistLevelPlan& d = l->levels.back();
+        *out = new iluamg_matrix_s{which == 0 ? ilug::csr_copy(d.R_full) : ilug::csr_copy(d.P_rows), "dist"};
+        return ILUAMG_OK;
+    });
+}
+
+void ilug_dist_levels_free(ilug_dist_levels* l) { delete l; }
 
 int ilug_dist_smooth_host(const ilug_dist_smoother* s, const double* bh, double* xh) {
     return ilug::capi_guarded([&] {

@@ -58,6 +58,9 @@ struct ilug_dist_plan_s {
 struct ilug_dist_comm_s {
     std::unique_ptr<ilug::DistComm> c;
 };
+struct ilug_dist_group_s {
+    std::shared_ptr<ilug::LocalGroup> g;
+};
 struct ilug_dist_smoother_s {
     ilug::DistSmoother s;
     long long nnz_A = 0;
@@ -66,4 +69,7 @@ struct ilug_dist_smoother_s {
 };
 struct ilug_dist_solver_s {
     ilug::DistSolver s;
+};
+struct ilug_dist_levels_s {
+    std::vector<ilug::DistLevelPlan> levels;
 };

@@ -154,7 +154,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     // timed solve: the V-cycle graph and the GMRES basis (multi-GB at C2)
     dh.prepare_graph();
     GmresWork gw;
-    if (kp.restart >= 1 && kp.restart <= 63) gw.ensure(A.nrows, kp.restart, kp.flexible); // else gmres reports it
+    if (kp.restart >= 1) gw.ensure(A.nrows, kp.restart, kp.flexible, kp.max_iters); // else gmres reports it
     oc.setup_seconds = since(t0);
 
     const i64 n = A.nrows;
@@ -170,7 +170,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     const bool late_anorm = !kp.form_iterates && !kp.nrbe_criterion;
     if (late_anorm) kpr.estimate_anorm = false;
     const auto t1 = std::chrono::steady_clock::now();
-    oc.kr = device_gmres(dh.A0(), A, dh, db.p, dx.p, kpr, st, nullptr, &gw);
+    oc.kr = device_gmres(dh.A0(), &A, vcycle_of(dh), db.p, dx.p, kpr, st, nullptr, &gw);
     ILUG_CUDA(cudaStreamSynchronize(st));
     oc.solve_seconds = since(t1);
     oc.x.resize(static_cast<size_t>(n));

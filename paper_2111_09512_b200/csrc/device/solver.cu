@@ -21,13 +21,13 @@ void DeviceMatrix::build(const Csr& host, const i64* rp, const i32* ci, const do
 void DeviceMatrix::residual(const double* x, const double* b, double* r, cudaStream_t st) const {
     if (!halo) return ilug::residual(A, x, b, r, st);
     halo->exchange(x, st);
-    residual_split(A, x, halo->halo.p, n, b, r, st);
+    residual_split(A, x, halo->halo.p, halo->nloc, b, r, st);
 }
 
 void DeviceMatrix::spmv(const double* x, double* y, cudaStream_t st) const {
     if (!halo) return ilug::spmv(A, x, y, st);
     halo->exchange(x, st);
-    spmv_split(A, x, halo->halo.p, n, y, st);
+    spmv_split(A, x, halo->halo.p, halo->nloc, y, st);
 }
 
 // ============================================================ DeviceIlu (K1-K5)
@@ -255,14 +255,15 @@ Vec inverted_diag(const Csr& A, const char* what) {
 } // namespace
 
 void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg,
-                           cudaStream_t st, DevFactors* pre) {
+                           cudaStream_t st, DevFactors* pre, const HaloPlan* dist) {
     if (cfg.sweeps < 0) fail_invalid("build_smoother_state: sweeps must be >= 0");
     if (cfg.poly_degree < 0) fail_invalid("build_smoother_state: poly_degree must be >= 0");
     cfg_ = cfg;
     n_ = A.nrows;
     A_ = &dA;
-    if (dA.halo && cfg.kind != SmootherKind::ilu)
-        fail_invalid("distributed smoothing: only the (block-Jacobi) ILU smoother is distributed");
+    if (dA.halo && (!dist || cfg.kind == SmootherKind::schur_ilut))
+        fail_invalid(dist ? "distributed smoothing: schur_ilut runs as its own distributed smoother"
+                          : "distributed smoothing: the rank's halo plan is required");
     switch (cfg.kind) {
     case SmootherKind::jacobi: {
         const Vec d = inverted_diag(A, "jacobi");
@@ -271,8 +272,9 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
     }
     case SmootherKind::l1_jacobi: {
         Vec d(static_cast<size_t>(n_), 0.0);
+        const Csr& rows = dist ? dist->A_ext : A; // the whole row, in its global entry order
         for (i64 i = 0; i < n_; ++i)
-            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k) d[i] += std::abs(A.v[k]);
+            for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k) d[i] += std::abs(rows.v[k]);
         for (i64 i = 0; i < n_; ++i) {
             if (d[i] == 0.0)
                 fail_numeric("l1_jacobi: row " + std::to_string(i) + " is entirely zero");
@@ -288,6 +290,7 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
                 fail_numeric("gauss_seidel_sweep: zero diagonal at row " + std::to_string(i));
         gs_ = std::make_unique<LevelPlan>();
         gs_->build(A, LevelPlan::Kind::gauss_seidel, st);
+        if (dist) sell_from_host(Aoff_, dist->A_off, Part::all, st); // hybrid GS: off-block part
         break;
     }
     case SmootherKind::poly_gs: {
@@ -419,18 +422,35 @@ void DeviceSmoother::smooth(const double* b, double* x, bool x_zero, cudaStream_
         switch (cfg_.kind) {
         case SmootherKind::jacobi:
         case SmootherKind::l1_jacobi:
-            residual_scale_step(A_->A, x, b, invd_.p, ws_.p, st);
+            if (const HaloExchange* h = A_->halo) {
+                h->exchange(x, st);
+                residual_scale_step_split(A_->A, x, h->halo.p, h->nloc, b, invd_.p, ws_.p, st);
+            } else {
+                residual_scale_step(A_->A, x, b, invd_.p, ws_.p, st);
+            }
             vec_copy(x, ws_.p, n, st);
             break;
         case SmootherKind::gauss_seidel:
-            gs_->solve(b, ws_.p, x, st);
+            if (const HaloExchange* h = A_->halo) {
+                // hybrid GS: b' = b - A_off x (current halo), then GS on the diagonal block
+                h->exchange(x, st);
+                residual_split(Aoff_, x, h->halo.p, h->nloc, b, ws_.p + n, st);
+                gs_->solve(ws_.p + n, ws_.p, x, st);
+            } else {
+                gs_->solve(b, ws_.p, x, st);
+            }
             vec_copy(x, ws_.p, n, st);
             break;
         case SmootherKind::poly_gs: {
             double* t0 = ws_.p;
             double* t1 = ws_.p + n;
             double* acc = ws_.p + 2 * n;
-            residual_scale_init(A_->A, x, b, invd_.p, t0, acc, st);
+            if (const HaloExchange* h = A_->halo) {
+                h->exchange(x, st);
+                residual_scale_init_split(A_->A, x, h->halo.p, h->nloc, b, invd_.p, t0, acc, st);
+            } else {
+                residual_scale_init(A_->A, x, b, invd_.p, t0, acc, st);
+            }
             for (i64 j = 1; j <= cfg_.poly_degree; ++j) {
                 neg_scale_acc(Lstrict_, t0, invd_.p, t1, acc, st);
                 std::swap(t0, t1);

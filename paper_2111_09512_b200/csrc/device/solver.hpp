@@ -10,6 +10,7 @@
 #pragma once
 
 #include "../host/amg.hpp"
+#include "../host/dist.hpp"
 #include "../host/schur.hpp"
 #include "../kernels/ilu0.hpp"
 #include "../kernels/levelset.hpp"
@@ -17,15 +18,18 @@
 #include "spsv_cusparse.hpp"
 
 #include <deque>
+#include <functional>
 #include <memory>
 
 namespace ilug {
 
+class Transport;
+
 /// Device side of a HaloPlan (host/dist.hpp): packs the rows other ranks need
-/// and exchanges them with NCCL point-to-point in one group (device/dist.cu).
+/// and hands the segments to the job's transport (device/dist.cu).
 struct HaloExchange {
-    void* comm = nullptr; ///< ncclComm_t
-    i64 nloc = 0, nhalo = 0;
+    const Transport* tr = nullptr;
+    i64 nloc = 0, nhalo = 0; ///< owned columns (split point of the extended operator), halo entries
     std::vector<i64> recv_ranks, recv_offsets, send_ranks, send_offsets;
     DBuf<i32> send_idx;
     mutable DBuf<double> sendbuf, halo;
@@ -149,8 +153,11 @@ private:
 class DeviceSmoother {
 public:
     /// `pre`: factors of A computed ahead (moved from; ILU kinds only).
+    /// `dist`: dA holds a rank's rows of a distributed operator (dA.halo set) —
+    /// A is then the plan's diagonal block and the smoother is its rank-local
+    /// form (block-Jacobi ILU / poly-GS, hybrid GS, global Jacobi / l1).
     void build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg, cudaStream_t st,
-               DevFactors* pre = nullptr);
+               DevFactors* pre = nullptr, const HaloPlan* dist = nullptr);
     /// x <- smooth(A, b, x). `x_zero`: caller guarantees x == 0 on entry, so the
     /// first residual is b itself (bitwise what the SpMV would give).
     void smooth(const double* b, double* x, bool x_zero, cudaStream_t st) const;
@@ -169,6 +176,7 @@ private:
     std::unique_ptr<DeviceSchur> schur_;
     std::unique_ptr<LevelPlan> gs_;
     Sell Lstrict_;               // poly_gs
+    Sell Aoff_;                  // hybrid GS: the rows' off-block entries (halo columns)
     DBuf<double> invd_;          // jacobi / l1 / poly_gs
     mutable DBuf<double> ws_;    // workspace (r, y ping-pong, bs, x ping-pong)
 };
@@ -253,8 +261,9 @@ struct KrylovReport {
     i64 vcycles = 0;
 };
 
-/// Right-preconditioned (F)GMRES on the device, CGS2 orthogonalisation.
-/// Host work per iteration: Givens rotations on (j+2) scalars.
+/// Right-preconditioned (F)GMRES on the device, CGS2 orthogonalisation; the
+/// Hessenberg/Givens/solve_y scalars stay on the device (one status read per
+/// iteration for the convergence test), any restart >= 1.
 struct DistComm;
 /// comm != nullptr: A holds this rank's rows (halo-exchanged SpMV), vectors are
 /// rank-local, every reduction is summed over ranks (NCCL allreduce), and M is
@@ -262,12 +271,26 @@ struct DistComm;
 /// GMRES work vectors (basis V, flexible Z, temporaries): allocated at setup
 /// by solve_with so the multi-GB basis allocation is not inside the timed solve.
 struct GmresWork {
-    DBuf<double> V, Z, w, r, xk, xc, vy, mz, ydev;
-    void ensure(i64 n, i64 restart, bool flexible);
+    DBuf<double> V, Z, w, r, xk, xc, vy, mz;
+    DBuf<double> S, hist, ws; ///< device scalars (H, rotations, g, y), history norms, reductions
+    double* stat = nullptr;   ///< pinned host status (8 doubles)
+    i64 R_ = 0;
+    GmresWork() = default;
+    GmresWork(const GmresWork&) = delete;
+    GmresWork& operator=(const GmresWork&) = delete;
+    ~GmresWork();
+    void ensure(i64 n, i64 restart, bool flexible, i64 max_iters = 200);
 };
-KrylovReport device_gmres(const DeviceMatrix& A, const Csr& A_host, DeviceHierarchy& M,
+/// The preconditioner z = M(r) (the reference's LinearOperator,
+/// include/iluamg/krylov.hpp:20): a V-cycle on this stream.
+using Preconditioner = std::function<void(const double* r, double* z, cudaStream_t st)>;
+/// A_host: the operator on the host for the |A|_2 power iteration (null: not estimated).
+KrylovReport device_gmres(const DeviceMatrix& A, const Csr* A_host, const Preconditioner& M,
                           const double* b_dev, double* x_dev, const KrylovParams& p, cudaStream_t st,
                           const DistComm* comm = nullptr, GmresWork* work = nullptr);
+inline Preconditioner vcycle_of(DeviceHierarchy& H) {
+    return [&H](const double* r, double* z, cudaStream_t st) { H.vcycle(r, z, st); };
+}
 
 /// 50-step power iteration on A^T A (src/krylov.cpp:14-28) on the device.
 double device_estimate_two_norm(const DeviceMatrix& A, const Csr& A_host, i64 steps,

@@ -4,8 +4,8 @@
 
 namespace ilug {
 
-RowPartition row_partition(i64 n, i64 p) {
-    if (p < 1 || p > std::max<i64>(n, 1)) fail_invalid("row_partition: rank count out of range");
+RowPartition row_partition(i64 n, i64 p, bool allow_empty) {
+    if (p < 1 || (!allow_empty && p > std::max<i64>(n, 1))) fail_invalid("row_partition: rank count out of range");
     RowPartition part;
     part.n = n;
     part.p = p;
@@ -20,7 +20,8 @@ i64 RowPartition::owner(i64 row) const {
     return static_cast<i64>(it - starts.begin()) - 1;
 }
 
-HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) {
+namespace {
+HaloPlan make_plan(const Csr& rows, const RowPartition& part, i64 rank, bool square) {
     if (rank < 0 || rank >= part.p) fail_invalid("halo_plan: rank out of range");
     HaloPlan h;
     h.rank = rank;
@@ -28,7 +29,7 @@ HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) {
     h.row0 = part.starts[rank];
     h.row1 = part.starts[rank + 1];
     h.nloc = h.row1 - h.row0;
-    if (rows.nrows != h.nloc) fail_invalid("halo_plan: local row count does not match the partition");
+    if (square && rows.nrows != h.nloc) fail_invalid("halo_plan: local row count does not match the partition");
     // halo = sorted unique off-range columns (contiguous ranges => grouped by owner)
     for (i64 k = 0; k < rows.nnz(); ++k) {
         const i64 j = rows.ci[k];
@@ -47,28 +48,93 @@ HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) {
     h.recv_offsets.push_back(h.nhalo);
 
     // extended matrix: same entry order, renumbered columns
-    h.A_ext.nrows = h.nloc;
+    const i64 nr = rows.nrows;
+    h.A_ext.nrows = nr;
     h.A_ext.ncols = h.nloc + h.nhalo;
     h.A_ext.rp = rows.rp;
     h.A_ext.ci.resize(rows.ci.size());
     h.A_ext.v = rows.v;
-    h.A_diag.nrows = h.A_diag.ncols = h.nloc;
-    h.A_diag.rp.assign(static_cast<size_t>(h.nloc) + 1, 0);
-    for (i64 i = 0; i < h.nloc; ++i) {
+    if (square) {
+        h.A_diag.nrows = h.A_diag.ncols = h.nloc;
+        h.A_diag.rp.assign(static_cast<size_t>(h.nloc) + 1, 0);
+        h.A_off.nrows = h.nloc;
+        h.A_off.ncols = h.nloc + h.nhalo;
+        h.A_off.rp.assign(static_cast<size_t>(h.nloc) + 1, 0);
+    }
+    for (i64 i = 0; i < nr; ++i) {
         for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k) {
             const i64 j = rows.ci[k];
             if (j >= h.row0 && j < h.row1) {
                 h.A_ext.ci[k] = static_cast<i32>(j - h.row0);
-                h.A_diag.ci.push_back(static_cast<i32>(j - h.row0));
-                h.A_diag.v.push_back(rows.v[k]);
+                if (square) {
+                    h.A_diag.ci.push_back(static_cast<i32>(j - h.row0));
+                    h.A_diag.v.push_back(rows.v[k]);
+                }
             } else {
                 const auto it = std::lower_bound(h.halo_global.begin(), h.halo_global.end(), j);
                 h.A_ext.ci[k] = static_cast<i32>(h.nloc + (it - h.halo_global.begin()));
+                if (square) {
+                    h.A_off.ci.push_back(h.A_ext.ci[k]);
+                    h.A_off.v.push_back(rows.v[k]);
+                }
             }
         }
-        h.A_diag.rp[i + 1] = static_cast<i64>(h.A_diag.ci.size());
+        if (square) {
+            h.A_diag.rp[i + 1] = static_cast<i64>(h.A_diag.ci.size());
+            h.A_off.rp[i + 1] = static_cast<i64>(h.A_off.ci.size());
+        }
     }
     return h;
+}
+} // namespace
+
+HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) { return make_plan(rows, part, rank, true); }
+
+HaloPlan halo_plan_rect(const Csr& rows, const RowPartition& cols, i64 rank) {
+    return make_plan(rows, cols, rank, false);
+}
+
+Csr csr_row_block(const Csr& M, i64 r0, i64 r1) {
+    if (r0 < 0 || r1 < r0 || r1 > M.nrows) fail_invalid("csr_row_block: row range out of bounds");
+    Csr B;
+    B.nrows = r1 - r0;
+    B.ncols = M.ncols;
+    B.rp.resize(static_cast<size_t>(B.nrows) + 1);
+    const i64 base = M.rp[r0];
+    for (i64 i = 0; i <= B.nrows; ++i) B.rp[i] = M.rp[r0 + i] - base;
+    B.ci.assign(M.ci.begin() + base, M.ci.begin() + M.rp[r1]);
+    B.v.assign(M.v.begin() + base, M.v.begin() + M.rp[r1]);
+    return B;
+}
+
+std::vector<DistLevelPlan> dist_level_plans(const HostHierarchy& h, i64 nranks, i64 rank) {
+    const i64 L = h.num_levels();
+    std::vector<DistLevelPlan> out;
+    if (L < 2) return out; // a single level is the replicated coarse solve
+    out.resize(static_cast<size_t>(L - 1));
+    std::vector<RowPartition> parts;
+    for (i64 k = 0; k < L; ++k) parts.push_back(row_partition(h.levels[k].A.nrows, nranks, true));
+    for (i64 k = 0; k + 1 < L; ++k) {
+        const HostLevel& hl = h.levels[k];
+        DistLevelPlan& d = out[k];
+        d.n = hl.A.nrows;
+        d.part = parts[k];
+        if (d.n < nranks)
+            fail_invalid("distributed AMG: level " + std::to_string(k) + " has " + std::to_string(d.n) +
+                         " rows for " + std::to_string(nranks) + " ranks (raise amg.coarse_size)");
+        const i64 f0 = d.part.starts[rank], f1 = d.part.starts[rank + 1];
+        d.A = halo_plan(csr_row_block(hl.A, f0, f1), d.part, rank);
+        d.last = k + 2 == L;
+        if (d.last) {
+            d.R_full = csr_copy(hl.R);
+            d.P_rows = csr_row_block(hl.P, f0, f1);
+        } else {
+            const RowPartition& cp = parts[k + 1];
+            d.R = halo_plan_rect(csr_row_block(hl.R, cp.starts[rank], cp.starts[rank + 1]), d.part, rank);
+            d.P = halo_plan_rect(csr_row_block(hl.P, f0, f1), cp, rank);
+        }
+    }
+    return out;
 }
 
 std::vector<i64> halo_requests(const HaloPlan& h, i64 q) {

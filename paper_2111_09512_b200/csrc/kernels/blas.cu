@@ -15,7 +15,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kRows = 4;                 // rows per thread in the tiled reductions
 constexpr int kTile = kBlock * kRows;    // rows per block
-constexpr int kMaxVec = 64;              // max basis vectors per fused call (restart <= 63)
+constexpr int kMaxVec = 64;              // dot outputs per pass of the fused CGS2 kernels
 
 inline unsigned ew_grid(i64 n) {
     const i64 g = (n + kBlock - 1) / kBlock;
@@ -44,6 +44,14 @@ __global__ void k_scale_div(double* o, const double* w, double h, i64 n) {
          i += static_cast<i64>(gridDim.x) * blockDim.x)
         o[i] = w[i] / h;
 }
+// out = w / *h, skipped when *h == 0 (GMRES happy breakdown leaves v_{j+1} unset)
+__global__ void k_scale_div_dev(double* o, const double* w, const double* h, i64 n) {
+    const double hv = *h;
+    if (hv == 0.0) return;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x)
+        o[i] = w[i] / hv;
+}
 __global__ void k_sub_into(double* __restrict__ o, const double* __restrict__ a,
                            const double* __restrict__ b, i64 n) {
     for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
@@ -64,22 +72,21 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // Sum `per` values of thread-local partials for k outputs over the block:
-// red[w][j] per warp, then warps summed in order by thread j.
+// red[w][j] per warp, then warps summed in order by thread j. Any k: the
+// outputs are produced in chunks of kMaxVec (the per-row axpy of MODE 3/4
+// always covers all k vectors before any dot is taken, so chunking the
+// outputs does not change a bit); partials are written with stride pstride.
 template <int MODE>
 __global__ void __launch_bounds__(kBlock)
 k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ hin,
-        double* __restrict__ w, const double* __restrict__ w2, i64 n, double* __restrict__ partial) {
+        double* __restrict__ w, const double* __restrict__ w2, i64 n, double* __restrict__ partial,
+        i64 pstride) {
     // MODE 0: dot(w, w2) -> 1 output; MODE 1: ||w||^2; MODE 2: V^T w (k outputs);
     // MODE 3: w -= V hin, then V^T w; MODE 4: w -= V hin, then ||w||^2;
     // MODE 5: sum_i (w_i - h v_i)^2 with h = hin[0], v = w2 (Schur h21^2).
     __shared__ double red[kBlock / 32][kMaxVec];
-    __shared__ double hs[kMaxVec];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const i64 base = blockIdx.x * static_cast<i64>(kTile) + threadIdx.x;
-    if (MODE == 3 || MODE == 4) {
-        for (int j = threadIdx.x; j < k; j += blockDim.x) hs[j] = hin[j];
-        __syncthreads();
-    }
     double wv[kRows];
 #pragma unroll
     for (int u = 0; u < kRows; ++u) {
@@ -88,7 +95,7 @@ k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ 
     }
     if (MODE == 3 || MODE == 4) {
         for (int j = 0; j < k; ++j) {
-            const double hj = hs[j];
+            const double hj = __ldg(hin + j); // uniform address: one broadcast per warp
 #pragma unroll
             for (int u = 0; u < kRows; ++u) {
                 const i64 i = base + u * kBlock;
@@ -101,8 +108,7 @@ k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ 
             if (i < n) w[i] = wv[u];
         }
     }
-    int nout = 1;
-    if (MODE == 0 || MODE == 1 || MODE == 4 || MODE == 5) {
+    if constexpr (MODE == 0 || MODE == 1 || MODE == 4 || MODE == 5) {
         double s = 0.0;
         const double h = MODE == 5 ? hin[0] : 0.0;
 #pragma unroll
@@ -118,34 +124,43 @@ k_tiled(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ 
         }
         s = warp_sum(s);
         if (lane == 0) red[warp][0] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < kBlock / 32; ++q) t += red[q][0];
+            partial[blockIdx.x * pstride] = t;
+        }
     } else {
-        nout = k;
-        for (int j = 0; j < k; ++j) {
+    for (int j0 = 0; j0 < k; j0 += kMaxVec) {
+        const int kc = min(kMaxVec, k - j0);
+        for (int j = 0; j < kc; ++j) {
             double s = 0.0;
 #pragma unroll
             for (int u = 0; u < kRows; ++u) {
                 const i64 i = base + u * kBlock;
-                if (i < n) s += V[j * ld + i] * wv[u];
+                if (i < n) s += V[(j0 + j) * ld + i] * wv[u];
             }
             s = warp_sum(s);
             if (lane == 0) red[warp][j] = s;
         }
+        __syncthreads();
+        for (int j = threadIdx.x; j < kc; j += blockDim.x) {
+            double s = 0.0;
+            for (int q = 0; q < kBlock / 32; ++q) s += red[q][j];
+            partial[blockIdx.x * pstride + j0 + j] = s;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < nout; j += blockDim.x) {
-        double s = 0.0;
-        for (int q = 0; q < kBlock / 32; ++q) s += red[q][j];
-        partial[blockIdx.x * static_cast<i64>(kMaxVec) + j] = s;
     }
 }
 
 // out[j] = sum over blocks b (in order, tree within one block) of partial[b][j]
-__global__ void k_finish(const double* __restrict__ partial, i64 nblocks, int nout,
+__global__ void k_finish(const double* __restrict__ partial, i64 nblocks, int nout, i64 pstride,
                          double* __restrict__ out) {
     __shared__ double sm[kBlock];
     for (int j = 0; j < nout; ++j) {
         double s = 0.0;
-        for (i64 b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[b * kMaxVec + j];
+        for (i64 b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[b * pstride + j];
         sm[threadIdx.x] = s;
         __syncthreads();
         for (int o = kBlock / 2; o > 0; o >>= 1) {
@@ -157,15 +172,13 @@ __global__ void k_finish(const double* __restrict__ partial, i64 nblocks, int no
     }
 }
 
+// y = base + sum_j c_j V_j, any k (c read through the uniform-address path)
 __global__ void k_combine(const double* __restrict__ V, i64 ld, int k, const double* __restrict__ c,
                           const double* __restrict__ base, double* __restrict__ y, i64 n) {
-    __shared__ double cs[kMaxVec];
-    for (int j = threadIdx.x; j < k; j += blockDim.x) cs[j] = c[j];
-    __syncthreads();
     for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<i64>(gridDim.x) * blockDim.x) {
         double s = base ? base[i] : 0.0;
-        for (int j = 0; j < k; ++j) s = s + cs[j] * V[j * ld + i];
+        for (int j = 0; j < k; ++j) s = s + __ldg(c + j) * V[j * ld + i];
         y[i] = s;
     }
 }
@@ -176,12 +189,12 @@ __global__ void k_combine(const double* __restrict__ V, i64 ld, int k, const dou
 template <int MODE>
 void tiled(const double* V, i64 ld, int k, const double* hin, double* w, const double* w2, i64 n,
            double* out, int nout, double* ws, cudaStream_t st) {
-    if (k > kMaxVec) fail_invalid("CGS2: more than 64 basis vectors per call");
     if (!ws) fail_invalid("reduction: no workspace");
     const i64 nb = std::max<i64>(1, (n + kTile - 1) / kTile);
-    k_tiled<MODE><<<static_cast<unsigned>(nb), kBlock, 0, st>>>(V, ld, k, hin, w, w2, n, ws);
+    const i64 pstride = std::max<i64>(kMaxVec, nout); // reduce_ws_doubles(n, k) covers nb * pstride
+    k_tiled<MODE><<<static_cast<unsigned>(nb), kBlock, 0, st>>>(V, ld, k, hin, w, w2, n, ws, pstride);
     ILUG_LAUNCH_CHECK();
-    k_finish<<<1, kBlock, 0, st>>>(ws, nb, nout, out);
+    k_finish<<<1, kBlock, 0, st>>>(ws, nb, nout, pstride, out);
     ILUG_LAUNCH_CHECK();
 }
 
@@ -240,6 +253,11 @@ void vec_scale_div(double* o, const double* w, double h, i64 n, cudaStream_t st)
     k_scale_div<<<ew_grid(n), kBlock, 0, st>>>(o, w, h, n);
     ILUG_LAUNCH_CHECK();
 }
+void vec_scale_div_dev(double* o, const double* w, const double* h, i64 n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_scale_div_dev<<<ew_grid(n), kBlock, 0, st>>>(o, w, h, n);
+    ILUG_LAUNCH_CHECK();
+}
 void vec_add_into(double* o, const double* a, const double* b, i64 n, cudaStream_t st) {
     if (n <= 0) return;
     k_add_into<<<ew_grid(n), kBlock, 0, st>>>(o, a, b, n);
@@ -250,7 +268,9 @@ void vec_sub_into(double* o, const double* a, const double* b, i64 n, cudaStream
     k_sub_into<<<ew_grid(n), kBlock, 0, st>>>(o, a, b, n);
     ILUG_LAUNCH_CHECK();
 }
-i64 reduce_ws_doubles(i64 n) { return std::max<i64>(1, (n + kTile - 1) / kTile) * kMaxVec; }
+i64 reduce_ws_doubles(i64 n, i64 k) {
+    return std::max<i64>(1, (n + kTile - 1) / kTile) * std::max<i64>(kMaxVec, k);
+}
 void dot_dev(const double* a, const double* b, i64 n, double* out, double* ws, cudaStream_t st) {
     tiled<0>(nullptr, 0, 0, nullptr, const_cast<double*>(a), b, n, out, 1, ws, st);
 }
@@ -275,7 +295,6 @@ void multi_axpy_nrm(const double* V, i64 ld, int k, const double* hin, double* w
 void multi_combine(const double* V, i64 ld, int k, const double* c, const double* base, double* y,
                    i64 n, cudaStream_t st) {
     if (n <= 0) return;
-    if (k > kMaxVec) fail_invalid("combine: more than 64 basis vectors");
     k_combine<<<ew_grid(n), kBlock, 0, st>>>(V, ld, k, c, base, y, n);
     ILUG_LAUNCH_CHECK();
 }

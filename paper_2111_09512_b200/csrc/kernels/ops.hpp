@@ -45,6 +45,12 @@ void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st);    
 void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
                     cudaStream_t st);
 void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st);
+/// Split forms of the fused smoother epilogues (distributed rows: columns >= nloc read the halo)
+void spmv_add_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* acc, cudaStream_t st);
+void residual_scale_step_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
+                               const double* scale, double* out, cudaStream_t st);
+void residual_scale_init_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
+                               const double* scale, double* term, double* acc, cudaStream_t st);
 void residual(const Sell& M, const double* x, const double* b, double* r, cudaStream_t st); // r = b - s
 /// out = (rhs - s) / div
 void sweep_div(const Sell& M, const double* x, const double* rhs, const double* div, double* out,
@@ -81,13 +87,16 @@ void vec_div(double* out, const double* a, const double* d, i64 n, cudaStream_t 
 void vec_acc(double* x, const double* z, i64 n, cudaStream_t st);                      // x += z
 void vec_acc_div(double* x, const double* z, const double* d, i64 n, cudaStream_t st); // x += z / d
 void vec_scale_div(double* out, const double* w, double h, i64 n, cudaStream_t st);    // out = w / h
+/// out = w / *h with h in device memory; no-op when *h == 0
+void vec_scale_div_dev(double* out, const double* w, const double* h, i64 n, cudaStream_t st);
 void vec_add_into(double* out, const double* a, const double* b, i64 n, cudaStream_t st); // out = a + b
 void vec_sub_into(double* out, const double* a, const double* b, i64 n, cudaStream_t st); // out = a - b
 
 /// Deterministic reductions: fixed grid, per-block partial sums, ordered final pass.
 /// Results are written to device memory (out[0..]); `ws` is caller-owned device
-/// workspace of reduce_ws_doubles(n) doubles (one in-flight reduction per ws).
-i64 reduce_ws_doubles(i64 n);
+/// workspace of reduce_ws_doubles(n, k) doubles (one in-flight reduction per ws;
+/// k = the widest multi-output call it serves, any k >= 1).
+i64 reduce_ws_doubles(i64 n, i64 k = 64);
 void dot_dev(const double* a, const double* b, i64 n, double* out, double* ws, cudaStream_t st);
 void nrm2sq_dev(const double* a, i64 n, double* out, double* ws, cudaStream_t st);
 /// out = sum_i (w_i - h v_i)^2 with the scalar h read from device memory

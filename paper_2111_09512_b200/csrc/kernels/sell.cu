@@ -770,18 +770,32 @@ Csr sell_to_host(const Sell& M) {
 void spmv(const Sell& M, const double* x, double* y, cudaStream_t st) {
     launch_rowdot(M, x, EpiStore{y}, st);
 }
-void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
-                    cudaStream_t st) {
+namespace {
+template <class Epi>
+void launch_split(const Sell& M, const double* x, const double* halo, i64 nloc, Epi epi, cudaStream_t st) {
     if (M.nrows_pad == 0) return;
-    k_rowdot_split<EpiResidual><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, halo,
-                                                                          static_cast<i32>(nloc), EpiResidual{b, r});
+    k_rowdot_split<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, halo,
+                                                                  static_cast<i32>(nloc), epi);
     ILUG_LAUNCH_CHECK();
 }
+} // namespace
+void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
+                    cudaStream_t st) {
+    launch_split(M, x, halo, nloc, EpiResidual{b, r}, st);
+}
 void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st) {
-    if (M.nrows_pad == 0) return;
-    k_rowdot_split<EpiStore><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, halo,
-                                                                       static_cast<i32>(nloc), EpiStore{y});
-    ILUG_LAUNCH_CHECK();
+    launch_split(M, x, halo, nloc, EpiStore{y}, st);
+}
+void spmv_add_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* acc, cudaStream_t st) {
+    launch_split(M, x, halo, nloc, EpiAdd{acc}, st);
+}
+void residual_scale_step_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
+                               const double* scale, double* out, cudaStream_t st) {
+    launch_split(M, x, halo, nloc, EpiScaleAcc{rhs, scale, x, out}, st);
+}
+void residual_scale_init_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
+                               const double* scale, double* term, double* acc, cudaStream_t st) {
+    launch_split(M, x, halo, nloc, EpiScaleInit{rhs, scale, term, acc}, st);
 }
 void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st) {
     launch_rowdot(M, x, EpiAdd{acc}, st);

@@ -143,3 +143,150 @@ def test_partition_rule():
     assert idist.partition(16, 4).tolist() == [0, 4, 8, 12, 16]
     with pytest.raises(Exception):
         idist.partition(3, 0)
+
+
+# ---------------------------------------------------------------------------
+# Distributed V-cycle host logic: every rank builds the global
+# host hierarchy, takes its per-level plans from ilug_dist_level_plans
+# (A_k / P_k rows by the level's partition, R_k rows by the next level's),
+# completes the send lists over gloo, and runs the V-cycle with the C port's
+# products on its extended matrices and gloo halo exchanges. Jacobi smoothing
+# (a global smoother: no block approximation), the last smoothed level's
+# residual all-reduced into the whole coarse rhs. Compared with the composed
+# single-process oracle (oracle/_ref ref_dist_vcycle at p ranks).
+
+def _halo(plan, world, rank, x_loc):
+    """Exchange the entries of x_loc other ranks read; return this rank's halo."""
+    reqs = []
+    for p in range(world):
+        if p != rank:
+            send = plan.sends(p)
+            if len(send):
+                reqs.append(dist.isend(torch.from_numpy(x_loc[send].copy()), dst=p))
+    halo = np.empty(plan.nhalo)
+    off = 0
+    for p in range(world):
+        if p != rank:
+            need = plan.requests(p)
+            if len(need):
+                buf = torch.empty(len(need), dtype=torch.float64)
+                dist.recv(buf, src=p)
+                halo[off:off + len(need)] = buf.numpy()
+                off += len(need)
+    for rq in reqs:
+        rq.wait()
+    return halo
+
+
+def _vcycle_worker(rank, world, port, spec, kv, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2111_09512_b200 as ilug
+        from paper_2111_09512_b200 import dist as idist
+        from oracle import oracle
+        P = oracle.Port()
+
+        def all_gather(obj):
+            out = [None] * world
+            dist.all_gather_object(out, obj)
+            return out
+
+        A = ilug.Matrix.generate(spec)
+        H = ilug.Hierarchy(A, ilug.Config().update(kv), host_only=True)
+        L = H.levels
+        LP = idist.LevelPlans(H, world, rank)
+        assert LP.count == L - 1
+        lev = []
+        for k in range(L - 1):
+            d = {"A": LP.plan(k, "A")}
+            d["A"].exchange_requests(all_gather)
+            last = k == L - 2
+            if not last:
+                for w in ("R", "P"):
+                    d[w] = LP.plan(k, w)
+                    d[w].exchange_requests(all_gather)
+            else:
+                d["R_full"] = LP.last("R").csr()
+                d["P_rows"] = LP.last("P").csr()
+            Aext = d["A"].matrix("ext").csr()
+            diag = np.zeros(d["A"].row1 - d["A"].row0)
+            drp, dci, dv = d["A"].matrix("diag").csr()
+            for i in range(len(diag)):
+                for t in range(drp[i], drp[i + 1]):
+                    if dci[t] == i:
+                        diag[i] = dv[t]
+            d["Aext"], d["invd"], d["last"] = Aext, 1.0 / diag, last
+            d["n"] = H.level_matrix(k, "A").rows
+            lev.append(d)
+        Ac = H.level_matrix(L - 1, "A")
+        crp, cci, cv = Ac.csr()
+        Cd = np.zeros((Ac.rows, Ac.rows))
+        for i in range(Ac.rows):
+            Cd[i, cci[crp[i]:crp[i + 1]]] = cv[crp[i]:crp[i + 1]]
+        sweeps = int(kv.get("smoother.sweeps", 2))
+
+        def smooth(d, b, x):
+            for _ in range(sweeps):
+                xe = np.concatenate([x, _halo(d["A"], world, rank, x)])
+                x = x + d["invd"] * (b - P.spmv(d["Aext"], xe))
+            return x
+
+        def cycle(k, b, x):
+            d = lev[k]
+            x = smooth(d, b, x)
+            r = P.residual(d["Aext"], np.concatenate([x, _halo(d["A"], world, rank, x)]), b)
+            if not d["last"]:
+                rc = P.spmv(d["R"].matrix("ext").csr(), np.concatenate([r, _halo(d["R"], world, rank, r)]))
+                e = np.zeros(lev[k + 1]["A"].row1 - lev[k + 1]["A"].row0)
+                e = cycle(k + 1, rc, e)
+                x = x + P.spmv(d["P"].matrix("ext").csr(), np.concatenate([e, _halo(d["P"], world, rank, e)]))
+            else:
+                full = torch.zeros(d["n"], dtype=torch.float64)
+                full[d["A"].row0:d["A"].row1] = torch.from_numpy(r)
+                dist.all_reduce(full)
+                bc = P.spmv(d["R_full"], full.numpy())
+                xc = np.linalg.solve(Cd, bc)
+                x = x + P.spmv(d["P_rows"], xc)
+            return smooth(d, b, x)
+
+        n = A.rows
+        r_glob = np.random.default_rng(31).uniform(-1, 1, n)
+        p0 = lev[0]["A"]
+        z = cycle(0, r_glob[p0.row0:p0.row1].copy(), np.zeros(p0.row1 - p0.row0))
+        zs = all_gather((p0.row0, z))
+        zfull = np.concatenate([t[1] for t in sorted(zs, key=lambda t: t[0])])
+        R = oracle.Ref()
+        Ar = R.mat(*A.csr())
+        want = R.dist_vcycle(R.dist_setup(Ar, R.cfg(kv), world), r_glob, np.zeros(n))
+        err = np.linalg.norm(zfull - want) / np.linalg.norm(want)
+        assert err < 1e-12, f"distributed V-cycle differs from the composed oracle: {err}"
+        q.put((rank, "ok"))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("spec", ["poisson3d(10,10,9)", "pressure27(9,9,8)"])
+def test_distributed_vcycle_plans_gloo(world, spec):
+    from oracle import oracle
+    if not os.path.exists(oracle.REF_SO):
+        pytest.skip("oracle/_ref not built")
+    kv = {"smoother.kind": "jacobi", "smoother.fallback.kind": "jacobi", "amg.coarsening": "pmis"}
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vcycle_worker, args=(r, world, port, spec, kv, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert results[r] == "ok", results[r]

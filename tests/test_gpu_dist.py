@@ -1,9 +1,20 @@
-"""GPU, one rank: the distributed objects (halo plan, NCCL communicator,
-block-Jacobi smoother, distributed GMRES+AMG) reduce exactly to the
-single-GPU path when there is one rank — same kernels, same order — so they
-are bitwise / iteration-exact against it. (More than one rank cannot run on
-this one-GPU pool; the multi-rank host logic is covered by
-tests/test_distributed.py with gloo.)"""
+"""GPU: the row-block distributed solve phase at p = 1, 2, 4, 8
+ranks against the composed oracle.
+
+The ranks run as host threads of this process on the one GPU, joined by the
+in-process transport (ilug_dist_group: every collective synchronises the
+caller's stream and meets at a host barrier, so no kernel waits on another
+rank's kernel). The data path is the one the NCCL ranks run — halo plans,
+pack kernels, split-gather products, rank-local smoothers, the all-gathered
+coarsest solve, summed GMRES reductions — only the transport differs.
+
+Oracle: oracle/_ref's ref_dist_* = the reference hierarchy with every level's
+smoother state rebuilt from the block-diagonal part (block-Jacobi ILU factors
+of blockdiag(A_k), block poly-GS, hybrid GS = residual with the off-block part
+then gauss_seidel_sweep on the blocks) and cycle_level restated around them.
+  * V-cycle and smoother: BITWISE (global entry order in every product).
+  * GMRES: iterations +-1 (the reductions are summed per rank, then over ranks).
+"""
 import numpy as np
 import pytest
 
@@ -11,95 +22,160 @@ from conftest import bitwise
 
 pytestmark = pytest.mark.gpu
 
-KV = {"smoother.kind": "ilu", "ilu.variant": "ilut", "trisolve.m_lower": "5", "trisolve.m_upper": "5",
-      "krylov.tol": "1e-8", "amg.coarsening": "pmis", "smoother.fallback.kind": "poly_gs"}
+BASE = {"amg.coarsening": "pmis", "krylov.tol": "1e-8"}
+CASES = [
+    # C4-like: ILU(0) block-Jacobi on the finest level, hybrid GS below
+    ("poisson3d(20,20,20)", {"smoother.kind": "ilu", "trisolve.m_lower": "5", "trisolve.m_upper": "5"}),
+    # C2-like: ILUT, poly-GS fallback
+    ("pressure27(14,14,14)", {"smoother.kind": "ilu", "ilu.variant": "ilut", "trisolve.m_lower": "5",
+                              "trisolve.m_upper": "5", "smoother.fallback.kind": "poly_gs"}),
+    # direct triangular solves, row/col scaling, W-cycle, l1-Jacobi below
+    ("cutcell(12,12,12)", {"smoother.kind": "ilu", "trisolve.mode": "direct", "scaling": "row_col",
+                           "amg.cycles_nu": "2", "smoother.fallback.kind": "l1_jacobi"}),
+    # no ILU: Jacobi everywhere (global), two smoothed levels of GS
+    ("poisson3d(16,16,12)", {"smoother.kind": "gauss_seidel", "smoother.levels": "2",
+                             "smoother.fallback.kind": "jacobi"}),
+]
 
 
-def _setup(ilug, spec):
+def _ranks(ilug, torch, spec, kv, p, body):
     from paper_2111_09512_b200 import dist as idist
     A = ilug.Matrix.generate(spec)
-    rows = idist.generate_rows(spec, 0, A.rows)
-    plan = idist.Plan(rows, A.rows, 1, 0)
-    comm = idist.Comm(1, 0, idist.unique_id())
-    return idist, A, plan, comm
+    cfg = ilug.Config().update(dict(BASE, **kv))
+    H = ilug.Hierarchy(A, cfg, host_only=True)
+    group = idist.LocalGroup(p)
+
+    def rank_fn(r):
+        comm = group.comm(r)
+        S = idist.Solver(H, comm)
+        st = torch.cuda.Stream()
+        return body(r, S, cfg, st)
+    return A, cfg, idist.run_ranks(p, rank_fn)
 
 
-@pytest.mark.parametrize("spec", ["pressure27(16,16,16)", "poisson3d(20,20,20)"])
-def test_dist_smoother_single_rank_bitwise(ilug, torch_cuda, spec):
-    idist, A, plan, comm = _setup(ilug, spec)
-    assert plan.nhalo == 0
-    cfg = ilug.Config().update(KV)
-    Sd = idist.Smoother(plan, comm, cfg)
-    S = ilug.Smoother(A, cfg)
-    rng = np.random.default_rng(3)
-    b = torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).cuda()
-    x0 = torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).cuda()
-    x1, x2 = x0.clone(), x0.clone()
-    Sd.smooth(b, x1)
-    S.smooth(b, x2)
-    torch_cuda.cuda.synchronize()
-    assert bitwise(x1.cpu().numpy(), x2.cpu().numpy())
-    r = torch_cuda.empty_like(b)
-    Sd.residual(x1, b, r)
-    D = ilug.DeviceMatrix(A)
-    r2 = torch_cuda.empty_like(b)
-    D.residual(x1, b, r2)
-    torch_cuda.cuda.synchronize()
-    assert bitwise(r.cpu().numpy(), r2.cpu().numpy())
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("spec,kv", CASES, ids=[c[0] for c in CASES])
+def test_dist_vcycle_bitwise(ilug, ref, torch_cuda, spec, kv, p):
+    torch = torch_cuda
+    n = ilug.Matrix.generate(spec).rows
+    r = np.random.default_rng(17).uniform(-1, 1, n)
+
+    def body(rank, S, cfg, st):
+        rl = torch.from_numpy(r[S.row0:S.row0 + S.nloc].copy()).cuda()
+        z = torch.empty_like(rl)
+        torch.cuda.synchronize()
+        for _ in range(2):  # repeated cycles reuse every buffer
+            S.vcycle(rl, z, stream=st)
+        st.synchronize()
+        return S.row0, z.cpu().numpy(), S.levels
+
+    A, cfg, out = _ranks(ilug, torch, spec, kv, p, body)
+    z = np.concatenate([o[1] for o in sorted(out, key=lambda o: o[0])])
+    Ar = ref.mat(*A.csr())
+    d = ref.dist_setup(Ar, ref.cfg(dict(BASE, **kv)), p)
+    assert out[0][2] == ref.L.ref_dist_nlevels(d)
+    want = ref.dist_vcycle(d, r, np.zeros(n))
+    assert bitwise(z, want), f"max diff {np.abs(z - want).max()}"
+    if p == 1:  # one rank: the composed oracle is the reference V-cycle itself
+        assert bitwise(z, ref.vcycle(ref.amg(Ar, ref.cfg(dict(BASE, **kv))), r, np.zeros(n)))
 
 
-def test_dist_gmres_single_rank_matches(ilug, torch_cuda):
-    idist, A, plan, comm = _setup(ilug, "pressure27(20,20,20)")
-    cfg = ilug.Config().update(dict(KV, **{"krylov.form_iterates": "false"}))
-    Sol = idist.Solver(plan, comm, cfg)
-    D = ilug.DeviceMatrix(A)
-    ones = torch_cuda.ones(A.rows, dtype=torch_cuda.float64, device="cuda")
-    b = torch_cuda.empty_like(ones)
-    D.spmv(ones, b)
-    x = torch_cuda.zeros_like(ones)
-    out = Sol.gmres(cfg, b, x)
-    H = ilug.Hierarchy(A, cfg)
-    x2 = torch_cuda.zeros_like(ones)
-    want = H.gmres(cfg, b, x2)
-    assert out["status"] == 0 and out["iterations"] == want["iterations"]
-    assert out["final_relres"] == want["final_relres"]
-    assert float((x - 1).abs().max()) < 1e-5
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("spec,kv", CASES[:2], ids=[c[0] for c in CASES[:2]])
+def test_dist_gmres_iterations(ilug, ref, torch_cuda, spec, kv, p):
+    torch = torch_cuda
+    A0 = ilug.Matrix.generate(spec)
+    n = A0.rows
+    b = np.random.default_rng(23).uniform(-1, 1, n)
+
+    def body(rank, S, cfg, st):
+        bl = torch.from_numpy(b[S.row0:S.row0 + S.nloc].copy()).cuda()
+        x = torch.zeros_like(bl)
+        torch.cuda.synchronize()
+        res = S.gmres(cfg, bl, x, stream=st)
+        st.synchronize()
+        return S.row0, x.cpu().numpy(), res
+
+    A, cfg, out = _ranks(ilug, torch, spec, kv, p, body)
+    its = {o[2]["iterations"] for o in out}
+    assert len(its) == 1, "ranks disagree on the iteration count"
+    got = its.pop()
+    Ar = ref.mat(*A.csr())
+    want = ref.dist_krylov(Ar, ref.dist_setup(Ar, ref.cfg(dict(BASE, **kv)), p), ref.cfg(dict(BASE, **kv)), b)
+    assert want["converged"]
+    assert abs(got - want["iterations"]) <= 1, f"{got} vs composed reference {want['iterations']}"
+    assert all(o[2]["status"] == 0 and o[2]["final_relres"] < 1e-8 for o in out)
+    x = np.concatenate([o[1] for o in sorted(out, key=lambda o: o[0])])
+    r = ref.residual(Ar, x, b)
+    assert np.linalg.norm(r) / np.linalg.norm(b) < 1e-8
 
 
-def test_dist_plan_two_virtual_ranks_structure(ilug):
-    """Two ranks' plans built in one process: requests of one are exactly what
-    the other can serve, and the extended matrices keep the global entry order."""
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("kind", ["ilu", "gauss_seidel", "poly_gs", "l1_jacobi"])
+def test_dist_smoother_bitwise(ilug, ref, torch_cuda, kind, p):
+    """ilug_dist_smoother (the bench's N > 1 object) = the composed level-0 smoother."""
     from paper_2111_09512_b200 import dist as idist
-    spec = "pressure27(10,10,8)"
+    torch = torch_cuda
+    spec = "pressure27(12,12,10)"
+    kv = dict(BASE, **{"smoother.kind": kind, "ilu.variant": "ilut", "trisolve.m_lower": "4",
+                       "trisolve.m_upper": "6"})
     A = ilug.Matrix.generate(spec)
-    starts = idist.partition(A.rows, 2)
-    plans = [idist.Plan(idist.generate_rows(spec, int(starts[r]), int(starts[r + 1])), A.rows, 2, r)
-             for r in range(2)]
-    need01 = plans[0].requests(1)
-    need10 = plans[1].requests(0)
-    assert len(need01) == plans[0].nhalo and len(need10) == plans[1].nhalo
-    assert need01.min() >= starts[1] and need10.max() < starts[1]
-    plans[1].set_sends(0, need01)
-    plans[0].set_sends(1, need10)
-    assert np.array_equal(plans[1].sends(0) + starts[1], need01)
+    n = A.rows
+    cfg = ilug.Config().update(kv)
+    rng = np.random.default_rng(4)
+    b, x0 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    starts = idist.partition(n, p)
+    group = idist.LocalGroup(p)
+
+    def rank_fn(r):
+        comm = group.comm(r)
+        r0, r1 = int(starts[r]), int(starts[r + 1])
+        plan = idist.Plan(idist.generate_rows(spec, r0, r1), n, p, r)
+        plan.exchange(comm)
+        S = idist.Smoother(plan, comm, cfg)
+        xl = torch.from_numpy(x0[r0:r1].copy()).cuda()
+        bl = torch.from_numpy(b[r0:r1].copy()).cuda()
+        torch.cuda.synchronize()
+        S.smooth(bl, xl)
+        torch.cuda.synchronize()
+        return r0, xl.cpu().numpy()
+
+    out = idist.run_ranks(p, rank_fn)
+    got = np.concatenate([o[1] for o in sorted(out, key=lambda o: o[0])])
+    Ar = ref.mat(*A.csr())
+    want = ref.dist_smooth(ref.dist_setup(Ar, ref.cfg(kv), p), 0, b, x0)
+    assert bitwise(got, want)
 
 
-def test_dist_smooth_host_many_single_rank(ilug, torch_cuda):
-    """ilug_dist_smooth_host_many at one rank = the single-GPU smoother applied
-    to each host pair, bitwise."""
-    idist, A, plan, comm = _setup(ilug, "pressure27(14,14,14)")
-    cfg = ilug.Config().update(KV)
-    Sd = idist.Smoother(plan, comm, cfg)
-    S = ilug.Smoother(A, cfg)
-    rng = np.random.default_rng(8)
-    bs = [rng.uniform(-1, 1, A.rows) for _ in range(3)]
-    xs = [rng.uniform(-1, 1, A.rows) for _ in range(3)]
-    want = []
-    for b, x in zip(bs, xs):
-        xd = torch_cuda.from_numpy(x.copy()).cuda()
-        S.smooth(torch_cuda.from_numpy(b).cuda(), xd)
-        torch_cuda.cuda.synchronize()
-        want.append(xd.cpu().numpy())
-    Sd.smooth_host_many(bs, xs)
-    for got, w in zip(xs, want):
-        assert bitwise(got, w)
+def test_dist_smooth_host_many_two_ranks(ilug, ref, torch_cuda):
+    """The bench's host-buffer pipeline at 2 ranks = the composed smoother per step."""
+    from paper_2111_09512_b200 import dist as idist
+    torch = torch_cuda
+    spec, p = "poisson3d(14,14,12)", 2
+    kv = dict(BASE, **{"smoother.kind": "ilu", "trisolve.m_lower": "5", "trisolve.m_upper": "5"})
+    A = ilug.Matrix.generate(spec)
+    n = A.rows
+    cfg = ilug.Config().update(kv)
+    rng = np.random.default_rng(9)
+    bs = [rng.uniform(-1, 1, n) for _ in range(3)]
+    xs = [rng.uniform(-1, 1, n) for _ in range(3)]
+    starts = idist.partition(n, p)
+    group = idist.LocalGroup(p)
+
+    def rank_fn(r):
+        comm = group.comm(r)
+        r0, r1 = int(starts[r]), int(starts[r + 1])
+        plan = idist.Plan(idist.generate_rows(spec, r0, r1), n, p, r)
+        plan.exchange(comm)
+        S = idist.Smoother(plan, comm, cfg)
+        bl = [bb[r0:r1].copy() for bb in bs]
+        xl = [xx[r0:r1].copy() for xx in xs]
+        S.smooth_host_many(bl, xl)
+        return r0, xl
+
+    out = sorted(idist.run_ranks(p, rank_fn), key=lambda o: o[0])
+    Ar = ref.mat(*A.csr())
+    d = ref.dist_setup(Ar, ref.cfg(kv), p)
+    for i in range(3):
+        got = np.concatenate([o[1][i] for o in out])
+        assert bitwise(got, ref.dist_smooth(d, 0, bs[i], xs[i]))

@@ -89,6 +89,11 @@ SOLVES = [
     ("poisson2d(32,32)", dict(ILU, **{"krylov.method": "fgmres"})),
     ("poisson2d(32,32)", dict(ILU, **{"krylov.criterion": "nrbe"})),
     ("poisson2d(40,40)", dict(ILU, **{"krylov.restart": 5})),
+    # basis wider than one 64-vector CGS2 pass, and a restart inside the run
+    # (the device scalar path takes any restart, like gmres_impl)
+    ("anisotropic2d(64,64,0.01)", {"smoother.kind": "jacobi", "krylov.restart": 100, "krylov.tol": "1e-10"}),
+    ("poisson2d(128,128)", {"amg.max_levels": 4, "smoother.kind": "jacobi", "krylov.restart": 80,
+                            "krylov.tol": "1e-12", "krylov.method": "fgmres"}),
 ]
 
 
