@@ -227,6 +227,8 @@ ILUAMG_API int ilug_dist_comm_create(int nranks, int rank, const char* id128, il
 typedef struct ilug_dist_group_s ilug_dist_group;
 ILUAMG_API int ilug_dist_group_create(int nranks, ilug_dist_group** out);
 ILUAMG_API void ilug_dist_group_free(ilug_dist_group* g);
+/* A rank that failed releases the others: every pending and later collective of the group fails. */
+ILUAMG_API void ilug_dist_group_abort(ilug_dist_group* g);
 ILUAMG_API int ilug_dist_comm_create_local(ilug_dist_group* g, int rank, ilug_dist_comm** out);
 /* Complete a plan's send lists over the communicator (collective; replaces
  * the caller-side request exchange). */

@@ -480,8 +480,10 @@ API int ref_dist_setup(const void* A, const void* cfg, int p, void** outp) {
                 st = build_smoother_state(Ak, sc);
                 st.strict_lower = std::get<0>(split_triangular(blk));
                 break;
-            case SmootherKind::schur_ilut:
-                fail_invalid("ref_dist_setup: schur_ilut has its own distributed form");
+            case SmootherKind::schur_ilut: // block b = rank b: the reference's own Schur smoother
+                if (sc.schur_blocks != p) fail_invalid("ref_dist_setup: schur.blocks must equal the rank count");
+                st = build_smoother_state(Ak, sc);
+                break;
             default:
                 st = build_smoother_state(Ak, sc);
             }

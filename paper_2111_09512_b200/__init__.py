@@ -101,6 +101,7 @@ _SIGS = {
     "ilug_dist_unique_id": (_i, [_vp]),
     "ilug_dist_comm_create": (_i, [_i, _i, _vp, _pvp]),
     "ilug_dist_group_create": (_i, [_i, _pvp]), "ilug_dist_group_free": (None, [_vp]),
+    "ilug_dist_group_abort": (None, [_vp]),
     "ilug_dist_comm_create_local": (_i, [_vp, _i, _pvp]),
     "ilug_dist_plan_exchange": (_i, [_vp, _vp]),
     "ilug_dist_allreduce_sum": (_i, [_vp, _vp, _ll, _vp]),

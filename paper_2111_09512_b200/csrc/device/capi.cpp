@@ -793,6 +793,9 @@ int ilug_dist_group_create(int nranks, ilug_dist_group** out) {
     });
 }
 void ilug_dist_group_free(ilug_dist_group* g) { delete g; }
+void ilug_dist_group_abort(ilug_dist_group* g) {
+    if (g) g->g->abort();
+}
 int ilug_dist_comm_create_local(ilug_dist_group* g, int rank, ilug_dist_comm** out) {
     return guarded([&] {
         need(g && out);

@@ -90,10 +90,10 @@ public:
     ~NcclTransport() override {
         if (comm_) nccl().CommDestroy(comm_);
     }
-    void allreduce_sum(double* buf, i64 count, cudaStream_t st) override {
+    void allreduce_sum(double* buf, i64 count, cudaStream_t st) const override {
         ILUG_NCCL(nccl().AllReduce(buf, buf, static_cast<size_t>(count), ncclDouble, ncclSum, comm_, st));
     }
-    void exchange(const HaloExchange& hx, cudaStream_t st) override {
+    void exchange(const HaloExchange& hx, cudaStream_t st) const override {
         if (hx.send_ranks.empty() && hx.recv_ranks.empty()) return;
         ILUG_NCCL(nccl().GroupStart());
         for (size_t k = 0; k < hx.send_ranks.size(); ++k)
@@ -106,7 +106,7 @@ public:
                                   static_cast<int>(hx.recv_ranks[k]), comm_, st));
         ILUG_NCCL(nccl().GroupEnd());
     }
-    std::vector<std::vector<char>> allgather(const std::vector<char>& mine) override {
+    std::vector<std::vector<char>> allgather(const std::vector<char>& mine) const override {
         // lengths, then the payloads padded to the longest (setup only)
         DBuf<i64> lens(nranks);
         const i64 my = static_cast<i64>(mine.size());
@@ -137,7 +137,7 @@ public:
         rank = r;
         if (r < 0 || r >= nranks) fail_invalid("local transport: rank out of range");
     }
-    void allreduce_sum(double* buf, i64 count, cudaStream_t st) override {
+    void allreduce_sum(double* buf, i64 count, cudaStream_t st) const override {
         // every rank sums the same staged copies in rank order: identical results
         auto& mine = g_->stage[static_cast<size_t>(rank)];
         mine.resize(static_cast<size_t>(count));
@@ -154,7 +154,7 @@ public:
         ILUG_CUDA(cudaMemcpyAsync(buf, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, st));
         ILUG_CUDA(cudaStreamSynchronize(st));
     }
-    void exchange(const HaloExchange& hx, cudaStream_t st) override {
+    void exchange(const HaloExchange& hx, cudaStream_t st) const override {
         ILUG_CUDA(cudaStreamSynchronize(st)); // the pack kernel has written sendbuf
         g_->slot[static_cast<size_t>(rank)] = &hx;
         g_->barrier();
@@ -171,7 +171,7 @@ public:
         ILUG_CUDA(cudaStreamSynchronize(st));
         g_->barrier(); // nobody repacks its send buffer before every peer has copied it
     }
-    std::vector<std::vector<char>> allgather(const std::vector<char>& mine) override {
+    std::vector<std::vector<char>> allgather(const std::vector<char>& mine) const override {
         g_->slot[static_cast<size_t>(rank)] = &mine;
         g_->barrier();
         std::vector<std::vector<char>> out;
@@ -216,6 +216,7 @@ LocalGroup::LocalGroup(int nranks) : slot(static_cast<size_t>(nranks)), stage(st
 
 void LocalGroup::barrier() {
     std::unique_lock<std::mutex> l(m_);
+    if (aborted_) fail_invalid("local rank group aborted: another rank failed");
     const unsigned long long g = gen_;
     if (++arrived_ == p_) {
         arrived_ = 0;
@@ -223,7 +224,14 @@ void LocalGroup::barrier() {
         cv_.notify_all();
         return;
     }
-    cv_.wait(l, [&] { return gen_ != g; });
+    cv_.wait(l, [&] { return gen_ != g || aborted_; });
+    if (gen_ == g) fail_invalid("local rank group aborted: another rank failed");
+}
+
+void LocalGroup::abort() {
+    std::lock_guard<std::mutex> l(m_);
+    aborted_ = true;
+    cv_.notify_all();
 }
 
 std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalGroup> g, int rank) {
@@ -237,10 +245,10 @@ void HaloExchange::exchange(const double* x, cudaStream_t st) const {
         k_pack<<<g, 256, 0, st>>>(ns, send_idx.p, x, sendbuf.p);
         ILUG_LAUNCH_CHECK();
     }
-    if (tr && tr->nranks > 1) const_cast<Transport*>(tr)->exchange(*this, st);
+    if (tr && tr->nranks > 1) tr->exchange(*this, st);
 }
 
-void plan_exchange(HaloPlan& plan, Transport& t) {
+void plan_exchange(HaloPlan& plan, const Transport& t) {
     if (t.nranks != plan.nranks || t.rank != plan.rank) fail_invalid("plan exchange: plan and transport ranks differ");
     // message: for every destination q: count, then the global ids wanted from q
     std::vector<char> mine;
@@ -268,17 +276,25 @@ void plan_exchange(HaloPlan& plan, Transport& t) {
     }
 }
 
+void HaloExchange::setup(const HaloPlan& plan, const Transport& t, cudaStream_t st) {
+    tr = &t;
+    nloc = plan.nloc;
+    nhalo = plan.nhalo;
+    recv_ranks = plan.recv_ranks;
+    recv_offsets = plan.recv_offsets;
+    send_ranks = plan.send_ranks;
+    send_offsets = plan.send_offsets;
+    send_idx.upload(plan.send_local.data(), static_cast<i64>(plan.send_local.size()), st);
+    sendbuf.alloc(static_cast<i64>(plan.send_local.size()));
+    halo.alloc(std::max<i64>(plan.nhalo, 1));
+}
+
+void transport_allreduce(const Transport* t, double* buf, i64 count, cudaStream_t st) {
+    if (t && t->nranks > 1) t->allreduce_sum(buf, count, st);
+}
+
 void DistOperator::build(const HaloPlan& plan, const Transport& t, cudaStream_t st) {
-    hx.tr = &t;
-    hx.nloc = plan.nloc;
-    hx.nhalo = plan.nhalo;
-    hx.recv_ranks = plan.recv_ranks;
-    hx.recv_offsets = plan.recv_offsets;
-    hx.send_ranks = plan.send_ranks;
-    hx.send_offsets = plan.send_offsets;
-    hx.send_idx.upload(plan.send_local.data(), static_cast<i64>(plan.send_local.size()), st);
-    hx.sendbuf.alloc(static_cast<i64>(plan.send_local.size()));
-    hx.halo.alloc(std::max<i64>(plan.nhalo, 1));
+    hx.setup(plan, t, st);
     M.build(plan.A_ext, st);
     M.n = plan.A_ext.nrows;
     M.halo = &hx;
@@ -296,7 +312,7 @@ void DistSmoother::build(const HaloPlan& plan, const DistComm& comm, const Smoot
 // ---------------------------------------------------------------- hierarchy
 void DistHierarchy::build(const HostHierarchy& h, const DistComm& comm, cudaStream_t st) {
     comm_ = &comm;
-    Transport& t = *comm.t;
+    const Transport& t = *comm.t;
     const int L = static_cast<int>(h.num_levels());
     if (L < 1) fail_invalid("distributed AMG: empty hierarchy");
     nlev_ = L;

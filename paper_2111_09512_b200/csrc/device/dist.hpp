@@ -39,11 +39,11 @@ class Transport {
 public:
     virtual ~Transport() = default;
     int nranks = 1, rank = 0;
-    virtual void allreduce_sum(double* buf, i64 count, cudaStream_t st) = 0;
+    virtual void allreduce_sum(double* buf, i64 count, cudaStream_t st) const = 0;
     /// hx.sendbuf segments to hx.send_ranks; hx.halo segments from hx.recv_ranks
-    virtual void exchange(const HaloExchange& hx, cudaStream_t st) = 0;
+    virtual void exchange(const HaloExchange& hx, cudaStream_t st) const = 0;
     /// every rank's byte string, in rank order (host, blocking, collective)
-    virtual std::vector<std::vector<char>> allgather(const std::vector<char>& mine) = 0;
+    virtual std::vector<std::vector<char>> allgather(const std::vector<char>& mine) const = 0;
 };
 
 std::unique_ptr<Transport> make_nccl_transport(int nranks, int rank, const char id[128]);
@@ -53,7 +53,9 @@ class LocalGroup {
 public:
     explicit LocalGroup(int nranks);
     int size() const { return p_; }
+    /// Throws once abort() was called: a rank that failed releases the others.
     void barrier();
+    void abort();
     std::vector<const void*> slot;    ///< per-rank published pointer of the current collective
     std::vector<std::vector<double>> stage; ///< per-rank host staging (allreduce)
 
@@ -63,6 +65,7 @@ private:
     std::condition_variable cv_;
     int arrived_ = 0;
     unsigned long long gen_ = 0;
+    bool aborted_ = false;
 };
 std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalGroup> g, int rank);
 
@@ -80,7 +83,7 @@ struct DistComm {
 
 /// Complete a plan's send lists over the transport (collective): every rank
 /// learns which of its rows the others read.
-void plan_exchange(HaloPlan& plan, Transport& t);
+void plan_exchange(HaloPlan& plan, const Transport& t);
 
 /// Device side of a plan: pack buffers, halo buffer, the extended operator.
 struct DistOperator {

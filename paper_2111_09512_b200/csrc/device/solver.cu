@@ -261,9 +261,7 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
     cfg_ = cfg;
     n_ = A.nrows;
     A_ = &dA;
-    if (dA.halo && (!dist || cfg.kind == SmootherKind::schur_ilut))
-        fail_invalid(dist ? "distributed smoothing: schur_ilut runs as its own distributed smoother"
-                          : "distributed smoothing: the rank's halo plan is required");
+    if (dA.halo && !dist) fail_invalid("distributed smoothing: the rank's halo plan is required");
     switch (cfg.kind) {
     case SmootherKind::jacobi: {
         const Vec d = inverted_diag(A, "jacobi");
@@ -310,7 +308,10 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
     }
     case SmootherKind::schur_ilut:
         schur_ = std::make_unique<DeviceSchur>();
-        schur_->build(A, cfg, st);
+        if (dist)
+            schur_->build_dist(*dist, *dA.halo->tr, cfg, st); // block b = rank b
+        else
+            schur_->build(A, cfg, st);
         break;
     }
     // r, y ping-pong, bs, x ping-pong, spare; then the wavefront intermediates

@@ -33,8 +33,11 @@ struct HaloExchange {
     std::vector<i64> recv_ranks, recv_offsets, send_ranks, send_offsets;
     DBuf<i32> send_idx;
     mutable DBuf<double> sendbuf, halo;
+    void setup(const HaloPlan& plan, const Transport& t, cudaStream_t st);
     void exchange(const double* x_local, cudaStream_t st) const;
 };
+/// Sum over the transport's ranks (no-op for null / one rank).
+void transport_allreduce(const Transport* t, double* buf, i64 count, cudaStream_t st);
 
 /// Device copy of an operator. With a halo, the rows are a rank's rows of a
 /// distributed matrix whose columns >= n index the halo buffer.
@@ -134,6 +137,10 @@ private:
 class DeviceSchur {
 public:
     void build(const Csr& A, const SmootherConfig& cfg, cudaStream_t st);
+    /// Distributed form (schur.blocks = ranks, block b = rank b's rows): B, E,
+    /// F are block-local; C couples the ranks' interface unknowns (halo
+    /// exchange); beta^2, h11, h21^2 are summed over the ranks (collective).
+    void build_dist(const HaloPlan& A, const Transport& t, const SmootherConfig& cfg, cudaStream_t st);
     /// x <- schur_smooth(A, b, x)
     void apply(const DeviceMatrix& A, const double* b, double* x, cudaStream_t st) const;
     i64 interface_size() const { return nf_; }
@@ -141,10 +148,14 @@ public:
 
 private:
     void block_solve(const double* f, double* out, cudaStream_t st) const;
-    i64 n_ = 0, ni_ = 0, nf_ = 0;
+    void finish_build(const Csr& B, const Csr& E, const Csr& F, const std::vector<i32>& perm, const SmootherConfig& cfg,
+                      cudaStream_t st, SchurSetup* host);
+    i64 n_ = 0, ni_ = 0, nf_ = 0, nf_global_ = 0;
     TriSolveConfig ts_;
     DeviceIlu blocks_;
     Sell E_, F_, C_;
+    const Transport* tr_ = nullptr; // distributed: C's halo exchange and the scalar sums
+    HaloExchange Chx_;
     DBuf<i32> perm_;
     mutable DBuf<double> ws_, red_, scal_;
 };

@@ -155,15 +155,20 @@ class LocalGroup:
     def comm(self, rank: int) -> Comm:
         return Comm(self.nranks, rank, group=self)
 
+    def abort(self) -> None:
+        """Release the other ranks of a failed collective (their calls raise)."""
+        lib.ilug_dist_group_abort(self.h)
+
     def __del__(self):
         if getattr(self, "h", None) and self.h.value and lib is not None:
             lib.ilug_dist_group_free(self.h)
             self.h = C.c_void_p()
 
 
-def run_ranks(nranks: int, fn: Callable[[int], object]) -> List[object]:
+def run_ranks(nranks: int, fn: Callable[[int], object], group: "LocalGroup" = None) -> List[object]:
     """fn(rank) on nranks host threads (ctypes drops the GIL inside the C ABI,
-    so the ranks' collectives meet); exceptions are re-raised."""
+    so the ranks' collectives meet); the first exception aborts the group
+    (the other ranks' pending collectives fail instead of waiting) and is re-raised."""
     import threading
     out: List[object] = [None] * nranks
     err: List[BaseException] = []
@@ -175,6 +180,8 @@ def run_ranks(nranks: int, fn: Callable[[int], object]) -> List[object]:
             out[r] = fn(r)
         except BaseException as e:  # noqa: BLE001
             err.append(e)
+            if group is not None:
+                group.abort()
 
     th = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
     for t in th:

@@ -50,7 +50,7 @@ def _ranks(ilug, torch, spec, kv, p, body):
         S = idist.Solver(H, comm)
         st = torch.cuda.Stream()
         return body(r, S, cfg, st)
-    return A, cfg, idist.run_ranks(p, rank_fn)
+    return A, cfg, idist.run_ranks(p, rank_fn, group)
 
 
 @pytest.mark.parametrize("p", [1, 2, 4, 8])
@@ -140,7 +140,7 @@ def test_dist_smoother_bitwise(ilug, ref, torch_cuda, kind, p):
         torch.cuda.synchronize()
         return r0, xl.cpu().numpy()
 
-    out = idist.run_ranks(p, rank_fn)
+    out = idist.run_ranks(p, rank_fn, group)
     got = np.concatenate([o[1] for o in sorted(out, key=lambda o: o[0])])
     Ar = ref.mat(*A.csr())
     want = ref.dist_smooth(ref.dist_setup(Ar, ref.cfg(kv), p), 0, b, x0)
@@ -173,9 +173,81 @@ def test_dist_smooth_host_many_two_ranks(ilug, ref, torch_cuda):
         S.smooth_host_many(bl, xl)
         return r0, xl
 
-    out = sorted(idist.run_ranks(p, rank_fn), key=lambda o: o[0])
+    out = sorted(idist.run_ranks(p, rank_fn, group), key=lambda o: o[0])
     Ar = ref.mat(*A.csr())
     d = ref.dist_setup(Ar, ref.cfg(kv), p)
     for i in range(3):
         got = np.concatenate([o[1][i] for o in out])
         assert bitwise(got, ref.dist_smooth(d, 0, bs[i], xs[i]))
+
+
+SCHUR = {"smoother.kind": "schur_ilut", "krylov.method": "fgmres", "schur.ilut.droptol": "1e-3",
+         "schur.ilut.lfill": "5", "schur.trisolve.mL": "10", "schur.trisolve.mU": "10"}
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_dist_schur_smoother_matches_reference(ilug, ref, torch_cuda, p):
+    """The ILUT Schur-complement smoother across p ranks (block b = rank b,
+    src/schur.cpp:158-219): B/E/F block-local, C's interface halo exchanged,
+    beta^2 / h11 / h21^2 summed over the ranks — the reference's schur_smooth
+    with p blocks to rounding (the three sums are the only reordering)."""
+    from paper_2111_09512_b200 import dist as idist
+    from conftest import rel_err
+    torch = torch_cuda
+    spec = "pressure27(16,16,16)"
+    kv = dict(BASE, **SCHUR, **{"schur.blocks": str(p)})
+    A = ilug.Matrix.generate(spec)
+    n = A.rows
+    cfg = ilug.Config().update(kv)
+    rng = np.random.default_rng(6)
+    b, x0 = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    starts = idist.partition(n, p)
+    group = idist.LocalGroup(p)
+
+    def rank_fn(r):
+        comm = group.comm(r)
+        r0, r1 = int(starts[r]), int(starts[r + 1])
+        plan = idist.Plan(idist.generate_rows(spec, r0, r1), n, p, r)
+        plan.exchange(comm)
+        S = idist.Smoother(plan, comm, cfg)
+        xl = torch.from_numpy(x0[r0:r1].copy()).cuda()
+        bl = torch.from_numpy(b[r0:r1].copy()).cuda()
+        torch.cuda.synchronize()
+        S.smooth(bl, xl)
+        torch.cuda.synchronize()
+        return r0, xl.cpu().numpy()
+
+    out = idist.run_ranks(p, rank_fn, group)
+    got = np.concatenate([o[1] for o in sorted(out, key=lambda o: o[0])])
+    Ar = ref.mat(*A.csr())
+    want, _ = ref.smooth(Ar, ref.smoother(Ar, ref.cfg(kv)), b, x0)
+    assert rel_err(got - x0, want - x0) < 1e-12
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_dist_schur_fgmres_iterations(ilug, ref, torch_cuda, p):
+    """C5 (BASELINE configs[4]) in miniature: FGMRES + AMG with the Schur
+    smoother on the finest level across p ranks, iterations +-1 of the
+    composed reference (its Schur smoother with p blocks, block smoothers below)."""
+    torch = torch_cuda
+    spec = "poisson3d(16,16,16)"  # reference: 5 / 8 / 9 / 9 iterations at p = 1 / 2 / 4 / 8
+    kv = dict(SCHUR, **{"schur.blocks": str(p)})
+    A0 = ilug.Matrix.generate(spec)
+    n = A0.rows
+    b = np.random.default_rng(29).uniform(-1, 1, n)
+
+    def body(rank, S, cfg, st):
+        bl = torch.from_numpy(b[S.row0:S.row0 + S.nloc].copy()).cuda()
+        x = torch.zeros_like(bl)
+        torch.cuda.synchronize()
+        res = S.gmres(cfg, bl, x, stream=st)
+        st.synchronize()
+        return S.row0, x.cpu().numpy(), res
+
+    A, cfg, out = _ranks(ilug, torch, spec, kv, p, body)
+    got = out[0][2]["iterations"]
+    assert all(o[2]["iterations"] == got and o[2]["status"] == 0 for o in out)
+    Ar = ref.mat(*A.csr())
+    kvr = dict(BASE, **kv)
+    want = ref.dist_krylov(Ar, ref.dist_setup(Ar, ref.cfg(kvr), p), ref.cfg(kvr), b)
+    assert want["converged"] and abs(got - want["iterations"]) <= 1, f"{got} vs {want['iterations']}"
