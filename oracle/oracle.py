@@ -81,6 +81,8 @@ class Ref:
             "ref_amg_level_mat": (_vp, [_vp, _ll, _i]), "ref_amg_vcycle": (_i, [_vp, _pd, _pd]),
             "ref_amg_operator_complexity": (_d, [_vp]), "ref_amg_free": (None, [_vp]),
             "ref_krylov_solve": (_i, [_vp, _vp, _vp, _pd, _pd, _pll, _pi, _pd, _pd, _ll, _pll, _pd]),
+            "ref_gen3d": (_i, [_i, _ll, _ll, _ll, _u64, _pvp]),
+            "ref_smoother_factor_nnz": (None, [_vp, _pll, _pll, _pll]),
             "ref_dist_setup": (_i, [_vp, _vp, _i, _pvp]), "ref_dist_free": (None, [_vp]),
             "ref_dist_nlevels": (_ll, [_vp]), "ref_dist_vcycle": (_i, [_vp, _pd, _pd]),
             "ref_dist_smooth": (_i, [_vp, _ll, _pd, _pd]),
@@ -126,6 +128,18 @@ class Ref:
     def write(self, h, path):
         """The reference's own Matrix Market writer."""
         self._ok(self.L.ref_mat_write(h, path.encode()))
+
+    def gen3d(self, spec):
+        """Oracle-side 3D generators (poisson3d / pressure27 / cutcell specs, the
+        device build's generator grammar) -> reference SparseMatrix handle."""
+        kind, args = spec.split("(", 1)
+        vals = [a.strip() for a in args.rstrip(")").split(",")]
+        k = {"poisson3d": 0, "pressure27": 1, "cutcell": 2}[kind.strip()]
+        nx, ny, nz = (int(v) for v in vals[:3])
+        seed = int(vals[3]) if len(vals) > 3 else 2111
+        out = C.c_void_p()
+        self._ok(self.L.ref_gen3d(k, nx, ny, nz, seed, C.byref(out)))
+        return out
 
     def generate(self, spec):
         out = C.c_void_p()

@@ -22,6 +22,7 @@
 #include "iluamg/trisolve.hpp"
 
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -92,6 +93,138 @@ API void ref_mat_copy(const void* A, int64_t* rp, int64_t* ci, double* v) {
     std::memcpy(v, M->values.data(), M->values.size() * 8);
 }
 API void ref_mat_free(void* A) { delete static_cast<SparseMatrix*>(A); }
+
+// ---- 3D synthetic inputs of the BASELINE configs ------------
+// The reference ships 2D generators only; these restate the survey's 3D
+// definitions serially on the reference's own hash_unit (include/iluamg/rng.hpp)
+// so the reference arm of bench.py builds its input without loading the
+// product library. tests/test_oracle.py pins them bitwise to the device build's
+// generators. Natural ordering, x fastest; entries in ascending column order.
+namespace {
+struct Rows {
+    std::vector<index_t> rp{0}, ci;
+    std::vector<double> v;
+    void put(index_t j, double x) {
+        ci.push_back(j);
+        v.push_back(x);
+    }
+    void end_row() { rp.push_back(static_cast<index_t>(ci.size())); }
+};
+
+SparseMatrix gen_poisson3d(index_t nx, index_t ny, index_t nz) {
+    const index_t pl = nx * ny, n = pl * nz;
+    Rows R;
+    for (index_t i = 0; i < n; ++i) {
+        const index_t ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
+        if (iz > 0) R.put(i - pl, -1.0);
+        if (iy > 0) R.put(i - nx, -1.0);
+        if (ix > 0) R.put(i - 1, -1.0);
+        R.put(i, 6.0);
+        if (ix + 1 < nx) R.put(i + 1, -1.0);
+        if (iy + 1 < ny) R.put(i + nx, -1.0);
+        if (iz + 1 < nz) R.put(i + pl, -1.0);
+        R.end_row();
+    }
+    return SparseMatrix::from_csr(n, n, std::move(R.rp), std::move(R.ci), std::move(R.v));
+}
+
+// 27-point box; off-diagonal magnitude coef(i, j or -1 outside, distance class);
+// the diagonal sums all 26 slots (outside ones included) in stencil order.
+template <typename Coef>
+SparseMatrix gen_box27(index_t nx, index_t ny, index_t nz, Coef coef) {
+    const index_t pl = nx * ny, n = pl * nz;
+    Rows R;
+    for (index_t i = 0; i < n; ++i) {
+        const index_t ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
+        std::size_t dpos = 0;
+        double diag = 0.0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (dx == 0 && dy == 0 && dz == 0) {
+                        dpos = R.v.size();
+                        R.put(i, 0.0);
+                        continue;
+                    }
+                    const int dist = (dx != 0) + (dy != 0) + (dz != 0);
+                    const bool inside = ix + dx >= 0 && ix + dx < nx && iy + dy >= 0 && iy + dy < ny &&
+                                        iz + dz >= 0 && iz + dz < nz;
+                    const index_t j = inside ? i + dz * pl + dy * nx + dx : -1;
+                    const double a = coef(i, j, dist);
+                    diag += a;
+                    if (inside) R.put(j, -a);
+                }
+        R.v[dpos] = diag;
+        R.end_row();
+    }
+    return SparseMatrix::from_csr(n, n, std::move(R.rp), std::move(R.ci), std::move(R.v));
+}
+
+SparseMatrix gen_pressure27(index_t nx, index_t ny, index_t nz, std::uint64_t seed) {
+    const index_t n = nx * ny * nz;
+    std::vector<double> kappa(static_cast<std::size_t>(n));
+    for (index_t i = 0; i < n; ++i)
+        kappa[i] = std::pow(10.0, 4.0 * hash_unit(seed, static_cast<std::uint64_t>(i)) - 2.0);
+    return gen_box27(nx, ny, nz, [&](index_t i, index_t j, int dist) {
+        const double w = dist == 1 ? 1.0 : (dist == 2 ? 0.5 : 0.25);
+        const double ki = kappa[i];
+        if (j < 0) return w * ki;
+        const double kj = kappa[j];
+        return w * (2.0 * ki * kj / (ki + kj));
+    });
+}
+
+SparseMatrix gen_cutcell(index_t nx, index_t ny, index_t nz, std::uint64_t seed) {
+    const index_t pl = nx * ny, n = pl * nz;
+    const double Rs = 0.3 * static_cast<double>(nx);
+    const double cx = 0.5 * nx, cy = 0.5 * ny, cz = 0.5 * nz;
+    auto cell = [&](index_t i, double& kap, double& rho) {
+        const double x = static_cast<double>(i % nx) + 0.5 - cx;
+        const double y = static_cast<double>((i / nx) % ny) + 0.5 - cy;
+        const double z = static_cast<double>(i / pl) + 0.5 - cz;
+        const double r = std::sqrt(x * x + y * y + z * z);
+        rho = r < Rs ? 1000.0 : 1.0;
+        kap = std::abs(r - Rs) < 0.75 ? std::pow(10.0, 16.0 * hash_unit(seed, static_cast<std::uint64_t>(i))) : 1.0;
+    };
+    Rows R;
+    for (index_t i = 0; i < n; ++i) {
+        const index_t ix = i % nx, iy = (i / nx) % ny, iz = i / pl;
+        double ki, ri;
+        cell(i, ki, ri);
+        const bool in[6] = {iz > 0, iy > 0, ix > 0, ix + 1 < nx, iy + 1 < ny, iz + 1 < nz};
+        const index_t nb[6] = {i - pl, i - nx, i - 1, i + 1, i + nx, i + pl};
+        double f[6], diag = 0.0;
+        for (int s = 0; s < 6; ++s) {
+            if (!in[s]) {
+                f[s] = ki / ri; // mirrored cell outside the grid
+            } else {
+                double kj, rj;
+                cell(nb[s], kj, rj);
+                f[s] = (ki + kj) / 2.0 * (2.0 / (ri + rj));
+            }
+            diag += f[s];
+        }
+        for (int s = 0; s < 3; ++s)
+            if (in[s]) R.put(nb[s], -f[s]);
+        R.put(i, diag);
+        for (int s = 3; s < 6; ++s)
+            if (in[s]) R.put(nb[s], -f[s]);
+        R.end_row();
+    }
+    return SparseMatrix::from_csr(n, n, std::move(R.rp), std::move(R.ci), std::move(R.v));
+}
+} // namespace
+
+// kind: 0 poisson3d, 1 pressure27, 2 cutcell
+API int ref_gen3d(int kind, int64_t nx, int64_t ny, int64_t nz, uint64_t seed, void** outp) {
+    return wrap([&] {
+        if (nx < 1 || ny < 1 || nz < 1) fail_invalid("ref_gen3d: grid dimensions must be >= 1");
+        SparseMatrix M = kind == 0 ? gen_poisson3d(nx, ny, nz)
+                         : kind == 1 ? gen_pressure27(nx, ny, nz, seed)
+                                     : gen_cutcell(nx, ny, nz, seed);
+        *outp = new SparseMatrix(std::move(M));
+    });
+}
 
 // ---- config ----------------------------------------------------------------
 API void* ref_cfg_create() { return new Cfg(); }
@@ -231,6 +364,12 @@ API int ref_ilu_smooth_sweep(const void* A, const void* st, const double* b, dou
 }
 API const void* ref_smoother_factors(const void* st) {
     return &static_cast<const SmootherState*>(st)->factors;
+}
+API void ref_smoother_factor_nnz(const void* st, int64_t* n, int64_t* nnz_L, int64_t* nnz_U) {
+    const IluFactors& f = static_cast<const SmootherState*>(st)->factors;
+    *n = f.U.nrows;
+    *nnz_L = f.L.nnz();
+    *nnz_U = f.U.nnz();
 }
 API const void* ref_smoother_schur(const void* st) {
     return static_cast<const SmootherState*>(st)->schur.get();

@@ -202,3 +202,20 @@ def test_port_against_golden_fixture(ilug, port, name):
     assert bitwise(port.richardson_upper_scaled(Us, d, None, b, int(g["m"])), g["x_upper"])
     assert bitwise(port.richardson_lower(Lc, b, int(g["m"])), g["y_lower"])
     assert bitwise(port.solve_upper_direct(Us, b / d), g["x_upper_direct"])
+
+
+@pytest.mark.parametrize("spec", ["poisson3d(9,7,5)", "pressure27(8,9,7)", "pressure27(6,5,4,77)",
+                                  "cutcell(10,10,10)", "cutcell(12,9,8,5)"])
+def test_oracle_3d_generators_bitwise(spec):
+    """oracle/_ref's 3D generators (ref_gen3d, restated from SURVEY.md §8d on
+    the reference's hash_unit) = the device build's generators, bit for bit —
+    the bench's reference arm builds its input with them and never loads libilug."""
+    import paper_2111_09512_b200 as ilug
+    from oracle import oracle
+    if not os.path.exists(oracle.REF_SO):
+        pytest.skip("oracle/_ref not built")
+    ref = oracle.Ref()
+    got = ref.arrays(ref.gen3d(spec))
+    want = ilug.Matrix.generate(spec).csr()
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g).view(np.int64), np.asarray(w).astype(g.dtype).view(np.int64))
