@@ -38,6 +38,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # no init banner on stdout (one JSON line)
 
 METRIC = "ILU sweep GB/s (% HBM peak); GMRES+AMG time-to-solution at 1/2/4/8 B200"
 SPEC = "pressure27(256,256,256)"
@@ -466,9 +467,11 @@ def strong_solve(ilug, spec, kv, comm_args, barrier, max_over_ranks, hierarchy=N
     solver = idist.Solver(H, comm)
     torch.cuda.synchronize()
     dev_s = max_over_ranks(time.perf_counter() - t)
-    g = torch.Generator(device="cpu").manual_seed(4242)
-    b_full = torch.rand(A.rows, dtype=torch.float64, generator=g) * 2 - 1  # same global rhs on every rank
-    b = b_full[solver.row0:solver.row0 + solver.nloc].contiguous().cuda()
+    # the reference driver's default right-hand side, b = A * ones (src/config.cpp:334-337)
+    import numpy as np
+    rp, _, v = A.csr()
+    r0, r1 = solver.row0, solver.row0 + solver.nloc
+    b = torch.from_numpy(np.add.reduceat(v[:rp[r1]], rp[r0:r1]) if r1 > r0 else np.zeros(0)).cuda()
     x = torch.zeros_like(b)
     # warm-up (lazy module loading) outside the timed solve
     solver.gmres(ilug.Config().update(dict(kv, **{"krylov.max_iters": "2"})), b, x)
@@ -488,15 +491,31 @@ def strong_solve(ilug, spec, kv, comm_args, barrier, max_over_ranks, hierarchy=N
                               "replicated coarsest solve"}
 
 
+class stdout_to_stderr:
+    """fd-level redirect: library banners (NCCL prints its version on init)
+    must not reach stdout, which carries exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def dist_comm(rank, world, local):
     """NCCL communicator of this rank (torch.distributed only broadcasts the id)."""
     from paper_2111_09512_b200 import dist as idist
-    if world == 1:
-        return idist.Comm(1, 0, idist.unique_id())
-    import torch.distributed as dist
-    uid = [idist.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    return idist.Comm(world, rank, uid[0])
+    with stdout_to_stderr():
+        if world == 1:
+            return idist.Comm(1, 0, idist.unique_id())
+        import torch.distributed as dist
+        uid = [idist.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        return idist.Comm(world, rank, uid[0])
 
 
 def run_strong(args):

@@ -163,7 +163,7 @@ void DeviceSchur::build_dist(const HaloPlan& A, const Transport& t, const Smooth
             Crows.rp.push_back(static_cast<i64>(Crows.ci.size()));
         }
     }
-    HaloPlan Cp = halo_plan(Crows, part, A.rank);
+    HaloPlan Cp = halo_plan(std::move(Crows), part, A.rank);
     plan_exchange(Cp, t);
     n_ = n;
     ni_ = ni;

@@ -21,7 +21,14 @@ i64 RowPartition::owner(i64 row) const {
 }
 
 namespace {
-HaloPlan make_plan(const Csr& rows, const RowPartition& part, i64 rank, bool square) {
+HaloPlan make_plan(Csr&& rows_in, const RowPartition& part, i64 rank, bool square) {
+    const Csr rows = [&] { // pattern view: row starts and columns stay, values move into A_ext
+        Csr r;
+        r.nrows = rows_in.nrows, r.ncols = rows_in.ncols;
+        r.rp = rows_in.rp;
+        r.ci = std::move(rows_in.ci);
+        return r;
+    }();
     if (rank < 0 || rank >= part.p) fail_invalid("halo_plan: rank out of range");
     HaloPlan h;
     h.rank = rank;
@@ -30,11 +37,23 @@ HaloPlan make_plan(const Csr& rows, const RowPartition& part, i64 rank, bool squ
     h.row1 = part.starts[rank + 1];
     h.nloc = h.row1 - h.row0;
     if (square && rows.nrows != h.nloc) fail_invalid("halo_plan: local row count does not match the partition");
-    // halo = sorted unique off-range columns (contiguous ranges => grouped by owner)
-    for (i64 k = 0; k < rows.nnz(); ++k) {
-        const i64 j = rows.ci[k];
-        if (j < h.row0 || j >= h.row1) h.halo_global.push_back(j);
-    }
+    const i64 nr = rows.nrows, r0 = h.row0, r1 = h.row1;
+    auto local = [&](i64 j) { return j >= r0 && j < r1; };
+    // halo = sorted unique off-range columns (contiguous ranges => grouped by owner);
+    // per-row off-range counts give the split of every row for the two-pass fills
+    std::vector<i64> off_cnt(static_cast<size_t>(nr) + 1, 0);
+    const int T = host_threads();
+    std::vector<std::vector<i64>> part_halo(static_cast<size_t>(T));
+    parallel_ranges(nr, [&](i64 b, i64 e, int t) {
+        auto& hv = part_halo[static_cast<size_t>(t)];
+        for (i64 i = b; i < e; ++i) {
+            i64 c = 0;
+            for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k)
+                if (!local(rows.ci[k])) ++c, hv.push_back(rows.ci[k]);
+            off_cnt[i + 1] = c;
+        }
+    });
+    for (auto& hv : part_halo) h.halo_global.insert(h.halo_global.end(), hv.begin(), hv.end());
     std::sort(h.halo_global.begin(), h.halo_global.end());
     h.halo_global.erase(std::unique(h.halo_global.begin(), h.halo_global.end()), h.halo_global.end());
     h.nhalo = static_cast<i64>(h.halo_global.size());
@@ -46,52 +65,55 @@ HaloPlan make_plan(const Csr& rows, const RowPartition& part, i64 rank, bool squ
         }
     }
     h.recv_offsets.push_back(h.nhalo);
+    for (i64 i = 0; i < nr; ++i) off_cnt[i + 1] += off_cnt[i];
 
     // extended matrix: same entry order, renumbered columns
-    const i64 nr = rows.nrows;
     h.A_ext.nrows = nr;
     h.A_ext.ncols = h.nloc + h.nhalo;
-    h.A_ext.rp = rows.rp;
+    h.A_ext.rp = std::move(rows_in.rp);
     h.A_ext.ci.resize(rows.ci.size());
-    h.A_ext.v = rows.v;
+    h.A_ext.v = std::move(rows_in.v);
+    const RawVec<double>& vals = h.A_ext.v;
     if (square) {
         h.A_diag.nrows = h.A_diag.ncols = h.nloc;
-        h.A_diag.rp.assign(static_cast<size_t>(h.nloc) + 1, 0);
-        h.A_off.nrows = h.nloc;
+        h.A_diag.rp.resize(static_cast<size_t>(nr) + 1);
+        h.A_off.nrows = nr;
         h.A_off.ncols = h.nloc + h.nhalo;
-        h.A_off.rp.assign(static_cast<size_t>(h.nloc) + 1, 0);
+        h.A_off.rp.resize(static_cast<size_t>(nr) + 1);
+        for (i64 i = 0; i <= nr; ++i) {
+            h.A_off.rp[i] = off_cnt[i];
+            h.A_diag.rp[i] = rows.rp[i] - rows.rp[0] - off_cnt[i];
+        }
+        h.A_diag.ci.resize(static_cast<size_t>(h.A_diag.rp[nr]));
+        h.A_diag.v.resize(static_cast<size_t>(h.A_diag.rp[nr]));
+        h.A_off.ci.resize(static_cast<size_t>(off_cnt[nr]));
+        h.A_off.v.resize(static_cast<size_t>(off_cnt[nr]));
     }
-    for (i64 i = 0; i < nr; ++i) {
-        for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k) {
-            const i64 j = rows.ci[k];
-            if (j >= h.row0 && j < h.row1) {
-                h.A_ext.ci[k] = static_cast<i32>(j - h.row0);
-                if (square) {
-                    h.A_diag.ci.push_back(static_cast<i32>(j - h.row0));
-                    h.A_diag.v.push_back(rows.v[k]);
-                }
-            } else {
-                const auto it = std::lower_bound(h.halo_global.begin(), h.halo_global.end(), j);
-                h.A_ext.ci[k] = static_cast<i32>(h.nloc + (it - h.halo_global.begin()));
-                if (square) {
-                    h.A_off.ci.push_back(h.A_ext.ci[k]);
-                    h.A_off.v.push_back(rows.v[k]);
+    parallel_ranges(nr, [&](i64 b, i64 e, int) {
+        for (i64 i = b; i < e; ++i) {
+            i64 dd = square ? h.A_diag.rp[i] : 0, oo = square ? h.A_off.rp[i] : 0;
+            for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k) {
+                const i64 j = rows.ci[k];
+                if (local(j)) {
+                    h.A_ext.ci[k] = static_cast<i32>(j - r0);
+                    if (square) h.A_diag.ci[dd] = static_cast<i32>(j - r0), h.A_diag.v[dd++] = vals[k];
+                } else {
+                    const auto it = std::lower_bound(h.halo_global.begin(), h.halo_global.end(), j);
+                    h.A_ext.ci[k] = static_cast<i32>(h.nloc + (it - h.halo_global.begin()));
+                    if (square) h.A_off.ci[oo] = h.A_ext.ci[k], h.A_off.v[oo++] = vals[k];
                 }
             }
         }
-        if (square) {
-            h.A_diag.rp[i + 1] = static_cast<i64>(h.A_diag.ci.size());
-            h.A_off.rp[i + 1] = static_cast<i64>(h.A_off.ci.size());
-        }
-    }
+    });
     return h;
 }
 } // namespace
 
-HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) { return make_plan(rows, part, rank, true); }
+HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank) { return make_plan(csr_copy(rows), part, rank, true); }
+HaloPlan halo_plan(Csr&& rows, const RowPartition& part, i64 rank) { return make_plan(std::move(rows), part, rank, true); }
 
-HaloPlan halo_plan_rect(const Csr& rows, const RowPartition& cols, i64 rank) {
-    return make_plan(rows, cols, rank, false);
+HaloPlan halo_plan_rect(Csr&& rows, const RowPartition& cols, i64 rank) {
+    return make_plan(std::move(rows), cols, rank, false);
 }
 
 Csr csr_row_block(const Csr& M, i64 r0, i64 r1) {
@@ -102,8 +124,13 @@ Csr csr_row_block(const Csr& M, i64 r0, i64 r1) {
     B.rp.resize(static_cast<size_t>(B.nrows) + 1);
     const i64 base = M.rp[r0];
     for (i64 i = 0; i <= B.nrows; ++i) B.rp[i] = M.rp[r0 + i] - base;
-    B.ci.assign(M.ci.begin() + base, M.ci.begin() + M.rp[r1]);
-    B.v.assign(M.v.begin() + base, M.v.begin() + M.rp[r1]);
+    const i64 nnz = M.rp[r1] - base;
+    B.ci.resize(static_cast<size_t>(nnz));
+    B.v.resize(static_cast<size_t>(nnz));
+    parallel_ranges(nnz, [&](i64 b, i64 e, int) { // first touch spread over the pool
+        std::copy(M.ci.begin() + base + b, M.ci.begin() + base + e, B.ci.begin() + b);
+        std::copy(M.v.begin() + base + b, M.v.begin() + base + e, B.v.begin() + b);
+    }, 1 << 16);
     return B;
 }
 

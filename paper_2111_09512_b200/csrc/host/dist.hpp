@@ -44,9 +44,11 @@ struct HaloPlan {
 /// Build the plan from this rank's rows (global column ids). Receives are
 /// fully determined locally; sends need the other ranks' requests.
 HaloPlan halo_plan(const Csr& rows, const RowPartition& part, i64 rank);
+/// Same, consuming the rows (no copy of the values).
+HaloPlan halo_plan(Csr&& rows, const RowPartition& part, i64 rank);
 /// Same for an operator whose rows are partitioned differently from the vector
 /// it reads (AMG restriction / prolongation): `cols` partitions the columns.
-HaloPlan halo_plan_rect(const Csr& rows, const RowPartition& cols, i64 rank);
+HaloPlan halo_plan_rect(Csr&& rows, const RowPartition& cols, i64 rank);
 
 /// Rows [r0, r1) of M, global column ids.
 Csr csr_row_block(const Csr& M, i64 r0, i64 r1);

@@ -554,6 +554,139 @@ k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x
     }
 }
 
+// Sub-warp form of the value-flag schedule: W lanes per row, a ticket per
+// group of 32/W rows of one slice. Lane j of a row's sub-warp holds entries
+// j, j+W, j+2W, ... (E of them per pass: a row of up to W*E entries is one
+// pass, so all its dependency polls are in flight together and no second
+// chunk waits behind the first); the products a_t x_t are formed in the
+// lanes and the row's leader lane subtracts them from b in ascending column
+// order through a shuffle chain — the reference's serial operation order, so
+// the result stays bitwise. Fewer registers per row than the thread-per-row
+// form (whose 16-entry chunk split the 17-19-entry ILUT rows into two
+// dependent polling rounds).
+template <int MODE, int W>
+__global__ void __launch_bounds__(kFlagBlock)
+k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, const double* __restrict__ xold,
+              unsigned* ticket, unsigned sleep_ns) {
+    constexpr int RPG = 32 / W; // rows per group (per warp)
+    constexpr int E = 32 / W;   // entries per lane per pass
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / W, j = lane % W;
+    for (;;) {
+        unsigned g = 0;
+        if (lane == 0) g = atomicAdd(ticket, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngroups) return;
+        const i64 sl = g / W;
+        const int q = static_cast<int>(g % W) * RPG + sub;
+        const i64 p = sl * kSlice + q;
+        int len = M.rowlen[p];
+        const i64 base = M.slice_ptr[sl] + q;
+        i64 row = M.perm[p];
+        const bool valid = row >= 0;
+        if (!valid) len = 0, row = 0;
+        double s = j == 0 ? b[row] : 0.0, d = 1.0;
+        // passes: every lane of the warp runs the same number (shuffles are warp-wide)
+        int maxlen = len;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        for (int t0 = 0; t0 < maxlen; t0 += W * E) {
+            i32 c[E];
+            double a[E], pr[E];
+            int kind[E]; // 0 product, 1 diagonal (pr = a_ii), 2 none
+            unsigned pend = 0;
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                const int t = t0 + j + W * u;
+                kind[u] = 2;
+                pr[u] = 0.0;
+                if (t < len) {
+                    const i64 qq = base + static_cast<i64>(t) * kSlice;
+                    c[u] = __ldg(M.cols + qq);
+                    a[u] = __ldg(M.vals + qq);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u) {
+                const int t = t0 + j + W * u;
+                if (t < len) {
+                    if (MODE != 0 && c[u] == row) {
+                        kind[u] = 1;
+                    } else if (is_dep<MODE>(c[u], row)) {
+                        const unsigned long long v = ld_relaxed_u64(x + c[u]);
+                        pr[u] = __longlong_as_double(static_cast<long long>(v));
+                        kind[u] = 0;
+                        if (v == kXSentinel) pend |= 1u << u;
+                    } else {
+                        pr[u] = __ldg(xold + c[u]); // GS (MODE 2) only
+                        kind[u] = 0;
+                    }
+                }
+            }
+            long long spins = 0;
+            while (pend) {
+                if (++spins > (1ll << 26)) {
+                    atomicExch(&g_levelset_timeout, 1u);
+                    break;
+                }
+                __nanosleep(sleep_ns);
+#pragma unroll
+                for (int u = 0; u < E; ++u)
+                    if ((pend >> u) & 1u) {
+                        const unsigned long long v = ld_relaxed_u64(x + c[u]);
+                        if (v != kXSentinel) {
+                            pr[u] = __longlong_as_double(static_cast<long long>(v));
+                            pend &= ~(1u << u);
+                        }
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u) pr[u] = kind[u] == 0 ? a[u] * pr[u] : (kind[u] == 1 ? a[u] : 0.0);
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < E; ++u)
+#pragma unroll
+                for (int jj = 0; jj < W; ++jj) {
+                    const double v = __shfl_sync(0xffffffffu, pr[u], sub * W + jj);
+                    const int k = __shfl_sync(0xffffffffu, kind[u], sub * W + jj);
+                    if (j == 0) {
+                        if (k == 0)
+                            s = s - v;
+                        else if (k == 1)
+                            d = v;
+                    }
+                }
+        }
+        if (j == 0 && valid) {
+            const double r = MODE == 0 ? s : s / d;
+            unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(r));
+            if (bits == kXSentinel) bits = 0x7FFFFFFFFFFFFFFFull;
+            st_relaxed_u64(x + row, bits);
+        }
+    }
+}
+
+int vf_sub_width() { // ILUG_VF_SUB: 0 thread-per-row value flags, 2 / 4 / 8 lanes per row
+    const char* e = std::getenv("ILUG_VF_SUB");
+    return e ? std::atoi(e) : 0;
+}
+unsigned vf_sleep_ns() {
+    const char* e = std::getenv("ILUG_VF_SLEEP");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 32u;
+}
+int vf_warps_per_sm() { // resident-warp cap of the sync-free grid (0: occupancy-limited)
+    const char* e = std::getenv("ILUG_VF_WARPS");
+    return e ? std::atoi(e) : 0;
+}
+template <int MODE>
+const void* vsub_kernel(int w) {
+    switch (w) {
+    case 2: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 2>);
+    case 8: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 8>);
+    default: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 4>);
+    }
+}
+
 __global__ void k_ticket_reset(unsigned* ticket) { *ticket = 0u; }
 
 template <int MODE>
@@ -758,9 +891,21 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
         k_fill_sentinel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, n);
         k_ticket_reset<<<1, 1, 0, st>>>(ticket);
         ILUG_LAUNCH_CHECK();
+        const int w = vf_sub_width();
+        int grid = grid_;
+        if (const int cap = vf_warps_per_sm(); cap > 0)
+            grid = std::max(1, std::min(grid, device_sm_count() * cap / (kFlagBlock / 32)));
+        if (w == 2 || w == 4 || w == 8) {
+            i64 ng = ns * w;
+            unsigned sl = vf_sleep_ns();
+            void* args[] = {&mv, &ng, &b, &x, &xold, &ticket, &sl};
+            const void* fn = mode == 0 ? vsub_kernel<0>(w) : mode == 1 ? vsub_kernel<1>(w) : vsub_kernel<2>(w);
+            ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kFlagBlock), args, 0, st));
+            return;
+        }
         void* args[] = {&mv, &ns, &b, &x, &xold, &ticket};
         const void* fn = mode == 0 ? vflag_kernel<0>() : mode == 1 ? vflag_kernel<1>() : vflag_kernel<2>();
-        ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid_)), dim3(kFlagBlock), args, 0, st));
+        ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kFlagBlock), args, 0, st));
         return;
     }
     k_epoch_bump<<<1, 1, 0, st>>>(epoch, ticket);

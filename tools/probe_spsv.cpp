@@ -14,6 +14,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <vector>
 
 #define CK(x)                                                                       \
@@ -72,6 +74,47 @@ int main(int argc, char** argv) {
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     const float our_u = time_ms(e0, e1) / reps;
+
+    // ---- K5 schedule variants (env knobs read per launch): "SUB=4,SLEEP=32,WARPS=8" ...
+    // each checked bitwise against the default schedule's solution
+    {
+        std::vector<double> ref_l(n), ref_u(n), got(n);
+        CK(ilug_solve_lower(f, b, x, nullptr));
+        cudaMemcpy(ref_l.data(), x, n * sizeof(double), cudaMemcpyDeviceToHost);
+        CK(ilug_solve_upper(f, b, x, nullptr));
+        cudaMemcpy(ref_u.data(), x, n * sizeof(double), cudaMemcpyDeviceToHost);
+        for (int a = 2; a < argc; ++a) {
+            std::string cfgs = argv[a];
+            unsetenv("ILUG_VF_SUB"), unsetenv("ILUG_VF_SLEEP"), unsetenv("ILUG_VF_WARPS");
+            size_t pos = 0;
+            while (pos < cfgs.size()) {
+                size_t comma = cfgs.find(',', pos);
+                if (comma == std::string::npos) comma = cfgs.size();
+                const std::string kv = cfgs.substr(pos, comma - pos);
+                const size_t eq = kv.find('=');
+                setenv(("ILUG_VF_" + kv.substr(0, eq)).c_str(), kv.substr(eq + 1).c_str(), 1);
+                pos = comma + 1;
+            }
+            float t[2];
+            bool same[2];
+            for (int part = 0; part < 2; ++part) {
+                auto solve = [&] { CK(part == 0 ? ilug_solve_lower(f, b, x, nullptr) : ilug_solve_upper(f, b, x, nullptr)); };
+                solve();
+                cudaMemcpy(got.data(), x, n * sizeof(double), cudaMemcpyDeviceToHost);
+                same[part] = std::memcmp(got.data(), part == 0 ? ref_l.data() : ref_u.data(), n * sizeof(double)) == 0;
+                cudaDeviceSynchronize();
+                cudaEventRecord(e0);
+                for (int r = 0; r < reps; ++r) solve();
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                t[part] = time_ms(e0, e1) / reps;
+            }
+            std::printf("{\"variant\": \"%s\", \"lower_ms\": %.3f, \"upper_ms\": %.3f, \"bitwise\": [%s, %s]}\n",
+                        cfgs.c_str(), t[0], t[1], same[0] ? "true" : "false", same[1] ? "true" : "false");
+            std::fflush(stdout);
+        }
+        unsetenv("ILUG_VF_SUB"), unsetenv("ILUG_VF_SLEEP"), unsetenv("ILUG_VF_WARPS");
+    }
 
     // ---- cuSPARSE SpSV on the same factors
     cusparseHandle_t h;
