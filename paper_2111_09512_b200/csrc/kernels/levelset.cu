@@ -472,11 +472,10 @@ __global__ void k_fill_sentinel(double* x, i64 n) {
 // HOIST: the row length and slice start are loaded with perm[p] (a padding
 // slot runs len = 0 and publishes nothing) instead of after the padding test,
 // which the compiler otherwise turns into two dependent round trips.
-template <int MODE, bool HOIST = true>
+template <int MODE, bool HOIST = true, int kChunk = 16>
 __global__ void __launch_bounds__(kFlagBlock)
 k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x, const double* __restrict__ xold,
                 unsigned* ticket) {
-    constexpr int kChunk = 16;
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned sl = 0;
@@ -564,12 +563,11 @@ k_levels_vflags(SellView M, i64 nslices, const double* __restrict__ b, double* x
 // the result stays bitwise. Fewer registers per row than the thread-per-row
 // form (whose 16-entry chunk split the 17-19-entry ILUT rows into two
 // dependent polling rounds).
-template <int MODE, int W>
+template <int MODE, int W, int E = 32 / W>
 __global__ void __launch_bounds__(kFlagBlock)
 k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, const double* __restrict__ xold,
               unsigned* ticket, unsigned sleep_ns) {
-    constexpr int RPG = 32 / W; // rows per group (per warp)
-    constexpr int E = 32 / W;   // entries per lane per pass
+    constexpr int RPG = 32 / W; // rows per group (per warp); E: entries per lane per pass
     const int lane = threadIdx.x & 31;
     const int sub = lane / W, j = lane % W;
     for (;;) {
@@ -644,7 +642,8 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
             for (int u = 0; u < E; ++u) pr[u] = kind[u] == 0 ? a[u] * pr[u] : (kind[u] == 1 ? a[u] : 0.0);
             __syncwarp();
 #pragma unroll
-            for (int u = 0; u < E; ++u)
+            for (int u = 0; u < E; ++u) {
+                if (t0 + W * u >= maxlen) break; // no row of the warp has entries in this slot
 #pragma unroll
                 for (int jj = 0; jj < W; ++jj) {
                     const double v = __shfl_sync(0xffffffffu, pr[u], sub * W + jj);
@@ -656,6 +655,7 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
                             d = v;
                     }
                 }
+            }
         }
         if (j == 0 && valid) {
             const double r = MODE == 0 ? s : s / d;
@@ -666,9 +666,9 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
     }
 }
 
-int vf_sub_width() { // ILUG_VF_SUB: 0 thread-per-row value flags, 2 / 4 / 8 lanes per row
+int vf_sub_override() { // ILUG_VF_SUB (A/B): 0 / 1 thread per row (16- / 8-entry chunks), 2 / 4 / 8 / 83 / 16 lanes
     const char* e = std::getenv("ILUG_VF_SUB");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : -1;
 }
 unsigned vf_sleep_ns() {
     const char* e = std::getenv("ILUG_VF_SLEEP");
@@ -683,6 +683,8 @@ const void* vsub_kernel(int w) {
     switch (w) {
     case 2: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 2>);
     case 8: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 8>);
+    case 83: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 8, 3>); // 24 entries per pass
+    case 16: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 16>);
     default: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 4>);
     }
 }
@@ -805,6 +807,14 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // CTAs for the widest level's slices, capped by what one GPC co-schedules.
     const i64 cmax = max_cluster_ctas();
     const i64 avg = n / std::max(nl, 1);
+    // value-flag form by row length (tools/probe_spsv.cpp, profiles/r02_k5_variants*.txt):
+    // short rows (7-point ILU(0), <= 8 entries) thread per row with 8-entry
+    // chunks (C4 465^3: L 13.1 ms vs 18.9 cuSPARSE); longer rows 8 lanes per
+    // row, 3 entries per lane (C2 ILUT 17-19-entry rows: L 4.65 / U 14.4 ms vs
+    // 10.3 / 26.4 thread per row, cuSPARSE 6.95 / 12.6)
+    i64 max_row = 0;
+    for (i64 i = 0; i < n; ++i) max_row = std::max(max_row, T.rp[i + 1] - T.rp[i]);
+    vf_form_ = max_row <= 8 ? 1 : (max_row <= 24 ? 83 : 8);
     // measured: the cluster kernel wins up to a few hundred rows per level
     // (coarse-level GS at 128^3: 258 rows/level 3.3 vs 4.6 ms), the value-flag
     // kernel beyond (ILUT factors at 128^3, 1564 rows/level: 4.9 vs 10.6 ms L)
@@ -891,12 +901,13 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
         k_fill_sentinel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, n);
         k_ticket_reset<<<1, 1, 0, st>>>(ticket);
         ILUG_LAUNCH_CHECK();
-        const int w = vf_sub_width();
+        const int ov = vf_sub_override();
+        const int w = ov >= 0 ? ov : vf_form_;
         int grid = grid_;
         if (const int cap = vf_warps_per_sm(); cap > 0)
             grid = std::max(1, std::min(grid, device_sm_count() * cap / (kFlagBlock / 32)));
-        if (w == 2 || w == 4 || w == 8) {
-            i64 ng = ns * w;
+        if (w == 2 || w == 4 || w == 8 || w == 83 || w == 16) {
+            i64 ng = ns * (w == 83 ? 8 : w);
             unsigned sl = vf_sleep_ns();
             void* args[] = {&mv, &ng, &b, &x, &xold, &ticket, &sl};
             const void* fn = mode == 0 ? vsub_kernel<0>(w) : mode == 1 ? vsub_kernel<1>(w) : vsub_kernel<2>(w);
@@ -904,7 +915,10 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
             return;
         }
         void* args[] = {&mv, &ns, &b, &x, &xold, &ticket};
-        const void* fn = mode == 0 ? vflag_kernel<0>() : mode == 1 ? vflag_kernel<1>() : vflag_kernel<2>();
+        const void* fn = w == 1 ? (mode == 0   ? reinterpret_cast<const void*>(k_levels_vflags<0, false, 8>)
+                                   : mode == 1 ? reinterpret_cast<const void*>(k_levels_vflags<1, false, 8>)
+                                               : reinterpret_cast<const void*>(k_levels_vflags<2, false, 8>))
+                                : mode == 0 ? vflag_kernel<0>() : mode == 1 ? vflag_kernel<1>() : vflag_kernel<2>();
         ILUG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kFlagBlock), args, 0, st));
         return;
     }

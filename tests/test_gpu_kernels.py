@@ -240,6 +240,34 @@ def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule,
     assert bitwise(_host(xd), want)
 
 
+@pytest.mark.parametrize("sub", ["0", "1", "2", "4", "8", "83", "16"])
+@pytest.mark.parametrize("spec,kv", [("poisson3d(40,40,30)", {}),
+                                     ("pressure27(24,24,20)", {"ilu.variant": "ilut", "ilu.droptol": "1e-3",
+                                                               "ilu.lfill": "5"})])
+def test_k5_value_flag_forms_bitwise(ilug, ref, torch_cuda, monkeypatch, sub, spec, kv):
+    """Every form of the sync-free value-flag kernel (thread per row with 16- or
+    8-entry chunks; 2/4/8/16 lanes per row with the ordered shuffle chain) gives
+    the serial solves and the GS sweep bitwise."""
+    monkeypatch.setenv("ILUG_LEVELSET", "vflags")
+    monkeypatch.setenv("ILUG_VF_SUB", sub)
+    A, L, U, f, fr = _factors(ilug, ref, spec, kv, "row", direct=True)
+    b = np.random.default_rng(37).uniform(-1, 1, A.rows)
+    bd = _dev(torch_cuda, b)
+    y = torch_cuda.empty_like(bd)
+    for _ in range(2):
+        f.solve_lower(bd, y)
+        assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
+        f.solve_upper(bd, y)
+        assert bitwise(_host(y), ref.solve_upper_scaled_direct(fr, b))
+    S = ilug.Smoother(A, ilug.Config().set("smoother.kind", "gauss_seidel"))
+    x0 = np.random.default_rng(38).uniform(-1, 1, A.rows)
+    xd = _dev(torch_cuda, x0)
+    S.smooth(bd, xd)
+    Ar = ref.mat(*A.csr())
+    want, _ = ref.smooth(Ar, ref.smoother(Ar, ref.cfg({"smoother.kind": "gauss_seidel"})), b, x0)
+    assert bitwise(_host(xd), want)
+
+
 @pytest.mark.parametrize("schedule", ["", "cta", "flags", "vflags"])
 def test_k5_wide_dag_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule):
     """A wide DAG (n / levels > 2048: levels wider than a cluster's threads,
