@@ -2,6 +2,7 @@
 // src/capi.cpp's handle/status/last-error conventions) and ilug_* (device
 // handles for the individual hot-path subsystems). No exception crosses it.
 #include "capi_handles.hpp"
+#include "../kernels/amg_setup.hpp"
 #include "../kernels/spgemm.hpp"
 #include "../host/problems.hpp"
 
@@ -581,7 +582,9 @@ int ilug_hierarchy_create(const iluamg_matrix* A, const iluamg_config* cfg, ilug
         need(A && cfg && out);
         auto* h = new ilug_hierarchy_s();
         try {
-            h->h = ilug::amg_setup(A->A, ilug::amg_params_from(cfg->cfg));
+            const ilug::AmgParams ap = ilug::amg_params_from(cfg->cfg);
+            h->h = ap.device_setup != 0 && ilug::amg_device_supported(ap) ? ilug::amg_setup_device(A->A, ap, {}, nullptr)
+                                                                         : ilug::amg_setup(A->A, ap);
             h->d.set_use_graph(cfg->cfg.get_bool("device.graph"));
             h->d.build(h->h, nullptr);
             h->on_device = true;
@@ -598,7 +601,11 @@ int ilug_hierarchy_create_host(const iluamg_matrix* A, const iluamg_config* cfg,
         need(A && cfg && out);
         auto* h = new ilug_hierarchy_s();
         try {
-            h->h = ilug::amg_setup(A->A, ilug::amg_params_from(cfg->cfg));
+            // host-only handles keep the host setup unless device.amg_setup=device asks for the GPU
+            const ilug::AmgParams ap = ilug::amg_params_from(cfg->cfg);
+            if (ap.device_setup == 2 && !ilug::amg_device_supported(ap))
+                ilug::fail_invalid("device.amg_setup=device needs amg.coarsening=pmis and amg.interpolation=direct");
+            h->h = ap.device_setup == 2 ? ilug::amg_setup_device(A->A, ap, {}, nullptr) : ilug::amg_setup(A->A, ap);
         } catch (...) {
             delete h;
             throw;

@@ -1,4 +1,5 @@
 #include "driver.hpp"
+#include "../kernels/amg_setup.hpp"
 #include "../host/problems.hpp"
 #include "../kernels/spgemm.hpp"
 
@@ -133,7 +134,17 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
         }
     } gguard{gst};
     try {
-        oc.hier = amg_setup(A, apd, [&](i64 k, const HostLevel& lev, bool last) {
+        // the hierarchy itself on the GPU when supported (kernels/amg_setup.cu), else the host
+        const bool dev_setup = apd.device_setup != 0 && amg_device_supported(apd);
+        if (apd.device_setup == 2 && !dev_setup)
+            fail_invalid("device.amg_setup=device needs amg.coarsening=pmis and amg.interpolation=direct");
+        cudaStream_t sst = nullptr;
+        if (dev_setup) ILUG_CUDA(cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking));
+        StreamGuard sguard{sst};
+        auto setup = [&](const LevelReady& cb) {
+            return dev_setup ? amg_setup_device(A, apd, cb, sst) : amg_setup(A, apd, cb);
+        };
+        oc.hier = setup([&](i64 k, const HostLevel& lev, bool last) {
             {
                 std::lock_guard<std::mutex> g(qm);
                 queue.push_back({k, &lev, last});

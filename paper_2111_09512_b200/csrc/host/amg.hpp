@@ -58,6 +58,8 @@ struct AmgParams {
     /// Galerkin product R (A P) override (the device SpGEMM when the setup runs
     /// next to a GPU, kernels/spgemm.cu); empty: host csr_matmul. Same bits.
     std::function<Csr(const Csr& A, const Csr& P, const Csr& R)> galerkin;
+    /// device.amg_setup: 0 host, 1 device when supported (auto), 2 device (required)
+    int device_setup = 1;
 };
 
 struct CfSplit {

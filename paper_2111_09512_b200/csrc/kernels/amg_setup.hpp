@@ -1,0 +1,36 @@
+// Device AMG setup (kernels/amg_setup.cu): strength, PMIS, direct
+// interpolation, transposes and the Galerkin product on the GPU, bitwise the
+// host setup (host/amg.cpp) and the reference (src/amg.cpp:18-390).
+#pragma once
+
+#include "../host/amg.hpp"
+#include "spgemm.hpp"
+
+namespace ilug {
+
+/// C/F split on the device: is_coarse (0/1), coarse_index (-1 for F points).
+struct DevSplit {
+    i64 n = 0, n_coarse = 0;
+    DBuf<char> is_coarse;
+    DBuf<i64> coarse_index;
+};
+
+/// Strength pattern of A (values not stored): S_ij iff j != i and
+/// |a_ij| >= theta max_{k != i} |a_ik| (src/amg.cpp:18-50).
+DevCsr strength_device(const DevCsr& A, double theta, cudaStream_t st);
+/// Transpose with every row's columns ascending (values optional).
+DevCsr transpose_device(const DevCsr& M, bool values, cudaStream_t st);
+/// PMIS split with the reference's hash jitter and repair pass (src/amg.cpp:56-158).
+DevSplit pmis_device(const DevCsr& S, const DevCsr& St, std::uint64_t seed, cudaStream_t st);
+/// Direct interpolation (src/amg.cpp:162-232).
+DevCsr interp_direct_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp, cudaStream_t st);
+
+/// PMIS coarsening + direct interpolation (the device path's scope; RS
+/// greedy coarsening and MM-ext interpolation stay on the host).
+bool amg_device_supported(const AmgParams& p);
+/// amg_setup on the device: the hierarchy is built level by level on the GPU
+/// and every level's A/P/R/split is handed to the host structures (and to
+/// on_level) as soon as it is final; the result equals amg_setup bit for bit.
+HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st);
+
+} // namespace ilug

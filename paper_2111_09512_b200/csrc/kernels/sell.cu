@@ -386,6 +386,136 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
     if (valid) epi(row, s, pr);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined form (B200 bulk-copy engine): a persistent grid of 12 warps
+// per SM; every warp owns a 2-stage shared-memory ring and works through the
+// slices s = warp, warp + W, ... For the next slice, lane 0 arms an mbarrier
+// and issues two cp.async.bulk copies (the slice's values and columns, one
+// contiguous 32*width block each) while every lane prefetches its next row's
+// metadata (perm, length) and epilogue operand; then the current slice is
+// computed from shared memory: the only global loads left on the row's
+// critical path are the x gathers. The sum order is unchanged (ascending t
+// from 0.0), so the result is bitwise the plain kernel's.
+constexpr int kTmaWarps = 12;
+constexpr int kTmaWmax = 20; // widest slice the ring holds (C2 ILUT factors: 18)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1) k_rowdot_tma(SellView M, i64 nrows, const double* __restrict__ x,
+                                                                  Epi epi) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr unsigned VB = 32 * kTmaWmax * 8, CB = 32 * kTmaWmax * 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = smem + static_cast<size_t>(warp) * 2 * (VB + CB);
+    unsigned long long* bar =
+        reinterpret_cast<unsigned long long*>(smem + static_cast<size_t>(kTmaWarps) * 2 * (VB + CB)) + 2 * warp;
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const i64 ns = M.nrows_pad / kSlice;
+    const i64 nw = static_cast<i64>(gridDim.x) * kTmaWarps;
+    i64 s = static_cast<i64>(blockIdx.x) * kTmaWarps + warp;
+    if (s >= ns) return;
+    using Pre = decltype(epi.pre(i64{0}));
+    // issue slice sl into stage stg: bulk copies + this lane's row metadata and epilogue operand
+    auto issue = [&](i64 sl, int stg, int& len, i64& row, bool& valid, Pre& pre) {
+        const i64 sp = M.slice_ptr[sl];
+        const unsigned w = static_cast<unsigned>((M.slice_ptr[sl + 1] - sp) / kSlice);
+        if (lane == 0 && w > 0) {
+            unsigned char* vb = ring + stg * (VB + CB);
+            mbar_expect_tx(&bar[stg], w * 32u * 12u);
+            bulk_g2s(vb, M.vals + sp, w * 32u * 8u, &bar[stg]);
+            bulk_g2s(vb + VB, M.cols + sp, w * 32u * 4u, &bar[stg]);
+        }
+        const i64 p = sl * kSlice + lane;
+        len = M.rowlen[p];
+        row = M.perm ? M.perm[p] : p;
+        valid = row >= 0 && row < nrows;
+        if (!valid) len = 0, row = 0;
+        pre = epi.pre(row);
+        return w;
+    };
+    int len, nlen = 0;
+    i64 row, nrow = 0;
+    bool valid, nvalid = false;
+    Pre pre, npre{};
+    unsigned w = issue(s, 0, len, row, valid, pre), nwid = 0;
+    unsigned phase[2] = {0u, 0u};
+    int stage = 0;
+    while (s < ns) {
+        const i64 sn = s + nw;
+        if (sn < ns) nwid = issue(sn, stage ^ 1, nlen, nrow, nvalid, npre);
+        if (w > 0) {
+            mbar_wait(&bar[stage], phase[stage]);
+            phase[stage] ^= 1u;
+        }
+        const double* sv = reinterpret_cast<const double*>(ring + stage * (VB + CB)) + lane;
+        const int* sc = reinterpret_cast<const int*>(ring + stage * (VB + CB) + VB) + lane;
+        double acc = 0.0;
+        int t = 0;
+        for (; t + 8 <= len; t += 8) {
+            double xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) xv[u] = ld_gather(x + sc[(t + u) * kSlice]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = acc + sv[(t + u) * kSlice] * xv[u];
+        }
+        if (t < len) {
+            double xv[7];
+#pragma unroll
+            for (int u = 0; u < 7; ++u)
+                if (t + u < len) xv[u] = ld_gather(x + sc[(t + u) * kSlice]);
+#pragma unroll
+            for (int u = 0; u < 7; ++u)
+                if (t + u < len) acc = acc + sv[(t + u) * kSlice] * xv[u];
+        }
+        if (valid) epi(row, acc, pre);
+        __syncwarp(); // every lane is done with this stage before it is refilled
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        s = sn;
+        stage ^= 1;
+        w = nwid, len = nlen, row = nrow, valid = nvalid, pre = npre;
+    }
+}
+
+size_t rowdot_tma_smem() {
+    return static_cast<size_t>(kTmaWarps) * 2 * (32 * kTmaWmax * 12) + kTmaWarps * 2 * sizeof(unsigned long long);
+}
+bool rowdot_tma() { // ILUG_ROWDOT_TMA=1: the bulk-copy pipelined sweep (A/B)
+    const char* e = std::getenv("ILUG_ROWDOT_TMA");
+    return e && e[0] == '1';
+}
+
 // Kernel variant knobs for A/B experiments (tools/probe_sweep.py):
 // ILUG_L2_HINTS=1 enables the L2 eviction-priority hints (measured neutral on
 // B200 at C2, so off by default); ILUG_ROWDOT=4|8 picks the batch width.
@@ -432,6 +562,18 @@ int rowdot_width() { // measured at C2: width 4 beats 8 (64 regs halve occupancy
 template <class Epi>
 void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
     if (M.nrows_pad == 0) return;
+    if (rowdot_tma() && M.max_row <= kTmaWmax && M.nrows_pad > kWarpRowMax) {
+        static bool attr = [] {
+            ILUG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rowdot_tma<Epi>),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(rowdot_tma_smem())));
+            return true;
+        }();
+        (void)attr;
+        k_rowdot_tma<Epi><<<device_sm_count(), kTmaWarps * 32, rowdot_tma_smem(), st>>>(view(M), M.nrows, x, epi);
+        ILUG_LAUNCH_CHECK();
+        return;
+    }
     if (M.nrows_pad <= kWarpRowMax && warp_rows_enabled()) {
         const i64 warps = M.nrows_pad;
         const unsigned g = static_cast<unsigned>(std::min<i64>((warps * 32 + kBlock - 1) / kBlock,
