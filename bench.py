@@ -461,7 +461,9 @@ def strong_solve(ilug, spec, kv, comm_args, barrier, max_over_ranks, hierarchy=N
     barrier()
     t = time.perf_counter()
     A = ilug.Matrix.generate(spec)
-    H = hierarchy or ilug.Hierarchy(A, cfg, host_only=True)
+    # the global hierarchy, built on this rank's GPU (device AMG setup, PMIS + direct)
+    H = hierarchy or ilug.Hierarchy(A, ilug.Config().update(dict(kv, **{"device.amg_setup": "device"})),
+                                    host_only=True)
     host_s = max_over_ranks(time.perf_counter() - t)
     t = time.perf_counter()
     solver = idist.Solver(H, comm)
