@@ -54,7 +54,8 @@ def test_config_registry_matches_reference(ilug, ref):
     assert len(want) == 42
     for k, v in want.items():
         assert got.get(k) == v, k
-    assert set(got) - set(want) == {"trisolve.upper", "krylov.form_iterates", "device.graph", "device.id"}
+    assert set(got) - set(want) == {"trisolve.upper", "krylov.form_iterates", "device.graph", "device.id",
+                                    "device.amg_setup"}
 
 
 def test_config_fail_fast(ilug):
