@@ -48,6 +48,11 @@ ILU_KV = {"smoother.kind": "ilu", "ilu.variant": "ilut", "ilu.droptol": "1e-3", 
           "trisolve.m_upper": "5", "smoother.sweeps": "1"}
 # BASELINE configs[3] (C4): 7-point Poisson 465^3 = 100.5 M rows, block-Jacobi ILU(0) row-scaled
 C4_SPEC = "poisson3d(465,465,465)"
+# BASELINE configs[0] / BASELINE.md §2 (C1): the reference's CPU-runnable case, GMRES+AMG
+C1_SPEC = "poisson3d(64,64,64)"
+C1_KV = {"smoother.kind": "ilu", "ilu.variant": "ilu0", "scaling": "row", "trisolve.mode": "richardson",
+         "trisolve.m_lower": "5", "trisolve.m_upper": "5", "smoother.sweeps": "2",
+         "smoother.fallback.kind": "gauss_seidel", "amg.coarsening": "pmis", "krylov.tol": "1e-8"}
 C4_KV = dict(ILU_KV, **{"ilu.variant": "ilu0"})
 
 
@@ -226,6 +231,18 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     v = base["value"]
+    # the reference's own time-to-solution at C1 (run_solve, src/driver.cpp:239-260; single-threaded)
+    tts_c1 = None
+    try:
+        from oracle import oracle
+        ref = oracle.Ref()
+        A1 = ref.gen3d(C1_SPEC)
+        rep = ref.run_solve(ref.arrays(A1), C1_KV)
+        tts_c1 = {"spec": C1_SPEC, "iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
+                  "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
+                  "final_relres": float(rep["final_relres"]), "cores": 1}
+    except Exception as e:  # report, never lose the line
+        tts_c1 = {"error": str(e)[:200]}
     why = None if full else (f"full {spec} needs ~{need_gb:.0f} GB host RAM in the reference's int64 CSR layout, "
                              f"{info['mem_available_gb']} GB available (or --ref-sample): a slab of the same "
                              f"matrix family with the same per-row work is timed")
@@ -237,7 +254,7 @@ def run_reference(args):
                    "same_config": bool(full), "why_not_same": why,
                    "parallelism": f"reference CPU code, {base['cores']} concurrent calls on rank 0's host"},
         "cpu_baseline": base, "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "vs_baseline": None}))
+        "tts": {"C1": tts_c1}, "vs_baseline": None}))
 
 
 def build_workload(ilug, args, rank, world, local, use_dist=False):
@@ -439,6 +456,8 @@ def main():
             res.setdefault("tts", {})["strong"] = tts_s
     if rank == 0 and not use_dist and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline()
+        if not args.no_tts:
+            res["tts"]["C1"] = c1_tts(ilug)
     if rank == 0:
         print(json.dumps(res))
     if use_dist:
@@ -624,6 +643,33 @@ def run_strong(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def c1_tts(ilug):
+    """C1 (BASELINE.md §2 keys) through iluamg_run_solve on the GPU, next to the
+    reference's run_solve on one host core (oracle/_ref, the same call the
+    reference arm makes). Small: ~0.3 s on the device, ~5 s on the CPU."""
+    out = {}
+    A = ilug.Matrix.generate(C1_SPEC)
+    ilug.run_solve(A, ilug.Config().update(C1_KV))  # warm-up (module loading)
+    rep = ilug.run_solve(A, ilug.Config().update(C1_KV))
+    out["device"] = {"spec": C1_SPEC, "iterations": int(rep["iterations"]), "converged": rep["converged"] == "true",
+                     "setup_s": float(rep["setup_seconds"]), "solve_s": float(rep["solve_seconds"]),
+                     "final_relres": float(rep["final_relres"])}
+    try:
+        from oracle import oracle
+        if os.path.exists(oracle.REF_SO):
+            ref = oracle.Ref()
+            r = ref.run_solve(ref.arrays(ref.gen3d(C1_SPEC)), C1_KV)
+            out["reference_cpu_1core"] = {"iterations": int(r["iterations"]), "converged": r["converged"] == "true",
+                                          "setup_s": float(r["setup_seconds"]),
+                                          "solve_s": float(r["solve_seconds"])}
+            out["speedup_solve"] = round(out["reference_cpu_1core"]["solve_s"] / out["device"]["solve_s"], 1)
+            rc, dv = out["reference_cpu_1core"], out["device"]
+            out["speedup_total"] = round((rc["setup_s"] + rc["solve_s"]) / (dv["setup_s"] + dv["solve_s"]), 1)
+    except Exception as e:
+        out["reference_cpu_1core"] = {"error": str(e)[:200]}
+    return out
 
 
 def time_to_solution(ilug, A, fallbacks=("poly_gs",)):

@@ -361,7 +361,12 @@ void launch_ilut(const IlutArgs& a, cudaStream_t st) {
     int per_sm = 0;
     ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, smem));
     if (per_sm < 1) fail_invalid("ilut (device): kernel does not fit an SM");
-    const i64 grid = std::min<i64>(static_cast<i64>(per_sm) * device_sm_count(), (a.n + WARPS - 1) / WARPS);
+    // ILUG_ILUT_SMS (A/B): SMs the persistent grid may occupy (the rest stay free
+    // for the AMG setup kernels that run concurrently inside run_solve)
+    i64 sms = device_sm_count();
+    if (const char* e = std::getenv("ILUG_ILUT_SMS"))
+        if (std::atoi(e) > 0) sms = std::min<i64>(sms, std::atoi(e));
+    const i64 grid = std::min<i64>(static_cast<i64>(per_sm) * sms, (a.n + WARPS - 1) / WARPS);
     fn<<<static_cast<unsigned>(std::max<i64>(grid, 1)), WARPS * 32, smem, st>>>(a);
     ILUG_LAUNCH_CHECK();
 }
