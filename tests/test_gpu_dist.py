@@ -251,3 +251,29 @@ def test_dist_schur_fgmres_iterations(ilug, ref, torch_cuda, p):
     kvr = dict(BASE, **kv)
     want = ref.dist_krylov(Ar, ref.dist_setup(Ar, ref.cfg(kvr), p), ref.cfg(kvr), b)
     assert want["converged"] and abs(got - want["iterations"]) <= 1, f"{got} vs {want['iterations']}"
+
+
+def test_dist_solver_nccl_world_one_matches_local(ilug, ref, torch_cuda):
+    """The NCCL transport (what torchrun ranks use) at world size 1 runs the same
+    distributed solver as the in-process group: identical V-cycle bits and
+    iteration count (at p = 1 both equal the reference V-cycle)."""
+    from paper_2111_09512_b200 import dist as idist
+    torch = torch_cuda
+    spec, kv = CASES[1]
+    A = ilug.Matrix.generate(spec)
+    cfg = ilug.Config().update(dict(BASE, **kv))
+    H = ilug.Hierarchy(A, cfg, host_only=True)
+    r = np.random.default_rng(3).uniform(-1, 1, A.rows)
+    rd = torch.from_numpy(r).cuda()
+    outs = []
+    for comm in (idist.Comm(1, 0, idist.unique_id()), idist.LocalGroup(1).comm(0)):
+        S = idist.Solver(H, comm)
+        z = torch.empty_like(rd)
+        S.vcycle(rd, z)
+        x = torch.zeros_like(rd)
+        res = S.gmres(cfg, rd, x)
+        torch.cuda.synchronize()
+        outs.append((z.cpu().numpy(), res["iterations"], x.cpu().numpy()))
+    assert bitwise(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1] and bitwise(outs[0][2], outs[1][2])
+    Hr = ref.amg(ref.mat(*A.csr()), ref.cfg(dict(BASE, **kv)))
+    assert bitwise(outs[0][0], ref.vcycle(Hr, r, np.zeros(A.rows)))
