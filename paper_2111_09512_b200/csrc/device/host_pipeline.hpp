@@ -24,8 +24,10 @@ struct HostPipeline {
         cudaStreamDestroy(in), cudaStreamDestroy(run_st), cudaStreamDestroy(out);
     }
 
-    /// step(b_dev, x_dev, stream) applies one step in place on x_dev.
-    /// Pairs (bh[i], xh[i]) may repeat only two or more positions apart.
+    /// step(b_dev, x_dev, stream) applies one step in place on x_dev. A step
+    /// whose input (b or x) is the previous step's output buffer (the natural
+    /// "smooth again in place" pattern) waits for that output's copy-out, so it
+    /// reads the updated values; otherwise copies overlap the neighbours' work.
     template <class Step>
     void run(i64 n, long long count, const double* const* bh, double* const* xh, Step&& step) {
         ensure(n);
@@ -35,6 +37,9 @@ struct HostPipeline {
             const int k = static_cast<int>(i & 1);
             // slot k is free once step i-2 is copied out (which follows its compute)
             if (i >= 2) ILUG_CUDA(cudaStreamWaitEvent(in, drained[k], 0));
+            // reading step i-1's output: wait for its copy-out (read-after-write on the host buffer)
+            if (i >= 1 && (bh[i] == xh[i - 1] || xh[i] == xh[i - 1]))
+                ILUG_CUDA(cudaStreamWaitEvent(in, drained[k ^ 1], 0));
             ILUG_CUDA(cudaMemcpyAsync(b[k].p, bh[i], bytes, cudaMemcpyHostToDevice, in));
             ILUG_CUDA(cudaMemcpyAsync(x[k].p, xh[i], bytes, cudaMemcpyHostToDevice, in));
             ILUG_CUDA(cudaEventRecord(loaded[k], in));

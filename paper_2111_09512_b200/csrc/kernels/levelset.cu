@@ -638,8 +638,22 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
                         }
                     }
             }
+            // one shuffle per slot: products in the lanes, +0.0 in empty and
+            // diagonal slots (s - 0.0 == s exactly); the diagonal (U: entry 0,
+            // GS: anywhere) is fetched once from the lane that holds it
+            bool has_d = false;
+            double dl = 0.0;
 #pragma unroll
-            for (int u = 0; u < E; ++u) pr[u] = kind[u] == 0 ? a[u] * pr[u] : (kind[u] == 1 ? a[u] : 0.0);
+            for (int u = 0; u < E; ++u) {
+                if (MODE != 0 && kind[u] == 1) dl = a[u], has_d = true;
+                pr[u] = kind[u] == 0 ? a[u] * pr[u] : 0.0;
+            }
+            if (MODE != 0) {
+                const unsigned bal = __ballot_sync(0xffffffffu, has_d);
+                const unsigned mine = (bal >> (sub * W)) & ((W == 32 ? 0u : (1u << W)) - 1u);
+                const double dv = __shfl_sync(0xffffffffu, dl, sub * W + (mine ? __ffs(mine) - 1 : 0));
+                if (mine) d = dv;
+            }
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < E; ++u) {
@@ -647,13 +661,7 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
 #pragma unroll
                 for (int jj = 0; jj < W; ++jj) {
                     const double v = __shfl_sync(0xffffffffu, pr[u], sub * W + jj);
-                    const int k = __shfl_sync(0xffffffffu, kind[u], sub * W + jj);
-                    if (j == 0) {
-                        if (k == 0)
-                            s = s - v;
-                        else if (k == 1)
-                            d = v;
-                    }
+                    if (j == 0 && t0 + W * u + jj < len) s = s - v;
                 }
             }
         }
@@ -807,18 +815,26 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // CTAs for the widest level's slices, capped by what one GPC co-schedules.
     const i64 cmax = max_cluster_ctas();
     const i64 avg = n / std::max(nl, 1);
-    // value-flag form by row length (tools/probe_spsv.cpp, profiles/r02_k5_variants*.txt):
-    // short rows (7-point ILU(0), <= 8 entries) thread per row with 8-entry
-    // chunks (C4 465^3: L 13.1 ms vs 18.9 cuSPARSE); longer rows 8 lanes per
-    // row, 3 entries per lane (C2 ILUT 17-19-entry rows: L 4.65 / U 14.4 ms vs
-    // 10.3 / 26.4 thread per row, cuSPARSE 6.95 / 12.6)
+    // value-flag form by row length and direction (tools/probe_spsv.cpp,
+    // profiles/r02_k5_*.txt): short rows (7-point ILU(0), <= 8 entries) thread
+    // per row — 8-entry chunks for L (C4: 12.3 ms vs 18.8 cuSPARSE), 16-entry
+    // chunks for U; longer rows 8 lanes per row with one shuffle per entry slot
+    // (C2 ILUT: L 4.6 ms, U 7.6 ms vs cuSPARSE 6.9 / 12.9) — 3 entries per lane
+    // for L rows up to 24 entries, 4 otherwise
     i64 max_row = 0;
     for (i64 i = 0; i < n; ++i) max_row = std::max(max_row, T.rp[i + 1] - T.rp[i]);
-    vf_form_ = max_row <= 8 ? 1 : (max_row <= 24 ? 83 : 8);
+    if (max_row <= 8)
+        vf_form_ = kind == Kind::lower_unit ? 1 : 0;
+    else
+        vf_form_ = kind == Kind::lower_unit && max_row <= 24 ? 83 : 8;
     // measured: the cluster kernel wins up to a few hundred rows per level
     // (coarse-level GS at 128^3: 258 rows/level 3.3 vs 4.6 ms), the value-flag
     // kernel beyond (ILUT factors at 128^3, 1564 rows/level: 4.9 vs 10.6 ms L)
-    single_cta_ = n <= 4 * kSmallBlock || avg <= 512;
+    // with the sub-warp value-flag kernel the sync-free schedule also wins on the
+    // coarse AMG levels' Gauss-Seidel (C2 levels 1-4, 8.5 K-1.4 M rows: 1.5-3.0 ms
+    // vs 2.0-13.4 ms per sweep, profiles/r02_gs_forms2.txt); the cluster kernel
+    // keeps the small operators
+    single_cta_ = n <= 4096 || (max_row <= 8 && avg <= 512);
     // wide levels (> 2 rows per warp of a 512-thread cluster): 1024-thread
     // CTAs. ILUG_LEVELSET_WIDE=slots2 takes 512-thread CTAs with two rows per
     // warp prefetched and processed together instead (measured slower at the
