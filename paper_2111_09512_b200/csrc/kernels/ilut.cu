@@ -70,6 +70,40 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+// Value-flag publication of U rows (VF): the row's slot starts filled with
+// sentinels (column -1, value = a signalling NaN no arithmetic produces,
+// length 0); the producer writes entries, pivot and length with relaxed .gpu
+// stores and a consumer validates every word it uses, so the data IS the
+// flag — one memory round trip per dependency step instead of a flag poll, an
+// acquire and a second fetch.
+constexpr unsigned long long kUSentinel = 0x7FF0DEAD5EA1ED01ull;
+__device__ __forceinline__ unsigned long long ldr_u64(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ldr_s32(const i32* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void str_f64(double* p, double x) {
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    if (b == kUSentinel) b = 0x7FFFFFFFFFFFFFFFull; // never publish the sentinel itself
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(b) : "memory");
+}
+__device__ __forceinline__ void str_s32(i32* p, int x) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+__global__ void k_ilut_vf_fill(i64 ucap, i64 n, i32* __restrict__ uci, double* __restrict__ uv, i32* __restrict__ ulen) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < ucap;
+         i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        uci[i] = -1;
+        reinterpret_cast<unsigned long long*>(uv)[i] = kUSentinel;
+        if (i < n) ulen[i] = 0;
+    }
+}
+
 // Rank fill candidates in [beg, end) that carry `want` and not kOrig: keep the
 // lfill best by (|w| desc, column asc) (the reference's nth_element comparator,
 // src/ilu.cpp:206-211). Pattern candidates are always kept. Marks kSel.
@@ -117,6 +151,7 @@ __device__ __forceinline__ void select_part(const i32* scol, const double* sval,
 }
 
 // Write the kSel entries of [beg, end) (ascending columns) to out_c/out_v; returns the count.
+template <bool VF = false>
 __device__ __forceinline__ int emit(const i32* scol, const double* sval, const unsigned char* sflag, int beg,
                                     int end, i32* out_c, double* out_v, int lane) {
     int base = 0;
@@ -126,15 +161,20 @@ __device__ __forceinline__ int emit(const i32* scol, const double* sval, const u
         const unsigned b = __ballot_sync(0xffffffffu, s);
         if (s) {
             const int o = base + __popc(b & lanemask_lt());
-            out_c[o] = scol[q];
-            out_v[o] = sval[q];
+            if (VF) {
+                str_s32(out_c + o, scol[q]);
+                str_f64(out_v + o, sval[q]);
+            } else {
+                out_c[o] = scol[q];
+                out_v[o] = sval[q];
+            }
         }
         base += __popc(b);
     }
     return base;
 }
 
-template <int CAP, int WARPS>
+template <int CAP, int WARPS, bool VF>
 __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -165,7 +205,16 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
         }
         if (bad) { // capacity exceeded somewhere: publish and let the host relaunch
             __syncwarp();
-            if (lane == 0) fi.store(E, cuda::memory_order_release);
+            if (lane == 0) {
+                if (VF) { // a valid (meaningless) one-entry row: consumers must not wait
+                    const i64 uo = a.uoff[i];
+                    str_s32(a.uci + uo, static_cast<i32>(i));
+                    str_f64(a.uv + uo, 1.0);
+                    str_s32(a.ulen + i, 1);
+                } else {
+                    fi.store(E, cuda::memory_order_release);
+                }
+            }
             continue;
         }
         for (int q = lane; q < alen; q += 32) {
@@ -187,11 +236,38 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
             // length are never used)
             const i64 ub = __ldg(a.uoff + k);
             const bool in_slot = lane + 1 < __ldg(a.uoff + k + 1) - ub;
-            if (!wait_flag(a.done + k, E)) atomicExch(a.err, 1u);
-            const int ul = a.ulen[k];
-            const double ukk = a.uv[ub];
-            const i32 j0 = in_slot ? a.uci[ub + 1 + lane] : INT_MAX;
-            const double u0 = in_slot ? a.uv[ub + 1 + lane] : 0.0;
+            int ul;
+            double ukk, u0;
+            i32 j0;
+            if (VF) { // length, pivot and the first 32 entries validated word by word
+                long long spins = 0;
+                for (;;) {
+                    ul = ldr_s32(a.ulen + k);
+                    const unsigned long long pb = ldr_u64(a.uv + ub);
+                    const i32 jj = in_slot ? ldr_s32(a.uci + ub + 1 + lane) : INT_MAX;
+                    const unsigned long long vb = in_slot ? ldr_u64(a.uv + ub + 1 + lane) : 0ull;
+                    const bool need = lane + 1 < ul;
+                    const bool ok = ul > 0 && pb != kUSentinel && (!need || (jj >= 0 && vb != kUSentinel));
+                    if (__all_sync(full, ok)) {
+                        ukk = __longlong_as_double(static_cast<long long>(pb));
+                        j0 = jj;
+                        u0 = __longlong_as_double(static_cast<long long>(vb));
+                        break;
+                    }
+                    if (++spins > (1ll << 26)) {
+                        if (lane == 0) atomicExch(a.err, 1u);
+                        ul = 1, ukk = 1.0, j0 = INT_MAX, u0 = 0.0;
+                        break;
+                    }
+                    __nanosleep(20);
+                }
+            } else {
+                if (!wait_flag(a.done + k, E)) atomicExch(a.err, 1u);
+                ul = a.ulen[k];
+                ukk = a.uv[ub];
+                j0 = in_slot ? a.uci[ub + 1 + lane] : INT_MAX;
+                u0 = in_slot ? a.uv[ub + 1 + lane] : 0.0;
+            }
             const double m = sval[p] / ukk;
             __syncwarp();
             if (fabs(m) < tau) { // dual-threshold drop of the multiplier
@@ -203,8 +279,19 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
             for (int c = 1; c < ul; c += 32) {
                 const int kk = c + lane;
                 const bool act = kk < ul;
-                const i32 j = !act ? INT_MAX : (c == 1 ? j0 : a.uci[ub + kk]);
-                const double u = !act ? 0.0 : (c == 1 ? u0 : a.uv[ub + kk]);
+                i32 j = !act ? INT_MAX : (c == 1 ? j0 : a.uci[ub + kk]);
+                double u = !act ? 0.0 : (c == 1 ? u0 : a.uv[ub + kk]);
+                if (VF && act && c > 1) { // entries past the first 32: validated one by one
+                    for (;;) {
+                        j = ldr_s32(a.uci + ub + kk);
+                        const unsigned long long vb = ldr_u64(a.uv + ub + kk);
+                        if (j >= 0 && vb != kUSentinel) {
+                            u = __longlong_as_double(static_cast<long long>(vb));
+                            break;
+                        }
+                        __nanosleep(20);
+                    }
+                }
                 int lo = p + 1, hi = len;
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
@@ -264,7 +351,16 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
         }
         if (bad) {
             __syncwarp();
-            if (lane == 0) fi.store(E, cuda::memory_order_release);
+            if (lane == 0) {
+                if (VF) {
+                    const i64 uo = a.uoff[i];
+                    str_s32(a.uci + uo, static_cast<i32>(i));
+                    str_f64(a.uv + uo, 1.0);
+                    str_s32(a.ulen + i, 1);
+                } else {
+                    fi.store(E, cuda::memory_order_release);
+                }
+            }
             continue;
         }
         // p: first position with column >= i
@@ -284,14 +380,22 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
         const int ub = p + (hasd ? 1 : 0);
         select_part(scol, sval, sflag, ub, len, kLive, true, tau, a.lfill, lane);
         const i64 uo = a.uoff[i];
-        const int nu = emit(scol, sval, sflag, ub, len, a.uci + uo + 1, a.uv + uo + 1, lane);
-        if (lane == 0) {
-            a.uci[uo] = static_cast<i32>(i);
-            a.uv[uo] = d;
-            a.ulen[i] = nu + 1;
+        const int nu = emit<VF>(scol, sval, sflag, ub, len, a.uci + uo + 1, a.uv + uo + 1, lane);
+        if (VF) {
+            if (lane == 0) {
+                str_s32(a.uci + uo, static_cast<i32>(i));
+                str_f64(a.uv + uo, d);
+                str_s32(a.ulen + i, nu + 1);
+            }
+        } else {
+            if (lane == 0) {
+                a.uci[uo] = static_cast<i32>(i);
+                a.uv[uo] = d;
+                a.ulen[i] = nu + 1;
+            }
+            __syncwarp(); // orders every lane's row writes before lane 0's release (cumulative)
+            if (lane == 0) fi.store(E, cuda::memory_order_release);
         }
-        __syncwarp(); // orders every lane's row writes before lane 0's release (cumulative)
-        if (lane == 0) fi.store(E, cuda::memory_order_release);
 
         select_part(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, lane);
         const i64 lo = a.loff[i];
@@ -352,11 +456,22 @@ void inclusive_scan(i64* d, i64 count, cudaStream_t st) {
     ILUG_CUDA(cudaStreamSynchronize(st)); // t is freed on return
 }
 
+bool ilut_value_flags() { // ILUG_ILUT_VF=0: publish U rows through the separate done flags (A/B)
+    const char* e = std::getenv("ILUG_ILUT_VF");
+    return !(e && e[0] == '0');
+}
+
 template <int CAP, int WARPS>
-void launch_ilut(const IlutArgs& a, cudaStream_t st) {
+void launch_ilut(const IlutArgs& a, i64 ucap, cudaStream_t st) {
     constexpr size_t smem = static_cast<size_t>(WARPS) * CAP * (sizeof(double) + sizeof(i32) + 1) +
                             static_cast<size_t>(WARPS) * 32 * sizeof(i32);
-    auto* fn = k_ilut<CAP, WARPS>;
+    const bool vf = ilut_value_flags();
+    if (vf) {
+        k_ilut_vf_fill<<<static_cast<unsigned>(std::min<i64>((ucap + 255) / 256, 148 * 64)), 256, 0, st>>>(
+            ucap, a.n, a.uci, a.uv, a.ulen);
+        ILUG_LAUNCH_CHECK();
+    }
+    auto* fn = vf ? k_ilut<CAP, WARPS, true> : k_ilut<CAP, WARPS, false>;
     ILUG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, smem));
@@ -429,11 +544,11 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
             k_ilut_bump<<<1, 1, 0, st>>>(sync.p + n, ctl.p, sync.p + n + 1);
             ILUG_LAUNCH_CHECK();
             if (cap_level == 0)
-                launch_ilut<256, 8>(a, st);
+                launch_ilut<256, 8>(a, ucap, st);
             else if (cap_level == 1)
-                launch_ilut<1024, 4>(a, st);
+                launch_ilut<1024, 4>(a, ucap, st);
             else
-                launch_ilut<6144, 2>(a, st);
+                launch_ilut<6144, 2>(a, ucap, st);
             ILUG_CUDA(cudaMemcpyAsync(err, sync.p + n + 1, sizeof err, cudaMemcpyDeviceToHost, st));
             ILUG_CUDA(cudaStreamSynchronize(st));
             if (err[0]) fail_numeric("ilut (device): dependency wait timed out (scheduling error)");

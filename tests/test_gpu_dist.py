@@ -53,7 +53,7 @@ def _ranks(ilug, torch, spec, kv, p, body):
     return A, cfg, idist.run_ranks(p, rank_fn, group)
 
 
-@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 7, 8])  # 3, 7: uneven blocks (the last rank takes the remainder)
 @pytest.mark.parametrize("spec,kv", CASES, ids=[c[0] for c in CASES])
 def test_dist_vcycle_bitwise(ilug, ref, torch_cuda, spec, kv, p):
     torch = torch_cuda
