@@ -456,9 +456,14 @@ void inclusive_scan(i64* d, i64 count, cudaStream_t st) {
     ILUG_CUDA(cudaStreamSynchronize(st)); // t is freed on return
 }
 
-bool ilut_value_flags() { // ILUG_ILUT_VF=0: publish U rows through the separate done flags (A/B)
+// ILUG_ILUT_VF=1: value-flag publication of U rows (A/B; bitwise the same).
+// Off: C2 factor kernel 1.71-1.73 s vs 1.64-1.67 s with the done flags in an
+// interleaved A/B (profiles/r02_ilut_vf_ab.txt) — the kernel is bound by its
+// per-row work across the SMs (2.1 / 2.9 / 5.8 s on 96 / 64 / 32 SMs), not by
+// the flag round trip of the dependency chain.
+bool ilut_value_flags() {
     const char* e = std::getenv("ILUG_ILUT_VF");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }
 
 template <int CAP, int WARPS>
