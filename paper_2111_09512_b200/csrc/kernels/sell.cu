@@ -550,6 +550,10 @@ bool rowdot_early() { // ILUG_ROWDOT_EARLY=1: every epilogue's inputs loaded bef
     const char* e = std::getenv("ILUG_ROWDOT_EARLY");
     return e && e[0] == '1';
 }
+bool rowdot_late_acc() { // ILUG_ROWDOT_LATE_ACC=1: read-modify-write epilogues load after the row loop (A/B)
+    const char* e = std::getenv("ILUG_ROWDOT_LATE_ACC");
+    return e && e[0] == '1';
+}
 bool rowdot_hoist() { // ILUG_ROWDOT_HOIST=0: row metadata loaded after the padding check (A/B)
     const char* e = std::getenv("ILUG_ROWDOT_HOIST");
     return !(e && e[0] == '0');
@@ -597,6 +601,8 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad, 64), 64, 0, st>>>(view(M), M.nrows, x, epi);
     else if (rowdot_early())
         k_rowdot<Epi, false, true, true, true><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (Epi::kEarly && rowdot_late_acc())
+        k_rowdot<Epi, false, true, true, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else if (!rowdot_hoist())
         k_rowdot<Epi, false, true, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else

@@ -13,12 +13,16 @@ import torch  # noqa: E402
 
 import paper_2111_09512_b200 as ilug  # noqa: E402
 
-what = sys.argv[1]
+what = sys.argv[1]  # u | l | k5u | k5l | step (one ilu_smooth_sweep: residual, L sweeps, U sweeps, x += ...)
 spec = sys.argv[2] if len(sys.argv) > 2 else "pressure27(256,256,256)"
 kv = {"ilu.variant": "ilut", "ilu.droptol": "1e-3", "ilu.lfill": "5"}
 torch.cuda.set_device(0)
 A = ilug.Matrix.generate(spec)
-F = ilug.Factors.create(A, ilug.Config().update(kv), scaling="row", direct=what.startswith("k5"))
+if what == "step":
+    S = ilug.Smoother(A, ilug.Config().update(dict(kv, **{"smoother.kind": "ilu", "trisolve.m_lower": "5",
+                                                          "trisolve.m_upper": "5"})))
+else:
+    F = ilug.Factors.create(A, ilug.Config().update(kv), scaling="row", direct=what.startswith("k5"))
 n = A.rows
 b = torch.rand(n, dtype=torch.float64, device="cuda")
 out = torch.empty_like(b)
@@ -31,5 +35,9 @@ elif what == "k5u":
     F.solve_upper(b, out)
 elif what == "k5l":
     F.solve_lower(b, out)
+elif what == "step":
+    x = torch.rand(n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    S.ilu_sweep(b, x)
 torch.cuda.synchronize()
 print("done", what)
