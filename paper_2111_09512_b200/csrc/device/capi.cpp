@@ -773,7 +773,7 @@ int ilug_dist_plan_matrix(const ilug_dist_plan* p, int which, iluamg_matrix** ou
     return guarded([&] {
         need(p && out);
         if (which < 0 || which > 2) ilug::fail_invalid("plan matrix: which must be 0 (ext), 1 (diag) or 2 (off)");
-        *out = new iluamg_matrix_s{which == 0 ? p->plan.A_ext : which == 1 ? p->plan.A_diag : p->plan.A_off, "dist"};
+        *out = new iluamg_matrix_s{which == 0 ? p->plan.A_ext : which == 1 ? p->plan.diag() : p->plan.A_off, "dist"};
         return ILUAMG_OK;
     });
 }

@@ -305,7 +305,7 @@ void DistSmoother::build(const HaloPlan& plan, const DistComm& comm, const Smoot
     if (plan.nranks > 1 && plan.send_offsets.size() != plan.send_ranks.size() + (plan.send_ranks.empty() ? 0 : 1))
         fail_invalid("distributed smoother: halo sends not set");
     op_.build(plan, *comm.t, st);
-    s_.build(plan.A_diag, op_.M, cfg, st, nullptr, &plan); // rank-local factors / level plans
+    s_.build(plan.diag(), op_.M, cfg, st, nullptr, &plan); // rank-local factors / level plans
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -337,7 +337,7 @@ void DistHierarchy::build(const HostHierarchy& h, const DistComm& comm, cudaStre
             sell_from_host(lv.P_rows, d.P_rows, Part::all, st);
             gather_.alloc(std::max<i64>(d.n, 1));
         }
-        lv.smoother.build(d.A.A_diag, lv.A.M, h.params.plan.for_level(k), st, nullptr, &d.A);
+        lv.smoother.build(d.A.diag(), lv.A.M, h.params.plan.for_level(k), st, nullptr, &d.A);
         lv.b.alloc(std::max<i64>(lv.n, 1));
         lv.x.alloc(std::max<i64>(lv.n, 1));
         lv.r.alloc(std::max<i64>(lv.n, 1));

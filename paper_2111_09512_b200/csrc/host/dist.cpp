@@ -74,12 +74,15 @@ HaloPlan make_plan(Csr&& rows_in, const RowPartition& part, i64 rank, bool squar
     h.A_ext.ci.resize(rows.ci.size());
     h.A_ext.v = std::move(rows_in.v);
     const RawVec<double>& vals = h.A_ext.v;
+    const bool split = square && h.nhalo > 0; // without a halo the block is A_ext (diag())
     if (square) {
-        h.A_diag.nrows = h.A_diag.ncols = h.nloc;
-        h.A_diag.rp.resize(static_cast<size_t>(nr) + 1);
         h.A_off.nrows = nr;
         h.A_off.ncols = h.nloc + h.nhalo;
-        h.A_off.rp.resize(static_cast<size_t>(nr) + 1);
+        h.A_off.rp.assign(static_cast<size_t>(nr) + 1, 0);
+    }
+    if (split) {
+        h.A_diag.nrows = h.A_diag.ncols = h.nloc;
+        h.A_diag.rp.resize(static_cast<size_t>(nr) + 1);
         for (i64 i = 0; i <= nr; ++i) {
             h.A_off.rp[i] = off_cnt[i];
             h.A_diag.rp[i] = rows.rp[i] - rows.rp[0] - off_cnt[i];
@@ -91,16 +94,16 @@ HaloPlan make_plan(Csr&& rows_in, const RowPartition& part, i64 rank, bool squar
     }
     parallel_ranges(nr, [&](i64 b, i64 e, int) {
         for (i64 i = b; i < e; ++i) {
-            i64 dd = square ? h.A_diag.rp[i] : 0, oo = square ? h.A_off.rp[i] : 0;
+            i64 dd = split ? h.A_diag.rp[i] : 0, oo = split ? h.A_off.rp[i] : 0;
             for (i64 k = rows.rp[i]; k < rows.rp[i + 1]; ++k) {
                 const i64 j = rows.ci[k];
                 if (local(j)) {
                     h.A_ext.ci[k] = static_cast<i32>(j - r0);
-                    if (square) h.A_diag.ci[dd] = static_cast<i32>(j - r0), h.A_diag.v[dd++] = vals[k];
+                    if (split) h.A_diag.ci[dd] = static_cast<i32>(j - r0), h.A_diag.v[dd++] = vals[k];
                 } else {
                     const auto it = std::lower_bound(h.halo_global.begin(), h.halo_global.end(), j);
                     h.A_ext.ci[k] = static_cast<i32>(h.nloc + (it - h.halo_global.begin()));
-                    if (square) h.A_off.ci[oo] = h.A_ext.ci[k], h.A_off.v[oo++] = vals[k];
+                    if (split) h.A_off.ci[oo] = h.A_ext.ci[k], h.A_off.v[oo++] = vals[k];
                 }
             }
         }

@@ -34,7 +34,9 @@ struct HaloPlan {
     Csr A_ext;
     /// Square operators: local diagonal block A[row0:row1, row0:row1] (sorted,
     /// local numbering) and the off-block rest (halo columns only, ext numbering).
+    /// Without a halo the block is A_ext itself (A_diag stays empty: use diag()).
     Csr A_diag, A_off;
+    const Csr& diag() const { return nhalo == 0 ? A_ext : A_diag; }
     std::vector<i64> halo_global;              ///< ascending global ids of the halo entries
     std::vector<i64> recv_ranks, recv_offsets; ///< per source rank: halo segment [off_k, off_k+1)
     std::vector<i64> send_ranks, send_offsets; ///< per destination rank: segment of send_local
