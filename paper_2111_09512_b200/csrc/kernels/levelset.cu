@@ -284,15 +284,16 @@ struct RowMeta {
 struct RowData {
     i32 c0 = -1, c1 = -1;
     double a0 = 0.0, a1 = 0.0, bv = 0.0;
+    double xo0 = 0.0, xo1 = 0.0; // SX, GS: xold at columns > row, prefetched with the row
 };
 
 // Q rows per warp at once (one per prefetch slot): every slot's x gathers are
 // issued before any slot's shuffle chain, so the slots' memory latencies
 // overlap. Entries 0..63 come from the prefetched registers; longer rows load
 // the rest inline.
-template <int MODE, int Q>
+template <int MODE, int Q, bool SX = false>
 __device__ __forceinline__ void warp_rows(const SellView& M, const RowMeta (&m)[Q], const RowData (&r)[Q], int lane,
-                                          double* x, const double* __restrict__ xold) {
+                                          double* x, const double* __restrict__ xold, double* sx = nullptr) {
     const unsigned full = 0xffffffffu;
     double s[Q], d[Q];
     int maxlen = 0;
@@ -313,18 +314,24 @@ __device__ __forceinline__ void warp_rows(const SellView& M, const RowMeta (&m)[
             const int t = t0 + lane;
             const bool act = valid && t < m[q].len;
             i32 c;
-            double a;
+            double a, xo = 0.0;
             if (t0 == 0) {
-                c = r[q].c0, a = r[q].a0;
+                c = r[q].c0, a = r[q].a0, xo = r[q].xo0;
             } else if (t0 == 32) {
-                c = r[q].c1, a = r[q].a1;
+                c = r[q].c1, a = r[q].a1, xo = r[q].xo1;
             } else {
                 c = act ? __ldg(M.cols + m[q].base + static_cast<i64>(t) * kSlice) : -1;
                 a = act ? __ldg(M.vals + m[q].base + static_cast<i64>(t) * kSlice) : 0.0;
+                if (SX && act && !is_dep<MODE>(c, row) && c != row) xo = __ldg(xold + c);
             }
             const bool isd = act && MODE != 0 && c == row;
             double xv = 0.0;
-            if (act && !isd) xv = is_dep<MODE>(c, row) ? __ldcg(x + c) : __ldg(xold + c); // xold: GS only
+            if (act && !isd) {
+                if (SX) // the solution lives in shared memory; GS's old values were prefetched
+                    xv = is_dep<MODE>(c, row) ? sx[c] : xo;
+                else
+                    xv = is_dep<MODE>(c, row) ? __ldcg(x + c) : __ldg(xold + c); // xold: GS only
+            }
             prod[q] = a * xv; // the serial loop's rounded product
             dm[q] = __ballot_sync(full, isd);
             if (dm[q]) d[q] = __shfl_sync(full, a, __ffs(dm[q]) - 1);
@@ -340,15 +347,29 @@ __device__ __forceinline__ void warp_rows(const SellView& M, const RowMeta (&m)[
     if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < Q; ++q)
-            if (m[q].row >= 0) x[m[q].row] = MODE == 0 ? s[q] : s[q] / d[q];
+            if (m[q].row >= 0) {
+                const double v = MODE == 0 ? s[q] : s[q] / d[q];
+                if (SX)
+                    sx[m[q].row] = v;
+                else
+                    x[m[q].row] = v;
+            }
     }
 }
 
-template <int MODE, int BLOCK, int Q>
+// SX (one CTA, n <= kSmemXRows): the solution is kept in shared memory, so a
+// row's dependency gathers are shared-memory reads (~30 cycles) instead of L2
+// round trips; the rows' matrix entries and GS's old neighbour values do not
+// depend on the sweep and are prefetched a level ahead as before. x is written
+// back once at the end.
+constexpr i64 kSmemXRows = 16384;
+
+template <int MODE, int BLOCK, int Q, bool SX = false>
 __global__ void __launch_bounds__(BLOCK, 1)
 k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const double* __restrict__ b, double* x,
-              const double* __restrict__ xold) {
+              const double* __restrict__ xold, i64 n) {
     __shared__ i64 slp[kMaxSmemLevels + 1];
+    extern __shared__ double sx[]; // SX: the solution vector
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned csize = cluster_size();
     const i64 gw = static_cast<i64>(cluster_rank()) * (BLOCK / 32) + warp;
@@ -373,6 +394,10 @@ k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const dou
         r.c1 = lane + 32 < m.len ? __ldg(M.cols + m.base + static_cast<i64>(lane + 32) * kSlice) : -1;
         r.a1 = lane + 32 < m.len ? __ldg(M.vals + m.base + static_cast<i64>(lane + 32) * kSlice) : 0.0;
         r.bv = b[m.row];
+        if (SX && MODE == 2) { // GS's old values at columns > row (independent of the sweep)
+            r.xo0 = r.c0 > m.row ? __ldg(xold + r.c0) : 0.0;
+            r.xo1 = r.c1 > m.row ? __ldg(xold + r.c1) : 0.0;
+        }
     };
 
     RowMeta mc[Q], m1[Q], m2[Q];
@@ -389,7 +414,7 @@ k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const dou
             load_data(m1[q], d1[q]);  // level L+1's rows, one level ahead
             load_meta(L + 2, q, m2[q]); // two ahead
         }
-        warp_rows<MODE, Q>(M, mc, dc, lane, x, xold);
+        warp_rows<MODE, Q, SX>(M, mc, dc, lane, x, xold, sx);
         // further rows of a level wider than the cluster's warps x slots
         for (i64 p = slp[L] + gw + Q * GW; p < slp[L + 1]; p += GW) {
             RowMeta m[1];
@@ -399,7 +424,7 @@ k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const dou
             m[0].len = M.rowlen[p];
             m[0].base = M.slice_ptr[p >> 5] + (p & 31);
             load_data(m[0], r[0]);
-            warp_rows<MODE, 1>(M, m, r, lane, x, xold);
+            warp_rows<MODE, 1, SX>(M, m, r, lane, x, xold, sx);
         }
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
@@ -414,6 +439,8 @@ k_levels_warp(SellView M, const i64* __restrict__ level_ptr, int nlev, const dou
             __syncthreads();
         }
     }
+    if (SX) // rows are computed once each; padding rows of the plan never touch sx
+        for (i64 i = threadIdx.x; i < n; i += blockDim.x) x[i] = sx[i];
 }
 
 __global__ void k_epoch_bump(unsigned* epoch, unsigned* ticket) {
@@ -719,6 +746,10 @@ const void* warp_kernel() {
     return reinterpret_cast<const void*>(k_levels_warp<MODE, BLOCK, Q>);
 }
 template <int MODE>
+const void* warp_kernel_sx() {
+    return reinterpret_cast<const void*>(k_levels_warp<MODE, kWarpBlockWide, 1, true>);
+}
+template <int MODE>
 const void* flag_kernel() {
     return reinterpret_cast<const void*>(k_levels_flags<MODE>);
 }
@@ -830,11 +861,12 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // measured: the cluster kernel wins up to a few hundred rows per level
     // (coarse-level GS at 128^3: 258 rows/level 3.3 vs 4.6 ms), the value-flag
     // kernel beyond (ILUT factors at 128^3, 1564 rows/level: 4.9 vs 10.6 ms L)
-    // with the sub-warp value-flag kernel the sync-free schedule also wins on the
-    // coarse AMG levels' Gauss-Seidel (C2 levels 1-4, 8.5 K-1.4 M rows: 1.5-3.0 ms
-    // vs 2.0-13.4 ms per sweep, profiles/r02_gs_forms2.txt); the cluster kernel
-    // keeps the small operators
-    single_cta_ = n <= 4096 || (max_row <= 8 && avg <= 512);
+    // with the sub-warp value-flag kernel the sync-free schedule wins on every
+    // coarse AMG level's Gauss-Seidel, down to a 59-row operator (C2 levels 1-8:
+    // 0.026-2.35 ms vs 0.031-13.6 ms per sweep; C1 levels 1-6 likewise,
+    // profiles/r02_gs_forms4.txt); the cluster kernel keeps the short-row
+    // (7-point ILU(0)) DAGs with narrow levels and the tiny ones
+    single_cta_ = max_row <= 8 && (n <= 4 * kSmallBlock || avg <= 512);
     // wide levels (> 2 rows per warp of a 512-thread cluster): 1024-thread
     // CTAs. ILUG_LEVELSET_WIDE=slots2 takes 512-thread CTAs with two rows per
     // warp prefetched and processed together instead (measured slower at the
@@ -852,6 +884,10 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     }
     cluster_ = 1;
     if (nl > kMaxSmemLevels) old_cta_ = true; // level pointers do not fit the warp kernel's shared memory
+    // shared-memory solution (one CTA): ILUG_LEVELSET=sx forces it where it fits (A/B)
+    sx_ = false;
+    if (const char* force = std::getenv("ILUG_LEVELSET"))
+        if (std::string(force) == "sx" && n > 0 && n <= kSmemXRows && nl <= kMaxSmemLevels) single_cta_ = true, sx_ = true;
     if (single_cta_ && !old_cta_)
         cluster_ = static_cast<int>(
             std::clamp<i64>((max_level_rows_ + block_ / 32 * slots_ - 1) / (block_ / 32 * slots_), 1, cmax));
@@ -889,6 +925,15 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
             ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kSmallBlock), args, 0, st));
             return;
         }
+        i64 nn = M_.nrows;
+        void* wargs[] = {&mv, &lp, &nl, &b, &x, &xold, &nn};
+        if (sx_) { // one CTA, the solution in shared memory
+            const void* fn = mode == 0 ? warp_kernel_sx<0>() : mode == 1 ? warp_kernel_sx<1>() : warp_kernel_sx<2>();
+            const int dyn = static_cast<int>(nn * static_cast<i64>(sizeof(double)));
+            ILUG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+            ILUG_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(kWarpBlockWide), wargs, static_cast<size_t>(dyn), st));
+            return;
+        }
         const bool wide = block_ == kWarpBlockWide, two = slots_ == 2;
         const void* fn =
             mode == 0   ? (wide ? warp_kernel<0, kWarpBlockWide>() : two ? warp_kernel<0, kWarpBlock, 2>() : warp_kernel<0>())
@@ -904,7 +949,7 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
         attr[0].val.clusterDim.y = attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        ILUG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+        ILUG_CUDA(cudaLaunchKernelExC(&cfg, fn, wargs));
         return;
     }
     const i64 n = M_.nrows;

@@ -42,7 +42,8 @@ private:
     int block_ = 512;       // threads per CTA of the warp-per-row cluster kernel
     int slots_ = 1;         // rows per warp prefetched and processed together
     bool value_flags_ = true; // sync-free schedule polls x itself (sentinel-filled) instead of flags
-    int vf_form_ = 0;         // value-flag kernel form: 1 thread per row (8-entry chunks), 8 / 83 lanes per row
+    int vf_form_ = 0;
+    bool sx_ = false;         // one-CTA warp kernel with the solution in shared memory         // value-flag kernel form: 1 thread per row (8-entry chunks), 8 / 83 lanes per row
     i64 max_level_rows_ = 0;
 };
 

@@ -16,7 +16,7 @@ import paper_2111_09512_b200 as ilug  # noqa: E402
 spec = sys.argv[1] if len(sys.argv) > 1 else "pressure27(256,256,256)"
 A = ilug.Matrix.generate(spec)
 H = ilug.Hierarchy(A, ilug.Config().update({"amg.coarsening": "pmis"}), host_only=True)
-forms = [("default", {}), ("cta", {"ILUG_LEVELSET": "cta"}), ("vflags_t16", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "0"}),
+forms = [("default", {}), ("sx", {"ILUG_LEVELSET": "sx"}), ("cta", {"ILUG_LEVELSET": "cta"}), ("vflags_t16", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "0"}),
          ("vflags_t8", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "1"}),
          ("vflags_w8e3", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "83"}),
          ("vflags_w8", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "8"})]
