@@ -277,3 +277,31 @@ def test_dist_solver_nccl_world_one_matches_local(ilug, ref, torch_cuda):
     assert bitwise(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1] and bitwise(outs[0][2], outs[1][2])
     Hr = ref.amg(ref.mat(*A.csr()), ref.cfg(dict(BASE, **kv)))
     assert bitwise(outs[0][0], ref.vcycle(Hr, r, np.zeros(A.rows)))
+
+
+def test_dist_failure_on_one_rank_does_not_hang(ilug, torch_cuda):
+    """A rank that fails (here: an invalid smoother configuration on rank 0
+    only) aborts the in-process group, so its peer's next collective raises
+    instead of waiting forever."""
+    from paper_2111_09512_b200 import dist as idist
+    torch = torch_cuda
+    spec, p = "poisson3d(12,12,12)", 2
+    A = ilug.Matrix.generate(spec)
+    n = A.rows
+    starts = idist.partition(n, p)
+    group = idist.LocalGroup(p)
+    good = {"smoother.kind": "ilu", "trisolve.m_lower": "3", "trisolve.m_upper": "3"}
+    bad = dict(good, **{"scaling": "none"})  # Richardson on unscaled factors: invalid
+
+    def rank_fn(r):
+        comm = group.comm(r)
+        r0, r1 = int(starts[r]), int(starts[r + 1])
+        plan = idist.Plan(idist.generate_rows(spec, r0, r1), n, p, r)
+        plan.exchange(comm)
+        S = idist.Smoother(plan, comm, ilug.Config().update(bad if r == 0 else good))
+        x = torch.zeros(r1 - r0, dtype=torch.float64, device="cuda")
+        S.smooth(torch.ones_like(x), x)  # rank 1 reaches the halo exchange alone
+        return r
+
+    with pytest.raises(ilug.IlugError):
+        idist.run_ranks(p, rank_fn, group)
