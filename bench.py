@@ -40,6 +40,24 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")  # no init banner on stdout (one JSON line)
 
+# stdout carries exactly one JSON line: the real stdout is kept aside and fd 1
+# points at stderr for everything else (library banners such as NCCL's version
+# line on communicator init, prints from native code)
+_JSON_OUT = None
+
+
+def emit(obj):
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
 METRIC = "ILU sweep GB/s (% HBM peak); GMRES+AMG time-to-solution at 1/2/4/8 B200"
 SPEC = "pressure27(256,256,256)"
 SAMPLE_SPEC = "pressure27(256,256,16)"  # CPU baseline sample: 16 of the 256 z-planes
@@ -228,7 +246,7 @@ def run_reference(args):
     sample = spec if full else (SAMPLE_SPEC if not args.strong else "poisson3d(465,465,16)")
     base = ref_smoother_rate(sample, kv, max_steps=max(1, args.steps), budget_s=90.0)
     if base is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref not built"})
         return
     v = base["value"]
     # the reference's own time-to-solution at C1 (run_solve, src/driver.cpp:239-260; single-threaded)
@@ -246,7 +264,7 @@ def run_reference(args):
     why = None if full else (f"full {spec} needs ~{need_gb:.0f} GB host RAM in the reference's int64 CSR layout, "
                              f"{info['mem_available_gb']} GB available (or --ref-sample): a slab of the same "
                              f"matrix family with the same per-row work is timed")
-    print(json.dumps({
+    emit({
         "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": base["steps_timed"],
         "warmup": 0, "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
         "impl": "reference", "dtype": "f64", "data": "synthetic",
@@ -254,7 +272,7 @@ def run_reference(args):
                    "same_config": bool(full), "why_not_same": why,
                    "parallelism": f"reference CPU code, {base['cores']} concurrent calls on rank 0's host"},
         "cpu_baseline": base, "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "tts": {"C1": tts_c1}, "vs_baseline": None}))
+        "tts": {"C1": tts_c1}, "vs_baseline": None})
 
 
 def build_workload(ilug, args, rank, world, local, use_dist=False):
@@ -314,6 +332,7 @@ def main():
     ap.add_argument("--ref-sample", action="store_true",
                     help="reference arm: time the slab sample even when the host could hold the full matrix")
     args = ap.parse_args()
+    _claim_stdout()
     if args.impl == "reference":
         return run_reference(args)
     if args.strong:
@@ -459,7 +478,7 @@ def main():
         if not args.no_tts:
             res["tts"]["C1"] = c1_tts(ilug)
     if rank == 0:
-        print(json.dumps(res))
+        emit(res)
     if use_dist:
         import torch.distributed as dist
         del W
@@ -639,7 +658,7 @@ def run_strong(args):
         except Exception as e:  # report, never lose the bench line
             res["tts"] = {"strong": {"error": str(e)[:300]}}
     if rank == 0:
-        print(json.dumps(res))
+        emit(res)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
