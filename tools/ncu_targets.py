@@ -38,6 +38,7 @@ elif what == "k5l":
 elif what == "step":
     x = torch.rand(n, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
-    S.ilu_sweep(b, x)
+    for _ in range(int(os.environ.get("NCU_REPS", "1"))):  # NCU_REPS > 1: warm repeats (take the last)
+        S.ilu_sweep(b, x)
 torch.cuda.synchronize()
 print("done", what)
