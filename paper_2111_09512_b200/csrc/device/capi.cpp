@@ -604,7 +604,7 @@ int ilug_hierarchy_create_host(const iluamg_matrix* A, const iluamg_config* cfg,
             // host-only handles keep the host setup unless device.amg_setup=device asks for the GPU
             const ilug::AmgParams ap = ilug::amg_params_from(cfg->cfg);
             if (ap.device_setup == 2 && !ilug::amg_device_supported(ap))
-                ilug::fail_invalid("device.amg_setup=device needs amg.coarsening=pmis and amg.interpolation=direct");
+                ilug::fail_invalid("device.amg_setup=device needs amg.coarsening=pmis");
             h->h = ap.device_setup == 2 ? ilug::amg_setup_device(A->A, ap, {}, nullptr) : ilug::amg_setup(A->A, ap);
         } catch (...) {
             delete h;

@@ -7,6 +7,7 @@
 #include <future>
 #include <thread>
 #include <mutex>
+#include <optional>
 #include <deque>
 #include <condition_variable>
 #include <cmath>
@@ -60,6 +61,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
                         bool use_graph, cudaStream_t st) {
     SolveOutcome oc;
     const auto t0 = std::chrono::steady_clock::now();
+    std::optional<DeferFrees> defer(std::in_place); // setup threads must not serialise on cudaFree
     // The finest level's factorisation (ILU(0)/ILUT on the device) runs
     // concurrently with the host AMG setup, which does not need it and does
     // not touch the GPU. Identical factors either way (same function, same input).
@@ -137,7 +139,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
         // the hierarchy itself on the GPU when supported (kernels/amg_setup.cu), else the host
         const bool dev_setup = apd.device_setup != 0 && amg_device_supported(apd);
         if (apd.device_setup == 2 && !dev_setup)
-            fail_invalid("device.amg_setup=device needs amg.coarsening=pmis and amg.interpolation=direct");
+            fail_invalid("device.amg_setup=device needs amg.coarsening=pmis");
         cudaStream_t sst = nullptr;
         if (dev_setup) ILUG_CUDA(cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking));
         StreamGuard sguard{sst};
@@ -166,6 +168,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     dh.prepare_graph();
     GmresWork gw;
     if (kp.restart >= 1) gw.ensure(A.nrows, kp.restart, kp.flexible, kp.max_iters); // else gmres reports it
+    defer.reset();
     oc.setup_seconds = since(t0);
 
     const i64 n = A.nrows;

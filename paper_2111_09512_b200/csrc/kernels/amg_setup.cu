@@ -1,5 +1,5 @@
 // Device AMG setup: strength of connection, PMIS
-// C/F splitting, direct interpolation, the transposes and the Galerkin
+// C/F splitting, direct and MM-ext interpolation, the transposes and the Galerkin
 // product R (A P), level after level on the GPU, bitwise equal to the host
 // setup and the reference (src/amg.cpp:18-390).
 //
@@ -13,6 +13,8 @@
 //    ascending candidate list, like the host;
 //  * direct interpolation: aii, beta, weak summed in the row's entry order,
 //    w = -(a + beta / |C_s|) / (aii + weak), exact zeros dropped;
+//  * MM-ext: the two scaled factors built per F-row (same sums, same zero
+//    rules as the host's triplet assembly), their product by the SpGEMM;
 //  * transposes list each row's columns ascending (entries gathered with
 //    atomics, then every row sorted: a transpose does no arithmetic);
 //  * the Galerkin products use the bitwise SpGEMM of kernels/spgemm.cu.
@@ -216,7 +218,59 @@ __global__ void k_coarse_index(i64 n, const char* __restrict__ isc, const i64* _
 }
 
 // ---- direct interpolation (src/amg.cpp:162-232) --------------------------------
-// pass 0: count (and status); pass 1: fill. Weights are recomputed per pass.
+// Weights of F-row i: returns the status (0 ok, 1 no strong C-neighbour, 2 zero
+// denominator); FILL writes the nonzero weights at pci/pv, otherwise *q counts
+// them. The weights are recomputed per pass instead of being stored.
+template <bool FILL>
+__device__ int direct_row(i64 i, const i64* __restrict__ rp, const i32* __restrict__ ci,
+                          const double* __restrict__ v, const i64* __restrict__ srp, const i32* __restrict__ sci,
+                          const char* __restrict__ isc, const i64* __restrict__ cidx, i64* q, i32* pci, double* pv) {
+    double aii = 0.0, beta = 0.0, weak = 0.0;
+    i64 nc = 0;
+    i64 s = srp[i];
+    const i64 se = srp[i + 1];
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+        const i64 j = ci[k];
+        const double a = v[k];
+        while (s < se && sci[s] < j) ++s;
+        const bool strong = s < se && sci[s] == j;
+        if (j == i) {
+            aii = a;
+        } else if (strong) {
+            if (isc[j])
+                ++nc;
+            else
+                beta += a;
+        } else {
+            weak += a;
+            if (isc[j]) beta += a;
+        }
+    }
+    const double denom = aii + weak;
+    const int code = nc == 0 ? 1 : (denom == 0.0 ? 2 : 0);
+    if (code) {
+        if (!FILL) *q = 0;
+        return code;
+    }
+    const double shift = beta / static_cast<double>(nc);
+    i64 cnt = 0;
+    s = srp[i];
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+        const i64 j = ci[k];
+        while (s < se && sci[s] < j) ++s;
+        const bool strong = s < se && sci[s] == j;
+        if (j == i || !strong || !isc[j]) continue;
+        const double w = -(v[k] + shift) / denom;
+        if (w == 0.0) continue; // the reference's from_triplets drops exact zeros
+        if (FILL)
+            pci[cnt] = static_cast<i32>(cidx[j]), pv[cnt] = w;
+        ++cnt;
+    }
+    if (!FILL) *q = cnt;
+    return 0;
+}
+
+// pass 0: count (and status); pass 1: fill
 template <int PASS>
 __global__ void k_interp(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, const double* __restrict__ v,
                          const i64* __restrict__ srp, const i32* __restrict__ sci, const char* __restrict__ isc,
@@ -233,55 +287,168 @@ __global__ void k_interp(i64 n, const i64* __restrict__ rp, const i32* __restric
             }
             continue;
         }
-        double aii = 0.0, beta = 0.0, weak = 0.0;
-        i64 nc = 0;
+        if (PASS == 0) {
+            const int code = direct_row<false>(i, rp, ci, v, srp, sci, isc, cidx, &cnt[i], nullptr, nullptr);
+            status[i] = code;
+            if (code) atomicMin(first_bad, static_cast<unsigned long long>(i));
+        } else {
+            direct_row<true>(i, rp, ci, v, srp, sci, isc, cidx, nullptr, pci + prp[i], pv + prp[i]);
+        }
+    }
+}
+
+// ---- MM-ext interpolation (src/amg.cpp:235-346) ---------------------------------
+// W = -[(D_FF + D_gamma)^-1 (A^s_FF + D_beta)] [D_beta^-1 A^s_FC] as the host
+// restates it (host/amg.cpp interp_mm_ext): per F-row the sums d_ff, beta
+// (strong C), gamma (weak) in the row's entry order; M1 = the row of
+// (A^s_FF + D_beta) times 1/(d_ff + gamma) with exact zeros dropped (it is built
+// from triplets), M2 = A^s_FC times 1/beta (0 on rows with beta == 0, which
+// fall back to direct weights), zeros kept (a scaled copy); W = M1 M2 by the
+// bitwise SpGEMM, negated.
+struct MmRow {
+    double dff, beta, gamma;
+    i64 nff, nfc;
+};
+__device__ MmRow mm_sums(i64 i, const i64* __restrict__ rp, const i32* __restrict__ ci, const double* __restrict__ v,
+                         const i64* __restrict__ srp, const i32* __restrict__ sci, const char* __restrict__ isc) {
+    MmRow r{0.0, 0.0, 0.0, 0, 0};
+    i64 s = srp[i];
+    const i64 se = srp[i + 1];
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+        const i64 j = ci[k];
+        while (s < se && sci[s] < j) ++s;
+        const bool strong = s < se && sci[s] == j;
+        if (j == i) {
+            r.dff = v[k];
+        } else if (strong) {
+            if (isc[j])
+                r.beta += v[k], ++r.nfc;
+            else
+                ++r.nff;
+        } else {
+            r.gamma += v[k];
+        }
+    }
+    return r;
+}
+
+__global__ void k_mm_count(i64 nf, const i64* __restrict__ fglob, const i64* __restrict__ rp,
+                           const i32* __restrict__ ci, const double* __restrict__ v, const i64* __restrict__ srp,
+                           const i32* __restrict__ sci, const char* __restrict__ isc, double* __restrict__ inv1,
+                           double* __restrict__ inv2, i64* __restrict__ c1, i64* __restrict__ c2,
+                           unsigned long long* __restrict__ bad, unsigned long long* __restrict__ nfb) {
+    GRID_STRIDE(fi, nf) {
+        const i64 i = fglob[fi];
+        const MmRow r = mm_sums(i, rp, ci, v, srp, sci, isc);
+        const double den = r.dff + r.gamma;
+        if (den == 0.0) {
+            atomicMin(bad, static_cast<unsigned long long>(fi));
+            c1[fi] = c2[fi] = 0;
+            continue;
+        }
+        const double inv = 1.0 / den;
+        inv1[fi] = inv;
+        const bool fb = r.beta == 0.0;
+        if (fb) atomicAdd(nfb, 1ull);
+        inv2[fi] = fb ? 0.0 : 1.0 / r.beta;
+        i64 q = r.beta * inv != 0.0;
         i64 s = srp[i];
         const i64 se = srp[i + 1];
         for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
             const i64 j = ci[k];
-            const double a = v[k];
             while (s < se && sci[s] < j) ++s;
-            const bool strong = s < se && sci[s] == j;
-            if (j == i) {
-                aii = a;
-            } else if (strong) {
-                if (isc[j])
-                    ++nc;
-                else
-                    beta += a;
-            } else {
-                weak += a;
-                if (isc[j]) beta += a;
-            }
+            if (j != i && s < se && sci[s] == j && !isc[j]) q += v[k] * inv != 0.0;
         }
-        const double denom = aii + weak;
-        if (PASS == 0) {
-            const int code = nc == 0 ? 1 : (denom == 0.0 ? 2 : 0);
-            status[i] = code;
-            if (code) atomicMin(first_bad, static_cast<unsigned long long>(i));
-            if (code) {
-                cnt[i] = 0;
-                continue;
-            }
+        c1[fi] = q;
+        c2[fi] = r.nfc;
+    }
+}
+
+__global__ void k_mm_fill(i64 nf, const i64* __restrict__ fglob, const i64* __restrict__ floc,
+                          const i64* __restrict__ rp, const i32* __restrict__ ci, const double* __restrict__ v,
+                          const i64* __restrict__ srp, const i32* __restrict__ sci, const char* __restrict__ isc,
+                          const i64* __restrict__ cidx, const double* __restrict__ inv1,
+                          const double* __restrict__ inv2, const i64* __restrict__ m1rp, i32* __restrict__ m1ci,
+                          double* __restrict__ m1v, const i64* __restrict__ m2rp, i32* __restrict__ m2ci,
+                          double* __restrict__ m2v) {
+    GRID_STRIDE(fi, nf) {
+        const i64 i = fglob[fi];
+        const double inv = inv1[fi], ib = inv2[fi];
+        double beta = 0.0;
+        i64 s = srp[i];
+        const i64 se = srp[i + 1];
+        for (i64 k = rp[i]; k < rp[i + 1]; ++k) { // beta again, in entry order
+            const i64 j = ci[k];
+            while (s < se && sci[s] < j) ++s;
+            if (j != i && s < se && sci[s] == j && isc[j]) beta += v[k];
         }
-        const double shift = beta / static_cast<double>(nc);
-        i64 q = 0, o = PASS == 1 ? prp[i] : 0;
+        const double dval = beta * inv;
+        bool dpending = dval != 0.0;
+        i64 o1 = m1rp[fi], o2 = m2rp[fi];
         s = srp[i];
         for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
             const i64 j = ci[k];
             while (s < se && sci[s] < j) ++s;
-            const bool strong = s < se && sci[s] == j;
-            if (j == i || !strong || !isc[j]) continue;
-            const double w = -(v[k] + shift) / denom;
-            if (w == 0.0) continue; // the reference's from_triplets drops exact zeros
-            if (PASS == 0) {
-                ++q;
-            } else {
-                pci[o] = static_cast<i32>(cidx[j]);
-                pv[o++] = w;
+            if (j == i || !(s < se && sci[s] == j)) continue;
+            if (isc[j]) {
+                m2ci[o2] = static_cast<i32>(cidx[j]);
+                m2v[o2++] = v[k] * ib;
+                continue;
             }
+            const i64 fj = floc[j];
+            if (dpending && fj > fi) { // the diagonal in column order
+                m1ci[o1] = static_cast<i32>(fi);
+                m1v[o1++] = dval;
+                dpending = false;
+            }
+            const double w = v[k] * inv;
+            if (w != 0.0) m1ci[o1] = static_cast<i32>(fj), m1v[o1++] = w;
         }
-        if (PASS == 0) cnt[i] = q;
+        if (dpending) m1ci[o1] = static_cast<i32>(fi), m1v[o1] = dval;
+    }
+}
+
+// P: C rows the identity entry, F rows -W (beta != 0) or their direct weights
+template <int PASS>
+__global__ void k_mm_assemble(i64 n, const i64* __restrict__ floc, const double* __restrict__ inv2,
+                              const i64* __restrict__ wrp, const i32* __restrict__ wci, const double* __restrict__ wv,
+                              const i64* __restrict__ rp, const i32* __restrict__ ci, const double* __restrict__ v,
+                              const i64* __restrict__ srp, const i32* __restrict__ sci, const char* __restrict__ isc,
+                              const i64* __restrict__ cidx, i64* __restrict__ cnt, int* __restrict__ status,
+                              unsigned long long* __restrict__ first_bad, const i64* __restrict__ prp,
+                              i32* __restrict__ pci, double* __restrict__ pv) {
+    GRID_STRIDE(i, n) {
+        if (isc[i]) {
+            if (PASS == 0)
+                cnt[i] = 1;
+            else
+                pci[prp[i]] = static_cast<i32>(cidx[i]), pv[prp[i]] = 1.0;
+            continue;
+        }
+        const i64 fi = floc[i];
+        if (inv2[fi] == 0.0) { // fallback: direct weights
+            if (PASS == 0) {
+                const int code = direct_row<false>(i, rp, ci, v, srp, sci, isc, cidx, &cnt[i], nullptr, nullptr);
+                status[i] = code;
+                if (code) atomicMin(first_bad, static_cast<unsigned long long>(i));
+            } else {
+                direct_row<true>(i, rp, ci, v, srp, sci, isc, cidx, nullptr, pci + prp[i], pv + prp[i]);
+            }
+            continue;
+        }
+        if (PASS == 0) {
+            cnt[i] = wrp[fi + 1] - wrp[fi];
+        } else {
+            i64 o = prp[i];
+            for (i64 k = wrp[fi]; k < wrp[fi + 1]; ++k) pci[o] = wci[k], pv[o++] = -wv[k];
+        }
+    }
+}
+
+__global__ void k_not(i64 n, const char* __restrict__ isc, char* __restrict__ isf, i64* __restrict__ cnt) {
+    GRID_STRIDE(i, n) {
+        isf[i] = !isc[i];
+        cnt[i] = !isc[i];
     }
 }
 
@@ -438,9 +605,87 @@ DevCsr interp_direct_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp
     return P;
 }
 
-bool amg_device_supported(const AmgParams& p) {
-    return p.coarsening == Coarsening::pmis && p.interpolation == Interpolation::direct;
+DevCsr interp_mm_ext_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp, i64* fallback_rows,
+                            cudaStream_t st) {
+    const i64 n = A.nrows, nc = sp.n_coarse;
+    const i64 n1 = std::max<i64>(n, 1);
+    // F numbering: floc = exclusive scan of the F flags, fglob = the F rows ascending
+    DBuf<char> isf(n1);
+    DBuf<i64> fcnt(n1), floc(n + 1), idx(n1), fglob(n1);
+    k_not<<<grid_n(n), kB, 0, st>>>(n, sp.is_coarse.p, isf.p, fcnt.p);
+    ILUG_LAUNCH_CHECK();
+    const i64 nf = scan_counts(fcnt.p, floc.p, n, st);
+    k_iota<<<grid_n(n), kB, 0, st>>>(n, idx.p);
+    ILUG_LAUNCH_CHECK();
+    select_flagged(idx.p, isf.p, fglob.p, n, st);
+    const i64 nf1 = std::max<i64>(nf, 1);
+    DBuf<double> inv1(nf1), inv2(nf1);
+    DBuf<i64> c1(nf1), c2(nf1);
+    DBuf<unsigned long long> flags(2); // [0] first singular F-row, [1] fallback rows
+    const unsigned long long init[2] = {~0ull, 0ull};
+    ILUG_CUDA(cudaMemcpyAsync(flags.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    k_mm_count<<<grid_n(nf), kB, 0, st>>>(nf, fglob.p, A.rp.p, A.ci.p, A.v.p, S.rp.p, S.ci.p, sp.is_coarse.p,
+                                           inv1.p, inv2.p, c1.p, c2.p, flags.p, flags.p + 1);
+    ILUG_LAUNCH_CHECK();
+    unsigned long long fl[2] = {0, 0};
+    ILUG_CUDA(cudaMemcpyAsync(fl, flags.p, sizeof fl, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    if (fl[0] != ~0ull) {
+        i64 row = 0;
+        ILUG_CUDA(cudaMemcpy(&row, fglob.p + fl[0], sizeof row, cudaMemcpyDeviceToHost));
+        fail_numeric("interp_mm_ext: singular D_FF + D_gamma at F-row " + std::to_string(row));
+    }
+    if (fallback_rows) *fallback_rows = static_cast<i64>(fl[1]);
+    DevCsr M1, M2, W;
+    M1.nrows = nf, M1.ncols = nf;
+    M2.nrows = nf, M2.ncols = nc;
+    M1.rp.alloc(nf + 1);
+    M2.rp.alloc(nf + 1);
+    M1.ci.alloc(scan_counts(c1.p, M1.rp.p, nf, st));
+    M1.v.alloc(M1.ci.n);
+    M2.ci.alloc(scan_counts(c2.p, M2.rp.p, nf, st));
+    M2.v.alloc(M2.ci.n);
+    k_mm_fill<<<grid_n(nf), kB, 0, st>>>(nf, fglob.p, floc.p, A.rp.p, A.ci.p, A.v.p, S.rp.p, S.ci.p, sp.is_coarse.p,
+                                          sp.coarse_index.p, inv1.p, inv2.p, M1.rp.p, M1.ci.p, M1.v.p, M2.rp.p,
+                                          M2.ci.p, M2.v.p);
+    ILUG_LAUNCH_CHECK();
+    if (!spgemm_device(nf, nc, M1, M2, W, st)) // a row too wide for the tables: the host product
+        W.upload(csr_matmul(M1.download(st), M2.download(st)), st);
+    M1 = DevCsr{};
+    M2 = DevCsr{};
+    DevCsr P;
+    P.nrows = n;
+    P.ncols = nc;
+    DBuf<i64> cnt(n1);
+    DBuf<int> status(n1);
+    const unsigned long long none = ~0ull;
+    ILUG_CUDA(cudaMemcpyAsync(flags.p, &none, sizeof none, cudaMemcpyHostToDevice, st));
+    k_mm_assemble<0><<<grid_n(n), kB, 0, st>>>(n, floc.p, inv2.p, W.rp.p, W.ci.p, W.v.p, A.rp.p, A.ci.p, A.v.p,
+                                                S.rp.p, S.ci.p, sp.is_coarse.p, sp.coarse_index.p, cnt.p, status.p,
+                                                flags.p, nullptr, nullptr, nullptr);
+    ILUG_LAUNCH_CHECK();
+    unsigned long long b = none;
+    ILUG_CUDA(cudaMemcpyAsync(&b, flags.p, sizeof b, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    if (b != none) {
+        int code = 0;
+        ILUG_CUDA(cudaMemcpy(&code, status.p + b, sizeof code, cudaMemcpyDeviceToHost));
+        if (code == 1)
+            fail_invalid("interp_direct: F-point " + std::to_string(b) +
+                         " has no strong C-neighbor (coarsening repair failed)");
+        fail_numeric("interp_direct: zero denominator at row " + std::to_string(b));
+    }
+    P.rp.alloc(n + 1);
+    P.ci.alloc(scan_counts(cnt.p, P.rp.p, n, st));
+    P.v.alloc(P.ci.n);
+    k_mm_assemble<1><<<grid_n(n), kB, 0, st>>>(n, floc.p, inv2.p, W.rp.p, W.ci.p, W.v.p, A.rp.p, A.ci.p, A.v.p,
+                                                S.rp.p, S.ci.p, sp.is_coarse.p, sp.coarse_index.p, nullptr, nullptr,
+                                                nullptr, P.rp.p, P.ci.p, P.v.p);
+    ILUG_LAUNCH_CHECK();
+    return P;
 }
+
+bool amg_device_supported(const AmgParams& p) { return p.coarsening == Coarsening::pmis; }
 
 HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st) {
     if (A.nrows != A.ncols) fail_invalid("setup: matrix must be square");
@@ -448,7 +693,7 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
     if (prm.coarse_size < 1) fail_invalid("setup: coarse_size must be >= 1");
     if (prm.max_levels < 1) fail_invalid("setup: max_levels must be >= 1");
     if (prm.cycles_nu < 1) fail_invalid("setup: cycles_nu must be >= 1");
-    if (!amg_device_supported(prm)) fail_invalid("device AMG setup: PMIS coarsening with direct interpolation only");
+    if (!amg_device_supported(prm)) fail_invalid("device AMG setup: PMIS coarsening only");
     HostHierarchy h;
     h.params = prm;
     h.levels.reserve(static_cast<size_t>(prm.max_levels)); // stable level addresses for on_level
@@ -469,7 +714,9 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
         tm.mark("pmis", k);
         if (static_cast<double>(sp.n_coarse) > 0.95 * static_cast<double>(lev.A.nrows)) break;
         St = DevCsr{};
-        DevCsr P = interp_direct_device(cur, S, sp, st);
+        DevCsr P = prm.interpolation == Interpolation::mm_ext
+                       ? interp_mm_ext_device(cur, S, sp, &lev.mm_ext_fallback_rows, st)
+                       : interp_direct_device(cur, S, sp, st);
         S = DevCsr{};
         DevCsr R = transpose_device(P, true, st);
         tm.mark("interp+transpose", k);

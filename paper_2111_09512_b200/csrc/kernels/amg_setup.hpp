@@ -1,4 +1,4 @@
-// Device AMG setup (kernels/amg_setup.cu): strength, PMIS, direct
+// Device AMG setup (kernels/amg_setup.cu): strength, PMIS, direct and MM-ext
 // interpolation, transposes and the Galerkin product on the GPU, bitwise the
 // host setup (host/amg.cpp) and the reference (src/amg.cpp:18-390).
 #pragma once
@@ -25,8 +25,13 @@ DevSplit pmis_device(const DevCsr& S, const DevCsr& St, std::uint64_t seed, cuda
 /// Direct interpolation (src/amg.cpp:162-232).
 DevCsr interp_direct_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp, cudaStream_t st);
 
-/// PMIS coarsening + direct interpolation (the device path's scope; RS
-/// greedy coarsening and MM-ext interpolation stay on the host).
+/// MM-ext interpolation (src/amg.cpp:235-346); rows with no strong C-neighbour
+/// sum take direct weights, counted in *fallback_rows.
+DevCsr interp_mm_ext_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp, i64* fallback_rows,
+                            cudaStream_t st);
+
+/// PMIS coarsening with direct or MM-ext interpolation (the device path's
+/// scope; the order-dependent RS greedy coarsening stays on the host).
 bool amg_device_supported(const AmgParams& p);
 /// amg_setup on the device: the hierarchy is built level by level on the GPU
 /// and every level's A/P/R/split is handed to the host structures (and to

@@ -38,7 +38,20 @@ void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void d2h_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
 constexpr size_t kStagedMin = size_t{32} << 20; // smaller copies take the plain path
 
-/// Owned device allocation (cudaMalloc / cudaFree), move-only.
+/// cudaFree synchronises the whole device, so a free on one setup thread waits
+/// for every kernel in flight on the others (the AMG setup would wait for the
+/// ILUT factorisation kernel). Inside a DeferFrees scope (any thread) frees are
+/// parked and done when the last scope closes, or when the parked bytes pass a
+/// cap (ILUG_DEFER_FREE=0 disables; A/B).
+void dev_free(void* p, size_t bytes);
+struct DeferFrees {
+    DeferFrees();
+    ~DeferFrees();
+    DeferFrees(const DeferFrees&) = delete;
+    DeferFrees& operator=(const DeferFrees&) = delete;
+};
+
+/// Owned device allocation (cudaMalloc / dev_free), move-only.
 template <typename T>
 struct DBuf {
     T* p = nullptr;
@@ -63,7 +76,7 @@ struct DBuf {
         if (count > 0) ILUG_CUDA(cudaMalloc(&p, static_cast<size_t>(count) * sizeof(T)));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p, static_cast<size_t>(n) * sizeof(T));
         p = nullptr;
         n = 0;
     }

@@ -8,7 +8,9 @@
 // (--fmad=false): bitwise equal to src/sparse.cpp:162-174.
 #include "ops.hpp"
 
+#include <atomic>
 #include <cstring>
+#include <vector>
 #include <mutex>
 
 #include <algorithm>
@@ -27,6 +29,51 @@ namespace ilug {
         e == cudaErrorInsufficientDriver)
         fail_invalid(msg);
     fail_numeric(msg);
+}
+
+namespace {
+std::atomic<int> g_defer{0};
+std::mutex g_defer_mu;
+std::vector<void*> g_deferred;
+size_t g_deferred_bytes = 0;
+constexpr size_t kDeferCap = size_t{16} << 30;
+bool defer_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ILUG_DEFER_FREE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+void free_all(std::vector<void*>& v) {
+    for (void* q : v) cudaFree(q);
+    v.clear();
+}
+} // namespace
+
+void dev_free(void* p, size_t bytes) {
+    if (g_defer.load(std::memory_order_acquire) > 0 && defer_enabled()) {
+        std::vector<void*> flush;
+        {
+            std::lock_guard<std::mutex> g(g_defer_mu);
+            g_deferred.push_back(p);
+            g_deferred_bytes += bytes;
+            if (g_deferred_bytes > kDeferCap) flush.swap(g_deferred), g_deferred_bytes = 0;
+        }
+        free_all(flush);
+        return;
+    }
+    cudaFree(p);
+}
+DeferFrees::DeferFrees() { g_defer.fetch_add(1, std::memory_order_acq_rel); }
+DeferFrees::~DeferFrees() {
+    if (g_defer.fetch_sub(1, std::memory_order_acq_rel) != 1) return;
+    std::vector<void*> flush;
+    {
+        std::lock_guard<std::mutex> g(g_defer_mu);
+        flush.swap(g_deferred);
+        g_deferred_bytes = 0;
+    }
+    free_all(flush);
 }
 
 int device_sm_count() {

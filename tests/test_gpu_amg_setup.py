@@ -1,5 +1,6 @@
 """Device AMG setup (kernels/amg_setup.cu): strength,
-PMIS, direct interpolation, transposes and the Galerkin products on the GPU.
+PMIS, direct and MM-ext interpolation, transposes and the Galerkin products on
+the GPU.
 Every level's A, P and R must be BITWISE the reference's (src/amg.cpp:18-390),
 and the device hierarchy must equal the host setup's at a larger size."""
 import numpy as np
@@ -20,7 +21,9 @@ def _same(a, b):
 
 
 @pytest.mark.parametrize("spec", SPECS)
-@pytest.mark.parametrize("extra", [{}, {"amg.theta": "0.5", "amg.pmis_seed": "7"}, {"amg.coarse_size": "40"}])
+@pytest.mark.parametrize("extra", [{}, {"amg.theta": "0.5", "amg.pmis_seed": "7"}, {"amg.coarse_size": "40"},
+                                   {"amg.interpolation": "mm_ext"},
+                                   {"amg.interpolation": "mm_ext", "amg.theta": "0.5", "amg.pmis_seed": "3"}])
 def test_device_setup_bitwise_reference(ilug, ref, torch_cuda, spec, extra):
     kv = dict(PMIS, **extra)
     A = ilug.Matrix.generate(spec)
@@ -33,17 +36,19 @@ def test_device_setup_bitwise_reference(ilug, ref, torch_cuda, spec, extra):
 
 
 @pytest.mark.parametrize("spec", ["pressure27(48,48,48)", "poisson3d(64,64,64)"])
-def test_device_setup_equals_host_setup(ilug, torch_cuda, spec):
+@pytest.mark.parametrize("interp", ["direct", "mm_ext"])
+def test_device_setup_equals_host_setup(ilug, torch_cuda, spec, interp):
+    kv = dict(PMIS, **{"amg.interpolation": interp})
     A = ilug.Matrix.generate(spec)
-    Hd = ilug.Hierarchy(A, ilug.Config().update(dict(PMIS, **{"device.amg_setup": "device"})), host_only=True)
-    Hh = ilug.Hierarchy(A, ilug.Config().update(dict(PMIS, **{"device.amg_setup": "host"})), host_only=True)
+    Hd = ilug.Hierarchy(A, ilug.Config().update(dict(kv, **{"device.amg_setup": "device"})), host_only=True)
+    Hh = ilug.Hierarchy(A, ilug.Config().update(dict(kv, **{"device.amg_setup": "host"})), host_only=True)
     assert Hd.levels == Hh.levels
     for k in range(Hd.levels):
         for which in ("A", "P", "R") if k + 1 < Hd.levels else ("A",):
             assert _same(Hd.level_matrix(k, which).csr(), Hh.level_matrix(k, which).csr()), f"level {k} {which}"
 
 
-def test_device_setup_requires_pmis_direct(ilug, torch_cuda):
+def test_device_setup_requires_pmis(ilug, torch_cuda):
     A = ilug.Matrix.generate("poisson2d(16,16)")
     with pytest.raises(ilug.IlugError):
         ilug.Hierarchy(A, ilug.Config().update({"device.amg_setup": "device"}), host_only=True)  # rs_greedy
