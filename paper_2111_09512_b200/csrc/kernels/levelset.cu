@@ -701,7 +701,7 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
     }
 }
 
-int vf_sub_override() { // ILUG_VF_SUB (A/B): 0 / 1 thread per row (16- / 8-entry chunks), 2 / 4 / 8 / 83 / 16 lanes
+int vf_sub_override() { // ILUG_VF_SUB (A/B): 0 / 1 thread per row (16- / 8-entry chunks), 2 / 4 / 8 / 83 / 16 / 88 / 164 / 168 / 324 lanes (x entries)
     const char* e = std::getenv("ILUG_VF_SUB");
     return e ? std::atoi(e) : -1;
 }
@@ -720,7 +720,22 @@ const void* vsub_kernel(int w) {
     case 8: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 8>);
     case 83: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 8, 3>); // 24 entries per pass
     case 16: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 16>);
+    case 88: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 8, 8>);   // 64 entries per pass
+    case 164: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 16, 4>); // 64
+    case 168: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 16, 8>); // 128
+    case 324: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 32, 4>); // 128
     default: return reinterpret_cast<const void*>(k_levels_vsub<MODE, 4>);
+    }
+}
+
+// lanes per row of a sub-warp form code (0: a thread-per-row form)
+int vsub_lanes(int w) {
+    switch (w) {
+    case 2: case 4: case 8: case 16: return w;
+    case 83: case 88: return 8;
+    case 164: case 168: return 16;
+    case 324: return 32;
+    default: return 0;
     }
 }
 
@@ -854,10 +869,19 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // for L rows up to 24 entries, 4 otherwise
     i64 max_row = 0;
     for (i64 i = 0; i < n; ++i) max_row = std::max(max_row, T.rp[i + 1] - T.rp[i]);
+    // rows longer than one 32-entry pass (coarse AMG operators: 36-115 entries
+    // at C2) take every entry in ONE pass, or the next pass's values/columns
+    // load only after the previous pass's dependencies arrived — a memory round
+    // trip per pass on every level's critical path (C2 GS levels 2-6: 2.97 /
+    // 2.29 / 1.48 / 0.68 / 0.22 -> 2.0 / 1.28 / 0.78 / 0.35 / 0.14 ms,
+    // profiles/r02_gs_forms5.txt): 16 lanes x 8 entries where levels are wide,
+    // a whole warp x 4 entries (one row per warp) where they are narrow
     if (max_row <= 8)
         vf_form_ = kind == Kind::lower_unit ? 1 : 0;
-    else
+    else if (max_row <= 32)
         vf_form_ = kind == Kind::lower_unit && max_row <= 24 ? 83 : 8;
+    else
+        vf_form_ = avg > 150 ? 168 : 324;
     // measured: the cluster kernel wins up to a few hundred rows per level
     // (coarse-level GS at 128^3: 258 rows/level 3.3 vs 4.6 ms), the value-flag
     // kernel beyond (ILUT factors at 128^3, 1564 rows/level: 4.9 vs 10.6 ms L)
@@ -967,8 +991,8 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
         int grid = grid_;
         if (const int cap = vf_warps_per_sm(); cap > 0)
             grid = std::max(1, std::min(grid, device_sm_count() * cap / (kFlagBlock / 32)));
-        if (w == 2 || w == 4 || w == 8 || w == 83 || w == 16) {
-            i64 ng = ns * (w == 83 ? 8 : w);
+        if (const int lanes = vsub_lanes(w); lanes > 0) {
+            i64 ng = ns * lanes;
             unsigned sl = vf_sleep_ns();
             void* args[] = {&mv, &ng, &b, &x, &xold, &ticket, &sl};
             const void* fn = mode == 0 ? vsub_kernel<0>(w) : mode == 1 ? vsub_kernel<1>(w) : vsub_kernel<2>(w);

@@ -240,7 +240,10 @@ def test_k5_both_schedules_bitwise(ilug, ref, torch_cuda, monkeypatch, schedule,
     assert bitwise(_host(xd), want)
 
 
-@pytest.mark.parametrize("sub", ["0", "1", "2", "4", "8", "83", "16"])
+VF_FORMS = ["0", "1", "2", "4", "8", "83", "16", "88", "164", "168", "324"]
+
+
+@pytest.mark.parametrize("sub", VF_FORMS)
 @pytest.mark.parametrize("spec,kv", [("poisson3d(40,40,30)", {}),
                                      ("pressure27(24,24,20)", {"ilu.variant": "ilut", "ilu.droptol": "1e-3",
                                                                "ilu.lfill": "5"})])
@@ -266,6 +269,33 @@ def test_k5_value_flag_forms_bitwise(ilug, ref, torch_cuda, monkeypatch, sub, sp
     Ar = ref.mat(*A.csr())
     want, _ = ref.smooth(Ar, ref.smoother(Ar, ref.cfg({"smoother.kind": "gauss_seidel"})), b, x0)
     assert bitwise(_host(xd), want)
+
+
+@pytest.mark.parametrize("sub", [""] + VF_FORMS)
+def test_k5_long_rows_gs_bitwise(ilug, ref, torch_cuda, monkeypatch, sub):
+    """Gauss-Seidel on coarse AMG operators (rows of 40-110 entries: several
+    32-entry passes for the narrow forms, one pass for the 64/128-entry
+    forms the default picks there) bitwise the reference's sweep."""
+    monkeypatch.setenv("ILUG_LEVELSET", "vflags")
+    if sub:
+        monkeypatch.setenv("ILUG_VF_SUB", sub)
+    A = ilug.Matrix.generate("pressure27(40,40,40)")
+    H = ilug.Hierarchy(A, ilug.Config().update({"amg.coarsening": "pmis"}), host_only=True)
+    widths = []
+    for lvl in range(1, min(H.levels - 1, 5)):
+        M = H.level_matrix(lvl, "A")
+        rp, ci, v = M.csr()
+        widths.append(int(np.diff(rp).max()))
+        b = np.random.default_rng(40 + lvl).uniform(-1, 1, M.rows)
+        x0 = np.random.default_rng(50 + lvl).uniform(-1, 1, M.rows)
+        S = ilug.Smoother(M, ilug.Config().update({"smoother.kind": "gauss_seidel", "smoother.sweeps": "2"}))
+        xd = _dev(torch_cuda, x0)
+        S.smooth(_dev(torch_cuda, b), xd)
+        Mr = ref.mat(rp, ci, v)
+        want, _ = ref.smooth(Mr, ref.smoother(Mr, ref.cfg({"smoother.kind": "gauss_seidel",
+                                                           "smoother.sweeps": "2"})), b, x0)
+        assert bitwise(_host(xd), want), f"level {lvl}"
+    assert max(widths) > 64
 
 
 @pytest.mark.parametrize("schedule", ["", "cta", "flags", "vflags"])

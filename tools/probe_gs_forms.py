@@ -16,10 +16,11 @@ import paper_2111_09512_b200 as ilug  # noqa: E402
 spec = sys.argv[1] if len(sys.argv) > 1 else "pressure27(256,256,256)"
 A = ilug.Matrix.generate(spec)
 H = ilug.Hierarchy(A, ilug.Config().update({"amg.coarsening": "pmis"}), host_only=True)
-forms = [("default", {}), ("sx", {"ILUG_LEVELSET": "sx"}), ("cta", {"ILUG_LEVELSET": "cta"}), ("vflags_t16", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "0"}),
-         ("vflags_t8", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "1"}),
-         ("vflags_w8e3", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "83"}),
-         ("vflags_w8", {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": "8"})]
+FORMS = {"default": {}, "sx": {"ILUG_LEVELSET": "sx"}, "cta": {"ILUG_LEVELSET": "cta"}}
+for code in ("0", "1", "83", "8", "88", "164", "168", "324"):
+    FORMS["vf" + code] = {"ILUG_LEVELSET": "vflags", "ILUG_VF_SUB": code}
+# FORMS env var: comma-separated subset (default: all)
+forms = [(k, FORMS[k]) for k in (os.environ.get("FORMS") or ",".join(FORMS)).split(",")]
 for lvl in range(1, H.levels - 1):
     M = H.level_matrix(lvl, "A")
     rp, _, _ = M.csr()
