@@ -874,14 +874,16 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     // load only after the previous pass's dependencies arrived — a memory round
     // trip per pass on every level's critical path (C2 GS levels 2-6: 2.97 /
     // 2.29 / 1.48 / 0.68 / 0.22 -> 2.0 / 1.28 / 0.78 / 0.35 / 0.14 ms,
-    // profiles/r02_gs_forms5.txt): 16 lanes x 8 entries where levels are wide,
-    // a whole warp x 4 entries (one row per warp) where they are narrow
+    // profiles/r02_gs_forms5.txt): 16 lanes x 8 entries where levels are wide
+    // (> 200 rows on average: C2 levels 1-2), a whole warp x 4 entries (one row
+    // per warp) where they are narrower (C1/C3 level 1, ~198 rows per level:
+    // 0.55 vs 0.64 ms, profiles/r02_gs_forms_c1.txt)
     if (max_row <= 8)
         vf_form_ = kind == Kind::lower_unit ? 1 : 0;
     else if (max_row <= 32)
         vf_form_ = kind == Kind::lower_unit && max_row <= 24 ? 83 : 8;
     else
-        vf_form_ = avg > 150 ? 168 : 324;
+        vf_form_ = avg > 200 ? 168 : 324;
     // measured: the cluster kernel wins up to a few hundred rows per level
     // (coarse-level GS at 128^3: 258 rows/level 3.3 vs 4.6 ms), the value-flag
     // kernel beyond (ILUT factors at 128^3, 1564 rows/level: 4.9 vs 10.6 ms L)
