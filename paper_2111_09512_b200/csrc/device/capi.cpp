@@ -389,7 +389,7 @@ int ilug_sweep_upper_host(const ilug_factors* f, const double* bh, double* xh, l
 int ilug_solve_lower(const ilug_factors* f, const double* b, double* y, void* stream) {
     return guarded([&] {
         need(f && b && y);
-        f->f.solve_lower(b, y, S(stream));
+        f->ser.run(S(stream), [&] { f->f.solve_lower(b, y, S(stream)); });
         ilug::levelset_check_error(S(stream));
         return ILUAMG_OK;
     });
@@ -398,7 +398,7 @@ int ilug_solve_upper(const ilug_factors* f, const double* b, double* x, void* st
     return guarded([&] {
         need(f && b && x);
         Ws ws(f->f.n(), S(stream));
-        f->f.solve_upper(b, x, ws.p, S(stream));
+        f->ser.run(S(stream), [&] { f->f.solve_upper(b, x, ws.p, S(stream)); });
         ilug::levelset_check_error(S(stream));
         return ILUAMG_OK;
     });
@@ -490,12 +490,16 @@ int ilug_smoother_create(const iluamg_matrix* A, const iluamg_config* cfg, int w
 int ilug_smooth(const ilug_smoother* s, const double* b, double* x, double* resnorm, void* stream) {
     return guarded([&] {
         need(s && b && x);
-        s->s.smooth(b, x, false, S(stream));
+        double h = 0.0;
+        s->ser.run(S(stream), [&] {
+            s->s.smooth(b, x, false, S(stream));
+            if (resnorm) {
+                ilug::residual(s->dA.A, x, b, s->r.p, S(stream));
+                ilug::nrm2sq_dev(s->r.p, s->A.nrows, s->scratch.p, s->scratch.p + 1, S(stream));
+                ILUG_CUDA(cudaMemcpyAsync(&h, s->scratch.p, sizeof h, cudaMemcpyDeviceToHost, S(stream)));
+            }
+        });
         if (resnorm) {
-            ilug::residual(s->dA.A, x, b, s->r.p, S(stream));
-            ilug::nrm2sq_dev(s->r.p, s->A.nrows, s->scratch.p, s->scratch.p + 1, S(stream));
-            double h = 0.0;
-            ILUG_CUDA(cudaMemcpyAsync(&h, s->scratch.p, sizeof h, cudaMemcpyDeviceToHost, S(stream)));
             ILUG_CUDA(cudaStreamSynchronize(S(stream)));
             *resnorm = std::sqrt(h);
         }
@@ -507,7 +511,7 @@ int ilug_ilu_smooth_sweep(const ilug_smoother* s, const double* b, double* x, vo
         need(s && b && x);
         if (s->s.config().kind != ilug::SmootherKind::ilu)
             ilug::fail_invalid("ilu_smooth_sweep: smoother is not an ILU smoother");
-        s->s.ilu_sweep(b, x, false, S(stream));
+        s->ser.run(S(stream), [&] { s->s.ilu_sweep(b, x, false, S(stream)); });
         return ILUAMG_OK;
     });
 }
@@ -515,20 +519,24 @@ int ilug_smooth_host(const ilug_smoother* s, const double* bh, double* xh) {
     return guarded([&] {
         need(s && bh && xh);
         const ilug::i64 n = s->A.nrows;
-        if (s->hb.n != n) s->hb.alloc(n), s->hx.alloc(n); // persistent staging buffers
-        s->hb.upload(bh, n);
-        s->hx.upload(xh, n);
-        s->s.smooth(s->hb.p, s->hx.p, false, nullptr);
-        s->hx.download(xh);
-        ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        s->ser.run_sync([&] {
+            if (s->hb.n != n) s->hb.alloc(n), s->hx.alloc(n); // persistent staging buffers
+            s->hb.upload(bh, n);
+            s->hx.upload(xh, n);
+            s->s.smooth(s->hb.p, s->hx.p, false, nullptr);
+            s->hx.download(xh);
+            ILUG_CUDA(cudaStreamSynchronize(nullptr));
+        });
         return ILUAMG_OK;
     });
 }
 int ilug_smooth_host_many(const ilug_smoother* s, long long count, const double* const* bh, double* const* xh) {
     return guarded([&] {
         need(s && count >= 0 && (count == 0 || (bh && xh)));
-        s->pipe.run(s->A.nrows, count, bh, xh,
-                    [&](const double* b, double* x, cudaStream_t st) { s->s.smooth(b, x, false, st); });
+        s->ser.run_sync([&] {
+            s->pipe.run(s->A.nrows, count, bh, xh,
+                        [&](const double* b, double* x, cudaStream_t st) { s->s.smooth(b, x, false, st); });
+        });
         return ILUAMG_OK;
     });
 }
@@ -668,7 +676,7 @@ int ilug_vcycle(ilug_hierarchy* h, const double* r, double* z, void* stream) {
     return guarded([&] {
         need(h && r && z);
         if (!h->on_device) ilug::fail_invalid("vcycle: hierarchy was created host-only");
-        h->d.vcycle(r, z, S(stream));
+        h->ser.run(S(stream), [&] { h->d.vcycle(r, z, S(stream)); });
         return ILUAMG_OK;
     });
 }
@@ -693,8 +701,10 @@ int ilug_gmres(ilug_hierarchy* h, const iluamg_config* cfg, const double* b, dou
         p.anorm_seed = static_cast<std::uint64_t>(c.get_index("krylov.anorm_seed"));
         p.form_iterates = c.get_bool("krylov.form_iterates");
         p.estimate_anorm = p.form_iterates || p.nrbe_criterion;
-        const ilug::KrylovReport r =
-            ilug::device_gmres(h->d.A0(), &h->h.levels[0].A, ilug::vcycle_of(h->d), b, x, p, S(stream));
+        ilug::KrylovReport r;
+        h->ser.run(S(stream), [&] {
+            r = ilug::device_gmres(h->d.A0(), &h->h.levels[0].A, ilug::vcycle_of(h->d), b, x, p, S(stream));
+        });
         ILUG_CUDA(cudaStreamSynchronize(S(stream)));
         if (iterations) *iterations = r.iterations;
         if (final_relres) *final_relres = r.final_relres;

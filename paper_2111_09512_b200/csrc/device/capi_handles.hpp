@@ -10,8 +10,48 @@
 #include "host_pipeline.hpp"
 
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
+
+namespace ilug {
+/// Calls on one handle from several host threads / streams share the handle's
+/// device workspaces (level vectors, smoother scratch, level-set tickets). The
+/// reference's contract is that concurrent V-cycles / smoothing on distinct
+/// right-hand sides are safe and equal to serial calls bit for bit
+/// (README.md:152-154, tests/test_amg.cpp:337-354), so each call's device work
+/// is ordered after the previous call's (an event on that call's stream; the
+/// host-side enqueue under a mutex). Same-stream callers pay one event record.
+struct HandleSerial {
+    std::mutex m;
+    cudaEvent_t done = nullptr;
+    bool armed = false;
+    HandleSerial() = default;
+    HandleSerial(const HandleSerial&) = delete;
+    HandleSerial& operator=(const HandleSerial&) = delete;
+    ~HandleSerial() {
+        if (done) cudaEventDestroy(done);
+    }
+    /// f enqueues device work on st
+    template <class F>
+    void run(cudaStream_t st, F&& f) {
+        std::lock_guard<std::mutex> g(m);
+        if (!done) ILUG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        if (armed) ILUG_CUDA(cudaStreamWaitEvent(st, done, 0));
+        f();
+        ILUG_CUDA(cudaEventRecord(done, st));
+        armed = true;
+    }
+    /// f is host-synchronous (its own streams, synchronised before it returns)
+    template <class F>
+    void run_sync(F&& f) {
+        std::lock_guard<std::mutex> g(m);
+        if (armed) ILUG_CUDA(cudaEventSynchronize(done));
+        armed = false;
+        f();
+    }
+};
+} // namespace ilug
 
 struct iluamg_matrix_s {
     ilug::Csr A;
@@ -35,6 +75,7 @@ struct ilug_factors_s {
     ilug::RawVec<ilug::i64> a_rp;
     std::uint64_t a_hash = 0;
     std::unique_ptr<ilug::Ilu0Symbolic> sym;
+    mutable ilug::HandleSerial ser; // direct solves share the level-set tickets
 };
 struct ilug_dmatrix_s {
     ilug::DeviceMatrix M;
@@ -46,11 +87,13 @@ struct ilug_smoother_s {
     ilug::DBuf<double> r, scratch;
     mutable ilug::DBuf<double> hb, hx; // staging for the host-buffer entry point
     mutable ilug::HostPipeline pipe;   // ilug_smooth_host_many
+    mutable ilug::HandleSerial ser;
 };
 struct ilug_hierarchy_s {
     ilug::HostHierarchy h;
     ilug::DeviceHierarchy d;
     bool on_device = false;
+    ilug::HandleSerial ser;
 };
 struct ilug_dist_plan_s {
     ilug::HaloPlan plan;
