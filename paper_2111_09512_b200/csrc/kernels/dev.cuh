@@ -117,8 +117,16 @@ struct Sell {
     DBuf<i32> cols;
     DBuf<double> vals;
     DBuf<i32> perm; ///< empty = identity
+    /// Dictionary-coded columns (SELL-D8): when a matrix has at most 255
+    /// distinct column offsets c - row (stencil operators and their ILU
+    /// factors: 27 / 30 / 84 at C2), codes[q] indexes offtab and the sweep
+    /// kernels read 1 byte per entry instead of 4 (col = row + offtab[code]).
+    /// cols stays for the other consumers. Empty = not coded.
+    DBuf<std::uint8_t> codes;
+    DBuf<i32> offtab; ///< kOffTab entries (unused slots 0)
     bool empty() const { return nrows == 0; }
 };
+constexpr int kOffTab = 256;
 
 /// Kernel-side view (trivially copyable).
 struct SellView {
@@ -128,9 +136,11 @@ struct SellView {
     const double* __restrict__ vals;
     const i32* __restrict__ perm;
     i64 nrows_pad;
+    const std::uint8_t* __restrict__ codes;
+    const i32* __restrict__ offtab;
 };
 inline SellView view(const Sell& s) {
-    return {s.slice_ptr.p, s.rowlen.p, s.cols.p, s.vals.p, s.perm.p, s.nrows_pad};
+    return {s.slice_ptr.p, s.rowlen.p, s.cols.p, s.vals.p, s.perm.p, s.nrows_pad, s.codes.p, s.offtab.p};
 }
 
 int device_sm_count();
@@ -148,6 +158,11 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 __device__ __forceinline__ int ld_stream(const int* p) {
     int v;
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ unsigned ld_stream(const std::uint8_t* p) {
+    unsigned v;
+    asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 // Gathered vector entries: read-only path, cached (stencil reuse across rows).

@@ -853,7 +853,7 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     rp.upload(T.rp.data(), n + 1, st);
     ci.upload(T.ci.data(), T.nnz(), st);
     if (!dev_vals) v.upload(T.v.data(), T.nnz(), st);
-    sell_from_device_csr(M_, T, rp.p, ci.p, dev_vals ? dev_vals : v.p, Part::all, perm, st);
+    sell_from_device_csr(M_, T, rp.p, ci.p, dev_vals ? dev_vals : v.p, Part::all, perm, st, false);
 
     // Level-synchronous on one cluster (warp per row) unless the levels
     // are wider than the cluster's warps can take in one pass on average (then

@@ -22,7 +22,11 @@ i64 sell_sigma();
 /// entries equal to -1 are padding rows.
 void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i32* ci,
                           const double* v, Part part, const std::vector<i32>& perm_host,
-                          cudaStream_t s);
+                          cudaStream_t s, bool encode = true);
+/// Dictionary-code the columns (Sell::codes) when the matrix has <= 255
+/// distinct offsets c - row; otherwise leaves it uncoded. The builders call it.
+void sell_encode(Sell& M, cudaStream_t s);
+bool sell_d8_enabled();
 
 /// Same from device CSR arrays when only the row starts are on the host: the
 /// selected part of row r has rp_host[r+1] - rp_host[r] - skip entries (skip =

@@ -9,6 +9,7 @@
 #include "ops.hpp"
 
 #include <atomic>
+#include <climits>
 #include <cstring>
 #include <vector>
 #include <mutex>
@@ -358,9 +359,17 @@ __global__ void __launch_bounds__(kBlock) k_rowdot_split(SellView M, i64 nrows, 
 // so there is no branch for the compiler to sink the loads past and the row's
 // metadata costs one memory round trip instead of two (SASS without it:
 // LDG perm -> EXIT -> LDG rowlen/slice_ptr).
-template <class Epi, bool HINT, bool PTAIL = true, bool HOIST = true, bool EARLY = Epi::kEarly>
+// D8: the columns come from the dictionary-coded byte stream (Sell::codes),
+// col = row + offtab[code] with the table in shared memory — 9 instead of 12
+// streamed bytes per entry, the same entries in the same order (bitwise).
+template <class Epi, bool HINT, bool PTAIL = true, bool HOIST = true, bool EARLY = Epi::kEarly, bool D8 = false>
 __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const double* __restrict__ x,
                                                     Epi epi) {
+    __shared__ i32 s_off[D8 ? kOffTab : 1];
+    if constexpr (D8) {
+        for (int i = threadIdx.x; i < kOffTab; i += blockDim.x) s_off[i] = __ldg(M.offtab + i);
+        __syncthreads();
+    }
     const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
     if (p >= M.nrows_pad) return;
     int len = 0;
@@ -384,10 +393,15 @@ __global__ void __launch_bounds__(kBlock) k_rowdot(SellView M, i64 nrows, const 
     }
     const double* vp = M.vals + sp + (p & 31);
     const int* cp = M.cols + sp + (p & 31);
+    const std::uint8_t* dp = D8 ? M.codes + sp + (p & 31) : nullptr;
+    const int r32 = static_cast<int>(row);
     unsigned long long pf = 0, pl = 0;
     if (HINT) pf = l2_policy_first(), pl = l2_policy_last();
     auto lv = [&](int t) { return HINT ? ld_stream(vp + t * kSlice, pf) : ld_stream(vp + t * kSlice); };
-    auto lc = [&](int t) { return HINT ? ld_stream(cp + t * kSlice, pf) : ld_stream(cp + t * kSlice); };
+    auto lc = [&](int t) -> int {
+        if constexpr (D8) return r32 + s_off[ld_stream(dp + t * kSlice)];
+        else return HINT ? ld_stream(cp + t * kSlice, pf) : ld_stream(cp + t * kSlice);
+    };
     auto lx = [&](int c) { return HINT ? ld_gather(x + c, pl) : ld_gather(x + c); };
     double s = 0.0;
     int t = 0;
@@ -652,6 +666,9 @@ void launch_rowdot(const Sell& M, const double* x, Epi epi, cudaStream_t st) {
         k_rowdot<Epi, false, true, true, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else if (!rowdot_hoist())
         k_rowdot<Epi, false, true, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
+    else if (M.codes.p)
+        k_rowdot<Epi, false, true, true, Epi::kEarly, true>
+            <<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     else
         k_rowdot<Epi, false><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, epi);
     ILUG_LAUNCH_CHECK();
@@ -855,11 +872,135 @@ std::vector<i32> sigma_order(i64 n, LenOf len_of) {
     return perm;
 }
 
+// ------------------------------------------------------- SELL-D8 coding
+// Distinct column offsets c - row of a SELL matrix: each CTA gathers its rows'
+// offsets into a shared-memory open-addressing set (plain reads first, CAS
+// only on an empty slot, so the hot keys cost no atomics), then merges its
+// keys into a global set; more than 255 distinct offsets anywhere leaves the
+// matrix uncoded.
+constexpr int kGSet = 1024, kCSet = 512;
+constexpr i32 kNoKey = INT_MIN;
+__device__ __forceinline__ unsigned off_hash(i32 v) { return (static_cast<unsigned>(v) * 2654435761u) >> 16; }
+
+__global__ void k_fill_i32(i32* a, int n, i32 v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = v;
+}
+
+// insert v into set[cap] (probing); returns 1 if newly inserted, 0 if present, -1 if full
+template <int CAP>
+__device__ int set_insert(volatile i32* set, i32 v) {
+    unsigned h = off_hash(v) & (CAP - 1);
+    for (int probe = 0; probe < CAP; ++probe) {
+        i32 cur = set[h];
+        if (cur == v) return 0;
+        if (cur == kNoKey) {
+            cur = atomicCAS(const_cast<i32*>(set) + h, kNoKey, v);
+            if (cur == kNoKey) return 1;
+            if (cur == v) return 0;
+        }
+        h = (h + 1) & (CAP - 1);
+    }
+    return -1;
+}
+
+__global__ void k_offsets_collect(SellView M, i64 nrows, i32* gset, unsigned* gstat) {
+    __shared__ i32 set[kCSet];
+    __shared__ int full;
+    for (int i = threadIdx.x; i < kCSet; i += blockDim.x) set[i] = kNoKey;
+    if (threadIdx.x == 0) full = 0;
+    __syncthreads();
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p < M.nrows_pad) {
+        const i64 row = M.perm ? M.perm[p] : p;
+        if (row >= 0 && row < nrows) {
+            const int len = M.rowlen[p];
+            const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+            for (int t = 0; t < len && !full; ++t)
+                if (set_insert<kCSet>(set, static_cast<i32>(M.cols[base + static_cast<i64>(t) * kSlice] - row)) < 0)
+                    full = 1;
+        }
+    }
+    __syncthreads();
+    if (full) {
+        if (threadIdx.x == 0) atomicOr(gstat + 1, 1u);
+        return;
+    }
+    for (int i = threadIdx.x; i < kCSet; i += blockDim.x) {
+        const i32 v = set[i];
+        if (v == kNoKey) continue;
+        const int r = set_insert<kGSet>(gset, v);
+        if (r > 0) atomicAdd(gstat, 1u);
+        if (r < 0) atomicOr(gstat + 1, 1u);
+    }
+}
+
+__global__ void k_offsets_encode(SellView M, i64 nrows, const i32* __restrict__ tab, int ntab,
+                                 std::uint8_t* __restrict__ codes) {
+    __shared__ i32 t_s[kOffTab];
+    for (int i = threadIdx.x; i < kOffTab; i += blockDim.x) t_s[i] = i < ntab ? tab[i] : INT_MAX;
+    __syncthreads();
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= M.nrows_pad) return;
+    const i64 row = M.perm ? M.perm[p] : p;
+    if (row < 0 || row >= nrows) return;
+    const int len = M.rowlen[p];
+    const i64 base = M.slice_ptr[p >> 5] + (p & 31);
+    for (int t = 0; t < len; ++t) {
+        const i64 q = base + static_cast<i64>(t) * kSlice;
+        const i32 off = static_cast<i32>(M.cols[q] - row);
+        int lo = 0, hi = ntab - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (t_s[mid] < off)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        codes[q] = static_cast<std::uint8_t>(lo);
+    }
+}
+
 } // namespace
+
+bool sell_d8_enabled() { // ILUG_SELL_D8=0: int32 column stream only (A/B; read at every build)
+    const char* e = std::getenv("ILUG_SELL_D8");
+    return !(e && e[0] == '0');
+}
+
+void sell_encode(Sell& M, cudaStream_t st) {
+    M.codes.release();
+    M.offtab.release();
+    if (!sell_d8_enabled() || M.nrows_pad == 0 || M.padded == 0 || M.nnz == 0) return;
+    DBuf<i32> gset(kGSet);
+    DBuf<unsigned> gstat(2);
+    k_fill_i32<<<(kGSet + 255) / 256, 256, 0, st>>>(gset.p, kGSet, kNoKey);
+    ILUG_CUDA(cudaMemsetAsync(gstat.p, 0, 2 * sizeof(unsigned), st));
+    k_offsets_collect<<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, gset.p, gstat.p);
+    ILUG_LAUNCH_CHECK();
+    unsigned stat[2] = {0, 0};
+    std::vector<i32> keys(kGSet);
+    ILUG_CUDA(cudaMemcpyAsync(stat, gstat.p, sizeof stat, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaMemcpyAsync(keys.data(), gset.p, kGSet * sizeof(i32), cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    if (stat[1] || stat[0] == 0 || stat[0] >= static_cast<unsigned>(kOffTab)) return;
+    std::vector<i32> tab;
+    for (i32 k : keys)
+        if (k != kNoKey) tab.push_back(k);
+    std::sort(tab.begin(), tab.end());
+    const int ntab = static_cast<int>(tab.size());
+    tab.resize(kOffTab, 0);
+    M.offtab.upload(tab.data(), kOffTab, st);
+    M.codes.alloc(M.padded);
+    ILUG_CUDA(cudaMemsetAsync(M.codes.p, 0, static_cast<size_t>(M.padded), st));
+    k_offsets_encode<<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, M.offtab.p, ntab, M.codes.p);
+    ILUG_LAUNCH_CHECK();
+    ILUG_CUDA(cudaStreamSynchronize(st)); // the host table dies here
+}
 
 void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i32* ci,
                           const double* v, Part part, const std::vector<i32>& perm_in,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool encode) {
     out.nrows = pattern.nrows;
     out.ncols = pattern.ncols;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
@@ -874,6 +1015,10 @@ void sell_from_device_csr(Sell& out, const Csr& pattern, const i64* rp, const i3
                                                      out.slice_ptr.p, out.cols.p, out.vals.p);
         ILUG_LAUNCH_CHECK();
     }
+    if (encode)
+        sell_encode(out, s);
+    else
+        out.codes.release(), out.offtab.release();
 }
 
 void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& rp_host, i64 skip, const i64* rp,
@@ -893,6 +1038,7 @@ void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& r
                                                      out.cols.p, out.vals.p);
         ILUG_LAUNCH_CHECK();
     }
+    sell_encode(out, s);
 }
 
 void sell_refill(Sell& M, const i64* rp, const i32* ci, const double* v, Part part, cudaStream_t s) {
@@ -913,6 +1059,7 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     const i64 pad = perm.empty() ? (A.nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
     layout(out, pad, perm, [&](i64 row) { return part_len(A, row, pc); }, s);
     tm.mark("layout+upload");
+    out.codes.release(), out.offtab.release();
     if (A.nnz() == 0 || pad == 0) return;
     DBuf<i64> rp;
     DBuf<i32> ci;
@@ -927,6 +1074,8 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     ILUG_LAUNCH_CHECK();
     ILUG_CUDA(cudaStreamSynchronize(s)); // temporaries die at scope exit
     tm.mark("fill");
+    sell_encode(out, s);
+    tm.mark("encode");
 }
 
 Csr sell_to_host(const Sell& M) {

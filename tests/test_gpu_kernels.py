@@ -427,3 +427,50 @@ def test_ilu0_refactor_rejects_other_patterns(ilug, torch_cuda):
     with pytest.raises(ilug.IlugError) as e:
         t.refactor(ilug.Matrix.generate("pressure27(10,10,10)"))
     assert e.value.status == 2
+
+
+def _random_dominant(ilug, n, per_row, seed):
+    """Unstructured diagonally dominant matrix: far more than 255 distinct
+    column offsets (the SELL-D8 coding must decline it)."""
+    rng = np.random.default_rng(seed)
+    cols = np.concatenate([np.arange(n)[:, None], rng.integers(0, n, (n, per_row))], axis=1)
+    cols.sort(axis=1)
+    keep = np.ones_like(cols, dtype=bool)
+    keep[:, 1:] = cols[:, 1:] != cols[:, :-1]
+    vals = rng.uniform(-1, 1, cols.shape)
+    vals[cols == np.arange(n)[:, None]] = per_row + 2.0
+    rp = np.concatenate([[0], np.cumsum(keep.sum(axis=1))])
+    return ilug.Matrix.from_csr(n, n, rp, cols[keep], vals[keep])
+
+
+@pytest.mark.parametrize("which", ["pressure27", "poisson3d", "random"])
+def test_sell_d8_coded_columns_bitwise(ilug, ref, torch_cuda, monkeypatch, which):
+    """SELL-D8 (1-byte dictionary-coded columns, col = row + offtab[code]) and
+    the int32 column stream give the same smoother step bit for bit, and both
+    the reference's ilu_smooth_sweep; an unstructured matrix (> 255 offsets)
+    stays on the int32 stream."""
+    torch = torch_cuda
+    if which == "random":
+        A = _random_dominant(ilug, 70000, 8, 5)
+    else:  # > 65536 rows: the thread-per-row sweep kernel (smaller operators take a warp per row)
+        A = ilug.Matrix.generate({"pressure27": "pressure27(48,48,32)", "poisson3d": "poisson3d(50,50,30)"}[which])
+    kv = {"smoother.kind": "ilu", "ilu.variant": "ilut", "ilu.droptol": "1e-3", "ilu.lfill": "5",
+          "trisolve.m_lower": "5", "trisolve.m_upper": "5", "smoother.sweeps": "1"}
+    b = np.random.default_rng(61).uniform(-1, 1, A.rows)
+    x0 = np.random.default_rng(62).uniform(-1, 1, A.rows)
+    got = {}
+    for d8 in ("1", "0"):
+        monkeypatch.setenv("ILUG_SELL_D8", d8)
+        S = ilug.Smoother(A, ilug.Config().update(kv))
+        xd = _dev(torch, x0)
+        S.ilu_sweep(_dev(torch, b), xd)
+        got[d8] = _host(xd)
+        y = torch.empty(A.rows, dtype=torch.float64, device="cuda")
+        DM = ilug.DeviceMatrix(A)
+        DM.spmv(_dev(torch, x0), y)
+        got[d8 + "spmv"] = _host(y)
+    assert bitwise(got["1"], got["0"]) and bitwise(got["1spmv"], got["0spmv"])
+    Ar = ref.mat(*A.csr())
+    want = ref.ilu_smooth_sweep(Ar, ref.smoother(Ar, ref.cfg(kv)), b, x0)
+    assert bitwise(got["1"], want)
+    assert bitwise(got["1spmv"], ref.spmv(Ar, x0, A.rows))
