@@ -238,14 +238,35 @@ std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalGroup> g, i
     return std::make_unique<LocalTransport>(std::move(g), rank);
 }
 
-void HaloExchange::exchange(const double* x, cudaStream_t st) const {
+HaloExchange::~HaloExchange() {
+    if (cst_) cudaStreamSynchronize(cst_), cudaStreamDestroy(cst_);
+    if (packed_) cudaEventDestroy(packed_);
+    if (done_) cudaEventDestroy(done_);
+}
+
+void HaloExchange::begin(const double* x, cudaStream_t st) const {
+    if (pending_) end(st); // a begin without its end: keep the buffers ordered
     const i64 ns = send_idx.n;
     if (ns > 0) {
         const unsigned g = static_cast<unsigned>(std::min<i64>((ns + 255) / 256, 4096));
         k_pack<<<g, 256, 0, st>>>(ns, send_idx.p, x, sendbuf.p);
         ILUG_LAUNCH_CHECK();
     }
-    if (tr && tr->nranks > 1) tr->exchange(*this, st);
+    if (!(tr && tr->nranks > 1)) return;
+    // the transfer on the exchange's stream, after the pack; the previous
+    // exchange's readers of halo (and writers of sendbuf) are ordered before
+    // this pack on the caller's stream, so the buffers are free
+    ILUG_CUDA(cudaEventRecord(packed_, st));
+    ILUG_CUDA(cudaStreamWaitEvent(cst_, packed_, 0));
+    tr->exchange(*this, cst_);
+    ILUG_CUDA(cudaEventRecord(done_, cst_));
+    pending_ = true;
+}
+
+void HaloExchange::end(cudaStream_t st) const {
+    if (!pending_) return;
+    ILUG_CUDA(cudaStreamWaitEvent(st, done_, 0));
+    pending_ = false;
 }
 
 void plan_exchange(HaloPlan& plan, const Transport& t) {
@@ -287,6 +308,11 @@ void HaloExchange::setup(const HaloPlan& plan, const Transport& t, cudaStream_t 
     send_idx.upload(plan.send_local.data(), static_cast<i64>(plan.send_local.size()), st);
     sendbuf.alloc(static_cast<i64>(plan.send_local.size()));
     halo.alloc(std::max<i64>(plan.nhalo, 1));
+    if (t.nranks > 1 && !cst_) {
+        ILUG_CUDA(cudaStreamCreateWithFlags(&cst_, cudaStreamNonBlocking));
+        ILUG_CUDA(cudaEventCreateWithFlags(&packed_, cudaEventDisableTiming));
+        ILUG_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
+    }
 }
 
 void transport_allreduce(const Transport* t, double* buf, i64 count, cudaStream_t st) {
@@ -295,7 +321,7 @@ void transport_allreduce(const Transport* t, double* buf, i64 count, cudaStream_
 
 void DistOperator::build(const HaloPlan& plan, const Transport& t, cudaStream_t st) {
     hx.setup(plan, t, st);
-    M.build(plan.A_ext, st);
+    sell_from_host_split(M.A, plan.A_ext, plan.nloc, st); // local-only rows first: they overlap the exchange
     M.n = plan.A_ext.nrows;
     M.halo = &hx;
 }
@@ -370,8 +396,9 @@ void DistHierarchy::cycle(int k, bool x_zero, cudaStream_t st) {
         lv.R.M.spmv(lv.r.p, nx.b.p, st); // halo of the fine residual
         vec_zero(nx.x.p, nx.n, st);
         for (i64 i = 0; i < nu_; ++i) cycle(k + 1, i == 0, st);
-        lv.P.hx.exchange(nx.x.p, st); // halo of the coarse correction
-        spmv_add_split(lv.P.M.A, nx.x.p, lv.P.hx.halo.p, lv.P.hx.nloc, lv.x.p, st);
+        lv.P.hx.begin(nx.x.p, st); // halo of the coarse correction; local rows overlap it
+        const HaloWait w = lv.P.hx.waiter();
+        spmv_add_split(lv.P.M.A, nx.x.p, lv.P.hx.halo.p, lv.P.hx.nloc, lv.x.p, st, &w);
     } else {
         // coarsest: all-gather this level's residual (zero-padded sum: exact),
         // form the whole coarse right-hand side, solve it on every rank

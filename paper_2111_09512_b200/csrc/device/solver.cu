@@ -20,14 +20,16 @@ void DeviceMatrix::build(const Csr& host, const i64* rp, const i32* ci, const do
 
 void DeviceMatrix::residual(const double* x, const double* b, double* r, cudaStream_t st) const {
     if (!halo) return ilug::residual(A, x, b, r, st);
-    halo->exchange(x, st);
-    residual_split(A, x, halo->halo.p, halo->nloc, b, r, st);
+    halo->begin(x, st); // the local-only rows run while the halo is in flight
+    const HaloWait w = halo->waiter();
+    residual_split(A, x, halo->halo.p, halo->nloc, b, r, st, &w);
 }
 
 void DeviceMatrix::spmv(const double* x, double* y, cudaStream_t st) const {
     if (!halo) return ilug::spmv(A, x, y, st);
-    halo->exchange(x, st);
-    spmv_split(A, x, halo->halo.p, halo->nloc, y, st);
+    halo->begin(x, st);
+    const HaloWait w = halo->waiter();
+    spmv_split(A, x, halo->halo.p, halo->nloc, y, st, &w);
 }
 
 // ============================================================ DeviceIlu (K1-K5)
@@ -288,7 +290,7 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
                 fail_numeric("gauss_seidel_sweep: zero diagonal at row " + std::to_string(i));
         gs_ = std::make_unique<LevelPlan>();
         gs_->build(A, LevelPlan::Kind::gauss_seidel, st);
-        if (dist) sell_from_host(Aoff_, dist->A_off, Part::all, st); // hybrid GS: off-block part
+        if (dist) sell_from_host_split(Aoff_, dist->A_off, dist->nloc, st); // hybrid GS: off-block part
         break;
     }
     case SmootherKind::poly_gs: {
@@ -424,8 +426,9 @@ void DeviceSmoother::smooth(const double* b, double* x, bool x_zero, cudaStream_
         case SmootherKind::jacobi:
         case SmootherKind::l1_jacobi:
             if (const HaloExchange* h = A_->halo) {
-                h->exchange(x, st);
-                residual_scale_step_split(A_->A, x, h->halo.p, h->nloc, b, invd_.p, ws_.p, st);
+                h->begin(x, st);
+                const HaloWait w = h->waiter();
+                residual_scale_step_split(A_->A, x, h->halo.p, h->nloc, b, invd_.p, ws_.p, st, &w);
             } else {
                 residual_scale_step(A_->A, x, b, invd_.p, ws_.p, st);
             }
@@ -434,8 +437,9 @@ void DeviceSmoother::smooth(const double* b, double* x, bool x_zero, cudaStream_
         case SmootherKind::gauss_seidel:
             if (const HaloExchange* h = A_->halo) {
                 // hybrid GS: b' = b - A_off x (current halo), then GS on the diagonal block
-                h->exchange(x, st);
-                residual_split(Aoff_, x, h->halo.p, h->nloc, b, ws_.p + n, st);
+                h->begin(x, st);
+                const HaloWait w = h->waiter();
+                residual_split(Aoff_, x, h->halo.p, h->nloc, b, ws_.p + n, st, &w);
                 gs_->solve(ws_.p + n, ws_.p, x, st);
             } else {
                 gs_->solve(b, ws_.p, x, st);
@@ -447,8 +451,9 @@ void DeviceSmoother::smooth(const double* b, double* x, bool x_zero, cudaStream_
             double* t1 = ws_.p + n;
             double* acc = ws_.p + 2 * n;
             if (const HaloExchange* h = A_->halo) {
-                h->exchange(x, st);
-                residual_scale_init_split(A_->A, x, h->halo.p, h->nloc, b, invd_.p, t0, acc, st);
+                h->begin(x, st);
+                const HaloWait w = h->waiter();
+                residual_scale_init_split(A_->A, x, h->halo.p, h->nloc, b, invd_.p, t0, acc, st, &w);
             } else {
                 residual_scale_init(A_->A, x, b, invd_.p, t0, acc, st);
             }

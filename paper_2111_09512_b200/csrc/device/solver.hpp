@@ -26,15 +26,36 @@ namespace ilug {
 class Transport;
 
 /// Device side of a HaloPlan (host/dist.hpp): packs the rows other ranks need
-/// and hands the segments to the job's transport (device/dist.cu).
+/// and hands the segments to the job's transport (device/dist.cu). The
+/// transfer runs on the exchange's own stream: begin() packs on the caller's
+/// stream and starts the transport behind an event, end() makes the caller's
+/// stream wait for the halo — the split products launch their local-only rows
+/// in between (HaloWait), so those rows overlap the exchange.
 struct HaloExchange {
     const Transport* tr = nullptr;
     i64 nloc = 0, nhalo = 0; ///< owned columns (split point of the extended operator), halo entries
     std::vector<i64> recv_ranks, recv_offsets, send_ranks, send_offsets;
     DBuf<i32> send_idx;
     mutable DBuf<double> sendbuf, halo;
+    HaloExchange() = default;
+    HaloExchange(const HaloExchange&) = delete;
+    HaloExchange& operator=(const HaloExchange&) = delete;
+    ~HaloExchange();
     void setup(const HaloPlan& plan, const Transport& t, cudaStream_t st);
-    void exchange(const double* x_local, cudaStream_t st) const;
+    void begin(const double* x_local, cudaStream_t st) const;
+    void end(cudaStream_t st) const;
+    /// end() as the split products' mid-launch callback
+    HaloWait waiter() const { return {&HaloExchange::end_cb, this}; }
+    void exchange(const double* x_local, cudaStream_t st) const {
+        begin(x_local, st);
+        end(st);
+    }
+
+private:
+    static void end_cb(const void* self, cudaStream_t st) { static_cast<const HaloExchange*>(self)->end(st); }
+    cudaStream_t cst_ = nullptr;
+    cudaEvent_t packed_ = nullptr, done_ = nullptr;
+    mutable bool pending_ = false;
 };
 /// Sum over the transport's ranks (no-op for null / one rank).
 void transport_allreduce(const Transport* t, double* buf, i64 count, cudaStream_t st);

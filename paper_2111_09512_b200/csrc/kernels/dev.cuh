@@ -124,6 +124,10 @@ struct Sell {
     /// cols stays for the other consumers. Empty = not coded.
     DBuf<std::uint8_t> codes;
     DBuf<i32> offtab; ///< kOffTab entries (unused slots 0)
+    /// Distributed rows (sell_from_host_split): slices [0, split_slices) hold
+    /// only rows whose columns are all local, the rest the rows that read the
+    /// halo, so the local part runs while the halo is in flight. -1: unsplit.
+    i64 split_slices = -1;
     bool empty() const { return nrows == 0; }
 };
 constexpr int kOffTab = 256;

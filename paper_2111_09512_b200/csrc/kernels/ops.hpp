@@ -45,16 +45,34 @@ Csr sell_to_host(const Sell& M);
 // s_i = sum_t M[i,t] x[col]  (ascending, from 0.0); then per row i:
 void spmv(const Sell& M, const double* x, double* y, cudaStream_t st);                 // y = s
 void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st);           // acc += s
+/// Makes a stream wait for an exchange in flight (device/dist.cu
+/// HaloExchange::end). Given to a split product, the rows that read only local
+/// columns are launched BEFORE the wait and the halo rows after it, so the
+/// local rows overlap the exchange (Sell::split_slices); without it (or on an
+/// unsplit SELL) the wait comes first and one launch covers every row.
+struct HaloWait {
+    void (*fn)(const void* ctx, cudaStream_t st) = nullptr;
+    const void* ctx = nullptr;
+    void operator()(cudaStream_t st) const {
+        if (fn) fn(ctx, st);
+    }
+};
+/// SELL of a rank's rows, local-only rows first (Sell::split_slices); columns
+/// >= nloc index the halo.
+void sell_from_host_split(Sell& out, const Csr& A, i64 nloc, cudaStream_t s);
 /// Distributed rows: columns < nloc read x, columns >= nloc read halo[c - nloc].
 void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
-                    cudaStream_t st);
-void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st);
+                    cudaStream_t st, const HaloWait* w = nullptr);
+void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st,
+                const HaloWait* w = nullptr);
 /// Split forms of the fused smoother epilogues (distributed rows: columns >= nloc read the halo)
-void spmv_add_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* acc, cudaStream_t st);
+void spmv_add_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* acc, cudaStream_t st,
+                    const HaloWait* w = nullptr);
 void residual_scale_step_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
-                               const double* scale, double* out, cudaStream_t st);
+                               const double* scale, double* out, cudaStream_t st, const HaloWait* w = nullptr);
 void residual_scale_init_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
-                               const double* scale, double* term, double* acc, cudaStream_t st);
+                               const double* scale, double* term, double* acc, cudaStream_t st,
+                               const HaloWait* w = nullptr);
 void residual(const Sell& M, const double* x, const double* b, double* r, cudaStream_t st); // r = b - s
 /// out = (rhs - s) / div
 void sweep_div(const Sell& M, const double* x, const double* rhs, const double* div, double* out,

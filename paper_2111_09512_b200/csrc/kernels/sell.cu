@@ -767,6 +767,7 @@ namespace {
 // rowlen per SELL row and slice offsets; `len_of(row)` gives the part length.
 template <typename LenOf>
 void layout(Sell& out, i64 nrows_pad, const std::vector<i32>& perm, LenOf len_of, cudaStream_t st) {
+    out.split_slices = -1;
     std::vector<std::uint16_t> rl(static_cast<size_t>(nrows_pad), 0);
     const i64 ns = nrows_pad / kSlice;
     std::vector<i64> sp(static_cast<size_t>(ns) + 1, 0);
@@ -1049,12 +1050,49 @@ void sell_refill(Sell& M, const i64* rp, const i32* ci, const double* v, Part pa
     ILUG_LAUNCH_CHECK();
 }
 
-void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
+namespace {
+void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>* perm_in, cudaStream_t s);
+// rows sorted by decreasing length inside windows of sigma (stable), padded
+// with -1 to whole slices: one group of a split SELL
+void append_group(std::vector<i32>& perm, const std::vector<i32>& rows, const Csr& A) {
+    const i64 sigma = std::max<i64>(1, sell_sigma());
+    std::vector<i32> g = rows;
+    for (size_t w = 0; w < g.size(); w += static_cast<size_t>(sigma)) {
+        auto lo = g.begin() + static_cast<i64>(w), hi = g.begin() + std::min<i64>(static_cast<i64>(g.size()), w + sigma);
+        std::stable_sort(lo, hi, [&](i32 a, i32 c) { return A.rp[a + 1] - A.rp[a] > A.rp[c + 1] - A.rp[c]; });
+    }
+    perm.insert(perm.end(), g.begin(), g.end());
+    while (perm.size() % kSlice) perm.push_back(-1);
+}
+} // namespace
+
+void sell_from_host_split(Sell& out, const Csr& A, i64 nloc, cudaStream_t s) {
+    std::vector<i32> inner, outer;
+    for (i64 i = 0; i < A.nrows; ++i) {
+        bool halo = false;
+        for (i64 k = A.rp[i]; k < A.rp[i + 1] && !halo; ++k) halo = A.ci[k] >= nloc;
+        (halo ? outer : inner).push_back(static_cast<i32>(i));
+    }
+    std::vector<i32> perm;
+    append_group(perm, inner, A);
+    const i64 split = static_cast<i64>(perm.size()) / kSlice;
+    append_group(perm, outer, A);
+    if (perm.empty()) perm.assign(kSlice, -1); // no rows: one empty slice keeps the layout valid
+    sell_host_build(out, A, Part::all, &perm, s);
+    out.split_slices = split;
+}
+
+void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) { sell_host_build(out, A, part, nullptr, s); }
+
+namespace {
+void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>* perm_in, cudaStream_t s) {
     SetupTimer tm("sell-host");
     out.nrows = A.nrows;
     out.ncols = A.ncols;
+    out.split_slices = -1;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
-    const std::vector<i32> perm = sigma_order(A.nrows, [&](i64 r) { return part_len(A, r, pc); });
+    const std::vector<i32> perm =
+        perm_in ? *perm_in : sigma_order(A.nrows, [&](i64 r) { return part_len(A, r, pc); });
     tm.mark("sigma order");
     const i64 pad = perm.empty() ? (A.nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
     layout(out, pad, perm, [&](i64 row) { return part_len(A, row, pc); }, s);
@@ -1077,6 +1115,7 @@ void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) {
     sell_encode(out, s);
     tm.mark("encode");
 }
+} // namespace
 
 Csr sell_to_host(const Sell& M) {
     ILUG_CUDA(cudaDeviceSynchronize()); // M may still be written on another stream
@@ -1115,31 +1154,53 @@ void spmv(const Sell& M, const double* x, double* y, cudaStream_t st) {
     launch_rowdot(M, x, EpiStore{y}, st);
 }
 namespace {
+// slices [s0, s1) of M as a kernel view (row metadata offset; values/columns
+// are addressed through slice_ptr, so they need no offset)
+SellView view_range(const Sell& M, i64 s0, i64 s1) {
+    SellView v = view(M);
+    v.slice_ptr += s0;
+    v.rowlen += s0 * kSlice;
+    if (v.perm) v.perm += s0 * kSlice;
+    v.nrows_pad = (s1 - s0) * kSlice;
+    return v;
+}
 template <class Epi>
-void launch_split(const Sell& M, const double* x, const double* halo, i64 nloc, Epi epi, cudaStream_t st) {
-    if (M.nrows_pad == 0) return;
-    k_rowdot_split<Epi><<<grid_for(M.nrows_pad), kBlock, 0, st>>>(view(M), M.nrows, x, halo,
-                                                                  static_cast<i32>(nloc), epi);
-    ILUG_LAUNCH_CHECK();
+void launch_split(const Sell& M, const double* x, const double* halo, i64 nloc, Epi epi, cudaStream_t st,
+                  const HaloWait* w) {
+    const i64 ns = M.nrows_pad / kSlice;
+    // local-only rows first when the halo is still in flight (split SELL)
+    const i64 si = w && M.split_slices >= 0 && M.perm.p ? std::min(M.split_slices, ns) : 0;
+    auto run = [&](i64 s0, i64 s1) {
+        if (s1 <= s0) return;
+        k_rowdot_split<Epi><<<grid_for((s1 - s0) * kSlice), kBlock, 0, st>>>(view_range(M, s0, s1), M.nrows, x, halo,
+                                                                            static_cast<i32>(nloc), epi);
+        ILUG_LAUNCH_CHECK();
+    };
+    run(0, si);
+    if (w) (*w)(st);
+    run(si, ns);
 }
 } // namespace
 void residual_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* b, double* r,
-                    cudaStream_t st) {
-    launch_split(M, x, halo, nloc, EpiResidual{b, r}, st);
+                    cudaStream_t st, const HaloWait* w) {
+    launch_split(M, x, halo, nloc, EpiResidual{b, r}, st, w);
 }
-void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st) {
-    launch_split(M, x, halo, nloc, EpiStore{y}, st);
+void spmv_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* y, cudaStream_t st,
+                const HaloWait* w) {
+    launch_split(M, x, halo, nloc, EpiStore{y}, st, w);
 }
-void spmv_add_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* acc, cudaStream_t st) {
-    launch_split(M, x, halo, nloc, EpiAdd{acc}, st);
+void spmv_add_split(const Sell& M, const double* x, const double* halo, i64 nloc, double* acc, cudaStream_t st,
+                    const HaloWait* w) {
+    launch_split(M, x, halo, nloc, EpiAdd{acc}, st, w);
 }
 void residual_scale_step_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
-                               const double* scale, double* out, cudaStream_t st) {
-    launch_split(M, x, halo, nloc, EpiScaleAcc{rhs, scale, x, out}, st);
+                               const double* scale, double* out, cudaStream_t st, const HaloWait* w) {
+    launch_split(M, x, halo, nloc, EpiScaleAcc{rhs, scale, x, out}, st, w);
 }
 void residual_scale_init_split(const Sell& M, const double* x, const double* halo, i64 nloc, const double* rhs,
-                               const double* scale, double* term, double* acc, cudaStream_t st) {
-    launch_split(M, x, halo, nloc, EpiScaleInit{rhs, scale, term, acc}, st);
+                               const double* scale, double* term, double* acc, cudaStream_t st,
+                               const HaloWait* w) {
+    launch_split(M, x, halo, nloc, EpiScaleInit{rhs, scale, term, acc}, st, w);
 }
 void spmv_add(const Sell& M, const double* x, double* acc, cudaStream_t st) {
     launch_rowdot(M, x, EpiAdd{acc}, st);
