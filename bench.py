@@ -419,7 +419,8 @@ def main():
     ach = kern["u_sweep"]["gbs"]
     roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_kind,
-                "kernel": "k_rowdot<EpiResidual> on strict row-scaled U (SELL-32, sigma-sorted)",
+                "kernel": "k_rowdot<EpiResidual> on strict row-scaled U (SELL-32, sigma-sorted, D8-coded columns)",
+                "bytes_rule": "SURVEY 8d formula 12*nnz+28n+4 (4 B per index; the 1-byte column stream is not credited)",
                 "bytes_per_launch": kern["u_sweep"]["bytes"], "ms_per_launch": round(kern["u_sweep"]["ms"], 5),
                 "frac_of_8TBs_nominal": round(ach / 8000.0, 4),
                 "l_sweep_gbs": round(kern["l_sweep"]["gbs"], 1)}
