@@ -162,9 +162,9 @@ def test_bench_trisolve_report(ilug, torch_cuda):
 
 
 def test_smooth_host_many_pipeline(ilug, torch_cuda):
-    """ilug_smooth_host_many (three streams, two device slots) = sequential
-    device smoothing of each pair, bitwise; a repeated pair — two positions
-    apart or back to back — sees its own previous output."""
+    """ilug_smooth_host_many (three streams, three device slots) = sequential
+    device smoothing of each pair, bitwise; a repeated pair — one, two or
+    three positions apart — sees its own previous output."""
     import numpy as np
     from conftest import bitwise
     A = ilug.Matrix.generate("poisson3d(24,22,20)")
@@ -172,8 +172,9 @@ def test_smooth_host_many_pipeline(ilug, torch_cuda):
                                                "trisolve.m_upper": 5}))
     rng = np.random.default_rng(9)
     pairs = [(torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).pin_memory(),
-              torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).pin_memory()) for _ in range(3)]
-    order = [0, 1, 2, 0, 1, 0, 0, 0, 2, 1, 1]  # including back-to-back repeats (in-place re-smoothing)
+              torch_cuda.from_numpy(rng.uniform(-1, 1, A.rows)).pin_memory()) for _ in range(4)]
+    # back-to-back repeats (in-place re-smoothing) and reuse 2, 3 and 4 steps later
+    order = [0, 1, 2, 0, 1, 0, 0, 0, 2, 1, 1, 3, 2, 0, 3, 1, 2, 3, 0, 1, 2, 3]
     want = {k: (b.cuda(), x.cuda()) for k, (b, x) in enumerate(pairs)}
     for k in order:
         S.smooth(want[k][0], want[k][1])
