@@ -1054,30 +1054,49 @@ namespace {
 void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>* perm_in, cudaStream_t s);
 // rows sorted by decreasing length inside windows of sigma (stable), padded
 // with -1 to whole slices: one group of a split SELL
-void append_group(std::vector<i32>& perm, const std::vector<i32>& rows, const Csr& A) {
+void append_group(std::vector<i32>& perm, std::vector<i32>&& g, const Csr& A) {
     const i64 sigma = std::max<i64>(1, sell_sigma());
-    std::vector<i32> g = rows;
-    for (size_t w = 0; w < g.size(); w += static_cast<size_t>(sigma)) {
-        auto lo = g.begin() + static_cast<i64>(w), hi = g.begin() + std::min<i64>(static_cast<i64>(g.size()), w + sigma);
-        std::stable_sort(lo, hi, [&](i32 a, i32 c) { return A.rp[a + 1] - A.rp[a] > A.rp[c + 1] - A.rp[c]; });
-    }
+    const i64 m = static_cast<i64>(g.size());
+    parallel_ranges((m + sigma - 1) / sigma, [&](i64 b, i64 e, int) {
+        for (i64 w = b; w < e; ++w)
+            std::stable_sort(g.begin() + w * sigma, g.begin() + std::min(m, (w + 1) * sigma),
+                             [&](i32 a, i32 c) { return A.rp[a + 1] - A.rp[a] > A.rp[c + 1] - A.rp[c]; });
+    }, 1);
     perm.insert(perm.end(), g.begin(), g.end());
     while (perm.size() % kSlice) perm.push_back(-1);
 }
 } // namespace
 
 void sell_from_host_split(Sell& out, const Csr& A, i64 nloc, cudaStream_t s) {
-    std::vector<i32> inner, outer;
-    for (i64 i = 0; i < A.nrows; ++i) {
-        bool halo = false;
-        for (i64 k = A.rp[i]; k < A.rp[i + 1] && !halo; ++k) halo = A.ci[k] >= nloc;
-        (halo ? outer : inner).push_back(static_cast<i32>(i));
+    bool any_halo = false;
+    std::vector<char> halo(static_cast<size_t>(A.nrows), 0);
+    std::atomic<bool> seen{false};
+    parallel_ranges(A.nrows, [&](i64 b, i64 e, int) {
+        bool local_seen = false;
+        for (i64 i = b; i < e; ++i) {
+            for (i64 k = A.rp[i]; k < A.rp[i + 1]; ++k)
+                if (A.ci[k] >= nloc) {
+                    halo[static_cast<size_t>(i)] = 1;
+                    local_seen = true;
+                    break;
+                }
+        }
+        if (local_seen) seen.store(true, std::memory_order_relaxed);
+    });
+    any_halo = seen.load();
+    if (!any_halo) { // one rank / no halo: the plain layout (every row is local)
+        sell_host_build(out, A, Part::all, nullptr, s);
+        out.split_slices = out.nrows_pad / kSlice;
+        return;
     }
+    std::vector<i32> inner, outer;
+    inner.reserve(static_cast<size_t>(A.nrows));
+    for (i64 i = 0; i < A.nrows; ++i) (halo[static_cast<size_t>(i)] ? outer : inner).push_back(static_cast<i32>(i));
     std::vector<i32> perm;
-    append_group(perm, inner, A);
+    perm.reserve(static_cast<size_t>(A.nrows + 2 * kSlice));
+    append_group(perm, std::move(inner), A);
     const i64 split = static_cast<i64>(perm.size()) / kSlice;
-    append_group(perm, outer, A);
-    if (perm.empty()) perm.assign(kSlice, -1); // no rows: one empty slice keeps the layout valid
+    append_group(perm, std::move(outer), A);
     sell_host_build(out, A, Part::all, &perm, s);
     out.split_slices = split;
 }
