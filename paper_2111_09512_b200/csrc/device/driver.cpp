@@ -62,6 +62,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     SolveOutcome oc;
     const auto t0 = std::chrono::steady_clock::now();
     std::optional<DeferFrees> defer(std::in_place); // setup threads must not serialise on cudaFree
+    SetupTimer tm("solve_with");
     // The finest level's factorisation (ILU(0)/ILUT on the device) runs
     // concurrently with the host AMG setup, which does not need it and does
     // not touch the GPU. Identical factors either way (same function, same input).
@@ -158,7 +159,9 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
         if (f0.valid()) f0.wait();
         throw;
     }
+    tm.mark("hierarchy");
     close_queue();
+    tm.mark("device objects");
     if (f0.valid()) pre = f0.get(); // single-level hierarchies: still surface factorisation errors
     (void)have_pre;
     if (build_err) std::rethrow_exception(build_err);
@@ -166,9 +169,11 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     // device-side setup that the first iteration would otherwise pay inside the
     // timed solve: the V-cycle graph and the GMRES basis (multi-GB at C2)
     dh.prepare_graph();
+    tm.mark("graph");
     GmresWork gw;
     if (kp.restart >= 1) gw.ensure(A.nrows, kp.restart, kp.flexible, kp.max_iters); // else gmres reports it
     defer.reset();
+    tm.mark("gmres basis + frees");
     oc.setup_seconds = since(t0);
 
     const i64 n = A.nrows;

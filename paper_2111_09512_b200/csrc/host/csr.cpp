@@ -140,11 +140,12 @@ SetupTimer::SetupTimer(const char* scope) : scope_(scope), on_(std::getenv("ILUG
 void SetupTimer::mark(const char* phase, i64 level) {
     if (!on_) return;
     const double t = now_s();
+    static const double t0 = t; // the first mark of the process: absolute times are relative to it
     if (level >= 0)
-        std::fprintf(stderr, "[setup] %s level %lld %-10s %8.3f s\n", scope_, static_cast<long long>(level), phase,
-                     t - t_);
+        std::fprintf(stderr, "[setup] %s level %lld %-10s %8.3f s  @%.3f\n", scope_, static_cast<long long>(level),
+                     phase, t - t_, t - t0);
     else
-        std::fprintf(stderr, "[setup] %s %-18s %8.3f s\n", scope_, phase, t - t_);
+        std::fprintf(stderr, "[setup] %s %-18s %8.3f s  @%.3f\n", scope_, phase, t - t_, t - t0);
     t_ = t;
 }
 
