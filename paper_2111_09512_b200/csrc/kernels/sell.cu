@@ -8,6 +8,8 @@
 // (--fmad=false): bitwise equal to src/sparse.cpp:162-174.
 #include "ops.hpp"
 
+#include <cub/cub.cuh>
+
 #include <atomic>
 #include <climits>
 #include <cstring>
@@ -817,6 +819,154 @@ void layout(Sell& out, i64 nrows_pad, const std::vector<i32>& perm, LenOf len_of
         out.perm.release();
 }
 
+// ---- device-side SELL-C-sigma layout (the host `layout` + `sigma_order`
+// without the host round trip: row lengths, the per-window stable sort by
+// decreasing length, the >= 3 % padding rule, slice widths and offsets all on
+// the GPU; the same permutation as the host path, so the same layout)
+__global__ void k_len_rows(i64 n, const i64* __restrict__ rp, i64 skip, i32* __restrict__ len) {
+    const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (i < n) len[i] = static_cast<i32>(rp[i + 1] - rp[i] - skip);
+}
+__global__ void k_len_part(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci, int pc,
+                           i32* __restrict__ len) {
+    const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    i32 c = 0;
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) c += pc == 1 ? ci[k] < i : ci[k] > i;
+    len[i] = c;
+}
+__global__ void k_iota_i32(i64 n, i32* __restrict__ a) {
+    const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (i < n) a[i] = static_cast<i32>(i);
+}
+__global__ void k_window_offsets(i64 nw, i64 sigma, i64 n, int* __restrict__ off) {
+    const i64 w = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (w <= nw) off[w] = static_cast<int>(std::min(n, w * sigma));
+}
+// per slice: width (max length) of the natural and of the sorted order
+__global__ void k_slice_widths(i64 ns, i64 n, const i32* __restrict__ len, const i32* __restrict__ slen,
+                               i64* __restrict__ wnat, i64* __restrict__ wsort) {
+    const i64 s = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (s >= ns) return;
+    i32 a = 0, b = 0;
+    for (int l = 0; l < kSlice; ++l) {
+        const i64 p = s * kSlice + l;
+        if (p < n) a = max(a, len[p]), b = max(b, slen ? slen[p] : 0);
+    }
+    wnat[s] = a;
+    if (wsort) wsort[s] = b;
+}
+__global__ void k_layout_rows(i64 pad, i64 n, const i32* __restrict__ len, const i32* __restrict__ order,
+                              i32* __restrict__ perm, std::uint16_t* __restrict__ rowlen) {
+    const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (p >= pad) return;
+    const i32 row = p < n ? (order ? order[p] : static_cast<i32>(p)) : -1;
+    if (perm) perm[p] = row;
+    rowlen[p] = static_cast<std::uint16_t>(row >= 0 ? len[row] : 0);
+}
+__global__ void k_slice_ptr_from_widths(i64 ns, const i64* __restrict__ w, i64* __restrict__ sp) {
+    const i64 s = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    if (s < ns) sp[s + 1] = w[s] * kSlice;
+    if (s == 0) sp[0] = 0;
+}
+
+struct WidenI32 {
+    __host__ __device__ i64 operator()(i32 v) const { return static_cast<i64>(v); }
+};
+template <class It, class Op>
+i64 dev_reduce(It in, i64 n, Op op, i64 init, cudaStream_t st) {
+    DBuf<i64> out(1);
+    size_t tmp = 0;
+    ILUG_CUDA(cub::DeviceReduce::Reduce(nullptr, tmp, in, out.p, static_cast<int>(n), op, init, st));
+    DBuf<unsigned char> t(static_cast<i64>(tmp) + 1);
+    ILUG_CUDA(cub::DeviceReduce::Reduce(t.p, tmp, in, out.p, static_cast<int>(n), op, init, st));
+    i64 h = 0;
+    ILUG_CUDA(cudaMemcpyAsync(&h, out.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+struct MaxI64 {
+    __host__ __device__ i64 operator()(i64 a, i64 b) const { return a > b ? a : b; }
+};
+struct SumI64 {
+    __host__ __device__ i64 operator()(i64 a, i64 b) const { return a + b; }
+};
+
+// len: the selected part's length of every row (device). Fills out's layout
+// fields exactly as layout(sigma_order(...)) does on the host.
+void layout_device(Sell& out, i64 n, const i32* len, cudaStream_t st) {
+    out.split_slices = -1;
+    const i64 pad = (n + kSlice - 1) / kSlice * kSlice;
+    const i64 ns = pad / kSlice;
+    DBuf<i64> wnat(std::max<i64>(ns, 1)), wsort;
+    DBuf<i32> keys_out, order;
+    const i64 sigma = sell_sigma();
+    bool sorted = false;
+    if (sigma > 1 && n >= 2 * kSlice) {
+        const i64 nw = (n + sigma - 1) / sigma;
+        DBuf<int> off(nw + 1);
+        DBuf<i32> iota(n);
+        keys_out.alloc(n);
+        order.alloc(n);
+        k_window_offsets<<<grid_for(nw + 1), kBlock, 0, st>>>(nw, sigma, n, off.p);
+        k_iota_i32<<<grid_for(n), kBlock, 0, st>>>(n, iota.p);
+        ILUG_LAUNCH_CHECK();
+        size_t tmp = 0;
+        ILUG_CUDA(cub::DeviceSegmentedSort::StableSortPairsDescending(
+            nullptr, tmp, len, keys_out.p, iota.p, order.p, static_cast<int>(n), static_cast<int>(nw), off.p,
+            off.p + 1, st));
+        DBuf<unsigned char> t(static_cast<i64>(tmp) + 1);
+        ILUG_CUDA(cub::DeviceSegmentedSort::StableSortPairsDescending(
+            t.p, tmp, len, keys_out.p, iota.p, order.p, static_cast<int>(n), static_cast<int>(nw), off.p,
+            off.p + 1, st));
+        wsort.alloc(ns);
+        k_slice_widths<<<grid_for(ns), kBlock, 0, st>>>(ns, n, len, keys_out.p, wnat.p, wsort.p);
+        ILUG_LAUNCH_CHECK();
+        const i64 pn = dev_reduce(wnat.p, ns, SumI64{}, 0, st), ps = dev_reduce(wsort.p, ns, SumI64{}, 0, st);
+        ILUG_CUDA(cudaStreamSynchronize(st)); // t, iota, off die here
+        sorted = !(static_cast<double>(ps) > 0.97 * static_cast<double>(pn));
+    }
+    if (!sorted) {
+        k_slice_widths<<<grid_for(std::max<i64>(ns, 1)), kBlock, 0, st>>>(ns, n, len, nullptr, wnat.p, nullptr);
+        ILUG_LAUNCH_CHECK();
+    }
+    const i64* w = sorted ? wsort.p : wnat.p;
+    out.nrows_pad = pad;
+    out.max_row = static_cast<int>(ns > 0 ? dev_reduce(w, ns, MaxI64{}, 0, st) : 0);
+    if (out.max_row > 65535) fail_invalid("SELL: a row has more than 65535 entries");
+    out.slice_ptr.alloc(ns + 1);
+    k_slice_ptr_from_widths<<<grid_for(std::max<i64>(ns, 1)), kBlock, 0, st>>>(ns, w, out.slice_ptr.p);
+    ILUG_LAUNCH_CHECK();
+    if (ns > 0) {
+        size_t tmp = 0;
+        ILUG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, out.slice_ptr.p + 1, out.slice_ptr.p + 1,
+                                                static_cast<int>(ns), st));
+        DBuf<unsigned char> t(static_cast<i64>(tmp) + 1);
+        ILUG_CUDA(cub::DeviceScan::InclusiveSum(t.p, tmp, out.slice_ptr.p + 1, out.slice_ptr.p + 1,
+                                                static_cast<int>(ns), st));
+        ILUG_CUDA(cudaMemcpyAsync(&out.padded, out.slice_ptr.p + ns, sizeof(i64), cudaMemcpyDeviceToHost, st));
+        ILUG_CUDA(cudaStreamSynchronize(st));
+    } else {
+        out.padded = 0;
+    }
+    out.rowlen.alloc(pad);
+    if (sorted) out.perm.alloc(pad); else out.perm.release();
+    if (pad > 0) {
+        k_layout_rows<<<grid_for(pad), kBlock, 0, st>>>(pad, n, len, sorted ? order.p : nullptr,
+                                                         sorted ? out.perm.p : nullptr, out.rowlen.p);
+        ILUG_LAUNCH_CHECK();
+    }
+    out.nnz = n > 0 ? dev_reduce(cub::TransformInputIterator<i64, WidenI32, const i32*>(len, WidenI32{}), n,
+                                 SumI64{}, 0, st)
+                    : 0;
+    out.cols.alloc(out.padded);
+    out.vals.alloc(out.padded);
+    if (out.padded > 0) {
+        ILUG_CUDA(cudaMemsetAsync(out.cols.p, 0, static_cast<size_t>(out.padded) * sizeof(i32), st));
+        ILUG_CUDA(cudaMemsetAsync(out.vals.p, 0, static_cast<size_t>(out.padded) * sizeof(double), st));
+    }
+}
+
 i64 part_len(const Csr& A, i64 row, int pc) {
     if (pc == 0) return A.rp[row + 1] - A.rp[row];
     i64 c = 0;
@@ -964,6 +1114,11 @@ __global__ void k_offsets_encode(SellView M, i64 nrows, const i32* __restrict__ 
 
 } // namespace
 
+bool device_layout() { // ILUG_SELL_DEVICE_LAYOUT=0: the host layout path (A/B; read at every build)
+    const char* e = std::getenv("ILUG_SELL_DEVICE_LAYOUT");
+    return !(e && e[0] == '0');
+}
+
 bool sell_d8_enabled() { // ILUG_SELL_D8=0: int32 column stream only (A/B; read at every build)
     const char* e = std::getenv("ILUG_SELL_D8");
     return !(e && e[0] == '0');
@@ -1028,12 +1183,24 @@ void sell_from_device_rows(Sell& out, i64 nrows, i64 ncols, const RawVec<i64>& r
     out.nrows = nrows;
     out.ncols = ncols;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
-    auto len = [&](i64 r) { return rp_host[r + 1] - rp_host[r] - skip; };
-    const std::vector<i32> perm = sigma_order(nrows, len);
-    tm.mark("sigma order");
-    const i64 pad = perm.empty() ? (nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
-    layout(out, pad, perm, len, s);
-    tm.mark("layout+upload");
+    i64 pad = 0;
+    if (device_layout()) {
+        DBuf<i32> len(std::max<i64>(nrows, 1));
+        if (nrows > 0) {
+            k_len_rows<<<grid_for(nrows), kBlock, 0, s>>>(nrows, rp, skip, len.p);
+            ILUG_LAUNCH_CHECK();
+        }
+        layout_device(out, nrows, len.p, s);
+        pad = out.nrows_pad;
+        tm.mark("device layout");
+    } else {
+        auto len = [&](i64 r) { return rp_host[r + 1] - rp_host[r] - skip; };
+        const std::vector<i32> perm = sigma_order(nrows, len);
+        tm.mark("sigma order");
+        pad = perm.empty() ? (nrows + kSlice - 1) / kSlice * kSlice : static_cast<i64>(perm.size());
+        layout(out, pad, perm, len, s);
+        tm.mark("layout+upload");
+    }
     if (pad > 0 && rp_host[nrows] > 0) {
         k_sell_fill<<<grid_for(pad), kBlock, 0, s>>>(pad, out.nrows, out.perm.p, rp, ci, v, pc, out.slice_ptr.p,
                                                      out.cols.p, out.vals.p);
@@ -1110,6 +1277,31 @@ void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>*
     out.ncols = A.ncols;
     out.split_slices = -1;
     const int pc = part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2);
+    if (!perm_in && device_layout() && A.nnz() > 0) { // layout on the GPU from the uploaded CSR
+        DBuf<i64> rp;
+        DBuf<i32> ci;
+        DBuf<double> v;
+        rp.upload(A.rp.data(), A.nrows + 1, s);
+        ci.upload(A.ci.data(), A.nnz(), s);
+        v.upload(A.v.data(), A.nnz(), s);
+        tm.mark("csr upload");
+        DBuf<i32> len(std::max<i64>(A.nrows, 1));
+        if (pc == 0)
+            k_len_rows<<<grid_for(A.nrows), kBlock, 0, s>>>(A.nrows, rp.p, 0, len.p);
+        else
+            k_len_part<<<grid_for(A.nrows), kBlock, 0, s>>>(A.nrows, rp.p, ci.p, pc, len.p);
+        ILUG_LAUNCH_CHECK();
+        layout_device(out, A.nrows, len.p, s);
+        out.codes.release(), out.offtab.release();
+        tm.mark("device layout");
+        k_sell_fill<<<grid_for(out.nrows_pad), kBlock, 0, s>>>(out.nrows_pad, out.nrows, out.perm.p, rp.p, ci.p, v.p,
+                                                               pc, out.slice_ptr.p, out.cols.p, out.vals.p);
+        ILUG_LAUNCH_CHECK();
+        sell_encode(out, s);
+        ILUG_CUDA(cudaStreamSynchronize(s)); // the CSR temporaries die here
+        tm.mark("fill+encode");
+        return;
+    }
     const std::vector<i32> perm =
         perm_in ? *perm_in : sigma_order(A.nrows, [&](i64 r) { return part_len(A, r, pc); });
     tm.mark("sigma order");

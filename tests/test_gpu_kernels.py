@@ -474,3 +474,36 @@ def test_sell_d8_coded_columns_bitwise(ilug, ref, torch_cuda, monkeypatch, which
     want = ref.ilu_smooth_sweep(Ar, ref.smoother(Ar, ref.cfg(kv)), b, x0)
     assert bitwise(got["1"], want)
     assert bitwise(got["1spmv"], ref.spmv(Ar, x0, A.rows))
+
+
+@pytest.mark.parametrize("which", ["pressure27", "poisson3d", "random"])
+def test_sell_device_layout_matches_host_layout(ilug, ref, torch_cuda, monkeypatch, which):
+    """The SELL-C-sigma layout computed on the GPU (row lengths, per-window
+    stable sort, the 3 % padding rule, slice offsets) equals the host layout:
+    same stored/padded entry counts, same smoother and SpMV bits, both the
+    reference's."""
+    torch = torch_cuda
+    if which == "random":
+        A = _random_dominant(ilug, 70000, 8, 7)
+    else:
+        A = ilug.Matrix.generate({"pressure27": "pressure27(48,48,32)", "poisson3d": "poisson3d(50,50,30)"}[which])
+    kv = {"smoother.kind": "ilu", "ilu.variant": "ilut", "ilu.droptol": "1e-3", "ilu.lfill": "5",
+          "trisolve.m_lower": "5", "trisolve.m_upper": "5", "smoother.sweeps": "1"}
+    b = np.random.default_rng(71).uniform(-1, 1, A.rows)
+    x0 = np.random.default_rng(72).uniform(-1, 1, A.rows)
+    got, stats = {}, {}
+    for dev in ("1", "0"):
+        monkeypatch.setenv("ILUG_SELL_DEVICE_LAYOUT", dev)
+        S = ilug.Smoother(A, ilug.Config().update(kv))
+        F = ilug.Factors.create(A, ilug.Config().update(kv), scaling="row")
+        stats[dev] = F.stats()
+        xd = _dev(torch, x0)
+        S.ilu_sweep(_dev(torch, b), xd)
+        got[dev] = _host(xd)
+        y = torch.empty(A.rows, dtype=torch.float64, device="cuda")
+        ilug.DeviceMatrix(A).spmv(_dev(torch, x0), y)
+        got[dev + "spmv"] = _host(y)
+    assert stats["1"] == stats["0"]
+    assert bitwise(got["1"], got["0"]) and bitwise(got["1spmv"], got["0spmv"])
+    Ar = ref.mat(*A.csr())
+    assert bitwise(got["1"], ref.ilu_smooth_sweep(Ar, ref.smoother(Ar, ref.cfg(kv)), b, x0))
