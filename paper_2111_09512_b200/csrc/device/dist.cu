@@ -344,7 +344,9 @@ void DistHierarchy::build(const HostHierarchy& h, const DistComm& comm, cudaStre
     nlev_ = L;
     nu_ = h.params.cycles_nu;
     levels_.clear();
+    SetupTimer tm("dist");
     std::vector<DistLevelPlan> plans = dist_level_plans(h, comm.nranks, comm.rank);
+    tm.mark("level plans");
     for (int k = 0; k + 1 < L; ++k) {
         DistLevelPlan& d = plans[k];
         Lev& lv = levels_.emplace_back();
@@ -363,7 +365,9 @@ void DistHierarchy::build(const HostHierarchy& h, const DistComm& comm, cudaStre
             sell_from_host(lv.P_rows, d.P_rows, Part::all, st);
             gather_.alloc(std::max<i64>(d.n, 1));
         }
+        tm.mark("operators", k);
         lv.smoother.build(d.A.diag(), lv.A.M, h.params.plan.for_level(k), st, nullptr, &d.A);
+        tm.mark("smoother", k);
         lv.b.alloc(std::max<i64>(lv.n, 1));
         lv.x.alloc(std::max<i64>(lv.n, 1));
         lv.r.alloc(std::max<i64>(lv.n, 1));
