@@ -62,6 +62,7 @@ struct IlutArgs {
     unsigned long long* ticket;
     unsigned long long* first_zero;
     unsigned* err;       // [0] wait timeout, [1] overflow (needed capacity)
+    int wrank;           // fill ranking in registers when <= 32 candidates (ILUG_ILUT_WRANK)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -109,7 +110,7 @@ __global__ void k_ilut_vf_fill(i64 ucap, i64 n, i32* __restrict__ uci, double* _
 // src/ilu.cpp:206-211). Pattern candidates are always kept. Marks kSel.
 __device__ __forceinline__ void select_part(const i32* scol, const double* sval, unsigned char* sflag, int beg,
                                             int end, unsigned char want, bool upper, double tau, i64 lfill,
-                                            int lane) {
+                                            int lane, bool wrank) {
     // pass 1: which candidates pass (U part: the threshold), count fill
     int nfill = 0;
     for (int q = beg + lane; q < end; q += 32) {
@@ -126,6 +127,46 @@ __device__ __forceinline__ void select_part(const i32* scol, const double* sval,
     for (int o = 16; o; o >>= 1) nfill += __shfl_xor_sync(0xffffffffu, nfill, o);
     __syncwarp();
     if (nfill <= lfill) return;
+    if (wrank && nfill <= 32) {
+        // pass 2 in registers: the fill candidates compacted into lanes
+        // 0..nfill-1 (ballot + nth-set-bit shuffles), each lane ranks its
+        // candidate against the others by shuffles — the same comparator, so
+        // the same survivors as the shared-memory ranking below. (A two-slot
+        // form for up to 64 candidates spilled at the 42-register budget and
+        // measured slower: 1.44 vs 1.33 s at C2.)
+        double myv = 0.0;
+        i32 myc = 0;
+        int myq = -1, base = 0;
+        for (int q0 = beg; q0 < end; q0 += 32) {
+            const int q = q0 + lane;
+            bool cand = false;
+            double v = 0.0;
+            i32 c = 0;
+            if (q < end) {
+                const unsigned char f = sflag[q];
+                cand = (f & kSel) && !(f & kOrig);
+                v = fabs(sval[q]);
+                c = scol[q];
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, cand);
+            const int cnt = __popc(bm);
+            const int k = lane - base; // this lane takes the chunk's k-th candidate
+            const int src = (k >= 0 && k < cnt) ? static_cast<int>(__fns(bm, 0, k + 1)) : 0;
+            const double sv = __shfl_sync(0xffffffffu, v, src);
+            const i32 sc = __shfl_sync(0xffffffffu, c, src);
+            if (k >= 0 && k < cnt) myv = sv, myc = sc, myq = q0 + src;
+            base += cnt;
+        }
+        i64 rank = 0;
+        for (int r = 0; r < nfill; ++r) {
+            const double vr = __shfl_sync(0xffffffffu, myv, r);
+            const i32 cr = __shfl_sync(0xffffffffu, myc, r);
+            if (r != lane) rank += (vr != myv) ? (vr > myv) : (cr < myc);
+        }
+        if (myq >= 0 && rank >= lfill) sflag[myq] = static_cast<unsigned char>(sflag[myq] & ~kSel);
+        __syncwarp();
+        return;
+    }
     // pass 2: rank each fill candidate against all others; losers get kDrop
     // (the ranking reads only kSel/kOrig, so marking while others rank is safe)
     for (int q = beg + lane; q < end; q += 32) {
@@ -378,7 +419,7 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
             }
         }
         const int ub = p + (hasd ? 1 : 0);
-        select_part(scol, sval, sflag, ub, len, kLive, true, tau, a.lfill, lane);
+        select_part(scol, sval, sflag, ub, len, kLive, true, tau, a.lfill, lane, a.wrank != 0);
         const i64 uo = a.uoff[i];
         const int nu = emit<VF>(scol, sval, sflag, ub, len, a.uci + uo + 1, a.uv + uo + 1, lane);
         if (VF) {
@@ -397,7 +438,7 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
             if (lane == 0) fi.store(E, cuda::memory_order_release);
         }
 
-        select_part(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, lane);
+        select_part(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, lane, a.wrank != 0);
         const i64 lo = a.loff[i];
         const int nl = emit(scol, sval, sflag, 0, p, a.lci + lo, a.lv + lo, lane);
         if (lane == 0) a.llen[i] = nl;
@@ -461,6 +502,12 @@ void inclusive_scan(i64* d, i64 count, cudaStream_t st) {
 // interleaved A/B (profiles/r02_ilut_vf_ab.txt) — the kernel is bound by its
 // per-row work across the SMs (2.1 / 2.9 / 5.8 s on 96 / 64 / 32 SMs), not by
 // the flag round trip of the dependency chain.
+// ILUG_ILUT_WRANK=0: the fill ranking always in shared memory (A/B)
+bool ilut_wrank() {
+    const char* e = std::getenv("ILUG_ILUT_WRANK");
+    return !(e && e[0] == '0');
+}
+
 bool ilut_value_flags() {
     const char* e = std::getenv("ILUG_ILUT_VF");
     return e && e[0] == '1';
@@ -540,7 +587,7 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
     ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
     IlutArgs a{n,       rp.p,   ci.p,   av.p,   tau.p,   p.lfill, anorm_f, 0,
                p.droptol, uoff.p, loff.p, uci.p, uv.p, ulen.p, lci.p, lv.p, llen.p, sync.p, sync.p + n,
-               ctl.p,   ctl.p + 1, sync.p + n + 1};
+               ctl.p,   ctl.p + 1, sync.p + n + 1, ilut_wrank() ? 1 : 0};
     unsigned err[2] = {0, 0};
     for (int pass = 0; pass < 2; ++pass) {
         for (int cap_level = 0;; ++cap_level) {
