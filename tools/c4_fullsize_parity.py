@@ -1,9 +1,11 @@
-"""One-off evidence (not in the test suite: ~4 min of single-threaded
-reference work): the C4 smoother step at FULL size — poisson3d(465^3),
-100.5 M rows, ILU(0) row-scaled, m_L = m_U = 5 — on the device (the
-distributed smoother's rank-local form at p = 1, i.e. the bench's `--strong`
-step at N = 1) versus the reference library's ilu_smooth_sweep on the same
-matrix built by the oracle-side generator. Prints one JSON line."""
+"""One-off evidence (not in the test suite: minutes of single-threaded
+reference work): a BASELINE smoother step at FULL size — by default C4,
+poisson3d(465^3), 100.5 M rows, ILU(0) row-scaled, m_L = m_U = 5 — on the
+device (the distributed smoother's rank-local form at p = 1, i.e. the bench's
+`--strong` step at N = 1) versus the reference library's ilu_smooth_sweep on
+the same matrix built by the oracle-side generator. Prints one JSON line.
+
+    python tools/c4_fullsize_parity.py [SPEC [scaling]]   (e.g. "cutcell(256,256,256)" row_col)"""
 import hashlib
 import json
 import os
@@ -18,11 +20,12 @@ import paper_2111_09512_b200 as ilug  # noqa: E402
 from paper_2111_09512_b200 import dist as idist  # noqa: E402
 from oracle import oracle  # noqa: E402
 
-SPEC = "poisson3d(465,465,465)"
-KV = {"smoother.kind": "ilu", "ilu.variant": "ilu0", "scaling": "row", "trisolve.mode": "richardson",
+SPEC = sys.argv[1] if len(sys.argv) > 1 else "poisson3d(465,465,465)"
+KV = {"smoother.kind": "ilu", "ilu.variant": "ilu0", "scaling": sys.argv[2] if len(sys.argv) > 2 else "row",
+      "trisolve.mode": "richardson",
       "trisolve.m_lower": "5", "trisolve.m_upper": "5", "smoother.sweeps": "1"}
 torch.cuda.set_device(0)
-out = {"spec": SPEC}
+out = {"spec": SPEC, "scaling": KV["scaling"], "sell_d8": os.environ.get("ILUG_SELL_D8", "1")}
 t = time.time()
 A = ilug.Matrix.generate(SPEC)
 n = A.rows
