@@ -453,12 +453,21 @@ __global__ void k_not(i64 n, const char* __restrict__ isc, char* __restrict__ is
 }
 
 // stable compaction of idx[0..m) by flags (cub::DeviceSelect keeps the order)
-i64 select_flagged(const i64* in, const char* flags, i64* out, i64 m, cudaStream_t st) {
+// ws: reusable CUB temporary + count slot (the PMIS rounds call this once per
+// round; no allocation per call)
+struct SelectWs {
+    DBuf<i64> nsel{1};
+    DBuf<unsigned char> t;
+};
+i64 select_flagged(const i64* in, const char* flags, i64* out, i64 m, cudaStream_t st, SelectWs* ws = nullptr) {
     if (m == 0) return 0;
-    DBuf<i64> nsel(1);
+    SelectWs local;
+    SelectWs& w = ws ? *ws : local;
+    DBuf<i64>& nsel = w.nsel;
     size_t tmp = 0;
     ILUG_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, in, flags, out, nsel.p, m, st));
-    DBuf<unsigned char> t(static_cast<i64>(tmp) + 1);
+    if (w.t.n < static_cast<i64>(tmp) + 1) w.t.alloc(static_cast<i64>(tmp) + 1);
+    DBuf<unsigned char>& t = w.t;
     ILUG_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, in, flags, out, nsel.p, m, st));
     i64 h = 0;
     ILUG_CUDA(cudaMemcpyAsync(&h, nsel.p, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -522,6 +531,7 @@ DevSplit pmis_device(const DevCsr& S, const DevCsr& St, std::uint64_t seed, cuda
         keep(std::max<i64>(n, 1));
     DBuf<i64> live(std::max<i64>(n, 1)), next(std::max<i64>(n, 1));
     DBuf<unsigned long long> found(1);
+    SelectWs sws;
     ILUG_CUDA(cudaMemsetAsync(fresh.p, 0, static_cast<size_t>(std::max<i64>(n, 1)), st));
     k_pmis_init<<<grid_n(n), kB, 0, st>>>(n, St.rp.p, seed, wt.p, state.p, live.p);
     ILUG_LAUNCH_CHECK();
@@ -545,7 +555,7 @@ DevSplit pmis_device(const DevCsr& S, const DevCsr& St, std::uint64_t seed, cuda
         ILUG_LAUNCH_CHECK();
         k_pmis_mark<<<grid_n(m), kB, 0, st>>>(m, live.p, picked.p, state.p, fresh.p, 0);
         ILUG_LAUNCH_CHECK();
-        m = select_flagged(live.p, keep.p, next.p, m, st);
+        m = select_flagged(live.p, keep.p, next.p, m, st, &sws);
         std::swap(live, next);
     }
     // repair pass (src/amg.cpp:56-84): parallel candidate search, serial ordered promotion
@@ -554,7 +564,7 @@ DevSplit pmis_device(const DevCsr& S, const DevCsr& St, std::uint64_t seed, cuda
     ILUG_LAUNCH_CHECK();
     k_iota<<<grid_n(n), kB, 0, st>>>(n, live.p);
     ILUG_LAUNCH_CHECK();
-    const i64 nc = select_flagged(live.p, cand.p, next.p, n, st);
+    const i64 nc = select_flagged(live.p, cand.p, next.p, n, st, &sws);
     if (nc > 0) {
         k_repair<<<1, 32, 0, st>>>(nc, next.p, S.rp.p, S.ci.p, state.p);
         ILUG_LAUNCH_CHECK();
