@@ -304,11 +304,15 @@ def build_workload(ilug, args, rank, world, local, use_dist=False):
     comm = dist_comm(rank, world, local)
     plan.exchange(comm)
     S = idist.Smoother(plan, comm, cfg)
+    # the smoother holds everything it needs on the device: drop this rank's host
+    # rows and plan (the strong-scaling solve that follows builds a global host
+    # hierarchy on every rank; host memory is shared by all the ranks of a node)
+    del rows, plan
     st = S.stats()
     once = lambda which, xin, rhs, out, stm: ilug._check(ilug.lib.ilug_dist_smoother_sweep_once(
         S.h, which, xin.data_ptr(), rhs.data_ptr(), out.data_ptr(), stm.cuda_stream))
     host = lambda bs, xs: S.smooth_host_many(bs, xs)
-    return dict(A=rows, S=S, plan=plan, comm=comm, n=st["nloc"], nnz_a=st["nnz_A"], nnz_l=st["nnz_Ls"],
+    return dict(A=None, S=S, comm=comm, n=st["nloc"], nnz_a=st["nnz_A"], nnz_l=st["nnz_Ls"],
                 nnz_u=st["nnz_Us"], pad_u=0, smooth=S.smooth, once=once, host=host, spec=spec)
 
 
@@ -516,6 +520,9 @@ def strong_solve(ilug, spec, kv, comm_args, barrier, max_over_ranks, hierarchy=N
     r0, r1 = solver.row0, solver.row0 + solver.nloc
     b = torch.from_numpy(np.add.reduceat(v[:rp[r1]], rp[r0:r1]) if r1 > r0 else np.zeros(0)).cuda()
     x = torch.zeros_like(b)
+    # the solver keeps only device data: release this rank's copies of the global
+    # matrix and hierarchy before the solve (all ranks of a node share its RAM)
+    del rp, v, A, H
     # warm-up (lazy module loading) outside the timed solve
     solver.gmres(ilug.Config().update(dict(kv, **{"krylov.max_iters": "2"})), b, x)
     x.zero_()
