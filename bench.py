@@ -604,6 +604,7 @@ def run_strong(args):
     plan = idist.Plan(idist.generate_rows(spec, int(starts[rank]), int(starts[rank + 1])), n_g, world, rank)
     plan.exchange(comm)
     S = idist.Smoother(plan, comm, ilug.Config().update(C4_KV))
+    del plan  # the smoother keeps only device data (host RAM is shared by the node's ranks)
     setup_s = max_over_ranks(time.perf_counter() - t0)
     st = S.stats()
     n, B = st["nloc"], step_bytes(st["nloc"], st["nnz_A"], st["nnz_Ls"], st["nnz_Us"])
