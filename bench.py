@@ -661,7 +661,7 @@ def run_strong(args):
                 "api": "ilug_dist_smooth_host_many (pinned host b, x per rank)"},
         "clocks": clk.summary(), "gpu_launches": 9 * args.steps,
     }
-    del S, plan
+    del S
     if not args.no_tts:
         kv = dict(C4_KV, **{"smoother.sweeps": "2", "krylov.tol": "1e-8", "amg.coarsening": "pmis",
                             "krylov.form_iterates": "false", "smoother.fallback.kind": "poly_gs"})
