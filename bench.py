@@ -229,6 +229,48 @@ def ref_smoother_rate(spec, kv, max_steps, budget_s, threads=None):
             "host": info, "steps_timed": steps}
 
 
+def ref_sweeps_only_rate(spec, kv, budget_s=20.0):
+    """SURVEY.md §8d's fairness figure beside the reference's own call: the
+    reference's sweep core alone — spmv_into (src/sparse.cpp:162-174) over its
+    own pre-split strict row-scaled U, without the per-call split and
+    allocations of richardson_upper_scaled (src/trisolve.cpp:123-147) — T
+    concurrent calls (the GIL is released in the library), GB/s on the same
+    per-sweep byte formula."""
+    import threading
+    import numpy as np
+    from oracle import oracle
+    if not os.path.exists(oracle.REF_SO):
+        return None
+    ref = oracle.Ref()
+    A = ref.gen3d(spec)
+    f = ref.scale(ref.ilu(A, ref.cfg(kv)), "row")
+    _, (urp, uci, uv), _, _ = ref.factors_arrays(f)
+    n = len(urp) - 1
+    keep = np.ones(len(uci), dtype=bool)
+    keep[urp[:-1][np.diff(urp) > 0]] = False  # every U row starts with its (unit) diagonal
+    rp = np.concatenate([[0], np.cumsum(np.diff(urp) - (np.diff(urp) > 0))])
+    Us = ref.mat(rp, uci[keep], uv[keep])
+    nnz = int(rp[-1])
+    T = os.cpu_count() or 1
+    xs = [np.random.default_rng(7 + t).uniform(-1, 1, n) for t in range(T)]
+    best, steps, t0 = 1e300, 0, time.perf_counter()
+    while steps < 3 and time.perf_counter() - t0 < budget_s:
+        th = [threading.Thread(target=ref.spmv, args=(Us, xs[t], n)) for t in range(T)]
+        t = time.perf_counter()
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        best = min(best, time.perf_counter() - t)
+        steps += 1
+    ref.free_mat(Us)
+    ref.free_mat(A)
+    return {"value": round(T * (12 * nnz + 28 * n + 4) / best / 1e9, 3), "unit": "GB/s", "cores": T,
+            "sample": f"{spec}: one strict-U sweep core (spmv_into, pre-split U_s, nnz {nnz}) per call, "
+                      f"{T} concurrent calls, best of {steps}",
+            "note": "for comparison with the device U sweep (roofline.achieved), not with the smoother step"}
+
+
 def cpu_baseline():
     """Bounded sample for the GPU arm's line (~10-30 s): the 16-plane slab."""
     return ref_smoother_rate(SAMPLE_SPEC, ILU_KV, max_steps=2, budget_s=15.0)
@@ -261,6 +303,10 @@ def run_reference(args):
                   "final_relres": float(rep["final_relres"]), "cores": 1}
     except Exception as e:  # report, never lose the line
         tts_c1 = {"error": str(e)[:200]}
+    try:
+        sweeps = ref_sweeps_only_rate(SAMPLE_SPEC if not args.strong else "poisson3d(465,465,16)", kv)
+    except Exception as e:  # report, never lose the line
+        sweeps = {"error": str(e)[:200]}
     why = None if full else (f"full {spec} needs ~{need_gb:.0f} GB host RAM in the reference's int64 CSR layout, "
                              f"{info['mem_available_gb']} GB available (or --ref-sample): a slab of the same "
                              f"matrix family with the same per-row work is timed")
@@ -272,7 +318,7 @@ def run_reference(args):
                    "same_config": bool(full), "why_not_same": why,
                    "parallelism": f"reference CPU code, {base['cores']} concurrent calls on rank 0's host"},
         "cpu_baseline": base, "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "tts": {"C1": tts_c1}, "vs_baseline": None})
+        "sweeps_only": sweeps, "tts": {"C1": tts_c1}, "vs_baseline": None})
 
 
 def build_workload(ilug, args, rank, world, local, use_dist=False):
