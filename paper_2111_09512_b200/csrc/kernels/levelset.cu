@@ -22,6 +22,7 @@
 //    cta1) and k_levels_flags (separate epoch-stamped flags, =flags).
 #include "levelset.hpp"
 
+#include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #include <algorithm>
@@ -701,6 +702,172 @@ k_levels_vsub(SellView M, i64 ngroups, const double* __restrict__ b, double* x, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster form of the value-flag schedule (small operators; ILUG_LEVELSET_DSM): the
+// solution lives in the distributed shared memory of one thread-block
+// cluster — row c in CTA c >> shift at c & (2^shift - 1) — and rows publish /
+// poll their values there (a cross-CTA DSMEM round trip, ~215 cycles, instead
+// of an L2 one). Rows are dealt round-robin in level order to the W-lane
+// sub-groups of the cluster (each walks its rows in level order; all are
+// co-resident), the next row's metadata and entries are loaded while the
+// current one waits; products and the ordered shuffle chain are the sub-warp
+// form's, so the result is bitwise the serial one.
+namespace cg = cooperative_groups;
+constexpr int kDsmBlock = 512;
+
+__device__ __forceinline__ unsigned long long ld_dsm(const double* p) {
+    return static_cast<unsigned long long>(*reinterpret_cast<const volatile long long*>(p));
+}
+__device__ __forceinline__ void st_dsm(double* p, unsigned long long v) {
+    *reinterpret_cast<volatile long long*>(p) = static_cast<long long>(v);
+}
+
+template <int MODE, int W>
+__global__ void __launch_bounds__(kDsmBlock, 1)
+k_levels_dsm(SellView M, i64 n, int shift, const double* __restrict__ b, double* x, const double* __restrict__ xold) {
+    constexpr int E = 4; // one pass: rows of up to W * 4 entries (the plan checks)
+    extern __shared__ __align__(16) double sx[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned rank = cluster.block_rank(), csize = cluster.num_blocks();
+    const int chunk = 1 << shift;
+    const unsigned cmask = static_cast<unsigned>(chunk - 1);
+    for (int i = threadIdx.x; i < chunk; i += blockDim.x) reinterpret_cast<unsigned long long*>(sx)[i] = kXSentinel;
+    cluster.sync();
+    auto xptr = [&](i32 c) -> double* {
+        return cluster.map_shared_rank(sx, static_cast<unsigned>(c) >> shift) + (static_cast<unsigned>(c) & cmask);
+    };
+    constexpr int RPG = 32 / W;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / W, j = lane % W;
+    const i64 G = static_cast<i64>(csize) * (kDsmBlock / 32) * RPG;
+    const i64 g0 = (static_cast<i64>(rank) * (kDsmBlock / 32) + (threadIdx.x >> 5)) * RPG + sub;
+    const i64 npad = M.nrows_pad;
+    const i64 rounds = (npad + G - 1) / G;
+    struct Row {
+        int len;
+        i32 row;
+        bool valid;
+        i32 c[E];
+        double a[E];
+    };
+    auto load = [&](i64 p, Row& r) {
+        r.len = 0, r.row = 0, r.valid = false;
+        i64 base = 0;
+        if (p < npad) {
+            const i32 rw = M.perm[p];
+            if (rw >= 0) r.valid = true, r.row = rw, r.len = M.rowlen[p], base = M.slice_ptr[p >> 5] + (p & 31);
+        }
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            const int t = j + W * u;
+            if (t < r.len) {
+                const i64 qq = base + static_cast<i64>(t) * kSlice;
+                r.c[u] = __ldg(M.cols + qq);
+                r.a[u] = __ldg(M.vals + qq);
+            }
+        }
+    };
+    Row cur, nxt;
+    load(g0, cur);
+    for (i64 k = 0; k < rounds; ++k) {
+        load(g0 + (k + 1) * G, nxt);
+        const int len = cur.len;
+        const i32 row = cur.row;
+        double s = j == 0 && cur.valid ? b[row] : 0.0, d = 1.0;
+        int maxlen = len;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        double pr[E];
+        int kind[E];
+        unsigned pend = 0;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            const int t = j + W * u;
+            kind[u] = 2;
+            pr[u] = 0.0;
+            if (t < len) {
+                if (MODE != 0 && cur.c[u] == row) {
+                    kind[u] = 1;
+                } else if (is_dep<MODE>(cur.c[u], row)) {
+                    const unsigned long long v = ld_dsm(xptr(cur.c[u]));
+                    pr[u] = __longlong_as_double(static_cast<long long>(v));
+                    kind[u] = 0;
+                    if (v == kXSentinel) pend |= 1u << u;
+                } else {
+                    pr[u] = __ldg(xold + cur.c[u]); // GS (MODE 2) only
+                    kind[u] = 0;
+                }
+            }
+        }
+        long long spins = 0;
+        while (pend) {
+            if (++spins > (1ll << 26)) {
+                atomicExch(&g_levelset_timeout, 1u);
+                break;
+            }
+#pragma unroll
+            for (int u = 0; u < E; ++u)
+                if ((pend >> u) & 1u) {
+                    const unsigned long long v = ld_dsm(xptr(cur.c[u]));
+                    if (v != kXSentinel) {
+                        pr[u] = __longlong_as_double(static_cast<long long>(v));
+                        pend &= ~(1u << u);
+                    }
+                }
+        }
+        bool has_d = false;
+        double dl = 0.0;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            if (MODE != 0 && kind[u] == 1) dl = cur.a[u], has_d = true;
+            pr[u] = kind[u] == 0 ? cur.a[u] * pr[u] : 0.0;
+        }
+        if (MODE != 0) {
+            const unsigned bal = __ballot_sync(0xffffffffu, has_d);
+            const unsigned mine = (bal >> (sub * W)) & ((W == 32 ? 0u : (1u << W)) - 1u);
+            const double dv = __shfl_sync(0xffffffffu, dl, sub * W + (mine ? __ffs(mine) - 1 : 0));
+            if (mine) d = dv;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            if (W * u >= maxlen) break;
+#pragma unroll
+            for (int jj = 0; jj < W; ++jj) {
+                const double v = __shfl_sync(0xffffffffu, pr[u], sub * W + jj);
+                if (j == 0 && W * u + jj < len) s = s - v;
+            }
+        }
+        if (j == 0 && cur.valid) {
+            const double r = MODE == 0 ? s : s / d;
+            unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(r));
+            if (bits == kXSentinel) bits = 0x7FFFFFFFFFFFFFFFull;
+            st_dsm(xptr(row), bits);
+        }
+        cur = nxt;
+    }
+    cluster.sync();
+    const i64 r0 = static_cast<i64>(rank) << shift;
+    for (int i = threadIdx.x; i < chunk && r0 + i < n; i += blockDim.x) x[r0 + i] = sx[i];
+}
+
+template <int MODE>
+const void* dsm_kernel(int max_row) {
+    return max_row <= 32 ? reinterpret_cast<const void*>(k_levels_dsm<MODE, 8>)
+                         : reinterpret_cast<const void*>(k_levels_dsm<MODE, 32>);
+}
+// ILUG_LEVELSET_DSM: unset = the cluster form for operators of up to 10 K rows
+// (the small coarse levels, where it measured 5-45 % faster per GS sweep:
+// C2 levels 4-8, C1 levels 3-6; wider levels need more than one cluster's SMs:
+// C2 level 2 3.07 vs 2.0 ms; profiles/r02_gs_dsm3.txt); 1 = wherever it fits;
+// 0 = never
+int dsm_mode(i64 n) {
+    const char* e = std::getenv("ILUG_LEVELSET_DSM");
+    if (e && e[0] == '0') return 0;
+    if (e && e[0] == '1') return 1;
+    return n <= 10000 ? 1 : 0;
+}
+
 int vf_sub_override() { // ILUG_VF_SUB (A/B): 0 / 1 thread per row (16- / 8-entry chunks), 2 / 4 / 8 / 83 / 16 / 88 / 164 / 168 / 324 lanes (x entries)
     const char* e = std::getenv("ILUG_VF_SUB");
     return e ? std::atoi(e) : -1;
@@ -920,6 +1087,41 @@ void LevelPlan::build(const Csr& T, Kind kind, cudaStream_t st, const double* de
     value_flags_ = true;
     if (const char* force = std::getenv("ILUG_LEVELSET"))
         if (std::string(force) == "flags") value_flags_ = false; // the separate-flag form (A/B, tests)
+    dsm_cs_ = 0;
+    dsm_max_row_ = static_cast<int>(max_row);
+    if (dsm_mode(n) && !single_cta_ && value_flags_ && n > 0 && max_row <= 128) {
+        const int mode = kind == Kind::lower_unit ? 0 : (kind == Kind::upper ? 1 : 2);
+        const void* fn = mode == 0 ? dsm_kernel<0>(dsm_max_row_) : mode == 1 ? dsm_kernel<1>(dsm_max_row_)
+                                                                             : dsm_kernel<2>(dsm_max_row_);
+        for (int cs : {8, 16}) {
+            int shift = 0;
+            while ((i64{1} << shift) * cs < n) ++shift;
+            const int smem = static_cast<int>((i64{1} << shift) * static_cast<i64>(sizeof(double)));
+            if (smem > 200 * 1024) continue;
+            // the attribute is per kernel, shared by every plan: the largest size any plan uses
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+                (cs > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+                (void)cudaGetLastError();
+                continue;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(cs));
+            cfg.blockDim = dim3(kDsmBlock);
+            cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+            at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, fn, &cfg) == cudaSuccess && nc >= 1) {
+                dsm_cs_ = cs, dsm_shift_ = shift, dsm_smem_ = smem;
+                break;
+            }
+            (void)cudaGetLastError();
+        }
+    }
     if (const char* force = std::getenv("ILUG_LEVELSET"))
         if (std::string(force) == "vflags" && n > 0) single_cta_ = false;
     if (!single_cta_) {
@@ -984,6 +1186,26 @@ void LevelPlan::solve(const double* b, double* x, const double* xold, cudaStream
     unsigned* ticket = flags_.p + n + 1;
     i64 ns = M_.nrows_pad / kSlice;
     if (value_flags_ && x != b && x != xold) {
+        if (dsm_cs_ > 0 && vf_sub_override() < 0) { // the cluster (DSMEM) form
+            const void* fn = mode == 0 ? dsm_kernel<0>(dsm_max_row_) : mode == 1 ? dsm_kernel<1>(dsm_max_row_)
+                                                                                 : dsm_kernel<2>(dsm_max_row_);
+            i64 nn = n;
+            int sh = dsm_shift_;
+            void* dargs[] = {&mv, &nn, &sh, &b, &x, &xold};
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(dsm_cs_));
+            cfg.blockDim = dim3(kDsmBlock);
+            cfg.dynamicSmemBytes = static_cast<size_t>(dsm_smem_);
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = static_cast<unsigned>(dsm_cs_);
+            at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            ILUG_CUDA(cudaLaunchKernelExC(&cfg, fn, dargs));
+            return;
+        }
         // the solution entries are the flags: fill x with the sentinel, reset the ticket
         k_fill_sentinel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, n);
         k_ticket_reset<<<1, 1, 0, st>>>(ticket);

@@ -45,6 +45,7 @@ private:
     int vf_form_ = 0;
     bool sx_ = false;         // one-CTA warp kernel with the solution in shared memory         // value-flag kernel form: 1 thread per row (8-entry chunks), 8 / 83 lanes per row
     i64 max_level_rows_ = 0;
+    int dsm_cs_ = 0, dsm_shift_ = 0, dsm_smem_ = 0, dsm_max_row_ = 0; // ILUG_LEVELSET_DSM=1 cluster form
 };
 
 /// Sync `st`, then raise ERR_NUMERIC if a sync-free level-set kernel hit its

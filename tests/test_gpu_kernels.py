@@ -507,3 +507,33 @@ def test_sell_device_layout_matches_host_layout(ilug, ref, torch_cuda, monkeypat
     assert bitwise(got["1"], got["0"]) and bitwise(got["1spmv"], got["0spmv"])
     Ar = ref.mat(*A.csr())
     assert bitwise(got["1"], ref.ilu_smooth_sweep(Ar, ref.smoother(Ar, ref.cfg(kv)), b, x0))
+
+
+@pytest.mark.parametrize("dsm", ["1", "0"])
+@pytest.mark.parametrize("spec,kv", [("poisson3d(40,40,30)", {}),
+                                     ("pressure27(24,24,20)", {"ilu.variant": "ilut", "ilu.droptol": "1e-3",
+                                                               "ilu.lfill": "5"})])
+def test_k5_cluster_dsmem_form_bitwise(ilug, ref, torch_cuda, monkeypatch, dsm, spec, kv):
+    """The thread-block-cluster form of the value-flag schedule (the solution
+    in the clusters' distributed shared memory; forced everywhere it fits with
+    ILUG_LEVELSET_DSM=1) and the global form give the serial L / U solves and
+    the GS sweep bitwise, repeatedly."""
+    monkeypatch.setenv("ILUG_LEVELSET", "vflags")
+    monkeypatch.setenv("ILUG_LEVELSET_DSM", dsm)
+    A, L, U, f, fr = _factors(ilug, ref, spec, kv, "row", direct=True)
+    b = np.random.default_rng(83).uniform(-1, 1, A.rows)
+    bd = _dev(torch_cuda, b)
+    y = torch_cuda.empty_like(bd)
+    for _ in range(2):
+        f.solve_lower(bd, y)
+        assert bitwise(_host(y), ref.solve_lower_direct(ref.mat(*L), b))
+        f.solve_upper(bd, y)
+        assert bitwise(_host(y), ref.solve_upper_scaled_direct(fr, b))
+    S = ilug.Smoother(A, ilug.Config().update({"smoother.kind": "gauss_seidel", "smoother.sweeps": "2"}))
+    x0 = np.random.default_rng(84).uniform(-1, 1, A.rows)
+    xd = _dev(torch_cuda, x0)
+    S.smooth(bd, xd)
+    Ar = ref.mat(*A.csr())
+    want, _ = ref.smooth(Ar, ref.smoother(Ar, ref.cfg({"smoother.kind": "gauss_seidel",
+                                                       "smoother.sweeps": "2"})), b, x0)
+    assert bitwise(_host(xd), want)
