@@ -44,6 +44,9 @@ constexpr size_t kStagedMin = size_t{32} << 20; // smaller copies take the plain
 /// parked and done when the last scope closes, or when the parked bytes pass a
 /// cap (ILUG_DEFER_FREE=0 disables; A/B).
 void dev_free(void* p, size_t bytes);
+/// cudaMalloc that, on out-of-memory, frees the parked (deferred) buffers and
+/// retries once before failing
+cudaError_t dev_malloc(void** p, size_t bytes);
 struct DeferFrees {
     DeferFrees();
     ~DeferFrees();
@@ -73,7 +76,7 @@ struct DBuf {
     void alloc(i64 count) {
         release();
         n = count;
-        if (count > 0) ILUG_CUDA(cudaMalloc(&p, static_cast<size_t>(count) * sizeof(T)));
+        if (count > 0) ILUG_CUDA(dev_malloc(reinterpret_cast<void**>(&p), static_cast<size_t>(count) * sizeof(T)));
     }
     void release() {
         if (p) dev_free(p, static_cast<size_t>(n) * sizeof(T));

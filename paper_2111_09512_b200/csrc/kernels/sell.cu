@@ -67,6 +67,21 @@ void dev_free(void* p, size_t bytes) {
     }
     cudaFree(p);
 }
+cudaError_t dev_malloc(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaErrorMemoryAllocation) return e;
+    (void)cudaGetLastError(); // clear the sticky-free error state of the failed call
+    std::vector<void*> flush;
+    {
+        std::lock_guard<std::mutex> g(g_defer_mu);
+        flush.swap(g_deferred);
+        g_deferred_bytes = 0;
+    }
+    if (flush.empty()) return e;
+    free_all(flush);
+    return cudaMalloc(p, bytes);
+}
+
 DeferFrees::DeferFrees() { g_defer.fetch_add(1, std::memory_order_acq_rel); }
 DeferFrees::~DeferFrees() {
     if (g_defer.fetch_sub(1, std::memory_order_acq_rel) != 1) return;
