@@ -860,16 +860,18 @@ __global__ void k_window_offsets(i64 nw, i64 sigma, i64 n, int* __restrict__ off
 }
 // per slice: width (max length) of the natural and of the sorted order
 __global__ void k_slice_widths(i64 ns, i64 n, const i32* __restrict__ len, const i32* __restrict__ slen,
-                               i64* __restrict__ wnat, i64* __restrict__ wsort) {
+                               i64* __restrict__ wnat, i64* __restrict__ wsort, i64* __restrict__ snnz) {
     const i64 s = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
     if (s >= ns) return;
     i32 a = 0, b = 0;
+    i64 t = 0;
     for (int l = 0; l < kSlice; ++l) {
         const i64 p = s * kSlice + l;
-        if (p < n) a = max(a, len[p]), b = max(b, slen ? slen[p] : 0);
+        if (p < n) a = max(a, len[p]), b = max(b, slen ? slen[p] : 0), t += len[p];
     }
     wnat[s] = a;
     if (wsort) wsort[s] = b;
+    if (snnz) snnz[s] = t;
 }
 __global__ void k_layout_rows(i64 pad, i64 n, const i32* __restrict__ len, const i32* __restrict__ order,
                               i32* __restrict__ perm, std::uint16_t* __restrict__ rowlen) {
@@ -885,9 +887,6 @@ __global__ void k_slice_ptr_from_widths(i64 ns, const i64* __restrict__ w, i64* 
     if (s == 0) sp[0] = 0;
 }
 
-struct WidenI32 {
-    __host__ __device__ i64 operator()(i32 v) const { return static_cast<i64>(v); }
-};
 template <class It, class Op>
 i64 dev_reduce(It in, i64 n, Op op, i64 init, cudaStream_t st) {
     DBuf<i64> out(1);
@@ -935,14 +934,15 @@ void layout_device(Sell& out, i64 n, const i32* len, cudaStream_t st) {
             t.p, tmp, len, keys_out.p, iota.p, order.p, static_cast<int>(n), static_cast<int>(nw), off.p,
             off.p + 1, st));
         wsort.alloc(ns);
-        k_slice_widths<<<grid_for(ns), kBlock, 0, st>>>(ns, n, len, keys_out.p, wnat.p, wsort.p);
+        k_slice_widths<<<grid_for(ns), kBlock, 0, st>>>(ns, n, len, keys_out.p, wnat.p, wsort.p, nullptr);
         ILUG_LAUNCH_CHECK();
         const i64 pn = dev_reduce(wnat.p, ns, SumI64{}, 0, st), ps = dev_reduce(wsort.p, ns, SumI64{}, 0, st);
         ILUG_CUDA(cudaStreamSynchronize(st)); // t, iota, off die here
         sorted = !(static_cast<double>(ps) > 0.97 * static_cast<double>(pn));
     }
     if (!sorted) {
-        k_slice_widths<<<grid_for(std::max<i64>(ns, 1)), kBlock, 0, st>>>(ns, n, len, nullptr, wnat.p, nullptr);
+        k_slice_widths<<<grid_for(std::max<i64>(ns, 1)), kBlock, 0, st>>>(ns, n, len, nullptr, wnat.p, nullptr,
+                                                                           nullptr);
         ILUG_LAUNCH_CHECK();
     }
     const i64* w = sorted ? wsort.p : wnat.p;
@@ -971,9 +971,14 @@ void layout_device(Sell& out, i64 n, const i32* len, cudaStream_t st) {
                                                          sorted ? out.perm.p : nullptr, out.rowlen.p);
         ILUG_LAUNCH_CHECK();
     }
-    out.nnz = n > 0 ? dev_reduce(cub::TransformInputIterator<i64, WidenI32, const i32*>(len, WidenI32{}), n,
-                                 SumI64{}, 0, st)
-                    : 0;
+    if (ns > 0) { // stored entries: per-slice sums of the lengths, then one reduction
+        DBuf<i64> snnz(ns);
+        k_slice_widths<<<grid_for(ns), kBlock, 0, st>>>(ns, n, len, nullptr, wnat.p, nullptr, snnz.p);
+        ILUG_LAUNCH_CHECK();
+        out.nnz = dev_reduce(static_cast<const i64*>(snnz.p), ns, SumI64{}, 0, st);
+    } else {
+        out.nnz = 0;
+    }
     out.cols.alloc(out.padded);
     out.vals.alloc(out.padded);
     if (out.padded > 0) {
