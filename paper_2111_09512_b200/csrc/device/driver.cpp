@@ -12,6 +12,7 @@
 #include <condition_variable>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <sstream>
 
 namespace ilug {
@@ -67,17 +68,37 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     // concurrently with the host AMG setup, which does not need it and does
     // not touch the GPU. Identical factors either way (same function, same input).
     const SmootherConfig& s0 = ap.plan.for_level(0);
+    // the hierarchy itself on the GPU when supported (kernels/amg_setup.cu), else the host
+    const bool dev_setup = ap.device_setup != 0 && amg_device_supported(ap);
+    if (ap.device_setup == 2 && !dev_setup) fail_invalid("device.amg_setup=device needs amg.coarsening=pmis");
+    const bool fact0 = s0.kind == SmootherKind::ilu && A.nrows > ap.coarse_size;
+    // With both on the GPU, A crosses PCIe once: the factorisation and the AMG
+    // setup read the same device copy, which then becomes the level-0 operator.
+    DevCsr Ad;
+    const char* sa = std::getenv("ILUG_SHARE_A"); // =0: separate uploads (A/B)
+    const bool share_A = dev_setup && fact0 && !(sa && sa[0] == '0');
+    if (share_A) {
+        Ad.upload(A, st);
+        ILUG_CUDA(cudaStreamSynchronize(st));
+        tm.mark("upload A (shared)");
+    }
     std::future<DevFactors> f0;
-    if (s0.kind == SmootherKind::ilu && A.nrows > ap.coarse_size)
-        f0 = std::async(std::launch::async, [&] { return factorize_resident(A, s0.ilu_params, st, true); });
+    if (fact0)
+        f0 = std::async(std::launch::async,
+                        [&] { return factorize_resident(A, s0.ilu_params, st, true, share_A ? &Ad : nullptr); });
     // The device objects of level k are built (own stream, own thread) as soon
     // as the host setup has finished level k, overlapping the host setup of
     // the coarser levels. Level 0's smoother takes the factors computed above.
     DeviceHierarchy dh;
     dh.set_use_graph(use_graph);
     dh.begin();
+    // The setup's other GPU work (AMG kernels, SELL layouts) runs at the
+    // highest stream priority: its CTAs take the slots the factorisation's
+    // retiring CTAs free (kernels/ilut.cu launch_ilut) instead of queueing behind it.
+    int prio_lo = 0, prio_hi = 0;
+    ILUG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     cudaStream_t bst = nullptr;
-    ILUG_CUDA(cudaStreamCreateWithFlags(&bst, cudaStreamNonBlocking));
+    ILUG_CUDA(cudaStreamCreateWithPriority(&bst, cudaStreamNonBlocking, prio_hi));
     struct Item {
         i64 k;
         const HostLevel* lev;
@@ -90,27 +111,58 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     std::exception_ptr build_err;
     DevFactors pre;
     bool have_pre = false;
+    // With A shared on the device, level 0's operators are built from it as
+    // soon as the AMG's level 0 is final, and its smoother once the factors
+    // are (the builder does not wait for the factorisation before level 1).
+    bool pending0 = false;
+    const HostLevel* lev0 = nullptr;
+    auto finish0 = [&](bool block) {
+        if (!pending0 || (!block && f0.wait_for(std::chrono::seconds(0)) != std::future_status::ready)) return;
+        pending0 = false;
+        pre = f0.get();
+        have_pre = true;
+        dh.build_smoother0(*lev0, ap.plan.for_level(0), &pre, bst);
+    };
     std::thread builder([&] {
         for (;;) {
             Item it;
+            bool done = false;
             {
                 std::unique_lock<std::mutex> g(qm);
                 qcv.wait(g, [&] { return closed || !queue.empty(); });
-                if (queue.empty()) return;
-                it = queue.front();
-                queue.pop_front();
-            }
-            if (build_err) continue; // drain after a failure
-            try {
-                DevFactors* l0 = nullptr;
-                if (it.k == 0 && !it.last && f0.valid()) { // the level-0 smoother uses the early factors
-                    pre = f0.get();
-                    have_pre = true;
-                    l0 = &pre;
+                if (queue.empty()) {
+                    done = true;
+                } else {
+                    it = queue.front();
+                    queue.pop_front();
                 }
-                dh.build_level(static_cast<int>(it.k), *it.lev, ap.plan.for_level(it.k), it.last, l0, bst);
+            }
+            if (build_err) {
+                if (done) return;
+                continue; // drain after a failure
+            }
+            try {
+                if (done) {
+                    finish0(true);
+                    return;
+                }
+                if (it.k == 0 && !it.last && f0.valid() && share_A) {
+                    dh.build_level0_ops(*it.lev, Ad.rp.p, Ad.ci.p, Ad.v.p, bst);
+                    pending0 = true;
+                    lev0 = it.lev;
+                } else {
+                    DevFactors* l0 = nullptr;
+                    if (it.k == 0 && !it.last && f0.valid()) { // the level-0 smoother uses the early factors
+                        pre = f0.get();
+                        have_pre = true;
+                        l0 = &pre;
+                    }
+                    dh.build_level(static_cast<int>(it.k), *it.lev, ap.plan.for_level(it.k), it.last, l0, bst);
+                }
+                finish0(false);
             } catch (...) {
                 build_err = std::current_exception();
+                if (done) return;
             }
         }
     });
@@ -127,7 +179,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     AmgParams apd = ap;
     cudaStream_t gst = nullptr;
     if (galerkin_on_device()) {
-        ILUG_CUDA(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
+        ILUG_CUDA(cudaStreamCreateWithPriority(&gst, cudaStreamNonBlocking, prio_hi));
         apd.galerkin = [gst](const Csr& Ak, const Csr& P, const Csr& R) { return galerkin_device(Ak, P, R, gst); };
     }
     struct StreamGuard {
@@ -137,15 +189,11 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
         }
     } gguard{gst};
     try {
-        // the hierarchy itself on the GPU when supported (kernels/amg_setup.cu), else the host
-        const bool dev_setup = apd.device_setup != 0 && amg_device_supported(apd);
-        if (apd.device_setup == 2 && !dev_setup)
-            fail_invalid("device.amg_setup=device needs amg.coarsening=pmis");
         cudaStream_t sst = nullptr;
-        if (dev_setup) ILUG_CUDA(cudaStreamCreateWithFlags(&sst, cudaStreamNonBlocking));
+        if (dev_setup) ILUG_CUDA(cudaStreamCreateWithPriority(&sst, cudaStreamNonBlocking, prio_hi));
         StreamGuard sguard{sst};
         auto setup = [&](const LevelReady& cb) {
-            return dev_setup ? amg_setup_device(A, apd, cb, sst) : amg_setup(A, apd, cb);
+            return dev_setup ? amg_setup_device(A, apd, cb, sst, share_A ? &Ad : nullptr) : amg_setup(A, apd, cb);
         };
         oc.hier = setup([&](i64 k, const HostLevel& lev, bool last) {
             {

@@ -519,6 +519,31 @@ void DeviceHierarchy::build_level(int k, const HostLevel& hl, const SmootherConf
     ILUG_CUDA(cudaStreamSynchronize(st));
 }
 
+void DeviceHierarchy::build_level0_ops(const HostLevel& hl, const i64* rp, const i32* ci, const double* v,
+                                       cudaStream_t st) {
+    if (num_levels() != 0) fail_invalid("device hierarchy: levels must be built in order");
+    SetupTimer tm("device");
+    Lev& lv = levels_.emplace_back();
+    lv.n = hl.A.nrows;
+    lv.A.build(hl.A, rp, ci, v, st);
+    sell_from_host(lv.P, hl.P, Part::all, st);
+    sell_from_host(lv.R, hl.R, Part::all, st);
+    lv.b.alloc(std::max<i64>(lv.n, 1));
+    lv.x.alloc(std::max<i64>(lv.n, 1));
+    lv.r.alloc(std::max<i64>(lv.n, 1));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    tm.mark("A,P,R", 0);
+}
+
+void DeviceHierarchy::build_smoother0(const HostLevel& hl, const SmootherConfig& sc, DevFactors* level0,
+                                      cudaStream_t st) {
+    SetupTimer tm("device");
+    Lev& lv = levels_.at(0);
+    lv.smoother.build(hl.A, lv.A, sc, st, level0);
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    tm.mark("smoother", 0);
+}
+
 void DeviceHierarchy::finish(const HostHierarchy& h, cudaStream_t st) {
     lu_.upload(h.coarse.lu.data(), static_cast<i64>(h.coarse.lu.size()), st);
     piv_.upload(h.coarse.piv.data(), static_cast<i64>(h.coarse.piv.size()), st);

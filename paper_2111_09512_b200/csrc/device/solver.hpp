@@ -223,6 +223,10 @@ public:
     void begin();
     void build_level(int k, const HostLevel& hl, const SmootherConfig& sc, bool last, DevFactors* level0,
                      cudaStream_t st);
+    /// Level 0's operators from a device copy of A (rp, ci, v) with its
+    /// smoother left for build_smoother0() (the factors are still computing).
+    void build_level0_ops(const HostLevel& hl, const i64* rp, const i32* ci, const double* v, cudaStream_t st);
+    void build_smoother0(const HostLevel& hl, const SmootherConfig& sc, DevFactors* level0, cudaStream_t st);
     void finish(const HostHierarchy& h, cudaStream_t st);
     /// z = M(r) with z zeroed first (the driver's precond lambda, src/driver.cpp:182-185).
     void vcycle(const double* r, double* z, cudaStream_t st);

@@ -47,6 +47,7 @@ class SetupTimer {
 public:
     explicit SetupTimer(const char* scope);
     void mark(const char* phase, i64 level = -1);
+    bool on() const { return on_; }
 
 private:
     const char* scope_;

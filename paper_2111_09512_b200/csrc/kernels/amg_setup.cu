@@ -697,7 +697,8 @@ DevCsr interp_mm_ext_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp
 
 bool amg_device_supported(const AmgParams& p) { return p.coarsening == Coarsening::pmis; }
 
-HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st) {
+HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st,
+                               const DevCsr* Ad) {
     if (A.nrows != A.ncols) fail_invalid("setup: matrix must be square");
     if (!(prm.theta > 0.0 && prm.theta <= 1.0)) fail_invalid("setup: theta must lie in (0, 1]");
     if (prm.coarse_size < 1) fail_invalid("setup: coarse_size must be >= 1");
@@ -708,15 +709,18 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
     h.params = prm;
     h.levels.reserve(static_cast<size_t>(prm.max_levels)); // stable level addresses for on_level
     SetupTimer tm("amg-device");
-    DevCsr cur;
-    cur.upload(A, st);
+    DevCsr own;
+    if (!Ad) own.upload(A, st);
     tm.mark("upload A");
+    const DevCsr* curp = Ad ? Ad : &own; // level k's operator on the device
     for (;;) {
         h.levels.emplace_back();
         HostLevel& lev = h.levels.back();
         const i64 k = h.num_levels() - 1;
-        lev.A = k == 0 ? csr_copy(A) : cur.download(st);
+        lev.A = k == 0 ? csr_copy(A) : curp->download(st);
+        tm.mark("host A", k);
         if (lev.A.nrows <= prm.coarse_size || k + 1 >= prm.max_levels) break;
+        const DevCsr& cur = *curp;
         DevCsr S = strength_device(cur, prm.theta, st);
         DevCsr St = transpose_device(S, false, st);
         tm.mark("strength", k);
@@ -747,7 +751,8 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
         ILUG_CUDA(cudaStreamSynchronize(st));
         tm.mark("download P,R", k);
         if (on_level) on_level(k, lev, false);
-        cur = std::move(C);
+        own = std::move(C);
+        curp = &own;
     }
     if (on_level) on_level(h.num_levels() - 1, h.levels.back(), true);
     h.coarse = dense_lu_factor(h.levels.back().A);

@@ -36,6 +36,9 @@ bool amg_device_supported(const AmgParams& p);
 /// amg_setup on the device: the hierarchy is built level by level on the GPU
 /// and every level's A/P/R/split is handed to the host structures (and to
 /// on_level) as soon as it is final; the result equals amg_setup bit for bit.
-HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st);
+/// Ad: A already on the device (read only; the caller keeps it alive until
+/// on_level(0) has been called), else A is uploaded.
+HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st,
+                               const DevCsr* Ad = nullptr);
 
 } // namespace ilug

@@ -12,6 +12,7 @@
 // the factors are bitwise the host ones. A bounded spin turns a scheduling bug
 // into an error instead of a hung GPU.
 #include "ilu0.hpp"
+#include "spgemm.hpp"
 
 #include <cuda/atomic>
 
@@ -214,6 +215,7 @@ void ilu0_eliminate(i64 n, const i64* rp, const i32* ci, const i64* dpos, const 
         ILUG_LAUNCH_CHECK();
         unsigned long long h = 0;
         unsigned bad = 0;
+        ILUG_CUDA(cudaStreamSynchronize(st)); // not inside the pageable copies (see ilut.cu)
         ILUG_CUDA(cudaMemcpyAsync(&h, fz.p, sizeof h, cudaMemcpyDeviceToHost, st));
         ILUG_CUDA(cudaMemcpyAsync(&bad, epoch + 2, sizeof bad, cudaMemcpyDeviceToHost, st));
         ILUG_CUDA(cudaStreamSynchronize(st));
@@ -288,7 +290,7 @@ DevFactors DevFactors::upload(const HostFactors& f, cudaStream_t st) {
     return d;
 }
 
-DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool keep_A) {
+DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool keep_A, const DevCsr* Ad) {
     if (A.nrows != A.ncols) fail_invalid("ilu0: matrix must be square");
     const i64 n = A.nrows;
     std::vector<i64> dpos(static_cast<size_t>(n), -1);
@@ -320,17 +322,22 @@ DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool k
     DBuf<i64> rp, dp;
     DBuf<i32> ci;
     DBuf<double> a, wd;
-    rp.upload(A.rp.data(), n + 1, st);
-    ci.upload(A.ci.data(), nnz, st);
+    if (!Ad) {
+        rp.upload(A.rp.data(), n + 1, st);
+        ci.upload(A.ci.data(), nnz, st);
+        a.upload(A.v.data(), nnz, st);
+    }
+    const i64* const rpp = Ad ? Ad->rp.p : rp.p;
+    const i32* const cip = Ad ? Ad->ci.p : ci.p;
+    const double* const ap = Ad ? Ad->v.p : a.p;
     dp.upload(dpos.data(), n, st);
-    a.upload(A.v.data(), nnz, st);
     wd.alloc(nnz);
     DBuf<i32> ord;
     {
         const std::vector<i32> o = ilu0_level_order(A, dpos);
         ord.upload(o.data(), n, st);
     }
-    ilu0_eliminate(n, rp.p, ci.p, dp.p, a.p, wd.p, nnz, patch, A, ord.p, st);
+    ilu0_eliminate(n, rpp, cip, dp.p, ap, wd.p, nnz, patch, A, ord.p, st);
     f.Lrp.upload(f.Lrp_h.data(), n + 1, st);
     f.Urp.upload(f.Urp_h.data(), n + 1, st);
     f.Lci.alloc(f.Lrp_h[n]);
@@ -338,11 +345,11 @@ DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool k
     f.Uci.alloc(f.Urp_h[n]);
     f.Uv.alloc(f.Urp_h[n]);
     const unsigned g = static_cast<unsigned>((n + kBlock - 1) / kBlock);
-    k_ilu0_split<<<g, kBlock, 0, st>>>(n, rp.p, ci.p, dp.p, wd.p, f.Lrp.p, f.Urp.p, f.Lci.p, f.Lv.p, f.Uci.p,
+    k_ilu0_split<<<g, kBlock, 0, st>>>(n, rpp, cip, dp.p, wd.p, f.Lrp.p, f.Urp.p, f.Lci.p, f.Lv.p, f.Uci.p,
                                        f.Uv.p);
     ILUG_LAUNCH_CHECK();
     ILUG_CUDA(cudaStreamSynchronize(st)); // temporaries die at scope exit
-    if (keep_A) f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(a);
+    if (keep_A && !Ad) f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(a);
     return f;
 }
 
@@ -455,9 +462,9 @@ HostFactors factorize(const Csr& A, const IluParams& p, cudaStream_t st) {
     return ilu_factorize(A, p);
 }
 
-DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A) {
-    if (p.variant == IluVariant::ilu0 && ilu0_on_device()) return ilu0_resident(A, p.pivot_patch, st, keep_A);
-    if (p.variant == IluVariant::ilut && ilut_on_device()) return ilut_resident(A, p, st, keep_A);
+DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A, const DevCsr* Ad) {
+    if (p.variant == IluVariant::ilu0 && ilu0_on_device()) return ilu0_resident(A, p.pivot_patch, st, keep_A, Ad);
+    if (p.variant == IluVariant::ilut && ilut_on_device()) return ilut_resident(A, p, st, keep_A, Ad);
     return DevFactors::upload(ilu_factorize(A, p), st);
 }
 

@@ -9,6 +9,8 @@
 
 namespace ilug {
 
+struct DevCsr; // spgemm.hpp
+
 /// Incomplete factors resident on the device, CSR: L strict (unit diagonal
 /// implicit), U upper. `diag_first`: every U row starts with its diagonal
 /// (true for every factorisation here), so the strict-upper part of row r has
@@ -33,11 +35,16 @@ struct DevFactors {
 };
 
 /// Device-resident ILU(0) / ILUT (no host round trip of the factors).
-DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool keep_A = false);
-DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false);
+/// Ad: A already on the device (shared with the concurrent AMG setup; read
+/// only, the caller keeps it, keep_A is then ignored), else A is uploaded.
+DevFactors ilu0_resident(const Csr& A, PivotPatch patch, cudaStream_t st, bool keep_A = false,
+                         const DevCsr* Ad = nullptr);
+DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false,
+                         const DevCsr* Ad = nullptr);
 /// factorize() that leaves the factors on the device (host factorisations,
 /// when forced with ILUG_ILU0_DEVICE=0 / ILUG_ILUT_DEVICE=0, are uploaded).
-DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false);
+DevFactors factorize_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A = false,
+                              const DevCsr* Ad = nullptr);
 
 /// Hash of a CSR's column pattern (pattern checks for refactorisation).
 std::uint64_t csr_pattern_hash(const Csr& A);

@@ -25,6 +25,7 @@
 // a larger capacity (fewer warps per CTA). A bounded spin turns a scheduling
 // bug into an error instead of a hung GPU.
 #include "ilu0.hpp"
+#include "spgemm.hpp"
 
 #include <cub/device/device_scan.cuh>
 #include <cuda/atomic>
@@ -64,6 +65,7 @@ struct IlutArgs {
     unsigned* err;       // [0] wait timeout, [1] overflow (needed capacity)
     int wrank;           // fill ranking in registers when <= 32 candidates (ILUG_ILUT_WRANK)
     unsigned backoff_ns; // longest poll back-off (ILUG_ILUT_BACKOFF)
+    int quota;           // rows a warp takes before its CTA may retire (ILUG_ILUT_QUOTA)
 };
 
 // Dependency wait with exponential back-off (32 ns doubling up to max_ns):
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
     const unsigned E = *a.epoch;
     const unsigned full = 0xffffffffu;
 
-    for (;;) {
+    for (int q = a.quota; q > 0; --q) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(a.ticket, 1ull);
         const i64 i = static_cast<i64>(__shfl_sync(full, t, 0));
@@ -531,6 +533,13 @@ bool ilut_wrank() {
     return !(e && e[0] == '0');
 }
 
+// ILUG_ILUT_QUOTA=<rows>: rows per warp before its CTA retires (0: persistent)
+int ilut_quota() {
+    const char* e = std::getenv("ILUG_ILUT_QUOTA");
+    const int q = e ? std::atoi(e) : 256;
+    return q > 0 ? q : INT_MAX;
+}
+
 bool ilut_value_flags() {
     const char* e = std::getenv("ILUG_ILUT_VF");
     return e && e[0] == '1';
@@ -556,7 +565,14 @@ void launch_ilut(const IlutArgs& a, i64 ucap, cudaStream_t st) {
     i64 sms = device_sm_count();
     if (const char* e = std::getenv("ILUG_ILUT_SMS"))
         if (std::atoi(e) > 0) sms = std::min<i64>(sms, std::atoi(e));
-    const i64 grid = std::min<i64>(static_cast<i64>(per_sm) * sms, (a.n + WARPS - 1) / WARPS);
+    // Each warp retires after a.quota rows, so the grid is the resident set
+    // plus enough CTAs to cover every row: CTAs of the concurrent AMG setup (on
+    // higher-priority streams) take the slots retiring CTAs free instead of
+    // waiting for the whole factorisation. Safe: a warp claims its ticket when
+    // it starts, so it only waits on rows claimed by running or finished warps.
+    const i64 resident = std::min<i64>(static_cast<i64>(per_sm) * sms, (a.n + WARPS - 1) / WARPS);
+    const i64 cover = (a.n + static_cast<i64>(WARPS) * a.quota - 1) / (static_cast<i64>(WARPS) * a.quota);
+    const i64 grid = std::min<i64>(std::max(resident, cover + resident), INT_MAX);
     fn<<<static_cast<unsigned>(std::max<i64>(grid, 1)), WARPS * 32, smem, st>>>(a);
     ILUG_LAUNCH_CHECK();
 }
@@ -568,7 +584,7 @@ bool ilut_on_device() {
     return !(e && e[0] == '0');
 }
 
-DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A) {
+DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool keep_A, const DevCsr* Ad) {
     if (A.nrows != A.ncols) fail_invalid("ilut: matrix must be square");
     if (!(p.droptol >= 0.0) || !std::isfinite(p.droptol)) fail_invalid("ilut: droptol must be finite and >= 0");
     if (p.lfill < 0) fail_invalid("ilut: lfill must be >= 0");
@@ -590,11 +606,16 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
     DBuf<i64> rp, uoff(n + 1), loff(n + 1);
     DBuf<i32> ci;
     DBuf<double> av, tau(n);
-    rp.upload(A.rp.data(), n + 1, st);
-    ci.upload(A.ci.data(), nnz, st);
-    av.upload(A.v.data(), nnz, st);
+    if (!Ad) {
+        rp.upload(A.rp.data(), n + 1, st);
+        ci.upload(A.ci.data(), nnz, st);
+        av.upload(A.v.data(), nnz, st);
+    }
+    const i64* const rpp = Ad ? Ad->rp.p : rp.p;
+    const i32* const cip = Ad ? Ad->ci.p : ci.p;
+    const double* const avp = Ad ? Ad->v.p : av.p;
     const unsigned g = static_cast<unsigned>((n + 255) / 256);
-    k_ilut_prep<<<g, 256, 0, st>>>(n, rp.p, ci.p, av.p, p.droptol, p.lfill, tau.p, uoff.p, loff.p);
+    k_ilut_prep<<<g, 256, 0, st>>>(n, rpp, cip, avp, p.droptol, p.lfill, tau.p, uoff.p, loff.p);
     ILUG_LAUNCH_CHECK();
     inclusive_scan(uoff.p, n + 1, st);
     inclusive_scan(loff.p, n + 1, st);
@@ -608,9 +629,9 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
     DBuf<unsigned> sync(n + 3); // done flags, epoch, err[2]
     DBuf<unsigned long long> ctl(2); // ticket, first zero
     ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
-    IlutArgs a{n,       rp.p,   ci.p,   av.p,   tau.p,   p.lfill, anorm_f, 0,
+    IlutArgs a{n,       rpp,    cip,    avp,    tau.p,   p.lfill, anorm_f, 0,
                p.droptol, uoff.p, loff.p, uci.p, uv.p, ulen.p, lci.p, lv.p, llen.p, sync.p, sync.p + n,
-               ctl.p,   ctl.p + 1, sync.p + n + 1, ilut_wrank() ? 1 : 0, ilut_backoff_ns()};
+               ctl.p,   ctl.p + 1, sync.p + n + 1, ilut_wrank() ? 1 : 0, ilut_backoff_ns(), ilut_quota()};
     unsigned err[2] = {0, 0};
     for (int pass = 0; pass < 2; ++pass) {
         for (int cap_level = 0;; ++cap_level) {
@@ -624,6 +645,10 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
                 launch_ilut<1024, 4>(a, ucap, st);
             else
                 launch_ilut<6144, 2>(a, ucap, st);
+            // wait in cudaStreamSynchronize, not inside the pageable copy: a
+            // thread blocked in that copy stalls other threads' cudaMalloc
+            // (the concurrent AMG setup) until the kernel ends
+            ILUG_CUDA(cudaStreamSynchronize(st));
             ILUG_CUDA(cudaMemcpyAsync(err, sync.p + n + 1, sizeof err, cudaMemcpyDeviceToHost, st));
             ILUG_CUDA(cudaStreamSynchronize(st));
             if (err[0]) fail_numeric("ilut (device): dependency wait timed out (scheduling error)");
@@ -645,7 +670,7 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
         a.patch = 1;
     }
     // compact the slots into CSR (stays on the device; row starts to the host)
-    if (keep_A) {
+    if (keep_A && !Ad) {
         f.Arp = std::move(rp), f.Aci = std::move(ci), f.Av = std::move(av);
     } else {
         rp.release(), ci.release(), av.release();
