@@ -39,7 +39,21 @@ std::atomic<int> g_defer{0};
 std::mutex g_defer_mu;
 std::vector<void*> g_deferred;
 size_t g_deferred_bytes = 0;
-constexpr size_t kDeferCap = size_t{16} << 30;
+// Parked bytes before a flush: a third of the device (60 GB on a B200; at
+// least 16 GB). A flush mid-setup costs seconds (cudaFree of many large
+// buffers holds the allocator, stalling every setup thread's cudaMalloc);
+// dev_malloc still flushes and retries when an allocation runs out of memory.
+size_t defer_cap() {
+    static const size_t cap = [] {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            (void)cudaGetLastError();
+            tot = 0;
+        }
+        return std::max(size_t{16} << 30, tot / 3);
+    }();
+    return cap;
+}
 bool defer_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("ILUG_DEFER_FREE");
@@ -60,9 +74,13 @@ void dev_free(void* p, size_t bytes) {
             std::lock_guard<std::mutex> g(g_defer_mu);
             g_deferred.push_back(p);
             g_deferred_bytes += bytes;
-            if (g_deferred_bytes > kDeferCap) flush.swap(g_deferred), g_deferred_bytes = 0;
+            if (g_deferred_bytes > defer_cap()) flush.swap(g_deferred), g_deferred_bytes = 0;
         }
-        free_all(flush);
+        if (!flush.empty()) {
+            SetupTimer tm("defer");
+            free_all(flush);
+            tm.mark("cap flush");
+        }
         return;
     }
     cudaFree(p);
