@@ -103,3 +103,14 @@ def test_device_ilut_large_bitwise(ilug, torch_cuda):
     A = ilug.Matrix.generate("pressure27(128,128,128)")
     cfg = _ilut_cfg(ilug, 1e-3, 5)
     _same(ilug.ilu_factorize_device(A, cfg), ilug.ilu_factorize(A, cfg))
+
+
+@pytest.mark.parametrize("quota", ["0", "1", "7", "256"])
+def test_device_ilut_row_quota_bitwise(ilug, torch_cuda, monkeypatch, quota):
+    """Warps retiring after `quota` rows (fresh CTAs take the next tickets;
+    0 = persistent grid) give the same factors: the row order is the ticket
+    order either way (kernels/ilut.cu launch_ilut)."""
+    monkeypatch.setenv("ILUG_ILUT_QUOTA", quota)
+    A = ilug.Matrix.generate("pressure27(20,20,20)")
+    cfg = _ilut_cfg(ilug, 1e-3, 5)
+    _same(ilug.ilu_factorize_device(A, cfg), ilug.ilu_factorize(A, cfg))

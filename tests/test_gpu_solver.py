@@ -221,3 +221,22 @@ def test_matrix_market_ingest_solve_matches_reference(ilug, ref, torch_cuda, tmp
     exp = ref.run_solve(want, kv)
     assert got["converged"] == "true"
     assert abs(int(got["iterations"]) - int(exp["iterations"])) <= 1
+
+
+@pytest.mark.parametrize("variant", ["ilu0", "ilut"])
+def test_shared_device_A_setup_identical(ilug, torch_cuda, monkeypatch, variant):
+    """solve_with uploads A once for the factorisation, the device AMG setup
+    and the level-0 operator (ILUG_SHARE_A=0: separate uploads); the level-0
+    operators are then built before the factors finish. Same iterations and
+    the same final residual, bit for bit, either way."""
+    A = ilug.Matrix.generate("pressure27(40,40,40)")
+    kv = {"krylov.tol": "1e-8", "smoother.kind": "ilu", "ilu.variant": variant, "ilu.droptol": "1e-3",
+          "ilu.lfill": "5", "trisolve.m_lower": 5, "trisolve.m_upper": 5, "amg.coarsening": "pmis",
+          "device.amg_setup": "device"}
+    seen = set()
+    for share in ("1", "0", "1"):
+        monkeypatch.setenv("ILUG_SHARE_A", share)
+        rep = ilug.run_solve(A, ilug.Config().update(kv))
+        assert rep["converged"] == "true"
+        seen.add((rep["iterations"], rep["final_relres"]))
+    assert len(seen) == 1, seen
