@@ -77,6 +77,10 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     DevCsr Ad;
     const char* sa = std::getenv("ILUG_SHARE_A"); // =0: separate uploads (A/B)
     const bool share_A = dev_setup && fact0 && !(sa && sa[0] == '0');
+    // the device hierarchy's operators built from the device AMG setup's own
+    // copies of A_k, P_k, R_k (ILUG_KEEP_DEVICE_LEVELS=0: re-uploaded from the host, A/B)
+    const char* kd = std::getenv("ILUG_KEEP_DEVICE_LEVELS");
+    const bool keep_dev = dev_setup && !(kd && kd[0] == '0');
     if (share_A) {
         Ad.upload(A, st);
         ILUG_CUDA(cudaStreamSynchronize(st));
@@ -125,7 +129,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     };
     std::thread builder([&] {
         for (;;) {
-            Item it;
+            Item it{};
             bool done = false;
             {
                 std::unique_lock<std::mutex> g(qm);
@@ -193,7 +197,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
         if (dev_setup) ILUG_CUDA(cudaStreamCreateWithPriority(&sst, cudaStreamNonBlocking, prio_hi));
         StreamGuard sguard{sst};
         auto setup = [&](const LevelReady& cb) {
-            return dev_setup ? amg_setup_device(A, apd, cb, sst, share_A ? &Ad : nullptr) : amg_setup(A, apd, cb);
+            return dev_setup ? amg_setup_device(A, apd, cb, sst, share_A ? &Ad : nullptr, keep_dev) : amg_setup(A, apd, cb);
         };
         oc.hier = setup([&](i64 k, const HostLevel& lev, bool last) {
             {
@@ -209,6 +213,7 @@ SolveOutcome solve_with(const Csr& A, const AmgParams& ap, const KrylovParams& k
     }
     tm.mark("hierarchy");
     close_queue();
+    for (const HostLevel& l : oc.hier.levels) l.dA.reset(), l.dP.reset(), l.dR.reset(); // any the builder left
     tm.mark("device objects");
     if (f0.valid()) pre = f0.get(); // single-level hierarchies: still surface factorisation errors
     (void)have_pre;

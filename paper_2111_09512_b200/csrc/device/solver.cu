@@ -1,5 +1,6 @@
 // Device ILU factors, smoothers and the V-cycle (see solver.hpp).
 #include "solver.hpp"
+#include "../kernels/spgemm.hpp"
 
 #include <cmath>
 #include <cstdio>
@@ -503,12 +504,16 @@ void DeviceHierarchy::build_level(int k, const HostLevel& hl, const SmootherConf
         lv.A.build(hl.A, level0->Arp.p, level0->Aci.p, level0->Av.p, st); // the factorisation's upload
         ILUG_CUDA(cudaStreamSynchronize(st));
         level0->Arp.release(), level0->Aci.release(), level0->Av.release();
+    } else if (hl.dA && hl.A.nnz() > 0) { // the device AMG setup's copy
+        lv.A.build(hl.A, hl.dA->rp.p, hl.dA->ci.p, hl.dA->v.p, st);
     } else {
         lv.A.build(hl.A, st);
     }
     if (!last) {
-        sell_from_host(lv.P, hl.P, Part::all, st);
-        sell_from_host(lv.R, hl.R, Part::all, st);
+        if (hl.dP) sell_from_device(lv.P, hl.dP->nrows, hl.dP->ncols, hl.dP->ci.n, hl.dP->rp.p, hl.dP->ci.p, hl.dP->v.p, st);
+        else sell_from_host(lv.P, hl.P, Part::all, st);
+        if (hl.dR) sell_from_device(lv.R, hl.dR->nrows, hl.dR->ncols, hl.dR->ci.n, hl.dR->rp.p, hl.dR->ci.p, hl.dR->v.p, st);
+        else sell_from_host(lv.R, hl.R, Part::all, st);
         tm.mark("A,P,R", k);
         lv.smoother.build(hl.A, lv.A, sc, st, level0);
         tm.mark("smoother", k);
@@ -517,6 +522,7 @@ void DeviceHierarchy::build_level(int k, const HostLevel& hl, const SmootherConf
     lv.x.alloc(std::max<i64>(lv.n, 1));
     lv.r.alloc(std::max<i64>(lv.n, 1));
     ILUG_CUDA(cudaStreamSynchronize(st));
+    hl.dA.reset(), hl.dP.reset(), hl.dR.reset(); // the SELL copies exist now
 }
 
 void DeviceHierarchy::build_level0_ops(const HostLevel& hl, const i64* rp, const i32* ci, const double* v,
@@ -526,12 +532,15 @@ void DeviceHierarchy::build_level0_ops(const HostLevel& hl, const i64* rp, const
     Lev& lv = levels_.emplace_back();
     lv.n = hl.A.nrows;
     lv.A.build(hl.A, rp, ci, v, st);
-    sell_from_host(lv.P, hl.P, Part::all, st);
-    sell_from_host(lv.R, hl.R, Part::all, st);
+    if (hl.dP) sell_from_device(lv.P, hl.dP->nrows, hl.dP->ncols, hl.dP->ci.n, hl.dP->rp.p, hl.dP->ci.p, hl.dP->v.p, st);
+    else sell_from_host(lv.P, hl.P, Part::all, st);
+    if (hl.dR) sell_from_device(lv.R, hl.dR->nrows, hl.dR->ncols, hl.dR->ci.n, hl.dR->rp.p, hl.dR->ci.p, hl.dR->v.p, st);
+    else sell_from_host(lv.R, hl.R, Part::all, st);
     lv.b.alloc(std::max<i64>(lv.n, 1));
     lv.x.alloc(std::max<i64>(lv.n, 1));
     lv.r.alloc(std::max<i64>(lv.n, 1));
     ILUG_CUDA(cudaStreamSynchronize(st));
+    hl.dA.reset(), hl.dP.reset(), hl.dR.reset();
     tm.mark("A,P,R", 0);
 }
 

@@ -10,6 +10,7 @@
 #include "ilu.hpp"
 
 #include <cstdint>
+#include <memory>
 
 namespace ilug {
 
@@ -68,10 +69,16 @@ struct CfSplit {
     i64 n_coarse = 0;
 };
 
+struct DevCsr; // kernels/spgemm.hpp
+
 struct HostLevel {
     Csr A, P, R;
     CfSplit split;
     i64 mm_ext_fallback_rows = 0;
+    /// Device copies the device AMG setup leaves for the device-hierarchy
+    /// builder when asked (solve_with): it builds its SELL copies from them
+    /// instead of re-uploading A, P, R, then releases them.
+    mutable std::shared_ptr<DevCsr> dA, dP, dR;
 };
 
 /// Dense LU with partial pivoting (first strict maximum wins), row-major.

@@ -698,7 +698,7 @@ DevCsr interp_mm_ext_device(const DevCsr& A, const DevCsr& S, const DevSplit& sp
 bool amg_device_supported(const AmgParams& p) { return p.coarsening == Coarsening::pmis; }
 
 HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st,
-                               const DevCsr* Ad) {
+                               const DevCsr* Ad, bool keep_device) {
     if (A.nrows != A.ncols) fail_invalid("setup: matrix must be square");
     if (!(prm.theta > 0.0 && prm.theta <= 1.0)) fail_invalid("setup: theta must lie in (0, 1]");
     if (prm.coarse_size < 1) fail_invalid("setup: coarse_size must be >= 1");
@@ -709,10 +709,11 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
     h.params = prm;
     h.levels.reserve(static_cast<size_t>(prm.max_levels)); // stable level addresses for on_level
     SetupTimer tm("amg-device");
-    DevCsr own;
-    if (!Ad) own.upload(A, st);
+    auto own = std::make_shared<DevCsr>();
+    if (!Ad) own->upload(A, st);
     tm.mark("upload A");
-    const DevCsr* curp = Ad ? Ad : &own; // level k's operator on the device
+    const DevCsr* curp = Ad ? Ad : own.get(); // level k's operator on the device
+    keep_device = keep_device && on_level;
     for (;;) {
         h.levels.emplace_back();
         HostLevel& lev = h.levels.back();
@@ -738,8 +739,13 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
         const bool ok = spgemm_device(cur.nrows, P.ncols, cur, P, AP, st) &&
                         spgemm_device(R.nrows, P.ncols, R, AP, C, st);
         tm.mark("R*(A*P)", k);
-        lev.P = P.download(st);
-        lev.R = R.download(st);
+        if (!keep_device || !ok) { // the consumer of keep_device builds from the device copies
+            lev.P = P.download(st);
+            lev.R = R.download(st);
+        } else {
+            lev.P.nrows = P.nrows, lev.P.ncols = P.ncols;
+            lev.R.nrows = R.nrows, lev.R.ncols = R.ncols;
+        }
         if (!ok) C.upload(csr_matmul(lev.R, csr_matmul(lev.A, lev.P)), st); // a row too wide for the tables
         lev.split.n_coarse = sp.n_coarse;
         lev.split.is_coarse.resize(static_cast<size_t>(sp.n));
@@ -750,9 +756,14 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
         }
         ILUG_CUDA(cudaStreamSynchronize(st));
         tm.mark("download P,R", k);
+        if (keep_device) {
+            if (curp == own.get()) lev.dA = own;
+            lev.dP = std::make_shared<DevCsr>(std::move(P));
+            lev.dR = std::make_shared<DevCsr>(std::move(R));
+        }
         if (on_level) on_level(k, lev, false);
-        own = std::move(C);
-        curp = &own;
+        own = std::make_shared<DevCsr>(std::move(C));
+        curp = own.get();
     }
     if (on_level) on_level(h.num_levels() - 1, h.levels.back(), true);
     h.coarse = dense_lu_factor(h.levels.back().A);

@@ -38,7 +38,10 @@ bool amg_device_supported(const AmgParams& p);
 /// on_level) as soon as it is final; the result equals amg_setup bit for bit.
 /// Ad: A already on the device (read only; the caller keeps it alive until
 /// on_level(0) has been called), else A is uploaded.
+/// keep_device: each level handed to on_level keeps its device A (k >= 1), P, R
+/// in HostLevel::dA/dP/dR for the consumer to build from and release; the host
+/// P and R then carry only their dimensions (no download).
 HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelReady& on_level, cudaStream_t st,
-                               const DevCsr* Ad = nullptr);
+                               const DevCsr* Ad = nullptr, bool keep_device = false);
 
 } // namespace ilug

@@ -13,6 +13,9 @@ enum class Part { all, strict_lower, strict_upper };
 
 /// Upload a host CSR and pack the selected part into SELL-32 on the device.
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s);
+/// The same SELL (all entries) from a device CSR (nrows x ncols, nnz entries).
+void sell_from_device(Sell& out, i64 nrows, i64 ncols, i64 nnz, const i64* rp, const i32* ci, const double* v,
+                      cudaStream_t s);
 /// SELL-C-sigma sorting window in rows (ILUG_SELL_SIGMA, default 1024; <=1 = unsorted).
 i64 sell_sigma();
 

@@ -1257,6 +1257,8 @@ void sell_refill(Sell& M, const i64* rp, const i32* ci, const double* v, Part pa
 
 namespace {
 void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>* perm_in, cudaStream_t s);
+void sell_device_build(Sell& out, i64 nrows, const i64* rp, const i32* ci, const double* v, int pc, cudaStream_t s,
+                       SetupTimer& tm);
 // rows sorted by decreasing length inside windows of sigma (stable), padded
 // with -1 to whole slices: one group of a split SELL
 void append_group(std::vector<i32>& perm, std::vector<i32>&& g, const Csr& A) {
@@ -1308,7 +1310,51 @@ void sell_from_host_split(Sell& out, const Csr& A, i64 nloc, cudaStream_t s) {
 
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) { sell_host_build(out, A, part, nullptr, s); }
 
+void sell_from_device(Sell& out, i64 nrows, i64 ncols, i64 nnz, const i64* rp, const i32* ci, const double* v,
+                      cudaStream_t s) {
+    if (!device_layout() || nnz == 0) { // the host layout (A/B knob) or nothing to lay out: via a host copy
+        Csr h;
+        h.nrows = nrows;
+        h.ncols = ncols;
+        h.rp.resize(static_cast<size_t>(nrows) + 1);
+        h.ci.resize(static_cast<size_t>(nnz));
+        h.v.resize(static_cast<size_t>(nnz));
+        ILUG_CUDA(cudaMemcpyAsync(h.rp.data(), rp, sizeof(i64) * (nrows + 1), cudaMemcpyDeviceToHost, s));
+        if (nnz > 0) {
+            ILUG_CUDA(cudaMemcpyAsync(h.ci.data(), ci, sizeof(i32) * nnz, cudaMemcpyDeviceToHost, s));
+            ILUG_CUDA(cudaMemcpyAsync(h.v.data(), v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
+        }
+        ILUG_CUDA(cudaStreamSynchronize(s));
+        return sell_from_host(out, h, Part::all, s);
+    }
+    SetupTimer tm("sell-devcsr");
+    out.nrows = nrows;
+    out.ncols = ncols;
+    out.split_slices = -1;
+    sell_device_build(out, nrows, rp, ci, v, 0, s, tm);
+}
+
 namespace {
+// Layout on the GPU from a device CSR (nrows rows; out.nrows/ncols set by the caller).
+void sell_device_build(Sell& out, i64 nrows, const i64* rp, const i32* ci, const double* v, int pc, cudaStream_t s,
+                       SetupTimer& tm) {
+    DBuf<i32> len(std::max<i64>(nrows, 1));
+    if (pc == 0)
+        k_len_rows<<<grid_for(nrows), kBlock, 0, s>>>(nrows, rp, 0, len.p);
+    else
+        k_len_part<<<grid_for(nrows), kBlock, 0, s>>>(nrows, rp, ci, pc, len.p);
+    ILUG_LAUNCH_CHECK();
+    layout_device(out, nrows, len.p, s);
+    out.codes.release(), out.offtab.release();
+    tm.mark("device layout");
+    k_sell_fill<<<grid_for(out.nrows_pad), kBlock, 0, s>>>(out.nrows_pad, out.nrows, out.perm.p, rp, ci, v, pc,
+                                                           out.slice_ptr.p, out.cols.p, out.vals.p);
+    ILUG_LAUNCH_CHECK();
+    sell_encode(out, s);
+    ILUG_CUDA(cudaStreamSynchronize(s)); // the CSR (and temporaries) may die after this
+    tm.mark("fill+encode");
+}
+
 void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>* perm_in, cudaStream_t s) {
     SetupTimer tm("sell-host");
     out.nrows = A.nrows;
@@ -1323,21 +1369,7 @@ void sell_host_build(Sell& out, const Csr& A, Part part, const std::vector<i32>*
         ci.upload(A.ci.data(), A.nnz(), s);
         v.upload(A.v.data(), A.nnz(), s);
         tm.mark("csr upload");
-        DBuf<i32> len(std::max<i64>(A.nrows, 1));
-        if (pc == 0)
-            k_len_rows<<<grid_for(A.nrows), kBlock, 0, s>>>(A.nrows, rp.p, 0, len.p);
-        else
-            k_len_part<<<grid_for(A.nrows), kBlock, 0, s>>>(A.nrows, rp.p, ci.p, pc, len.p);
-        ILUG_LAUNCH_CHECK();
-        layout_device(out, A.nrows, len.p, s);
-        out.codes.release(), out.offtab.release();
-        tm.mark("device layout");
-        k_sell_fill<<<grid_for(out.nrows_pad), kBlock, 0, s>>>(out.nrows_pad, out.nrows, out.perm.p, rp.p, ci.p, v.p,
-                                                               pc, out.slice_ptr.p, out.cols.p, out.vals.p);
-        ILUG_LAUNCH_CHECK();
-        sell_encode(out, s);
-        ILUG_CUDA(cudaStreamSynchronize(s)); // the CSR temporaries die here
-        tm.mark("fill+encode");
+        sell_device_build(out, A.nrows, rp.p, ci.p, v.p, pc, s, tm);
         return;
     }
     const std::vector<i32> perm =
