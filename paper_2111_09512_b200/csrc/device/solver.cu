@@ -246,6 +246,42 @@ Csr DeviceIlu::scaled_upper_host() const {
 // ============================================================ DeviceSmoother
 namespace {
 
+// 1/a_ii per row from a device CSR: the first entry with column i, 0.0 when
+// absent (csr_diag); the lowest zero row fails like inverted_diag below.
+__global__ void k_inv_diag(i64 n, const i64* __restrict__ rp, const i32* __restrict__ ci,
+                           const double* __restrict__ v, double* __restrict__ invd,
+                           unsigned long long* __restrict__ first_zero) {
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<i64>(gridDim.x) * blockDim.x) {
+        double d = 0.0;
+        for (i64 k = rp[i]; k < rp[i + 1]; ++k)
+            if (ci[k] == i) {
+                d = v[k];
+                break;
+            }
+        if (d == 0.0) atomicMin(first_zero, static_cast<unsigned long long>(i));
+        invd[i] = 1.0 / d;
+    }
+}
+
+void inverted_diag_device(const DevCsr& M, DBuf<double>& invd, const char* what, cudaStream_t st) {
+    const i64 n = M.nrows;
+    invd.alloc(std::max<i64>(n, 1));
+    DBuf<unsigned long long> fz(1);
+    const unsigned long long none = ~0ull;
+    ILUG_CUDA(cudaMemcpyAsync(fz.p, &none, sizeof none, cudaMemcpyHostToDevice, st));
+    if (n > 0) {
+        k_inv_diag<<<static_cast<unsigned>(std::min<i64>((n + 255) / 256, 148 * 32)), 256, 0, st>>>(
+            n, M.rp.p, M.ci.p, M.v.p, invd.p, fz.p);
+        ILUG_LAUNCH_CHECK();
+    }
+    unsigned long long z = 0;
+    ILUG_CUDA(cudaStreamSynchronize(st)); // not inside the pageable copy (kernels/ilut.cu)
+    ILUG_CUDA(cudaMemcpyAsync(&z, fz.p, sizeof z, cudaMemcpyDeviceToHost, st));
+    ILUG_CUDA(cudaStreamSynchronize(st));
+    if (z != ~0ull) fail_numeric(std::string(what) + ": zero diagonal at row " + std::to_string(z));
+}
+
 Vec inverted_diag(const Csr& A, const char* what) {
     Vec d = csr_diag(A);
     for (i64 i = 0; i < A.nrows; ++i) {
@@ -258,7 +294,7 @@ Vec inverted_diag(const Csr& A, const char* what) {
 } // namespace
 
 void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg,
-                           cudaStream_t st, DevFactors* pre, const HaloPlan* dist) {
+                           cudaStream_t st, DevFactors* pre, const HaloPlan* dist, const DevCsr* dcsr) {
     if (cfg.sweeps < 0) fail_invalid("build_smoother_state: sweeps must be >= 0");
     if (cfg.poly_degree < 0) fail_invalid("build_smoother_state: poly_degree must be >= 0");
     cfg_ = cfg;
@@ -295,6 +331,12 @@ void DeviceSmoother::build(const Csr& A, const DeviceMatrix& dA, const SmootherC
         break;
     }
     case SmootherKind::poly_gs: {
+        if (dcsr && !dist && dcsr->nrows == n_) { // from the device copy: no second upload of A
+            inverted_diag_device(*dcsr, invd_, "poly_gs", st);
+            sell_from_device(Lstrict_, dcsr->nrows, dcsr->ncols, dcsr->ci.n, dcsr->rp.p, dcsr->ci.p, dcsr->v.p, st,
+                             Part::strict_lower);
+            break;
+        }
         const Vec d = inverted_diag(A, "poly_gs");
         invd_.upload(d.data(), n_, st);
         sell_from_host(Lstrict_, A, Part::strict_lower, st);
@@ -515,7 +557,7 @@ void DeviceHierarchy::build_level(int k, const HostLevel& hl, const SmootherConf
         if (hl.dR) sell_from_device(lv.R, hl.dR->nrows, hl.dR->ncols, hl.dR->ci.n, hl.dR->rp.p, hl.dR->ci.p, hl.dR->v.p, st);
         else sell_from_host(lv.R, hl.R, Part::all, st);
         tm.mark("A,P,R", k);
-        lv.smoother.build(hl.A, lv.A, sc, st, level0);
+        lv.smoother.build(hl.A, lv.A, sc, st, level0, nullptr, hl.dA.get());
         tm.mark("smoother", k);
     }
     lv.b.alloc(std::max<i64>(lv.n, 1));

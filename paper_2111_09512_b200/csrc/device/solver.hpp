@@ -23,6 +23,8 @@
 
 namespace ilug {
 
+struct DevCsr; // kernels/spgemm.hpp
+
 class Transport;
 
 /// Device side of a HaloPlan (host/dist.hpp): packs the rows other ranks need
@@ -188,8 +190,10 @@ public:
     /// `dist`: dA holds a rank's rows of a distributed operator (dA.halo set) —
     /// A is then the plan's diagonal block and the smoother is its rank-local
     /// form (block-Jacobi ILU / poly-GS, hybrid GS, global Jacobi / l1).
+    /// `dcsr`: a device copy of A (the device AMG setup's), used where a
+    /// smoother would otherwise re-upload A (poly-GS: diagonal and strict lower part).
     void build(const Csr& A, const DeviceMatrix& dA, const SmootherConfig& cfg, cudaStream_t st,
-               DevFactors* pre = nullptr, const HaloPlan* dist = nullptr);
+               DevFactors* pre = nullptr, const HaloPlan* dist = nullptr, const DevCsr* dcsr = nullptr);
     /// x <- smooth(A, b, x). `x_zero`: caller guarantees x == 0 on entry, so the
     /// first residual is b itself (bitwise what the SpMV would give).
     void smooth(const double* b, double* x, bool x_zero, cudaStream_t st) const;

@@ -15,7 +15,7 @@ enum class Part { all, strict_lower, strict_upper };
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s);
 /// The same SELL (all entries) from a device CSR (nrows x ncols, nnz entries).
 void sell_from_device(Sell& out, i64 nrows, i64 ncols, i64 nnz, const i64* rp, const i32* ci, const double* v,
-                      cudaStream_t s);
+                      cudaStream_t s, Part part = Part::all);
 /// SELL-C-sigma sorting window in rows (ILUG_SELL_SIGMA, default 1024; <=1 = unsorted).
 i64 sell_sigma();
 

@@ -1311,7 +1311,7 @@ void sell_from_host_split(Sell& out, const Csr& A, i64 nloc, cudaStream_t s) {
 void sell_from_host(Sell& out, const Csr& A, Part part, cudaStream_t s) { sell_host_build(out, A, part, nullptr, s); }
 
 void sell_from_device(Sell& out, i64 nrows, i64 ncols, i64 nnz, const i64* rp, const i32* ci, const double* v,
-                      cudaStream_t s) {
+                      cudaStream_t s, Part part) {
     if (!device_layout() || nnz == 0) { // the host layout (A/B knob) or nothing to lay out: via a host copy
         Csr h;
         h.nrows = nrows;
@@ -1325,13 +1325,13 @@ void sell_from_device(Sell& out, i64 nrows, i64 ncols, i64 nnz, const i64* rp, c
             ILUG_CUDA(cudaMemcpyAsync(h.v.data(), v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
         }
         ILUG_CUDA(cudaStreamSynchronize(s));
-        return sell_from_host(out, h, Part::all, s);
+        return sell_from_host(out, h, part, s);
     }
     SetupTimer tm("sell-devcsr");
     out.nrows = nrows;
     out.ncols = ncols;
     out.split_slices = -1;
-    sell_device_build(out, nrows, rp, ci, v, 0, s, tm);
+    sell_device_build(out, nrows, rp, ci, v, part == Part::all ? 0 : (part == Part::strict_lower ? 1 : 2), s, tm);
 }
 
 namespace {
