@@ -124,15 +124,60 @@ __global__ void k_ilut_vf_fill(i64 ucap, i64 n, i32* __restrict__ uci, double* _
     }
 }
 
+// A lane group of G lanes (G = 32: the warp; G = 16: each half-warp works
+// on its own row): group-relative shuffles, ballots, masks and sync.
+template <int G>
+struct Grp {
+    unsigned mask;
+    int lane, shift;
+    __device__ __forceinline__ Grp() {
+        const int l = static_cast<int>(threadIdx.x & 31);
+        lane = l & (G - 1);
+        shift = l & ~(G - 1);
+        mask = G == 32 ? 0xffffffffu : (((1u << (G & 31)) - 1u) << shift);
+    }
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        const unsigned b = __ballot_sync(mask, p);
+        return G == 32 ? b : (b >> shift) & ((1u << (G & 31)) - 1u);
+    }
+    template <class T>
+    __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, G); }
+    __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p); }
+    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+    __device__ __forceinline__ unsigned lt() const { return (1u << lane) - 1u; } // lanes below, group-relative
+    __device__ __forceinline__ int sum(int x) const {
+        for (int o = G / 2; o; o >>= 1) x += __shfl_xor_sync(mask, x, o, G);
+        return x;
+    }
+};
+// the whole warp: every mask a constant, lanemask_lt from the special register
+template <>
+struct Grp<32> {
+    static constexpr unsigned mask = 0xffffffffu;
+    int lane;
+    __device__ __forceinline__ Grp() : lane(static_cast<int>(threadIdx.x & 31)) {}
+    __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(mask, p); }
+    template <class T>
+    __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src); }
+    __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p); }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    __device__ __forceinline__ unsigned lt() const { return lanemask_lt(); }
+    __device__ __forceinline__ int sum(int x) const {
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(mask, x, o);
+        return x;
+    }
+};
+
 // Rank fill candidates in [beg, end) that carry `want` and not kOrig: keep the
 // lfill best by (|w| desc, column asc) (the reference's nth_element comparator,
 // src/ilu.cpp:206-211). Pattern candidates are always kept. Marks kSel.
+template <int G>
 __device__ __forceinline__ void select_part(const i32* scol, const double* sval, unsigned char* sflag, int beg,
                                             int end, unsigned char want, bool upper, double tau, i64 lfill,
-                                            int lane, bool wrank) {
+                                            const Grp<G>& gr, bool wrank) {
     // pass 1: which candidates pass (U part: the threshold), count fill
     int nfill = 0;
-    for (int q = beg + lane; q < end; q += 32) {
+    for (int q = beg + gr.lane; q < end; q += G) {
         unsigned char f = sflag[q];
         bool pass = (f & want) && !(upper && fabs(sval[q]) < tau);
         if (pass) {
@@ -143,10 +188,10 @@ __device__ __forceinline__ void select_part(const i32* scol, const double* sval,
         }
         sflag[q] = f;
     }
-    for (int o = 16; o; o >>= 1) nfill += __shfl_xor_sync(0xffffffffu, nfill, o);
-    __syncwarp();
+    nfill = gr.sum(nfill);
+    gr.sync();
     if (nfill <= lfill) return;
-    if (wrank && nfill <= 32) {
+    if (wrank && nfill <= G) {
         // pass 2 in registers: the fill candidates compacted into lanes
         // 0..nfill-1 (ballot + nth-set-bit shuffles), each lane ranks its
         // candidate against the others by shuffles — the same comparator, so
@@ -156,8 +201,8 @@ __device__ __forceinline__ void select_part(const i32* scol, const double* sval,
         double myv = 0.0;
         i32 myc = 0;
         int myq = -1, base = 0;
-        for (int q0 = beg; q0 < end; q0 += 32) {
-            const int q = q0 + lane;
+        for (int q0 = beg; q0 < end; q0 += G) {
+            const int q = q0 + gr.lane;
             bool cand = false;
             double v = 0.0;
             i32 c = 0;
@@ -167,28 +212,28 @@ __device__ __forceinline__ void select_part(const i32* scol, const double* sval,
                 v = fabs(sval[q]);
                 c = scol[q];
             }
-            const unsigned bm = __ballot_sync(0xffffffffu, cand);
+            const unsigned bm = gr.ballot(cand);
             const int cnt = __popc(bm);
-            const int k = lane - base; // this lane takes the chunk's k-th candidate
+            const int k = gr.lane - base; // this lane takes the chunk's k-th candidate
             const int src = (k >= 0 && k < cnt) ? static_cast<int>(__fns(bm, 0, k + 1)) : 0;
-            const double sv = __shfl_sync(0xffffffffu, v, src);
-            const i32 sc = __shfl_sync(0xffffffffu, c, src);
+            const double sv = gr.shfl(v, src);
+            const i32 sc = gr.shfl(c, src);
             if (k >= 0 && k < cnt) myv = sv, myc = sc, myq = q0 + src;
             base += cnt;
         }
         i64 rank = 0;
         for (int r = 0; r < nfill; ++r) {
-            const double vr = __shfl_sync(0xffffffffu, myv, r);
-            const i32 cr = __shfl_sync(0xffffffffu, myc, r);
-            if (r != lane) rank += (vr != myv) ? (vr > myv) : (cr < myc);
+            const double vr = gr.shfl(myv, r);
+            const i32 cr = gr.shfl(myc, r);
+            if (r != gr.lane) rank += (vr != myv) ? (vr > myv) : (cr < myc);
         }
         if (myq >= 0 && rank >= lfill) sflag[myq] = static_cast<unsigned char>(sflag[myq] & ~kSel);
-        __syncwarp();
+        gr.sync();
         return;
     }
     // pass 2: rank each fill candidate against all others; losers get kDrop
     // (the ranking reads only kSel/kOrig, so marking while others rank is safe)
-    for (int q = beg + lane; q < end; q += 32) {
+    for (int q = beg + gr.lane; q < end; q += G) {
         const unsigned char f = sflag[q];
         if (!(f & kSel) || (f & kOrig)) continue;
         const double vq = fabs(sval[q]);
@@ -202,25 +247,25 @@ __device__ __forceinline__ void select_part(const i32* scol, const double* sval,
         }
         if (rank >= lfill) sflag[q] = f | kDrop;
     }
-    __syncwarp();
-    for (int q = beg + lane; q < end; q += 32) {
+    gr.sync();
+    for (int q = beg + gr.lane; q < end; q += G) {
         const unsigned char f = sflag[q];
         if (f & kDrop) sflag[q] = static_cast<unsigned char>(f & ~(kSel | kDrop));
     }
-    __syncwarp();
+    gr.sync();
 }
 
 // Write the kSel entries of [beg, end) (ascending columns) to out_c/out_v; returns the count.
-template <bool VF = false>
+template <bool VF, int G>
 __device__ __forceinline__ int emit(const i32* scol, const double* sval, const unsigned char* sflag, int beg,
-                                    int end, i32* out_c, double* out_v, int lane) {
+                                    int end, i32* out_c, double* out_v, const Grp<G>& gr) {
     int base = 0;
-    for (int q0 = beg; q0 < end; q0 += 32) {
-        const int q = q0 + lane;
+    for (int q0 = beg; q0 < end; q0 += G) {
+        const int q = q0 + gr.lane;
         const bool s = q < end && (sflag[q] & kSel);
-        const unsigned b = __ballot_sync(0xffffffffu, s);
+        const unsigned b = gr.ballot(s);
         if (s) {
-            const int o = base + __popc(b & lanemask_lt());
+            const int o = base + __popc(b & gr.lt());
             if (VF) {
                 str_s32(out_c + o, scol[q]);
                 str_f64(out_v + o, sval[q]);
@@ -234,37 +279,39 @@ __device__ __forceinline__ int emit(const i32* scol, const double* sval, const u
     return base;
 }
 
-template <int CAP, int WARPS, bool VF>
+template <int CAP, int WARPS, bool VF, int G>
 __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
     extern __shared__ double smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // [WARPS*CAP values][WARPS*CAP columns][WARPS*32 merge positions][WARPS*CAP flags]
-    i32* const col_base = reinterpret_cast<i32*>(smem + static_cast<size_t>(WARPS) * CAP);
-    double* const sval = smem + static_cast<size_t>(warp) * CAP;
-    i32* const scol = col_base + static_cast<size_t>(warp) * CAP;
-    i32* const snew = col_base + static_cast<size_t>(WARPS) * CAP + warp * 32;
-    unsigned char* const sflag = reinterpret_cast<unsigned char*>(col_base + static_cast<size_t>(WARPS) * CAP +
-                                                                  WARPS * 32) + static_cast<size_t>(warp) * CAP;
+    // NS row slots per CTA: one per lane group (G = 32: per warp)
+    constexpr int NS = WARPS * (32 / G);
+    const Grp<G> gr;
+    const int slot = static_cast<int>(threadIdx.x) / G, lane = gr.lane;
+    // [NS*CAP values][NS*CAP columns][NS*G merge positions][NS*CAP flags]
+    i32* const col_base = reinterpret_cast<i32*>(smem + static_cast<size_t>(NS) * CAP);
+    double* const sval = smem + static_cast<size_t>(slot) * CAP;
+    i32* const scol = col_base + static_cast<size_t>(slot) * CAP;
+    i32* const snew = col_base + static_cast<size_t>(NS) * CAP + slot * G;
+    unsigned char* const sflag = reinterpret_cast<unsigned char*>(col_base + static_cast<size_t>(NS) * CAP +
+                                                                  NS * G) + static_cast<size_t>(slot) * CAP;
     const unsigned E = *a.epoch;
-    const unsigned full = 0xffffffffu;
 
     for (int q = a.quota; q > 0; --q) {
         unsigned long long t = 0;
         if (lane == 0) t = atomicAdd(a.ticket, 1ull);
-        const i64 i = static_cast<i64>(__shfl_sync(full, t, 0));
+        const i64 i = static_cast<i64>(gr.shfl(t, 0));
         if (i >= a.n) return;
         cuda::atomic_ref<unsigned, cuda::thread_scope_device> fi(a.done[i]);
         const i64 beg = a.rp[i];
         const int alen = static_cast<int>(a.rp[i + 1] - beg);
         unsigned ov = 0;
         if (lane == 0) ov = *reinterpret_cast<volatile unsigned*>(a.err + 1);
-        bool bad = __shfl_sync(full, ov, 0) != 0u;
+        bool bad = gr.shfl(ov, 0) != 0u;
         if (!bad && alen > CAP) {
             if (lane == 0) atomicMax(a.err + 1, static_cast<unsigned>(alen));
             bad = true;
         }
         if (bad) { // capacity exceeded somewhere: publish and let the host relaunch
-            __syncwarp();
+            gr.sync();
             if (lane == 0) {
                 if (VF) { // a valid (meaningless) one-entry row: consumers must not wait
                     const i64 uo = a.uoff[i];
@@ -277,14 +324,14 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
             }
             continue;
         }
-        for (int q = lane; q < alen; q += 32) {
+        for (int q = lane; q < alen; q += G) {
             scol[q] = a.ci[beg + q];
             sval[q] = a.av[beg + q];
             sflag[q] = kLive | kOrig;
         }
         int len = alen;
         const double tau = a.tau[i];
-        __syncwarp();
+        gr.sync();
 
         int p = 0;
         for (; p < len && !bad; ++p) {
@@ -308,7 +355,7 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                     const unsigned long long vb = in_slot ? ldr_u64(a.uv + ub + 1 + lane) : 0ull;
                     const bool need = lane + 1 < ul;
                     const bool ok = ul > 0 && pb != kUSentinel && (!need || (jj >= 0 && vb != kUSentinel));
-                    if (__all_sync(full, ok)) {
+                    if (gr.all(ok)) {
                         ukk = __longlong_as_double(static_cast<long long>(pb));
                         j0 = jj;
                         u0 = __longlong_as_double(static_cast<long long>(vb));
@@ -329,14 +376,14 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                 u0 = in_slot ? a.uv[ub + 1 + lane] : 0.0;
             }
             const double m = sval[p] / ukk;
-            __syncwarp();
+            gr.sync();
             if (fabs(m) < tau) { // dual-threshold drop of the multiplier
                 if (lane == 0) sval[p] = 0.0, sflag[p] = 0;
-                __syncwarp();
+                gr.sync();
                 continue;
             }
             if (lane == 0) sval[p] = m, sflag[p] = kLive | kKept | (sflag[p] & kOrig);
-            for (int c = 1; c < ul; c += 32) {
+            for (int c = 1; c < ul; c += G) {
                 const int kk = c + lane;
                 const bool act = kk < ul;
                 i32 j = !act ? INT_MAX : (c == 1 ? j0 : a.uci[ub + kk]);
@@ -361,9 +408,9 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                 const bool found = act && lo < len && scol[lo] == j;
                 const double prod = m * u;
                 if (found) sval[lo] = sval[lo] - prod;
-                const unsigned nm = __ballot_sync(full, act && !found);
+                const unsigned nm = gr.ballot(act && !found);
                 if (nm == 0u) {
-                    __syncwarp();
+                    gr.sync();
                     continue;
                 }
                 const int nnew = __popc(nm);
@@ -372,13 +419,13 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                     bad = true;
                     break;
                 }
-                const int rank = __popc(nm & lanemask_lt());
+                const int rank = __popc(nm & gr.lt());
                 if (act && !found) snew[rank] = lo;
-                __syncwarp();
+                gr.sync();
                 const int minpos = snew[0];
                 // shift the tail [minpos, len) up by the number of new entries before
                 // each element, from the back (destinations never reach unread slots)
-                for (int top = len; top > minpos; top -= 32) {
+                for (int top = len; top > minpos; top -= G) {
                     const int q = top - 1 - lane;
                     const bool mv = q >= minpos;
                     i32 cc = 0;
@@ -395,9 +442,9 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                         }
                         dst = q + l2;
                     }
-                    __syncwarp();
+                    gr.sync();
                     if (mv) scol[dst] = cc, sval[dst] = vv, sflag[dst] = ff;
-                    __syncwarp();
+                    gr.sync();
                 }
                 if (act && !found) {
                     const int dst = lo + rank;
@@ -406,11 +453,11 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                     sflag[dst] = kLive;
                 }
                 len += nnew;
-                __syncwarp();
+                gr.sync();
             }
         }
         if (bad) {
-            __syncwarp();
+            gr.sync();
             if (lane == 0) {
                 if (VF) {
                     const i64 uo = a.uoff[i];
@@ -438,9 +485,9 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
             }
         }
         const int ub = p + (hasd ? 1 : 0);
-        select_part(scol, sval, sflag, ub, len, kLive, true, tau, a.lfill, lane, a.wrank != 0);
+        select_part<G>(scol, sval, sflag, ub, len, kLive, true, tau, a.lfill, gr, a.wrank != 0);
         const i64 uo = a.uoff[i];
-        const int nu = emit<VF>(scol, sval, sflag, ub, len, a.uci + uo + 1, a.uv + uo + 1, lane);
+        const int nu = emit<VF, G>(scol, sval, sflag, ub, len, a.uci + uo + 1, a.uv + uo + 1, gr);
         if (VF) {
             if (lane == 0) {
                 str_s32(a.uci + uo, static_cast<i32>(i));
@@ -453,15 +500,15 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                 a.uv[uo] = d;
                 a.ulen[i] = nu + 1;
             }
-            __syncwarp(); // orders every lane's row writes before lane 0's release (cumulative)
+            gr.sync(); // orders every lane's row writes before lane 0's release (cumulative)
             if (lane == 0) fi.store(E, cuda::memory_order_release);
         }
 
-        select_part(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, lane, a.wrank != 0);
+        select_part<G>(scol, sval, sflag, 0, p, kKept, false, tau, a.lfill, gr, a.wrank != 0);
         const i64 lo = a.loff[i];
-        const int nl = emit(scol, sval, sflag, 0, p, a.lci + lo, a.lv + lo, lane);
+        const int nl = emit<false, G>(scol, sval, sflag, 0, p, a.lci + lo, a.lv + lo, gr);
         if (lane == 0) a.llen[i] = nl;
-        __syncwarp();
+        gr.sync();
     }
 }
 
@@ -540,22 +587,30 @@ int ilut_quota() {
     return q > 0 ? q : INT_MAX;
 }
 
+// ILUG_ILUT_HALF=1: two rows per warp, one per 16-lane half (twice the rows
+// in flight; working rows up to 160 entries before the capacity relaunch)
+bool ilut_half() {
+    const char* e = std::getenv("ILUG_ILUT_HALF");
+    return e && e[0] == '1';
+}
+
 bool ilut_value_flags() {
     const char* e = std::getenv("ILUG_ILUT_VF");
     return e && e[0] == '1';
 }
 
-template <int CAP, int WARPS>
+template <int CAP, int WARPS, int G = 32>
 void launch_ilut(const IlutArgs& a, i64 ucap, cudaStream_t st) {
-    constexpr size_t smem = static_cast<size_t>(WARPS) * CAP * (sizeof(double) + sizeof(i32) + 1) +
-                            static_cast<size_t>(WARPS) * 32 * sizeof(i32);
+    constexpr int NS = WARPS * (32 / G); // rows in flight per CTA
+    constexpr size_t smem = static_cast<size_t>(NS) * CAP * (sizeof(double) + sizeof(i32) + 1) +
+                            static_cast<size_t>(NS) * G * sizeof(i32);
     const bool vf = ilut_value_flags();
     if (vf) {
         k_ilut_vf_fill<<<static_cast<unsigned>(std::min<i64>((ucap + 255) / 256, 148 * 64)), 256, 0, st>>>(
             ucap, a.n, a.uci, a.uv, a.ulen);
         ILUG_LAUNCH_CHECK();
     }
-    auto* fn = vf ? k_ilut<CAP, WARPS, true> : k_ilut<CAP, WARPS, false>;
+    auto* fn = vf ? k_ilut<CAP, WARPS, true, G> : k_ilut<CAP, WARPS, false, G>;
     ILUG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     ILUG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, smem));
@@ -570,8 +625,8 @@ void launch_ilut(const IlutArgs& a, i64 ucap, cudaStream_t st) {
     // higher-priority streams) take the slots retiring CTAs free instead of
     // waiting for the whole factorisation. Safe: a warp claims its ticket when
     // it starts, so it only waits on rows claimed by running or finished warps.
-    const i64 resident = std::min<i64>(static_cast<i64>(per_sm) * sms, (a.n + WARPS - 1) / WARPS);
-    const i64 cover = (a.n + static_cast<i64>(WARPS) * a.quota - 1) / (static_cast<i64>(WARPS) * a.quota);
+    const i64 resident = std::min<i64>(static_cast<i64>(per_sm) * sms, (a.n + NS - 1) / NS);
+    const i64 cover = (a.n + static_cast<i64>(NS) * a.quota - 1) / (static_cast<i64>(NS) * a.quota);
     const i64 grid = std::min<i64>(std::max(resident, cover + resident), INT_MAX);
     fn<<<static_cast<unsigned>(std::max<i64>(grid, 1)), WARPS * 32, smem, st>>>(a);
     ILUG_LAUNCH_CHECK();
@@ -639,7 +694,9 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
             ILUG_CUDA(cudaMemcpyAsync(ctl.p, init, sizeof init, cudaMemcpyHostToDevice, st));
             k_ilut_bump<<<1, 1, 0, st>>>(sync.p + n, ctl.p, sync.p + n + 1);
             ILUG_LAUNCH_CHECK();
-            if (cap_level == 0)
+            if (cap_level == 0 && ilut_half())
+                launch_ilut<160, 8, 16>(a, ucap, st);
+            else if (cap_level == 0)
                 launch_ilut<256, 8>(a, ucap, st);
             else if (cap_level == 1)
                 launch_ilut<1024, 4>(a, ucap, st);

@@ -114,3 +114,14 @@ def test_device_ilut_row_quota_bitwise(ilug, torch_cuda, monkeypatch, quota):
     A = ilug.Matrix.generate("pressure27(20,20,20)")
     cfg = _ilut_cfg(ilug, 1e-3, 5)
     _same(ilug.ilu_factorize_device(A, cfg), ilug.ilu_factorize(A, cfg))
+
+
+@pytest.mark.parametrize("spec", ["pressure27(20,20,20)", "cutcell(14,14,14)", "stencil27(9,7,5)"])
+@pytest.mark.parametrize("droptol,lfill", [(1e-3, 5), (0.0, 40)])
+def test_device_ilut_half_warp_rows_bitwise(ilug, torch_cuda, monkeypatch, spec, droptol, lfill):
+    """ILUG_ILUT_HALF=1: two rows per warp, one per 16-lane half, 160-entry
+    working rows (wider ones take the capacity relaunch): identical factors."""
+    monkeypatch.setenv("ILUG_ILUT_HALF", "1")
+    A = ilug.Matrix.generate(spec)
+    cfg = _ilut_cfg(ilug, droptol, lfill)
+    _same(ilug.ilu_factorize_device(A, cfg), ilug.ilu_factorize(A, cfg))
