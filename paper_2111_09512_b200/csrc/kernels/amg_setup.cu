@@ -26,6 +26,8 @@
 
 #include <cub/cub.cuh>
 
+#include <future>
+
 namespace ilug {
 
 namespace {
@@ -714,20 +716,27 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
     tm.mark("upload A");
     const DevCsr* curp = Ad ? Ad : own.get(); // level k's operator on the device
     keep_device = keep_device && on_level;
+    // level 0's host copy of A (GBs) overlaps the level's GPU work; joined
+    // before anything reads it
+    std::future<Csr> a0 = std::async(std::launch::async, [&A] { return csr_copy(A); });
+    auto join_a0 = [&] {
+        if (a0.valid()) h.levels.front().A = a0.get();
+    };
     for (;;) {
         h.levels.emplace_back();
         HostLevel& lev = h.levels.back();
         const i64 k = h.num_levels() - 1;
-        lev.A = k == 0 ? csr_copy(A) : curp->download(st);
+        if (k > 0) lev.A = curp->download(st);
         tm.mark("host A", k);
-        if (lev.A.nrows <= prm.coarse_size || k + 1 >= prm.max_levels) break;
+        const i64 nk = k == 0 ? A.nrows : lev.A.nrows;
+        if (nk <= prm.coarse_size || k + 1 >= prm.max_levels) break;
         const DevCsr& cur = *curp;
         DevCsr S = strength_device(cur, prm.theta, st);
         DevCsr St = transpose_device(S, false, st);
         tm.mark("strength", k);
         DevSplit sp = pmis_device(S, St, prm.pmis_seed, st);
         tm.mark("pmis", k);
-        if (static_cast<double>(sp.n_coarse) > 0.95 * static_cast<double>(lev.A.nrows)) break;
+        if (static_cast<double>(sp.n_coarse) > 0.95 * static_cast<double>(nk)) break;
         St = DevCsr{};
         DevCsr P = prm.interpolation == Interpolation::mm_ext
                        ? interp_mm_ext_device(cur, S, sp, &lev.mm_ext_fallback_rows, st)
@@ -746,11 +755,16 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
             lev.P.nrows = P.nrows, lev.P.ncols = P.ncols;
             lev.R.nrows = R.nrows, lev.R.ncols = R.ncols;
         }
-        if (!ok) C.upload(csr_matmul(lev.R, csr_matmul(lev.A, lev.P)), st); // a row too wide for the tables
+        if (!ok) { // a row too wide for the tables
+            join_a0();
+            C.upload(csr_matmul(lev.R, csr_matmul(lev.A, lev.P)), st);
+        }
         lev.split.n_coarse = sp.n_coarse;
-        lev.split.is_coarse.resize(static_cast<size_t>(sp.n));
-        lev.split.coarse_index.resize(static_cast<size_t>(sp.n));
-        if (sp.n > 0) {
+        if (!keep_device) { // (the device-hierarchy consumer never reads the C/F split)
+            lev.split.is_coarse.resize(static_cast<size_t>(sp.n));
+            lev.split.coarse_index.resize(static_cast<size_t>(sp.n));
+        }
+        if (sp.n > 0 && !keep_device) {
             sp.is_coarse.download(lev.split.is_coarse.data(), st);
             sp.coarse_index.download(lev.split.coarse_index.data(), st);
         }
@@ -761,10 +775,12 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
             lev.dP = std::make_shared<DevCsr>(std::move(P));
             lev.dR = std::make_shared<DevCsr>(std::move(R));
         }
+        join_a0();
         if (on_level) on_level(k, lev, false);
         own = std::make_shared<DevCsr>(std::move(C));
         curp = own.get();
     }
+    join_a0();
     if (on_level) on_level(h.num_levels() - 1, h.levels.back(), true);
     h.coarse = dense_lu_factor(h.levels.back().A);
     return h;
