@@ -66,6 +66,7 @@ struct IlutArgs {
     int wrank;           // fill ranking in registers when <= 32 candidates (ILUG_ILUT_WRANK)
     unsigned backoff_ns; // longest poll back-off (ILUG_ILUT_BACKOFF)
     int quota;           // rows a warp takes before its CTA may retire (ILUG_ILUT_QUOTA)
+    int chunk;           // consecutive rows per ticket (ILUG_ILUT_CHUNK)
 };
 
 // Dependency wait with exponential back-off (32 ns doubling up to max_ns):
@@ -295,11 +296,21 @@ __global__ void __launch_bounds__(WARPS * 32, 48 / WARPS) k_ilut(IlutArgs a) {
                                                                   NS * G) + static_cast<size_t>(slot) * CAP;
     const unsigned E = *a.epoch;
 
-    for (int q = a.quota; q > 0; --q) {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(a.ticket, 1ull);
-        const i64 i = static_cast<i64>(gr.shfl(t, 0));
-        if (i >= a.n) return;
+    // Rows are claimed in chunks of a.chunk consecutive rows: a line of the
+    // grid then advances inside one warp (row i's dependency on row i-1 is its
+    // own last row, no cross-SM flag round trip) and the claimed-but-waiting
+    // window covers a.chunk times more lines. A started chunk is always
+    // finished (its rows are claimed), whatever the quota says.
+    i64 next = 0, cend = 0;
+    for (int q = a.quota; q > 0 || next < cend; --q) {
+        if (next >= cend) {
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(a.ticket, static_cast<unsigned long long>(a.chunk));
+            next = static_cast<i64>(gr.shfl(t, 0));
+            if (next >= a.n) return;
+            cend = next + a.chunk < a.n ? next + a.chunk : a.n;
+        }
+        const i64 i = next++;
         cuda::atomic_ref<unsigned, cuda::thread_scope_device> fi(a.done[i]);
         const i64 beg = a.rp[i];
         const int alen = static_cast<int>(a.rp[i + 1] - beg);
@@ -580,6 +591,13 @@ bool ilut_wrank() {
     return !(e && e[0] == '0');
 }
 
+// ILUG_ILUT_CHUNK=<rows>: consecutive rows a warp claims per ticket
+int ilut_chunk() {
+    const char* e = std::getenv("ILUG_ILUT_CHUNK");
+    const int c = e ? std::atoi(e) : 1;
+    return c > 0 ? c : 1;
+}
+
 // ILUG_ILUT_QUOTA=<rows>: rows per warp before its CTA retires (0: persistent)
 int ilut_quota() {
     const char* e = std::getenv("ILUG_ILUT_QUOTA");
@@ -686,7 +704,7 @@ DevFactors ilut_resident(const Csr& A, const IluParams& p, cudaStream_t st, bool
     ILUG_CUDA(cudaMemsetAsync(sync.p, 0, static_cast<size_t>(n + 3) * sizeof(unsigned), st));
     IlutArgs a{n,       rpp,    cip,    avp,    tau.p,   p.lfill, anorm_f, 0,
                p.droptol, uoff.p, loff.p, uci.p, uv.p, ulen.p, lci.p, lv.p, llen.p, sync.p, sync.p + n,
-               ctl.p,   ctl.p + 1, sync.p + n + 1, ilut_wrank() ? 1 : 0, ilut_backoff_ns(), ilut_quota()};
+               ctl.p,   ctl.p + 1, sync.p + n + 1, ilut_wrank() ? 1 : 0, ilut_backoff_ns(), ilut_quota(), ilut_chunk()};
     unsigned err[2] = {0, 0};
     for (int pass = 0; pass < 2; ++pass) {
         for (int cap_level = 0;; ++cap_level) {

@@ -125,3 +125,14 @@ def test_device_ilut_half_warp_rows_bitwise(ilug, torch_cuda, monkeypatch, spec,
     A = ilug.Matrix.generate(spec)
     cfg = _ilut_cfg(ilug, droptol, lfill)
     _same(ilug.ilu_factorize_device(A, cfg), ilug.ilu_factorize(A, cfg))
+
+
+@pytest.mark.parametrize("chunk", ["2", "5"])
+def test_device_ilut_chunked_tickets_bitwise(ilug, torch_cuda, monkeypatch, chunk):
+    """ILUG_ILUT_CHUNK: consecutive rows per warp ticket (a started chunk is
+    finished past the quota): identical factors."""
+    monkeypatch.setenv("ILUG_ILUT_CHUNK", chunk)
+    monkeypatch.setenv("ILUG_ILUT_QUOTA", "3")
+    A = ilug.Matrix.generate("pressure27(20,20,20)")
+    cfg = _ilut_cfg(ilug, 1e-3, 5)
+    _same(ilug.ilu_factorize_device(A, cfg), ilug.ilu_factorize(A, cfg))
