@@ -158,12 +158,13 @@ def test_device_ilu0_large_bitwise(ilug, torch_cuda):
     assert bitwise(Ud.csr()[2], Uh.csr()[2]) and bitwise(Ld.csr()[2], Lh.csr()[2])
 
 
-@pytest.mark.parametrize("kind", ["gauss_seidel", "ilu"])
+@pytest.mark.parametrize("kind", ["gauss_seidel", "ilu", "poly_gs"])
 def test_setup_pipeline_errors_propagate(ilug, ref, torch_cuda, kind):
     """A failure inside the overlapped setup (the device builder thread for a
     GS smoother with a zero diagonal, the early factorisation thread for an ILU
-    zero pivot) surfaces as the reference's status-3 error, and the next solve
-    in the process still works."""
+    zero pivot, the poly-GS inverted diagonal computed on the device from the
+    AMG setup's copy of A) surfaces as the reference's status-3 error, and the
+    next solve in the process still works."""
     A = ilug.Matrix.generate("poisson2d(16,16)")
     rp, ci, v = A.csr()
     v = v.copy()
