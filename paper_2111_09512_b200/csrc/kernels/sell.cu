@@ -39,20 +39,19 @@ std::atomic<int> g_defer{0};
 std::mutex g_defer_mu;
 std::vector<void*> g_deferred;
 size_t g_deferred_bytes = 0;
-// Parked bytes before a flush: a third of the device (60 GB on a B200; at
-// least 16 GB). A flush mid-setup costs seconds (cudaFree of many large
-// buffers holds the allocator, stalling every setup thread's cudaMalloc);
-// dev_malloc still flushes and retries when an allocation runs out of memory.
-size_t defer_cap() {
-    static const size_t cap = [] {
-        size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
-            (void)cudaGetLastError();
-            tot = 0;
-        }
-        return std::max(size_t{16} << 30, tot / 3);
-    }();
-    return cap;
+// When to flush parked frees: only once memory is actually short (less than
+// a quarter of the device free, checked after 16 GB are parked). A flush
+// mid-setup costs up to a second (cudaFree of many large buffers holds the
+// allocator, stalling every setup thread's cudaMalloc); dev_malloc still
+// flushes and retries when an allocation runs out of memory.
+bool defer_should_flush(size_t parked) {
+    if (parked <= (size_t{16} << 30)) return false;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return true;
+    }
+    return fr < tot / 4;
 }
 bool defer_enabled() {
     static const bool on = [] {
@@ -74,7 +73,7 @@ void dev_free(void* p, size_t bytes) {
             std::lock_guard<std::mutex> g(g_defer_mu);
             g_deferred.push_back(p);
             g_deferred_bytes += bytes;
-            if (g_deferred_bytes > defer_cap()) flush.swap(g_deferred), g_deferred_bytes = 0;
+            if (defer_should_flush(g_deferred_bytes)) flush.swap(g_deferred), g_deferred_bytes = 0;
         }
         if (!flush.empty()) {
             SetupTimer tm("defer");
