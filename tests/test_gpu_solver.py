@@ -240,3 +240,22 @@ def test_shared_device_A_setup_identical(ilug, torch_cuda, monkeypatch, variant)
         assert rep["converged"] == "true"
         seen.add((rep["iterations"], rep["final_relres"]))
     assert len(seen) == 1, seen
+
+
+@pytest.mark.parametrize("env", [("ILUG_KEEP_DEVICE_LEVELS", "0"), ("ILUG_SELL_DEVICE_LAYOUT", "0"),
+                                 ("ILUG_ILUT_QUOTA", "0")])
+@pytest.mark.parametrize("fallback", ["poly_gs", "gauss_seidel"])
+def test_setup_paths_identical(ilug, torch_cuda, monkeypatch, env, fallback):
+    """The device hierarchy built from the device AMG setup's own A/P/R copies
+    (default) vs from host copies, the device vs host SELL layout of those
+    copies, and retiring vs persistent ILUT warps: same iterations and the
+    same final residual, bit for bit."""
+    A = ilug.Matrix.generate("pressure27(40,40,40)")
+    kv = {"krylov.tol": "1e-8", "smoother.kind": "ilu", "ilu.variant": "ilut", "ilu.droptol": "1e-3",
+          "ilu.lfill": "5", "trisolve.m_lower": 5, "trisolve.m_upper": 5, "amg.coarsening": "pmis",
+          "smoother.fallback.kind": fallback, "device.amg_setup": "device"}
+    base = ilug.run_solve(A, ilug.Config().update(kv))
+    monkeypatch.setenv(*env)
+    alt = ilug.run_solve(A, ilug.Config().update(kv))
+    assert base["converged"] == "true"
+    assert (alt["iterations"], alt["final_relres"]) == (base["iterations"], base["final_relres"])
