@@ -784,6 +784,12 @@ def time_to_solution(ilug, A, fallbacks=("poly_gs",)):
         if "direct_cusparse" in res:
             res["speedup_iterative_vs_cusparse_direct"] = round(
                 res["direct_cusparse"]["solve_s"] / res["richardson"]["solve_s"], 3)
+        # against the faster direct solve, and end to end (setup + solve)
+        best = min((res[m] for m in ("direct", "direct_cusparse") if m in res), key=lambda r: r["solve_s"])
+        it = res["richardson"]
+        res["speedup_iterative_vs_best_direct"] = round(best["solve_s"] / it["solve_s"], 3)
+        res["speedup_total_vs_best_direct"] = round((best["setup_s"] + best["solve_s"]) /
+                                                    (it["setup_s"] + it["solve_s"]), 3)
         out[f"fallback_{fb}"] = res
     return out
 
