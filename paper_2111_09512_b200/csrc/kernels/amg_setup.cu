@@ -716,19 +716,32 @@ HostHierarchy amg_setup_device(const Csr& A, const AmgParams& prm, const LevelRe
     tm.mark("upload A");
     const DevCsr* curp = Ad ? Ad : own.get(); // level k's operator on the device
     keep_device = keep_device && on_level;
-    // level 0's host copy of A (GBs) overlaps the level's GPU work; joined
-    // before anything reads it
+    // Each level's host copy of A (GBs at the fine levels: a host copy at
+    // level 0, a download from its own stream below it) overlaps the level's
+    // GPU work; joined before anything reads it and before the device copy
+    // can change.
+    cudaStream_t dl = nullptr;
+    ILUG_CUDA(cudaStreamCreateWithFlags(&dl, cudaStreamNonBlocking));
+    struct StreamDel {
+        cudaStream_t s;
+        ~StreamDel() { cudaStreamDestroy(s); }
+    } dl_guard{dl};
     std::future<Csr> a0 = std::async(std::launch::async, [&A] { return csr_copy(A); });
+    HostLevel* a0_lev = nullptr;
     auto join_a0 = [&] {
-        if (a0.valid()) h.levels.front().A = a0.get();
+        if (a0.valid()) a0_lev->A = a0.get();
     };
     for (;;) {
         h.levels.emplace_back();
         HostLevel& lev = h.levels.back();
         const i64 k = h.num_levels() - 1;
-        if (k > 0) lev.A = curp->download(st);
+        if (k > 0) { // the device A_k is complete (the previous level synchronised st)
+            const DevCsr* src = curp;
+            a0 = std::async(std::launch::async, [src, dl] { return src->download(dl); });
+        }
+        a0_lev = &lev;
         tm.mark("host A", k);
-        const i64 nk = k == 0 ? A.nrows : lev.A.nrows;
+        const i64 nk = curp->nrows;
         if (nk <= prm.coarse_size || k + 1 >= prm.max_levels) break;
         const DevCsr& cur = *curp;
         DevCsr S = strength_device(cur, prm.theta, st);
